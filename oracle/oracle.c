@@ -1,0 +1,465 @@
+/*
+ * oracle.c -- TEST INFRASTRUCTURE ONLY.  Plain, slow, obviously-correct fp64 CPU
+ * implementation of what the p-BiCGStab hot path computes, written from the paper
+ * (arXiv 1809.01948, S. Cools, "Analyzing and improving maximal attainable accuracy
+ * in the communication hiding pipelined BiCGStab method").
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+ * legs may load this library.  It shares NO code with the CUDA path
+ * (paper_1809_01948_b200/csrc) and includes none of its headers.
+ *
+ * Citation convention: "P:n" is line n of the paper's text, with the
+ * algorithm / equation it falls in.  Readings of ambiguous passages are the
+ * A-numbers of DESIGN.md section "Readings".
+ *
+ * Conventions (readings A4-A6):
+ *   - every vector expression is evaluated left to right with the brackets as
+ *     printed; build with -ffp-contract=off so no FMA contraction
+ *     happens anywhere except the explicit fma() inside TwoProd;
+ *   - SpMV sums a row's stored entries in ascending column order, starting from
+ *     +0.0 (A5);
+ *   - dot products are Dot2 (TwoProd + TwoSum compensated, rounded once) (A6);
+ *     flag ORC_PLAIN_DOT switches to a plain sequential sum (diagnostic only);
+ *   - Jacobi: dinv_j = 1.0 / a_jj, applied as fl(dinv_j * v_j) (A3).
+ *
+ * Parity status of each function: see the pins in tests/test_oracle_*.py and
+ * DESIGN.md "Oracle pins".  pcg / pipecg: the paper gives no p-CG pseudocode
+ * (P:465-472 defers to companion work); the reconstruction is pinned only by
+ * exact rational equivalence with PCG (tests/test_oracle_rational.py).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_BENCH 1      /* run maxit iterations: no exit on convergence (A23) */
+#define ORC_PLAIN_DOT 2  /* plain left-to-right dot instead of Dot2 (diagnostic) */
+#define ORC_GAP 4        /* compute the residual gap history */
+
+#define OUT_CONVERGED 0
+#define OUT_MAXIT 1
+#define OUT_BREAKDOWN 2
+
+/* ------------------------------------------------------------------------- */
+/* Dot2 (Ogita-Rump-Oishi): error-free TwoProd + TwoSum, one final rounding.  */
+/* The paper only fixes the error bound |(v,w) - fl((v,w))| <= N|v||w|eps     */
+/* (P:49); Dot2 is reading A6.                                               */
+/* ------------------------------------------------------------------------- */
+static void two_sum(double a, double b, double* s, double* e) {
+  double ss = a + b;
+  double z = ss - a;
+  *e = (a - (ss - z)) + (b - z);
+  *s = ss;
+}
+
+double orc_dot2(int64_t n, const double* x, const double* y) {
+  double P = 0.0, S = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    double h = x[j] * y[j];
+    double r = fma(x[j], y[j], -h); /* exact low part of the product */
+    double q;
+    two_sum(P, h, &P, &q);
+    S = S + (q + r);
+  }
+  return P + S;
+}
+
+double orc_dot_plain(int64_t n, const double* x, const double* y) {
+  double s = 0.0;
+  for (int64_t j = 0; j < n; ++j) s = s + x[j] * y[j];
+  return s;
+}
+
+static double dotf(int flags, int64_t n, const double* x, const double* y) {
+  return (flags & ORC_PLAIN_DOT) ? orc_dot_plain(n, x, y) : orc_dot2(n, x, y);
+}
+
+/* ------------------------------------------------------------------------- */
+/* Sparse matrix in CSR, columns ascending per row.                           */
+/* ------------------------------------------------------------------------- */
+/* y = A x: "fl(Av)" of P:48.  Row sum over stored entries in ascending column
+ * order, starting from +0.0 (reading A5). */
+void orc_spmv(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+              const double* x, double* y) {
+  for (int64_t i = 0; i < n; ++i) {
+    double acc = 0.0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) acc = acc + va[p] * x[ci[p]];
+    y[i] = acc;
+  }
+}
+
+/* Jacobi preconditioner M = diag(A) (reading A3): dinv_j = 1 / a_jj.
+ * Returns -1 if a diagonal entry is missing or zero. */
+int orc_jacobi_dinv(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+                    double* dinv) {
+  for (int64_t i = 0; i < n; ++i) {
+    double d = 0.0;
+    int found = 0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (ci[p] == i) { d = va[p]; found = 1; }
+    if (!found || d == 0.0) return -1;
+    dinv[i] = 1.0 / d;
+  }
+  return 0;
+}
+
+/* v := M^{-1} u, pointwise fl(dinv_j * u_j). */
+static void prec(int64_t n, const double* dinv, const double* u, double* v) {
+  for (int64_t j = 0; j < n; ++j) v[j] = dinv[j] * u[j];
+}
+
+/* Constant-coefficient 5-point (dim=2) / 7-point (dim=3) stencil written out
+ * as CSR, natural x-fastest ordering row = x + nx*(y + ny*z), Dirichlet legs
+ * dropped (Table 1 P:645-704 shapes; reading A5).  coef = {centre, -x, +x,
+ * -y, +y, -z, +z}.  Entries of a row are emitted in ascending column order:
+ * -z, -y, -x, centre, +x, +y, +z.  rp has n+1 entries; ci/va need 7n room.
+ * Returns nnz. */
+int64_t orc_stencil_csr(int dim, int64_t nx, int64_t ny, int64_t nz, const double* coef,
+                        int64_t* rp, int64_t* ci, double* va) {
+  if (dim == 2) nz = 1;
+  int64_t n = nx * ny * nz, nnz = 0;
+  for (int64_t zz = 0; zz < nz; ++zz)
+    for (int64_t yy = 0; yy < ny; ++yy)
+      for (int64_t xx = 0; xx < nx; ++xx) {
+        int64_t row = xx + nx * (yy + ny * zz);
+        rp[row] = nnz;
+        if (dim == 3 && zz > 0) { ci[nnz] = row - nx * ny; va[nnz++] = coef[5]; }
+        if (yy > 0) { ci[nnz] = row - nx; va[nnz++] = coef[3]; }
+        if (xx > 0) { ci[nnz] = row - 1; va[nnz++] = coef[1]; }
+        ci[nnz] = row; va[nnz++] = coef[0];
+        if (xx < nx - 1) { ci[nnz] = row + 1; va[nnz++] = coef[2]; }
+        if (yy < ny - 1) { ci[nnz] = row + nx; va[nnz++] = coef[4]; }
+        if (dim == 3 && zz < nz - 1) { ci[nnz] = row + nx * ny; va[nnz++] = coef[6]; }
+      }
+  rp[n] = nnz;
+  return nnz;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Workspace helper                                                          */
+/* ------------------------------------------------------------------------- */
+static double* vec(int64_t n) { return (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double)); }
+
+/* gap = || (b - A x) - r ||  (eq:res_gap; reading A13). */
+static double res_gap(int flags, int64_t n, const int64_t* rp, const int64_t* ci,
+                      const double* va, const double* b, const double* x, const double* r,
+                      double* tmp) {
+  orc_spmv(n, rp, ci, va, x, tmp);
+  for (int64_t j = 0; j < n; ++j) tmp[j] = (b[j] - tmp[j]) - r[j];
+  return sqrt(dotf(flags, n, tmp, tmp));
+}
+
+/* Number of vectors recorded per trace slot by orc_pbicgstab. */
+#define NTRACE 15
+/* trace slot layout (slot i = iteration i, slot maxit = final state):
+ *  0 x_i  1 r_i  2 k_i  3 w_i  4 m_i  5 t_i        (state entering iteration i)
+ *  6 g_i  7 s_i  8 l_i  9 z_i 10 q_i 11 u_i 12 y_i 13 n_i 14 v_i  (lines 5-14)  */
+
+/* ------------------------------------------------------------------------- */
+/* Preconditioned pipelined BiCGStab: Algorithm 2, step by step,   */
+/* with periodic residual replacement (eq:rr P:596-601, placed after line 20  */
+/* P:602-603, period policy P:607 / P:764) and the residual-gap history       */
+/* (eq:res_gap P:113).                                                        */
+/*                                                                            */
+/* Readings: A1 (previous-iteration vectors = 0, omega_{-1} = 0), A2 (r^_0 =   */
+/* r_0), A7 (stop when ||r_i|| <= tol*||b||), A8 ((r,r) added to reduction 2),*/
+/* A9 (breakdown guards), A10-A12 (replacement placement/schedule/sqrt(eps)  */
+/* stop, latched), A26 (n_i, v_i are not replaced).                           */
+/* sc_trace (optional): per iteration i: alpha_i, beta_i, omega_i, rho_i.     */
+/* ------------------------------------------------------------------------- */
+int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+                  const double* b, const double* x0, double tol, int32_t maxit,
+                  int32_t rr_period, int32_t flags, double* x, double* rhist,
+                  double* gaphist, int32_t* iters_out, int32_t* outcome_out,
+                  double* sc_trace, double* vec_trace) {
+  if (n < 0 || maxit < 0 || rr_period < 0) return -2;
+  double* dinv = vec(n);
+  if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
+  double *r = vec(n), *rh = vec(n), *k = vec(n), *w = vec(n), *m = vec(n), *t = vec(n);
+  double *g = vec(n), *s = vec(n), *l = vec(n), *z = vec(n), *nn = vec(n), *v = vec(n);
+  double *q = vec(n), *u = vec(n), *y = vec(n), *tmp = vec(n);
+  int fgap = (flags & ORC_GAP) && gaphist;
+  const double sqrt_eps = sqrt(ldexp(1.0, -53)); /* reading A12: eps = 2^-53 */
+
+  memcpy(x, x0, (size_t)n * sizeof(double));
+  /* line 2: r0 := b - A x0; k0 := M^-1 r0; w0 := A k0; m0 := M^-1 w0 */
+  orc_spmv(n, rp, ci, va, x, tmp);
+  for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
+  memcpy(rh, r, (size_t)n * sizeof(double)); /* A2: shadow residual r^ := r0 */
+  prec(n, dinv, r, k);
+  orc_spmv(n, rp, ci, va, k, w);
+  prec(n, dinv, w, m);
+  /* line 3: t0 := A m0; alpha0 := (r0,r0)/(r0,w0); beta0 := 0 */
+  orc_spmv(n, rp, ci, va, m, t);
+  double rho = dotf(flags, n, rh, r);
+  double alpha = rho / dotf(flags, n, rh, w);
+  double beta = 0.0, omega = 0.0; /* A1: omega_{-1} := 0; g,s,l,z,n,v := 0 (calloc) */
+  double nb = sqrt(dotf(flags, n, b, b));
+  rhist[0] = sqrt(dotf(flags, n, r, r));
+  if (fgap) gaphist[0] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
+  double h0 = rhist[0];
+  int rr_off = 0; /* A12: replacements stop for good once ||r_i|| < sqrt(eps)||r_0|| */
+  if (h0 < sqrt_eps * h0) rr_off = 1;
+  int32_t iters = 0, outcome = OUT_MAXIT;
+  int done = 0;
+  if (rhist[0] <= tol * nb && !(flags & ORC_BENCH)) { outcome = OUT_CONVERGED; done = 1; }
+  else if (!isfinite(alpha)) { outcome = OUT_BREAKDOWN; done = 1; }
+
+  for (int32_t i = 0; i < maxit && !done; ++i) {
+    if (vec_trace) {
+      double* T = vec_trace + (size_t)i * NTRACE * (size_t)n;
+      const double* src[6] = {x, r, k, w, m, t};
+      for (int a = 0; a < 6; ++a) memcpy(T + (size_t)a * n, src[a], (size_t)n * sizeof(double));
+    }
+    if (sc_trace) { sc_trace[4 * i + 0] = alpha; sc_trace[4 * i + 1] = beta; sc_trace[4 * i + 3] = rho; }
+    for (int64_t j = 0; j < n; ++j) {
+      /* lines 5-8, n_{i-1} and v_{i-1} as stored (A26) */
+      g[j] = k[j] + beta * (g[j] - omega * l[j]);
+      s[j] = w[j] + beta * (s[j] - omega * z[j]);
+      l[j] = m[j] + beta * (l[j] - omega * nn[j]);
+      z[j] = t[j] + beta * (z[j] - omega * v[j]);
+    }
+    for (int64_t j = 0; j < n; ++j) {
+      /* lines 9-11 */
+      q[j] = r[j] - alpha * s[j];
+      u[j] = k[j] - alpha * l[j];
+      y[j] = w[j] - alpha * z[j];
+    }
+    /* line 12: reduction (q,y), (y,y) */
+    double qy = dotf(flags, n, q, y);
+    double yy = dotf(flags, n, y, y);
+    /* lines 13-14: n := M^-1 z; v := A n */
+    prec(n, dinv, z, nn);
+    orc_spmv(n, rp, ci, va, nn, v);
+    if (vec_trace) {
+      double* T = vec_trace + (size_t)i * NTRACE * (size_t)n;
+      const double* src[9] = {g, s, l, z, q, u, y, nn, v};
+      for (int a = 0; a < 9; ++a)
+        memcpy(T + (size_t)(6 + a) * n, src[a], (size_t)n * sizeof(double));
+    }
+    /* line 16: omega := (q,y)/(y,y); A9: (y,y) = 0 => omega := 0 */
+    omega = (yy == 0.0) ? 0.0 : qy / yy;
+    if (sc_trace) sc_trace[4 * i + 2] = omega;
+    if (!isfinite(omega)) { outcome = OUT_BREAKDOWN; iters = i; done = 1; break; }
+    /* lines 17-20 */
+    for (int64_t j = 0; j < n; ++j) {
+      x[j] = (x[j] + alpha * g[j]) + omega * u[j];
+      r[j] = q[j] - omega * y[j];
+      k[j] = u[j] - omega * (m[j] - alpha * nn[j]);
+      w[j] = y[j] - omega * (t[j] - alpha * v[j]);
+    }
+    /* residual replacement after line 20, eq:rr:
+     * r := b - A x; k := M^-1 r; w := A k; s := A g; l := M^-1 s; z := A l.
+     * Schedule (A11): loop index i replaces when (i+1) mod P_rr == 0. */
+    if (rr_period > 0 && (i + 1) % rr_period == 0 && !rr_off) {
+      orc_spmv(n, rp, ci, va, x, tmp);
+      for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
+      prec(n, dinv, r, k);
+      orc_spmv(n, rp, ci, va, k, w);
+      orc_spmv(n, rp, ci, va, g, s);
+      prec(n, dinv, s, l);
+      orc_spmv(n, rp, ci, va, l, z);
+    }
+    /* line 21: reduction (r0,r), (r0,w), (r0,s), (r0,z); + (r,r) (A8) */
+    double rho1 = dotf(flags, n, rh, r);
+    double dw = dotf(flags, n, rh, w);
+    double ds = dotf(flags, n, rh, s);
+    double dz = dotf(flags, n, rh, z);
+    rhist[i + 1] = sqrt(dotf(flags, n, r, r));
+    /* lines 22-23: m := M^-1 w; t := A m */
+    prec(n, dinv, w, m);
+    orc_spmv(n, rp, ci, va, m, t);
+    if (fgap) gaphist[i + 1] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
+    iters = i + 1;
+    if (rhist[i + 1] < sqrt_eps * h0) rr_off = 1;
+    if (rhist[i + 1] <= tol * nb && !(flags & ORC_BENCH)) { outcome = OUT_CONVERGED; done = 1; break; }
+    /* lines 25-26 */
+    double beta1 = ((alpha / omega) * rho1) / rho;
+    double den = (dw + beta1 * ds) - (beta1 * omega) * dz;
+    double alpha1 = rho1 / den;
+    beta = beta1;
+    alpha = alpha1;
+    rho = rho1;
+    if (!isfinite(beta) || !isfinite(alpha) || den == 0.0 || rho1 == 0.0) {
+      outcome = OUT_BREAKDOWN; done = 1; break;
+    }
+  }
+  if (vec_trace && !done) {
+    double* T = vec_trace + (size_t)maxit * NTRACE * (size_t)n;
+    const double* src[6] = {x, r, k, w, m, t};
+    for (int a = 0; a < 6; ++a) memcpy(T + (size_t)a * n, src[a], (size_t)n * sizeof(double));
+  }
+  *iters_out = iters;
+  *outcome_out = outcome;
+  free(dinv); free(r); free(rh); free(k); free(w); free(m); free(t); free(g); free(s);
+  free(l); free(z); free(nn); free(v); free(q); free(u); free(y); free(tmp);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Classic preconditioned BiCGStab: Algorithm 1, step by step.       */
+/* Same conventions; rhist[i] = ||r_i||, stop when ||r_i|| <= tol ||b|| (A7). */
+/* sc_trace: alpha_i, beta_i, omega_i, rho_i per iteration.                   */
+/* ------------------------------------------------------------------------- */
+int orc_bicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+                 const double* b, const double* x0, double tol, int32_t maxit, int32_t flags,
+                 double* x, double* rhist, double* gaphist, int32_t* iters_out,
+                 int32_t* outcome_out, double* sc_trace) {
+  if (n < 0 || maxit < 0) return -2;
+  double* dinv = vec(n);
+  if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
+  double *r = vec(n), *rh = vec(n), *p = vec(n), *g = vec(n), *s = vec(n), *q = vec(n);
+  double *u = vec(n), *y = vec(n), *tmp = vec(n);
+  int fgap = (flags & ORC_GAP) && gaphist;
+  memcpy(x, x0, (size_t)n * sizeof(double));
+  /* line 2: r0 := b - A x0; p0 := r0 */
+  orc_spmv(n, rp, ci, va, x, tmp);
+  for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
+  memcpy(rh, r, (size_t)n * sizeof(double));
+  memcpy(p, r, (size_t)n * sizeof(double));
+  double rho = dotf(flags, n, rh, r);
+  double nb = sqrt(dotf(flags, n, b, b));
+  rhist[0] = sqrt(dotf(flags, n, r, r));
+  if (fgap) gaphist[0] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
+  int32_t iters = 0, outcome = OUT_MAXIT;
+  int done = 0;
+  if (rhist[0] <= tol * nb && !(flags & ORC_BENCH)) { outcome = OUT_CONVERGED; done = 1; }
+  for (int32_t i = 0; i < maxit && !done; ++i) {
+    prec(n, dinv, p, g);                   /* line 4 */
+    orc_spmv(n, rp, ci, va, g, s);         /* line 5 */
+    double rs = dotf(flags, n, rh, s);     /* line 6 */
+    double alpha = rho / rs;               /* line 7 */
+    for (int64_t j = 0; j < n; ++j) q[j] = r[j] - alpha * s[j]; /* line 8 */
+    prec(n, dinv, q, u);                   /* line 9 */
+    orc_spmv(n, rp, ci, va, u, y);         /* line 10 */
+    double qy = dotf(flags, n, q, y);      /* line 11 */
+    double yy = dotf(flags, n, y, y);
+    double omega = (yy == 0.0) ? 0.0 : qy / yy; /* line 12, guard A9 */
+    if (sc_trace) { sc_trace[4 * i] = alpha; sc_trace[4 * i + 2] = omega; sc_trace[4 * i + 3] = rho; }
+    if (!isfinite(alpha) || !isfinite(omega)) { outcome = OUT_BREAKDOWN; iters = i; done = 1; break; }
+    for (int64_t j = 0; j < n; ++j) {
+      x[j] = (x[j] + alpha * g[j]) + omega * u[j]; /* line 13, eq:auxrec0 */
+      r[j] = q[j] - omega * y[j];                   /* line 14 */
+    }
+    double rho1 = dotf(flags, n, rh, r);   /* line 15 */
+    rhist[i + 1] = sqrt(dotf(flags, n, r, r));
+    if (fgap) gaphist[i + 1] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
+    iters = i + 1;
+    if (rhist[i + 1] <= tol * nb && !(flags & ORC_BENCH)) { outcome = OUT_CONVERGED; done = 1; break; }
+    double beta = ((alpha / omega) * rho1) / rho; /* line 16 */
+    if (sc_trace) sc_trace[4 * i + 1] = beta;
+    for (int64_t j = 0; j < n; ++j) p[j] = r[j] + beta * (p[j] - omega * s[j]); /* line 17 */
+    rho = rho1;
+    if (!isfinite(beta) || rho1 == 0.0) { outcome = OUT_BREAKDOWN; done = 1; break; }
+  }
+  *iters_out = iters;
+  *outcome_out = outcome;
+  free(dinv); free(r); free(rh); free(p); free(g); free(s); free(q); free(u); free(y); free(tmp);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Preconditioned CG (Hestenes-Stiefel form) -- comparison solver for cfg1.   */
+/* Not an algorithm printed in the paper (cited at P:30); standard PCG.       */
+/* ------------------------------------------------------------------------- */
+int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+            const double* b, const double* x0, double tol, int32_t maxit, int32_t flags,
+            double* x, double* rhist, double* gaphist, int32_t* iters_out,
+            int32_t* outcome_out) {
+  double* dinv = vec(n);
+  if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
+  double *r = vec(n), *u = vec(n), *p = vec(n), *s = vec(n), *tmp = vec(n);
+  int fgap = (flags & ORC_GAP) && gaphist;
+  memcpy(x, x0, (size_t)n * sizeof(double));
+  orc_spmv(n, rp, ci, va, x, tmp);
+  for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
+  prec(n, dinv, r, u);
+  memcpy(p, u, (size_t)n * sizeof(double));
+  double gam = dotf(flags, n, r, u);
+  double nb = sqrt(dotf(flags, n, b, b));
+  rhist[0] = sqrt(dotf(flags, n, r, r));
+  if (fgap) gaphist[0] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
+  int32_t iters = 0, outcome = OUT_MAXIT;
+  int done = (rhist[0] <= tol * nb && !(flags & ORC_BENCH));
+  if (done) outcome = OUT_CONVERGED;
+  for (int32_t i = 0; i < maxit && !done; ++i) {
+    orc_spmv(n, rp, ci, va, p, s);
+    double alpha = gam / dotf(flags, n, p, s);
+    for (int64_t j = 0; j < n; ++j) { x[j] = x[j] + alpha * p[j]; r[j] = r[j] - alpha * s[j]; }
+    prec(n, dinv, r, u);
+    double gam1 = dotf(flags, n, r, u);
+    rhist[i + 1] = sqrt(dotf(flags, n, r, r));
+    if (fgap) gaphist[i + 1] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
+    iters = i + 1;
+    if (rhist[i + 1] <= tol * nb && !(flags & ORC_BENCH)) { outcome = OUT_CONVERGED; break; }
+    double beta = gam1 / gam;
+    for (int64_t j = 0; j < n; ++j) p[j] = u[j] + beta * p[j];
+    gam = gam1;
+    if (!isfinite(alpha) || !isfinite(beta)) { outcome = OUT_BREAKDOWN; break; }
+  }
+  *iters_out = iters;
+  *outcome_out = outcome;
+  free(dinv); free(r); free(u); free(p); free(s); free(tmp);
+  return 0;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Preconditioned pipelined CG (Ghysels-Vanroose form).  The paper compares   */
+/* against p-CG (Figs. 1-2) but prints no pseudocode (reading      */
+/* A19); this reconstruction is pinned only by exact rational equivalence     */
+/* with PCG.  One reduction {(r,u),(w,u)} per iteration, overlapped with      */
+/* m := M^-1 w, n := A m.                                                     */
+/* ------------------------------------------------------------------------- */
+int orc_pipecg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+               const double* b, const double* x0, double tol, int32_t maxit, int32_t flags,
+               double* x, double* rhist, double* gaphist, int32_t* iters_out,
+               int32_t* outcome_out) {
+  double* dinv = vec(n);
+  if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
+  double *r = vec(n), *u = vec(n), *w = vec(n), *m = vec(n), *nn = vec(n);
+  double *z = vec(n), *q = vec(n), *s = vec(n), *p = vec(n), *tmp = vec(n);
+  int fgap = (flags & ORC_GAP) && gaphist;
+  memcpy(x, x0, (size_t)n * sizeof(double));
+  orc_spmv(n, rp, ci, va, x, tmp);
+  for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
+  prec(n, dinv, r, u);
+  orc_spmv(n, rp, ci, va, u, w);
+  double nb = sqrt(dotf(flags, n, b, b));
+  rhist[0] = sqrt(dotf(flags, n, r, r));
+  if (fgap) gaphist[0] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
+  int32_t iters = 0, outcome = OUT_MAXIT;
+  int done = (rhist[0] <= tol * nb && !(flags & ORC_BENCH));
+  if (done) outcome = OUT_CONVERGED;
+  double gam_old = 0.0, alpha_old = 0.0;
+  for (int32_t i = 0; i < maxit && !done; ++i) {
+    double gam = dotf(flags, n, r, u);
+    double del = dotf(flags, n, w, u);
+    prec(n, dinv, w, m);
+    orc_spmv(n, rp, ci, va, m, nn);
+    double beta, alpha;
+    if (i == 0) { beta = 0.0; alpha = gam / del; }
+    else { beta = gam / gam_old; alpha = gam / (del - (beta * gam) / alpha_old); }
+    if (!isfinite(alpha) || !isfinite(beta)) { outcome = OUT_BREAKDOWN; iters = i; break; }
+    for (int64_t j = 0; j < n; ++j) {
+      z[j] = nn[j] + beta * z[j];
+      q[j] = m[j] + beta * q[j];
+      s[j] = w[j] + beta * s[j];
+      p[j] = u[j] + beta * p[j];
+      x[j] = x[j] + alpha * p[j];
+      r[j] = r[j] - alpha * s[j];
+      u[j] = u[j] - alpha * q[j];
+      w[j] = w[j] - alpha * z[j];
+    }
+    gam_old = gam;
+    alpha_old = alpha;
+    rhist[i + 1] = sqrt(dotf(flags, n, r, r));
+    if (fgap) gaphist[i + 1] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
+    iters = i + 1;
+    if (rhist[i + 1] <= tol * nb && !(flags & ORC_BENCH)) { outcome = OUT_CONVERGED; break; }
+  }
+  *iters_out = iters;
+  *outcome_out = outcome;
+  free(dinv); free(r); free(u); free(w); free(m); free(nn); free(z); free(q); free(s); free(p);
+  free(tmp);
+  return 0;
+}
