@@ -1,0 +1,302 @@
+#!/usr/bin/env python
+"""bench.py -- p-BiCGStab fp64 iterations/s and % of HBM roofline on B200.
+
+Contract:
+  python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--config cfg4]
+
+A step = one full solve of the configured workload through the public API
+(init + `maxit` p-BiCGStab iterations in bench mode, replacement every
+`rr_period`), inputs resident in HBM.  value = iterations/s of the whole job.
+Rank 0 prints one JSON line.  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1809_01948_b200 import problems  # noqa: E402
+
+METRIC = "p-BiCGStab fp64 iterations/s and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "iterations/s"
+L2_BYTES = 126 * 2 ** 20
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel: str):
+    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        d = json.load(open(p))
+        return d[kernel]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def workload(cfg_name: str):
+    cfg = problems.configs()[cfg_name]
+    if cfg.kind != "stencil":
+        raise SystemExit("bench: only stencil configs are wired as the headline workload")
+    st = cfg.stencil
+    maxit = cfg.maxit if cfg.bench else 200
+    rr = 50  # replacement every 50 iterations (cfg3's period) so every 8(a) row runs
+    return cfg, st, maxit, rr
+
+
+def oracle_sample(st, maxit_sample: int, nz_sample: int):
+    """Time the oracle (1 core) on an nx*ny*nz_sample slab of the workload."""
+    from oracle import oracle as orc
+    nzs = min(nz_sample, st.nz if st.dim == 3 else st.ny)
+    if st.dim == 3:
+        A = orc.stencil_csr(3, st.nx, st.ny, nzs, st.coef)
+    else:
+        A = orc.stencil_csr(2, st.nx, nzs, 1, st.coef)
+    xs = problems.x_star(A.n, 0)
+    b = orc.spmv(A, xs)
+    t0 = time.perf_counter()
+    orc.pbicgstab(A, b, tol=0.0, maxit=0, bench=True, gap=False)
+    t_init = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r = orc.pbicgstab(A, b, tol=0.0, maxit=maxit_sample, rr_period=0, bench=True, gap=False)
+    t = time.perf_counter() - t0 - t_init
+    rows_per_s = A.n * r.iters / t
+    return rows_per_s, A.n, r.iters, t
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    cfg, st, maxit, rr = workload(args.config)
+    n_full = st.n
+    vals = []
+    sample = None
+    for s in range(args.warmup + args.steps):
+        rows_per_s, n_s, its, t = oracle_sample(st, 6, 64)
+        if s >= args.warmup:
+            vals.append(rows_per_s / n_full)
+            sample = (f"oracle p-BiCGStab (C, 1 core) on a {st.nx}x{st.ny}x64 slab of {cfg.name} "
+                      f"({n_s} rows), {its} iterations per step, scaled by rows to {n_full} rows")
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * maxit / v,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": n_full,
+                                            "maxit": maxit, "rr_period": rr},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args, rank, world):
+    import torch
+    from paper_1809_01948_b200 import Solver
+
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(dev)
+    cfg, st, maxit, rr = workload(args.config)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    stream = torch.cuda.Stream()
+    S = Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef, stream=stream)
+    n = S.n_local
+    xs_full = problems.x_star(st.n, seed=0)
+    xs = torch.from_numpy(xs_full[S.row_begin:S.row_begin + n]).to(f"cuda:{dev}")
+    del xs_full
+    b = S.apply(xs)
+    x0 = torch.zeros_like(b)
+    x = torch.empty_like(b)
+    S.set_option("bench", 1)
+    S.set_option("graphs", 1)
+    gap = bool(args.gap)
+
+    def step():
+        return S.solve(b, x0, tol=0.0, maxit=maxit, rr_period=rr, gap=gap, x_out=x)
+
+    for _ in range(args.warmup):
+        r = step()
+    assert r.iters == maxit, (r.iters, r.outcome)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # ---- timed region: device time with CUDA events on the solver's stream
+    S.set_option("timing", 1)  # events around every kernel (graphs off; launches are ms-long)
+    S.kernel_time("all", reset=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        e0.record(stream)
+        iters = 0
+        for _ in range(args.steps):
+            iters += step().iters
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    launches, _ = S.kernel_time("all")
+    per_kernel = {}
+    for k in ("sweepA", "sweepC", "rr1", "rr2", "gap", "init", "apply"):
+        nk, tk = S.kernel_time(k)
+        if nk:
+            per_kernel[k] = {"launches": nk, "avg_ms": tk / nk, "bytes": S.kernel_bytes(k)}
+    S.set_option("timing", 0)
+
+    # ---- end to end: host (pinned) b, x0 -> solve -> host x, through the C ABI
+    hb = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    hb.copy_(b.cpu())
+    hx0 = torch.zeros(n, dtype=torch.float64, pin_memory=True)
+    hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    hbn, hx0n, hxn = hb.numpy(), hx0.numpy(), hx.numpy()
+    S.solve_host(hbn, hx0n, tol=0.0, maxit=maxit, rr_period=rr, gap=gap, x_out=hxn)  # warm
+    barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    e2e_iters = 0
+    for _ in range(max(1, args.steps // 2)):
+        e2e_iters += S.solve_host(hbn, hx0n, tol=0.0, maxit=maxit, rr_period=rr, gap=gap,
+                                  x_out=hxn).iters
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    if rank != 0:
+        return 0
+
+    peak, peak_src = measured_peak()
+    value = iters * world / (ms / 1000.0)
+    dom = "sweepC"
+    kb = per_kernel[dom]["bytes"]
+    k_avg_s = per_kernel[dom]["avg_ms"] / 1000.0
+    achieved = kb / k_avg_s / 1e9
+    it_bytes = S.kernel_bytes("iteration")
+    traffic = ncu_traffic(dom)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded x* ~ U[-1,1], b = A x* on device)",
+        "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": st.n, "grid": [st.nx, st.ny, st.nz],
+                   "maxit_per_step": maxit, "rr_period": rr, "gap_tracking": gap,
+                   "schedule": "fused 2-sweep (stencil)", "l2": "inputs larger than L2 (%.1f GB)"
+                   % (14 * 8 * n / 1e9), "parallelism": f"z-slab x{world}"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
+                     "iteration_frac": (it_bytes * value / world / 1e9) / peak},
+        "kernels": per_kernel,
+        "gpu_launches": launches,
+        "e2e": {"value": e2e_iters * world / (e2e_ms / 1000.0), "unit": UNIT,
+                "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 8 * n + 8 * (maxit + 1)
+                * (2 if gap else 1)},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        rows_per_s, n_s, its, t = oracle_sample(st, 6, 64)
+        line["cpu_baseline"] = {
+            "value": rows_per_s / st.n, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle p-BiCGStab (C, 1 core) on a {st.nx}x{st.ny}x64 slab of {cfg.name} "
+                      f"({n_s} rows), {its} iterations in {t:.1f} s, scaled by rows to {st.n}"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--gap", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    return run_ours(args, rank, world)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

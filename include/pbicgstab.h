@@ -1,0 +1,182 @@
+/*
+ * pbicgstab.h -- C ABI of the B200-native preconditioned pipelined BiCGStab
+ * (p-BiCGStab) library, arXiv 1809.01948 (S. Cools).
+ *
+ * The library solves A x = b for a sparse N x N matrix A with
+ * Algorithm 2 "Preconditioned pipelined BiCGStab", Jacobi
+ * preconditioner M = diag(A) (BASELINE; reading A3), periodic residual
+ * replacement (eq:rr P:596-601, placed after line 20 P:602-603, period policy
+ * P:607) and the true-vs-recursive residual gap history (eq:res_gap P:112-116).
+ * All arithmetic is fp64 on the GPU (sm_100a); every step of the iteration runs
+ * in this library's own CUDA kernels.  There is no CPU fallback: on a machine
+ * without a usable CUDA device every call that needs the device returns
+ * PBICG_ECUDA.
+ *
+ * Conventions shared by every entry point
+ *  - Every call returns pbicg_status; 0 = PBICG_OK.  No exception crosses the ABI.
+ *    On error, pbicgstab_last_error(handle) (or NULL for create errors) returns a
+ *    thread-local / handle-owned message.
+ *  - Pointers are BORROWED for the duration of the call only, unless stated.
+ *  - "_dev" pointers are CUDA device pointers of the calling process's current
+ *    device; "host" pointers are ordinary host memory.
+ *  - Vector layout: natural x-fastest row order, row = x + nx*(y + ny*z), fp64.
+ *  - A handle is not thread-safe; use one handle per thread/stream.
+ */
+#ifndef PBICGSTAB_H
+#define PBICGSTAB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pbicg_ctx* pbicg_handle;
+
+typedef enum {
+  PBICG_OK = 0,
+  PBICG_EINVAL = 1, /* bad argument (sizes, NULL, zero diagonal, bad option key) */
+  PBICG_ECUDA = 2,  /* CUDA runtime error or no CUDA device */
+  PBICG_ENCCL = 3,  /* NCCL error (multi-GPU) */
+  PBICG_ENOMEM = 4, /* device or host allocation failed */
+  PBICG_ESTATE = 5  /* handle in a failed state, or feature not available in this build */
+} pbicg_status;
+
+/* Outcome of a solve (reading A9). */
+typedef enum {
+  PBICG_CONVERGED = 0, /* ||r_i|| <= tol * ||b|| with r_i the recursive residual (A7) */
+  PBICG_MAXIT = 1,     /* maxit iterations done without convergence */
+  PBICG_BREAKDOWN = 2  /* non-finite or zero scalar denominator (A9); x = last finite iterate */
+} pbicg_outcome;
+
+typedef enum { PBICG_PREC_JACOBI = 1 } pbicg_prec; /* M = diag(A), dinv_j = 1/a_jj (A3) */
+
+/* Matrix-free constant-coefficient stencil (Table 1 shapes).
+ *   dim = 2: 5-point on an nx x ny grid (nz ignored, treated as 1)
+ *   dim = 3: 7-point on an nx x ny x nz grid
+ *   coef = {centre, -x, +x, -y, +y, -z, +z}: row `row` has coef[1] at column
+ *   row-1, coef[2] at row+1, coef[3] at row-nx, coef[4] at row+nx, coef[5] at
+ *   row-nx*ny, coef[6] at row+nx*ny.  Legs leaving the grid are dropped
+ *   (homogeneous Dirichlet, reading A5).  Each row is summed in ascending column
+ *   order: -z, -y, -x, centre, +x, +y, +z.  coef[0] must be nonzero (Jacobi). */
+typedef struct {
+  int32_t dim;
+  int64_t nx, ny, nz;
+  double coef[7];
+} pbicg_stencil;
+
+/* General sparse matrix, this rank's rows in CSR (host arrays, copied).
+ *   rows [row_begin, row_begin + n_local) of an n_global x n_global matrix;
+ *   row_ptr[n_local+1] offsets into col/val (row_ptr[0] may be nonzero);
+ *   col = GLOBAL column ids, sorted ascending within each row; every row must
+ *   contain its diagonal entry with a nonzero value (Jacobi).  Rows are summed
+ *   in the stored (ascending) order.  Multi-GPU: columns must lie within the
+ *   neighbouring ranks' rows [row_begin - H, row_begin + n_local + H) with
+ *   H = PBICG_CSR_HALO (nearest-neighbour halo only), else PBICG_EINVAL. */
+typedef struct {
+  int64_t n_global, row_begin, n_local;
+  const int64_t* row_ptr;
+  const int32_t* col;
+  const double* val;
+} pbicg_csr;
+
+#define PBICG_CSR_HALO 4096
+
+/* Multi-GPU description (one process per GPU).  NULL => single GPU.
+ * nccl_id_halo / nccl_id_red: 128-byte ncclUniqueId blobs from
+ * pbicgstab_get_unique_id() on rank 0, broadcast to all ranks by the caller.
+ * Stencils are split into contiguous z-slabs (3D) / y-slabs (2D) chosen by the
+ * library (pbicgstab_local_rows reports them); CSR uses the caller's rows. */
+typedef struct {
+  int32_t nranks, rank;
+  const void* nccl_id_halo;
+  const void* nccl_id_red;
+} pbicg_dist;
+
+/* Create a solver for a stencil operator.  `cuda_stream` (cudaStream_t or NULL
+ * for the legacy default stream) is the stream every kernel of this handle is
+ * launched on.  Allocates the device workspace (12 fp64 vectors of n_local rows
+ * plus ghost planes).  Errors: EINVAL (dim not 2/3, nx/ny/nz < 1, coef[0] == 0,
+ * nranks/rank inconsistent), ECUDA, ENOMEM, ENCCL. */
+pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
+                                      const pbicg_dist* dist, void* cuda_stream,
+                                      pbicg_handle* out);
+
+/* Create a solver for a CSR operator (copied to the device as a column-major
+ * padded ELL matrix in the same per-row order).  Errors as above, plus EINVAL
+ * for unsorted/out-of-range columns or a missing/zero diagonal. */
+pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pbicg_dist* dist,
+                                  void* cuda_stream, pbicg_handle* out);
+
+/* Global rows owned by this rank: [row_begin, row_begin + n_local). */
+pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n_local);
+
+/* Options (int64 values):
+ *   "bench"      1 => run exactly maxit iterations, no exit on convergence (A23)
+ *   "graphs"     1 (default) => replay chunks of iterations as CUDA graphs
+ *   "timing"     1 => record CUDA events around every kernel (disables graphs);
+ *                read with pbicgstab_kernel_time
+ *   "overlap"    1 (default) => multi-GPU: reductions overlap the SpMV (split
+ *                schedule); 0 => blocking
+ *   "schedule"   0 (default) auto, 1 fused 2-sweep (stencil only), 2 split 4-phase
+ * Errors: EINVAL for an unknown key or bad value. */
+pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value);
+
+/* y = A x for this rank's rows (x_dev, y_dev: n_local doubles on the device).
+ * Same arithmetic as the solver's SpMV (ascending column order, no FMA).  Used
+ * to form b = A x* for synthetic problems.  Collective for nranks > 1. */
+pbicg_status pbicgstab_apply(pbicg_handle h, const double* x_dev, double* y_dev);
+
+/* Solve A x = b with p-BiCGStab (Alg. 2).  Collective: every rank calls it with
+ * identical scalar arguments.  Host-synchronous: returns after the histories are
+ * on the host.
+ *   b_dev, x0_dev   device, n_local doubles (this rank's rows)
+ *   tol             relative to ||b||_2: stop when ||r_i|| <= tol*||b|| (A7)
+ *   maxit >= 0      iteration cap
+ *   rr_period >= 0  residual replacement after line 20 of every iteration i with
+ *                   (i+1) % rr_period == 0, until ||r_i|| < sqrt(eps)||r_0||
+ *                   (A11, A12); 0 disables replacement
+ *   x_dev_out       device, n_local doubles; may alias x0_dev
+ *   rnorm_hist      host, >= maxit+1 doubles: ||r_i|| for i = 0..iters
+ *   gap_hist        host, >= maxit+1 doubles, or NULL (no gap tracking):
+ *                   ||(b - A x_i) - r_i|| for i = 0..iters (eq:res_gap P:113)
+ *   iters_out       completed iterations;  outcome_out  pbicg_outcome
+ * Entries beyond iters are left untouched. */
+pbicg_status pbicgstab_solve(pbicg_handle h, const double* b_dev, const double* x0_dev,
+                             double tol, int32_t maxit, int32_t rr_period, double* x_dev_out,
+                             double* rnorm_hist, double* gap_hist, int32_t* iters_out,
+                             int32_t* outcome_out);
+
+/* Same as pbicgstab_solve with HOST b, x0 and x_out (n_local doubles each); the
+ * host<->device copies happen inside the call (end-to-end entry point). */
+pbicg_status pbicgstab_solve_host(pbicg_handle h, const double* b_host, const double* x0_host,
+                                  double tol, int32_t maxit, int32_t rr_period,
+                                  double* x_host_out, double* rnorm_hist, double* gap_hist,
+                                  int32_t* iters_out, int32_t* outcome_out);
+
+/* Per-kernel statistics since the last reset (reset = 1 clears them).
+ *   name: "init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap",
+ *   "apply", or "all" (launch count only; time = NaN).
+ *   launches: kernel launches issued (graph nodes count once per replay);
+ *   ms: summed CUDA-event time (only with option "timing"; else NaN). */
+pbicg_status pbicgstab_kernel_time(pbicg_handle h, const char* name, int64_t* launches,
+                                   double* ms, int32_t reset);
+
+/* Algorithmic HBM bytes one launch of kernel `name` must move for this handle's
+ * operator; 0 if unknown. */
+pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* bytes);
+
+/* ncclUniqueId blob (128 bytes) for multi-GPU creation; ESTATE without NCCL. */
+pbicg_status pbicgstab_get_unique_id(void* out128);
+
+/* Error message for the last failing call on h (h may be NULL: last create error
+ * on this thread).  Owned by the library; valid until the next call. */
+const char* pbicgstab_last_error(pbicg_handle h);
+
+/* Release every resource of h.  NULL is a no-op. */
+void pbicgstab_destroy(pbicg_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PBICGSTAB_H */

@@ -1,0 +1,244 @@
+// csr_kernels.cuh -- general sparse (CSR in, column-major ELL on the device)
+// path: the split 4-phase schedule of Algorithm 2.
+//
+// A general matrix is too expensive to re-apply inside the AXPY sweeps (the
+// matrix bytes dominate), so t_i = A M^-1 w_i and v_i = A M^-1 z_i are stored
+// as in the paper's own schedule:
+//   sweepA (lines 5-12) -> spmvB (lines 13-14) -> sweepC (lines 17-21)
+//   [-> rr1 -> rr2 (eq:rr)] -> spmvD (lines 22-23)
+// Each row is summed in its stored (ascending column) order (reading A5); a
+// padded slot (rows shorter than the ELL width) is skipped, never added.
+// Buffers: V.w0 = w, V.w1 = t, V.z0 = z, V.z1 = v, V.zrr = replaced z (A26).
+#pragma once
+#include "dd.cuh"
+#include "state.cuh"
+#include "stencil_kernels.cuh"  // Vecs
+
+struct CsrOp {
+  int64_t n;             // local rows
+  int32_t width;         // ELL slots per row
+  const int32_t* col;    // [width][n] column-major, LOCAL index (may be < 0 / >= n: ghosts)
+  const double* val;     // [width][n]
+  const int32_t* len;    // [n] row lengths, or nullptr when every row has `width` entries
+  const double* dinv;    // [n + 2H] ghosted Jacobi inverse diagonal (A3)
+};
+
+// fl(A v)_j or fl(A M^-1 v)_j
+template <bool PREC>
+__device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restrict__ v, int64_t j) {
+  const int len = A.len ? A.len[j] : A.width;
+  double acc = 0.0;
+  for (int p = 0; p < len; ++p) {
+    const int64_t c = A.col[(int64_t)p * A.n + j];
+    const double a = A.val[(int64_t)p * A.n + j];
+    const double x = PREC ? A.dinv[c] * __ldg(v + c) : __ldg(v + c);
+    acc = acc + a * x;
+  }
+  return acc;
+}
+
+#define ROW_LOOP for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < A.n; \
+                      j += (int64_t)gridDim.x * blockDim.x)
+
+__global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                               Dd* __restrict__ part) {
+  Dd acc[2] = {dd_zero(), dd_zero()};
+  ROW_LOOP {
+    const double bj = V.b[j];
+    const double rj = bj - ell_row<false>(A, V.x, j);
+    V.r[j] = rj;
+    V.rh[j] = rj;
+    V.k[j] = A.dinv[j] * rj;
+    dd_fma(acc[0], rj, rj);
+    dd_fma(acc[1], bj, bj);
+  }
+  Dd tot[2];
+  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_INIT1], tot) && threadIdx.x == 0) {
+    sc->tmp0 = dd_round(tot[0]);
+    sc->tmp1 = dd_round(tot[1]);
+  }
+}
+
+__global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                               Dd* __restrict__ part, Hist h) {
+  Dd acc[1] = {dd_zero()};
+  ROW_LOOP {
+    const double wj = ell_row<true>(A, V.r, j);  // w0 = A M^-1 r0 = A k0
+    V.w0[j] = wj;
+    dd_fma(acc[0], V.rh[j], wj);
+  }
+  Dd tot[1];
+  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_INIT2], tot) && threadIdx.x == 0) {
+    const double rho = sc->tmp0;
+    sc->rho = rho;
+    sc->alpha = rho / dd_round(tot[0]);
+    sc->beta = 0.0;
+    sc->omega = 0.0;
+    sc->h0 = sqrt(rho);
+    sc->nb = sqrt(sc->tmp1);
+    sc->tol_abs = sc->tol * sc->nb;
+    h.rnorm[0] = sc->h0;
+    if (sc->h0 <= sc->tol_abs && !sc->bench) {
+      sc->done = 1;
+      sc->outcome = OUT_CONVERGED;
+    } else if (!isfinite(sc->alpha)) {
+      sc->done = 1;
+      sc->outcome = OUT_BREAKDOWN;
+    }
+  }
+}
+
+// lines 5-12 with stored t_i, v_{i-1}; n_{i-1} = M^-1 z_{i-1} (pre-replacement, A26)
+__global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                                Dd* __restrict__ part) {
+  if (sc->done) return;
+  const int it = sc->iter;
+  const double al = sc->alpha, be = sc->beta, om = sc->omega;
+  const bool rr = sc->use_rr != 0;
+  Dd acc[2] = {dd_zero(), dd_zero()};
+  ROW_LOOP {
+    const double dj = A.dinv[j];
+    const double wc = V.w0[j], zc = V.z0[j];
+    const double zo = rr ? V.zrr[j] : zc;
+    const double m = dj * wc, n = dj * zc;
+    const double t = V.w1[j], v = V.z1[j];
+    const double lj = V.l[j];
+    const double gn = V.k[j] + be * (V.g[j] - om * lj);
+    const double sn = wc + be * (V.s[j] - om * zo);
+    const double ln = m + be * (lj - om * n);
+    const double zn = t + be * (zo - om * v);
+    const double q = V.r[j] - al * sn;
+    const double y = wc - al * zn;
+    dd_fma(acc[0], q, y);
+    dd_fma(acc[1], y, y);
+    V.g[j] = gn;
+    V.s[j] = sn;
+    V.l[j] = ln;
+    V.z0[j] = zn;
+  }
+  (void)it;
+  Dd tot[2];
+  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0) {
+    const double qy = dd_round(tot[0]), yy = dd_round(tot[1]);
+    const double omn = (yy == 0.0) ? 0.0 : qy / yy;
+    sc->omega = omn;
+    sc->use_rr = 0;
+    if (!isfinite(omn)) {
+      sc->done = 1;
+      sc->outcome = OUT_BREAKDOWN;
+      sc->iters = sc->iter;
+    }
+  }
+}
+
+// lines 13-14: n_i = M^-1 z_i, v_i = A n_i
+__global__ void __launch_bounds__(256) c_spmvB(CsrOp A, Vecs V, Scal* __restrict__ sc) {
+  if (sc->done) return;
+  ROW_LOOP { V.z1[j] = ell_row<true>(A, V.z0, j); }
+}
+
+// lines 17-21
+__global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                                Dd* __restrict__ part, Hist h) {
+  if (sc->done) return;
+  const double al = sc->alpha, om = sc->omega;
+  Dd acc[5] = {dd_zero(), dd_zero(), dd_zero(), dd_zero(), dd_zero()};
+  ROW_LOOP {
+    const double dj = A.dinv[j];
+    const double wc = V.w0[j], zc = V.z0[j];
+    const double m = dj * wc, n = dj * zc;
+    const double t = V.w1[j], v = V.z1[j];
+    const double sj = V.s[j];
+    const double u = V.k[j] - al * V.l[j];
+    const double q = V.r[j] - al * sj;
+    const double y = wc - al * zc;
+    const double xn = (V.x[j] + al * V.g[j]) + om * u;
+    const double rn = q - om * y;
+    const double kn = u - om * (m - al * n);
+    const double wn = y - om * (t - al * v);
+    const double rhj = V.rh[j];
+    dd_fma(acc[0], rhj, rn);
+    dd_fma(acc[1], rhj, wn);
+    dd_fma(acc[2], rhj, sj);
+    dd_fma(acc[3], rhj, zc);
+    dd_fma(acc[4], rn, rn);
+    V.x[j] = xn;
+    V.r[j] = rn;
+    V.k[j] = kn;
+    V.w0[j] = wn;
+  }
+  Dd tot[5];
+  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0) {
+    if (rr_scheduled(sc)) {
+      sc->rr_fire = 1;
+    } else {
+      finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
+                         dd_round(tot[3]), dd_round(tot[4]));
+    }
+  }
+}
+
+// eq:rr: r := b - A x; k := M^-1 r; s := A g; l := M^-1 s
+__global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__ sc) {
+  if (sc->done || !sc->rr_fire) return;
+  ROW_LOOP {
+    const double dj = A.dinv[j];
+    const double rj = V.b[j] - ell_row<false>(A, V.x, j);
+    const double sj = ell_row<false>(A, V.g, j);
+    V.r[j] = rj;
+    V.k[j] = dj * rj;
+    V.s[j] = sj;
+    V.l[j] = dj * sj;
+  }
+}
+
+// w := A k; z := A l (into zrr); line-21 dots on the replaced vectors
+__global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                             Dd* __restrict__ part, Hist h) {
+  if (sc->done || !sc->rr_fire) return;
+  Dd acc[5] = {dd_zero(), dd_zero(), dd_zero(), dd_zero(), dd_zero()};
+  ROW_LOOP {
+    const double wn = ell_row<true>(A, V.r, j);
+    const double zr = ell_row<true>(A, V.s, j);
+    V.w0[j] = wn;
+    V.zrr[j] = zr;
+    const double rhj = V.rh[j], rc = V.r[j];
+    dd_fma(acc[0], rhj, rc);
+    dd_fma(acc[1], rhj, wn);
+    dd_fma(acc[2], rhj, V.s[j]);
+    dd_fma(acc[3], rhj, zr);
+    dd_fma(acc[4], rc, rc);
+  }
+  Dd tot[5];
+  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_RR2], tot) && threadIdx.x == 0) {
+    finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
+                       dd_round(tot[3]), dd_round(tot[4]));
+    sc->use_rr = 1;
+  }
+}
+
+// lines 22-23: m_{i+1} = M^-1 w_{i+1}, t_{i+1} = A m_{i+1} (also t_0 at init)
+__global__ void __launch_bounds__(256) c_spmvD(CsrOp A, Vecs V, Scal* __restrict__ sc) {
+  if (sc->done) return;
+  ROW_LOOP { V.w1[j] = ell_row<true>(A, V.w0, j); }
+}
+
+__global__ void __launch_bounds__(256) c_gap(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                             Dd* __restrict__ part, Hist h) {
+  if (sc->gap_iter >= sc->iter) return;
+  Dd acc[1] = {dd_zero()};
+  ROW_LOOP {
+    const double d = (V.b[j] - ell_row<false>(A, V.x, j)) - V.r[j];
+    dd_fma(acc[0], d, d);
+  }
+  Dd tot[1];
+  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_GAP], tot) && threadIdx.x == 0) {
+    h.gap[sc->iter] = sqrt(dd_round(tot[0]));
+    sc->gap_iter = sc->iter;
+  }
+}
+
+__global__ void __launch_bounds__(256) c_apply(CsrOp A, const double* __restrict__ xin,
+                                               double* __restrict__ yout) {
+  ROW_LOOP { yout[j] = ell_row<false>(A, xin, j); }
+}

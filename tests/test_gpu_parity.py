@@ -1,0 +1,197 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.
+
+Bars (BASELINE.json north star): ||r_i|| within 1e-9 relative for i <= 30;
+final relative error within 10x of the oracle's; iteration count within +-2.
+Integer/structural results (SpMV with the same leg order, replacement zeroing
+the gap, iteration counts of bitwise-equal runs) are checked exactly.  The
+design target is bitwise equality (same operations in the same order; Dot2 makes
+the dot products order-insensitive), asserted where it is expected to hold.
+"""
+import numpy as np
+import pytest
+
+from paper_1809_01948_b200 import problems
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_1809_01948_b200 import Solver
+    assert torch.cuda.is_available()
+    return Solver
+
+
+def stencil_case(S, orc, dim, nx, ny, nz, coef, seed=0):
+    solver = S.stencil(dim, nx, ny, nz, coef)
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, seed)
+    xs_d = torch.from_numpy(xs).cuda()
+    b_d = solver.apply(xs_d)
+    b = orc.spmv(A, xs)
+    return solver, A, xs, b, b_d
+
+
+def check_parity(res, ref, xs, window=30, bitwise=True):
+    k = min(window, ref.iters, res.iters)
+    rel = np.abs(res.rnorm[:k + 1] - ref.rnorm[:k + 1]) / np.maximum(ref.rnorm[:k + 1], 1e-300)
+    assert np.all(rel <= 1e-9), f"||r_i|| rel diff {rel.max():.3e}"
+    assert abs(res.iters - ref.iters) <= 2, (res.iters, ref.iters)
+    x = res.x.cpu().numpy() if hasattr(res.x, "cpu") else res.x
+    e_gpu = np.linalg.norm(x - xs) / np.linalg.norm(xs)
+    e_ref = np.linalg.norm(ref.x - xs) / np.linalg.norm(xs)
+    assert e_gpu <= 10 * e_ref + 1e-15, (e_gpu, e_ref)
+    if bitwise:
+        assert res.iters == ref.iters
+        assert np.array_equal(res.rnorm, ref.rnorm), "rnorm not bitwise"
+        assert np.array_equal(x, ref.x), "x not bitwise"
+        if res.gap is not None and ref.gap is not None:
+            assert np.array_equal(res.gap, ref.gap), "gap not bitwise"
+
+
+SHAPES = [
+    (2, 100, 100, 1, "poisson"),     # cfg1 shape
+    (2, 37, 53, 1, "cd2"),           # ragged: nx not a multiple of 32
+    (2, 300, 7, 1, "cd2"),           # nx > block
+    (3, 13, 7, 19, "cd3"),           # ragged 3D
+    (3, 5, 6, 7, "cd3"),             # nx < 32
+    (3, 40, 33, 31, "cd3"),
+    (3, 1, 1, 1, "cd3"),             # N = 1
+    (2, 1, 9, 1, "poisson"),         # single column
+]
+
+
+def coef_of(kind):
+    return {"poisson": problems.poisson2d_coef(), "cd2": problems.cfg2_coef(),
+            "cd3": problems.cfg34_coef()}[kind]
+
+
+@pytest.mark.parametrize("dim,nx,ny,nz,kind", SHAPES)
+def test_apply_bitwise(S, orc, dim, nx, ny, nz, kind):
+    solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of(kind))
+    assert np.array_equal(b_d.cpu().numpy(), b)
+
+
+@pytest.mark.parametrize("dim,nx,ny,nz,kind", SHAPES)
+@pytest.mark.parametrize("rr", [0, 7])
+def test_solve_parity_stencil(S, orc, dim, nx, ny, nz, kind, rr):
+    solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of(kind))
+    maxit = 120
+    res = solver.solve(b_d, tol=1e-10, maxit=maxit, rr_period=rr, gap=True)
+    ref = orc.pbicgstab(A, b, tol=1e-10, maxit=maxit, rr_period=rr)
+    assert res.outcome == ref.outcome
+    check_parity(res, ref, xs)
+
+
+def test_cfg1_500_iterations_bench_mode(S, orc):
+    """cfg1: 100^2 Poisson, Jacobi, 500 fixed iterations (no early exit)."""
+    cfg = problems.configs()["cfg1"]
+    st = cfg.stencil
+    solver, A, xs, b, b_d = stencil_case(S, orc, st.dim, st.nx, st.ny, st.nz, st.coef)
+    solver.set_option("bench", 1)
+    for rr in (0, 50):
+        res = solver.solve(b_d, tol=0.0, maxit=500, rr_period=rr, gap=True)
+        ref = orc.pbicgstab(A, b, tol=0.0, maxit=500, rr_period=rr, bench=True)
+        assert res.iters == 500 and ref.iters == 500
+        check_parity(res, ref, xs)
+        if rr:
+            for it in range(rr, 501, rr):
+                if ref.rnorm[it - 1] >= np.sqrt(2.0 ** -53) * ref.rnorm[0] and ref.gap[it] == 0.0:
+                    assert res.gap[it] == 0.0
+
+
+def test_graphs_and_timing_modes_identical(S, orc):
+    solver, A, xs, b, b_d = stencil_case(S, orc, 3, 24, 20, 18, problems.cfg34_coef())
+    out = []
+    for graphs, timing in ((1, 0), (0, 0), (0, 1), (1, 1)):
+        solver.set_option("graphs", graphs)
+        solver.set_option("timing", timing)
+        r = solver.solve(b_d, tol=1e-10, maxit=300, rr_period=11, gap=True)
+        out.append(r)
+    for r in out[1:]:
+        assert r.iters == out[0].iters
+        assert np.array_equal(r.rnorm, out[0].rnorm)
+        assert np.array_equal(r.x.cpu().numpy(), out[0].x.cpu().numpy())
+    n, ms = solver.kernel_time("sweepC")
+    assert n > 0 and ms > 0
+
+
+def test_solve_host_matches_device(S, orc):
+    solver, A, xs, b, b_d = stencil_case(S, orc, 3, 16, 16, 16, problems.cfg34_coef())
+    r1 = solver.solve(b_d, tol=1e-10, maxit=200, rr_period=25)
+    r2 = solver.solve_host(b, tol=1e-10, maxit=200, rr_period=25)
+    assert r1.iters == r2.iters
+    assert np.array_equal(r1.rnorm, r2.rnorm)
+    assert np.array_equal(r1.x.cpu().numpy(), r2.x)
+
+
+def test_degenerate_cases(S, orc):
+    solver, A, xs, b, b_d = stencil_case(S, orc, 2, 33, 17, 1, problems.cfg2_coef())
+    z = torch.zeros_like(b_d)
+    r = solver.solve(z, tol=1e-10, maxit=10)
+    assert r.outcome == "converged" and r.iters == 0
+    assert torch.count_nonzero(r.x).item() == 0
+    r = solver.solve(b_d, tol=1e-10, maxit=0)
+    assert r.outcome == "maxit" and r.iters == 0 and r.rnorm.shape == (1,)
+    ref = orc.pbicgstab(A, b, tol=1e-10, maxit=0)
+    assert r.rnorm[0] == ref.rnorm[0]
+    # x0 = exact solution with exact integer data => r0 = 0 exactly
+    xi = np.arange(A.n, dtype=float)
+    bi = orc.spmv(A, xi)
+    r = solver.solve(torch.from_numpy(bi).cuda(), x0=torch.from_numpy(xi).cuda(), tol=0.0, maxit=3)
+    assert r.rnorm[0] == 0.0 and r.outcome == "converged"
+    # x_out may alias x0
+    x0 = torch.zeros_like(b_d)
+    r = solver.solve(b_d, x0=x0, tol=1e-8, maxit=100, x_out=x0)
+    ref = orc.pbicgstab(A, b, tol=1e-8, maxit=100)
+    assert np.array_equal(x0.cpu().numpy(), ref.x)
+
+
+def test_identity_stencil_lucky_breakdown(S, orc):
+    """A = I (centre 1, no legs): y0 = 0 => omega := 0, r1 = 0, converged in 1 (A9)."""
+    solver = S.stencil(3, 8, 8, 8, [1, 0, 0, 0, 0, 0, 0])
+    b = torch.from_numpy(problems.x_star(512, 3)).cuda()
+    r = solver.solve(b, tol=1e-14, maxit=5)
+    assert r.outcome == "converged" and r.iters == 1
+    assert torch.equal(r.x, b)
+
+
+def test_csr_parity(S, orc):
+    P = problems.csr_band(20000, nnz_row=27, band=500, seed=1)
+    solver = S.csr(P.n, P.row_ptr, P.col, P.val)
+    A = orc.csr(P.row_ptr, P.col, P.val)
+    xs = problems.x_star(P.n, 0)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    for rr in (0, 3):
+        res = solver.solve(b_d, tol=1e-12, maxit=100, rr_period=rr)
+        ref = orc.pbicgstab(A, b, tol=1e-12, maxit=100, rr_period=rr)
+        check_parity(res, ref, xs)
+
+
+def test_csr_ragged_rows(S, orc):
+    """Rows of different lengths (padded ELL slots are skipped, never added)."""
+    A0 = orc.stencil_csr(2, 23, 19, 1, problems.cfg2_coef())  # 3..5 entries per row
+    solver = S.csr(A0.n, A0.rp, A0.ci.astype(np.int32), A0.va)
+    xs = problems.x_star(A0.n, 1)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A0, xs)
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    res = solver.solve(b_d, tol=1e-11, maxit=300, rr_period=9)
+    ref = orc.pbicgstab(A0, b, tol=1e-11, maxit=300, rr_period=9)
+    check_parity(res, ref, xs)
+
+
+def test_cfg3_full_size_first_iterations(S, orc):
+    """cfg3 at full size (256^3) in the bench launch configuration: the first 3
+    iterations (with a replacement at i=1 via rr_period=2) against the oracle."""
+    st = problems.configs()["cfg3"].stencil
+    solver, A, xs, b, b_d = stencil_case(S, orc, st.dim, st.nx, st.ny, st.nz, st.coef)
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    res = solver.solve(b_d, tol=0.0, maxit=3, rr_period=2, gap=True)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=3, rr_period=2)
+    check_parity(res, ref, xs)
+    assert res.gap[2] == 0.0
