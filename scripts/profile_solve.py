@@ -1,0 +1,27 @@
+"""Small driver for ncu captures: one solve of a config through the public API."""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_1809_01948_b200 import Solver, problems  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="cfg4")
+ap.add_argument("--maxit", type=int, default=4)
+ap.add_argument("--rr", type=int, default=2)
+ap.add_argument("--gap", type=int, default=0)
+a = ap.parse_args()
+cfg = problems.configs()[a.config]
+st = cfg.stencil
+S = Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef)
+xs = torch.from_numpy(problems.x_star(st.n, 0)).cuda()
+b = S.apply(xs)
+S.set_option("bench", 1)
+S.set_option("graphs", 0)
+r = S.solve(b, tol=0.0, maxit=a.maxit, rr_period=a.rr, gap=bool(a.gap))
+print("iters", r.iters, r.outcome, r.rnorm[-1])
