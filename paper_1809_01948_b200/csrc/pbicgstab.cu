@@ -21,6 +21,7 @@
 #include "../../include/pbicgstab.h"
 #include "csr_kernels.cuh"
 #include "stencil_kernels.cuh"
+#include "tile_sweeps.cuh"
 
 namespace {
 
@@ -48,6 +49,10 @@ struct pbicg_ctx {
   cudaEvent_t ev_entry = nullptr, ev_poll[2] = {nullptr, nullptr};
   int64_t n_local = 0, row_begin = 0, n_global = 0, H = 0;
   Geo geo{};
+  TileGeo tg{};
+  bool tile_ok = false;  // TMA 2.5D sweeps eligible for this operator
+  int tile_on = 1;       // option "tile"
+  size_t tile_smem[2] = {0, 0};
   CsrOp csr{};
   std::vector<void*> allocs;
   Vecs V{};
@@ -179,11 +184,20 @@ void enq_init_stencil(pbicg_ctx* h) {
 
 template <int DIM>
 void enq_iter_stencil(pbicg_ctx* h, bool with_rr, bool with_gap) {
-  { LaunchScope ls(h, K_SWEEPA);
-    k_sweepA<DIM><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part); }
-  { LaunchScope ls(h, K_SWEEPC);
-    k_sweepC<DIM><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part,
-                                                                   h->hist); }
+  if (h->tile_ok && h->tile_on) {
+    { LaunchScope ls(h, K_SWEEPA);
+      t_sweep<DIM, 0><<<h->tg.units < h->num_sm ? h->tg.units : h->num_sm, TNT, h->tile_smem[0],
+                         h->stream>>>(h->tg, h->V, h->scal, h->part, h->hist); }
+    { LaunchScope ls(h, K_SWEEPC);
+      t_sweep<DIM, 1><<<h->tg.units < h->num_sm ? h->tg.units : h->num_sm, TNT, h->tile_smem[1],
+                         h->stream>>>(h->tg, h->V, h->scal, h->part, h->hist); }
+  } else {
+    { LaunchScope ls(h, K_SWEEPA);
+      k_sweepA<DIM><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part); }
+    { LaunchScope ls(h, K_SWEEPC);
+      k_sweepC<DIM><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part,
+                                                                     h->hist); }
+  }
   if (with_rr) {
     { LaunchScope ls(h, K_RR1);
       k_rr1<DIM><<<h->grid[K_RR1], h->block, 0, h->stream>>>(h->geo, h->V, h->scal); }
@@ -314,6 +328,84 @@ pbicg_status ensure_hist(pbicg_ctx* h, int64_t need) {
   return PBICG_OK;
 }
 
+// Tile geometry of the TMA 2.5D sweeps (tile_sweeps.cuh): TY full x-lines per
+// tile (3D) or one x-line (2D), a chunk of planes per work unit, units spread
+// statically over one CTA per SM (deterministic accumulation order).
+void setup_tile(pbicg_ctx* h) {
+  const Geo& g = h->geo;
+  TileGeo& t = h->tg;
+  h->tile_ok = false;
+  const int dim = h->dim;
+  const int64_t tpmax = 2LL * TNT * TKMAX;
+  if (g.nx > tpmax) return;
+  const int64_t lines = dim == 3 ? g.ny : 1;
+  int64_t TY = dim == 3 ? (1024 / g.nx) : 1;
+  if (TY < 1) TY = 1;
+  if (TY > lines) TY = lines;
+  int max_smem = 0;
+  cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+  const size_t reserve = 4096;  // static shared memory of the block reductions
+  for (; TY >= 1; --TY) {
+    t.nx = g.nx;
+    t.ny = lines;
+    t.nol = g.nol;
+    t.o0 = g.o0;
+    t.nog = g.nog;
+    t.pxy = g.pxy;
+    t.TY = (int32_t)TY;
+    t.halo = (int32_t)(dim == 3 ? g.nx + 2 : 2);
+    const int64_t TP = TY * g.nx;
+    t.st_stride = (int32_t)((TP + 2 + 1) & ~1LL);
+    t.sv_stride = (int32_t)((TP + 2 * t.halo + 2 + 1) & ~1LL);
+    if (tile_smem_bytes(t, 1) + reserve <= (size_t)max_smem &&
+        tile_smem_bytes(t, 0) + reserve <= (size_t)max_smem)
+      break;
+  }
+  if (TY < 1) return;
+  for (int i = 0; i < 7; ++i) t.c[i] = g.c[i];
+  t.dinv = g.dinv;
+  t.ncols = (int32_t)((lines + TY - 1) / TY);
+  // chunk count: minimise the idle fraction of the last round of units
+  const int grid = h->num_sm;
+  int64_t best_n = 1;
+  double best_w = 1e30;
+  for (int64_t nch = 1; nch <= g.nol; ++nch) {
+    const int64_t chunk = (g.nol + nch - 1) / nch;
+    const int64_t nchk = (g.nol + chunk - 1) / chunk;
+    const int64_t units = nchk * t.ncols;
+    const int64_t rounds = (units + grid - 1) / grid;
+    // work per CTA ~ rounds * (chunk + 2 prologue planes); ideal ~ units*chunk/grid
+    const double w = (double)rounds * (double)(chunk + 2) * 1.0;
+    if (w < best_w - 1e-9) {
+      best_w = w;
+      best_n = nch;
+    }
+    if (units > 64LL * grid) break;
+  }
+  t.chunk = (int32_t)((g.nol + best_n - 1) / best_n);
+  t.nchunks = (int32_t)((g.nol + t.chunk - 1) / t.chunk);
+  t.units = t.nchunks * t.ncols;
+  h->tile_smem[0] = tile_smem_bytes(t, 0);
+  h->tile_smem[1] = tile_smem_bytes(t, 1);
+  cudaError_t e1, e2;
+  if (dim == 3) {
+    e1 = cudaFuncSetAttribute(t_sweep<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)h->tile_smem[0]);
+    e2 = cudaFuncSetAttribute(t_sweep<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)h->tile_smem[1]);
+  } else {
+    e1 = cudaFuncSetAttribute(t_sweep<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)h->tile_smem[0]);
+    e2 = cudaFuncSetAttribute(t_sweep<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)h->tile_smem[1]);
+  }
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  h->tile_ok = true;
+}
+
 pbicg_status common_setup(pbicg_ctx* h, void* cuda_stream) {
   int ndev = 0;
   cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -399,7 +491,7 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
   h->n_local = g.nx * g.pxy / g.nx * g.nol;
   h->n_local = (op->dim == 3) ? g.pxy * g.nol : g.nx * g.nol;
   h->row_begin = g.o0 * g.pxy;
-  h->H = g.pxy;
+  h->H = g.pxy + g.nx + 4;  // ghost planes + staging slack of the tile kernels
   h->block = 256;
   if (g.nx < 256) h->block = (int)(((g.nx + 31) / 32) * 32);
   if (h->block < 64) h->block = 64;
@@ -427,7 +519,8 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
     h->grid[K_GAP] = occ_grid(h, k_gap<2>, L);
     h->grid[K_APPLY] = occ_grid(h, k_apply<2>, L);
   }
-  int gmax = 0;
+  setup_tile(h);
+  int gmax = h->num_sm;
   for (int k = 0; k < K_N; ++k) gmax = h->grid[k] > gmax ? h->grid[k] : gmax;
   void* p = nullptr;
   st = dalloc(h, &p, (size_t)gmax * 8 * sizeof(Dd));
@@ -580,6 +673,10 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
   else if (k == "graphs") h->use_graphs = value != 0;
   else if (k == "timing") h->timing = value != 0;
   else if (k == "overlap") h->overlap = value != 0;
+  else if (k == "tile") {
+    h->tile_on = value != 0;
+    destroy_graphs(h);
+  }
   else if (k == "schedule") {
     if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "schedule must be 0, 1 or 2");
     if (value == 1 && h->kind == KIND_CSR) return fail(h, PBICG_EINVAL, "fused schedule is stencil-only");

@@ -195,3 +195,17 @@ def test_cfg3_full_size_first_iterations(S, orc):
     ref = orc.pbicgstab(A, b, tol=0.0, maxit=3, rr_period=2)
     check_parity(res, ref, xs)
     assert res.gap[2] == 0.0
+
+
+@pytest.mark.parametrize("dim,nx,ny,nz,kind", [
+    (3, 40, 33, 31, "cd3"), (2, 100, 100, 1, "poisson"), (3, 13, 7, 19, "cd3"), (2, 37, 53, 1, "cd2"),
+    (3, 64, 64, 64, "cd3"), (2, 1024, 64, 1, "cd2"), (3, 3000, 2, 3, "cd3")])
+def test_tile_and_simple_kernels_agree_with_oracle(S, orc, dim, nx, ny, nz, kind):
+    """The TMA 2.5D sweeps (option tile=1) and the plain line sweeps (tile=0)
+    both reproduce the oracle, with and without replacement."""
+    solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of(kind))
+    ref = orc.pbicgstab(A, b, tol=1e-11, maxit=150, rr_period=6)
+    for tile in (1, 0):
+        solver.set_option("tile", tile)
+        res = solver.solve(b_d, tol=1e-11, maxit=150, rr_period=6, gap=True)
+        check_parity(res, ref, xs)
