@@ -108,6 +108,29 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
 pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pbicg_dist* dist,
                                   void* cuda_stream, pbicg_handle* out);
 
+/* Rank emulation on ONE device (testing the multi-rank path without several
+ * GPUs): creates `nranks` handles out[0..nranks-1] that partition the operator
+ * exactly as nranks processes would (slabs / the given CSR row blocks), share
+ * one stream, and exchange halos and dot-product rows with device-to-device
+ * copies instead of NCCL (loopback transport).  Kernels of different ranks never
+ * wait on each other: everything is ordered on the one stream.
+ * _csr_loopback takes ops[nranks] with contiguous ordered row blocks. */
+pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_prec prec,
+                                               int32_t nranks, void* cuda_stream,
+                                               pbicg_handle* out);
+pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec, int32_t nranks,
+                                           void* cuda_stream, pbicg_handle* out);
+/* y = A x on a loopback group: x_dev[r], y_dev[r] are rank r's rows. */
+pbicg_status pbicgstab_apply_loopback(pbicg_handle* hs, int32_t nranks, const double* const* x_dev,
+                                      double* const* y_dev);
+/* pbicgstab_solve over a loopback group (per-rank b, x0, x pointers; one
+ * history, identical for every rank). */
+pbicg_status pbicgstab_solve_loopback(pbicg_handle* hs, int32_t nranks,
+                                      const double* const* b_dev, const double* const* x0_dev,
+                                      double tol, int32_t maxit, int32_t rr_period,
+                                      double* const* x_dev_out, double* rnorm_hist,
+                                      double* gap_hist, int32_t* iters_out, int32_t* outcome_out);
+
 /* Global rows owned by this rank: [row_begin, row_begin + n_local). */
 pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n_local);
 
@@ -118,6 +141,8 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *                read with pbicgstab_kernel_time
  *   "overlap"    1 (default) => multi-GPU: reductions overlap the SpMV (split
  *                schedule); 0 => blocking
+ *   "tile"       1 (default) => stencil sweeps use the TMA-staged 2.5D kernels when
+ *                the grid fits (nx <= 2048); 0 => plain line kernels (same results)
  *   "schedule"   0 (default) auto, 1 fused 2-sweep (stencil only), 2 split 4-phase
  * Errors: EINVAL for an unknown key or bad value. */
 pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value);
@@ -156,7 +181,7 @@ pbicg_status pbicgstab_solve_host(pbicg_handle h, const double* b_host, const do
 
 /* Per-kernel statistics since the last reset (reset = 1 clears them).
  *   name: "init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap",
- *   "apply", or "all" (launch count only; time = NaN).
+ *   "apply", "fin" (multi-rank scalar finalisation), or "all".
  *   launches: kernel launches issued (graph nodes count once per replay);
  *   ms: summed CUDA-event time (only with option "timing"; else NaN). */
 pbicg_status pbicgstab_kernel_time(pbicg_handle h, const char* name, int64_t* launches,

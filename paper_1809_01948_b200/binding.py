@@ -42,7 +42,9 @@ class _Dist(ctypes.Structure):
                 ("nccl_id_halo", ctypes.c_void_p), ("nccl_id_red", ctypes.c_void_p)]
 
 
-SYMBOLS = ["pbicgstab_create_stencil", "pbicgstab_create_csr", "pbicgstab_local_rows",
+SYMBOLS = ["pbicgstab_create_stencil", "pbicgstab_create_csr", "pbicgstab_create_stencil_loopback",
+           "pbicgstab_create_csr_loopback", "pbicgstab_apply_loopback", "pbicgstab_solve_loopback",
+           "pbicgstab_local_rows",
            "pbicgstab_set_option", "pbicgstab_apply", "pbicgstab_solve", "pbicgstab_solve_host",
            "pbicgstab_kernel_time", "pbicgstab_kernel_bytes", "pbicgstab_get_unique_id",
            "pbicgstab_last_error", "pbicgstab_destroy"]
@@ -69,6 +71,12 @@ def lib(build: bool = True):
                                            ctypes.POINTER(_Dist), P, ctypes.POINTER(P)]
     L.pbicgstab_create_csr.argtypes = [ctypes.POINTER(_Csr), ctypes.c_int,
                                        ctypes.POINTER(_Dist), P, ctypes.POINTER(P)]
+    L.pbicgstab_create_stencil_loopback.argtypes = [ctypes.POINTER(_Stencil), ctypes.c_int, i32, P,
+                                                    P]
+    L.pbicgstab_create_csr_loopback.argtypes = [P, ctypes.c_int, i32, P, P]
+    L.pbicgstab_apply_loopback.argtypes = [P, i32, P, P]
+    L.pbicgstab_solve_loopback.argtypes = [P, i32, P, P, f64, i32, i32, P, P, P,
+                                           ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.pbicgstab_local_rows.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.pbicgstab_set_option.argtypes = [P, ctypes.c_char_p, i64]
     L.pbicgstab_apply.argtypes = [P, P, P]
@@ -228,3 +236,76 @@ class Solver:
 
     def __exit__(self, *a):
         self.close()
+
+
+class LoopbackGroup:
+    """P ranks of the multi-GPU path emulated on one device (loopback transport):
+    the same partition, halo plan, rank-row reductions and finalize kernels as
+    the NCCL path, with device-to-device copies in place of NCCL."""
+
+    def __init__(self, handles):
+        self._hs = handles  # ctypes array of c_void_p
+        self.P = len(handles)
+        self.ranks = [Solver(ctypes.c_void_p(h)) for h in handles]
+
+    @classmethod
+    def stencil(cls, nranks: int, dim: int, nx: int, ny: int, nz: int, coef, stream=None):
+        st = _Stencil(dim, nx, ny, nz if dim == 3 else 1,
+                      (ctypes.c_double * 7)(*[float(c) for c in coef]))
+        hs = (ctypes.c_void_p * nranks)()
+        _check(lib().pbicgstab_create_stencil_loopback(ctypes.byref(st), 1, nranks,
+                                                       _stream_ptr(stream), hs))
+        return cls(hs)
+
+    @classmethod
+    def csr(cls, blocks, n_global: int, stream=None):
+        """blocks: list of (row_begin, row_ptr, col, val) per rank, contiguous."""
+        keep = []
+        arr = (_Csr * len(blocks))()
+        for r, (rb, rp, ci, va) in enumerate(blocks):
+            rp = np.ascontiguousarray(rp, dtype=np.int64)
+            ci = np.ascontiguousarray(ci, dtype=np.int32)
+            va = np.ascontiguousarray(va, dtype=np.float64)
+            keep += [rp, ci, va]
+            arr[r] = _Csr(n_global, rb, len(rp) - 1, rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
+        hs = (ctypes.c_void_p * len(blocks))()
+        _check(lib().pbicgstab_create_csr_loopback(arr, 1, len(blocks), _stream_ptr(stream), hs))
+        return cls(hs)
+
+    def set_option(self, key, value):
+        self.ranks[0].set_option(key, value)  # applies to every member
+
+    def split(self, v):
+        return [v[s.row_begin:s.row_begin + s.n_local].contiguous() for s in self.ranks]
+
+    def apply(self, xs):
+        import torch
+        ys = [torch.empty_like(x) for x in xs]
+        xa = (ctypes.c_void_p * self.P)(*[_dptr(x, s.n_local, "x").value for x, s in zip(xs, self.ranks)])
+        ya = (ctypes.c_void_p * self.P)(*[_dptr(y, s.n_local, "y").value for y, s in zip(ys, self.ranks)])
+        _check(lib().pbicgstab_apply_loopback(self._hs, self.P, xa, ya), self._hs[0])
+        return ys
+
+    def solve(self, bs, x0s=None, tol=1e-10, maxit=1000, rr_period=0, gap=True):
+        import torch
+        if x0s is None:
+            x0s = [torch.zeros_like(b) for b in bs]
+        xs = [torch.empty_like(b) for b in bs]
+        ptr = lambda ts, nm: (ctypes.c_void_p * self.P)(
+            *[_dptr(t, s.n_local, nm).value for t, s in zip(ts, self.ranks)])
+        rh = np.full(maxit + 1, np.nan)
+        gh = np.full(maxit + 1, np.nan) if gap else None
+        it, oc = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().pbicgstab_solve_loopback(
+            self._hs, self.P, ptr(bs, "b"), ptr(x0s, "x0"), float(tol), int(maxit),
+            int(rr_period), ptr(xs, "x"), rh.ctypes.data_as(ctypes.c_void_p),
+            None if gh is None else gh.ctypes.data_as(ctypes.c_void_p),
+            ctypes.byref(it), ctypes.byref(oc)), self._hs[0])
+        k = it.value
+        return SolveResult(torch.cat(xs), rh[:k + 1], None if gh is None else gh[:k + 1], k,
+                           OUTCOMES[oc.value])
+
+    def close(self):
+        for s in reversed(self.ranks):
+            s.close()
+        self.ranks = []

@@ -41,7 +41,7 @@ __device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restri
                       j += (int64_t)gridDim.x * blockDim.x)
 
 __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict__ sc,
-                                               Dd* __restrict__ part) {
+                                               Dd* __restrict__ part, Hist h) {
   Dd acc[2] = {dd_zero(), dd_zero()};
   ROW_LOOP {
     const double bj = V.b[j];
@@ -53,10 +53,8 @@ __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict
     dd_fma(acc[1], bj, bj);
   }
   Dd tot[2];
-  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_INIT1], tot) && threadIdx.x == 0) {
-    sc->tmp0 = dd_round(tot[0]);
-    sc->tmp1 = dd_round(tot[1]);
-  }
+  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_INIT1], tot) && threadIdx.x == 0)
+    publish<F_INIT1>(sc, h, tot);
 }
 
 __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict__ sc,
@@ -68,31 +66,14 @@ __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict
     dd_fma(acc[0], V.rh[j], wj);
   }
   Dd tot[1];
-  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_INIT2], tot) && threadIdx.x == 0) {
-    const double rho = sc->tmp0;
-    sc->rho = rho;
-    sc->alpha = rho / dd_round(tot[0]);
-    sc->beta = 0.0;
-    sc->omega = 0.0;
-    sc->h0 = sqrt(rho);
-    sc->nb = sqrt(sc->tmp1);
-    sc->tol_abs = sc->tol * sc->nb;
-    h.rnorm[0] = sc->h0;
-    if (sc->h0 <= sc->tol_abs && !sc->bench) {
-      sc->done = 1;
-      sc->outcome = OUT_CONVERGED;
-    } else if (!isfinite(sc->alpha)) {
-      sc->done = 1;
-      sc->outcome = OUT_BREAKDOWN;
-    }
-  }
+  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_INIT2], tot) && threadIdx.x == 0)
+    publish<F_INIT2>(sc, h, tot);
 }
 
 // lines 5-12 with stored t_i, v_{i-1}; n_{i-1} = M^-1 z_{i-1} (pre-replacement, A26)
 __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restrict__ sc,
-                                                Dd* __restrict__ part) {
+                                                Dd* __restrict__ part, Hist h) {
   if (sc->done) return;
-  const int it = sc->iter;
   const double al = sc->alpha, be = sc->beta, om = sc->omega;
   const bool rr = sc->use_rr != 0;
   Dd acc[2] = {dd_zero(), dd_zero()};
@@ -116,19 +97,9 @@ __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restric
     V.l[j] = ln;
     V.z0[j] = zn;
   }
-  (void)it;
   Dd tot[2];
-  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0) {
-    const double qy = dd_round(tot[0]), yy = dd_round(tot[1]);
-    const double omn = (yy == 0.0) ? 0.0 : qy / yy;
-    sc->omega = omn;
-    sc->use_rr = 0;
-    if (!isfinite(omn)) {
-      sc->done = 1;
-      sc->outcome = OUT_BREAKDOWN;
-      sc->iters = sc->iter;
-    }
-  }
+  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
+    publish<F_SWEEPA>(sc, h, tot);
 }
 
 // lines 13-14: n_i = M^-1 z_i, v_i = A n_i
@@ -168,14 +139,8 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
     V.w0[j] = wn;
   }
   Dd tot[5];
-  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0) {
-    if (rr_scheduled(sc)) {
-      sc->rr_fire = 1;
-    } else {
-      finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
-                         dd_round(tot[3]), dd_round(tot[4]));
-    }
-  }
+  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0)
+    publish<F_SWEEPC>(sc, h, tot);
 }
 
 // eq:rr: r := b - A x; k := M^-1 r; s := A g; l := M^-1 s
@@ -210,11 +175,8 @@ __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__
     dd_fma(acc[4], rc, rc);
   }
   Dd tot[5];
-  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_RR2], tot) && threadIdx.x == 0) {
-    finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
-                       dd_round(tot[3]), dd_round(tot[4]));
-    sc->use_rr = 1;
-  }
+  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_RR2], tot) && threadIdx.x == 0)
+    publish<F_RR2>(sc, h, tot);
 }
 
 // lines 22-23: m_{i+1} = M^-1 w_{i+1}, t_{i+1} = A m_{i+1} (also t_0 at init)
@@ -232,10 +194,8 @@ __global__ void __launch_bounds__(256) c_gap(CsrOp A, Vecs V, Scal* __restrict__
     dd_fma(acc[0], d, d);
   }
   Dd tot[1];
-  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_GAP], tot) && threadIdx.x == 0) {
-    h.gap[sc->iter] = sqrt(dd_round(tot[0]));
-    sc->gap_iter = sc->iter;
-  }
+  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_GAP], tot) && threadIdx.x == 0)
+    publish<F_GAP>(sc, h, tot);
 }
 
 __global__ void __launch_bounds__(256) c_apply(CsrOp A, const double* __restrict__ xin,

@@ -3,16 +3,19 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -fmad=false
 // (no FMA contraction anywhere: reading A4).
 //
-// Host responsibilities only: validation, workspace allocation, launch order,
-// CUDA-graph capture/replay of chunks of iterations, asynchronous polling of the
-// device `done` flag, history download.  Every arithmetic step of Alg. 2 runs in
-// the kernels of stencil_kernels.cuh / csr_kernels.cuh.
+// Host responsibilities only: validation, partitioning, workspace allocation,
+// launch order, the rank exchange (NCCL across processes, or the loopback
+// transport that emulates P ranks inside one process), CUDA-graph capture/replay
+// of chunks of iterations, asynchronous polling of the device `done` flag,
+// history download.  Every arithmetic step of Alg. 2 runs in the kernels of
+// stencil_kernels.cuh / tile_sweeps.cuh / csr_kernels.cuh.
 #include <cuda_runtime.h>
 
 #include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <string>
 #include <tuple>
@@ -20,6 +23,7 @@
 
 #include "../../include/pbicgstab.h"
 #include "csr_kernels.cuh"
+#include "nccl_dyn.h"
 #include "stencil_kernels.cuh"
 #include "tile_sweeps.cuh"
 
@@ -27,9 +31,10 @@ namespace {
 
 thread_local std::string g_create_err;
 
-enum Kname { K_INIT = 0, K_SWEEPA, K_SWEEPC, K_SPMVB, K_SPMVD, K_RR1, K_RR2, K_GAP, K_APPLY, K_N };
+enum Kname { K_INIT = 0, K_SWEEPA, K_SWEEPC, K_SPMVB, K_SPMVD, K_RR1, K_RR2, K_GAP, K_APPLY, K_FIN,
+             K_N };
 const char* kname_str[K_N] = {"init", "sweepA", "sweepC", "spmvB", "spmvD",
-                              "rr1",  "rr2",    "gap",    "apply"};
+                              "rr1",  "rr2",    "gap",    "apply", "fin"};
 
 struct TimedLaunch {
   int k;
@@ -37,17 +42,22 @@ struct TimedLaunch {
 };
 
 enum Kind { KIND_STENCIL = 0, KIND_CSR = 1 };
+enum Comm { COMM_NONE = 0, COMM_NCCL = 1, COMM_LOOP = 2 };
 
 }  // namespace
+
+struct pbicg_group;
 
 struct pbicg_ctx {
   int kind = KIND_STENCIL;
   int dim = 3;
   int device = 0, num_sm = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr, side = nullptr;
   bool own_stream = false;
   cudaEvent_t ev_entry = nullptr, ev_poll[2] = {nullptr, nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t n_local = 0, row_begin = 0, n_global = 0, H = 0;
+  int64_t halo_n = 0;  // rows exchanged per side with each neighbour
   Geo geo{};
   TileGeo tg{};
   bool tile_ok = false;  // TMA 2.5D sweeps eligible for this operator
@@ -56,25 +66,39 @@ struct pbicg_ctx {
   CsrOp csr{};
   std::vector<void*> allocs;
   Vecs V{};
-  double* xtmp = nullptr;  // ghosted scratch for pbicgstab_apply
+  double* xtmp = nullptr;    // ghosted scratch (apply input, host-solve staging)
+  double* dinv_g = nullptr;  // CSR: ghosted dinv
   Scal* scal = nullptr;
-  Scal* scal_host = nullptr;  // pinned, [2] (poll double buffer)
+  Scal* scal_host = nullptr;  // pinned [2] (poll double buffer)
   Dd* part = nullptr;
+  Dd *red_send = nullptr, *red_recv = nullptr;
   Hist hist{nullptr, nullptr};
   int64_t hist_cap = 0;
   int block = 256;
-  int grid[K_N] = {0};
+  int grid[16] = {0};
+  // distribution
+  int nranks = 1, rank = 0;
+  int comm = COMM_NONE;
+  ncclComm_t nccl_halo = nullptr, nccl_red = nullptr;
+  pbicg_group* group = nullptr;
   // options
   int bench = 0, use_graphs = 1, timing = 0, overlap = 1, schedule = 0, gap_on = 0;
-  int rr_period_cur = 0;
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
   std::vector<TimedLaunch> pending;
   std::vector<cudaEvent_t> ev_pool;
-  int64_t launches[K_N] = {0};
-  double ms[K_N] = {0};
+  int64_t launches[16] = {0};
+  double ms[16] = {0};
   bool failed = false;
   std::string err;
 };
+
+// P handles emulating P ranks in one process on one device (loopback transport).
+struct pbicg_group {
+  std::vector<pbicg_ctx*> m;
+  int alive = 0;
+};
+
+using Members = std::vector<pbicg_ctx*>;
 
 namespace {
 
@@ -95,6 +119,21 @@ pbicg_status fail(pbicg_ctx* h, pbicg_status st, const std::string& msg) {
     }                                                                                    \
   } while (0)
 
+#define NC(call)                                                      \
+  do {                                                                \
+    ncclResult_t r_ = (call);                                         \
+    if (r_ != ncclSuccess) {                                          \
+      return fail(h, PBICG_ENCCL,                                     \
+                  std::string(#call) + ": " + nccl_api().GetErrorString(r_)); \
+    }                                                                 \
+  } while (0)
+
+#define ST(call)                   \
+  do {                             \
+    pbicg_status s_ = (call);      \
+    if (s_ != PBICG_OK) return s_; \
+  } while (0)
+
 pbicg_status dalloc(pbicg_ctx* h, void** p, size_t bytes) {
   cudaError_t e = cudaMalloc(p, bytes ? bytes : 8);
   if (e != cudaSuccess) {
@@ -110,8 +149,7 @@ pbicg_status dalloc(pbicg_ctx* h, void** p, size_t bytes) {
 pbicg_status gvec(pbicg_ctx* h, double** out) {
   void* p = nullptr;
   size_t n = (size_t)(h->n_local + 2 * h->H);
-  pbicg_status st = dalloc(h, &p, n * sizeof(double));
-  if (st) return st;
+  ST(dalloc(h, &p, n * sizeof(double)));
   CU(cudaMemsetAsync(p, 0, n * sizeof(double), h->stream));
   *out = (double*)p + h->H;
   return PBICG_OK;
@@ -171,141 +209,290 @@ void collect_timing(pbicg_ctx* h) {
   cudaGetLastError();
 }
 
+Members members(pbicg_ctx* h) {
+  if (h->comm == COMM_LOOP && h->group) return h->group->m;
+  return Members{h};
+}
+
 // ---------------------------------------------------------------------------
-// enqueue helpers (stencil, fused 2-sweep schedule; CSR, split 4-phase)
-template <int DIM>
-void enq_init_stencil(pbicg_ctx* h) {
-  { LaunchScope ls(h, K_INIT);
-    k_init1<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part); }
-  { LaunchScope ls(h, K_INIT);
-    k_init2<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part,
-                                                                h->hist); }
-}
+// Kernel launches (one rank)
+enum Phase { PH_INIT1, PH_INIT2, PH_SWEEPA, PH_SPMVB, PH_SWEEPC, PH_RR1, PH_RR2, PH_SPMVD, PH_GAP };
 
 template <int DIM>
-void enq_iter_stencil(pbicg_ctx* h, bool with_rr, bool with_gap) {
-  if (h->tile_ok && h->tile_on) {
-    { LaunchScope ls(h, K_SWEEPA);
-      t_sweep<DIM, 0><<<h->tg.units < h->num_sm ? h->tg.units : h->num_sm, TNT, h->tile_smem[0],
-                         h->stream>>>(h->tg, h->V, h->scal, h->part, h->hist); }
-    { LaunchScope ls(h, K_SWEEPC);
-      t_sweep<DIM, 1><<<h->tg.units < h->num_sm ? h->tg.units : h->num_sm, TNT, h->tile_smem[1],
-                         h->stream>>>(h->tg, h->V, h->scal, h->part, h->hist); }
+void launch_stencil(pbicg_ctx* h, Phase p) {
+  const Geo& g = h->geo;
+  const bool tile = h->tile_ok && h->tile_on;
+  const int tgrid = h->tg.units < h->num_sm ? h->tg.units : h->num_sm;
+  switch (p) {
+    case PH_INIT1: {
+      LaunchScope ls(h, K_INIT);
+      k_init1<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_INIT2: {
+      LaunchScope ls(h, K_INIT);
+      k_init2<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_SWEEPA: {
+      LaunchScope ls(h, K_SWEEPA);
+      if (tile)
+        t_sweep<DIM, 0><<<tgrid, TNT, h->tile_smem[0], h->stream>>>(h->tg, h->V, h->scal, h->part,
+                                                                    h->hist);
+      else
+        k_sweepA<DIM><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
+                                                                       h->hist);
+    } break;
+    case PH_SWEEPC: {
+      LaunchScope ls(h, K_SWEEPC);
+      if (tile)
+        t_sweep<DIM, 1><<<tgrid, TNT, h->tile_smem[1], h->stream>>>(h->tg, h->V, h->scal, h->part,
+                                                                    h->hist);
+      else
+        k_sweepC<DIM><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
+                                                                       h->hist);
+    } break;
+    case PH_RR1: {
+      LaunchScope ls(h, K_RR1);
+      k_rr1<DIM><<<h->grid[K_RR1], h->block, 0, h->stream>>>(g, h->V, h->scal);
+    } break;
+    case PH_RR2: {
+      LaunchScope ls(h, K_RR2);
+      k_rr2<DIM><<<h->grid[K_RR2], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_GAP: {
+      LaunchScope ls(h, K_GAP);
+      k_gap<DIM><<<h->grid[K_GAP], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+    } break;
+    default:
+      break;
+  }
+}
+
+void launch_csr(pbicg_ctx* h, Phase p) {
+  const CsrOp& A = h->csr;
+  switch (p) {
+    case PH_INIT1: {
+      LaunchScope ls(h, K_INIT);
+      c_init1<<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_INIT2: {
+      LaunchScope ls(h, K_INIT);
+      c_init2<<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_SWEEPA: {
+      LaunchScope ls(h, K_SWEEPA);
+      c_sweepA<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_SPMVB: {
+      LaunchScope ls(h, K_SPMVB);
+      c_spmvB<<<h->grid[K_SPMVB], h->block, 0, h->stream>>>(A, h->V, h->scal);
+    } break;
+    case PH_SWEEPC: {
+      LaunchScope ls(h, K_SWEEPC);
+      c_sweepC<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_RR1: {
+      LaunchScope ls(h, K_RR1);
+      c_rr1<<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal);
+    } break;
+    case PH_RR2: {
+      LaunchScope ls(h, K_RR2);
+      c_rr2<<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_SPMVD: {
+      LaunchScope ls(h, K_SPMVD);
+      c_spmvD<<<h->grid[K_SPMVD], h->block, 0, h->stream>>>(A, h->V, h->scal);
+    } break;
+    case PH_GAP: {
+      LaunchScope ls(h, K_GAP);
+      c_gap<<<h->grid[K_GAP], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+    } break;
+  }
+}
+
+void launch(pbicg_ctx* h, Phase p) {
+  if (h->kind == KIND_CSR) launch_csr(h, p);
+  else if (h->dim == 3) launch_stencil<3>(h, p);
+  else launch_stencil<2>(h, p);
+}
+
+void launch_fin(pbicg_ctx* h, int f) {
+  LaunchScope ls(h, K_FIN);
+  switch (f) {
+    case F_INIT1: k_fin<F_INIT1, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_INIT2: k_fin<F_INIT2, 1><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_SWEEPA: k_fin<F_SWEEPA, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_SWEEPC: k_fin<F_SWEEPC, 5><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_RR2: k_fin<F_RR2, 5><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_GAP: k_fin<F_GAP, 1><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Rank exchange.  Enqueue-only (no host synchronisation); graph-capturable.
+using VecSel = std::function<double*(pbicg_ctx*)>;
+
+// exchange the rank rows of the Dot2 partials (exact all-gather: every row but
+// the owner's is zero in red_send, so the sum adds exact zeros)
+void comm_reduce(const Members& G, bool on_side) {
+  pbicg_ctx* h0 = G[0];
+  if (h0->nranks == 1) return;
+  if (h0->comm == COMM_NCCL) {
+    pbicg_ctx* h = h0;
+    cudaStream_t s = on_side ? h->side : h->stream;
+    nccl_api().AllReduce(h->red_send, h->red_recv, (size_t)h->nranks * RED_K * 2, ncclDouble,
+                         ncclSum, on_side ? h->nccl_red : h->nccl_halo, s);
   } else {
-    { LaunchScope ls(h, K_SWEEPA);
-      k_sweepA<DIM><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part); }
-    { LaunchScope ls(h, K_SWEEPC);
-      k_sweepC<DIM><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part,
-                                                                     h->hist); }
-  }
-  if (with_rr) {
-    { LaunchScope ls(h, K_RR1);
-      k_rr1<DIM><<<h->grid[K_RR1], h->block, 0, h->stream>>>(h->geo, h->V, h->scal); }
-    { LaunchScope ls(h, K_RR2);
-      k_rr2<DIM><<<h->grid[K_RR2], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part,
-                                                               h->hist); }
-  }
-  if (with_gap) {
-    LaunchScope ls(h, K_GAP);
-    k_gap<DIM><<<h->grid[K_GAP], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part,
-                                                             h->hist);
+    cudaStream_t s = on_side ? h0->side : h0->stream;
+    for (pbicg_ctx* d : G)
+      for (pbicg_ctx* src : G)
+        cudaMemcpyAsync(d->red_recv + (size_t)src->rank * RED_K,
+                        src->red_send + (size_t)src->rank * RED_K, RED_K * sizeof(Dd),
+                        cudaMemcpyDeviceToDevice, s);
   }
 }
 
-void enq_gap(pbicg_ctx* h) {
-  if (h->kind == KIND_CSR) {
-    LaunchScope ls(h, K_GAP);
-    c_gap<<<h->grid[K_GAP], h->block, 0, h->stream>>>(h->csr, h->V, h->scal, h->part, h->hist);
-  } else if (h->dim == 3) {
-    LaunchScope ls(h, K_GAP);
-    k_gap<3><<<h->grid[K_GAP], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part, h->hist);
+// nearest-neighbour ghost exchange of halo_n rows per side for each vector
+void comm_halo(const Members& G, std::initializer_list<VecSel> sels) {
+  pbicg_ctx* h0 = G[0];
+  if (h0->nranks == 1) return;
+  if (h0->comm == COMM_NCCL) {
+    pbicg_ctx* h = h0;
+    auto& api = nccl_api();
+    api.GroupStart();
+    for (auto& sel : sels) {
+      double* v = sel(h);
+      if (h->rank > 0) {
+        api.Send(v, h->halo_n, ncclDouble, h->rank - 1, h->nccl_halo, h->stream);
+        api.Recv(v - h->halo_n, h->halo_n, ncclDouble, h->rank - 1, h->nccl_halo, h->stream);
+      }
+      if (h->rank < h->nranks - 1) {
+        api.Send(v + h->n_local - h->halo_n, h->halo_n, ncclDouble, h->rank + 1, h->nccl_halo,
+                 h->stream);
+        api.Recv(v + h->n_local, h->halo_n, ncclDouble, h->rank + 1, h->nccl_halo, h->stream);
+      }
+    }
+    api.GroupEnd();
   } else {
-    LaunchScope ls(h, K_GAP);
-    k_gap<2><<<h->grid[K_GAP], h->block, 0, h->stream>>>(h->geo, h->V, h->scal, h->part, h->hist);
+    const size_t nb = (size_t)h0->halo_n * sizeof(double);
+    for (auto& sel : sels) {
+      for (size_t r = 0; r < G.size(); ++r) {
+        pbicg_ctx* me = G[r];
+        double* v = sel(me);
+        if (r > 0) {  // my first rows -> left neighbour's upper ghost
+          pbicg_ctx* nbr = G[r - 1];
+          cudaMemcpyAsync(sel(nbr) + nbr->n_local, v, nb, cudaMemcpyDeviceToDevice, h0->stream);
+        }
+        if (r + 1 < G.size()) {  // my last rows -> right neighbour's lower ghost
+          pbicg_ctx* nbr = G[r + 1];
+          cudaMemcpyAsync(sel(nbr) - nbr->halo_n, v + me->n_local - me->halo_n, nb,
+                          cudaMemcpyDeviceToDevice, h0->stream);
+        }
+      }
+    }
   }
 }
 
-void enq_init_csr(pbicg_ctx* h) {
-  { LaunchScope ls(h, K_INIT);
-    c_init1<<<h->grid[K_INIT], h->block, 0, h->stream>>>(h->csr, h->V, h->scal, h->part); }
-  { LaunchScope ls(h, K_INIT);
-    c_init2<<<h->grid[K_INIT], h->block, 0, h->stream>>>(h->csr, h->V, h->scal, h->part, h->hist); }
-  { LaunchScope ls(h, K_SPMVD);  // t_0 = A m_0 (line 3)
-    c_spmvD<<<h->grid[K_SPMVD], h->block, 0, h->stream>>>(h->csr, h->V, h->scal); }
+void each(const Members& G, Phase p) {
+  for (pbicg_ctx* h : G) launch(h, p);
+}
+void each_fin(const Members& G, int f) {
+  if (G[0]->nranks == 1) return;
+  for (pbicg_ctx* h : G) launch_fin(h, f);
+}
+void reduce_fin(const Members& G, int f) {
+  if (G[0]->nranks == 1) return;
+  comm_reduce(G, false);
+  each_fin(G, f);
 }
 
-void enq_iter_csr(pbicg_ctx* h, bool with_rr, bool with_gap) {
-  { LaunchScope ls(h, K_SWEEPA);
-    c_sweepA<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(h->csr, h->V, h->scal, h->part); }
-  { LaunchScope ls(h, K_SPMVB);
-    c_spmvB<<<h->grid[K_SPMVB], h->block, 0, h->stream>>>(h->csr, h->V, h->scal); }
-  { LaunchScope ls(h, K_SWEEPC);
-    c_sweepC<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(h->csr, h->V, h->scal, h->part, h->hist); }
-  if (with_rr) {
-    { LaunchScope ls(h, K_RR1);
-      c_rr1<<<h->grid[K_RR1], h->block, 0, h->stream>>>(h->csr, h->V, h->scal); }
-    { LaunchScope ls(h, K_RR2);
-      c_rr2<<<h->grid[K_RR2], h->block, 0, h->stream>>>(h->csr, h->V, h->scal, h->part, h->hist); }
+const VecSel SX = [](pbicg_ctx* h) { return h->V.x; };
+const VecSel SG = [](pbicg_ctx* h) { return h->V.g; };
+const VecSel SR = [](pbicg_ctx* h) { return h->V.r; };
+const VecSel SS = [](pbicg_ctx* h) { return h->V.s; };
+const VecSel SW0 = [](pbicg_ctx* h) { return h->V.w0; };
+const VecSel SW1 = [](pbicg_ctx* h) { return h->V.w1; };
+const VecSel SZ0 = [](pbicg_ctx* h) { return h->V.z0; };
+const VecSel SZ1 = [](pbicg_ctx* h) { return h->V.z1; };
+
+// Alg. 2 lines 2-3 [+ gap of iteration 0]
+void enq_init(const Members& G) {
+  pbicg_ctx* h0 = G[0];
+  const bool dist = h0->nranks > 1;
+  if (dist) comm_halo(G, {SX});
+  each(G, PH_INIT1);
+  reduce_fin(G, F_INIT1);
+  if (dist) comm_halo(G, {SR});
+  each(G, PH_INIT2);
+  reduce_fin(G, F_INIT2);
+  if (dist) comm_halo(G, {SW0});  // w_0 is read with the stencil / SpMV
+  if (h0->kind == KIND_CSR) each(G, PH_SPMVD);  // t_0 = A M^-1 w_0 (line 3)
+  if (h0->gap_on) {
+    each(G, PH_GAP);
+    reduce_fin(G, F_GAP);
   }
-  { LaunchScope ls(h, K_SPMVD);
-    c_spmvD<<<h->grid[K_SPMVD], h->block, 0, h->stream>>>(h->csr, h->V, h->scal); }
-  if (with_gap) enq_gap(h);
 }
 
-void enq_init(pbicg_ctx* h) {
-  if (h->kind == KIND_CSR) enq_init_csr(h);
-  else if (h->dim == 3) enq_init_stencil<3>(h);
-  else enq_init_stencil<2>(h);
-  if (h->gap_on) enq_gap(h);
-}
-
-void enq_iter(pbicg_ctx* h, bool with_rr) {
-  if (h->kind == KIND_CSR) enq_iter_csr(h, with_rr, h->gap_on);
-  else if (h->dim == 3) enq_iter_stencil<3>(h, with_rr, h->gap_on);
-  else enq_iter_stencil<2>(h, with_rr, h->gap_on);
-}
-
-// chunk of L iterations starting at a multiple of L (L a multiple of P when P>0):
-// iteration offset o replaces iff P > 0 && (o+1) % P == 0.
-void enq_chunk(pbicg_ctx* h, int L, int P) {
-  for (int o = 0; o < L; ++o) enq_iter(h, P > 0 && ((o + 1) % P) == 0);
-}
-
-pbicg_status run_chunk(pbicg_ctx* h, int L, int P) {
-  if (!h->use_graphs || h->timing) {
-    enq_chunk(h, L, P);
-    CU(cudaGetLastError());
-    return PBICG_OK;
+// one iteration i (par = i & 1 selects the double-buffered w and z)
+void enq_iter(const Members& G, bool with_rr, int par) {
+  pbicg_ctx* h0 = G[0];
+  const bool dist = h0->nranks > 1;
+  if (h0->kind == KIND_STENCIL) {
+    // fused 2-sweep schedule: sweep A (l.5-12) -> omega; sweep C (l.16-21) -> beta, alpha
+    each(G, PH_SWEEPA);
+    if (dist) {
+      comm_reduce(G, false);
+      comm_halo(G, {par ? SZ1 : SZ0});  // z_i for sweep C's stencil
+      each_fin(G, F_SWEEPA);
+    }
+    each(G, PH_SWEEPC);
+    reduce_fin(G, F_SWEEPC);
+    if (with_rr) {  // eq:rr after line 20
+      if (dist) comm_halo(G, {SX, SG});
+      each(G, PH_RR1);
+      if (dist) comm_halo(G, {SR, SS});
+      each(G, PH_RR2);
+      reduce_fin(G, F_RR2);
+    }
+    if (dist) comm_halo(G, {par ? SW0 : SW1});  // w_{i+1}
+  } else {
+    // split 4-phase schedule; reduction #1 overlaps the halo + spmv_B
+    each(G, PH_SWEEPA);
+    const bool ov = dist && h0->overlap;
+    if (ov) {
+      cudaEventRecord(h0->ev_fork, h0->stream);
+      cudaStreamWaitEvent(h0->side, h0->ev_fork, 0);
+      comm_reduce(G, true);
+      cudaEventRecord(h0->ev_join, h0->side);
+    } else if (dist) {
+      comm_reduce(G, false);
+    }
+    if (dist) comm_halo(G, {SZ0});
+    each(G, PH_SPMVB);  // lines 13-14
+    if (ov) cudaStreamWaitEvent(h0->stream, h0->ev_join, 0);
+    each_fin(G, F_SWEEPA);
+    each(G, PH_SWEEPC);
+    reduce_fin(G, F_SWEEPC);
+    if (with_rr) {
+      if (dist) comm_halo(G, {SX, SG});
+      each(G, PH_RR1);
+      if (dist) comm_halo(G, {SR, SS});
+      each(G, PH_RR2);
+      reduce_fin(G, F_RR2);
+    }
+    if (dist) comm_halo(G, {SW0});
+    each(G, PH_SPMVD);  // lines 22-23
   }
-  auto key = std::make_tuple(L, P, h->gap_on);
-  auto it = h->graphs.find(key);
-  if (it == h->graphs.end()) {
-    // capture without counting: counts are added per replay below
-    int64_t saved[K_N];
-    memcpy(saved, h->launches, sizeof(saved));
-    CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
-    enq_chunk(h, L, P);
-    cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
-    memcpy(h->launches, saved, sizeof(saved));
-    if (ce != cudaSuccess) return fail(h, PBICG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
-    cudaGraphExec_t ge = nullptr;
-    ce = cudaGraphInstantiate(&ge, g, 0);
-    cudaGraphDestroy(g);
-    if (ce != cudaSuccess) return fail(h, PBICG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
-    it = h->graphs.emplace(key, ge).first;
+  if (h0->gap_on) {
+    if (dist) comm_halo(G, {SX});
+    each(G, PH_GAP);
+    reduce_fin(G, F_GAP);
   }
-  CU(cudaGraphLaunch(it->second, h->stream));
-  // account the replay's launches
-  for (int o = 0; o < L; ++o) {
-    bool rr = P > 0 && ((o + 1) % P) == 0;
-    h->launches[K_SWEEPA]++;
-    h->launches[K_SWEEPC]++;
-    if (h->kind == KIND_CSR) { h->launches[K_SPMVB]++; h->launches[K_SPMVD]++; }
-    if (rr) { h->launches[K_RR1]++; h->launches[K_RR2]++; }
-    if (h->gap_on) h->launches[K_GAP]++;
-  }
-  return PBICG_OK;
+}
+
+// chunk of L iterations starting at a multiple of L (L even, multiple of P when
+// P > 0): offset o replaces iff P > 0 && (o+1) % P == 0.
+void enq_chunk(const Members& G, int L, int P) {
+  for (int o = 0; o < L; ++o) enq_iter(G, P > 0 && ((o + 1) % P) == 0, o & 1);
 }
 
 void destroy_graphs(pbicg_ctx* h) {
@@ -313,15 +500,48 @@ void destroy_graphs(pbicg_ctx* h) {
   h->graphs.clear();
 }
 
+pbicg_status run_chunk(const Members& G, int L, int P) {
+  pbicg_ctx* h = G[0];
+  const bool graphs = h->use_graphs && !h->timing;
+  if (!graphs) {
+    enq_chunk(G, L, P);
+    CU(cudaGetLastError());
+    return PBICG_OK;
+  }
+  std::vector<std::vector<int64_t>> before;
+  for (pbicg_ctx* m : G) before.emplace_back(m->launches, m->launches + K_N);
+  auto key = std::make_tuple(L, P, h->gap_on);
+  auto it = h->graphs.find(key);
+  // the enqueue pass below (capture or, for cached graphs, counted separately)
+  // establishes how many launches one replay contains
+  CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  enq_chunk(G, L, P);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
+  if (ce != cudaSuccess)
+    return fail(h, PBICG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  if (it == h->graphs.end()) {
+    cudaGraphExec_t ge = nullptr;
+    ce = cudaGraphInstantiate(&ge, g, 0);
+    if (ce != cudaSuccess) {
+      cudaGraphDestroy(g);
+      return fail(h, PBICG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+    }
+    it = h->graphs.emplace(key, ge).first;
+  }
+  cudaGraphDestroy(g);
+  CU(cudaGraphLaunch(it->second, h->stream));
+  (void)before;
+  return PBICG_OK;
+}
+
 pbicg_status ensure_hist(pbicg_ctx* h, int64_t need) {
   if (need <= h->hist_cap) return PBICG_OK;
   destroy_graphs(h);  // graphs captured the old pointers
   int64_t cap = need < 1024 ? 1024 : need;
   void *a = nullptr, *b = nullptr;
-  pbicg_status st = dalloc(h, &a, (size_t)cap * sizeof(double));
-  if (st) return st;
-  st = dalloc(h, &b, (size_t)cap * sizeof(double));
-  if (st) return st;
+  ST(dalloc(h, &a, (size_t)cap * sizeof(double)));
+  ST(dalloc(h, &b, (size_t)cap * sizeof(double)));
   h->hist.rnorm = (double*)a;
   h->hist.gap = (double*)b;
   h->hist_cap = cap;
@@ -365,7 +585,7 @@ void setup_tile(pbicg_ctx* h) {
   for (int i = 0; i < 7; ++i) t.c[i] = g.c[i];
   t.dinv = g.dinv;
   t.ncols = (int32_t)((lines + TY - 1) / TY);
-  // chunk count: minimise the idle fraction of the last round of units
+  // chunk count: minimise rounds * (chunk + 2 prologue planes) per CTA
   const int grid = h->num_sm;
   int64_t best_n = 1;
   double best_w = 1e30;
@@ -374,8 +594,7 @@ void setup_tile(pbicg_ctx* h) {
     const int64_t nchk = (g.nol + chunk - 1) / chunk;
     const int64_t units = nchk * t.ncols;
     const int64_t rounds = (units + grid - 1) / grid;
-    // work per CTA ~ rounds * (chunk + 2 prologue planes); ideal ~ units*chunk/grid
-    const double w = (double)rounds * (double)(chunk + 2) * 1.0;
+    const double w = (double)rounds * (double)(chunk + 2);
     if (w < best_w - 1e-9) {
       best_w = w;
       best_n = nch;
@@ -421,87 +640,130 @@ pbicg_status common_setup(pbicg_ctx* h, void* cuda_stream) {
     CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream = true;
   }
+  CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_poll[0], cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_poll[1], cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
   void* p = nullptr;
-  pbicg_status st = dalloc(h, &p, sizeof(Scal));
-  if (st) return st;
+  ST(dalloc(h, &p, sizeof(Scal)));
   h->scal = (Scal*)p;
   CU(cudaMemsetAsync(h->scal, 0, sizeof(Scal), h->stream));
   CU(cudaMallocHost(&h->scal_host, 2 * sizeof(Scal)));
   return PBICG_OK;
 }
 
+pbicg_status alloc_common(pbicg_ctx* h) {
+  double** vs[] = {&h->V.x, &h->V.r, &h->V.rh, &h->V.k, &h->V.g, &h->V.s, &h->V.l, &h->V.b,
+                   &h->V.w0, &h->V.w1, &h->V.z0, &h->V.z1, &h->V.zrr, &h->xtmp};
+  for (double** v : vs) ST(gvec(h, v));
+  const int nr = h->nranks;
+  void *a = nullptr, *b = nullptr;
+  ST(dalloc(h, &a, (size_t)nr * RED_K * sizeof(Dd)));
+  ST(dalloc(h, &b, (size_t)nr * RED_K * sizeof(Dd)));
+  h->red_send = (Dd*)a;
+  h->red_recv = (Dd*)b;
+  CU(cudaMemsetAsync(a, 0, (size_t)nr * RED_K * sizeof(Dd), h->stream));
+  CU(cudaMemsetAsync(b, 0, (size_t)nr * RED_K * sizeof(Dd), h->stream));
+  int gmax = h->num_sm;
+  for (int k = 0; k < K_N; ++k) gmax = h->grid[k] > gmax ? h->grid[k] : gmax;
+  void* p = nullptr;
+  ST(dalloc(h, &p, (size_t)gmax * 8 * sizeof(Dd)));
+  h->part = (Dd*)p;
+  ST(ensure_hist(h, 1024));
+  // rank fields of the device state (kept across solves)
+  Scal s;
+  memset(&s, 0, sizeof(s));
+  s.nranks = h->nranks;
+  s.rank = h->rank;
+  s.red_send = h->red_send;
+  s.red_recv = h->red_recv;
+  CU(cudaMemcpyAsync(h->scal, &s, sizeof(Scal), cudaMemcpyHostToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  return PBICG_OK;
+}
+
 // order the handle's stream after prior work on the legacy default stream
 pbicg_status entry_sync(pbicg_ctx* h) {
-  if (h->own_stream) {
+  if (h->own_stream || h->comm == COMM_LOOP) {
     CU(cudaEventRecord(h->ev_entry, 0));
     CU(cudaStreamWaitEvent(h->stream, h->ev_entry, 0));
   }
   return PBICG_OK;
 }
 
-}  // namespace
+pbicg_status nccl_setup(pbicg_ctx* h, const pbicg_dist* d) {
+  auto& api = nccl_api();
+  if (!api.ok) return fail(h, PBICG_ESTATE, api.err);
+  if (!d->nccl_id_halo) return fail(h, PBICG_EINVAL, "nccl_id_halo is NULL");
+  ncclUniqueId id;
+  memcpy(&id, d->nccl_id_halo, sizeof(id));
+  NC(api.CommInitRank(&h->nccl_halo, d->nranks, id, d->rank));
+  if (d->nccl_id_red) {
+    memcpy(&id, d->nccl_id_red, sizeof(id));
+    NC(api.CommInitRank(&h->nccl_red, d->nranks, id, d->rank));
+  } else {
+    h->nccl_red = h->nccl_halo;
+    h->overlap = 0;  // one communicator: its operations must stay on one stream
+  }
+  h->comm = COMM_NCCL;
+  return PBICG_OK;
+}
 
-// ===========================================================================
-extern "C" {
-
-pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
-                                      const pbicg_dist* dist, void* cuda_stream,
-                                      pbicg_handle* out) {
-  pbicg_ctx* h = nullptr;
-  if (!op || !out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
-  *out = nullptr;
-  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+// ------------------------- stencil construction ------------------------------
+pbicg_status validate_stencil(const pbicg_stencil* op, int nranks) {
+  if (!op) return fail(nullptr, PBICG_EINVAL, "NULL argument");
   if (op->dim != 2 && op->dim != 3) return fail(nullptr, PBICG_EINVAL, "dim must be 2 or 3");
-  int64_t nz = op->dim == 3 ? op->nz : 1;
-  if (op->nx < 1 || op->ny < 1 || nz < 1) return fail(nullptr, PBICG_EINVAL, "grid sizes must be >= 1");
-  if (op->coef[0] == 0.0 || !std::isfinite(op->coef[0]))
-    return fail(nullptr, PBICG_EINVAL, "centre coefficient must be finite and nonzero (Jacobi)");
+  const int64_t nz = op->dim == 3 ? op->nz : 1;
+  if (op->nx < 1 || op->ny < 1 || nz < 1)
+    return fail(nullptr, PBICG_EINVAL, "grid sizes must be >= 1");
+  if (op->nx > (1LL << 24) || op->ny > (1LL << 24) || nz > (1LL << 24))
+    return fail(nullptr, PBICG_EINVAL, "grid extent too large");
   for (int i = 0; i < 7; ++i)
     if (!std::isfinite(op->coef[i])) return fail(nullptr, PBICG_EINVAL, "non-finite coefficient");
-  if (dist && dist->nranks > 1)
-    return fail(nullptr, PBICG_ESTATE, "multi-GPU stencil path not available in this build");
-  h = new pbicg_ctx();
+  if (op->coef[0] == 0.0)
+    return fail(nullptr, PBICG_EINVAL, "centre coefficient must be nonzero (Jacobi)");
+  const int64_t outer = op->dim == 3 ? nz : op->ny;
+  if (nranks < 1 || nranks > outer)
+    return fail(nullptr, PBICG_EINVAL, "need 1 <= nranks <= number of slabs (nz in 3D, ny in 2D)");
+  return PBICG_OK;
+}
+
+// slab partition: rank r owns outer planes [o0, o0 + nol)
+void slab(int64_t outer, int nranks, int rank, int64_t* o0, int64_t* nol) {
+  const int64_t base = outer / nranks, rem = outer % nranks;
+  *nol = base + (rank < rem ? 1 : 0);
+  *o0 = rank * base + (rank < rem ? rank : rem);
+}
+
+pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op) {
   h->kind = KIND_STENCIL;
   h->dim = op->dim;
-  pbicg_status st = common_setup(h, cuda_stream);
-  if (st) { g_create_err = h->err; pbicgstab_destroy(h); return st; }
+  const int64_t nz = op->dim == 3 ? op->nz : 1;
   Geo& g = h->geo;
   g.nx = op->nx;
   g.ny = op->ny;
-  if (op->dim == 3) {
-    g.nog = nz;
-    g.o0 = 0;
-    g.nol = nz;
-    g.pxy = op->nx * op->ny;
-    g.nlines = op->ny * g.nol;
-  } else {
-    g.nog = op->ny;
-    g.o0 = 0;
-    g.nol = op->ny;
-    g.pxy = op->nx;
-    g.nlines = g.nol;
-  }
+  const int64_t outer = op->dim == 3 ? nz : op->ny;
+  g.nog = outer;
+  slab(outer, h->nranks, h->rank, &g.o0, &g.nol);
+  g.pxy = op->dim == 3 ? op->nx * op->ny : op->nx;
+  g.nlines = op->dim == 3 ? op->ny * g.nol : g.nol;
   for (int i = 0; i < 7; ++i) g.c[i] = op->coef[i];
-  if (op->dim == 2) { g.c[5] = 0.0; g.c[6] = 0.0; }
-  g.dinv = 1.0 / op->coef[0];
+  if (op->dim == 2) {
+    g.c[5] = 0.0;
+    g.c[6] = 0.0;
+  }
+  g.dinv = 1.0 / op->coef[0];  // A3
   h->n_global = op->nx * op->ny * nz;
-  h->n_local = g.nx * g.pxy / g.nx * g.nol;
-  h->n_local = (op->dim == 3) ? g.pxy * g.nol : g.nx * g.nol;
+  h->n_local = g.pxy * g.nol;
   h->row_begin = g.o0 * g.pxy;
-  h->H = g.pxy + g.nx + 4;  // ghost planes + staging slack of the tile kernels
+  h->H = g.pxy + g.nx + 4;  // ghost plane + staging slack of the tile kernels
+  h->halo_n = g.pxy;
   h->block = 256;
   if (g.nx < 256) h->block = (int)(((g.nx + 31) / 32) * 32);
   if (h->block < 64) h->block = 64;
-  double** vs[] = {&h->V.x, &h->V.r, &h->V.rh, &h->V.k, &h->V.g, &h->V.s, &h->V.l, &h->V.b,
-                   &h->V.w0, &h->V.w1, &h->V.z0, &h->V.z1, &h->V.zrr, &h->xtmp};
-  for (double** v : vs) {
-    st = gvec(h, v);
-    if (st) { g_create_err = h->err; pbicgstab_destroy(h); return st; }
-  }
-  int64_t L = g.nlines;
+  const int64_t L = g.nlines;
   if (op->dim == 3) {
     h->grid[K_INIT] = occ_grid(h, k_init1<3>, L);
     h->grid[K_SWEEPA] = occ_grid(h, k_sweepA<3>, L);
@@ -520,117 +782,95 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
     h->grid[K_APPLY] = occ_grid(h, k_apply<2>, L);
   }
   setup_tile(h);
-  int gmax = h->num_sm;
-  for (int k = 0; k < K_N; ++k) gmax = h->grid[k] > gmax ? h->grid[k] : gmax;
-  void* p = nullptr;
-  st = dalloc(h, &p, (size_t)gmax * 8 * sizeof(Dd));
-  if (st) { g_create_err = h->err; pbicgstab_destroy(h); return st; }
-  h->part = (Dd*)p;
-  st = ensure_hist(h, 1024);
-  if (st) { g_create_err = h->err; pbicgstab_destroy(h); return st; }
-  cudaError_t e = cudaStreamSynchronize(h->stream);
-  if (e != cudaSuccess) {
-    g_create_err = cudaGetErrorString(e);
-    pbicgstab_destroy(h);
-    return PBICG_ECUDA;
-  }
-  *out = h;
-  return PBICG_OK;
+  return alloc_common(h);
 }
 
-pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pbicg_dist* dist,
-                                  void* cuda_stream, pbicg_handle* out) {
-  pbicg_ctx* h = nullptr;
-  if (!op || !out || !op->row_ptr || (!op->col && op->n_local > 0) || (!op->val && op->n_local > 0))
+// ---------------------------- CSR construction --------------------------------
+pbicg_status validate_csr(const pbicg_csr* op, int nranks, std::vector<double>* dinv,
+                          int64_t* width, bool* uniform) {
+  if (!op || !op->row_ptr || (op->n_local > 0 && (!op->col || !op->val)))
     return fail(nullptr, PBICG_EINVAL, "NULL argument");
-  *out = nullptr;
-  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
   const int64_t n = op->n_local;
   if (op->n_global < 1 || n < 1 || op->row_begin < 0 || op->row_begin + n > op->n_global)
     return fail(nullptr, PBICG_EINVAL, "bad row range");
-  if (dist && dist->nranks > 1)
-    return fail(nullptr, PBICG_ESTATE, "multi-GPU CSR path not available in this build");
-  if (op->row_begin != 0 || n != op->n_global)
-    return fail(nullptr, PBICG_EINVAL, "single GPU: the rank must own all rows");
   if (op->n_global > INT32_MAX) return fail(nullptr, PBICG_EINVAL, "n_global must fit int32");
+  const int64_t H = nranks > 1 ? PBICG_CSR_HALO : 0;
+  if (nranks == 1 && (op->row_begin != 0 || n != op->n_global))
+    return fail(nullptr, PBICG_EINVAL, "single rank: the rank must own all rows");
+  if (nranks > 1 && n < H)
+    return fail(nullptr, PBICG_EINVAL, "multi-rank CSR: every rank needs >= PBICG_CSR_HALO rows");
+  const int64_t lo = op->row_begin - H, hi = op->row_begin + n + H;
   const int64_t* rp = op->row_ptr;
-  int64_t width = 0;
-  bool uniform = true;
-  std::vector<double> dinv(n);
+  *width = 0;
+  *uniform = true;
+  dinv->assign(n, 0.0);
   for (int64_t i = 0; i < n; ++i) {
-    int64_t len = rp[i + 1] - rp[i];
+    const int64_t len = rp[i + 1] - rp[i];
     if (len < 1) return fail(nullptr, PBICG_EINVAL, "row without entries (needs a diagonal)");
-    if (i > 0 && len != width) uniform = false;
-    if (len > width) width = len;
+    if (i > 0 && len != *width) *uniform = false;
+    if (len > *width) *width = len;
     bool diag = false;
     for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
-      int64_t c = op->col[p];
+      const int64_t c = op->col[p];
       if (c < 0 || c >= op->n_global) return fail(nullptr, PBICG_EINVAL, "column out of range");
+      if (c < lo || c >= hi)
+        return fail(nullptr, PBICG_EINVAL, "column outside the nearest-neighbour halo band");
       if (p > rp[i] && c <= op->col[p - 1])
         return fail(nullptr, PBICG_EINVAL, "columns must be strictly ascending within a row");
       if (!std::isfinite(op->val[p])) return fail(nullptr, PBICG_EINVAL, "non-finite value");
       if (c == op->row_begin + i) {
-        if (op->val[p] == 0.0) return fail(nullptr, PBICG_EINVAL, "zero diagonal (Jacobi undefined)");
-        dinv[i] = 1.0 / op->val[p];  // A3
+        if (op->val[p] == 0.0)
+          return fail(nullptr, PBICG_EINVAL, "zero diagonal (Jacobi undefined)");
+        (*dinv)[i] = 1.0 / op->val[p];  // A3
         diag = true;
       }
     }
     if (!diag) return fail(nullptr, PBICG_EINVAL, "missing diagonal entry");
   }
-  if (width > 4096) return fail(nullptr, PBICG_EINVAL, "row too long for the ELL path (> 4096)");
-  h = new pbicg_ctx();
+  if (*width > 4096) return fail(nullptr, PBICG_EINVAL, "row too long for the ELL path (> 4096)");
+  return PBICG_OK;
+}
+
+pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<double>& dinv,
+                       int64_t width, bool uniform) {
   h->kind = KIND_CSR;
-  pbicg_status st = common_setup(h, cuda_stream);
-  if (st) { g_create_err = h->err; pbicgstab_destroy(h); return st; }
+  const int64_t n = op->n_local;
+  const int64_t* rp = op->row_ptr;
   h->n_global = op->n_global;
   h->n_local = n;
   h->row_begin = op->row_begin;
-  h->H = 0;
+  h->H = h->nranks > 1 ? PBICG_CSR_HALO : 0;
+  h->halo_n = h->H;
   h->block = 256;
   // column-major ELL in stored row order; padding slots are never read (len[])
   std::vector<int32_t> ecol((size_t)width * n);
   std::vector<double> eval((size_t)width * n, 0.0);
   std::vector<int32_t> elen(uniform ? 0 : n);
   for (int64_t i = 0; i < n; ++i) {
-    int64_t len = rp[i + 1] - rp[i];
+    const int64_t len = rp[i + 1] - rp[i];
     if (!uniform) elen[i] = (int32_t)len;
     for (int64_t q = 0; q < width; ++q) {
-      bool real = q < len;
+      const bool real = q < len;
       ecol[(size_t)q * n + i] = real ? (int32_t)(op->col[rp[i] + q] - op->row_begin) : (int32_t)i;
       eval[(size_t)q * n + i] = real ? op->val[rp[i] + q] : 0.0;
     }
   }
-  void *pc = nullptr, *pv = nullptr, *pl = nullptr, *pd = nullptr;
-  if ((st = dalloc(h, &pc, ecol.size() * sizeof(int32_t))) ||
-      (st = dalloc(h, &pv, eval.size() * sizeof(double))) ||
-      (st = dalloc(h, &pd, (size_t)n * sizeof(double)))) {
-    g_create_err = h->err; pbicgstab_destroy(h); return st;
-  }
-  if (!uniform && (st = dalloc(h, &pl, (size_t)n * sizeof(int32_t)))) {
-    g_create_err = h->err; pbicgstab_destroy(h); return st;
-  }
-  cudaError_t e = cudaMemcpy(pc, ecol.data(), ecol.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(pv, eval.data(), eval.size() * sizeof(double), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMemcpy(pd, dinv.data(), (size_t)n * sizeof(double), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess && !uniform)
-    e = cudaMemcpy(pl, elen.data(), (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) {
-    g_create_err = cudaGetErrorString(e);
-    pbicgstab_destroy(h);
-    return PBICG_ECUDA;
-  }
+  void *pc = nullptr, *pv = nullptr, *pl = nullptr;
+  ST(dalloc(h, &pc, ecol.size() * sizeof(int32_t)));
+  ST(dalloc(h, &pv, eval.size() * sizeof(double)));
+  if (!uniform) ST(dalloc(h, &pl, (size_t)n * sizeof(int32_t)));
+  CU(cudaMemcpy(pc, ecol.data(), ecol.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(pv, eval.data(), eval.size() * sizeof(double), cudaMemcpyHostToDevice));
+  if (!uniform)
+    CU(cudaMemcpy(pl, elen.data(), (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  ST(gvec(h, &h->dinv_g));
+  CU(cudaMemcpy(h->dinv_g, dinv.data(), (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
   h->csr.n = n;
   h->csr.width = (int32_t)width;
   h->csr.col = (const int32_t*)pc;
   h->csr.val = (const double*)pv;
   h->csr.len = uniform ? nullptr : (const int32_t*)pl;
-  h->csr.dinv = (const double*)pd;
-  double** vs[] = {&h->V.x, &h->V.r, &h->V.rh, &h->V.k, &h->V.g, &h->V.s, &h->V.l, &h->V.b,
-                   &h->V.w0, &h->V.w1, &h->V.z0, &h->V.z1, &h->V.zrr, &h->xtmp};
-  for (double** v : vs) {
-    st = gvec(h, v);
-    if (st) { g_create_err = h->err; pbicgstab_destroy(h); return st; }
-  }
+  h->csr.dinv = h->dinv_g;
   const int64_t blocks = (n + h->block - 1) / h->block;
   h->grid[K_INIT] = occ_grid(h, c_init1, blocks);
   h->grid[K_SWEEPA] = occ_grid(h, c_sweepA, blocks);
@@ -641,21 +881,300 @@ pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pb
   h->grid[K_RR2] = occ_grid(h, c_rr2, blocks);
   h->grid[K_GAP] = occ_grid(h, c_gap, blocks);
   h->grid[K_APPLY] = occ_grid(h, c_apply, blocks);
-  int gmax = 0;
-  for (int k = 0; k < K_N; ++k) gmax = h->grid[k] > gmax ? h->grid[k] : gmax;
-  void* p = nullptr;
-  st = dalloc(h, &p, (size_t)gmax * 8 * sizeof(Dd));
-  if (st) { g_create_err = h->err; pbicgstab_destroy(h); return st; }
-  h->part = (Dd*)p;
-  st = ensure_hist(h, 1024);
-  if (st) { g_create_err = h->err; pbicgstab_destroy(h); return st; }
-  e = cudaStreamSynchronize(h->stream);
-  if (e != cudaSuccess) {
-    g_create_err = cudaGetErrorString(e);
-    pbicgstab_destroy(h);
-    return PBICG_ECUDA;
+  return alloc_common(h);
+}
+
+void destroy_one(pbicg_ctx* h) {
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  collect_timing(h);
+  destroy_graphs(h);
+  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  for (void* p : h->allocs) cudaFree(p);
+  if (h->scal_host) cudaFreeHost(h->scal_host);
+  cudaEvent_t evs[] = {h->ev_entry, h->ev_poll[0], h->ev_poll[1], h->ev_fork, h->ev_join};
+  for (cudaEvent_t e : evs)
+    if (e) cudaEventDestroy(e);
+  if (h->side) cudaStreamDestroy(h->side);
+  if (h->comm == COMM_NCCL && nccl_api().ok) {
+    if (h->nccl_red && h->nccl_red != h->nccl_halo) nccl_api().CommDestroy(h->nccl_red);
+    if (h->nccl_halo) nccl_api().CommDestroy(h->nccl_halo);
+  }
+  bool own_stream = h->own_stream;
+  cudaStream_t s = h->stream;
+  if (pbicg_group* grp = h->group) {
+    // the group's shared stream is destroyed with its last member
+    for (auto& m : grp->m)
+      if (m == h) m = nullptr;
+    grp->alive--;
+    if (own_stream && grp->alive > 0) {
+      for (auto& m : grp->m)
+        if (m) {
+          m->own_stream = true;
+          own_stream = false;
+          break;
+        }
+    }
+    if (grp->alive == 0) delete grp;
+  }
+  if (own_stream && s) cudaStreamDestroy(s);
+  cudaGetLastError();
+  delete h;
+}
+
+// ------------------------------- solve ----------------------------------------
+struct SolveArgs {
+  const double* b;
+  const double* x0;
+  double* x;
+};
+
+pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, double tol,
+                           int32_t maxit, int32_t rr_period, double* rnorm_hist, double* gap_hist,
+                           int32_t* iters_out, int32_t* outcome_out) {
+  pbicg_ctx* h = G[0];
+  for (pbicg_ctx* m : G)
+    if (m->failed) return fail(h, PBICG_ESTATE, "handle is in a failed state");
+  if (!rnorm_hist || !iters_out || !outcome_out) return fail(h, PBICG_EINVAL, "NULL argument");
+  if (maxit < 0 || rr_period < 0 || !(tol >= 0.0))
+    return fail(h, PBICG_EINVAL, "maxit, rr_period and tol must be >= 0");
+  for (size_t r = 0; r < G.size(); ++r) {
+    if (!io[r].b || !io[r].x0 || !io[r].x) return fail(h, PBICG_EINVAL, "NULL vector argument");
+    ST(ensure_hist(G[r], (int64_t)maxit + 1));
+  }
+  ST(entry_sync(h));
+  for (size_t r = 0; r < G.size(); ++r) {
+    pbicg_ctx* m = G[r];
+    m->gap_on = gap_hist != nullptr;
+    const size_t nb = (size_t)m->n_local * sizeof(double);
+    CU(cudaMemcpyAsync(m->V.b, io[r].b, nb, cudaMemcpyDeviceToDevice, m->stream));
+    CU(cudaMemcpyAsync(m->V.x, io[r].x0, nb, cudaMemcpyDeviceToDevice, m->stream));
+    // A1: g, s, l, z_{-1} (and the spare buffers) start at zero
+    double* zs[] = {m->V.g, m->V.s, m->V.l, m->V.z0, m->V.z1, m->V.zrr};
+    for (double* v : zs)
+      CU(cudaMemsetAsync(v - m->H, 0, nb + 2 * m->H * sizeof(double), m->stream));
+    Scal s0;
+    memset(&s0, 0, sizeof(s0));
+    s0.tol = tol;
+    s0.sqrt_eps = std::sqrt(std::ldexp(1.0, -53));
+    s0.outcome = OUT_MAXIT;
+    s0.gap_iter = -1;
+    s0.bench = m->bench;
+    s0.rr_period = rr_period;
+    s0.nranks = m->nranks;
+    s0.rank = m->rank;
+    s0.red_send = m->red_send;
+    s0.red_recv = m->red_recv;
+    m->scal_host[0] = s0;
+    CU(cudaMemcpyAsync(m->scal, m->scal_host, sizeof(Scal), cudaMemcpyHostToDevice, m->stream));
+  }
+  enq_init(G);
+  CU(cudaGetLastError());
+  // chunk length: even (double-buffer parity) and a multiple of the replacement
+  // period so every chunk has the same replacement pattern (A11)
+  const int P = rr_period;
+  int L = 32;
+  if (P > 0) {
+    L = P;
+    while (L < 32 || (L & 1)) L += P;
+  }
+  int64_t done_its = 0;
+  int slot = 0;
+  bool have_prev = false, stop = false;
+  while (done_its < maxit && !stop) {
+    const int n = (int)((maxit - done_its) < L ? (maxit - done_its) : L);
+    pbicg_status st = run_chunk(G, n, P);
+    if (st) {
+      for (pbicg_ctx* m : G) m->failed = true;
+      return st;
+    }
+    done_its += n;
+    CU(cudaMemcpyAsync(h->scal_host + slot, h->scal, sizeof(Scal), cudaMemcpyDeviceToHost,
+                       h->stream));
+    CU(cudaEventRecord(h->ev_poll[slot], h->stream));
+    if (have_prev) {
+      CU(cudaEventSynchronize(h->ev_poll[slot ^ 1]));
+      if (h->scal_host[slot ^ 1].done) stop = true;
+    }
+    have_prev = true;
+    slot ^= 1;
+  }
+  CU(cudaStreamSynchronize(h->stream));
+  CU(cudaMemcpy(h->scal_host, h->scal, sizeof(Scal), cudaMemcpyDeviceToHost));
+  const Scal S = h->scal_host[0];
+  int32_t iters = S.done ? S.iters : S.iter;
+  if (iters > maxit) iters = maxit;
+  if (iters < 0) iters = 0;
+  CU(cudaMemcpy(rnorm_hist, h->hist.rnorm, (size_t)(iters + 1) * sizeof(double),
+                cudaMemcpyDeviceToHost));
+  if (gap_hist)
+    CU(cudaMemcpy(gap_hist, h->hist.gap, (size_t)(iters + 1) * sizeof(double),
+                  cudaMemcpyDeviceToHost));
+  for (size_t r = 0; r < G.size(); ++r) {
+    pbicg_ctx* m = G[r];
+    CU(cudaMemcpyAsync(io[r].x, m->V.x, (size_t)m->n_local * sizeof(double),
+                       cudaMemcpyDeviceToDevice, m->stream));
+  }
+  CU(cudaStreamSynchronize(h->stream));
+  for (pbicg_ctx* m : G)
+    if (m->timing) collect_timing(m);
+  *iters_out = iters;
+  *outcome_out = S.done ? S.outcome : OUT_MAXIT;
+  return PBICG_OK;
+}
+
+// P handles sharing one stream (loopback transport)
+pbicg_group* new_group(void* cuda_stream, cudaStream_t* s, bool* own) {
+  *s = (cudaStream_t)cuda_stream;
+  *own = false;
+  if (!*s) {
+    if (cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    *own = true;
+  }
+  return new pbicg_group();
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
+                                      const pbicg_dist* dist, void* cuda_stream,
+                                      pbicg_handle* out) {
+  if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+  const int nranks = dist ? dist->nranks : 1;
+  if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
+    return fail(nullptr, PBICG_EINVAL, "inconsistent nranks/rank");
+  ST(validate_stencil(op, nranks));
+  pbicg_ctx* h = new pbicg_ctx();
+  h->nranks = nranks;
+  h->rank = dist ? dist->rank : 0;
+  pbicg_status st = common_setup(h, cuda_stream);
+  if (!st && nranks > 1) st = nccl_setup(h, dist);
+  if (!st) st = build_stencil(h, op);
+  if (st) {
+    g_create_err = h->err;
+    destroy_one(h);
+    return st;
   }
   *out = h;
+  return PBICG_OK;
+}
+
+pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pbicg_dist* dist,
+                                  void* cuda_stream, pbicg_handle* out) {
+  if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
+  *out = nullptr;
+  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+  const int nranks = dist ? dist->nranks : 1;
+  if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
+    return fail(nullptr, PBICG_EINVAL, "inconsistent nranks/rank");
+  std::vector<double> dinv;
+  int64_t width = 0;
+  bool uniform = true;
+  ST(validate_csr(op, nranks, &dinv, &width, &uniform));
+  pbicg_ctx* h = new pbicg_ctx();
+  h->nranks = nranks;
+  h->rank = dist ? dist->rank : 0;
+  pbicg_status st = common_setup(h, cuda_stream);
+  if (!st && nranks > 1) st = nccl_setup(h, dist);
+  if (!st) st = build_csr(h, op, dinv, width, uniform);
+  if (!st && nranks > 1) {  // dinv ghosts, once (collective)
+    comm_halo(Members{h}, {[](pbicg_ctx* c) { return c->dinv_g; }});
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) st = fail(h, PBICG_ECUDA, cudaGetErrorString(e));
+  }
+  if (st) {
+    g_create_err = h->err;
+    destroy_one(h);
+    return st;
+  }
+  *out = h;
+  return PBICG_OK;
+}
+
+pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_prec prec,
+                                               int32_t nranks, void* cuda_stream,
+                                               pbicg_handle* out) {
+  if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
+  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+  ST(validate_stencil(op, nranks));
+  for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+  cudaStream_t s;
+  bool own;
+  pbicg_group* grp = new_group(cuda_stream, &s, &own);
+  if (!grp) return fail(nullptr, PBICG_ECUDA, "stream creation failed");
+  pbicg_status st = PBICG_OK;
+  for (int r = 0; r < nranks && !st; ++r) {
+    pbicg_ctx* h = new pbicg_ctx();
+    h->nranks = nranks;
+    h->rank = r;
+    h->comm = COMM_LOOP;
+    h->group = grp;
+    grp->m.push_back(h);
+    grp->alive++;
+    st = common_setup(h, s);
+    if (r == 0) h->own_stream = own;
+    if (!st) st = build_stencil(h, op);
+    if (st) g_create_err = h->err;
+  }
+  if (st) {
+    Members m = grp->m;
+    for (auto it = m.rbegin(); it != m.rend(); ++it) destroy_one(*it);
+    return st;
+  }
+  for (int r = 0; r < nranks; ++r) out[r] = grp->m[r];
+  return PBICG_OK;
+}
+
+pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec, int32_t nranks,
+                                           void* cuda_stream, pbicg_handle* out) {
+  if (!out || !ops || nranks < 1) return fail(nullptr, PBICG_EINVAL, "bad argument");
+  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+  for (int r = 0; r < nranks; ++r) out[r] = nullptr;
+  std::vector<std::vector<double>> dinv(nranks);
+  std::vector<int64_t> width(nranks);
+  std::vector<char> uni(nranks);
+  int64_t next = 0;
+  for (int r = 0; r < nranks; ++r) {
+    bool u = true;
+    ST(validate_csr(&ops[r], nranks, &dinv[r], &width[r], &u));
+    uni[r] = u;
+    if (ops[r].row_begin != next || ops[r].n_global != ops[0].n_global)
+      return fail(nullptr, PBICG_EINVAL, "rank row ranges must be contiguous and ordered");
+    next += ops[r].n_local;
+  }
+  if (next != ops[0].n_global) return fail(nullptr, PBICG_EINVAL, "ranks must cover all rows");
+  cudaStream_t s;
+  bool own;
+  pbicg_group* grp = new_group(cuda_stream, &s, &own);
+  if (!grp) return fail(nullptr, PBICG_ECUDA, "stream creation failed");
+  pbicg_status st = PBICG_OK;
+  for (int r = 0; r < nranks && !st; ++r) {
+    pbicg_ctx* h = new pbicg_ctx();
+    h->nranks = nranks;
+    h->rank = r;
+    h->comm = COMM_LOOP;
+    h->group = grp;
+    grp->m.push_back(h);
+    grp->alive++;
+    st = common_setup(h, s);
+    if (r == 0) h->own_stream = own;
+    if (!st) st = build_csr(h, &ops[r], dinv[r], width[r], uni[r] != 0);
+    if (st) g_create_err = h->err;
+  }
+  if (!st) {
+    comm_halo(grp->m, {[](pbicg_ctx* c) { return c->dinv_g; }});
+    if (cudaStreamSynchronize(s) != cudaSuccess) st = fail(nullptr, PBICG_ECUDA, "dinv halo");
+  }
+  if (st) {
+    Members m = grp->m;
+    for (auto it = m.rbegin(); it != m.rend(); ++it) destroy_one(*it);
+    return st;
+  }
+  for (int r = 0; r < nranks; ++r) out[r] = grp->m[r];
   return PBICG_OK;
 }
 
@@ -669,28 +1188,40 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
 pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value) {
   if (!h || !key) return fail(h, PBICG_EINVAL, "NULL argument");
   std::string k(key);
-  if (k == "bench") h->bench = value != 0;
-  else if (k == "graphs") h->use_graphs = value != 0;
-  else if (k == "timing") h->timing = value != 0;
-  else if (k == "overlap") h->overlap = value != 0;
-  else if (k == "tile") {
-    h->tile_on = value != 0;
-    destroy_graphs(h);
+  for (pbicg_ctx* m : members(h)) {
+    if (k == "bench") {
+      m->bench = value != 0;
+    } else if (k == "graphs") {
+      m->use_graphs = value != 0;
+    } else if (k == "timing") {
+      m->timing = value != 0;
+    } else if (k == "overlap") {
+      m->overlap = value != 0 && (m->comm != COMM_NCCL || m->nccl_red != m->nccl_halo);
+      destroy_graphs(m);
+    } else if (k == "tile") {
+      m->tile_on = value != 0;
+      destroy_graphs(m);
+    } else if (k == "schedule") {
+      if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "schedule must be 0, 1 or 2");
+      if (value == 2 && m->kind == KIND_STENCIL)
+        return fail(h, PBICG_EINVAL, "split schedule is not built for stencils in this version");
+      if (value == 1 && m->kind == KIND_CSR)
+        return fail(h, PBICG_EINVAL, "fused schedule is stencil-only");
+      m->schedule = (int)value;
+    } else {
+      return fail(h, PBICG_EINVAL, "unknown option '" + k + "'");
+    }
   }
-  else if (k == "schedule") {
-    if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "schedule must be 0, 1 or 2");
-    if (value == 1 && h->kind == KIND_CSR) return fail(h, PBICG_EINVAL, "fused schedule is stencil-only");
-    h->schedule = (int)value;
-  } else return fail(h, PBICG_EINVAL, "unknown option '" + k + "'");
   return PBICG_OK;
 }
 
 pbicg_status pbicgstab_apply(pbicg_handle h, const double* x_dev, double* y_dev) {
   if (!h || !x_dev || !y_dev) return fail(h, PBICG_EINVAL, "NULL argument");
-  pbicg_status st = entry_sync(h);
-  if (st) return st;
+  if (h->comm == COMM_LOOP) return fail(h, PBICG_EINVAL, "use pbicgstab_apply_loopback");
+  ST(entry_sync(h));
   CU(cudaMemcpyAsync(h->xtmp, x_dev, (size_t)h->n_local * sizeof(double),
                      cudaMemcpyDeviceToDevice, h->stream));
+  comm_halo(Members{h}, {[](pbicg_ctx* c) { return c->xtmp; }});
   {
     LaunchScope ls(h, K_APPLY);
     if (h->kind == KIND_CSR)
@@ -706,81 +1237,61 @@ pbicg_status pbicgstab_apply(pbicg_handle h, const double* x_dev, double* y_dev)
   return PBICG_OK;
 }
 
+pbicg_status pbicgstab_apply_loopback(pbicg_handle* hs, int32_t nranks, const double* const* x_dev,
+                                      double* const* y_dev) {
+  if (!hs || nranks < 1 || !x_dev || !y_dev) return fail(nullptr, PBICG_EINVAL, "NULL argument");
+  pbicg_ctx* h = hs[0];
+  if (!h || h->comm != COMM_LOOP || (int)h->group->m.size() != nranks)
+    return fail(h, PBICG_EINVAL, "not a loopback group of this size");
+  Members G = h->group->m;
+  ST(entry_sync(h));
+  for (int r = 0; r < nranks; ++r) {
+    pbicg_ctx* m = G[r];
+    CU(cudaMemcpyAsync(m->xtmp, x_dev[r], (size_t)m->n_local * sizeof(double),
+                       cudaMemcpyDeviceToDevice, m->stream));
+  }
+  comm_halo(G, {[](pbicg_ctx* c) { return c->xtmp; }});
+  for (int r = 0; r < nranks; ++r) {
+    pbicg_ctx* m = G[r];
+    LaunchScope ls(m, K_APPLY);
+    if (m->kind == KIND_CSR)
+      c_apply<<<m->grid[K_APPLY], m->block, 0, m->stream>>>(m->csr, m->xtmp, y_dev[r]);
+    else if (m->dim == 3)
+      k_apply<3><<<m->grid[K_APPLY], m->block, 0, m->stream>>>(m->geo, m->xtmp, y_dev[r]);
+    else
+      k_apply<2><<<m->grid[K_APPLY], m->block, 0, m->stream>>>(m->geo, m->xtmp, y_dev[r]);
+  }
+  CU(cudaGetLastError());
+  CU(cudaStreamSynchronize(h->stream));
+  return PBICG_OK;
+}
+
 pbicg_status pbicgstab_solve(pbicg_handle h, const double* b_dev, const double* x0_dev,
                              double tol, int32_t maxit, int32_t rr_period, double* x_dev_out,
                              double* rnorm_hist, double* gap_hist, int32_t* iters_out,
                              int32_t* outcome_out) {
   if (!h) return fail(nullptr, PBICG_EINVAL, "NULL handle");
-  if (h->failed) return fail(h, PBICG_ESTATE, "handle is in a failed state");
-  if (!b_dev || !x0_dev || !x_dev_out || !rnorm_hist || !iters_out || !outcome_out)
-    return fail(h, PBICG_EINVAL, "NULL argument");
-  if (maxit < 0 || rr_period < 0 || !(tol >= 0.0))
-    return fail(h, PBICG_EINVAL, "maxit, rr_period and tol must be >= 0");
-  pbicg_status st = ensure_hist(h, (int64_t)maxit + 1);
-  if (st) return st;
-  st = entry_sync(h);
-  if (st) return st;
-  h->gap_on = gap_hist != nullptr;
-  const size_t nb = (size_t)h->n_local * sizeof(double);
-  CU(cudaMemcpyAsync(h->V.b, b_dev, nb, cudaMemcpyDeviceToDevice, h->stream));
-  CU(cudaMemcpyAsync(h->V.x, x0_dev, nb, cudaMemcpyDeviceToDevice, h->stream));
-  // A1: g, s, l, z_{-1} (and the spare buffers) start at zero
-  double* zs[] = {h->V.g, h->V.s, h->V.l, h->V.z0, h->V.z1, h->V.zrr};
-  for (double* v : zs) CU(cudaMemsetAsync(v - h->H, 0, nb + 2 * h->H * sizeof(double), h->stream));
-  Scal s0;
-  memset(&s0, 0, sizeof(s0));
-  s0.tol = tol;
-  s0.sqrt_eps = std::sqrt(std::ldexp(1.0, -53));
-  s0.outcome = OUT_MAXIT;
-  s0.gap_iter = -1;
-  s0.bench = h->bench;
-  s0.rr_period = rr_period;
-  *h->scal_host = s0;
-  CU(cudaMemcpyAsync(h->scal, h->scal_host, sizeof(Scal), cudaMemcpyHostToDevice, h->stream));
-  enq_init(h);
-  CU(cudaGetLastError());
-  // chunk length: a multiple of the replacement period so every chunk has the
-  // same replacement pattern (A11)
-  int P = rr_period;
-  int L = 32;
-  if (P > 0) L = P >= 32 ? P : P * ((32 + P - 1) / P);
-  int64_t done_its = 0;
-  int slot = 0;
-  bool have_prev = false;
-  bool stop = false;
-  while (done_its < maxit && !stop) {
-    int n = (int)((maxit - done_its) < L ? (maxit - done_its) : L);
-    st = run_chunk(h, n, P);
-    if (st) { h->failed = true; return st; }
-    done_its += n;
-    // async poll: copy the state, check the previous chunk's copy
-    CU(cudaMemcpyAsync(h->scal_host + slot, h->scal, sizeof(Scal), cudaMemcpyDeviceToHost,
-                       h->stream));
-    CU(cudaEventRecord(h->ev_poll[slot], h->stream));
-    if (have_prev) {
-      CU(cudaEventSynchronize(h->ev_poll[slot ^ 1]));
-      if (h->scal_host[slot ^ 1].done) stop = true;
-    }
-    have_prev = true;
-    slot ^= 1;
-  }
-  CU(cudaStreamSynchronize(h->stream));
-  CU(cudaMemcpy(h->scal_host, h->scal, sizeof(Scal), cudaMemcpyDeviceToHost));
-  const Scal& S = *h->scal_host;
-  int32_t iters = S.done ? S.iters : S.iter;
-  if (S.done && S.outcome == OUT_BREAKDOWN) iters = S.iters;
-  if (iters > maxit) iters = maxit;
-  CU(cudaMemcpy(rnorm_hist, h->hist.rnorm, (size_t)(iters + 1) * sizeof(double),
-                cudaMemcpyDeviceToHost));
-  if (gap_hist)
-    CU(cudaMemcpy(gap_hist, h->hist.gap, (size_t)(iters + 1) * sizeof(double),
-                  cudaMemcpyDeviceToHost));
-  CU(cudaMemcpyAsync(x_dev_out, h->V.x, nb, cudaMemcpyDeviceToDevice, h->stream));
-  CU(cudaStreamSynchronize(h->stream));
-  if (h->timing) collect_timing(h);
-  *iters_out = iters;
-  *outcome_out = S.done ? S.outcome : OUT_MAXIT;
-  return PBICG_OK;
+  if (h->comm == COMM_LOOP) return fail(h, PBICG_EINVAL, "use pbicgstab_solve_loopback");
+  std::vector<SolveArgs> io{{b_dev, x0_dev, x_dev_out}};
+  return solve_members(Members{h}, io, tol, maxit, rr_period, rnorm_hist, gap_hist, iters_out,
+                       outcome_out);
+}
+
+pbicg_status pbicgstab_solve_loopback(pbicg_handle* hs, int32_t nranks,
+                                      const double* const* b_dev, const double* const* x0_dev,
+                                      double tol, int32_t maxit, int32_t rr_period,
+                                      double* const* x_dev_out, double* rnorm_hist,
+                                      double* gap_hist, int32_t* iters_out,
+                                      int32_t* outcome_out) {
+  if (!hs || nranks < 1 || !b_dev || !x0_dev || !x_dev_out)
+    return fail(nullptr, PBICG_EINVAL, "NULL argument");
+  pbicg_ctx* h = hs[0];
+  if (!h || h->comm != COMM_LOOP || (int)h->group->m.size() != nranks)
+    return fail(h, PBICG_EINVAL, "not a loopback group of this size");
+  std::vector<SolveArgs> io;
+  for (int r = 0; r < nranks; ++r) io.push_back({b_dev[r], x0_dev[r], x_dev_out[r]});
+  return solve_members(h->group->m, io, tol, maxit, rr_period, rnorm_hist, gap_hist, iters_out,
+                       outcome_out);
 }
 
 pbicg_status pbicgstab_solve_host(pbicg_handle h, const double* b_host, const double* x0_host,
@@ -789,15 +1300,14 @@ pbicg_status pbicgstab_solve_host(pbicg_handle h, const double* b_host, const do
                                   int32_t* iters_out, int32_t* outcome_out) {
   if (!h) return fail(nullptr, PBICG_EINVAL, "NULL handle");
   if (!b_host || !x0_host || !x_host_out) return fail(h, PBICG_EINVAL, "NULL argument");
+  if (h->comm == COMM_LOOP) return fail(h, PBICG_EINVAL, "host entry is per process");
   const size_t nb = (size_t)h->n_local * sizeof(double);
-  pbicg_status st = entry_sync(h);
-  if (st) return st;
-  // stage through the handle's own buffers: b -> V.b, x0 -> xtmp
+  ST(entry_sync(h));
+  // stage through the handle's own buffers: b -> V.rh (overwritten by init), x0 -> xtmp
   CU(cudaMemcpyAsync(h->xtmp, x0_host, nb, cudaMemcpyHostToDevice, h->stream));
   CU(cudaMemcpyAsync(h->V.rh, b_host, nb, cudaMemcpyHostToDevice, h->stream));
-  st = pbicgstab_solve(h, h->V.rh, h->xtmp, tol, maxit, rr_period, h->xtmp, rnorm_hist,
-                       gap_hist, iters_out, outcome_out);
-  if (st) return st;
+  ST(pbicgstab_solve(h, h->V.rh, h->xtmp, tol, maxit, rr_period, h->xtmp, rnorm_hist, gap_hist,
+                     iters_out, outcome_out));
   CU(cudaMemcpy(x_host_out, h->xtmp, nb, cudaMemcpyDeviceToHost));
   return PBICG_OK;
 }
@@ -820,7 +1330,10 @@ pbicg_status pbicgstab_kernel_time(pbicg_handle h, const char* name, int64_t* la
   if (launches) *launches = L;
   if (ms) *ms = h->timing ? t : NAN;
   if (reset) {
-    for (int k = 0; k < K_N; ++k) { h->launches[k] = 0; h->ms[k] = 0; }
+    for (int k = 0; k < K_N; ++k) {
+      h->launches[k] = 0;
+      h->ms[k] = 0;
+    }
   }
   return PBICG_OK;
 }
@@ -831,7 +1344,7 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
   const double N = (double)h->n_local;
   double b = 0;
   if (h->kind == KIND_STENCIL) {
-    // fused schedule: streams read + written once per launch (DESIGN.md Roofline)
+    // fused schedule: every vector read / written once per launch
     if (n == "sweepA") b = 11 * 8 * N;       // read k,g,l,w,s,z,r; write g,s,l,z
     else if (n == "sweepC") b = 13 * 8 * N;  // read x,g,k,l,r,s,w,z,r^; write x,r,k,w
     else if (n == "rr1") b = 7 * 8 * N;      // read x,b,g; write r,k,s,l
@@ -840,11 +1353,12 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "apply") b = 2 * 8 * N;
     else if (n == "iteration") b = 24 * 8 * N;
   } else {
-    const double nnz = (double)h->csr.width;  // ELL width
-    const double mat = 12.0 * nnz * N;        // val (8) + col (4) per slot
-    if (n == "sweepA") b = 14 * 8 * N;        // read k,g,l,w,s,z,t,v,r,dinv; write g,s,l,z
-    else if (n == "spmvB" || n == "spmvD" || n == "apply") b = mat + 3 * 8 * N;  // in, dinv, out
-    else if (n == "sweepC") b = 16 * 8 * N;   // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w
+    const double slots = (double)h->csr.width;  // ELL width
+    const double mat = 12.0 * slots * N;        // val (8) + col (4) per slot
+    if (n == "sweepA") b = 14 * 8 * N;          // read k,g,l,w,s,z,t,v,r,dinv; write g,s,l,z
+    else if (n == "spmvB" || n == "spmvD") b = mat + 3 * 8 * N;  // in, dinv, out
+    else if (n == "apply") b = mat + 2 * 8 * N;
+    else if (n == "sweepC") b = 16 * 8 * N;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w
     else if (n == "rr1") b = 2 * mat + 8 * 8 * N;
     else if (n == "rr2") b = 2 * mat + 7 * 8 * N;
     else if (n == "gap") b = mat + 3 * 8 * N;
@@ -855,8 +1369,14 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
 }
 
 pbicg_status pbicgstab_get_unique_id(void* out128) {
-  (void)out128;
-  return fail(nullptr, PBICG_ESTATE, "NCCL support not built");
+  if (!out128) return fail(nullptr, PBICG_EINVAL, "NULL argument");
+  auto& api = nccl_api();
+  if (!api.ok) return fail(nullptr, PBICG_ESTATE, api.err);
+  ncclUniqueId id;
+  ncclResult_t r = api.GetUniqueId(&id);
+  if (r != ncclSuccess) return fail(nullptr, PBICG_ENCCL, api.GetErrorString(r));
+  memcpy(out128, &id, sizeof(id));
+  return PBICG_OK;
 }
 
 const char* pbicgstab_last_error(pbicg_handle h) {
@@ -865,18 +1385,7 @@ const char* pbicgstab_last_error(pbicg_handle h) {
 
 void pbicgstab_destroy(pbicg_handle h) {
   if (!h) return;
-  if (h->stream) cudaStreamSynchronize(h->stream);
-  collect_timing(h);
-  destroy_graphs(h);
-  for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
-  for (void* p : h->allocs) cudaFree(p);
-  if (h->scal_host) cudaFreeHost(h->scal_host);
-  if (h->ev_entry) cudaEventDestroy(h->ev_entry);
-  if (h->ev_poll[0]) cudaEventDestroy(h->ev_poll[0]);
-  if (h->ev_poll[1]) cudaEventDestroy(h->ev_poll[1]);
-  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
-  cudaGetLastError();
-  delete h;
+  destroy_one(h);
 }
 
 }  // extern "C"

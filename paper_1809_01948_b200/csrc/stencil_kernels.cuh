@@ -103,7 +103,7 @@ __device__ __forceinline__ double apply_row(const double* __restrict__ v, int64_
 // dots (r0,r0) and (b,b).
 template <int DIM>
 __global__ void __launch_bounds__(256) k_init1(Geo g, Vecs V, Scal* __restrict__ sc,
-                                               Dd* __restrict__ part) {
+                                               Dd* __restrict__ part, Hist h) {
   Dd acc[2] = {dd_zero(), dd_zero()};
   STENCIL_LOOP_BEGIN
   const double xc = V.x[j];
@@ -117,10 +117,8 @@ __global__ void __launch_bounds__(256) k_init1(Geo g, Vecs V, Scal* __restrict__
   dd_fma(acc[1], bj, bj);
   STENCIL_LOOP_END
   Dd tot[2];
-  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_INIT1], tot) && threadIdx.x == 0) {
-    sc->tmp0 = dd_round(tot[0]);  // (r0, r0) = (r^0, r0) = rho_0
-    sc->tmp1 = dd_round(tot[1]);  // (b, b)
-  }
+  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_INIT1], tot) && threadIdx.x == 0)
+    publish<F_INIT1>(sc, h, tot);
 }
 
 // init2 (lines 2-3): w0 := A k0 = A M^-1 r0; (r0, w0);
@@ -136,25 +134,8 @@ __global__ void __launch_bounds__(256) k_init2(Geo g, Vecs V, Scal* __restrict__
   dd_fma(acc[0], V.rh[j], wj);
   STENCIL_LOOP_END
   Dd tot[1];
-  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_INIT2], tot) && threadIdx.x == 0) {
-    const double rho = sc->tmp0;
-    const double rw = dd_round(tot[0]);
-    sc->rho = rho;
-    sc->alpha = rho / rw;
-    sc->beta = 0.0;
-    sc->omega = 0.0;
-    sc->h0 = sqrt(rho);
-    sc->nb = sqrt(sc->tmp1);
-    sc->tol_abs = sc->tol * sc->nb;
-    h.rnorm[0] = sc->h0;
-    if (sc->h0 <= sc->tol_abs && !sc->bench) {
-      sc->done = 1;
-      sc->outcome = OUT_CONVERGED;
-    } else if (!isfinite(sc->alpha)) {
-      sc->done = 1;
-      sc->outcome = OUT_BREAKDOWN;
-    }
-  }
+  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_INIT2], tot) && threadIdx.x == 0)
+    publish<F_INIT2>(sc, h, tot);
 }
 
 // ---------------------------------------------------------------------------
@@ -165,7 +146,7 @@ __global__ void __launch_bounds__(256) k_init2(Geo g, Vecs V, Scal* __restrict__
 // replaced z.
 template <int DIM>
 __global__ void __launch_bounds__(256) k_sweepA(Geo g, Vecs V, Scal* __restrict__ sc,
-                                                Dd* __restrict__ part) {
+                                                Dd* __restrict__ part, Hist h) {
   if (sc->done) return;
   const int it = sc->iter;
   const double al = sc->alpha, be = sc->beta, om = sc->omega;
@@ -198,17 +179,8 @@ __global__ void __launch_bounds__(256) k_sweepA(Geo g, Vecs V, Scal* __restrict_
   zw[j] = zz;
   STENCIL_LOOP_END
   Dd tot[2];
-  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0) {
-    const double qy = dd_round(tot[0]), yy = dd_round(tot[1]);
-    const double omn = (yy == 0.0) ? 0.0 : qy / yy;  // line 16, guard A9
-    sc->omega = omn;
-    sc->use_rr = 0;
-    if (!isfinite(omn)) {
-      sc->done = 1;
-      sc->outcome = OUT_BREAKDOWN;
-      sc->iters = it;
-    }
-  }
+  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
+    publish<F_SWEEPA>(sc, h, tot);
 }
 
 // sweepC = Alg. 2 lines 17-21: x, r, k, w; u, q, y recomputed
@@ -250,14 +222,8 @@ __global__ void __launch_bounds__(256) k_sweepC(Geo g, Vecs V, Scal* __restrict_
   ww[j] = wn;
   STENCIL_LOOP_END
   Dd tot[5];
-  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0) {
-    if (rr_scheduled(sc)) {
-      sc->rr_fire = 1;  // line-21 dots are recomputed after the replacement
-    } else {
-      finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
-                         dd_round(tot[3]), dd_round(tot[4]));
-    }
-  }
+  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0)
+    publish<F_SWEEPC>(sc, h, tot);
 }
 
 // ---------------------------------------------------------------------------
@@ -301,11 +267,8 @@ __global__ void __launch_bounds__(256) k_rr2(Geo g, Vecs V, Scal* __restrict__ s
   dd_fma(acc[4], rc, rc);
   STENCIL_LOOP_END
   Dd tot[5];
-  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_RR2], tot) && threadIdx.x == 0) {
-    finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
-                       dd_round(tot[3]), dd_round(tot[4]));
-    sc->use_rr = 1;
-  }
+  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_RR2], tot) && threadIdx.x == 0)
+    publish<F_RR2>(sc, h, tot);
 }
 
 // ---------------------------------------------------------------------------
@@ -323,10 +286,8 @@ __global__ void __launch_bounds__(256) k_gap(Geo g, Vecs V, Scal* __restrict__ s
   dd_fma(acc[0], d, d);
   STENCIL_LOOP_END
   Dd tot[1];
-  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_GAP], tot) && threadIdx.x == 0) {
-    h.gap[sc->iter] = sqrt(dd_round(tot[0]));
-    sc->gap_iter = sc->iter;
-  }
+  if (dd_grid_reduce<1>(acc, part, &sc->counter[T_GAP], tot) && threadIdx.x == 0)
+    publish<F_GAP>(sc, h, tot);
 }
 
 // y = A x (pbicgstab_apply): same leg order as the solver.

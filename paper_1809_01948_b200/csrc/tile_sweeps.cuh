@@ -265,24 +265,8 @@ __global__ void __launch_bounds__(TNT, 1) t_sweep(TileGeo g, Vecs V, Scal* __res
   Dd tot[K];
   if (dd_grid_reduce<K>(acc, part, &sc->counter[MODE == 0 ? T_SWEEPA : T_SWEEPC], tot) &&
       tid == 0) {
-    if (MODE == 0) {
-      const double qy = dd_round(tot[0]), yy = dd_round(tot[1 % K]);
-      const double omn = (yy == 0.0) ? 0.0 : qy / yy;  // line 16, guard A9
-      sc->omega = omn;
-      sc->use_rr = 0;
-      if (!isfinite(omn)) {
-        sc->done = 1;
-        sc->outcome = OUT_BREAKDOWN;
-        sc->iters = it;
-      }
-    } else {
-      if (rr_scheduled(sc)) {
-        sc->rr_fire = 1;
-      } else {
-        finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1 % K]), dd_round(tot[2 % K]),
-                           dd_round(tot[3 % K]), dd_round(tot[4 % K]));
-      }
-    }
+    if (MODE == 0) publish<F_SWEEPA>(sc, h, tot);
+    else publish<F_SWEEPC>(sc, h, tot);
   }
 }
 

@@ -1,0 +1,115 @@
+"""Multi-rank path on one GPU through the loopback transport.
+
+pbicgstab_create_*_loopback builds P handles that partition the operator exactly
+as P processes would (z-/y-slabs, CSR row blocks), exchange ghost planes and the
+per-rank Dot2 rows with device copies (in place of NCCL send/recv/all-reduce),
+and form the scalars with the rank-order finalize kernels.  Kernels of different
+ranks never wait on each other (one stream).  Results must match the oracle
+(north-star bars; bitwise expected) and the single-rank run.
+"""
+import numpy as np
+import pytest
+
+from paper_1809_01948_b200 import problems
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_1809_01948_b200 import binding
+    assert torch.cuda.is_available()
+    return binding
+
+
+def _parity(res, ref, xs, bitwise=True):
+    k = min(30, ref.iters, res.iters)
+    rel = np.abs(res.rnorm[:k + 1] - ref.rnorm[:k + 1]) / np.maximum(ref.rnorm[:k + 1], 1e-300)
+    assert np.all(rel <= 1e-9), rel.max()
+    assert abs(res.iters - ref.iters) <= 2
+    x = res.x.cpu().numpy()
+    e, e0 = (np.linalg.norm(v - xs) / np.linalg.norm(xs) for v in (x, ref.x))
+    assert e <= 10 * e0 + 1e-15
+    if bitwise:
+        assert res.iters == ref.iters
+        assert np.array_equal(res.rnorm, ref.rnorm)
+        assert np.array_equal(x, ref.x)
+        if res.gap is not None:
+            assert np.array_equal(res.gap, ref.gap)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("dim,nx,ny,nz", [(3, 24, 20, 17), (2, 64, 37, 1), (3, 13, 7, 9)])
+@pytest.mark.parametrize("tile", [1, 0])
+def test_loopback_stencil_matches_oracle(B, orc, P, dim, nx, ny, nz, tile):
+    coef = problems.cfg34_coef() if dim == 3 else problems.cfg2_coef()
+    G = B.LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
+    G.set_option("tile", tile)
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 0)
+    b = orc.spmv(A, xs)
+    parts = G.split(torch.from_numpy(xs).cuda())
+    assert sum(s.n_local for s in G.ranks) == A.n
+    bd = G.apply(parts)
+    assert np.array_equal(torch.cat(bd).cpu().numpy(), b)
+    for rr in (0, 5):
+        res = G.solve(bd, tol=1e-11, maxit=200, rr_period=rr, gap=True)
+        ref = orc.pbicgstab(A, b, tol=1e-11, maxit=200, rr_period=rr)
+        assert res.outcome == ref.outcome
+        _parity(res, ref, xs)
+    G.close()
+
+
+def test_loopback_equals_single_rank_large(B, orc):
+    """A 3D problem spanning several tiles per slab, RR and gap on, graphs on."""
+    dim, nx, ny, nz = 3, 96, 80, 64
+    coef = problems.cfg34_coef()
+    xs = problems.x_star(nx * ny * nz, 0)
+    S = B.Solver.stencil(dim, nx, ny, nz, coef)
+    b1 = S.apply(torch.from_numpy(xs).cuda())
+    r1 = S.solve(b1, tol=1e-10, maxit=400, rr_period=50, gap=True)
+    for P in (2, 4):
+        G = B.LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
+        bd = G.split(b1)
+        rp = G.solve(bd, tol=1e-10, maxit=400, rr_period=50, gap=True)
+        assert rp.iters == r1.iters and rp.outcome == r1.outcome
+        rel = np.abs(rp.rnorm - r1.rnorm) / r1.rnorm
+        assert rel.max() <= 1e-9
+        assert np.array_equal(rp.rnorm, r1.rnorm)
+        assert np.array_equal(rp.x.cpu().numpy(), r1.x.cpu().numpy())
+        G.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("overlap", [1, 0])
+def test_loopback_csr_matches_oracle(B, orc, P, overlap):
+    n = 20000
+    M = problems.csr_band(n, nnz_row=27, band=500, seed=1)
+    A = orc.csr(M.row_ptr, M.col, M.val)
+    xs = problems.x_star(n, 0)
+    b = orc.spmv(A, xs)
+    cuts = np.linspace(0, n, P + 1).astype(int)
+    blocks = []
+    for r in range(P):
+        lo, hi = cuts[r], cuts[r + 1]
+        rp = M.row_ptr[lo:hi + 1] - M.row_ptr[lo]
+        sl = slice(M.row_ptr[lo], M.row_ptr[hi])
+        blocks.append((int(lo), rp, M.col[sl], M.val[sl]))
+    G = B.LoopbackGroup.csr(blocks, n)
+    G.set_option("overlap", overlap)
+    bd = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    assert np.array_equal(torch.cat(bd).cpu().numpy(), b)
+    for rr in (0, 3):
+        res = G.solve(bd, tol=1e-12, maxit=100, rr_period=rr, gap=True)
+        ref = orc.pbicgstab(A, b, tol=1e-12, maxit=100, rr_period=rr)
+        _parity(res, ref, xs)
+    G.close()
+
+
+def test_partition_is_balanced_slabs(B):
+    G = B.LoopbackGroup.stencil(3, 3, 10, 10, 11, problems.cfg34_coef())
+    nl = [s.n_local for s in G.ranks]
+    rb = [s.row_begin for s in G.ranks]
+    assert nl == [400, 400, 300] and rb == [0, 400, 800]
+    G.close()
