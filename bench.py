@@ -154,18 +154,30 @@ def run_reference(args, rank, world):
     return 0
 
 
+def setup_solver(args, st, rank, world, dev, stream):
+    """One handle per process; NCCL communicators for world > 1 (ids broadcast
+    over the torch process group)."""
+    import torch
+    from paper_1809_01948_b200 import Solver, binding
+    if world == 1:
+        return Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef, stream=stream)
+    ids = [binding.nccl_unique_id(), binding.nccl_unique_id()] if rank == 0 else [None, None]
+    torch.distributed.broadcast_object_list(ids, src=0)
+    dist = binding.make_dist(world, rank, ids[0], ids[1])
+    return Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef, stream=stream, dist=dist)
+
+
 def run_ours(args, rank, world):
     import torch
-    from paper_1809_01948_b200 import Solver
 
     dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
     cfg, st, maxit, rr = workload(args.config)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     stream = torch.cuda.Stream()
-    S = Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef, stream=stream)
+    S = setup_solver(args, st, rank, world, dev, stream)
     n = S.n_local
     xs_full = problems.x_star(st.n, seed=0)
     xs = torch.from_numpy(xs_full[S.row_begin:S.row_begin + n]).to(f"cuda:{dev}")
@@ -188,6 +200,13 @@ def run_ours(args, rank, world):
         if world > 1:
             torch.distributed.barrier()
 
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{dev}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
     # ---- timed region: device time with CUDA events on the solver's stream
     S.set_option("timing", 1)  # events around every kernel (graphs off; launches are ms-long)
     S.kernel_time("all", reset=True)
@@ -202,14 +221,10 @@ def run_ours(args, rank, world):
         e1.record(stream)
         torch.cuda.synchronize()
     barrier()
-    ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(e0.elapsed_time(e1))
     launches, _ = S.kernel_time("all")
     per_kernel = {}
-    for k in ("sweepA", "sweepC", "rr1", "rr2", "gap", "init", "apply"):
+    for k in ("sweepA", "sweepC", "rr1", "rr2", "gap", "init", "apply", "fin"):
         nk, tk = S.kernel_time(k)
         if nk:
             per_kernel[k] = {"launches": nk, "avg_ms": tk / nk, "bytes": S.kernel_bytes(k)}
@@ -227,27 +242,25 @@ def run_ours(args, rank, world):
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
     e2e_iters = 0
-    for _ in range(max(1, args.steps // 2)):
+    e2e_steps = max(1, args.steps // 2)
+    for _ in range(e2e_steps):
         e2e_iters += S.solve_host(hbn, hx0n, tol=0.0, maxit=maxit, rr_period=rr, gap=gap,
                                   x_out=hxn).iters
     f1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1)
-    if world > 1:
-        t = torch.tensor([e2e_ms], device=f"cuda:{dev}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1))
     if rank != 0:
         return 0
 
     peak, peak_src = measured_peak()
-    value = iters * world / (ms / 1000.0)
+    # strong scaling: every rank advances the same global iterations
+    value = iters / (ms / 1000.0)
     dom = "sweepC"
     kb = per_kernel[dom]["bytes"]
     k_avg_s = per_kernel[dom]["avg_ms"] / 1000.0
     achieved = kb / k_avg_s / 1e9
-    it_bytes = S.kernel_bytes("iteration")
-    traffic = ncu_traffic(dom)
+    it_bytes = S.kernel_bytes("iteration") * world  # all ranks' algorithmic bytes per iteration
+    traffic = ncu_traffic(dom) if world == 1 else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
@@ -255,17 +268,19 @@ def run_ours(args, rank, world):
         "data": "synthetic (seeded x* ~ U[-1,1], b = A x* on device)",
         "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": st.n, "grid": [st.nx, st.ny, st.nz],
                    "maxit_per_step": maxit, "rr_period": rr, "gap_tracking": gap,
-                   "schedule": "fused 2-sweep (stencil)", "l2": "inputs larger than L2 (%.1f GB)"
-                   % (14 * 8 * n / 1e9), "parallelism": f"z-slab x{world}"},
+                   "schedule": "fused 2-sweep (stencil), TMA 2.5D sweeps",
+                   "l2": "inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9),
+                   "parallelism": f"z-slab x{world}" + (" (NCCL halo + rank-row all-gather)"
+                                                        if world > 1 else "")},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
                      "iteration_frac": (it_bytes * value / world / 1e9) / peak},
         "kernels": per_kernel,
         "gpu_launches": launches,
-        "e2e": {"value": e2e_iters * world / (e2e_ms / 1000.0), "unit": UNIT,
-                "h2d_bytes_per_step": 2 * 8 * n, "d2h_bytes_per_step": 8 * n + 8 * (maxit + 1)
-                * (2 if gap else 1)},
+        "e2e": {"value": e2e_iters / (e2e_ms / 1000.0), "unit": UNIT,
+                "h2d_bytes_per_step": 2 * 8 * n * world,
+                "d2h_bytes_per_step": 8 * n * world + 8 * (maxit + 1) * (2 if gap else 1)},
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and world == 1:
@@ -278,6 +293,33 @@ def run_ours(args, rank, world):
     return 0
 
 
+def run_loopback(args):
+    """--loopback P: the multi-rank code path (partition, halos, rank-row
+    reductions, finalize kernels) with P ranks emulated on ONE GPU.  Not a
+    scaling number: it measures the overhead of the distributed schedule."""
+    import torch
+    from paper_1809_01948_b200 import binding
+    cfg, st, maxit, rr = workload(args.config)
+    P = args.loopback
+    G = binding.LoopbackGroup.stencil(P, st.dim, st.nx, st.ny, st.nz, st.coef)
+    xs = torch.from_numpy(problems.x_star(st.n, 0)).cuda()
+    bs = G.apply(G.split(xs))
+    del xs
+    G.set_option("bench", 1)
+    for _ in range(args.warmup):
+        G.solve(bs, tol=0.0, maxit=maxit, rr_period=rr, gap=bool(args.gap))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        r = G.solve(bs, tol=0.0, maxit=maxit, rr_period=rr, gap=bool(args.gap))
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    print(json.dumps({"mode": f"loopback x{P} on 1 GPU", "config": cfg.name,
+                      "iterations_per_s": args.steps * maxit / dt, "iters": r.iters}), flush=True)
+    G.close()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -287,14 +329,21 @@ def main():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--gap", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--loopback", type=int, default=0,
+                    help="emulate P ranks on one GPU (multi-rank code path check)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup raised to 3 (timing rules)", file=sys.stderr)
         args.warmup = 3
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", str(args.gpus if args.gpus == 1 else 1)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != world and args.impl == "ours":
+        print(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; launch with torchrun for N>1",
+              file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, rank, world)
+    if args.loopback:
+        return run_loopback(args)
     return run_ours(args, rank, world)
 
 

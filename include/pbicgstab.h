@@ -131,6 +131,13 @@ pbicg_status pbicgstab_solve_loopback(pbicg_handle* hs, int32_t nranks,
                                       double* const* x_dev_out, double* rnorm_hist,
                                       double* gap_hist, int32_t* iters_out, int32_t* outcome_out);
 
+/* Host-only (no device needed): the slab a stencil handle of `rank` out of
+ * `nranks` will own -- contiguous z-slabs (3D) / y-slabs (2D) of floor or ceil
+ * (outer/nranks) planes, lower ranks taking the remainder.  Rows
+ * [row_begin, row_begin + n_local).  EINVAL if nranks exceeds the slab count. */
+pbicg_status pbicgstab_stencil_partition(const pbicg_stencil* op, int32_t nranks, int32_t rank,
+                                         int64_t* row_begin, int64_t* n_local);
+
 /* Global rows owned by this rank: [row_begin, row_begin + n_local). */
 pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n_local);
 

@@ -44,7 +44,7 @@ class _Dist(ctypes.Structure):
 
 SYMBOLS = ["pbicgstab_create_stencil", "pbicgstab_create_csr", "pbicgstab_create_stencil_loopback",
            "pbicgstab_create_csr_loopback", "pbicgstab_apply_loopback", "pbicgstab_solve_loopback",
-           "pbicgstab_local_rows",
+           "pbicgstab_local_rows", "pbicgstab_stencil_partition",
            "pbicgstab_set_option", "pbicgstab_apply", "pbicgstab_solve", "pbicgstab_solve_host",
            "pbicgstab_kernel_time", "pbicgstab_kernel_bytes", "pbicgstab_get_unique_id",
            "pbicgstab_last_error", "pbicgstab_destroy"]
@@ -78,6 +78,8 @@ def lib(build: bool = True):
     L.pbicgstab_solve_loopback.argtypes = [P, i32, P, P, f64, i32, i32, P, P, P,
                                            ctypes.POINTER(i32), ctypes.POINTER(i32)]
     L.pbicgstab_local_rows.argtypes = [P, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.pbicgstab_stencil_partition.argtypes = [ctypes.POINTER(_Stencil), i32, i32,
+                                              ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.pbicgstab_set_option.argtypes = [P, ctypes.c_char_p, i64]
     L.pbicgstab_apply.argtypes = [P, P, P]
     L.pbicgstab_solve.argtypes = [P, P, P, f64, i32, i32, P, P, P, ctypes.POINTER(i32),
@@ -116,6 +118,32 @@ def _stream_ptr(stream):
     if stream is None:
         return None
     return ctypes.c_void_p(int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def stencil_partition(dim: int, nx: int, ny: int, nz: int, nranks: int, rank: int):
+    """Rows [row_begin, row_begin + n_local) the stencil handle of `rank` owns (host-only)."""
+    st = _Stencil(dim, nx, ny, nz if dim == 3 else 1, (ctypes.c_double * 7)(1, 0, 0, 0, 0, 0, 0))
+    rb, nl = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().pbicgstab_stencil_partition(ctypes.byref(st), nranks, rank, ctypes.byref(rb),
+                                             ctypes.byref(nl)))
+    return rb.value, nl.value
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId from the library's NCCL (rank 0 calls this)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().pbicgstab_get_unique_id(buf))
+    return buf.raw
+
+
+def make_dist(nranks: int, rank: int, uid_halo: bytes, uid_red: bytes | None = None):
+    """pbicg_dist for one process of an NCCL job (keeps the id buffers alive)."""
+    bh = ctypes.create_string_buffer(uid_halo, 128)
+    br = ctypes.create_string_buffer(uid_red, 128) if uid_red else None
+    d = _Dist(nranks, rank, ctypes.cast(bh, ctypes.c_void_p),
+              ctypes.cast(br, ctypes.c_void_p) if br is not None else None)
+    d._keep = (bh, br)
+    return d
 
 
 @dataclass

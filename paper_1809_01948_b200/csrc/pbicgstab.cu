@@ -61,6 +61,7 @@ struct pbicg_ctx {
   Geo geo{};
   TileGeo tg{};
   bool tile_ok = false;  // TMA 2.5D sweeps eligible for this operator
+  bool tile_vec = false; // ... with 16-byte aligned pairs (nx even)
   int tile_on = 1;       // option "tile"
   size_t tile_smem[2] = {0, 0};
   CsrOp csr{};
@@ -234,18 +235,24 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SWEEPA: {
       LaunchScope ls(h, K_SWEEPA);
-      if (tile)
-        t_sweep<DIM, 0><<<tgrid, TNT, h->tile_smem[0], h->stream>>>(h->tg, h->V, h->scal, h->part,
-                                                                    h->hist);
+      if (tile && h->tile_vec)
+        t_sweep<DIM, 0, true><<<tgrid, TNT, h->tile_smem[0], h->stream>>>(h->tg, h->V, h->scal,
+                                                                          h->part, h->hist);
+      else if (tile)
+        t_sweep<DIM, 0, false><<<tgrid, TNT, h->tile_smem[0], h->stream>>>(h->tg, h->V, h->scal,
+                                                                           h->part, h->hist);
       else
         k_sweepA<DIM><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
                                                                        h->hist);
     } break;
     case PH_SWEEPC: {
       LaunchScope ls(h, K_SWEEPC);
-      if (tile)
-        t_sweep<DIM, 1><<<tgrid, TNT, h->tile_smem[1], h->stream>>>(h->tg, h->V, h->scal, h->part,
-                                                                    h->hist);
+      if (tile && h->tile_vec)
+        t_sweep<DIM, 1, true><<<tgrid, TNT, h->tile_smem[1], h->stream>>>(h->tg, h->V, h->scal,
+                                                                          h->part, h->hist);
+      else if (tile)
+        t_sweep<DIM, 1, false><<<tgrid, TNT, h->tile_smem[1], h->stream>>>(h->tg, h->V, h->scal,
+                                                                           h->part, h->hist);
       else
         k_sweepC<DIM><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
                                                                        h->hist);
@@ -556,10 +563,11 @@ void setup_tile(pbicg_ctx* h) {
   TileGeo& t = h->tg;
   h->tile_ok = false;
   const int dim = h->dim;
-  const int64_t tpmax = 2LL * TNT * TKMAX;
+  const int64_t tpmax = 2LL * TNT;  // one row pair per thread
   if (g.nx > tpmax) return;
+  h->tile_vec = (g.nx % 2) == 0;  // then every staged range / vector is 16-byte aligned
   const int64_t lines = dim == 3 ? g.ny : 1;
-  int64_t TY = dim == 3 ? (1024 / g.nx) : 1;
+  int64_t TY = dim == 3 ? (tpmax / g.nx) : 1;
   if (TY < 1) TY = 1;
   if (TY > lines) TY = lines;
   int max_smem = 0;
@@ -606,19 +614,21 @@ void setup_tile(pbicg_ctx* h) {
   t.units = t.nchunks * t.ncols;
   h->tile_smem[0] = tile_smem_bytes(t, 0);
   h->tile_smem[1] = tile_smem_bytes(t, 1);
-  cudaError_t e1, e2;
+  const int a0 = (int)h->tile_smem[0], a1 = (int)h->tile_smem[1];
+  const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  cudaError_t e = cudaSuccess;
   if (dim == 3) {
-    e1 = cudaFuncSetAttribute(t_sweep<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)h->tile_smem[0]);
-    e2 = cudaFuncSetAttribute(t_sweep<3, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)h->tile_smem[1]);
+    e = (cudaError_t)(cudaFuncSetAttribute(t_sweep<3, 0, true>, A, a0) |
+                      cudaFuncSetAttribute(t_sweep<3, 1, true>, A, a1) |
+                      cudaFuncSetAttribute(t_sweep<3, 0, false>, A, a0) |
+                      cudaFuncSetAttribute(t_sweep<3, 1, false>, A, a1));
   } else {
-    e1 = cudaFuncSetAttribute(t_sweep<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)h->tile_smem[0]);
-    e2 = cudaFuncSetAttribute(t_sweep<2, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)h->tile_smem[1]);
+    e = (cudaError_t)(cudaFuncSetAttribute(t_sweep<2, 0, true>, A, a0) |
+                      cudaFuncSetAttribute(t_sweep<2, 1, true>, A, a1) |
+                      cudaFuncSetAttribute(t_sweep<2, 0, false>, A, a0) |
+                      cudaFuncSetAttribute(t_sweep<2, 1, false>, A, a1));
   }
-  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+  if (e != cudaSuccess) {
     cudaGetLastError();
     return;
   }
@@ -1175,6 +1185,21 @@ pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec
     return st;
   }
   for (int r = 0; r < nranks; ++r) out[r] = grp->m[r];
+  return PBICG_OK;
+}
+
+pbicg_status pbicgstab_stencil_partition(const pbicg_stencil* op, int32_t nranks, int32_t rank,
+                                         int64_t* row_begin, int64_t* n_local) {
+  if (!row_begin || !n_local) return fail(nullptr, PBICG_EINVAL, "NULL argument");
+  if (rank < 0 || rank >= nranks) return fail(nullptr, PBICG_EINVAL, "inconsistent nranks/rank");
+  ST(validate_stencil(op, nranks));
+  const int64_t nz = op->dim == 3 ? op->nz : 1;
+  const int64_t outer = op->dim == 3 ? nz : op->ny;
+  const int64_t plane = op->dim == 3 ? op->nx * op->ny : op->nx;
+  int64_t o0 = 0, nol = 0;
+  slab(outer, nranks, rank, &o0, &nol);
+  *row_begin = o0 * plane;
+  *n_local = nol * plane;
   return PBICG_OK;
 }
 
