@@ -56,5 +56,5 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force=True, verbose=True)
+    build(force=True, verbose="-v" in __import__("sys").argv)
     print(LIB)

@@ -8,11 +8,15 @@
 //   [-> rr1 -> rr2 (eq:rr)] -> spmvD (lines 22-23)
 // Each row is summed in its stored (ascending column) order (reading A5); a
 // padded slot (rows shorter than the ELL width) is skipped, never added.
-// Buffers: V.w0 = w, V.w1 = t, V.z0 = z, V.z1 = v, V.zrr = replaced z (A26).
+// Buffers: V.w0 = w, V.w1 = t, V.z0 = z, V.z1 = v, V.zrr = replaced z (A26),
+// V.nv = n_i = M^-1 z_i (written by sweep A), V.mv = m_i = M^-1 w_i (written by
+// sweep C / rr2 / init2): the SpMVs read n and m, so each gathered operand is
+// one vector (the same values the oracle forms in lines 13 and 22).
 #pragma once
 #include "dd.cuh"
 #include "state.cuh"
 #include "stencil_kernels.cuh"  // Vecs
+#include "tma.cuh"
 
 struct CsrOp {
   int64_t n;             // local rows
@@ -23,15 +27,34 @@ struct CsrOp {
   const double* dinv;    // [n + 2H] ghosted Jacobi inverse diagonal (A3)
 };
 
-// fl(A v)_j or fl(A M^-1 v)_j
+// fl(A v)_j or fl(A M^-1 v)_j, summed left to right in stored (ascending
+// column) order from +0.0 (A5).  Slots are processed in groups of ELL_U with all
+// loads of a group issued before its adds (memory-level parallelism); the
+// matrix is streamed with evict-first loads so L1/L2 keep the gathered window.
+#define ELL_U 9
 template <bool PREC>
 __device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restrict__ v, int64_t j) {
   const int len = A.len ? A.len[j] : A.width;
   double acc = 0.0;
-  for (int p = 0; p < len; ++p) {
-    const int64_t c = A.col[(int64_t)p * A.n + j];
-    const double a = A.val[(int64_t)p * A.n + j];
-    const double x = PREC ? A.dinv[c] * __ldg(v + c) : __ldg(v + c);
+  int p = 0;
+  for (; p + ELL_U <= len; p += ELL_U) {
+    int c[ELL_U];
+    double a[ELL_U], x[ELL_U];
+#pragma unroll
+    for (int u = 0; u < ELL_U; ++u) {
+      c[u] = __ldcs(A.col + (int64_t)(p + u) * A.n + j);
+      a[u] = __ldcs(A.val + (int64_t)(p + u) * A.n + j);
+    }
+#pragma unroll
+    for (int u = 0; u < ELL_U; ++u)
+      x[u] = PREC ? __ldg(A.dinv + c[u]) * __ldg(v + c[u]) : __ldg(v + c[u]);
+#pragma unroll
+    for (int u = 0; u < ELL_U; ++u) acc = acc + a[u] * x[u];
+  }
+  for (; p < len; ++p) {
+    const int c = __ldcs(A.col + (int64_t)p * A.n + j);
+    const double a = __ldcs(A.val + (int64_t)p * A.n + j);
+    const double x = PREC ? __ldg(A.dinv + c) * __ldg(v + c) : __ldg(v + c);
     acc = acc + a * x;
   }
   return acc;
@@ -63,6 +86,7 @@ __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict
   ROW_LOOP {
     const double wj = ell_row<true>(A, V.r, j);  // w0 = A M^-1 r0 = A k0
     V.w0[j] = wj;
+    V.mv[j] = A.dinv[j] * wj;                     // m0 = M^-1 w0 (line 2)
     dd_fma(acc[0], V.rh[j], wj);
   }
   Dd tot[1];
@@ -96,16 +120,17 @@ __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restric
     V.s[j] = sn;
     V.l[j] = ln;
     V.z0[j] = zn;
+    V.nv[j] = dj * zn;  // n_i = M^-1 z_i (line 13)
   }
   Dd tot[2];
   if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
     publish<F_SWEEPA>(sc, h, tot);
 }
 
-// lines 13-14: n_i = M^-1 z_i, v_i = A n_i
+// line 14: v_i = A n_i (gather version; c_spmv_win is the staged one)
 __global__ void __launch_bounds__(256) c_spmvB(CsrOp A, Vecs V, Scal* __restrict__ sc) {
   if (sc->done) return;
-  ROW_LOOP { V.z1[j] = ell_row<true>(A, V.z0, j); }
+  ROW_LOOP { V.z1[j] = ell_row<false>(A, V.nv, j); }
 }
 
 // lines 17-21
@@ -137,6 +162,7 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
     V.r[j] = rn;
     V.k[j] = kn;
     V.w0[j] = wn;
+    V.mv[j] = dj * wn;  // m_{i+1} = M^-1 w_{i+1} (line 22)
   }
   Dd tot[5];
   if (dd_grid_reduce<5>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0)
@@ -166,6 +192,7 @@ __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__
     const double wn = ell_row<true>(A, V.r, j);
     const double zr = ell_row<true>(A, V.s, j);
     V.w0[j] = wn;
+    V.mv[j] = A.dinv[j] * wn;  // m_{i+1} follows the replaced w (A27)
     V.zrr[j] = zr;
     const double rhj = V.rh[j], rc = V.r[j];
     dd_fma(acc[0], rhj, rc);
@@ -179,10 +206,109 @@ __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__
     publish<F_RR2>(sc, h, tot);
 }
 
-// lines 22-23: m_{i+1} = M^-1 w_{i+1}, t_{i+1} = A m_{i+1} (also t_0 at init)
+// line 23: t_{i+1} = A m_{i+1} (also t_0 at init); gather version
 __global__ void __launch_bounds__(256) c_spmvD(CsrOp A, Vecs V, Scal* __restrict__ sc) {
   if (sc->done) return;
-  ROW_LOOP { V.w1[j] = ell_row<true>(A, V.w0, j); }
+  ROW_LOOP { V.w1[j] = ell_row<false>(A, V.mv, j); }
+}
+
+// ---------------------------------------------------------------------------
+// Window SpMV y = A u for banded matrices (|col - row| <= bw): a CTA walks a
+// contiguous row range in steps of WTB rows; the operand window
+// [j0 - bw, j0 + WTB + bw) lives in a 2^k shared-memory ring filled by TMA
+// bulk copies two steps ahead, so the 27 gathers per row are shared-memory
+// loads (position = (e + off) & (WRS - 1)) and each operand element comes from
+// HBM/L2 once per CTA.  Each row is summed in stored order from +0.0 (A5).
+#define WTB 2048
+#define WRS 16384
+#define WNT 512
+
+struct WinGeo {
+  int64_t lo, hi;     // valid operand range [lo, hi) (ghosts included)
+  int64_t off;        // element offset making (e + off) >= 0 and chunk-aligned
+  int32_t bw;         // half bandwidth
+  int32_t rows_cta;   // rows per CTA (multiple of WTB)
+};
+
+__device__ __forceinline__ void win_issue(double* ring, const double* __restrict__ u, int64_t x0,
+                                          int64_t x1, const WinGeo& w, uint64_t* bar) {
+  // load elements [x0, x1) clamped to the valid range, chunk by chunk (no wrap)
+  int64_t a = x0 > w.lo ? x0 : w.lo;
+  const int64_t b = x1 < w.hi ? x1 : w.hi;
+  uint32_t total = 0;
+  for (int64_t c = a; c < b;) {
+    const int64_t cend = ((c + w.off) / WTB + 1) * WTB - w.off;
+    const int64_t e = cend < b ? cend : b;
+    total += (uint32_t)(((e - c) * 8 + 15) & ~15);
+    c = e;
+  }
+  mbar_arrive_expect_tx(bar, total);
+  for (int64_t c = a; c < b;) {
+    const int64_t cend = ((c + w.off) / WTB + 1) * WTB - w.off;
+    const int64_t e = cend < b ? cend : b;
+    const uint32_t bytes = (uint32_t)(((e - c) * 8 + 15) & ~15);
+    bulk_g2s(ring + ((c + w.off) & (WRS - 1)), u + c, bytes, bar);
+    c = e;
+  }
+}
+
+template <int WHICH>  // 0: v = A n (line 14), 1: t = A m (line 23)
+__global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                                     WinGeo w) {
+  if (sc->done) return;
+  const double* __restrict__ u = WHICH == 0 ? V.nv : V.mv;
+  double* __restrict__ y = WHICH == 0 ? V.z1 : V.w1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  double* ring = reinterpret_cast<double*>(smem_raw + 64);
+  const int64_t R0 = (int64_t)blockIdx.x * w.rows_cta;
+  if (R0 >= A.n) return;
+  const int64_t R1 = (R0 + w.rows_cta) < A.n ? (R0 + w.rows_cta) : A.n;
+  const int nsteps = (int)((R1 - R0 + WTB - 1) / WTB);
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    win_issue(ring, u, R0 - w.bw, R0 + WTB + w.bw, w, &bar[0]);
+    if (nsteps > 1) win_issue(ring, u, R0 + WTB + w.bw, R0 + 2 * WTB + w.bw, w, &bar[1]);
+  }
+  uint32_t ph = 0;
+  for (int s = 0; s < nsteps; ++s) {
+    const int b = s & 1;
+    mbar_wait(&bar[b], (ph >> b) & 1u);
+    ph ^= 1u << b;
+    const int64_t j0 = R0 + (int64_t)s * WTB;
+#pragma unroll
+    for (int q = 0; q < WTB / WNT; ++q) {
+      const int64_t j = j0 + threadIdx.x + q * WNT;
+      if (j >= R1) break;
+      const int len = A.len ? A.len[j] : A.width;
+      double acc = 0.0;
+      int p = 0;
+      for (; p + ELL_U <= len; p += ELL_U) {
+        int c[ELL_U];
+        double a[ELL_U];
+#pragma unroll
+        for (int k = 0; k < ELL_U; ++k) {
+          c[k] = __ldcs(A.col + (int64_t)(p + k) * A.n + j);
+          a[k] = __ldcs(A.val + (int64_t)(p + k) * A.n + j);
+        }
+#pragma unroll
+        for (int k = 0; k < ELL_U; ++k) acc = acc + a[k] * ring[(c[k] + w.off) & (WRS - 1)];
+      }
+      for (; p < len; ++p) {
+        const int c = __ldcs(A.col + (int64_t)p * A.n + j);
+        acc = acc + __ldcs(A.val + (int64_t)p * A.n + j) * ring[(c + w.off) & (WRS - 1)];
+      }
+      __stcs(y + j, acc);
+    }
+    __syncthreads();  // step s done: its oldest chunk may be overwritten
+    if (threadIdx.x == 0 && s + 2 < nsteps)
+      win_issue(ring, u, j0 + 2 * WTB + w.bw, j0 + 3 * WTB + w.bw, w, &bar[b]);
+  }
 }
 
 __global__ void __launch_bounds__(256) c_gap(CsrOp A, Vecs V, Scal* __restrict__ sc,

@@ -30,6 +30,7 @@
 namespace {
 
 thread_local std::string g_create_err;
+constexpr int WIN_SMEM = 64 + WRS * (int)sizeof(double);
 
 enum Kname { K_INIT = 0, K_SWEEPA, K_SWEEPC, K_SPMVB, K_SPMVD, K_RR1, K_RR2, K_GAP, K_APPLY, K_FIN,
              K_N };
@@ -65,6 +66,9 @@ struct pbicg_ctx {
   int tile_on = 1;       // option "tile"
   size_t tile_smem[2] = {0, 0};
   CsrOp csr{};
+  WinGeo wg{};
+  bool win_ok = false;  // banded CSR: window SpMV (c_spmv_win) eligible
+  int win_grid = 0;
   std::vector<void*> allocs;
   Vecs V{};
   double* xtmp = nullptr;    // ghosted scratch (apply input, host-solve staging)
@@ -149,7 +153,7 @@ pbicg_status dalloc(pbicg_ctx* h, void** p, size_t bytes) {
 // ghosted vector: H doubles before and after n_local rows, zero-filled
 pbicg_status gvec(pbicg_ctx* h, double** out) {
   void* p = nullptr;
-  size_t n = (size_t)(h->n_local + 2 * h->H);
+  size_t n = (size_t)(h->n_local + 2 * h->H) + 2;  // +2: 16-byte rounding of bulk copies
   ST(dalloc(h, &p, n * sizeof(double)));
   CU(cudaMemsetAsync(p, 0, n * sizeof(double), h->stream));
   *out = (double*)p + h->H;
@@ -291,7 +295,10 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SPMVB: {
       LaunchScope ls(h, K_SPMVB);
-      c_spmvB<<<h->grid[K_SPMVB], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      if (h->win_ok)
+        c_spmv_win<0><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg);
+      else
+        c_spmvB<<<h->grid[K_SPMVB], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
     case PH_SWEEPC: {
       LaunchScope ls(h, K_SWEEPC);
@@ -307,7 +314,10 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SPMVD: {
       LaunchScope ls(h, K_SPMVD);
-      c_spmvD<<<h->grid[K_SPMVD], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      if (h->win_ok)
+        c_spmv_win<1><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg);
+      else
+        c_spmvD<<<h->grid[K_SPMVD], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
     case PH_GAP: {
       LaunchScope ls(h, K_GAP);
@@ -420,6 +430,8 @@ const VecSel SW0 = [](pbicg_ctx* h) { return h->V.w0; };
 const VecSel SW1 = [](pbicg_ctx* h) { return h->V.w1; };
 const VecSel SZ0 = [](pbicg_ctx* h) { return h->V.z0; };
 const VecSel SZ1 = [](pbicg_ctx* h) { return h->V.z1; };
+const VecSel SNV = [](pbicg_ctx* h) { return h->V.nv; };
+const VecSel SMV = [](pbicg_ctx* h) { return h->V.mv; };
 
 // Alg. 2 lines 2-3 [+ gap of iteration 0]
 void enq_init(const Members& G) {
@@ -431,8 +443,12 @@ void enq_init(const Members& G) {
   if (dist) comm_halo(G, {SR});
   each(G, PH_INIT2);
   reduce_fin(G, F_INIT2);
-  if (dist) comm_halo(G, {SW0});  // w_0 is read with the stencil / SpMV
-  if (h0->kind == KIND_CSR) each(G, PH_SPMVD);  // t_0 = A M^-1 w_0 (line 3)
+  if (h0->kind == KIND_CSR) {  // t_0 = A m_0 (line 3)
+    if (dist) comm_halo(G, {SMV});
+    each(G, PH_SPMVD);
+  } else if (dist) {
+    comm_halo(G, {SW0});  // w_0 is read with the stencil
+  }
   if (h0->gap_on) {
     each(G, PH_GAP);
     reduce_fin(G, F_GAP);
@@ -473,7 +489,7 @@ void enq_iter(const Members& G, bool with_rr, int par) {
     } else if (dist) {
       comm_reduce(G, false);
     }
-    if (dist) comm_halo(G, {SZ0});
+    if (dist) comm_halo(G, {SNV});  // n_i ghosts for v_i = A n_i
     each(G, PH_SPMVB);  // lines 13-14
     if (ov) cudaStreamWaitEvent(h0->stream, h0->ev_join, 0);
     each_fin(G, F_SWEEPA);
@@ -486,7 +502,7 @@ void enq_iter(const Members& G, bool with_rr, int par) {
       each(G, PH_RR2);
       reduce_fin(G, F_RR2);
     }
-    if (dist) comm_halo(G, {SW0});
+    if (dist) comm_halo(G, {SMV});  // m_{i+1} ghosts
     each(G, PH_SPMVD);  // lines 22-23
   }
   if (h0->gap_on) {
@@ -891,6 +907,32 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
   h->grid[K_RR2] = occ_grid(h, c_rr2, blocks);
   h->grid[K_GAP] = occ_grid(h, c_gap, blocks);
   h->grid[K_APPLY] = occ_grid(h, c_apply, blocks);
+  ST(gvec(h, &h->V.nv));
+  ST(gvec(h, &h->V.mv));
+  // window SpMV: half bandwidth of this rank's rows, ring of WRS doubles
+  int64_t bw = 0;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t q = rp[i]; q < rp[i + 1]; ++q) {
+      const int64_t d = op->col[q] - (op->row_begin + i);
+      bw = d < 0 ? (-d > bw ? -d : bw) : (d > bw ? d : bw);
+    }
+  if (3LL * WTB + 2 * bw <= WRS) {
+    WinGeo& w = h->wg;
+    w.bw = (int32_t)bw;
+    w.lo = -h->H;
+    w.hi = n + h->H;
+    w.off = ((h->H + WTB - 1) / WTB) * WTB;
+    int64_t per = (n + h->num_sm - 1) / h->num_sm;
+    per = ((per + WTB - 1) / WTB) * WTB;
+    w.rows_cta = (int32_t)per;
+    h->win_grid = (int)((n + per - 1) / per);
+    cudaError_t e1 = cudaFuncSetAttribute(c_spmv_win<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          WIN_SMEM);
+    cudaError_t e2 = cudaFuncSetAttribute(c_spmv_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          WIN_SMEM);
+    h->win_ok = e1 == cudaSuccess && e2 == cudaSuccess;
+    cudaGetLastError();
+  }
   return alloc_common(h);
 }
 
@@ -1380,10 +1422,9 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
   } else {
     const double slots = (double)h->csr.width;  // ELL width
     const double mat = 12.0 * slots * N;        // val (8) + col (4) per slot
-    if (n == "sweepA") b = 14 * 8 * N;          // read k,g,l,w,s,z,t,v,r,dinv; write g,s,l,z
-    else if (n == "spmvB" || n == "spmvD") b = mat + 3 * 8 * N;  // in, dinv, out
-    else if (n == "apply") b = mat + 2 * 8 * N;
-    else if (n == "sweepC") b = 16 * 8 * N;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w
+    if (n == "sweepA") b = 15 * 8 * N;  // read k,g,l,w,s,z,t,v,r,dinv; write g,s,l,z,n
+    else if (n == "spmvB" || n == "spmvD" || n == "apply") b = mat + 2 * 8 * N;  // n|m in, out
+    else if (n == "sweepC") b = 17 * 8 * N;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w,m
     else if (n == "rr1") b = 2 * mat + 8 * 8 * N;
     else if (n == "rr2") b = 2 * mat + 7 * 8 * N;
     else if (n == "gap") b = mat + 3 * 8 * N;

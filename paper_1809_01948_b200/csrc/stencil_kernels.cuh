@@ -33,6 +33,7 @@ struct Geo {
 struct Vecs {
   double *x, *r, *rh, *k, *g, *s, *l, *b;
   double *w0, *w1, *z0, *z1, *zrr;
+  double *nv, *mv;  // CSR path: n = M^-1 z and m = M^-1 w, inputs of the window SpMVs
 };
 
 template <int DIM>

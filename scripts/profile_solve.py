@@ -17,9 +17,15 @@ ap.add_argument("--rr", type=int, default=2)
 ap.add_argument("--gap", type=int, default=0)
 a = ap.parse_args()
 cfg = problems.configs()[a.config]
-st = cfg.stencil
-S = Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef)
-xs = torch.from_numpy(problems.x_star(st.n, 0)).cuda()
+if cfg.kind == "csr":
+    M = problems.csr_band(cfg.csr_n, nnz_row=27, band=4096, seed=1)
+    S = Solver.csr(M.n, M.row_ptr, M.col, M.val)
+    n = M.n
+else:
+    st = cfg.stencil
+    S = Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef)
+    n = st.n
+xs = torch.from_numpy(problems.x_star(n, 0)).cuda()
 b = S.apply(xs)
 S.set_option("bench", 1)
 S.set_option("graphs", 0)

@@ -209,3 +209,18 @@ def test_tile_and_simple_kernels_agree_with_oracle(S, orc, dim, nx, ny, nz, kind
         solver.set_option("tile", tile)
         res = solver.solve(b_d, tol=1e-11, maxit=150, rr_period=6, gap=True)
         check_parity(res, ref, xs)
+
+
+def test_csr_wide_band_uses_gather_path(S, orc):
+    """Half bandwidth 6000 exceeds the window SpMV's ring: the gather SpMV runs;
+    results identical to the oracle either way."""
+    P = problems.csr_band(30000, nnz_row=27, band=6000, seed=2)
+    solver = S.csr(P.n, P.row_ptr, P.col, P.val)
+    A = orc.csr(P.row_ptr, P.col, P.val)
+    xs = problems.x_star(P.n, 0)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    res = solver.solve(b_d, tol=1e-12, maxit=100, rr_period=4)
+    ref = orc.pbicgstab(A, b, tol=1e-12, maxit=100, rr_period=4)
+    check_parity(res, ref, xs)
