@@ -1,0 +1,64 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times
+(TMA tile sweeps / window SpMV, CUDA graphs, bench mode), against the oracle run
+on the same full-size inputs for the first iterations (the GPU box has the RAM
+for the 512^3 oracle: ~35 GB for a few iterations).
+"""
+import numpy as np
+import pytest
+
+from paper_1809_01948_b200 import problems
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _compare(res, ref, xs):
+    assert res.iters == ref.iters and res.outcome == ref.outcome
+    k = min(30, ref.iters)
+    rel = np.abs(res.rnorm[:k + 1] - ref.rnorm[:k + 1]) / ref.rnorm[:k + 1]
+    assert rel.max() <= 1e-9, rel.max()
+    x = res.x.cpu().numpy()
+    e = np.linalg.norm(x - xs) / np.linalg.norm(xs)
+    e0 = np.linalg.norm(ref.x - xs) / np.linalg.norm(xs)
+    assert e <= 10 * e0 + 1e-15
+    # design target: bitwise
+    assert np.array_equal(res.rnorm, ref.rnorm)
+    assert np.array_equal(x, ref.x)
+    if res.gap is not None:
+        assert np.array_equal(res.gap, ref.gap)
+
+
+def test_cfg4_full_size_first_iterations(orc):
+    from paper_1809_01948_b200 import Solver
+    st = problems.configs()["cfg4"].stencil
+    S = Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef)
+    xs = problems.x_star(st.n, 0)
+    b_d = S.apply(torch.from_numpy(xs).cuda())
+    S.set_option("bench", 1)
+    # 4 iterations, replacement at i = 1 and 3 (rr_period 2), gap tracking on
+    res = S.solve(b_d, tol=0.0, maxit=4, rr_period=2, gap=True)
+    A = orc.stencil_csr(st.dim, st.nx, st.ny, st.nz, st.coef)
+    b = orc.spmv(A, xs)
+    assert np.array_equal(b_d.cpu().numpy(), b)  # SpMV, 134M rows, bitwise
+    del b_d
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=4, rr_period=2, bench=True)
+    _compare(res, ref, xs)
+    assert res.gap[0] == 0.0 and res.gap[2] == 0.0 and res.gap[4] == 0.0
+
+
+def test_cfg5_full_size_solve(orc):
+    """cfg5 (CSR band N = 2^23, 27 nnz/row): the normal-mode solve to 1e-10
+    (converges in ~8 iterations, so the period-100 replacement never fires)."""
+    from paper_1809_01948_b200 import Solver
+    cfg = problems.configs()["cfg5"]
+    M = problems.csr_band(cfg.csr_n, nnz_row=27, band=4096, seed=1)
+    S = Solver.csr(M.n, M.row_ptr, M.col, M.val)
+    xs = problems.x_star(M.n, 0)
+    b_d = S.apply(torch.from_numpy(xs).cuda())
+    res = S.solve(b_d, tol=cfg.tol, maxit=cfg.maxit, rr_period=cfg.rr_period, gap=True)
+    A = orc.csr(M.row_ptr, M.col, M.val)
+    b = orc.spmv(A, xs)
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    ref = orc.pbicgstab(A, b, tol=cfg.tol, maxit=cfg.maxit, rr_period=cfg.rr_period)
+    assert ref.outcome == "converged"
+    _compare(res, ref, xs)
