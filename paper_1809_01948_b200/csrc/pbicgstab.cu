@@ -64,7 +64,8 @@ struct pbicg_ctx {
   bool tile_ok = false;  // TMA 2.5D sweeps eligible for this operator
   bool tile_vec = false; // ... with 16-byte aligned pairs (nx even)
   int tile_on = 1;       // option "tile"
-  size_t tile_smem[2] = {0, 0};
+  size_t tile_smem[TM_N] = {0};
+  int tile_occ[TM_N] = {0};  // resident CTAs per SM of each tile kernel
   CsrOp csr{};
   WinGeo wg{};
   bool win_ok = false;  // banded CSR: window SpMV (c_spmv_win) eligible
@@ -223,55 +224,60 @@ Members members(pbicg_ctx* h) {
 // Kernel launches (one rank)
 enum Phase { PH_INIT1, PH_INIT2, PH_SWEEPA, PH_SPMVB, PH_SWEEPC, PH_RR1, PH_RR2, PH_SPMVD, PH_GAP };
 
+template <int DIM, int MODE>
+void launch_tile(pbicg_ctx* h) {
+  const int per_sm = h->tile_occ[MODE] > 0 ? h->tile_occ[MODE] : 1;
+  const int cap = h->num_sm * per_sm;
+  const int grid = h->tg.units < cap ? h->tg.units : cap;
+  if (h->tile_vec)
+    t_tile<DIM, MODE, true><<<grid, TNT, h->tile_smem[MODE], h->stream>>>(h->tg, h->V, h->scal,
+                                                                          h->part, h->hist);
+  else
+    t_tile<DIM, MODE, false><<<grid, TNT, h->tile_smem[MODE], h->stream>>>(h->tg, h->V, h->scal,
+                                                                           h->part, h->hist);
+}
+
 template <int DIM>
 void launch_stencil(pbicg_ctx* h, Phase p) {
   const Geo& g = h->geo;
   const bool tile = h->tile_ok && h->tile_on;
-  const int tgrid = h->tg.units < h->num_sm ? h->tg.units : h->num_sm;
   switch (p) {
     case PH_INIT1: {
       LaunchScope ls(h, K_INIT);
-      k_init1<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+      if (tile) launch_tile<DIM, TM_INIT1>(h);
+      else k_init1<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_INIT2: {
       LaunchScope ls(h, K_INIT);
-      k_init2<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+      if (tile) launch_tile<DIM, TM_INIT2>(h);
+      else k_init2<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SWEEPA: {
       LaunchScope ls(h, K_SWEEPA);
-      if (tile && h->tile_vec)
-        t_sweep<DIM, 0, true><<<tgrid, TNT, h->tile_smem[0], h->stream>>>(h->tg, h->V, h->scal,
-                                                                          h->part, h->hist);
-      else if (tile)
-        t_sweep<DIM, 0, false><<<tgrid, TNT, h->tile_smem[0], h->stream>>>(h->tg, h->V, h->scal,
-                                                                           h->part, h->hist);
-      else
-        k_sweepA<DIM><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
-                                                                       h->hist);
+      if (tile) launch_tile<DIM, TM_A>(h);
+      else k_sweepA<DIM><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
+                                                                          h->hist);
     } break;
     case PH_SWEEPC: {
       LaunchScope ls(h, K_SWEEPC);
-      if (tile && h->tile_vec)
-        t_sweep<DIM, 1, true><<<tgrid, TNT, h->tile_smem[1], h->stream>>>(h->tg, h->V, h->scal,
-                                                                          h->part, h->hist);
-      else if (tile)
-        t_sweep<DIM, 1, false><<<tgrid, TNT, h->tile_smem[1], h->stream>>>(h->tg, h->V, h->scal,
-                                                                           h->part, h->hist);
-      else
-        k_sweepC<DIM><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
-                                                                       h->hist);
+      if (tile) launch_tile<DIM, TM_C>(h);
+      else k_sweepC<DIM><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
+                                                                          h->hist);
     } break;
     case PH_RR1: {
       LaunchScope ls(h, K_RR1);
-      k_rr1<DIM><<<h->grid[K_RR1], h->block, 0, h->stream>>>(g, h->V, h->scal);
+      if (tile) launch_tile<DIM, TM_RR1>(h);
+      else k_rr1<DIM><<<h->grid[K_RR1], h->block, 0, h->stream>>>(g, h->V, h->scal);
     } break;
     case PH_RR2: {
       LaunchScope ls(h, K_RR2);
-      k_rr2<DIM><<<h->grid[K_RR2], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+      if (tile) launch_tile<DIM, TM_RR2>(h);
+      else k_rr2<DIM><<<h->grid[K_RR2], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_GAP: {
       LaunchScope ls(h, K_GAP);
-      k_gap<DIM><<<h->grid[K_GAP], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+      if (tile) launch_tile<DIM, TM_GAP>(h);
+      else k_gap<DIM><<<h->grid[K_GAP], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     default:
       break;
@@ -571,6 +577,33 @@ pbicg_status ensure_hist(pbicg_ctx* h, int64_t need) {
   return PBICG_OK;
 }
 
+template <int DIM, int MODE>
+cudaError_t set_tile_attr(pbicg_ctx* h) {
+  const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  cudaError_t e = cudaFuncSetAttribute(t_tile<DIM, MODE, true>, A, (int)h->tile_smem[MODE]);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(t_tile<DIM, MODE, false>, A, (int)h->tile_smem[MODE]);
+  // light modes (few streams) fit 2 CTAs per SM: twice the bytes in flight
+  int occ = 1;
+  if (e == cudaSuccess)
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, t_tile<DIM, MODE, true>, TNT,
+                                                  h->tile_smem[MODE]);
+  h->tile_occ[MODE] = occ < 1 ? 1 : occ;
+  return e;
+}
+
+template <int DIM>
+cudaError_t set_tile_attrs(pbicg_ctx* h) {
+  cudaError_t e = set_tile_attr<DIM, TM_A>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_C>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_RR1>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_RR2>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_GAP>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_INIT1>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_INIT2>(h);
+  return e;
+}
+
 // Tile geometry of the TMA 2.5D sweeps (tile_sweeps.cuh): TY full x-lines per
 // tile (3D) or one x-line (2D), a chunk of planes per work unit, units spread
 // statically over one CTA per SM (deterministic accumulation order).
@@ -601,9 +634,9 @@ void setup_tile(pbicg_ctx* h) {
     const int64_t TP = TY * g.nx;
     t.st_stride = (int32_t)((TP + 2 + 1) & ~1LL);
     t.sv_stride = (int32_t)((TP + 2 * t.halo + 2 + 1) & ~1LL);
-    if (tile_smem_bytes(t, 1) + reserve <= (size_t)max_smem &&
-        tile_smem_bytes(t, 0) + reserve <= (size_t)max_smem)
-      break;
+    size_t worst = 0;
+    for (int m = 0; m < TM_N; ++m) worst = tile_smem_bytes(t, m) > worst ? tile_smem_bytes(t, m) : worst;
+    if (worst + reserve <= (size_t)max_smem) break;
   }
   if (TY < 1) return;
   for (int i = 0; i < 7; ++i) t.c[i] = g.c[i];
@@ -628,22 +661,8 @@ void setup_tile(pbicg_ctx* h) {
   t.chunk = (int32_t)((g.nol + best_n - 1) / best_n);
   t.nchunks = (int32_t)((g.nol + t.chunk - 1) / t.chunk);
   t.units = t.nchunks * t.ncols;
-  h->tile_smem[0] = tile_smem_bytes(t, 0);
-  h->tile_smem[1] = tile_smem_bytes(t, 1);
-  const int a0 = (int)h->tile_smem[0], a1 = (int)h->tile_smem[1];
-  const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  cudaError_t e = cudaSuccess;
-  if (dim == 3) {
-    e = (cudaError_t)(cudaFuncSetAttribute(t_sweep<3, 0, true>, A, a0) |
-                      cudaFuncSetAttribute(t_sweep<3, 1, true>, A, a1) |
-                      cudaFuncSetAttribute(t_sweep<3, 0, false>, A, a0) |
-                      cudaFuncSetAttribute(t_sweep<3, 1, false>, A, a1));
-  } else {
-    e = (cudaError_t)(cudaFuncSetAttribute(t_sweep<2, 0, true>, A, a0) |
-                      cudaFuncSetAttribute(t_sweep<2, 1, true>, A, a1) |
-                      cudaFuncSetAttribute(t_sweep<2, 0, false>, A, a0) |
-                      cudaFuncSetAttribute(t_sweep<2, 1, false>, A, a1));
-  }
+  for (int m = 0; m < TM_N; ++m) h->tile_smem[m] = tile_smem_bytes(t, m);
+  const cudaError_t e = dim == 3 ? set_tile_attrs<3>(h) : set_tile_attrs<2>(h);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return;

@@ -1,29 +1,45 @@
-// tile_sweeps.cuh -- the two fused sweeps of the stencil schedule as
-// TMA-staged 2.5D z-marching kernels (the hot path on B200).
+// tile_sweeps.cuh -- every step of the stencil path as a TMA-staged 2.5D
+// z-marching kernel (the hot path on B200).
 //
-// Same arithmetic, same operation order as k_sweepA / k_sweepC
-// (stencil_kernels.cuh) -- only the data movement differs:
+// Same arithmetic, same operation order as the line kernels of
+// stencil_kernels.cuh -- only the data movement differs:
 //   * a CTA owns a tile of TY full x-lines of a plane (3D) or one x-line (2D)
 //     and marches the outer dimension (z in 3D, y in 2D) over a chunk of planes;
 //   * one elected thread streams every vector the step needs into shared memory
 //     with cp.async.bulk (TMA bulk copies) one plane ahead, completion tracked by
 //     mbarriers, so ~100 KB per SM is in flight while the CTA computes;
-//   * the stencil operands w and z (z_{i-1} in sweepA) are staged as planes with
-//     one halo line on each side (a 3-slot ring: z, z+1 resident, z+2 in flight);
-//     the -z leg comes from registers (the previous step's centre values);
+//   * the stencil operands (w and z in the sweeps; x, g / r, s in the
+//     replacement; x or r in init and gap) are staged as planes with one halo
+//     line on each side (a 3-slot ring: z, z+1 resident, z+2 in flight); the -z
+//     leg comes from registers (the previous step's centre values);
 //   * one row pair per thread; 16-byte shared loads / global streaming stores
-//     when nx is even; a warp-uniform interior path drops the boundary selects;
-//   * outputs are written with streaming stores.
+//     when nx is even; a warp-uniform interior path drops the boundary selects.
 // Per row the kernels touch DRAM exactly once per vector (tile halos hit L2).
+//
+// Modes (Alg. 2 lines):
+//   TM_A    sweep A, lines 5-12          TM_C    sweep C, lines 16-21
+//   TM_RR1  eq:rr r, k, s, l TM_RR2  eq:rr w, z + line-21 dots
+//   TM_GAP  eq:res_gap           TM_INIT1 / TM_INIT2  lines 2-3
 #pragma once
 #include "dd.cuh"
 #include "state.cuh"
 #include "stencil_kernels.cuh"
 #include "tma.cuh"
 
-#define TNT 512      // threads per CTA
-#define TNSTR_A 6    // sweepA streams: k, g, l, s, r (+ replaced z_{i-1})
-#define TNSTR_C 7    // sweepC streams: x, g, k, l, r, s, r^
+#define TNT 512  // threads per CTA
+
+enum TileMode { TM_A = 0, TM_C, TM_RR1, TM_RR2, TM_GAP, TM_INIT1, TM_INIT2, TM_N };
+
+// per mode: stencil operands, whether they enter as A M^-1 v (PREC) or A v,
+// the maximum number of streamed vectors, outputs, dot products
+template <int M> struct TileTraits;
+template <> struct TileTraits<TM_A> { enum { NSV = 2, PREC = 1, NSTR = 6, NOUT = 4, K = 2 }; };
+template <> struct TileTraits<TM_C> { enum { NSV = 2, PREC = 1, NSTR = 7, NOUT = 4, K = 5 }; };
+template <> struct TileTraits<TM_RR1> { enum { NSV = 2, PREC = 0, NSTR = 1, NOUT = 4, K = 0 }; };
+template <> struct TileTraits<TM_RR2> { enum { NSV = 2, PREC = 1, NSTR = 1, NOUT = 2, K = 5 }; };
+template <> struct TileTraits<TM_GAP> { enum { NSV = 1, PREC = 0, NSTR = 2, NOUT = 0, K = 1 }; };
+template <> struct TileTraits<TM_INIT1> { enum { NSV = 1, PREC = 0, NSTR = 1, NOUT = 3, K = 2 }; };
+template <> struct TileTraits<TM_INIT2> { enum { NSV = 1, PREC = 1, NSTR = 1, NOUT = 1, K = 1 }; };
 
 struct TileGeo {
   int64_t nx, ny;     // x extent; lines per plane (3D: ny, 2D: 1)
@@ -41,7 +57,7 @@ __device__ __forceinline__ int align_off(const double* p) {
   return (int)(((uintptr_t)p & 15u) >> 3);
 }
 
-// stage `n` vectors' element range [e0, e0 + len) of plane p into dst slots
+// stage `n` vectors' element range [e0, e0 + len) into dst slots
 __device__ __forceinline__ void stage(double* dst, int stride, const double* const* src, int n,
                                       int64_t e0, int len, uint64_t* bar) {
   const double* s0 = src[0] + e0;
@@ -81,20 +97,26 @@ __device__ __forceinline__ double leg(unsigned b, unsigned bit, double acc, doub
   return (INTERIOR || (b & bit)) ? acc + term : acc;
 }
 
-// fl(A M^-1 v) for the row pair (r, r+1) of plane z.  W points at row r of
-// plane z in shared memory, W1 at row r of plane z+1; m0/m1 are the plane z-1
-// centre values.  Legs in ascending column order (A5); every leg is
-// fl(c * fl(dinv * v)) added left to right from +0.0, exactly as the oracle's
-// "n := M^-1 z; v := A n".  Products fl(dinv * v) shared by the two rows are
-// formed once (same values).  bnd bits: 1 zm, 2 ym, 4 xm, 8 xp, 16 yp, 32 zp.
-template <int DIM, bool VEC, bool INTERIOR>
+template <bool PREC>
+__device__ __forceinline__ double pre(double d, double v) {
+  return PREC ? d * v : v;
+}
+
+// fl(A M^-1 v) (PREC) or fl(A v) for the row pair (r, r+1) of plane z.  W points
+// at row r of plane z in shared memory, W1 at row r of plane z+1; m0/m1 are the
+// plane z-1 centre values.  Legs in ascending column order (A5), added left to
+// right from +0.0; with PREC every leg is fl(c * fl(dinv * v)), exactly the
+// oracle's "n := M^-1 z; v := A n".  Products shared by the two rows are formed
+// once (same values).  bnd bits: 1 zm, 2 ym, 4 xm, 8 xp, 16 yp, 32 zp.
+template <int DIM, bool VEC, bool INTERIOR, bool PREC>
 __device__ __forceinline__ void stencil_pair(const TileGeo& g, int nx, const double* W,
                                              const double* W1, double zm0, double zm1,
                                              unsigned b0, unsigned b1, double& c0, double& c1,
                                              double& t0, double& t1) {
   const double d = g.dinv;
   ld2<VEC>(W, c0, c1);
-  const double pm = d * W[-1], p0 = d * c0, p1 = d * c1, p2 = d * W[2];
+  const double pm = pre<PREC>(d, W[-1]), p0 = pre<PREC>(d, c0), p1 = pre<PREC>(d, c1);
+  const double p2 = pre<PREC>(d, W[2]);
   double ym0 = 0.0, ym1 = 0.0, yp0 = 0.0, yp1 = 0.0, zp0, zp1;
   if (DIM == 3) {
     ld2<VEC>(W - nx, ym0, ym1);
@@ -103,73 +125,111 @@ __device__ __forceinline__ void stencil_pair(const TileGeo& g, int nx, const dou
   ld2<VEC>(W1, zp0, zp1);
   const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
   double a = 0.0;
-  a = leg<INTERIOR>(b0, 1u, a, czm * (d * zm0));
-  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * (d * ym0));
+  a = leg<INTERIOR>(b0, 1u, a, czm * pre<PREC>(d, zm0));
+  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * pre<PREC>(d, ym0));
   a = leg<INTERIOR>(b0, 4u, a, g.c[1] * pm);
   a = a + g.c[0] * p0;
   a = leg<INTERIOR>(b0, 8u, a, g.c[2] * p1);
-  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * (d * yp0));
-  a = leg<INTERIOR>(b0, 32u, a, czp * (d * zp0));
+  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * pre<PREC>(d, yp0));
+  a = leg<INTERIOR>(b0, 32u, a, czp * pre<PREC>(d, zp0));
   t0 = a;
   a = 0.0;
-  a = leg<INTERIOR>(b1, 1u, a, czm * (d * zm1));
-  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * (d * ym1));
+  a = leg<INTERIOR>(b1, 1u, a, czm * pre<PREC>(d, zm1));
+  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * pre<PREC>(d, ym1));
   a = leg<INTERIOR>(b1, 4u, a, g.c[1] * p0);
   a = a + g.c[0] * p1;
   a = leg<INTERIOR>(b1, 8u, a, g.c[2] * p2);
-  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * (d * yp1));
-  a = leg<INTERIOR>(b1, 32u, a, czp * (d * zp1));
+  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * pre<PREC>(d, yp1));
+  a = leg<INTERIOR>(b1, 32u, a, czp * pre<PREC>(d, zp1));
   t1 = a;
 }
 
-// Lines 5-12 (MODE 0) or 17-21 (MODE 1) for one row, given t = A M^-1 w and
-// v = A M^-1 z at that row.  S = stream slot (row already applied), st = stride.
+// Per-row arithmetic of each mode.  S = stream slot at this row, st = stride;
+// c0/c1 = the stencil operands' centre values, t0/t1 = their stencil products.
 template <int MODE, int K>
-__device__ __forceinline__ void row_update(const double* S, int st, bool rr, double wc, double zc,
-                                           double t, double v, double al, double be, double om,
-                                           double dinv, Dd (&acc)[K], double (&o)[4]) {
-  if (MODE == 0) {
+__device__ __forceinline__ void row_update(const double* S, int st, bool rr, double c0, double c1,
+                                           double t0, double t1, double al, double be, double om,
+                                           double dinv, Dd* acc, double* o) {
+  if (MODE == TM_A) {  // c0 = w_i, c1 = z_{i-1}; t0 = t_i, t1 = v_{i-1}
     const double kj = S[0], gj = S[st], lj = S[2 * st], sj = S[3 * st], rj = S[4 * st];
-    const double zoc = rr ? S[5 * st] : zc;    // replaced z_{i-1} (A26)
-    const double m = dinv * wc;                // m_i
-    const double nn = dinv * zc;               // n_{i-1}
+    const double zoc = rr ? S[5 * st] : c1;    // replaced z_{i-1} (A26)
+    const double m = dinv * c0;                // m_i
+    const double nn = dinv * c1;               // n_{i-1}
     o[0] = kj + be * (gj - om * lj);           // line 5: g
-    o[1] = wc + be * (sj - om * zoc);          // line 6: s
+    o[1] = c0 + be * (sj - om * zoc);          // line 6: s
     o[2] = m + be * (lj - om * nn);            // line 7: l
-    o[3] = t + be * (zoc - om * v);            // line 8: z
+    o[3] = t0 + be * (zoc - om * t1);          // line 8: z
     const double qq = rj - al * o[1];          // line 9
-    const double yy = wc - al * o[3];          // line 11
+    const double yy = c0 - al * o[3];          // line 11
     dd_fma(acc[0], qq, yy);                    // line 12
     dd_fma(acc[1 % K], yy, yy);
-  } else {
+  } else if (MODE == TM_C) {  // c0 = w_i, c1 = z_i; t0 = t_i, t1 = v_i
     const double xj = S[0], gj = S[st], kj = S[2 * st], lj = S[3 * st], rj = S[4 * st];
     const double sj = S[5 * st], rhj = S[6 * st];
-    const double m = dinv * wc;                // m_i
-    const double nn = dinv * zc;               // n_i (line 13)
+    const double m = dinv * c0;                // m_i
+    const double nn = dinv * c1;               // n_i (line 13)
     const double uu = kj - al * lj;            // line 10
     const double qq = rj - al * sj;            // line 9
-    const double yy = wc - al * zc;            // line 11
+    const double yy = c0 - al * c1;            // line 11
     o[0] = (xj + al * gj) + om * uu;           // line 17: x
     o[1] = qq - om * yy;                       // line 18: r
     o[2] = uu - om * (m - al * nn);            // line 19: k
-    o[3] = yy - om * (t - al * v);             // line 20: w
+    o[3] = yy - om * (t0 - al * t1);           // line 20: w
     dd_fma(acc[0], rhj, o[1]);                 // line 21
     dd_fma(acc[1 % K], rhj, o[3]);
     dd_fma(acc[2 % K], rhj, sj);
-    dd_fma(acc[3 % K], rhj, zc);
+    dd_fma(acc[3 % K], rhj, c1);
     dd_fma(acc[4 % K], o[1], o[1]);
+  } else if (MODE == TM_RR1) {  // c = x, g; t0 = A x, t1 = A g
+    const double rj = S[0] - t0;               // r := b - A x
+    o[0] = rj;
+    o[1] = dinv * rj;                          // k := M^-1 r
+    o[2] = t1;                                 // s := A g
+    o[3] = dinv * t1;                          // l := M^-1 s
+  } else if (MODE == TM_RR2) {  // c = r, s; t0 = A M^-1 r = A k, t1 = A M^-1 s = A l
+    const double rhj = S[0];
+    o[0] = t0;                                 // w := A k
+    o[1] = t1;                                 // z := A l
+    dd_fma(acc[0], rhj, c0);                   // line 21 on the replaced vectors
+    dd_fma(acc[1 % K], rhj, t0);
+    dd_fma(acc[2 % K], rhj, c1);
+    dd_fma(acc[3 % K], rhj, t1);
+    dd_fma(acc[4 % K], c0, c0);
+  } else if (MODE == TM_GAP) {  // c = x; t0 = A x
+    const double dg = (S[0] - t0) - S[st];     // (b - A x) - r
+    dd_fma(acc[0], dg, dg);
+  } else if (MODE == TM_INIT1) {  // c = x0; t0 = A x0
+    const double bj = S[0];
+    const double rj = bj - t0;                 // r0 := b - A x0
+    o[0] = rj;
+    o[1] = rj;                                 // r^ := r0 (A2)
+    o[2] = dinv * rj;                          // k0 := M^-1 r0
+    dd_fma(acc[0], rj, rj);
+    dd_fma(acc[1 % K], bj, bj);
+  } else if (MODE == TM_INIT2) {  // c = r0; t0 = A M^-1 r0 = A k0
+    o[0] = t0;                                 // w0
+    dd_fma(acc[0], S[0], t0);                  // (r^, w0)
   }
 }
 
-// MODE 0 = sweepA (lines 5-12), MODE 1 = sweepC (lines 17-21).  VEC: every
-// staged range and every vector is 16-byte aligned (nx even) -> paired loads
-// and stores.  One row pair per thread: TP <= 2 * TNT.
+// Generic tile kernel.  VEC: every staged range and every vector is 16-byte
+// aligned (nx even) -> paired loads and stores.  One row pair per thread:
+// TP <= 2 * TNT.
 template <int DIM, int MODE, bool VEC>
-__global__ void __launch_bounds__(TNT, 1) t_sweep(TileGeo g, Vecs V, Scal* __restrict__ sc,
-                                                  Dd* __restrict__ part, Hist h) {
-  constexpr int NSTR_MAX = MODE == 0 ? TNSTR_A : TNSTR_C;
-  constexpr int K = MODE == 0 ? 2 : 5;
-  if (sc->done) return;
+__global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
+                                                 Dd* __restrict__ part, Hist h) {
+  using T = TileTraits<MODE>;
+  constexpr int NSV = T::NSV, NSTR_MAX = T::NSTR;
+  constexpr int NOUT = T::NOUT > 0 ? T::NOUT : 1;
+  constexpr int K = T::K > 0 ? T::K : 1;
+  constexpr bool PREC = T::PREC != 0;
+  if (MODE == TM_A || MODE == TM_C) {
+    if (sc->done) return;
+  } else if (MODE == TM_RR1 || MODE == TM_RR2) {
+    if (sc->done || !sc->rr_fire) return;
+  } else if (MODE == TM_GAP) {
+    if (sc->gap_iter >= sc->iter) return;
+  }
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);  // [0,1] streams, [2..4] stencil
   double* st = reinterpret_cast<double*>(smem_raw + 64);
@@ -180,27 +240,48 @@ __global__ void __launch_bounds__(TNT, 1) t_sweep(TileGeo g, Vecs V, Scal* __res
 
   const int it = sc->iter;
   const double al = sc->alpha, be = sc->beta, om = sc->omega;
-  const bool rr = MODE == 0 && sc->use_rr != 0;
-  const double* svp[2];
+  const bool rr = MODE == TM_A && sc->use_rr != 0;
+  const double* svp[2] = {nullptr, nullptr};
   const double* stp[NSTR_MAX];
-  int nstr;
-  double* outp[4];
-  if (MODE == 0) {
+  int nstr = NSTR_MAX;
+  double* outp[NOUT];
+  if (MODE == TM_A) {
     svp[0] = (it & 1) ? V.w1 : V.w0;                 // w_i
     svp[1] = (it & 1) ? V.z0 : V.z1;                 // z_{i-1} pre-replacement
-    stp[0] = V.k; stp[1] = V.g; stp[2] = V.l; stp[3] = V.s; stp[4] = V.r;
+    stp[0] = V.k; stp[1 % NSTR_MAX] = V.g; stp[2 % NSTR_MAX] = V.l; stp[3 % NSTR_MAX] = V.s;
+    stp[4 % NSTR_MAX] = V.r;
     stp[NSTR_MAX - 1] = V.zrr;                       // z_{i-1} replaced (A26)
     nstr = rr ? 6 : 5;
-    outp[0] = V.g; outp[1] = V.s; outp[2] = V.l;
-    outp[3] = (it & 1) ? V.z1 : V.z0;                // z_i
-  } else {
+    outp[0] = V.g; outp[1 % NOUT] = V.s; outp[2 % NOUT] = V.l;
+    outp[3 % NOUT] = (it & 1) ? V.z1 : V.z0;         // z_i
+  } else if (MODE == TM_C) {
     svp[0] = (it & 1) ? V.w1 : V.w0;                 // w_i
     svp[1] = (it & 1) ? V.z1 : V.z0;                 // z_i
-    stp[0] = V.x; stp[1] = V.g; stp[2] = V.k; stp[3] = V.l; stp[4] = V.r; stp[5] = V.s;
+    stp[0] = V.x; stp[1 % NSTR_MAX] = V.g; stp[2 % NSTR_MAX] = V.k; stp[3 % NSTR_MAX] = V.l;
+    stp[4 % NSTR_MAX] = V.r; stp[5 % NSTR_MAX] = V.s;
     stp[NSTR_MAX - 1] = V.rh;
-    nstr = 7;
-    outp[0] = V.x; outp[1] = V.r; outp[2] = V.k;
-    outp[3] = (it & 1) ? V.w0 : V.w1;                // w_{i+1}
+    outp[0] = V.x; outp[1 % NOUT] = V.r; outp[2 % NOUT] = V.k;
+    outp[3 % NOUT] = (it & 1) ? V.w0 : V.w1;         // w_{i+1}
+  } else if (MODE == TM_RR1) {
+    svp[0] = V.x; svp[1] = V.g;
+    stp[0] = V.b;
+    outp[0] = V.r; outp[1 % NOUT] = V.k; outp[2 % NOUT] = V.s; outp[3 % NOUT] = V.l;
+  } else if (MODE == TM_RR2) {
+    svp[0] = V.r; svp[1] = V.s;
+    stp[0] = V.rh;
+    outp[0] = (it & 1) ? V.w0 : V.w1;                // w_{i+1}
+    outp[1 % NOUT] = V.zrr;                          // replaced z_i (A26)
+  } else if (MODE == TM_GAP) {
+    svp[0] = V.x;
+    stp[0] = V.b; stp[1 % NSTR_MAX] = V.r;
+  } else if (MODE == TM_INIT1) {
+    svp[0] = V.x;
+    stp[0] = V.b;
+    outp[0] = V.r; outp[1 % NOUT] = V.rh; outp[2 % NOUT] = V.k;
+  } else {  // TM_INIT2
+    svp[0] = V.r;
+    stp[0] = V.rh;
+    outp[0] = V.w0;
   }
   if (tid == 0) {
     for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
@@ -243,11 +324,11 @@ __global__ void __launch_bounds__(TNT, 1) t_sweep(TileGeo g, Vecs V, Scal* __res
     const unsigned xy_all = DIM == 3 ? 30u : 12u;
     const bool xy_int = __all_sync(0xffffffffu, !act || ((b0 & xy_all) == xy_all &&
                                                          (b1 & xy_all) == xy_all));
-    double mw0 = 0.0, mw1 = 0.0, mz0 = 0.0, mz1 = 0.0;  // plane z-1 centre values
+    double m1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // plane z-1 centre values per operand
     if (tid == 0) {
       for (int m = 0; m < 3 && m < nsv; ++m) {
         const int s = (svc + m) % 3;
-        stage(sv + (size_t)s * 2 * svs, svs, svp, 2, (z0 - 1 + m) * g.pxy + toff - g.halo,
+        stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, (z0 - 1 + m) * g.pxy + toff - g.halo,
               TP + 2 * g.halo, &bar[2 + s]);
       }
       const int s = stc % 2;
@@ -257,11 +338,11 @@ __global__ void __launch_bounds__(TNT, 1) t_sweep(TileGeo g, Vecs V, Scal* __res
       const int s = svc % 3;
       mbar_wait(&bar[2 + s], (ph >> (2 + s)) & 1u);
       ph ^= 1u << (2 + s);
-      const double* b0p = sv + (size_t)s * 2 * svs +
+      const double* b0p = sv + (size_t)s * NSV * svs +
                           align_off(svp[0] + (z0 - 1) * g.pxy + toff - g.halo) + g.halo + r;
       if (act) {
-        ld2<VEC>(b0p, mw0, mw1);
-        ld2<VEC>(b0p + svs, mz0, mz1);
+#pragma unroll
+        for (int v = 0; v < NSV; ++v) ld2<VEC>(b0p + v * svs, m1[v][0], m1[v][1]);
       }
       const int s1 = (svc + 1) % 3;  // plane z0
       mbar_wait(&bar[2 + s1], (ph >> (2 + s1)) & 1u);
@@ -273,7 +354,7 @@ __global__ void __launch_bounds__(TNT, 1) t_sweep(TileGeo g, Vecs V, Scal* __res
       if (tid == 0) {
         if (n + 3 < nsv) {  // plane z+2
           const int s = (svc + n + 3) % 3;
-          stage(sv + (size_t)s * 2 * svs, svs, svp, 2, (z + 2) * g.pxy + toff - g.halo,
+          stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, (z + 2) * g.pxy + toff - g.halo,
                 TP + 2 * g.halo, &bar[2 + s]);
         }
         if (n + 1 < nst) {  // streams z+1
@@ -291,51 +372,71 @@ __global__ void __launch_bounds__(TNT, 1) t_sweep(TileGeo g, Vecs V, Scal* __res
       const int oz = align_off(svp[0] + z * g.pxy + toff - g.halo) + g.halo;
       const int oz1 = align_off(svp[0] + (z + 1) * g.pxy + toff - g.halo) + g.halo;
       const int os = align_off(stp[0] + z * g.pxy + toff);
-      const double* Wz = sv + (size_t)s_z * 2 * svs + oz + r;
-      const double* Wz1 = sv + (size_t)s_z1 * 2 * svs + oz1 + r;
+      const double* Wz = sv + (size_t)s_z * NSV * svs + oz + r;
+      const double* Wz1 = sv + (size_t)s_z1 * NSV * svs + oz1 + r;
       const double* S0 = st + (size_t)s_st * NSTR_MAX * sts + os + r;
       const bool zin = (g.o0 + z) > 0 && (g.o0 + z) < g.nog - 1;
       const unsigned zb = ((g.o0 + z) > 0 ? 1u : 0u) | ((g.o0 + z) < g.nog - 1 ? 32u : 0u);
-      double wc0, wc1, zc0, zc1, t0, t1, v0, v1;
+      double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
       if (xy_int && zin) {
-        stencil_pair<DIM, VEC, true>(g, nx, Wz, Wz1, mw0, mw1, 0u, 0u, wc0, wc1, t0, t1);
-        stencil_pair<DIM, VEC, true>(g, nx, Wz + svs, Wz1 + svs, mz0, mz1, 0u, 0u, zc0, zc1, v0,
-                                     v1);
-      } else {
-        stencil_pair<DIM, VEC, false>(g, nx, Wz, Wz1, mw0, mw1, b0 | zb, b1 | zb, wc0, wc1, t0,
-                                      t1);
-        stencil_pair<DIM, VEC, false>(g, nx, Wz + svs, Wz1 + svs, mz0, mz1, b0 | zb, b1 | zb,
-                                      zc0, zc1, v0, v1);
-      }
-      mw0 = wc0;
-      mw1 = wc1;
-      mz0 = zc0;
-      mz1 = zc1;
-      double o0[4], o1[4];
-      row_update<MODE, K>(S0, sts, rr, wc0, zc0, t0, v0, al, be, om, g.dinv, acc, o0);
-      if (valid1) {
-        row_update<MODE, K>(S0 + 1, sts, rr, wc1, zc1, t1, v1, al, be, om, g.dinv, acc, o1);
-      } else {
-        o1[0] = o1[1] = o1[2] = o1[3] = 0.0;
-      }
-      const int64_t gi = z * g.pxy + toff + r;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) st2<VEC>(outp[k] + gi, o0[k], o1[k], valid1);
+        for (int v = 0; v < NSV; ++v)
+          stencil_pair<DIM, VEC, true, PREC>(g, nx, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                             m1[v][1], 0u, 0u, c[v][0], c[v][1], t[v][0], t[v][1]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < NSV; ++v)
+          stencil_pair<DIM, VEC, false, PREC>(g, nx, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                              m1[v][1], b0 | zb, b1 | zb, c[v][0], c[v][1],
+                                              t[v][0], t[v][1]);
+      }
+#pragma unroll
+      for (int v = 0; v < NSV; ++v) {
+        m1[v][0] = c[v][0];
+        m1[v][1] = c[v][1];
+      }
+      double o0[4] = {0.0, 0.0, 0.0, 0.0}, o1[4] = {0.0, 0.0, 0.0, 0.0};
+      row_update<MODE, K>(S0, sts, rr, c[0][0], c[1][0], t[0][0], t[1][0], al, be, om, g.dinv,
+                          acc, o0);
+      if (valid1)
+        row_update<MODE, K>(S0 + 1, sts, rr, c[0][1], c[1][1], t[0][1], t[1][1], al, be, om,
+                            g.dinv, acc, o1);
+      const int64_t gi = z * g.pxy + toff + r;
+      if (T::NOUT > 0) {
+#pragma unroll
+        for (int k = 0; k < NOUT; ++k) st2<VEC>(outp[k] + gi, o0[k], o1[k], valid1);
+      }
     }
     __syncthreads();  // unit done: every slot is free
     svc = (svc + nsv) % 3;
     stc = (stc + nst) % 2;
   }
-  Dd tot[K];
-  if (dd_grid_reduce<K>(acc, part, &sc->counter[MODE == 0 ? T_SWEEPA : T_SWEEPC], tot) &&
-      tid == 0) {
-    if (MODE == 0) publish<F_SWEEPA>(sc, h, tot);
-    else publish<F_SWEEPC>(sc, h, tot);
+  if (T::K > 0) {
+    Dd tot[K];
+    const int slot = MODE == TM_A ? T_SWEEPA : MODE == TM_C ? T_SWEEPC : MODE == TM_RR2 ? T_RR2
+                   : MODE == TM_GAP ? T_GAP : MODE == TM_INIT1 ? T_INIT1 : T_INIT2;
+    if (dd_grid_reduce<K>(acc, part, &sc->counter[slot], tot) && tid == 0) {
+      if (MODE == TM_A) publish<F_SWEEPA>(sc, h, tot);
+      else if (MODE == TM_C) publish<F_SWEEPC>(sc, h, tot);
+      else if (MODE == TM_RR2) publish<F_RR2>(sc, h, tot);
+      else if (MODE == TM_GAP) publish<F_GAP>(sc, h, tot);
+      else if (MODE == TM_INIT1) publish<F_INIT1>(sc, h, tot);
+      else publish<F_INIT2>(sc, h, tot);
+    }
   }
 }
 
-// host-side helper: shared-memory bytes of a t_sweep<., MODE> launch
+// host-side helper: shared-memory bytes of a t_tile<., MODE, .> launch
 inline size_t tile_smem_bytes(const TileGeo& g, int mode) {
-  const int nstr = mode == 0 ? TNSTR_A : TNSTR_C;
-  return 64 + sizeof(double) * ((size_t)2 * nstr * g.st_stride + (size_t)3 * 2 * g.sv_stride);
+  int nstr = 1, nsv = 1;
+  switch (mode) {
+    case TM_A: nstr = TileTraits<TM_A>::NSTR; nsv = TileTraits<TM_A>::NSV; break;
+    case TM_C: nstr = TileTraits<TM_C>::NSTR; nsv = TileTraits<TM_C>::NSV; break;
+    case TM_RR1: nstr = TileTraits<TM_RR1>::NSTR; nsv = TileTraits<TM_RR1>::NSV; break;
+    case TM_RR2: nstr = TileTraits<TM_RR2>::NSTR; nsv = TileTraits<TM_RR2>::NSV; break;
+    case TM_GAP: nstr = TileTraits<TM_GAP>::NSTR; nsv = TileTraits<TM_GAP>::NSV; break;
+    case TM_INIT1: nstr = TileTraits<TM_INIT1>::NSTR; nsv = TileTraits<TM_INIT1>::NSV; break;
+    default: nstr = TileTraits<TM_INIT2>::NSTR; nsv = TileTraits<TM_INIT2>::NSV; break;
+  }
+  return 64 + sizeof(double) * ((size_t)2 * nstr * g.st_stride + (size_t)3 * nsv * g.sv_stride);
 }
