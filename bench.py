@@ -256,7 +256,8 @@ def run_ours(args, rank, world):
         return float(t.item())
 
     # ---- timed region: device time with CUDA events on the solver's stream
-    S.set_option("timing", 1)  # events around every kernel (graphs off; launches are ms-long)
+    # events around every kernel (graphs off; the headline's launches are ms-long)
+    S.set_option("timing", 1 if args.kernel_timing else 0)
     S.kernel_time("all", reset=True)
     barrier()
     torch.cuda.synchronize()
@@ -275,7 +276,8 @@ def run_ours(args, rank, world):
     for k in ("sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap", "init", "apply", "fin"):
         nk, tk = S.kernel_time(k)
         if nk:
-            per_kernel[k] = {"launches": nk, "avg_ms": tk / nk, "bytes": S.kernel_bytes(k)}
+            per_kernel[k] = {"launches": nk, "avg_ms": tk / nk if args.kernel_timing else None,
+                             "bytes": S.kernel_bytes(k)}
     S.set_option("timing", 0)
 
     # ---- end to end: host (pinned) b, x0 -> solve -> host x, through the C ABI
@@ -304,9 +306,12 @@ def run_ours(args, rank, world):
     # strong scaling: every rank advances the same global iterations
     value = iters / (ms / 1000.0)
     # dominant kernel = largest share of the timed region
-    dom = max(per_kernel, key=lambda k: per_kernel[k]["avg_ms"] * per_kernel[k]["launches"])
+    if args.kernel_timing:
+        dom = max(per_kernel, key=lambda k: per_kernel[k]["avg_ms"] * per_kernel[k]["launches"])
+        k_avg_s = per_kernel[dom]["avg_ms"] / 1000.0
+    else:
+        dom, k_avg_s = "sweepC", float("nan")
     kb = per_kernel[dom]["bytes"]
-    k_avg_s = per_kernel[dom]["avg_ms"] / 1000.0
     achieved = kb / k_avg_s / 1e9
     it_bytes = S.kernel_bytes("iteration") * world  # all ranks' algorithmic bytes per iteration
     traffic = ncu_traffic(dom) if (world == 1 and cfg.name == "cfg4") else None
@@ -380,6 +385,9 @@ def main():
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--gap", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--kernel-timing", type=int, default=1,
+                    help="1: CUDA events around every kernel in the timed region (graphs off); "
+                         "0: CUDA-graph replay, no per-kernel times")
     ap.add_argument("--loopback", type=int, default=0,
                     help="emulate P ranks on one GPU (multi-rank code path check)")
     args = ap.parse_args()
