@@ -29,6 +29,11 @@ sys.path.insert(0, ROOT)
 from paper_1809_01948_b200 import problems  # noqa: E402
 
 METRIC = "p-BiCGStab fp64 iterations/s and % of HBM roofline at 1/2/4/8 B200"
+SCHEDULES = {
+    "pbicgstab": "fused 2-sweep (stencil), TMA 2.5D sweeps",
+    "bicgstab": "classic Alg. 1: 3 TMA sweeps (p,s | q,y dots | x,r), 3 reductions",
+    "pipecg": "p-CG: 1 TMA sweep, 1 reduction (Laplacian coefficients: CG needs SPD)",
+}
 UNIT = "iterations/s"
 L2_BYTES = 126 * 2 ** 20
 
@@ -128,34 +133,36 @@ def csr_matrix(cfg):
     return _CSR_CACHE[cfg.name]
 
 
-def oracle_sample(st, maxit_sample: int, nz_sample: int, cfg=None):
+def oracle_sample(st, maxit_sample: int, nz_sample: int, cfg=None, method="pbicgstab"):
     """Time the oracle (1 core) on an nx*ny*nz_sample slab of the workload
     (CSR: the full matrix for maxit_sample iterations)."""
     from oracle import oracle as orc
+    solve = {"pbicgstab": orc.pbicgstab, "bicgstab": orc.bicgstab, "pipecg": orc.pipecg}[method]
     if isinstance(st, CsrShape):
         M = csr_matrix(cfg)
         A = orc.csr(M.row_ptr, M.col, M.val)
         xs = problems.x_star(A.n, 0)
         b = orc.spmv(A, xs)
         t0 = time.perf_counter()
-        orc.pbicgstab(A, b, tol=0.0, maxit=0, bench=True, gap=False)
+        solve(A, b, tol=0.0, maxit=0, bench=True, gap=False)
         t_init = time.perf_counter() - t0
         t0 = time.perf_counter()
-        r = orc.pbicgstab(A, b, tol=0.0, maxit=maxit_sample, bench=True, gap=False)
+        r = solve(A, b, tol=0.0, maxit=maxit_sample, bench=True, gap=False)
         t = time.perf_counter() - t0 - t_init
         return A.n * r.iters / t, A.n, r.iters, t
     nzs = min(nz_sample, st.nz if st.dim == 3 else st.ny)
+    coef = [2.0 * st.dim] + [-1.0] * 6 if method == "pipecg" else st.coef
     if st.dim == 3:
-        A = orc.stencil_csr(3, st.nx, st.ny, nzs, st.coef)
+        A = orc.stencil_csr(3, st.nx, st.ny, nzs, coef)
     else:
-        A = orc.stencil_csr(2, st.nx, nzs, 1, st.coef)
+        A = orc.stencil_csr(2, st.nx, nzs, 1, coef)
     xs = problems.x_star(A.n, 0)
     b = orc.spmv(A, xs)
     t0 = time.perf_counter()
-    orc.pbicgstab(A, b, tol=0.0, maxit=0, bench=True, gap=False)
+    solve(A, b, tol=0.0, maxit=0, bench=True, gap=False)
     t_init = time.perf_counter() - t0
     t0 = time.perf_counter()
-    r = orc.pbicgstab(A, b, tol=0.0, maxit=maxit_sample, rr_period=0, bench=True, gap=False)
+    r = solve(A, b, tol=0.0, maxit=maxit_sample, bench=True, gap=False)
     t = time.perf_counter() - t0 - t_init
     rows_per_s = A.n * r.iters / t
     return rows_per_s, A.n, r.iters, t
@@ -183,7 +190,7 @@ def run_reference(args, rank, world):
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * maxit / v,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": n_full,
                                             "maxit": maxit, "rr_period": rr},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -191,6 +198,14 @@ def run_reference(args, rank, world):
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def method_coef(args, st):
+    """p-CG needs an SPD operator: --method pipecg runs the same grid with the
+    pure-diffusion (Laplacian) coefficients; the other solvers use the config's."""
+    if args.method == "pipecg" and not isinstance(st, CsrShape):
+        return [2.0 * st.dim] + [-1.0] * 6
+    return st.coef
 
 
 def setup_solver(args, cfg, st, rank, world, dev, stream):
@@ -202,7 +217,7 @@ def setup_solver(args, cfg, st, rank, world, dev, stream):
         if isinstance(st, CsrShape):
             M = csr_matrix(cfg)
             return Solver.csr(st.n, M.row_ptr, M.col, M.val, stream=stream)
-        return Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef, stream=stream)
+        return Solver.stencil(st.dim, st.nx, st.ny, st.nz, method_coef(args, st), stream=stream)
     ids = [binding.nccl_unique_id(), binding.nccl_unique_id()] if rank == 0 else [None, None]
     torch.distributed.broadcast_object_list(ids, src=0)
     dist = binding.make_dist(world, rank, ids[0], ids[1])
@@ -212,7 +227,8 @@ def setup_solver(args, cfg, st, rank, world, dev, stream):
         rp = M.row_ptr[lo:hi + 1] - M.row_ptr[lo]
         sl = slice(int(M.row_ptr[lo]), int(M.row_ptr[hi]))
         return Solver.csr(st.n, rp, M.col[sl], M.val[sl], row_begin=lo, stream=stream, dist=dist)
-    return Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef, stream=stream, dist=dist)
+    return Solver.stencil(st.dim, st.nx, st.ny, st.nz, method_coef(args, st), stream=stream,
+                          dist=dist)
 
 
 def run_ours(args, rank, world):
@@ -226,6 +242,10 @@ def run_ours(args, rank, world):
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{dev}"))
     stream = torch.cuda.Stream()
     S = setup_solver(args, cfg, st, rank, world, dev, stream)
+    from paper_1809_01948_b200.binding import METHODS
+    S.set_option("method", METHODS[args.method])
+    if args.method != "pbicgstab":
+        rr = 0  # residual replacement is an Alg. 2 feature
     n = S.n_local
     xs_full = problems.x_star(st.n, seed=0)
     xs = torch.from_numpy(xs_full[S.row_begin:S.row_begin + n]).to(f"cuda:{dev}")
@@ -273,7 +293,8 @@ def run_ours(args, rank, world):
     ms = max_over_ranks(e0.elapsed_time(e1))
     launches, _ = S.kernel_time("all")
     per_kernel = {}
-    for k in ("sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap", "init", "apply", "fin"):
+    for k in ("sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap", "init", "apply", "fin",
+              "cl1", "cl2", "cl3", "pcg"):
         nk, tk = S.kernel_time(k)
         if nk:
             per_kernel[k] = {"launches": nk, "avg_ms": tk / nk if args.kernel_timing else None,
@@ -323,8 +344,9 @@ def run_ours(args, rank, world):
         "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": st.n,
                    "grid": [st.nx, st.ny, st.nz] if st.dim else "csr 27 nnz/row, band 4096",
                    "maxit_per_step": maxit, "rr_period": rr, "gap_tracking": gap,
-                   "schedule": ("fused 2-sweep (stencil), TMA 2.5D sweeps" if st.dim else
-                                "split 4-phase (CSR as ELL), reduction #1 overlapped"),
+                   "method": args.method,
+                   "schedule": SCHEDULES[args.method] if st.dim else
+                               "split 4-phase (CSR as ELL), reduction #1 overlapped",
                    "l2": "inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9),
                    "parallelism": f"z-slab x{world}" + (" (NCCL halo + rank-row all-gather)"
                                                         if world > 1 else "")},
@@ -340,10 +362,10 @@ def run_ours(args, rank, world):
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and world == 1:
-        rows_per_s, n_s, its, t = oracle_sample(st, 6 if st.dim else 3, 64, cfg)
+        rows_per_s, n_s, its, t = oracle_sample(st, 6 if st.dim else 3, 64, cfg, args.method)
         line["cpu_baseline"] = {
             "value": rows_per_s / st.n, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle p-BiCGStab (C, 1 core) on {sample_desc(st, cfg)} "
+            "sample": f"oracle {args.method} (C, 1 core) on {sample_desc(st, cfg)} "
                       f"({n_s} rows), {its} iterations in {t:.1f} s, scaled by rows to {st.n}"}
     print(json.dumps(line), flush=True)
     return 0
@@ -383,6 +405,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--method", choices=["pbicgstab", "bicgstab", "pipecg"], default="pbicgstab",
+                    help="solver: p-BiCGStab (the headline), classic BiCGStab or p-CG")
     ap.add_argument("--gap", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-timing", type=int, default=1,

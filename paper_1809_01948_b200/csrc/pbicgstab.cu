@@ -33,9 +33,12 @@ thread_local std::string g_create_err;
 constexpr int WIN_SMEM = 64 + WRS * (int)sizeof(double);
 
 enum Kname { K_INIT = 0, K_SWEEPA, K_SWEEPC, K_SPMVB, K_SPMVD, K_RR1, K_RR2, K_GAP, K_APPLY, K_FIN,
-             K_N };
-const char* kname_str[K_N] = {"init", "sweepA", "sweepC", "spmvB", "spmvD",
-                              "rr1",  "rr2",    "gap",    "apply", "fin"};
+             K_CL1, K_CL2, K_CL3, K_PC, K_N };
+const char* kname_str[K_N] = {"init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2",
+                              "gap",  "apply",  "fin",    "cl1",   "cl2",   "cl3", "pcg"};
+
+// solver selected with option "method"
+enum Method { M_PBICGSTAB = 0, M_BICGSTAB = 1, M_PIPECG = 2 };
 
 struct TimedLaunch {
   int k;
@@ -89,6 +92,7 @@ struct pbicg_ctx {
   pbicg_group* group = nullptr;
   // options
   int bench = 0, use_graphs = 1, timing = 0, overlap = 1, schedule = 0, gap_on = 0;
+  int method = M_PBICGSTAB;
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
   std::vector<TimedLaunch> pending;
   std::vector<cudaEvent_t> ev_pool;
@@ -222,7 +226,8 @@ Members members(pbicg_ctx* h) {
 
 // ---------------------------------------------------------------------------
 // Kernel launches (one rank)
-enum Phase { PH_INIT1, PH_INIT2, PH_SWEEPA, PH_SPMVB, PH_SWEEPC, PH_RR1, PH_RR2, PH_SPMVD, PH_GAP };
+enum Phase { PH_INIT1, PH_INIT2, PH_SWEEPA, PH_SPMVB, PH_SWEEPC, PH_RR1, PH_RR2, PH_SPMVD, PH_GAP,
+             PH_CL1, PH_CL2, PH_CL3, PH_PC, PH_PCI1, PH_PCI2 };
 
 template <int DIM, int MODE>
 void launch_tile(pbicg_ctx* h) {
@@ -279,6 +284,13 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
       if (tile) launch_tile<DIM, TM_GAP>(h);
       else k_gap<DIM><<<h->grid[K_GAP], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
+    // comparison solvers: TMA tile kernels only (set_option("method") checks tile_ok)
+    case PH_CL1: { LaunchScope ls(h, K_CL1); launch_tile<DIM, TM_CL1>(h); } break;
+    case PH_CL2: { LaunchScope ls(h, K_CL2); launch_tile<DIM, TM_CL2>(h); } break;
+    case PH_CL3: { LaunchScope ls(h, K_CL3); launch_tile<DIM, TM_CL3>(h); } break;
+    case PH_PC: { LaunchScope ls(h, K_PC); launch_tile<DIM, TM_PC>(h); } break;
+    case PH_PCI1: { LaunchScope ls(h, K_INIT); launch_tile<DIM, TM_PCI1>(h); } break;
+    case PH_PCI2: { LaunchScope ls(h, K_INIT); launch_tile<DIM, TM_PCI2>(h); } break;
     default:
       break;
   }
@@ -329,6 +341,8 @@ void launch_csr(pbicg_ctx* h, Phase p) {
       LaunchScope ls(h, K_GAP);
       c_gap<<<h->grid[K_GAP], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
+    default:
+      break;
   }
 }
 
@@ -347,6 +361,11 @@ void launch_fin(pbicg_ctx* h, int f) {
     case F_SWEEPC: k_fin<F_SWEEPC, 5><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
     case F_RR2: k_fin<F_RR2, 5><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
     case F_GAP: k_fin<F_GAP, 1><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_CL1: k_fin<F_CL1, 1><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_CL2: k_fin<F_CL2, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_CL3: k_fin<F_CL3, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_PINIT2: k_fin<F_PINIT2, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_PC: k_fin<F_PC, 3><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
   }
 }
 
@@ -438,11 +457,71 @@ const VecSel SZ0 = [](pbicg_ctx* h) { return h->V.z0; };
 const VecSel SZ1 = [](pbicg_ctx* h) { return h->V.z1; };
 const VecSel SNV = [](pbicg_ctx* h) { return h->V.nv; };
 const VecSel SMV = [](pbicg_ctx* h) { return h->V.mv; };
+const VecSel SK = [](pbicg_ctx* h) { return h->V.k; };
+const VecSel SL = [](pbicg_ctx* h) { return h->V.l; };
+const VecSel SZRR = [](pbicg_ctx* h) { return h->V.zrr; };
+
+// Alg. 1 (method 1) on the stencil: p_i, s_i, r_i double-buffered by parity
+// (tile_sweeps.cuh TM_CL*): r in {r, k}, p in {g, l}, s in {s, zrr}
+void enq_init_classic(const Members& G) {
+  const bool dist = G[0]->nranks > 1;
+  if (dist) comm_halo(G, {SX});
+  each(G, PH_INIT1);  // r0 := b - A x0, r^0 := r0; rho_0, ||b|| (F_INIT1, method 1)
+  reduce_fin(G, F_INIT1);
+  if (dist) comm_halo(G, {SR});
+}
+
+void enq_iter_classic(const Members& G, int par) {
+  const bool dist = G[0]->nranks > 1;
+  each(G, PH_CL1);  // l.17 (previous i) + l.4-6: p_i, s_i, (r^0, s_i)
+  if (dist) {
+    comm_reduce(G, false);
+    comm_halo(G, {par ? SL : SG, par ? SZRR : SS});  // p_i, s_i ghosts
+    each_fin(G, F_CL1);
+  }
+  each(G, PH_CL2);  // l.8-12: (q, y), (y, y) -> omega
+  reduce_fin(G, F_CL2);
+  each(G, PH_CL3);  // l.13-16: x, r; (r^0, r), ||r|| -> beta
+  reduce_fin(G, F_CL3);
+  if (dist) comm_halo(G, {par ? SR : SK});  // r_{i+1}
+}
+
+// p-CG (method 2): one kernel and one reduction per iteration
+void enq_init_pipecg(const Members& G) {
+  const bool dist = G[0]->nranks > 1;
+  if (dist) comm_halo(G, {SX});
+  each(G, PH_PCI1);  // r0, u0; ||r0||, ||b|| (F_INIT1, method 2)
+  reduce_fin(G, F_INIT1);
+  if (dist) comm_halo(G, {SR});
+  each(G, PH_PCI2);  // w0 = A u0; (r0,u0), (w0,u0) -> alpha_0
+  reduce_fin(G, F_PINIT2);
+  if (dist) comm_halo(G, {SW0});
+}
+
+void enq_iter_pipecg(const Members& G, int par) {
+  const bool dist = G[0]->nranks > 1;
+  each(G, PH_PC);
+  reduce_fin(G, F_PC);
+  if (dist) comm_halo(G, {par ? SW0 : SW1});  // w_{i+1}
+}
+
+void enq_gap(const Members& G) {
+  if (!G[0]->gap_on) return;
+  if (G[0]->nranks > 1) comm_halo(G, {SX});
+  each(G, PH_GAP);
+  reduce_fin(G, F_GAP);
+}
 
 // Alg. 2 lines 2-3 [+ gap of iteration 0]
 void enq_init(const Members& G) {
   pbicg_ctx* h0 = G[0];
   const bool dist = h0->nranks > 1;
+  if (h0->method != M_PBICGSTAB) {
+    if (h0->method == M_BICGSTAB) enq_init_classic(G);
+    else enq_init_pipecg(G);
+    enq_gap(G);
+    return;
+  }
   if (dist) comm_halo(G, {SX});
   each(G, PH_INIT1);
   reduce_fin(G, F_INIT1);
@@ -465,6 +544,12 @@ void enq_init(const Members& G) {
 void enq_iter(const Members& G, bool with_rr, int par) {
   pbicg_ctx* h0 = G[0];
   const bool dist = h0->nranks > 1;
+  if (h0->method != M_PBICGSTAB) {
+    if (h0->method == M_BICGSTAB) enq_iter_classic(G, par);
+    else enq_iter_pipecg(G, par);
+    enq_gap(G);
+    return;
+  }
   if (h0->kind == KIND_STENCIL) {
     // fused 2-sweep schedule: sweep A (l.5-12) -> omega; sweep C (l.16-21) -> beta, alpha
     each(G, PH_SWEEPA);
@@ -601,6 +686,12 @@ cudaError_t set_tile_attrs(pbicg_ctx* h) {
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_GAP>(h);
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_INIT1>(h);
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_INIT2>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_CL1>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_CL2>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_CL3>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_PC>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_PCI1>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_PCI2>(h);
   return e;
 }
 
@@ -1008,6 +1099,8 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
   if (!rnorm_hist || !iters_out || !outcome_out) return fail(h, PBICG_EINVAL, "NULL argument");
   if (maxit < 0 || rr_period < 0 || !(tol >= 0.0))
     return fail(h, PBICG_EINVAL, "maxit, rr_period and tol must be >= 0");
+  if (h->method != M_PBICGSTAB && rr_period != 0)
+    return fail(h, PBICG_EINVAL, "residual replacement is defined for p-BiCGStab only (method 0)");
   for (size_t r = 0; r < G.size(); ++r) {
     if (!io[r].b || !io[r].x0 || !io[r].x) return fail(h, PBICG_EINVAL, "NULL vector argument");
     ST(ensure_hist(G[r], (int64_t)maxit + 1));
@@ -1031,6 +1124,7 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
     s0.gap_iter = -1;
     s0.bench = m->bench;
     s0.rr_period = rr_period;
+    s0.method = m->method;
     s0.nranks = m->nranks;
     s0.rank = m->rank;
     s0.red_send = m->red_send;
@@ -1287,6 +1381,14 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
     } else if (k == "tile") {
       m->tile_on = value != 0;
       destroy_graphs(m);
+    } else if (k == "method") {
+      if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "method must be 0, 1 or 2");
+      if (value != M_PBICGSTAB && (m->kind != KIND_STENCIL || !m->tile_ok))
+        return fail(h, PBICG_EINVAL,
+                    "methods 1 (BiCGStab) and 2 (p-CG) need a stencil operator with nx <= 1024 "
+                    "(TMA tile kernels)");
+      m->method = (int)value;
+      destroy_graphs(m);
     } else if (k == "schedule") {
       if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "schedule must be 0, 1 or 2");
       if (value == 2 && m->kind == KIND_STENCIL)
@@ -1431,7 +1533,13 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
   double b = 0;
   if (h->kind == KIND_STENCIL) {
     // fused schedule: every vector read / written once per launch
-    if (n == "sweepA") b = 11 * 8 * N;       // read k,g,l,w,s,z,r; write g,s,l,z
+    if (n == "cl1") b = 6 * 8 * N;        // Alg. 1: read r,p,s,r^; write p,s
+    else if (n == "cl2") b = 2 * 8 * N;   // read r,s
+    else if (n == "cl3") b = 7 * 8 * N;   // read r,s,x,p,r^; write x,r
+    else if (n == "pcg") b = 16 * 8 * N;  // p-CG: read w,z,q,s,p,x,r,u; write the same 8
+    else if (n == "iteration" && h->method == M_BICGSTAB) b = 15 * 8 * N;
+    else if (n == "iteration" && h->method == M_PIPECG) b = 16 * 8 * N;
+    else if (n == "sweepA") b = 11 * 8 * N;  // read k,g,l,w,s,z,r; write g,s,l,z
     else if (n == "sweepC") b = 13 * 8 * N;  // read x,g,k,l,r,s,w,z,r^; write x,r,k,w
     else if (n == "rr1") b = 7 * 8 * N;      // read x,b,g; write r,k,s,l
     else if (n == "rr2") b = 5 * 8 * N;      // read r,s,r^; write w,z

@@ -32,16 +32,20 @@ struct Scal {
   int32_t rr_off;                  // ||r_i|| < sqrt(eps)||r_0|| seen: no more replacements
   int32_t gap_iter;                // last iteration whose gap was written
   int32_t bench, rr_period;
+  int32_t method;                  // 0 p-BiCGStab (Alg. 2), 1 BiCGStab (Alg. 1), 2 p-CG
+  double g_old, a_old;             // p-CG: gamma_{i-1}, alpha_{i-1}
   int32_t nranks, rank;
   Dd* red_send;                    // [nranks][RED_K]: only row `rank` is ever written
   Dd* red_recv;                    // [nranks][RED_K]: all rows after the exchange
-  unsigned int counter[8];         // last-CTA tickets, one per kernel kind
+  unsigned int counter[16];        // last-CTA tickets, one per kernel kind
 };
 
-enum TicketSlot { T_INIT1 = 0, T_INIT2, T_SWEEPA, T_SWEEPC, T_RR2, T_GAP, T_APPLY, T_MISC };
+enum TicketSlot { T_INIT1 = 0, T_INIT2, T_SWEEPA, T_SWEEPC, T_RR2, T_GAP, T_APPLY, T_MISC,
+                  T_CL1, T_CL2, T_CL3, T_PC, T_PCI1, T_PCI2 };
 
 // which scalar-forming step a reduction feeds
-enum FinKind { F_INIT1 = 0, F_INIT2, F_SWEEPA, F_SWEEPC, F_RR2, F_GAP };
+enum FinKind { F_INIT1 = 0, F_INIT2, F_SWEEPA, F_SWEEPC, F_RR2, F_GAP,
+               F_CL1, F_CL2, F_CL3, F_PINIT2, F_PC };
 
 struct Hist {
   double* rnorm;  // [maxit+1]
@@ -89,6 +93,96 @@ __device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot) {
   if (F == F_INIT1) {
     sc->tmp0 = dd_round(tot[0]);  // (r0, r0) = (r^0, r0) = rho_0
     sc->tmp1 = dd_round(tot[1]);  // (b, b)
+    if (sc->method != 0) {
+      // Alg. 1 lines 2-3 / p-CG init: rho_0 := (r^0, r0) = (r0, r0) (r^0 := r0,
+      // A2); ||r0||, ||b||, stop test (A7); beta, omega := 0 (line 17 with p_{-1} = 0)
+      sc->rho = sc->tmp0;
+      sc->alpha = 0.0;
+      sc->beta = 0.0;
+      sc->omega = 0.0;
+      sc->h0 = sqrt(sc->tmp0);
+      sc->nb = sqrt(sc->tmp1);
+      sc->tol_abs = sc->tol * sc->nb;
+      h.rnorm[0] = sc->h0;
+      if (sc->h0 <= sc->tol_abs && !sc->bench) {
+        sc->done = 1;
+        sc->outcome = OUT_CONVERGED;
+      }
+    }
+  } else if (F == F_CL1) {
+    // Alg. 1 lines 6-7: alpha_i := rho_i / (r^0, s_i)
+    sc->alpha = sc->rho / dd_round(tot[0]);
+  } else if (F == F_CL2) {
+    // Alg. 1 lines 11-12: omega_i := (q_i, y_i) / (y_i, y_i), guard A9
+    const double qy = dd_round(tot[0]), yy = dd_round(tot[1]);
+    const double om = (yy == 0.0) ? 0.0 : qy / yy;
+    sc->omega = om;
+    if (!isfinite(sc->alpha) || !isfinite(om)) {
+      sc->done = 1;
+      sc->outcome = OUT_BREAKDOWN;
+      sc->iters = sc->iter;
+    }
+  } else if (F == F_CL3) {
+    // Alg. 1 lines 15-16: rho_{i+1} := (r^0, r_{i+1}); ||r_{i+1}||; stop
+    // test (A7); beta_i := (alpha_i / omega_i) (rho_{i+1} / rho_i), left to right (A4)
+    const int i = sc->iter;
+    const double rho1 = dd_round(tot[0]);
+    const double hn = sqrt(dd_round(tot[1]));
+    h.rnorm[i + 1] = hn;
+    sc->iters = i + 1;
+    sc->iter = i + 1;
+    if (hn <= sc->tol_abs && !sc->bench) {
+      sc->done = 1;
+      sc->outcome = OUT_CONVERGED;
+      return;
+    }
+    const double beta = ((sc->alpha / sc->omega) * rho1) / sc->rho;
+    sc->beta = beta;
+    sc->rho = rho1;
+    if (!isfinite(beta) || rho1 == 0.0) {
+      sc->done = 1;
+      sc->outcome = OUT_BREAKDOWN;
+    }
+  } else if (F == F_PINIT2) {
+    // p-CG iteration 0 scalars (reading A19): gamma_0 := (r0, u0), delta_0 := (w0, u0),
+    // beta_0 := 0, alpha_0 := gamma_0 / delta_0
+    if (sc->done) return;  // converged at i = 0
+    const double gam = dd_round(tot[0]), del = dd_round(tot[1]);
+    const double alpha = gam / del;
+    sc->alpha = alpha;
+    sc->beta = 0.0;
+    sc->g_old = gam;
+    sc->a_old = alpha;
+    if (!isfinite(alpha)) {
+      sc->done = 1;
+      sc->outcome = OUT_BREAKDOWN;
+      sc->iters = 0;
+    }
+  } else if (F == F_PC) {
+    // p-CG end of iteration i: ||r_{i+1}||, stop test, then the scalars of iteration
+    // i+1 from its single reduction {(r,u), (w,u)}: beta := gamma / gamma_old;
+    // alpha := gamma / (delta - (beta gamma) / alpha_old)   (reading A19)
+    const int i = sc->iter;
+    const double gam = dd_round(tot[0]), del = dd_round(tot[1]);
+    const double hn = sqrt(dd_round(tot[2]));
+    h.rnorm[i + 1] = hn;
+    sc->iters = i + 1;
+    sc->iter = i + 1;
+    if (hn <= sc->tol_abs && !sc->bench) {
+      sc->done = 1;
+      sc->outcome = OUT_CONVERGED;
+      return;
+    }
+    const double beta = gam / sc->g_old;
+    const double alpha = gam / (del - (beta * gam) / sc->a_old);
+    sc->alpha = alpha;
+    sc->beta = beta;
+    sc->g_old = gam;
+    sc->a_old = alpha;
+    if (!isfinite(alpha) || !isfinite(beta)) {
+      sc->done = 1;
+      sc->outcome = OUT_BREAKDOWN;
+    }
   } else if (F == F_INIT2) {
     // line 3: alpha0 := (r0,r0)/(r0,w0); beta0 := 0; omega_{-1} := 0 (A1)
     const double rho = sc->tmp0;

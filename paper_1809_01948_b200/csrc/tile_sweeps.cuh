@@ -20,6 +20,19 @@
 //   TM_A    sweep A, lines 5-12          TM_C    sweep C, lines 16-21
 //   TM_RR1  eq:rr r, k, s, l TM_RR2  eq:rr w, z + line-21 dots
 //   TM_GAP  eq:res_gap           TM_INIT1 / TM_INIT2  lines 2-3
+// Comparison solvers on the same machinery:
+//   TM_CL1  Alg. 1 line 17 + lines 4-6: p := r + beta (p - omega s),
+//           s := A M^-1 p, (r^0, s)     -- stencil of the DERIVED operand p
+//   TM_CL2  Alg. 1 lines 8-11: q := r - alpha s (derived), y := A M^-1 q,
+//           (q, y), (y, y)              -- reads r, s only, writes nothing
+//   TM_CL3  Alg. 1 lines 13-15: x, r; (r^0, r), (r, r)
+//   TM_PC   p-CG iteration (reading A19): n := A M^-1 w, z, q, s, p, x, r, u, w;
+//           next iteration's (r, u), (w, u), (r, r)
+//   TM_PCI1 / TM_PCI2  p-CG init: r0, u0; w0 := A M^-1 r0, (r0, u0), (w0, u0)
+// A DERIVED mode stages NSV vectors with halos and applies the stencil to one
+// operand formed from them element by element (derive<MODE>), so the operand is
+// never written to HBM; it is formed with the same operations as the oracle's
+// stored vector, hence bitwise equal.
 #pragma once
 #include "dd.cuh"
 #include "state.cuh"
@@ -28,18 +41,26 @@
 
 #define TNT 512  // threads per CTA
 
-enum TileMode { TM_A = 0, TM_C, TM_RR1, TM_RR2, TM_GAP, TM_INIT1, TM_INIT2, TM_N };
+enum TileMode { TM_A = 0, TM_C, TM_RR1, TM_RR2, TM_GAP, TM_INIT1, TM_INIT2,
+                TM_CL1, TM_CL2, TM_CL3, TM_PC, TM_PCI1, TM_PCI2, TM_N };
 
-// per mode: stencil operands, whether they enter as A M^-1 v (PREC) or A v,
-// the maximum number of streamed vectors, outputs, dot products
+// per mode: staged stencil vectors (NSV), whether they form ONE derived operand
+// (DER), whether the operand enters as A M^-1 v (PREC) or A v, the maximum number
+// of streamed vectors, outputs, dot products
 template <int M> struct TileTraits;
-template <> struct TileTraits<TM_A> { enum { NSV = 2, PREC = 1, NSTR = 6, NOUT = 4, K = 2 }; };
-template <> struct TileTraits<TM_C> { enum { NSV = 2, PREC = 1, NSTR = 7, NOUT = 4, K = 5 }; };
-template <> struct TileTraits<TM_RR1> { enum { NSV = 2, PREC = 0, NSTR = 1, NOUT = 4, K = 0 }; };
-template <> struct TileTraits<TM_RR2> { enum { NSV = 2, PREC = 1, NSTR = 1, NOUT = 2, K = 5 }; };
-template <> struct TileTraits<TM_GAP> { enum { NSV = 1, PREC = 0, NSTR = 2, NOUT = 0, K = 1 }; };
-template <> struct TileTraits<TM_INIT1> { enum { NSV = 1, PREC = 0, NSTR = 1, NOUT = 3, K = 2 }; };
-template <> struct TileTraits<TM_INIT2> { enum { NSV = 1, PREC = 1, NSTR = 1, NOUT = 1, K = 1 }; };
+template <> struct TileTraits<TM_A> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 6, NOUT = 4, K = 2 }; };
+template <> struct TileTraits<TM_C> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 7, NOUT = 4, K = 5 }; };
+template <> struct TileTraits<TM_RR1> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 0 }; };
+template <> struct TileTraits<TM_RR2> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 5 }; };
+template <> struct TileTraits<TM_GAP> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 2, NOUT = 0, K = 1 }; };
+template <> struct TileTraits<TM_INIT1> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 1, NOUT = 3, K = 2 }; };
+template <> struct TileTraits<TM_INIT2> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 1, NOUT = 1, K = 1 }; };
+template <> struct TileTraits<TM_CL1> { enum { NSV = 3, DER = 1, PREC = 1, NSTR = 1, NOUT = 2, K = 1 }; };
+template <> struct TileTraits<TM_CL2> { enum { NSV = 2, DER = 1, PREC = 1, NSTR = 0, NOUT = 0, K = 2 }; };
+template <> struct TileTraits<TM_CL3> { enum { NSV = 2, DER = 1, PREC = 1, NSTR = 3, NOUT = 2, K = 2 }; };
+template <> struct TileTraits<TM_PC> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 7, NOUT = 8, K = 3 }; };
+template <> struct TileTraits<TM_PCI1> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 1, NOUT = 2, K = 2 }; };
+template <> struct TileTraits<TM_PCI2> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 2 }; };
 
 struct TileGeo {
   int64_t nx, ny;     // x extent; lines per plane (3D: ny, 2D: 1)
@@ -144,9 +165,78 @@ __device__ __forceinline__ void stencil_pair(const TileGeo& g, int nx, const dou
   t1 = a;
 }
 
+// The derived operand of a DERIVED mode from the staged values v[0..NSV-1] of
+// one element (same expression, same order as the oracle's stored vector).
+template <int MODE>
+__device__ __forceinline__ double derive(double v0, double v1, double v2, double al, double be,
+                                         double om) {
+  if (MODE == TM_CL1) return v0 + be * (v1 - om * v2);  // Alg. 1 l.17: r + beta (p - omega s)
+  return v0 - al * v1;                                  // Alg. 1 l.8: q := r - alpha s
+}
+
+// derived values of the element pair at P (vector k at P + k * svs)
+template <bool VEC, int NSV, int MODE>
+__device__ __forceinline__ void derive_pair(const double* P, int svs, double al, double be,
+                                            double om, double& a, double& b) {
+  double a0, b0, a1 = 0.0, b1 = 0.0, a2 = 0.0, b2 = 0.0;
+  ld2<VEC>(P, a0, b0);
+  if (NSV > 1) ld2<VEC>(P + svs, a1, b1);
+  if (NSV > 2) ld2<VEC>(P + 2 * svs, a2, b2);
+  a = derive<MODE>(a0, a1, a2, al, be, om);
+  b = derive<MODE>(b0, b1, b2, al, be, om);
+}
+
+template <int NSV, int MODE>
+__device__ __forceinline__ double derive_one(const double* P, int svs, double al, double be,
+                                             double om) {
+  return derive<MODE>(P[0], NSV > 1 ? P[svs] : 0.0, NSV > 2 ? P[2 * svs] : 0.0, al, be, om);
+}
+
+// stencil_pair for a DERIVED operand: W points at row r of plane z in the slot
+// of staged vector 0 (vector k at W + k * svs), W1 likewise for plane z+1; zm0/zm1
+// are the derived values of plane z-1.  Returns the derived centre pair (c0, c1)
+// and fl(A M^-1 op) (PREC) or fl(A op) for the row pair, legs as in stencil_pair.
+template <int DIM, bool VEC, bool INTERIOR, bool PREC, int NSV, int MODE>
+__device__ __forceinline__ void stencil_pair_der(const TileGeo& g, int nx, const double* W,
+                                                 int svs, const double* W1, double zm0,
+                                                 double zm1, unsigned b0, unsigned b1,
+                                                 double al, double be, double om, double& c0,
+                                                 double& c1, double& t0, double& t1) {
+  const double d = g.dinv;
+  derive_pair<VEC, NSV, MODE>(W, svs, al, be, om, c0, c1);
+  const double pm = pre<PREC>(d, derive_one<NSV, MODE>(W - 1, svs, al, be, om));
+  const double p0 = pre<PREC>(d, c0), p1 = pre<PREC>(d, c1);
+  const double p2 = pre<PREC>(d, derive_one<NSV, MODE>(W + 2, svs, al, be, om));
+  double ym0 = 0.0, ym1 = 0.0, yp0 = 0.0, yp1 = 0.0, zp0, zp1;
+  if (DIM == 3) {
+    derive_pair<VEC, NSV, MODE>(W - nx, svs, al, be, om, ym0, ym1);
+    derive_pair<VEC, NSV, MODE>(W + nx, svs, al, be, om, yp0, yp1);
+  }
+  derive_pair<VEC, NSV, MODE>(W1, svs, al, be, om, zp0, zp1);
+  const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
+  double a = 0.0;
+  a = leg<INTERIOR>(b0, 1u, a, czm * pre<PREC>(d, zm0));
+  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * pre<PREC>(d, ym0));
+  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * pm);
+  a = a + g.c[0] * p0;
+  a = leg<INTERIOR>(b0, 8u, a, g.c[2] * p1);
+  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * pre<PREC>(d, yp0));
+  a = leg<INTERIOR>(b0, 32u, a, czp * pre<PREC>(d, zp0));
+  t0 = a;
+  a = 0.0;
+  a = leg<INTERIOR>(b1, 1u, a, czm * pre<PREC>(d, zm1));
+  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * pre<PREC>(d, ym1));
+  a = leg<INTERIOR>(b1, 4u, a, g.c[1] * p0);
+  a = a + g.c[0] * p1;
+  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * p2);
+  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * pre<PREC>(d, yp1));
+  a = leg<INTERIOR>(b1, 32u, a, czp * pre<PREC>(d, zp1));
+  t1 = a;
+}
+
 // Per-row arithmetic of each mode.  S = stream slot at this row, st = stride;
 // c0/c1 = the stencil operands' centre values, t0/t1 = their stencil products.
-template <int MODE, int K>
+template <int MODE, int K, int NOUTC>
 __device__ __forceinline__ void row_update(const double* S, int st, bool rr, double c0, double c1,
                                            double t0, double t1, double al, double be, double om,
                                            double dinv, Dd* acc, double* o) {
@@ -209,6 +299,50 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, dou
   } else if (MODE == TM_INIT2) {  // c = r0; t0 = A M^-1 r0 = A k0
     o[0] = t0;                                 // w0
     dd_fma(acc[0], S[0], t0);                  // (r^, w0)
+  } else if (MODE == TM_CL1) {  // c0 = p_i (derived, l.17), t0 = A M^-1 p_i (l.4-5)
+    o[0] = c0;                                 // p_i
+    o[1] = t0;                                 // s_i
+    dd_fma(acc[0], S[0], t0);                  // l.6: (r^0, s_i)
+  } else if (MODE == TM_CL2) {  // c0 = q_i (derived, l.8), t0 = y_i = A M^-1 q_i (l.9-10)
+    dd_fma(acc[0], c0, t0);                    // l.11: (q, y)
+    dd_fma(acc[1 % K], t0, t0);                //       (y, y)
+  } else if (MODE == TM_CL3) {  // c0 = q_i, t0 = y_i; streams x, p, r^0
+    const double xj = S[0], pj = S[st], rhj = S[2 * st];
+    const double gj = dinv * pj;               // l.4: g := M^-1 p
+    const double uj = dinv * c0;               // l.9: u := M^-1 q
+    o[0] = (xj + al * gj) + om * uj;           // l.13: x
+    o[1] = c0 - om * t0;                       // l.14: r
+    dd_fma(acc[0], rhj, o[1]);                 // l.15: (r^0, r)
+    dd_fma(acc[1 % K], o[1], o[1]);            //       ||r||^2 (A8)
+  } else if (MODE == TM_PC) {  // c0 = w_i, t0 = n_i = A M^-1 w_i; streams z,q,s,p,x,r,u
+    const double mj = dinv * c0;               // m := M^-1 w
+    const double zj = S[0], qj = S[st], sj = S[2 * st], pj = S[3 * st];
+    const double xj = S[4 * st], rj = S[5 * st], uj = S[6 * st];
+    const double zn = t0 + be * zj;            // z := n + beta z
+    const double qn = mj + be * qj;            // q := m + beta q
+    const double sn = c0 + be * sj;            // s := w + beta s
+    const double pn = uj + be * pj;            // p := u + beta p
+    const double xn = xj + al * pn;            // x := x + alpha p
+    const double rn = rj - al * sn;            // r := r - alpha s
+    const double un = uj - al * qn;            // u := u - alpha q
+    const double wn = c0 - al * zn;            // w := w - alpha z
+    o[0] = zn; o[1 % NOUTC] = qn; o[2 % NOUTC] = sn; o[3 % NOUTC] = pn;
+    o[4 % NOUTC] = xn; o[5 % NOUTC] = rn; o[6 % NOUTC] = un; o[7 % NOUTC] = wn;
+    dd_fma(acc[0], rn, un);                    // next iteration's (r, u)
+    dd_fma(acc[1 % K], wn, un);                //                  (w, u)
+    dd_fma(acc[2 % K], rn, rn);                //                  ||r||^2
+  } else if (MODE == TM_PCI1) {  // c = x0; t0 = A x0; stream b
+    const double bj = S[0];
+    const double rj = bj - t0;                 // r0 := b - A x0
+    o[0] = rj;
+    o[1 % NOUTC] = dinv * rj;                  // u0 := M^-1 r0
+    dd_fma(acc[0], rj, rj);
+    dd_fma(acc[1 % K], bj, bj);
+  } else if (MODE == TM_PCI2) {  // c = r0; t0 = A M^-1 r0 = A u0
+    const double uj = dinv * c0;               // u0 (same value as stored)
+    o[0] = t0;                                 // w0
+    dd_fma(acc[0], c0, uj);                    // (r0, u0)
+    dd_fma(acc[1 % K], t0, uj);                // (w0, u0)
   }
 }
 
@@ -219,11 +353,16 @@ template <int DIM, int MODE, bool VEC>
 __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
                                                  Dd* __restrict__ part, Hist h) {
   using T = TileTraits<MODE>;
-  constexpr int NSV = T::NSV, NSTR_MAX = T::NSTR;
+  constexpr int NSV = T::NSV, NST = T::NSTR;
+  constexpr int NSTR_MAX = NST > 0 ? NST : 1;  // array extent
+  constexpr bool HAS_STR = NST > 0;
+  constexpr bool DER = T::DER != 0;
+  constexpr int NSO = DER ? 1 : NSV;           // stencil operands
   constexpr int NOUT = T::NOUT > 0 ? T::NOUT : 1;
   constexpr int K = T::K > 0 ? T::K : 1;
   constexpr bool PREC = T::PREC != 0;
-  if (MODE == TM_A || MODE == TM_C) {
+  if (MODE == TM_A || MODE == TM_C || MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3 ||
+      MODE == TM_PC) {
     if (sc->done) return;
   } else if (MODE == TM_RR1 || MODE == TM_RR2) {
     if (sc->done || !sc->rr_fire) return;
@@ -233,7 +372,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);  // [0,1] streams, [2..4] stencil
   double* st = reinterpret_cast<double*>(smem_raw + 64);
-  double* sv = st + 2 * NSTR_MAX * g.st_stride;
+  double* sv = st + 2 * NST * g.st_stride;
   const int tid = threadIdx.x;
   const int nx = (int)g.nx;
   const int sts = g.st_stride, svs = g.sv_stride;
@@ -241,7 +380,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   const int it = sc->iter;
   const double al = sc->alpha, be = sc->beta, om = sc->omega;
   const bool rr = MODE == TM_A && sc->use_rr != 0;
-  const double* svp[2] = {nullptr, nullptr};
+  const double* svp[3] = {nullptr, nullptr, nullptr};
   const double* stp[NSTR_MAX];
   int nstr = NSTR_MAX;
   double* outp[NOUT];
@@ -273,12 +412,48 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     outp[1 % NOUT] = V.zrr;                          // replaced z_i (A26)
   } else if (MODE == TM_GAP) {
     svp[0] = V.x;
-    stp[0] = V.b; stp[1 % NSTR_MAX] = V.r;
+    stp[0] = V.b;
+    stp[1 % NSTR_MAX] = (sc->method == 1 && (it & 1)) ? V.k : V.r;  // Alg. 1: r double-buffered
+  } else if (MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3) {
+    // Alg. 1 buffers: r_i in {r, k}[i&1], p_i in {g, l}[i&1], s_i in {s, zrr}[i&1]
+    const bool odd = (it & 1) != 0;
+    double* const Rc = odd ? V.k : V.r;   // r_i
+    double* const Ro = odd ? V.r : V.k;   // r_{i+1}
+    double* const Pc = odd ? V.l : V.g;   // p_i
+    double* const Po = odd ? V.g : V.l;   // p_{i-1}
+    double* const Sc = odd ? V.zrr : V.s; // s_i
+    double* const So = odd ? V.s : V.zrr; // s_{i-1}
+    if (MODE == TM_CL1) {
+      svp[0] = Rc; svp[1] = Po; svp[2] = So;          // r_i, p_{i-1}, s_{i-1}
+      stp[0] = V.rh;
+      outp[0] = Pc; outp[1 % NOUT] = Sc;               // p_i, s_i
+    } else if (MODE == TM_CL2) {
+      svp[0] = Rc; svp[1] = Sc;                        // q_i = r_i - alpha s_i
+    } else {
+      svp[0] = Rc; svp[1] = Sc;
+      stp[0] = V.x; stp[1 % NSTR_MAX] = Pc; stp[2 % NSTR_MAX] = V.rh;
+      outp[0] = V.x; outp[1 % NOUT] = Ro;              // x_{i+1}, r_{i+1}
+    }
+  } else if (MODE == TM_PC) {
+    // p-CG buffers: z -> z0, q -> l, s, p -> g, x, r, u -> k; w_i in {w0, w1}[i&1]
+    svp[0] = (it & 1) ? V.w1 : V.w0;
+    stp[0] = V.z0; stp[1 % NSTR_MAX] = V.l; stp[2 % NSTR_MAX] = V.s; stp[3 % NSTR_MAX] = V.g;
+    stp[4 % NSTR_MAX] = V.x; stp[5 % NSTR_MAX] = V.r; stp[6 % NSTR_MAX] = V.k;
+    outp[0] = V.z0; outp[1 % NOUT] = V.l; outp[2 % NOUT] = V.s; outp[3 % NOUT] = V.g;
+    outp[4 % NOUT] = V.x; outp[5 % NOUT] = V.r; outp[6 % NOUT] = V.k;
+    outp[7 % NOUT] = (it & 1) ? V.w0 : V.w1;
+  } else if (MODE == TM_PCI1) {
+    svp[0] = V.x;
+    stp[0] = V.b;
+    outp[0] = V.r; outp[1 % NOUT] = V.k;              // r0, u0
+  } else if (MODE == TM_PCI2) {
+    svp[0] = V.r;
+    outp[0] = V.w0;
   } else if (MODE == TM_INIT1) {
     svp[0] = V.x;
     stp[0] = V.b;
     outp[0] = V.r; outp[1 % NOUT] = V.rh; outp[2 % NOUT] = V.k;
-  } else {  // TM_INIT2
+  } else if (MODE == TM_INIT2) {
     svp[0] = V.r;
     stp[0] = V.rh;
     outp[0] = V.w0;
@@ -324,15 +499,19 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     const unsigned xy_all = DIM == 3 ? 30u : 12u;
     const bool xy_int = __all_sync(0xffffffffu, !act || ((b0 & xy_all) == xy_all &&
                                                          (b1 & xy_all) == xy_all));
-    double m1[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // plane z-1 centre values per operand
+    double m1[NSO][2];  // plane z-1 centre values per stencil operand
+#pragma unroll
+    for (int v = 0; v < NSO; ++v) m1[v][0] = m1[v][1] = 0.0;
     if (tid == 0) {
       for (int m = 0; m < 3 && m < nsv; ++m) {
         const int s = (svc + m) % 3;
         stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, (z0 - 1 + m) * g.pxy + toff - g.halo,
               TP + 2 * g.halo, &bar[2 + s]);
       }
-      const int s = stc % 2;
-      stage(st + (size_t)s * NSTR_MAX * sts, sts, stp, nstr, z0 * g.pxy + toff, TP, &bar[s]);
+      if (HAS_STR) {
+        const int s = stc % 2;
+        stage(st + (size_t)s * NST * sts, sts, stp, nstr, z0 * g.pxy + toff, TP, &bar[s]);
+      }
     }
     {  // plane z0-1 -> registers
       const int s = svc % 3;
@@ -341,8 +520,12 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       const double* b0p = sv + (size_t)s * NSV * svs +
                           align_off(svp[0] + (z0 - 1) * g.pxy + toff - g.halo) + g.halo + r;
       if (act) {
+        if (DER) {
+          derive_pair<VEC, NSV, MODE>(b0p, svs, al, be, om, m1[0][0], m1[0][1]);
+        } else {
 #pragma unroll
-        for (int v = 0; v < NSV; ++v) ld2<VEC>(b0p + v * svs, m1[v][0], m1[v][1]);
+          for (int v = 0; v < NSO; ++v) ld2<VEC>(b0p + v * svs, m1[v][0], m1[v][1]);
+        }
       }
       const int s1 = (svc + 1) % 3;  // plane z0
       mbar_wait(&bar[2 + s1], (ph >> (2 + s1)) & 1u);
@@ -357,50 +540,65 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
           stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, (z + 2) * g.pxy + toff - g.halo,
                 TP + 2 * g.halo, &bar[2 + s]);
         }
-        if (n + 1 < nst) {  // streams z+1
+        if (HAS_STR && n + 1 < nst) {  // streams z+1
           const int s = (stc + n + 1) % 2;
-          stage(st + (size_t)s * NSTR_MAX * sts, sts, stp, nstr, (z + 1) * g.pxy + toff, TP,
+          stage(st + (size_t)s * NST * sts, sts, stp, nstr, (z + 1) * g.pxy + toff, TP,
                 &bar[s]);
         }
       }
       const int s_z = (svc + n + 1) % 3, s_z1 = (svc + n + 2) % 3, s_st = (stc + n) % 2;
       mbar_wait(&bar[2 + s_z1], (ph >> (2 + s_z1)) & 1u);
       ph ^= 1u << (2 + s_z1);
-      mbar_wait(&bar[s_st], (ph >> s_st) & 1u);
-      ph ^= 1u << s_st;
+      if (HAS_STR) {
+        mbar_wait(&bar[s_st], (ph >> s_st) & 1u);
+        ph ^= 1u << s_st;
+      }
       if (!act) continue;
       const int oz = align_off(svp[0] + z * g.pxy + toff - g.halo) + g.halo;
       const int oz1 = align_off(svp[0] + (z + 1) * g.pxy + toff - g.halo) + g.halo;
-      const int os = align_off(stp[0] + z * g.pxy + toff);
       const double* Wz = sv + (size_t)s_z * NSV * svs + oz + r;
       const double* Wz1 = sv + (size_t)s_z1 * NSV * svs + oz1 + r;
-      const double* S0 = st + (size_t)s_st * NSTR_MAX * sts + os + r;
+      const double* S0 = HAS_STR ? st + (size_t)s_st * NST * sts +
+                                       align_off(stp[0] + z * g.pxy + toff) + r
+                                 : nullptr;
       const bool zin = (g.o0 + z) > 0 && (g.o0 + z) < g.nog - 1;
       const unsigned zb = ((g.o0 + z) > 0 ? 1u : 0u) | ((g.o0 + z) < g.nog - 1 ? 32u : 0u);
       double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-      if (xy_int && zin) {
+      if (DER) {
+        if (xy_int && zin)
+          stencil_pair_der<DIM, VEC, true, PREC, NSV, MODE>(g, nx, Wz, svs, Wz1, m1[0][0],
+                                                            m1[0][1], 0u, 0u, al, be, om, c[0][0],
+                                                            c[0][1], t[0][0], t[0][1]);
+        else
+          stencil_pair_der<DIM, VEC, false, PREC, NSV, MODE>(g, nx, Wz, svs, Wz1, m1[0][0],
+                                                             m1[0][1], b0 | zb, b1 | zb, al, be,
+                                                             om, c[0][0], c[0][1], t[0][0],
+                                                             t[0][1]);
+      } else if (xy_int && zin) {
 #pragma unroll
-        for (int v = 0; v < NSV; ++v)
+        for (int v = 0; v < NSO; ++v)
           stencil_pair<DIM, VEC, true, PREC>(g, nx, Wz + v * svs, Wz1 + v * svs, m1[v][0],
                                              m1[v][1], 0u, 0u, c[v][0], c[v][1], t[v][0], t[v][1]);
       } else {
 #pragma unroll
-        for (int v = 0; v < NSV; ++v)
+        for (int v = 0; v < NSO; ++v)
           stencil_pair<DIM, VEC, false, PREC>(g, nx, Wz + v * svs, Wz1 + v * svs, m1[v][0],
                                               m1[v][1], b0 | zb, b1 | zb, c[v][0], c[v][1],
                                               t[v][0], t[v][1]);
       }
 #pragma unroll
-      for (int v = 0; v < NSV; ++v) {
+      for (int v = 0; v < NSO; ++v) {
         m1[v][0] = c[v][0];
         m1[v][1] = c[v][1];
       }
-      double o0[4] = {0.0, 0.0, 0.0, 0.0}, o1[4] = {0.0, 0.0, 0.0, 0.0};
-      row_update<MODE, K>(S0, sts, rr, c[0][0], c[1][0], t[0][0], t[1][0], al, be, om, g.dinv,
-                          acc, o0);
+      double o0[NOUT], o1[NOUT];
+#pragma unroll
+      for (int k = 0; k < NOUT; ++k) o0[k] = o1[k] = 0.0;
+      row_update<MODE, K, NOUT>(S0, sts, rr, c[0][0], c[1][0], t[0][0], t[1][0], al, be, om,
+                                g.dinv, acc, o0);
       if (valid1)
-        row_update<MODE, K>(S0 + 1, sts, rr, c[0][1], c[1][1], t[0][1], t[1][1], al, be, om,
-                            g.dinv, acc, o1);
+        row_update<MODE, K, NOUT>(HAS_STR ? S0 + 1 : nullptr, sts, rr, c[0][1], c[1][1], t[0][1],
+                                  t[1][1], al, be, om, g.dinv, acc, o1);
       const int64_t gi = z * g.pxy + toff + r;
       if (T::NOUT > 0) {
 #pragma unroll
@@ -414,29 +612,46 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   if (T::K > 0) {
     Dd tot[K];
     const int slot = MODE == TM_A ? T_SWEEPA : MODE == TM_C ? T_SWEEPC : MODE == TM_RR2 ? T_RR2
-                   : MODE == TM_GAP ? T_GAP : MODE == TM_INIT1 ? T_INIT1 : T_INIT2;
+                   : MODE == TM_GAP ? T_GAP : MODE == TM_INIT1 ? T_INIT1 : MODE == TM_INIT2 ? T_INIT2
+                   : MODE == TM_CL1 ? T_CL1 : MODE == TM_CL2 ? T_CL2 : MODE == TM_CL3 ? T_CL3
+                   : MODE == TM_PC ? T_PC : MODE == TM_PCI1 ? T_PCI1 : T_PCI2;
     if (dd_grid_reduce<K>(acc, part, &sc->counter[slot], tot) && tid == 0) {
       if (MODE == TM_A) publish<F_SWEEPA>(sc, h, tot);
       else if (MODE == TM_C) publish<F_SWEEPC>(sc, h, tot);
       else if (MODE == TM_RR2) publish<F_RR2>(sc, h, tot);
       else if (MODE == TM_GAP) publish<F_GAP>(sc, h, tot);
-      else if (MODE == TM_INIT1) publish<F_INIT1>(sc, h, tot);
-      else publish<F_INIT2>(sc, h, tot);
+      else if (MODE == TM_INIT1 || MODE == TM_PCI1) publish<F_INIT1>(sc, h, tot);
+      else if (MODE == TM_INIT2) publish<F_INIT2>(sc, h, tot);
+      else if (MODE == TM_CL1) publish<F_CL1>(sc, h, tot);
+      else if (MODE == TM_CL2) publish<F_CL2>(sc, h, tot);
+      else if (MODE == TM_CL3) publish<F_CL3>(sc, h, tot);
+      else if (MODE == TM_PC) publish<F_PC>(sc, h, tot);
+      else publish<F_PINIT2>(sc, h, tot);
     }
   }
 }
 
 // host-side helper: shared-memory bytes of a t_tile<., MODE, .> launch
+template <int M>
+inline size_t tile_smem_bytes_t(const TileGeo& g) {
+  return 64 + sizeof(double) * ((size_t)2 * TileTraits<M>::NSTR * g.st_stride +
+                                (size_t)3 * TileTraits<M>::NSV * g.sv_stride);
+}
+
 inline size_t tile_smem_bytes(const TileGeo& g, int mode) {
-  int nstr = 1, nsv = 1;
   switch (mode) {
-    case TM_A: nstr = TileTraits<TM_A>::NSTR; nsv = TileTraits<TM_A>::NSV; break;
-    case TM_C: nstr = TileTraits<TM_C>::NSTR; nsv = TileTraits<TM_C>::NSV; break;
-    case TM_RR1: nstr = TileTraits<TM_RR1>::NSTR; nsv = TileTraits<TM_RR1>::NSV; break;
-    case TM_RR2: nstr = TileTraits<TM_RR2>::NSTR; nsv = TileTraits<TM_RR2>::NSV; break;
-    case TM_GAP: nstr = TileTraits<TM_GAP>::NSTR; nsv = TileTraits<TM_GAP>::NSV; break;
-    case TM_INIT1: nstr = TileTraits<TM_INIT1>::NSTR; nsv = TileTraits<TM_INIT1>::NSV; break;
-    default: nstr = TileTraits<TM_INIT2>::NSTR; nsv = TileTraits<TM_INIT2>::NSV; break;
+    case TM_A: return tile_smem_bytes_t<TM_A>(g);
+    case TM_C: return tile_smem_bytes_t<TM_C>(g);
+    case TM_RR1: return tile_smem_bytes_t<TM_RR1>(g);
+    case TM_RR2: return tile_smem_bytes_t<TM_RR2>(g);
+    case TM_GAP: return tile_smem_bytes_t<TM_GAP>(g);
+    case TM_INIT1: return tile_smem_bytes_t<TM_INIT1>(g);
+    case TM_INIT2: return tile_smem_bytes_t<TM_INIT2>(g);
+    case TM_CL1: return tile_smem_bytes_t<TM_CL1>(g);
+    case TM_CL2: return tile_smem_bytes_t<TM_CL2>(g);
+    case TM_CL3: return tile_smem_bytes_t<TM_CL3>(g);
+    case TM_PC: return tile_smem_bytes_t<TM_PC>(g);
+    case TM_PCI1: return tile_smem_bytes_t<TM_PCI1>(g);
+    default: return tile_smem_bytes_t<TM_PCI2>(g);
   }
-  return 64 + sizeof(double) * ((size_t)2 * nstr * g.st_stride + (size_t)3 * nsv * g.sv_stride);
 }
