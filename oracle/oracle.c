@@ -35,6 +35,7 @@
 #define ORC_BENCH 1      /* run maxit iterations: no exit on convergence (A23) */
 #define ORC_PLAIN_DOT 2  /* plain left-to-right dot instead of Dot2 (diagnostic) */
 #define ORC_GAP 4        /* compute the residual gap history */
+#define ORC_AUTO_RR 8    /* automated replacement: bound f^r_i (eq:DDr_bound) + eq:criterion */
 
 #define OUT_CONVERGED 0
 #define OUT_MAXIT 1
@@ -135,6 +136,26 @@ int64_t orc_stencil_csr(int dim, int64_t nx, int64_t ny, int64_t nz, const doubl
   return nnz;
 }
 
+/* ||A||_2 <= sqrt(||A||_1 ||A||_inf) (Hoelder): the upper bound the run-time
+ * gap bound uses for ||A|| (reading A29).  Row sums in ascending column order,
+ * column sums in ascending row order, |a_ij| summed from +0.0. */
+double orc_anorm_bound(int64_t n, const int64_t* rp, const int64_t* ci, const double* va) {
+  double* col = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+  double rmax = 0.0, cmax = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    double rs = 0.0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      rs = rs + fabs(va[p]);
+      col[ci[p]] = col[ci[p]] + fabs(va[p]);
+    }
+    if (rs > rmax) rmax = rs;
+  }
+  for (int64_t j = 0; j < n; ++j)
+    if (col[j] > cmax) cmax = col[j];
+  free(col);
+  return sqrt(cmax * rmax);
+}
+
 /* ------------------------------------------------------------------------- */
 /* Workspace helper                                                          */
 /* ------------------------------------------------------------------------- */
@@ -167,11 +188,43 @@ static double res_gap(int flags, int64_t n, const int64_t* rp, const int64_t* ci
 /* stop, latched), A26 (n_i, v_i are not replaced).                           */
 /* sc_trace (optional): per iteration i: alpha_i, beta_i, omega_i, rho_i.     */
 /* ------------------------------------------------------------------------- */
+/* Automated residual replacement, flag ORC_AUTO_RR.  The run-time
+ * bound f^r_i on ||Delta^r_i|| (eq:DDr_bound P:613-616) is propagated by the
+ * triangle inequality over the one-step gap recurrences eq:Dr, eq:Ds
+ * (P:276-280), eq:Dw, eq:Dz, with every local error
+ * replaced by its bound eq:errbounds1-4:
+ *   Dz_i     = |b_i| Dz_{i-1} + ||A|| e^l_i + e^z_i
+ *   Ds_i     = Dw_i + |b_i| Ds_{i-1} + |b_i w_{i-1}| Dz_{i-1} + ||A|| e^g_i + e^s_i
+ *   Dw_{i+1} = Dw_i + |a_i| Dz_i + ||A|| e^k_{i+1} + e^w_{i+1} + ||A|| e^u_i + e^y_i
+ *   f_{i+1}  = f_i + |a_i| Ds_i + |w_i| Dw_i + |w_i a_i| Dz_i
+ *              + ||A|| e^x_{i+1} + e^r_{i+1} + |w_i| ||A|| e^u_i + e^q_i + |w_i| e^y_i
+ * Initial values: f_0 = ((mu sqrt N + 1)||A|| ||x_0||
+ * + ||b||) eps, Dw_0 = mu sqrt N ||A|| ||k_0|| eps, Ds_{-1} = Dz_{-1} = 0 (g, l, z
+ * at i = -1 are exact zeros, A1).  After a replacement in iteration i the gaps
+ * are those of the explicit recomputation (reading A31): f_{i+1} = ((mu sqrt N
+ * + 1)||A|| ||x_{i+1}|| + ||b||) eps, Ds_i = mu sqrt N ||A|| ||g_i|| eps, Dw_{i+1} =
+ * mu sqrt N ||A|| ||k_{i+1}|| eps, Dz_i = mu sqrt N ||A|| ||l_i|| eps.
+ * Criterion eq:criterion, tau = sqrt(eps): replace in iteration i
+ * (after line 20, A10) iff f_{i-1} <= tau ||r_{i-1}|| and f_i > tau ||r_i||
+ * (decided at the end of iteration i-1; i >= 1).  eps = 2^-53 (A12); ||A|| =
+ * orc_anorm_bound (A29); ||M^-1|| = max |dinv_j|; mu = max nnz per row of A,
+ * mu~ = 1 (Jacobi, A25).  Norms are 2-norms sqrt((v,v)) with Dot2 (A6).
+ * Every vector whose norm enters is stored by this transcription, so the norms
+ * are taken directly from the vectors of the current and previous iteration. */
+typedef struct {
+  double f, f_prev, Dw, Ds, Dz; /* f_i, f_{i-1}, Dw_i, Ds_{i-1}, Dz_{i-1} */
+  double nA, muN, mutN;         /* ||A||, mu sqrt N, mu~ sqrt N ||M^-1|| */
+  double eps, tau;
+} autorr;
+
+static double nrm2(int64_t n, const double* v) { return sqrt(orc_dot2(n, v, v)); }
+
 int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
                   const double* b, const double* x0, double tol, int32_t maxit,
                   int32_t rr_period, int32_t flags, double* x, double* rhist,
                   double* gaphist, int32_t* iters_out, int32_t* outcome_out,
-                  double* sc_trace, double* vec_trace) {
+                  double* sc_trace, double* vec_trace, double* bound_trace,
+                  int32_t* rr_list, int32_t* n_rr) {
   if (n < 0 || maxit < 0 || rr_period < 0) return -2;
   double* dinv = vec(n);
   if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
@@ -198,6 +251,35 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
   rhist[0] = sqrt(dotf(flags, n, r, r));
   if (fgap) gaphist[0] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
   double h0 = rhist[0];
+  /* automated replacement state */
+  const int fauto = (flags & ORC_AUTO_RR) != 0;
+  autorr ar;
+  memset(&ar, 0, sizeof(ar));
+  int rr_next = 0, nrr = 0;
+  if (fauto) {
+    int64_t mu = 0;
+    double mi = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+      if (rp[j + 1] - rp[j] > mu) mu = rp[j + 1] - rp[j];
+      if (fabs(dinv[j]) > mi) mi = fabs(dinv[j]);
+    }
+    ar.eps = ldexp(1.0, -53);
+    ar.tau = sqrt(ar.eps);
+    ar.nA = orc_anorm_bound(n, rp, ci, va);
+    ar.muN = (double)mu * sqrt((double)n);
+    ar.mutN = 1.0 * sqrt((double)n) * mi;
+    ar.f = ((ar.muN + 1.0) * ar.nA * nrm2(n, x) + nb) * ar.eps;
+    ar.f_prev = ar.f;
+    ar.Dw = ar.muN * ar.nA * nrm2(n, k) * ar.eps;
+    ar.Ds = 0.0;
+    ar.Dz = 0.0;
+    if (bound_trace) {
+      bound_trace[0] = ar.f;
+      bound_trace[1] = ar.Dw;
+      bound_trace[2] = NAN;
+      bound_trace[3] = NAN;
+    }
+  }
   int rr_off = 0; /* A12: replacements stop for good once ||r_i|| < sqrt(eps)||r_0|| */
   if (h0 < sqrt_eps * h0) rr_off = 1;
   int32_t iters = 0, outcome = OUT_MAXIT;
@@ -212,6 +294,17 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
       for (int a = 0; a < 6; ++a) memcpy(T + (size_t)a * n, src[a], (size_t)n * sizeof(double));
     }
     if (sc_trace) { sc_trace[4 * i + 0] = alpha; sc_trace[4 * i + 1] = beta; sc_trace[4 * i + 3] = rho; }
+    /* norms of the previous iteration's g, s, l, z, n, v (zero at i = 0, A1;
+     * after a replacement s, l, z are the replaced vectors, n, v are not, A26)
+     * and of this iteration's x, k, w, m, t, for the bound f^r */
+    double nGp = 0, nSp = 0, nLp = 0, nZp = 0, nNp = 0, nVp = 0;
+    double nX = 0, nK = 0, nW = 0, nM = 0, nT = 0;
+    const double om_prev = omega;
+    if (fauto) {
+      nGp = nrm2(n, g); nSp = nrm2(n, s); nLp = nrm2(n, l); nZp = nrm2(n, z);
+      nNp = nrm2(n, nn); nVp = nrm2(n, v);
+      nX = nrm2(n, x); nK = nrm2(n, k); nW = nrm2(n, w); nM = nrm2(n, m); nT = nrm2(n, t);
+    }
     for (int64_t j = 0; j < n; ++j) {
       /* lines 5-8, n_{i-1} and v_{i-1} as stored (A26) */
       g[j] = k[j] + beta * (g[j] - omega * l[j]);
@@ -241,6 +334,37 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     omega = (yy == 0.0) ? 0.0 : qy / yy;
     if (sc_trace) sc_trace[4 * i + 2] = omega;
     if (!isfinite(omega)) { outcome = OUT_BREAKDOWN; iters = i; done = 1; break; }
+    /* bound recursion of iteration i, before x, r, k, w move on */
+    double nG = 0, nS = 0, nL = 0, nZ = 0, nQ = 0, nU = 0, nY = 0, nN = 0, nV = 0;
+    double Dz_i = 0, Ds_i = 0, Dw_1 = 0, f_1 = 0;
+    if (fauto) {
+      nG = nrm2(n, g); nS = nrm2(n, s); nL = nrm2(n, l); nZ = nrm2(n, z);
+      nQ = nrm2(n, q); nU = nrm2(n, u); nY = nrm2(n, y); nN = nrm2(n, nn); nV = nrm2(n, v);
+      const double R = rhist[i];
+      const double ab = fabs(beta), abw = fabs(beta * om_prev);
+      const double aa = fabs(alpha), aw = fabs(omega), awa = fabs(omega * alpha);
+      const double nA = ar.nA, muN = ar.muN, mutN = ar.mutN, e = ar.eps;
+      /* eq:errbounds1-4 without the common factor eps */
+      const double eg = nK + 3.0 * ab * nGp + 4.0 * abw * nLp;
+      const double es = nW + 3.0 * ab * nSp + 4.0 * abw * nZp;
+      const double el = nM + mutN * nW + 3.0 * ab * nLp + 4.0 * abw * nNp + mutN * abw * nZp;
+      const double ez = nT + muN * nA * nM + mutN * nA * nW + 3.0 * ab * nZp + 4.0 * abw * nVp +
+                        muN * nA * abw * nNp + mutN * nA * abw * nZp;
+      const double eq = R + 2.0 * aa * nS;
+      const double eu = nK + 2.0 * aa * nL;
+      const double ey = nW + 2.0 * aa * nZ;
+      const double ex = 2.0 * nX + 3.0 * aa * nG + 2.0 * aw * nU;
+      const double er = nQ + 2.0 * aw * nY;
+      const double ek = nU + 3.0 * aw * nM + mutN * aw * nW + 4.0 * awa * nN + mutN * awa * nZ;
+      const double ew = nY + 3.0 * aw * nT + muN * nA * aw * nM + mutN * nA * aw * nW +
+                        4.0 * awa * nV + muN * nA * awa * nN + mutN * nA * awa * nZ;
+      /* eq:Dz, eq:Ds, eq:Dw, eq:Dr by the triangle inequality */
+      Dz_i = ab * ar.Dz + nA * el * e + ez * e;
+      Ds_i = ar.Dw + ab * ar.Ds + abw * ar.Dz + nA * eg * e + es * e;
+      Dw_1 = ar.Dw + aa * Dz_i + nA * ek * e + ew * e + nA * eu * e + ey * e;
+      f_1 = ar.f + aa * Ds_i + aw * ar.Dw + awa * Dz_i + nA * ex * e + er * e +
+            aw * nA * eu * e + eq * e + aw * ey * e;
+    }
     /* lines 17-20 */
     for (int64_t j = 0; j < n; ++j) {
       x[j] = (x[j] + alpha * g[j]) + omega * u[j];
@@ -251,7 +375,9 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     /* residual replacement after line 20, eq:rr:
      * r := b - A x; k := M^-1 r; w := A k; s := A g; l := M^-1 s; z := A l.
      * Schedule (A11): loop index i replaces when (i+1) mod P_rr == 0. */
-    if (rr_period > 0 && (i + 1) % rr_period == 0 && !rr_off) {
+    const int fire = fauto ? rr_next
+                           : (rr_period > 0 && (i + 1) % rr_period == 0 && !rr_off);
+    if (fire) {
       orc_spmv(n, rp, ci, va, x, tmp);
       for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
       prec(n, dinv, r, k);
@@ -259,6 +385,15 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
       orc_spmv(n, rp, ci, va, g, s);
       prec(n, dinv, s, l);
       orc_spmv(n, rp, ci, va, l, z);
+      if (fauto) {
+        /* gaps of the explicit recomputation (reading A31) */
+        f_1 = ((ar.muN + 1.0) * ar.nA * nrm2(n, x) + nb) * ar.eps;
+        Ds_i = ar.muN * ar.nA * nG * ar.eps;
+        Dw_1 = ar.muN * ar.nA * nrm2(n, k) * ar.eps;
+        Dz_i = ar.muN * ar.nA * nrm2(n, l) * ar.eps;
+        if (rr_list) rr_list[nrr] = i;
+        nrr++;
+      }
     }
     /* line 21: reduction (r0,r), (r0,w), (r0,s), (r0,z); + (r,r) (A8) */
     double rho1 = dotf(flags, n, rh, r);
@@ -271,6 +406,23 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     orc_spmv(n, rp, ci, va, m, t);
     if (fgap) gaphist[i + 1] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
     iters = i + 1;
+    if (fauto) {
+      /* eq:criterion for iteration i+1 */
+      rr_next = (ar.f <= ar.tau * rhist[i]) && (f_1 > ar.tau * rhist[i + 1]);
+      ar.f_prev = ar.f;
+      ar.f = f_1;
+      ar.Dw = Dw_1;
+      ar.Ds = Ds_i;
+      ar.Dz = Dz_i;
+      if (bound_trace) {
+        bound_trace[4 * (i + 1) + 0] = f_1;
+        bound_trace[4 * (i + 1) + 1] = Dw_1;
+        bound_trace[4 * i + 2] = Ds_i;
+        bound_trace[4 * i + 3] = Dz_i;
+        bound_trace[4 * (i + 1) + 2] = NAN;
+        bound_trace[4 * (i + 1) + 3] = NAN;
+      }
+    }
     if (rhist[i + 1] < sqrt_eps * h0) rr_off = 1;
     if (rhist[i + 1] <= tol * nb && !(flags & ORC_BENCH)) { outcome = OUT_CONVERGED; done = 1; break; }
     /* lines 25-26 */
@@ -291,6 +443,7 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
   }
   *iters_out = iters;
   *outcome_out = outcome;
+  if (n_rr) *n_rr = nrr;
   free(dinv); free(r); free(rh); free(k); free(w); free(m); free(t); free(g); free(s);
   free(l); free(z); free(nn); free(v); free(q); free(u); free(y); free(tmp);
   return 0;

@@ -20,6 +20,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 BENCH = 1
 PLAIN_DOT = 2
 GAP = 4
+AUTO_RR = 8
 NTRACE = 15
 TRACE_NAMES = ["x", "r", "k", "w", "m", "t", "g", "s", "l", "z", "q", "u", "y", "n", "v"]
 OUTCOMES = {0: "converged", 1: "maxit", 2: "breakdown"}
@@ -54,7 +55,10 @@ def lib():
         L.orc_stencil_csr.restype = i64
         L.orc_stencil_csr.argtypes = [ctypes.c_int, i64, i64, i64, P, P, P, P]
         L.orc_pbicgstab.restype = ctypes.c_int
-        L.orc_pbicgstab.argtypes = [i64, P, P, P, P, P, f64, i32, i32, i32, P, P, P, P, P, P, P]
+        L.orc_pbicgstab.argtypes = [i64, P, P, P, P, P, f64, i32, i32, i32, P, P, P, P, P, P, P,
+                                    P, P, P]
+        L.orc_anorm_bound.restype = f64
+        L.orc_anorm_bound.argtypes = [i64, P, P, P]
         L.orc_bicgstab.restype = ctypes.c_int
         L.orc_bicgstab.argtypes = [i64, P, P, P, P, P, f64, i32, i32, P, P, P, P, P, P]
         for name in ("orc_pcg", "orc_pipecg"):
@@ -137,10 +141,12 @@ class Result:
     outcome: str
     scalars: np.ndarray | None = None  # [iters, 4]: alpha, beta, omega, rho
     trace: np.ndarray | None = None    # [maxit+1, NTRACE, n]
+    bounds: np.ndarray | None = None   # [iters+1, 4]: f^r_i, Dw_i, Ds_i, Dz_i (auto RR)
+    rr_iters: list | None = None       # iterations i that replaced r_{i+1} (auto RR)
 
 
 def _run(fn, A: CSR, b, x0, tol, maxit, flags, extra=(), want_sc=False, want_trace=False,
-         gap=True):
+         gap=True, want_bounds=False):
     b = _f64(b)
     x0 = np.zeros(A.n) if x0 is None else _f64(x0)
     x = np.zeros(A.n)
@@ -156,23 +162,38 @@ def _run(fn, A: CSR, b, x0, tol, maxit, flags, extra=(), want_sc=False, want_tra
     if fn in ("orc_pbicgstab", "orc_bicgstab"):
         sc = np.full((maxit + 1, 4), np.nan) if want_sc else None
         args.append(_p(sc))
+    bt = rl = None
+    nrr = ctypes.c_int32(0)
     if fn == "orc_pbicgstab":
         tr = np.zeros((maxit + 1, NTRACE, A.n)) if want_trace else None
         args.append(_p(tr))
+        bt = np.full((maxit + 1, 4), np.nan) if want_bounds else None
+        rl = np.zeros(max(maxit, 1), np.int32)
+        args += [_p(bt), _p(rl), ctypes.byref(nrr)]
     rc = getattr(lib(), fn)(*args)
     if rc != 0:
         raise ValueError(f"{fn} failed with code {rc}")
     n_it = it.value
     return Result(x, rh[: n_it + 1], None if gh is None else gh[: n_it + 1], n_it,
-                  OUTCOMES[oc.value], None if sc is None else sc[:n_it + 1], tr)
+                  OUTCOMES[oc.value], None if sc is None else sc[:n_it + 1], tr,
+                  None if bt is None else bt[:n_it + 1],
+                  None if rl is None else [int(v) for v in rl[:nrr.value]])
 
 
 def pbicgstab(A: CSR, b, x0=None, tol=0.0, maxit=100, rr_period=0, bench=False,
-              plain_dot=False, gap=True, want_scalars=False, want_trace=False) -> Result:
-    """Alg. 2 with periodic replacement and gap history."""
-    flags = (BENCH if bench else 0) | (PLAIN_DOT if plain_dot else 0)
+              plain_dot=False, gap=True, want_scalars=False, want_trace=False,
+              auto_rr=False) -> Result:
+    """Alg. 2 with periodic replacement or, with auto_rr, the
+    automated replacement of P:609-623 (bound f^r_i history in .bounds, replacement
+    iterations in .rr_iters), and the gap history."""
+    flags = (BENCH if bench else 0) | (PLAIN_DOT if plain_dot else 0) | (AUTO_RR if auto_rr else 0)
     return _run("orc_pbicgstab", A, b, x0, tol, maxit, flags, extra=(int(rr_period),),
-                want_sc=want_scalars, want_trace=want_trace, gap=gap)
+                want_sc=want_scalars, want_trace=want_trace, gap=gap, want_bounds=auto_rr)
+
+
+def anorm_bound(A: CSR) -> float:
+    """sqrt(||A||_1 ||A||_inf) >= ||A||_2, the ||A|| of the run-time bound (reading A29)."""
+    return lib().orc_anorm_bound(A.n, _p(A.rp), _p(A.ci), _p(A.va))
 
 
 def bicgstab(A: CSR, b, x0=None, tol=0.0, maxit=100, bench=False, plain_dot=False, gap=True,
