@@ -255,6 +255,7 @@ def run_ours(args, rank, world):
     x = torch.empty_like(b)
     S.set_option("bench", 1)
     S.set_option("graphs", 1)
+    S.set_option("overlap", args.overlap)
     gap = bool(args.gap)
 
     def step():
@@ -349,7 +350,8 @@ def run_ours(args, rank, world):
                                "split 4-phase (CSR as ELL), reduction #1 overlapped",
                    "l2": "inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9),
                    "parallelism": f"z-slab x{world}" + (" (NCCL halo + rank-row all-gather)"
-                                                        if world > 1 else "")},
+                                                        if world > 1 else ""),
+                   "overlap": bool(args.overlap) if world > 1 else None},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
@@ -384,6 +386,7 @@ def run_loopback(args):
     bs = G.apply(G.split(xs))
     del xs
     G.set_option("bench", 1)
+    G.set_option("overlap", args.overlap)
     for _ in range(args.warmup):
         G.solve(bs, tol=0.0, maxit=maxit, rr_period=rr, gap=bool(args.gap))
     torch.cuda.synchronize()
@@ -408,6 +411,9 @@ def main():
     ap.add_argument("--method", choices=["pbicgstab", "bicgstab", "pipecg"], default="pbicgstab",
                     help="solver: p-BiCGStab (the headline), classic BiCGStab or p-CG")
     ap.add_argument("--gap", type=int, default=0)
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="P > 1: dot-product reductions overlap the halo exchange / SpMV (1) "
+                         "or block the compute stream (0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-timing", type=int, default=1,
                     help="1: CUDA events around every kernel in the timed region (graphs off); "

@@ -151,6 +151,16 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *   "tile"       1 (default) => stencil sweeps use the TMA-staged 2.5D kernels when
  *                the grid fits (nx <= 2048); 0 => plain line kernels (same results)
  *   "schedule"   0 (default) auto, 1 fused 2-sweep (stencil only), 2 split 4-phase
+ *   "method"     0 (default) p-BiCGStab, Alg. 2; 1 classic preconditioned
+ *                BiCGStab, Alg. 1; 2 preconditioned pipelined CG (the
+ *                paper's p-CG comparison, reconstructed: DESIGN.md A19).
+ *                Methods 1 and 2 need a stencil operator with nx <= 1024 and
+ *                rr_period = 0 (EINVAL otherwise)
+ *   "rr_auto"    1 => automated residual replacement: the run-time bound
+ *                f^r_i on the residual gap (eq:DDr_bound) is propagated on the device
+ *                and iteration i replaces when f_{i-1} <= sqrt(eps)||r_{i-1}|| and
+ *                f_i > sqrt(eps)||r_i|| (eq:criterion).  Needs method 0, a stencil
+ *                operator with nx <= 1024 and rr_period = 0 in pbicgstab_solve
  * Errors: EINVAL for an unknown key or bad value. */
 pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value);
 
@@ -197,6 +207,15 @@ pbicg_status pbicgstab_kernel_time(pbicg_handle h, const char* name, int64_t* la
 /* Algorithmic HBM bytes one launch of kernel `name` must move for this handle's
  * operator; 0 if unknown. */
 pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* bytes);
+
+/* Replacement record of the last solve on h (rank 0's handle for a loopback
+ * group).  fr_hist (host, >= iters+1 doubles, or NULL): f^r_i, i = 0..iters, with
+ * option rr_auto (NaN otherwise).  rr_iters (host, cap ints, or NULL): the
+ * iterations i whose line 20 was followed by a replacement (periodic or
+ * automated), ascending; *n_rr = their number (may exceed cap).
+ * ESTATE before the first solve. */
+pbicg_status pbicgstab_rr_info(pbicg_handle h, double* fr_hist, int32_t* rr_iters, int32_t cap,
+                               int32_t* n_rr);
 
 /* ncclUniqueId blob (128 bytes) for multi-GPU creation; ESTATE without NCCL. */
 pbicg_status pbicgstab_get_unique_id(void* out128);

@@ -391,9 +391,9 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
         Ds_i = ar.muN * ar.nA * nG * ar.eps;
         Dw_1 = ar.muN * ar.nA * nrm2(n, k) * ar.eps;
         Dz_i = ar.muN * ar.nA * nrm2(n, l) * ar.eps;
-        if (rr_list) rr_list[nrr] = i;
-        nrr++;
       }
+      if (rr_list) rr_list[nrr] = i; /* record (periodic or automated) */
+      nrr++;
     }
     /* line 21: reduction (r0,r), (r0,w), (r0,s), (r0,z); + (r,r) (A8) */
     double rho1 = dotf(flags, n, rh, r);

@@ -49,7 +49,8 @@ SYMBOLS = ["pbicgstab_create_stencil", "pbicgstab_create_csr", "pbicgstab_create
            "pbicgstab_create_csr_loopback", "pbicgstab_apply_loopback", "pbicgstab_solve_loopback",
            "pbicgstab_local_rows", "pbicgstab_stencil_partition",
            "pbicgstab_set_option", "pbicgstab_apply", "pbicgstab_solve", "pbicgstab_solve_host",
-           "pbicgstab_kernel_time", "pbicgstab_kernel_bytes", "pbicgstab_get_unique_id",
+           "pbicgstab_kernel_time", "pbicgstab_kernel_bytes", "pbicgstab_rr_info",
+           "pbicgstab_get_unique_id",
            "pbicgstab_last_error", "pbicgstab_destroy"]
 
 _lib = None
@@ -91,6 +92,7 @@ def lib(build: bool = True):
     L.pbicgstab_kernel_time.argtypes = [P, ctypes.c_char_p, ctypes.POINTER(i64),
                                         ctypes.POINTER(f64), i32]
     L.pbicgstab_kernel_bytes.argtypes = [P, ctypes.c_char_p, ctypes.POINTER(f64)]
+    L.pbicgstab_rr_info.argtypes = [P, P, P, i32, ctypes.POINTER(i32)]
     L.pbicgstab_get_unique_id.argtypes = [P]
     L.pbicgstab_last_error.argtypes = [P]
     L.pbicgstab_last_error.restype = ctypes.c_char_p
@@ -239,6 +241,18 @@ class Solver:
             None if gh is None else vp(gh), ctypes.byref(it), ctypes.byref(oc)), self._h)
         k = it.value
         return SolveResult(x, rh[:k + 1], None if gh is None else gh[:k + 1], k, OUTCOMES[oc.value])
+
+    def rr_info(self, iters: int):
+        """(f^r history [iters+1] (NaN without rr_auto), replacement iterations) of the
+        last solve (pbicgstab_rr_info)."""
+        fr = np.full(iters + 1, np.nan)
+        cap = max(iters, 1)
+        rl = np.zeros(cap, np.int32)
+        n = ctypes.c_int32()
+        _check(lib().pbicgstab_rr_info(self._h, fr.ctypes.data_as(ctypes.c_void_p),
+                                       rl.ctypes.data_as(ctypes.c_void_p), cap,
+                                       ctypes.byref(n)), self._h)
+        return fr, [int(v) for v in rl[:min(n.value, cap)]]
 
     def kernel_time(self, name: str = "all", reset: bool = False) -> tuple[int, float]:
         n, ms = ctypes.c_int64(), ctypes.c_double()

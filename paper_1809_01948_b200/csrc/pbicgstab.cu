@@ -93,6 +93,11 @@ struct pbicg_ctx {
   // options
   int bench = 0, use_graphs = 1, timing = 0, overlap = 1, schedule = 0, gap_on = 0;
   int method = M_PBICGSTAB;
+  int auto_rr = 0;                           // option rr_auto
+  double ar_nA = 0, ar_muN = 0, ar_mutN = 0;  // bound constants (reading A29)
+  bool ar_ok = false;                        // constants known for this operator
+  int32_t last_iters = -1;                   // iterations of the last solve
+  int32_t last_nrr = 0;                      // replacements of the last solve
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
   std::vector<TimedLaunch> pending;
   std::vector<cudaEvent_t> ev_pool;
@@ -249,7 +254,8 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
   switch (p) {
     case PH_INIT1: {
       LaunchScope ls(h, K_INIT);
-      if (tile) launch_tile<DIM, TM_INIT1>(h);
+      if (h->auto_rr) launch_tile<DIM, TM_INIT1N>(h);
+      else if (tile) launch_tile<DIM, TM_INIT1>(h);
       else k_init1<DIM><<<h->grid[K_INIT], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_INIT2: {
@@ -259,24 +265,28 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SWEEPA: {
       LaunchScope ls(h, K_SWEEPA);
-      if (tile) launch_tile<DIM, TM_A>(h);
+      if (h->auto_rr) launch_tile<DIM, TM_AN>(h);
+      else if (tile) launch_tile<DIM, TM_A>(h);
       else k_sweepA<DIM><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
                                                                           h->hist);
     } break;
     case PH_SWEEPC: {
       LaunchScope ls(h, K_SWEEPC);
-      if (tile) launch_tile<DIM, TM_C>(h);
+      if (h->auto_rr) launch_tile<DIM, TM_CN>(h);
+      else if (tile) launch_tile<DIM, TM_C>(h);
       else k_sweepC<DIM><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part,
                                                                           h->hist);
     } break;
     case PH_RR1: {
       LaunchScope ls(h, K_RR1);
-      if (tile) launch_tile<DIM, TM_RR1>(h);
+      if (h->auto_rr) launch_tile<DIM, TM_RR1N>(h);
+      else if (tile) launch_tile<DIM, TM_RR1>(h);
       else k_rr1<DIM><<<h->grid[K_RR1], h->block, 0, h->stream>>>(g, h->V, h->scal);
     } break;
     case PH_RR2: {
       LaunchScope ls(h, K_RR2);
-      if (tile) launch_tile<DIM, TM_RR2>(h);
+      if (h->auto_rr) launch_tile<DIM, TM_RR2N>(h);
+      else if (tile) launch_tile<DIM, TM_RR2>(h);
       else k_rr2<DIM><<<h->grid[K_RR2], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_GAP: {
@@ -355,11 +365,25 @@ void launch(pbicg_ctx* h, Phase p) {
 void launch_fin(pbicg_ctx* h, int f) {
   LaunchScope ls(h, K_FIN);
   switch (f) {
-    case F_INIT1: k_fin<F_INIT1, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    // with automated replacement the reductions also carry the bound norms
+    case F_INIT1:
+      if (h->auto_rr) k_fin<F_INIT1, 4><<<1, 32, 0, h->stream>>>(h->scal, h->hist);
+      else k_fin<F_INIT1, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist);
+      break;
     case F_INIT2: k_fin<F_INIT2, 1><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
-    case F_SWEEPA: k_fin<F_SWEEPA, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
-    case F_SWEEPC: k_fin<F_SWEEPC, 5><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
-    case F_RR2: k_fin<F_RR2, 5><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_SWEEPA:
+      if (h->auto_rr) k_fin<F_SWEEPA, 12><<<1, 32, 0, h->stream>>>(h->scal, h->hist);
+      else k_fin<F_SWEEPA, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist);
+      break;
+    case F_SWEEPC:
+      if (h->auto_rr) k_fin<F_SWEEPC, 9><<<1, 32, 0, h->stream>>>(h->scal, h->hist);
+      else k_fin<F_SWEEPC, 5><<<1, 32, 0, h->stream>>>(h->scal, h->hist);
+      break;
+    case F_RR1: k_fin<F_RR1, 4><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
+    case F_RR2:
+      if (h->auto_rr) k_fin<F_RR2, 6><<<1, 32, 0, h->stream>>>(h->scal, h->hist);
+      else k_fin<F_RR2, 5><<<1, 32, 0, h->stream>>>(h->scal, h->hist);
+      break;
     case F_GAP: k_fin<F_GAP, 1><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
     case F_CL1: k_fin<F_CL1, 1><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
     case F_CL2: k_fin<F_CL2, 2><<<1, 32, 0, h->stream>>>(h->scal, h->hist); break;
@@ -433,6 +457,16 @@ void comm_halo(const Members& G, std::initializer_list<VecSel> sels) {
     }
   }
 }
+
+// reduction on the side stream, ordered after everything enqueued so far
+void fork_reduce(const Members& G) {
+  pbicg_ctx* h0 = G[0];
+  cudaEventRecord(h0->ev_fork, h0->stream);
+  cudaStreamWaitEvent(h0->side, h0->ev_fork, 0);
+  comm_reduce(G, true);
+  cudaEventRecord(h0->ev_join, h0->side);
+}
+void join_reduce(const Members& G) { cudaStreamWaitEvent(G[0]->stream, G[0]->ev_join, 0); }
 
 void each(const Members& G, Phase p) {
   for (pbicg_ctx* h : G) launch(h, p);
@@ -551,18 +585,41 @@ void enq_iter(const Members& G, bool with_rr, int par) {
     return;
   }
   if (h0->kind == KIND_STENCIL) {
-    // fused 2-sweep schedule: sweep A (l.5-12) -> omega; sweep C (l.16-21) -> beta, alpha
+    // fused 2-sweep schedule: sweep A (l.5-12) -> omega; sweep C (l.16-21) -> beta, alpha.
+    // P ranks: each reduction runs on the side stream (own communicator) while the
+    // halo of the vector the next sweep reads with its stencil moves on the compute
+    // stream (the exchange the reduction can hide behind)
     each(G, PH_SWEEPA);
     if (dist) {
-      comm_reduce(G, false);
+      const bool ov = h0->overlap != 0;
+      if (ov) {
+        fork_reduce(G);
+      } else {
+        comm_reduce(G, false);
+      }
       comm_halo(G, {par ? SZ1 : SZ0});  // z_i for sweep C's stencil
+      if (ov) join_reduce(G);
       each_fin(G, F_SWEEPA);
     }
     each(G, PH_SWEEPC);
+    if (dist && !with_rr && h0->overlap) {
+      // reduction #2 || halo of w_{i+1} (no replacement can rewrite w this iteration)
+      fork_reduce(G);
+      comm_halo(G, {par ? SW0 : SW1});
+      join_reduce(G);
+      each_fin(G, F_SWEEPC);
+      if (h0->gap_on) {
+        comm_halo(G, {SX});
+        each(G, PH_GAP);
+        reduce_fin(G, F_GAP);
+      }
+      return;
+    }
     reduce_fin(G, F_SWEEPC);
     if (with_rr) {  // eq:rr after line 20
       if (dist) comm_halo(G, {SX, SG});
       each(G, PH_RR1);
+      if (h0->auto_rr) reduce_fin(G, F_RR1);  // norms of the replaced vectors
       if (dist) comm_halo(G, {SR, SS});
       each(G, PH_RR2);
       reduce_fin(G, F_RR2);
@@ -606,7 +663,10 @@ void enq_iter(const Members& G, bool with_rr, int par) {
 // chunk of L iterations starting at a multiple of L (L even, multiple of P when
 // P > 0): offset o replaces iff P > 0 && (o+1) % P == 0.
 void enq_chunk(const Members& G, int L, int P) {
-  for (int o = 0; o < L; ++o) enq_iter(G, P > 0 && ((o + 1) % P) == 0, o & 1);
+  // automated replacement: decided on the device, so every iteration carries the
+  // (early-exiting) replacement kernels
+  const bool every = G[0]->auto_rr != 0;
+  for (int o = 0; o < L; ++o) enq_iter(G, every || (P > 0 && ((o + 1) % P) == 0), o & 1);
 }
 
 void destroy_graphs(pbicg_ctx* h) {
@@ -624,7 +684,7 @@ pbicg_status run_chunk(const Members& G, int L, int P) {
   }
   std::vector<std::vector<int64_t>> before;
   for (pbicg_ctx* m : G) before.emplace_back(m->launches, m->launches + K_N);
-  auto key = std::make_tuple(L, P, h->gap_on);
+  auto key = std::make_tuple(L, P, h->gap_on * 2 + h->auto_rr);
   auto it = h->graphs.find(key);
   // the enqueue pass below (capture or, for cached graphs, counted separately)
   // establishes how many launches one replay contains
@@ -653,11 +713,15 @@ pbicg_status ensure_hist(pbicg_ctx* h, int64_t need) {
   if (need <= h->hist_cap) return PBICG_OK;
   destroy_graphs(h);  // graphs captured the old pointers
   int64_t cap = need < 1024 ? 1024 : need;
-  void *a = nullptr, *b = nullptr;
+  void *a = nullptr, *b = nullptr, *c = nullptr, *d = nullptr;
   ST(dalloc(h, &a, (size_t)cap * sizeof(double)));
   ST(dalloc(h, &b, (size_t)cap * sizeof(double)));
+  ST(dalloc(h, &c, (size_t)cap * sizeof(double)));
+  ST(dalloc(h, &d, (size_t)cap * sizeof(int32_t)));
   h->hist.rnorm = (double*)a;
   h->hist.gap = (double*)b;
+  h->hist.fr = (double*)c;
+  h->hist.rrl = (int32_t*)d;
   h->hist_cap = cap;
   return PBICG_OK;
 }
@@ -692,6 +756,11 @@ cudaError_t set_tile_attrs(pbicg_ctx* h) {
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_PC>(h);
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_PCI1>(h);
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_PCI2>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_AN>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_CN>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_RR1N>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_RR2N>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_INIT1N>(h);
   return e;
 }
 
@@ -805,7 +874,7 @@ pbicg_status alloc_common(pbicg_ctx* h) {
   int gmax = h->num_sm;
   for (int k = 0; k < K_N; ++k) gmax = h->grid[k] > gmax ? h->grid[k] : gmax;
   void* p = nullptr;
-  ST(dalloc(h, &p, (size_t)gmax * 8 * sizeof(Dd)));
+  ST(dalloc(h, &p, (size_t)gmax * RED_K * sizeof(Dd)));  // K <= RED_K partials per CTA
   h->part = (Dd*)p;
   ST(ensure_hist(h, 1024));
   // rank fields of the device state (kept across solves)
@@ -873,8 +942,70 @@ void slab(int64_t outer, int nranks, int rank, int64_t* o0, int64_t* nol) {
   *o0 = rank * base + (rank < rem ? rank : rem);
 }
 
+// Constants of the automated-replacement bound for a stencil (reading A29):
+// ||A|| <= sqrt(||A||_1 ||A||_inf) with the row sums in ascending column order
+// (legs -z,-y,-x,c,+x,+y,+z) and the column sums in ascending row order (the
+// rows j-pxy, j-nx, j-1, j, j+1, j+nx, j+pxy contribute c[6], c[4], c[2], c[0],
+// c[1], c[3], c[5]), maximised over the leg patterns that occur (first, second
+// and last point of every dimension); mu = max legs per row.  Bitwise the same
+// doubles as oracle.c's orc_anorm_bound on the written-out matrix.
+void stencil_bound_consts(pbicg_ctx* h, const pbicg_stencil* op) {
+  const int dim = op->dim;
+  const int64_t n3[3] = {op->nx, op->ny, dim == 3 ? op->nz : 1};
+  const double* c = op->coef;
+  const int cm[3] = {1, 3, 5}, cp[3] = {2, 4, 6};  // -d / +d coefficient index
+  double rmax = 0.0, cmax = 0.0;
+  int64_t mu = 0;
+  int64_t pos[3][3];
+  int npos[3];
+  for (int d = 0; d < 3; ++d) {
+    npos[d] = 0;
+    const int64_t cand[3] = {0, 1, n3[d] - 1};
+    for (int q = 0; q < 3; ++q) {
+      if (cand[q] < 0 || cand[q] >= n3[d]) continue;
+      bool dup = false;
+      for (int u = 0; u < npos[d]; ++u) dup |= pos[d][u] == cand[q];
+      if (!dup) pos[d][npos[d]++] = cand[q];
+    }
+  }
+  for (int a = 0; a < npos[0]; ++a)
+    for (int b = 0; b < npos[1]; ++b)
+      for (int e = 0; e < npos[2]; ++e) {
+        const int64_t p[3] = {pos[0][a], pos[1][b], pos[2][e]};
+        bool lo[3], hi[3];
+        for (int d = 0; d < 3; ++d) {
+          lo[d] = d < dim && p[d] > 0;
+          hi[d] = d < dim && p[d] < n3[d] - 1;
+        }
+        // row: -z, -y, -x, c, +x, +y, +z
+        double rs = 0.0;
+        int64_t cnt = 1;
+        for (int d = 2; d >= 0; --d)
+          if (lo[d]) { rs = rs + std::fabs(c[cm[d]]); cnt++; }
+        rs = rs + std::fabs(c[0]);
+        for (int d = 0; d < 3; ++d)
+          if (hi[d]) { rs = rs + std::fabs(c[cp[d]]); cnt++; }
+        // column j: rows j-pxy (+z leg), j-nx (+y), j-1 (+x), j, j+1 (-x), j+nx (-y), j+pxy (-z)
+        double cs = 0.0;
+        for (int d = 2; d >= 0; --d)
+          if (lo[d]) cs = cs + std::fabs(c[cp[d]]);
+        cs = cs + std::fabs(c[0]);
+        for (int d = 0; d < 3; ++d)
+          if (hi[d]) cs = cs + std::fabs(c[cm[d]]);
+        if (rs > rmax) rmax = rs;
+        if (cs > cmax) cmax = cs;
+        if (cnt > mu) mu = cnt;
+      }
+  const double n = (double)(n3[0] * n3[1] * n3[2]);
+  h->ar_nA = std::sqrt(cmax * rmax);
+  h->ar_muN = (double)mu * std::sqrt(n);
+  h->ar_mutN = 1.0 * std::sqrt(n) * std::fabs(1.0 / c[0]);
+  h->ar_ok = true;
+}
+
 pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op) {
   h->kind = KIND_STENCIL;
+  stencil_bound_consts(h, op);
   h->dim = op->dim;
   const int64_t nz = op->dim == 3 ? op->nz : 1;
   Geo& g = h->geo;
@@ -1101,6 +1232,8 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
     return fail(h, PBICG_EINVAL, "maxit, rr_period and tol must be >= 0");
   if (h->method != M_PBICGSTAB && rr_period != 0)
     return fail(h, PBICG_EINVAL, "residual replacement is defined for p-BiCGStab only (method 0)");
+  if (h->auto_rr && rr_period != 0)
+    return fail(h, PBICG_EINVAL, "rr_period must be 0 with automated replacement (rr_auto)");
   for (size_t r = 0; r < G.size(); ++r) {
     if (!io[r].b || !io[r].x0 || !io[r].x) return fail(h, PBICG_EINVAL, "NULL vector argument");
     ST(ensure_hist(G[r], (int64_t)maxit + 1));
@@ -1125,6 +1258,12 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
     s0.bench = m->bench;
     s0.rr_period = rr_period;
     s0.method = m->method;
+    s0.auto_rr = m->auto_rr;
+    s0.ar_nA = m->ar_nA;
+    s0.ar_muN = m->ar_muN;
+    s0.ar_mutN = m->ar_mutN;
+    s0.ar_eps = std::ldexp(1.0, -53);
+    s0.ar_tau = std::sqrt(s0.ar_eps);
     s0.nranks = m->nranks;
     s0.rank = m->rank;
     s0.red_send = m->red_send;
@@ -1184,6 +1323,8 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
     if (m->timing) collect_timing(m);
   *iters_out = iters;
   *outcome_out = S.done ? S.outcome : OUT_MAXIT;
+  for (pbicg_ctx* m : G) m->last_iters = iters;
+  h->last_nrr = S.n_rr;
   return PBICG_OK;
 }
 
@@ -1381,7 +1522,17 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
     } else if (k == "tile") {
       m->tile_on = value != 0;
       destroy_graphs(m);
+    } else if (k == "rr_auto") {
+      if (value != 0 && (m->kind != KIND_STENCIL || !m->tile_ok || !m->ar_ok ||
+                         m->method != M_PBICGSTAB))
+        return fail(h, PBICG_EINVAL,
+                    "rr_auto needs method 0 on a stencil operator with nx <= 1024 (TMA tile "
+                    "kernels)");
+      m->auto_rr = value != 0;
+      destroy_graphs(m);
     } else if (k == "method") {
+      if (value != M_PBICGSTAB && m->auto_rr)
+        return fail(h, PBICG_EINVAL, "switch rr_auto off before selecting method 1 or 2");
       if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "method must be 0, 1 or 2");
       if (value != M_PBICGSTAB && (m->kind != KIND_STENCIL || !m->tile_ok))
         return fail(h, PBICG_EINVAL,
@@ -1558,6 +1709,29 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "iteration") b = 2 * mat + 36 * 8 * N;
   }
   *bytes = b;
+  return PBICG_OK;
+}
+
+pbicg_status pbicgstab_rr_info(pbicg_handle h, double* fr_hist, int32_t* rr_iters, int32_t cap,
+                               int32_t* n_rr) {
+  if (!h || !n_rr || cap < 0) return fail(h, PBICG_EINVAL, "NULL argument");
+  if (h->last_iters < 0) return fail(h, PBICG_ESTATE, "no solve has completed on this handle");
+  if (h->comm == COMM_LOOP && h->group && h->group->m[0] != h)
+    return fail(h, PBICG_EINVAL, "loopback group: ask rank 0's handle");
+  const int32_t n = h->last_nrr;
+  *n_rr = n;
+  if (fr_hist) {
+    if (h->auto_rr) {
+      CU(cudaMemcpy(fr_hist, h->hist.fr, (size_t)(h->last_iters + 1) * sizeof(double),
+                    cudaMemcpyDeviceToHost));
+    } else {
+      for (int32_t i = 0; i <= h->last_iters; ++i) fr_hist[i] = NAN;
+    }
+  }
+  if (rr_iters && n > 0) {
+    const int32_t c = n < cap ? n : cap;
+    CU(cudaMemcpy(rr_iters, h->hist.rrl, (size_t)c * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  }
   return PBICG_OK;
 }
 

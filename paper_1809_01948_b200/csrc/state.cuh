@@ -18,7 +18,7 @@
 #define OUT_CONVERGED 0
 #define OUT_MAXIT 1
 #define OUT_BREAKDOWN 2
-#define RED_K 8  // dot slots per rank in the reduction buffers
+#define RED_K 16  // dot slots per rank in the reduction buffers
 
 struct Scal {
   double alpha, beta, omega, rho;  // alpha_i, beta_i, omega (latest), (r0, r_i)
@@ -34,6 +34,19 @@ struct Scal {
   int32_t bench, rr_period;
   int32_t method;                  // 0 p-BiCGStab (Alg. 2), 1 BiCGStab (Alg. 1), 2 p-CG
   double g_old, a_old;             // p-CG: gamma_{i-1}, alpha_{i-1}
+  // automated residual replacement (oracle.c orc_pbicgstab, ORC_AUTO_RR)
+  int32_t auto_rr;                 // option rr_auto
+  int32_t rr_next;                 // eq:criterion decided for the next iteration
+  int32_t n_rr;                    // replacements so far (Hist.rrl)
+  double ar_nA, ar_muN, ar_mutN;   // ||A|| bound (A29), mu sqrt N, mu~ sqrt N ||M^-1||
+  double ar_eps, ar_tau;           // 2^-53, sqrt(eps)
+  double ar_f, ar_Dw, ar_Ds, ar_Dz; // f_i, Dw_i, Ds_{i-1}, Dz_{i-1}
+  double ar_omp;                   // omega_{i-1} (0 at i = 0, A1)
+  double nA_[10];                  // sweep A norms: k, w, m, t, g, s, l, z, q, y (iteration i)
+  double nC_[4];                   // sweep C norms: x_i, u_i, n_i, v_i
+  double nR_[4];                   // rr1 norms: x_{i+1}, k_{i+1}, s_i, l_i (replaced)
+  double nP_[6];                   // previous iteration: g, s, l, z, n, v
+  double nX0, nK0;                 // init: ||x_0||, ||k_0||
   int32_t nranks, rank;
   Dd* red_send;                    // [nranks][RED_K]: only row `rank` is ever written
   Dd* red_recv;                    // [nranks][RED_K]: all rows after the exchange
@@ -41,16 +54,83 @@ struct Scal {
 };
 
 enum TicketSlot { T_INIT1 = 0, T_INIT2, T_SWEEPA, T_SWEEPC, T_RR2, T_GAP, T_APPLY, T_MISC,
-                  T_CL1, T_CL2, T_CL3, T_PC, T_PCI1, T_PCI2 };
+                  T_CL1, T_CL2, T_CL3, T_PC, T_PCI1, T_PCI2, T_RR1 };
 
 // which scalar-forming step a reduction feeds
 enum FinKind { F_INIT1 = 0, F_INIT2, F_SWEEPA, F_SWEEPC, F_RR2, F_GAP,
-               F_CL1, F_CL2, F_CL3, F_PINIT2, F_PC };
+               F_CL1, F_CL2, F_CL3, F_PINIT2, F_PC, F_RR1 };
 
 struct Hist {
   double* rnorm;  // [maxit+1]
   double* gap;    // [maxit+1]
+  double* fr;     // [maxit+1] run-time gap bound f^r_i (automated replacement)
+  int32_t* rrl;   // [maxit] iterations i that replaced r_{i+1}
 };
+
+// ---------------------------------------------------------------------------
+// Automated replacement bookkeeping, one thread, same formulas and
+// operation order as oracle.c (the norms are the kernels' sums of squares, so
+// f^r agrees with the oracle to rounding, not bitwise; reading A30).
+__device__ __forceinline__ void auto_step(Scal* s, Hist h, double R1) {
+  const int i = s->iter;
+  const double R = h.rnorm[i];
+  const double nK = s->nA_[0], nW = s->nA_[1], nM = s->nA_[2], nT = s->nA_[3];
+  const double nG = s->nA_[4], nS = s->nA_[5], nL = s->nA_[6], nZ = s->nA_[7];
+  const double nQ = s->nA_[8], nY = s->nA_[9];
+  const double nX = s->nC_[0], nU = s->nC_[1], nN = s->nC_[2], nV = s->nC_[3];
+  const double nGp = s->nP_[0], nSp = s->nP_[1], nLp = s->nP_[2], nZp = s->nP_[3];
+  const double nNp = s->nP_[4], nVp = s->nP_[5];
+  const double alpha = s->alpha, beta = s->beta, omega = s->omega, om_prev = s->ar_omp;
+  const double ab = fabs(beta), abw = fabs(beta * om_prev);
+  const double aa = fabs(alpha), aw = fabs(omega), awa = fabs(omega * alpha);
+  const double nA = s->ar_nA, muN = s->ar_muN, mutN = s->ar_mutN, e = s->ar_eps;
+  const double eg = nK + 3.0 * ab * nGp + 4.0 * abw * nLp;
+  const double es = nW + 3.0 * ab * nSp + 4.0 * abw * nZp;
+  const double el = nM + mutN * nW + 3.0 * ab * nLp + 4.0 * abw * nNp + mutN * abw * nZp;
+  const double ez = nT + muN * nA * nM + mutN * nA * nW + 3.0 * ab * nZp + 4.0 * abw * nVp +
+                    muN * nA * abw * nNp + mutN * nA * abw * nZp;
+  const double eq = R + 2.0 * aa * nS;
+  const double eu = nK + 2.0 * aa * nL;
+  const double ey = nW + 2.0 * aa * nZ;
+  const double ex = 2.0 * nX + 3.0 * aa * nG + 2.0 * aw * nU;
+  const double er = nQ + 2.0 * aw * nY;
+  const double ek = nU + 3.0 * aw * nM + mutN * aw * nW + 4.0 * awa * nN + mutN * awa * nZ;
+  const double ew = nY + 3.0 * aw * nT + muN * nA * aw * nM + mutN * nA * aw * nW +
+                    4.0 * awa * nV + muN * nA * awa * nN + mutN * nA * awa * nZ;
+  const double Dz_i = ab * s->ar_Dz + nA * el * e + ez * e;
+  const double Ds_i = s->ar_Dw + ab * s->ar_Ds + abw * s->ar_Dz + nA * eg * e + es * e;
+  const double Dw_1 = s->ar_Dw + aa * Dz_i + nA * ek * e + ew * e + nA * eu * e + ey * e;
+  const double f_1 = s->ar_f + aa * Ds_i + aw * s->ar_Dw + awa * Dz_i + nA * ex * e + er * e +
+                     aw * nA * eu * e + eq * e + aw * ey * e;
+  s->rr_next = (s->ar_f <= s->ar_tau * R) && (f_1 > s->ar_tau * R1);  // eq:criterion
+  s->ar_f = f_1;
+  s->ar_Dw = Dw_1;
+  s->ar_Ds = Ds_i;
+  s->ar_Dz = Dz_i;
+  h.fr[i + 1] = f_1;
+  s->nP_[0] = nG; s->nP_[1] = nS; s->nP_[2] = nL; s->nP_[3] = nZ;
+  s->nP_[4] = nN; s->nP_[5] = nV;
+}
+
+// after a replacement in iteration i: the gaps of the explicit recomputation
+// (reading A31); nZr = ||z_i|| replaced (rr2)
+__device__ __forceinline__ void auto_reset(Scal* s, Hist h, double R1, double nZr) {
+  const int i = s->iter;
+  const double R = h.rnorm[i];
+  const double nA = s->ar_nA, muN = s->ar_muN, e = s->ar_eps;
+  const double f_1 = ((muN + 1.0) * nA * s->nR_[0] + s->nb) * e;
+  const double Ds_i = muN * nA * s->nA_[4] * e;
+  const double Dw_1 = muN * nA * s->nR_[1] * e;
+  const double Dz_i = muN * nA * s->nR_[3] * e;
+  s->rr_next = (s->ar_f <= s->ar_tau * R) && (f_1 > s->ar_tau * R1);
+  s->ar_f = f_1;
+  s->ar_Dw = Dw_1;
+  s->ar_Ds = Ds_i;
+  s->ar_Dz = Dz_i;
+  h.fr[i + 1] = f_1;
+  s->nP_[0] = s->nA_[4]; s->nP_[1] = s->nR_[2]; s->nP_[2] = s->nR_[3]; s->nP_[3] = nZr;
+  s->nP_[4] = s->nC_[2]; s->nP_[5] = s->nC_[3];
+}
 
 // Line 21-26 bookkeeping once the five dots of reduction #2 are
 // known: history, sqrt(eps) latch (A12), stop test (A7), beta_{i+1},
@@ -76,6 +156,7 @@ __device__ __forceinline__ void finalize_iteration(Scal* s, Hist h, double rho1,
   s->beta = beta1;
   s->alpha = alpha1;
   s->rho = rho1;
+  s->ar_omp = omega;  // omega_i is omega_{(i+1)-1} of the next auto_step
   if (!isfinite(beta1) || !isfinite(alpha1) || den == 0.0 || rho1 == 0.0) {
     s->done = 1;
     s->outcome = OUT_BREAKDOWN;
@@ -84,6 +165,7 @@ __device__ __forceinline__ void finalize_iteration(Scal* s, Hist h, double rho1,
 
 // Replacement decision for iteration i (A11: (i+1) mod P == 0; A12 latch).
 __device__ __forceinline__ bool rr_scheduled(const Scal* s) {
+  if (s->auto_rr) return s->rr_next != 0;  // eq:criterion
   return s->rr_period > 0 && ((s->iter + 1) % s->rr_period) == 0 && !s->rr_off;
 }
 
@@ -93,6 +175,10 @@ __device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot) {
   if (F == F_INIT1) {
     sc->tmp0 = dd_round(tot[0]);  // (r0, r0) = (r^0, r0) = rho_0
     sc->tmp1 = dd_round(tot[1]);  // (b, b)
+    if (sc->auto_rr) {            // ||x_0||, ||k_0|| for f_0, Dw_0
+      sc->nX0 = sqrt(dd_round(tot[2]));
+      sc->nK0 = sqrt(dd_round(tot[3]));
+    }
     if (sc->method != 0) {
       // Alg. 1 lines 2-3 / p-CG init: rho_0 := (r^0, r0) = (r0, r0) (r^0 := r0,
       // A2); ||r0||, ||b||, stop test (A7); beta, omega := 0 (line 17 with p_{-1} = 0)
@@ -194,6 +280,16 @@ __device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot) {
     sc->nb = sqrt(sc->tmp1);
     sc->tol_abs = sc->tol * sc->nb;
     h.rnorm[0] = sc->h0;
+    if (sc->auto_rr) {  // initial gap bounds; Ds_{-1} = Dz_{-1} = 0 (A1)
+      sc->ar_f = ((sc->ar_muN + 1.0) * sc->ar_nA * sc->nX0 + sc->nb) * sc->ar_eps;
+      sc->ar_Dw = sc->ar_muN * sc->ar_nA * sc->nK0 * sc->ar_eps;
+      sc->ar_Ds = 0.0;
+      sc->ar_Dz = 0.0;
+      sc->ar_omp = 0.0;
+      for (int k = 0; k < 6; ++k) sc->nP_[k] = 0.0;
+      sc->rr_next = 0;
+      h.fr[0] = sc->ar_f;
+    }
     if (sc->h0 <= sc->tol_abs && !sc->bench) {
       sc->done = 1;
       sc->outcome = OUT_CONVERGED;
@@ -207,19 +303,28 @@ __device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot) {
     const double omn = (yy == 0.0) ? 0.0 : qy / yy;
     sc->omega = omn;
     sc->use_rr = 0;
+    if (sc->auto_rr)
+      for (int k = 0; k < 10; ++k) sc->nA_[k] = sqrt(dd_round(tot[2 + k]));
     if (!isfinite(omn)) {
       sc->done = 1;
       sc->outcome = OUT_BREAKDOWN;
       sc->iters = sc->iter;
     }
   } else if (F == F_SWEEPC) {
+    if (sc->auto_rr)
+      for (int k = 0; k < 4; ++k) sc->nC_[k] = sqrt(dd_round(tot[5 + k]));
     if (rr_scheduled(sc)) {
       sc->rr_fire = 1;  // the line-21 dots are recomputed after the replacement
+      h.rrl[sc->n_rr++] = sc->iter;
     } else {
+      if (sc->auto_rr) auto_step(sc, h, sqrt(dd_round(tot[4])));
       finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
                          dd_round(tot[3]), dd_round(tot[4]));
     }
+  } else if (F == F_RR1) {  // norms of the replaced x_{i+1}, k_{i+1}, s_i, l_i
+    for (int k = 0; k < 4; ++k) sc->nR_[k] = sqrt(dd_round(tot[k]));
   } else if (F == F_RR2) {
+    if (sc->auto_rr) auto_reset(sc, h, sqrt(dd_round(tot[4])), sqrt(dd_round(tot[5])));
     finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
                        dd_round(tot[3]), dd_round(tot[4]));
     sc->use_rr = 1;
@@ -248,7 +353,7 @@ __global__ void k_fin(Scal* __restrict__ sc, Hist h) {
   if (threadIdx.x != 0) return;
   if (F == F_GAP) {
     if (sc->gap_iter >= sc->iter) return;
-  } else if (F == F_RR2) {
+  } else if (F == F_RR2 || F == F_RR1) {
     if (sc->done || !sc->rr_fire) return;
   } else if (F != F_INIT1 && F != F_INIT2) {
     if (sc->done) return;

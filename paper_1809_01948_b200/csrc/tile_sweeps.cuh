@@ -42,7 +42,17 @@
 #define TNT 512  // threads per CTA
 
 enum TileMode { TM_A = 0, TM_C, TM_RR1, TM_RR2, TM_GAP, TM_INIT1, TM_INIT2,
-                TM_CL1, TM_CL2, TM_CL3, TM_PC, TM_PCI1, TM_PCI2, TM_N };
+                TM_CL1, TM_CL2, TM_CL3, TM_PC, TM_PCI1, TM_PCI2,
+                // the same steps plus the vector norms of the automated-replacement
+                // bound f^r: sums of squares ride the step's reduction
+                TM_AN, TM_CN, TM_RR1N, TM_RR2N, TM_INIT1N, TM_N };
+
+template <int M> struct BaseOf { enum { v = M }; };
+template <> struct BaseOf<TM_AN> { enum { v = TM_A }; };
+template <> struct BaseOf<TM_CN> { enum { v = TM_C }; };
+template <> struct BaseOf<TM_RR1N> { enum { v = TM_RR1 }; };
+template <> struct BaseOf<TM_RR2N> { enum { v = TM_RR2 }; };
+template <> struct BaseOf<TM_INIT1N> { enum { v = TM_INIT1 }; };
 
 // per mode: staged stencil vectors (NSV), whether they form ONE derived operand
 // (DER), whether the operand enters as A M^-1 v (PREC) or A v, the maximum number
@@ -61,6 +71,16 @@ template <> struct TileTraits<TM_CL3> { enum { NSV = 2, DER = 1, PREC = 1, NSTR 
 template <> struct TileTraits<TM_PC> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 7, NOUT = 8, K = 3 }; };
 template <> struct TileTraits<TM_PCI1> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 1, NOUT = 2, K = 2 }; };
 template <> struct TileTraits<TM_PCI2> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 2 }; };
+// + norms: A: k, w, m, t, g, s, l, z, q, y; C: x, u, n, v; RR1: x, k, s, l; RR2: z;
+// INIT1: x0, k0
+template <> struct TileTraits<TM_AN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 6, NOUT = 4, K = 12 }; };
+template <> struct TileTraits<TM_CN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 7, NOUT = 4, K = 9 }; };
+template <> struct TileTraits<TM_RR1N> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 4 }; };
+template <> struct TileTraits<TM_RR2N> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 6 }; };
+template <> struct TileTraits<TM_INIT1N> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 1, NOUT = 3, K = 4 }; };
+
+// sum of squares for a bound norm (plain fp64 per thread; reading A30)
+__device__ __forceinline__ void nrm_add(Dd& a, double v) { a.hi = a.hi + v * v; }
 
 struct TileGeo {
   int64_t nx, ny;     // x extent; lines per plane (3D: ny, 2D: 1)
@@ -236,7 +256,7 @@ __device__ __forceinline__ void stencil_pair_der(const TileGeo& g, int nx, const
 
 // Per-row arithmetic of each mode.  S = stream slot at this row, st = stride;
 // c0/c1 = the stencil operands' centre values, t0/t1 = their stencil products.
-template <int MODE, int K, int NOUTC>
+template <int MODE, int K, int NOUTC, bool NRM>
 __device__ __forceinline__ void row_update(const double* S, int st, bool rr, double c0, double c1,
                                            double t0, double t1, double al, double be, double om,
                                            double dinv, Dd* acc, double* o) {
@@ -253,6 +273,12 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, dou
     const double yy = c0 - al * o[3];          // line 11
     dd_fma(acc[0], qq, yy);                    // line 12
     dd_fma(acc[1 % K], yy, yy);
+    if (NRM) {
+      nrm_add(acc[2 % K], kj); nrm_add(acc[3 % K], c0); nrm_add(acc[4 % K], m);
+      nrm_add(acc[5 % K], t0); nrm_add(acc[6 % K], o[0]); nrm_add(acc[7 % K], o[1]);
+      nrm_add(acc[8 % K], o[2]); nrm_add(acc[9 % K], o[3]); nrm_add(acc[10 % K], qq);
+      nrm_add(acc[11 % K], yy);
+    }
   } else if (MODE == TM_C) {  // c0 = w_i, c1 = z_i; t0 = t_i, t1 = v_i
     const double xj = S[0], gj = S[st], kj = S[2 * st], lj = S[3 * st], rj = S[4 * st];
     const double sj = S[5 * st], rhj = S[6 * st];
@@ -270,12 +296,20 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, dou
     dd_fma(acc[2 % K], rhj, sj);
     dd_fma(acc[3 % K], rhj, c1);
     dd_fma(acc[4 % K], o[1], o[1]);
+    if (NRM) {
+      nrm_add(acc[5 % K], xj); nrm_add(acc[6 % K], uu); nrm_add(acc[7 % K], nn);
+      nrm_add(acc[8 % K], t1);
+    }
   } else if (MODE == TM_RR1) {  // c = x, g; t0 = A x, t1 = A g
     const double rj = S[0] - t0;               // r := b - A x
     o[0] = rj;
     o[1] = dinv * rj;                          // k := M^-1 r
     o[2] = t1;                                 // s := A g
     o[3] = dinv * t1;                          // l := M^-1 s
+    if (NRM) {
+      nrm_add(acc[0], c0); nrm_add(acc[1 % K], o[1]); nrm_add(acc[2 % K], o[2]);
+      nrm_add(acc[3 % K], o[3]);
+    }
   } else if (MODE == TM_RR2) {  // c = r, s; t0 = A M^-1 r = A k, t1 = A M^-1 s = A l
     const double rhj = S[0];
     o[0] = t0;                                 // w := A k
@@ -285,6 +319,7 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, dou
     dd_fma(acc[2 % K], rhj, c1);
     dd_fma(acc[3 % K], rhj, t1);
     dd_fma(acc[4 % K], c0, c0);
+    if (NRM) nrm_add(acc[5 % K], t1);
   } else if (MODE == TM_GAP) {  // c = x; t0 = A x
     const double dg = (S[0] - t0) - S[st];     // (b - A x) - r
     dd_fma(acc[0], dg, dg);
@@ -296,6 +331,10 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, dou
     o[2] = dinv * rj;                          // k0 := M^-1 r0
     dd_fma(acc[0], rj, rj);
     dd_fma(acc[1 % K], bj, bj);
+    if (NRM) {
+      nrm_add(acc[2 % K], c0);
+      nrm_add(acc[3 % K], o[2]);
+    }
   } else if (MODE == TM_INIT2) {  // c = r0; t0 = A M^-1 r0 = A k0
     o[0] = t0;                                 // w0
     dd_fma(acc[0], S[0], t0);                  // (r^, w0)
@@ -349,10 +388,12 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, dou
 // Generic tile kernel.  VEC: every staged range and every vector is 16-byte
 // aligned (nx even) -> paired loads and stores.  One row pair per thread:
 // TP <= 2 * TNT.
-template <int DIM, int MODE, bool VEC>
+template <int DIM, int MODE_, bool VEC>
 __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
                                                  Dd* __restrict__ part, Hist h) {
-  using T = TileTraits<MODE>;
+  using T = TileTraits<MODE_>;
+  constexpr int MODE = BaseOf<MODE_>::v;
+  constexpr bool NRM = MODE_ != MODE;
   constexpr int NSV = T::NSV, NST = T::NSTR;
   constexpr int NSTR_MAX = NST > 0 ? NST : 1;  // array extent
   constexpr bool HAS_STR = NST > 0;
@@ -361,6 +402,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   constexpr int NOUT = T::NOUT > 0 ? T::NOUT : 1;
   constexpr int K = T::K > 0 ? T::K : 1;
   constexpr bool PREC = T::PREC != 0;
+  static_assert(K <= RED_K, "partials buffer holds RED_K pairs per CTA");
   if (MODE == TM_A || MODE == TM_C || MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3 ||
       MODE == TM_PC) {
     if (sc->done) return;
@@ -594,10 +636,10 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       double o0[NOUT], o1[NOUT];
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) o0[k] = o1[k] = 0.0;
-      row_update<MODE, K, NOUT>(S0, sts, rr, c[0][0], c[1][0], t[0][0], t[1][0], al, be, om,
+      row_update<MODE, K, NOUT, NRM>(S0, sts, rr, c[0][0], c[1][0], t[0][0], t[1][0], al, be, om,
                                 g.dinv, acc, o0);
       if (valid1)
-        row_update<MODE, K, NOUT>(HAS_STR ? S0 + 1 : nullptr, sts, rr, c[0][1], c[1][1], t[0][1],
+        row_update<MODE, K, NOUT, NRM>(HAS_STR ? S0 + 1 : nullptr, sts, rr, c[0][1], c[1][1], t[0][1],
                                   t[1][1], al, be, om, g.dinv, acc, o1);
       const int64_t gi = z * g.pxy + toff + r;
       if (T::NOUT > 0) {
@@ -614,7 +656,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     const int slot = MODE == TM_A ? T_SWEEPA : MODE == TM_C ? T_SWEEPC : MODE == TM_RR2 ? T_RR2
                    : MODE == TM_GAP ? T_GAP : MODE == TM_INIT1 ? T_INIT1 : MODE == TM_INIT2 ? T_INIT2
                    : MODE == TM_CL1 ? T_CL1 : MODE == TM_CL2 ? T_CL2 : MODE == TM_CL3 ? T_CL3
-                   : MODE == TM_PC ? T_PC : MODE == TM_PCI1 ? T_PCI1 : T_PCI2;
+                   : MODE == TM_PC ? T_PC : MODE == TM_PCI1 ? T_PCI1 : MODE == TM_RR1 ? T_RR1
+                   : T_PCI2;
     if (dd_grid_reduce<K>(acc, part, &sc->counter[slot], tot) && tid == 0) {
       if (MODE == TM_A) publish<F_SWEEPA>(sc, h, tot);
       else if (MODE == TM_C) publish<F_SWEEPC>(sc, h, tot);
@@ -626,6 +669,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       else if (MODE == TM_CL2) publish<F_CL2>(sc, h, tot);
       else if (MODE == TM_CL3) publish<F_CL3>(sc, h, tot);
       else if (MODE == TM_PC) publish<F_PC>(sc, h, tot);
+      else if (MODE == TM_RR1) publish<F_RR1>(sc, h, tot);
       else publish<F_PINIT2>(sc, h, tot);
     }
   }
@@ -652,6 +696,11 @@ inline size_t tile_smem_bytes(const TileGeo& g, int mode) {
     case TM_CL3: return tile_smem_bytes_t<TM_CL3>(g);
     case TM_PC: return tile_smem_bytes_t<TM_PC>(g);
     case TM_PCI1: return tile_smem_bytes_t<TM_PCI1>(g);
+    case TM_AN: return tile_smem_bytes_t<TM_AN>(g);
+    case TM_CN: return tile_smem_bytes_t<TM_CN>(g);
+    case TM_RR1N: return tile_smem_bytes_t<TM_RR1N>(g);
+    case TM_RR2N: return tile_smem_bytes_t<TM_RR2N>(g);
+    case TM_INIT1N: return tile_smem_bytes_t<TM_INIT1N>(g);
     default: return tile_smem_bytes_t<TM_PCI2>(g);
   }
 }

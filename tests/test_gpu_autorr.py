@@ -1,0 +1,157 @@
+"""GPU parity of the automated residual replacement (SURVEY 8(f) NEXT-1, P:609-623;
+option rr_auto) against the oracle.
+
+The decisions (which iterations replace) are integers decided by the fp64 bound
+f^r_i against tau ||r_i||: both sides decide in fp64 from the same formulas; the
+GPU's vector norms are per-thread fp64 sums of squares combined by its fixed
+tree, the oracle's are sequential Dot2 (reading A30), so f^r agrees to rounding
+(asserted <= 1e-12 relative) and the replacement lists must be identical.  With
+identical decisions the iterates stay bitwise equal (the norms never feed back).
+"""
+import numpy as np
+import pytest
+
+from paper_1809_01948_b200 import problems
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from test_gpu_parity import check_parity, coef_of, stencil_case  # noqa: E402
+
+FR_TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_1809_01948_b200 import Solver
+    assert torch.cuda.is_available()
+    return Solver
+
+
+def check_auto(res, fr, rrl, ref, xs):
+    """Decisions identical; north-star bars; bitwise iterates and f^r within
+    FR_TOL while ||r_i|| >= 1e-16 ||r_0||.  Below that the recursive residual is
+    rounding noise: dot products of noise vectors are ill-conditioned beyond
+    Dot2's guarantee, their rounding depends on the summation order, so the
+    GPU's tree and the oracle's sequential sum may part (DESIGN.md parity rule)."""
+    assert rrl == ref.rr_iters, (rrl, ref.rr_iters)
+    check_parity(res, ref, xs, bitwise=False)
+    assert res.iters == ref.iters
+    noise = np.nonzero(ref.rnorm < 1e-16 * ref.rnorm[0])[0]
+    k = int(noise[0]) if noise.size else ref.iters + 1
+    assert np.array_equal(res.rnorm[:k], ref.rnorm[:k]), "rnorm not bitwise before the noise floor"
+    if res.gap is not None and ref.gap is not None:
+        assert np.array_equal(res.gap[:k], ref.gap[:k]), "gap not bitwise before the noise floor"
+    if k > ref.iters:
+        assert np.array_equal(res.x.cpu().numpy(), ref.x), "x not bitwise"
+    rel = np.abs(fr[:k] - ref.bounds[:k, 0]) / ref.bounds[:k, 0]
+    assert np.all(rel <= FR_TOL), rel.max()
+
+
+CASES = [
+    (2, 100, 100, 1, "poisson", 400),  # cfg1 shape
+    (2, 64, 64, 1, "cd2", 300),
+    (3, 20, 20, 20, "cd3", 200),
+    (3, 13, 7, 19, "cd3", 200),        # ragged
+    (2, 37, 53, 1, "cd2", 300),        # odd nx
+]
+
+
+@pytest.mark.parametrize("dim,nx,ny,nz,kind,maxit", CASES)
+def test_auto_rr_parity(S, orc, dim, nx, ny, nz, kind, maxit):
+    solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of(kind))
+    solver.set_option("bench", 1)
+    solver.set_option("rr_auto", 1)
+    res = solver.solve(b_d, tol=0.0, maxit=maxit, gap=True)
+    fr, rrl = solver.rr_info(res.iters)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=maxit, bench=True, auto_rr=True)
+    assert len(ref.rr_iters) >= 1
+    check_auto(res, fr, rrl, ref, xs)
+    for j in rrl:
+        assert res.gap[j + 1] == 0.0
+
+
+def test_auto_rr_converging_and_graph_modes(S, orc):
+    solver, A, xs, b, b_d = stencil_case(S, orc, 3, 24, 20, 18, problems.cfg34_coef())
+    solver.set_option("rr_auto", 1)
+    ref = orc.pbicgstab(A, b, tol=1e-13, maxit=600, auto_rr=True)
+    out = []
+    for graphs, timing in ((1, 0), (0, 0), (0, 1)):
+        solver.set_option("graphs", graphs)
+        solver.set_option("timing", timing)
+        res = solver.solve(b_d, tol=1e-13, maxit=600, gap=True)
+        fr, rrl = solver.rr_info(res.iters)
+        assert res.outcome == ref.outcome
+        check_auto(res, fr, rrl, ref, xs)
+        out.append((res, fr))
+    for res, fr in out[1:]:
+        assert np.array_equal(fr, out[0][1])  # deterministic on the device
+
+
+def test_periodic_rr_info_and_switching(S, orc):
+    """rr_info also lists periodic replacements; switching rr_auto off restores the
+    periodic schedule bitwise."""
+    solver, A, xs, b, b_d = stencil_case(S, orc, 2, 64, 64, 1, problems.cfg2_coef())
+    solver.set_option("bench", 1)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=200, rr_period=30, bench=True)
+    for auto in (1, 0):
+        solver.set_option("rr_auto", auto)
+        if auto:
+            solver.solve(b_d, tol=0.0, maxit=200, gap=True)
+            continue
+        res = solver.solve(b_d, tol=0.0, maxit=200, rr_period=30, gap=True)
+        fr, rrl = solver.rr_info(res.iters)
+        check_parity(res, ref, xs)
+        assert rrl == ref.rr_iters
+        assert np.all(np.isnan(fr))
+
+
+def test_auto_rr_errors(S, orc):
+    from paper_1809_01948_b200.binding import PbicgError
+    solver, A, xs, b, b_d = stencil_case(S, orc, 2, 33, 17, 1, problems.cfg2_coef())
+    solver.set_option("rr_auto", 1)
+    with pytest.raises(PbicgError):
+        solver.solve(b_d, tol=1e-10, maxit=10, rr_period=5)
+    with pytest.raises(PbicgError):
+        solver.set_option("method", 1)
+    solver.set_option("rr_auto", 0)
+    solver.set_option("method", 1)
+    with pytest.raises(PbicgError):
+        solver.set_option("rr_auto", 1)
+    P = problems.csr_band(5000, nnz_row=9, band=50, seed=1)
+    cs = S.csr(P.n, P.row_ptr, P.col, P.val)
+    with pytest.raises(PbicgError):
+        cs.set_option("rr_auto", 1)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_auto_rr_loopback_multirank(S, orc, P):
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    dim, nx, ny, nz = 3, 20, 17, 12
+    coef = problems.cfg34_coef()
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 0)
+    b = orc.spmv(A, xs)
+    G = LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
+    G.set_option("bench", 1)
+    G.set_option("rr_auto", 1)
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=0.0, maxit=250, gap=True)
+    fr, rrl = G.ranks[0].rr_info(res.iters)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=250, bench=True, auto_rr=True)
+    assert len(ref.rr_iters) >= 1
+    check_auto(res, fr, rrl, ref, xs)
+    G.close()
+
+
+def test_auto_rr_fullsize_cfg3_first_iterations(S, orc):
+    """cfg3 at full size (256^3): 12 iterations with rr_auto; the bound history
+    and the (empty or not) decision list match the oracle; iterates bitwise."""
+    st = problems.configs()["cfg3"].stencil
+    solver, A, xs, b, b_d = stencil_case(S, orc, st.dim, st.nx, st.ny, st.nz, st.coef)
+    solver.set_option("bench", 1)
+    solver.set_option("rr_auto", 1)
+    res = solver.solve(b_d, tol=0.0, maxit=12, gap=False)
+    fr, rrl = solver.rr_info(res.iters)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=12, bench=True, auto_rr=True, gap=False)
+    check_auto(res, fr, rrl, ref, xs)
