@@ -246,6 +246,9 @@ def run_ours(args, rank, world):
     S.set_option("method", METHODS[args.method])
     if args.method != "pbicgstab":
         rr = 0  # residual replacement is an Alg. 2 feature
+    if args.rr_auto:
+        S.set_option("rr_auto", 1)  # automated replacement instead of the period
+        rr = 0
     n = S.n_local
     xs_full = problems.x_star(st.n, seed=0)
     xs = torch.from_numpy(xs_full[S.row_begin:S.row_begin + n]).to(f"cuda:{dev}")
@@ -345,6 +348,7 @@ def run_ours(args, rank, world):
         "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": st.n,
                    "grid": [st.nx, st.ny, st.nz] if st.dim else "csr 27 nnz/row, band 4096",
                    "maxit_per_step": maxit, "rr_period": rr, "gap_tracking": gap,
+                   "rr_auto": bool(args.rr_auto),
                    "method": args.method,
                    "schedule": SCHEDULES[args.method] if st.dim else
                                "split 4-phase (CSR as ELL), reduction #1 overlapped",
@@ -411,6 +415,9 @@ def main():
     ap.add_argument("--method", choices=["pbicgstab", "bicgstab", "pipecg"], default="pbicgstab",
                     help="solver: p-BiCGStab (the headline), classic BiCGStab or p-CG")
     ap.add_argument("--gap", type=int, default=0)
+    ap.add_argument("--rr-auto", type=int, default=0,
+                    help="automated residual replacement (bound f^r + eq:criterion) instead of "
+                         "the periodic schedule")
     ap.add_argument("--overlap", type=int, default=1,
                     help="P > 1: dot-product reductions overlap the halo exchange / SpMV (1) "
                          "or block the compute stream (0)")
