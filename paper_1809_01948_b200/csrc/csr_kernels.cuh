@@ -63,20 +63,33 @@ __device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restri
 #define ROW_LOOP for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < A.n; \
                       j += (int64_t)gridDim.x * blockDim.x)
 
+// NRM (automated replacement): the step's reduction also carries the
+// sums of squares of the vectors the bound f^r needs (plain fp64, reading A30)
+__device__ __forceinline__ void c_nrm(Dd& a, double v) { a.hi = a.hi + v * v; }
+
+template <bool NRM>
 __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                Dd* __restrict__ part, Hist h) {
-  Dd acc[2] = {dd_zero(), dd_zero()};
+  constexpr int K = NRM ? 4 : 2;
+  Dd acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   ROW_LOOP {
     const double bj = V.b[j];
     const double rj = bj - ell_row<false>(A, V.x, j);
+    const double kj = A.dinv[j] * rj;
     V.r[j] = rj;
     V.rh[j] = rj;
-    V.k[j] = A.dinv[j] * rj;
+    V.k[j] = kj;
     dd_fma(acc[0], rj, rj);
     dd_fma(acc[1], bj, bj);
+    if (NRM) {
+      c_nrm(acc[2 % K], V.x[j]);
+      c_nrm(acc[3 % K], kj);
+    }
   }
-  Dd tot[2];
-  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_INIT1], tot) && threadIdx.x == 0)
+  Dd tot[K];
+  if (dd_grid_reduce<K>(acc, part, &sc->counter[T_INIT1], tot) && threadIdx.x == 0)
     publish<F_INIT1>(sc, h, tot);
 }
 
@@ -95,12 +108,16 @@ __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict
 }
 
 // lines 5-12 with stored t_i, v_{i-1}; n_{i-1} = M^-1 z_{i-1} (pre-replacement, A26)
+template <bool NRM>
 __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                 Dd* __restrict__ part, Hist h) {
+  constexpr int K = NRM ? 12 : 2;
   if (sc->done) return;
   const double al = sc->alpha, be = sc->beta, om = sc->omega;
   const bool rr = sc->use_rr != 0;
-  Dd acc[2] = {dd_zero(), dd_zero()};
+  Dd acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   ROW_LOOP {
     const double dj = A.dinv[j];
     const double wc = V.w0[j], zc = V.z0[j];
@@ -116,15 +133,93 @@ __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restric
     const double y = wc - al * zn;
     dd_fma(acc[0], q, y);
     dd_fma(acc[1], y, y);
+    if (NRM) {  // k, w, m, t, g, s, l, z, q, y of iteration i
+      c_nrm(acc[2 % K], V.k[j]); c_nrm(acc[3 % K], wc); c_nrm(acc[4 % K], m);
+      c_nrm(acc[5 % K], t); c_nrm(acc[6 % K], gn); c_nrm(acc[7 % K], sn);
+      c_nrm(acc[8 % K], ln); c_nrm(acc[9 % K], zn); c_nrm(acc[10 % K], q);
+      c_nrm(acc[11 % K], y);
+    }
     V.g[j] = gn;
     V.s[j] = sn;
     V.l[j] = ln;
     V.z0[j] = zn;
     V.nv[j] = dj * zn;  // n_i = M^-1 z_i (line 13)
   }
-  Dd tot[2];
-  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
+  Dd tot[K];
+  if (dd_grid_reduce<K>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
     publish<F_SWEEPA>(sc, h, tot);
+}
+
+// ---------------------------------------------------------------------------
+// SpMV y = A u of one step, with the step's epilogue (store, dots).  The same
+// modes run as the gather kernel c_spmv_g (any matrix) and as the window kernel
+// c_spmv_win (banded matrices, operand window staged in shared memory).
+enum SpmvMode {
+  SP_V = 0,   // Alg. 2 line 14: v_i = A n_i
+  SP_T,       // Alg. 2 line 23: t_{i+1} = A m_{i+1}
+  SP_CLS,     // Alg. 1 lines 5-6: s_i = A (M^-1 p_i) [mv]; (r^0, s_i)
+  SP_CLY,     // Alg. 1 lines 10-11: y_i = A (M^-1 q_i) [nv]; q_i = r_i - alpha s_i; (q,y), (y,y)
+  SP_PCW0,    // p-CG init: w0 = A u0 [k]; m0 = M^-1 w0; (r0,u0), (w0,u0)
+  SP_PCN,     // p-CG: n_i = A m_i [mv]
+  SP_N
+};
+template <int M> struct SpmvK { enum { K = 0 }; };
+template <> struct SpmvK<SP_CLS> { enum { K = 1 }; };
+template <> struct SpmvK<SP_CLY> { enum { K = 2 }; };
+template <> struct SpmvK<SP_PCW0> { enum { K = 2 }; };
+
+template <int M>
+__device__ __forceinline__ const double* spmv_in(const Vecs& V) {
+  return (M == SP_V || M == SP_CLY) ? V.nv : M == SP_PCW0 ? V.k : V.mv;
+}
+
+template <int M, int K>
+__device__ __forceinline__ void spmv_epi(const CsrOp& A, const Vecs& V, int64_t j, double y,
+                                         double al, Dd* acc) {
+  if (M == SP_V || M == SP_CLY || M == SP_PCN) __stcs(V.z1 + j, y);
+  if (M == SP_T) __stcs(V.w1 + j, y);
+  if (M == SP_CLS) {
+    V.s[j] = y;
+    dd_fma(acc[0], V.rh[j], y);
+  } else if (M == SP_CLY) {
+    const double q = V.r[j] - al * V.s[j];  // line 8, recomputed (same value)
+    dd_fma(acc[0], q, y);
+    dd_fma(acc[1 % K], y, y);
+  } else if (M == SP_PCW0) {
+    V.w0[j] = y;
+    V.mv[j] = A.dinv[j] * y;
+    const double u = V.k[j];
+    dd_fma(acc[0], V.r[j], u);
+    dd_fma(acc[1 % K], y, u);
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void spmv_fin(Scal* sc, Hist h, Dd* part, Dd (&acc)[SpmvK<M>::K > 0 ? SpmvK<M>::K : 1]) {
+  constexpr int K = SpmvK<M>::K > 0 ? SpmvK<M>::K : 1;
+  if (SpmvK<M>::K == 0) return;
+  Dd tot[K];
+  const int slot = M == SP_CLS ? T_CL1 : M == SP_CLY ? T_CL2 : T_PCI2;
+  if (dd_grid_reduce<K>(acc, part, &sc->counter[slot], tot) && threadIdx.x == 0) {
+    if (M == SP_CLS) publish<F_CL1>(sc, h, tot);
+    else if (M == SP_CLY) publish<F_CL2>(sc, h, tot);
+    else publish<F_PINIT2>(sc, h, tot);
+  }
+}
+
+// gather version (any sparsity within the ghost band)
+template <int M>
+__global__ void __launch_bounds__(256) c_spmv_g(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                                Dd* __restrict__ part, Hist h) {
+  constexpr int K = SpmvK<M>::K > 0 ? SpmvK<M>::K : 1;
+  if (M != SP_PCW0 && sc->done) return;
+  const double al = sc->alpha;
+  const double* __restrict__ u = spmv_in<M>(V);
+  Dd acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = dd_zero();
+  ROW_LOOP { spmv_epi<M, K>(A, V, j, ell_row<false>(A, u, j), al, acc); }
+  spmv_fin<M>(sc, h, part, acc);
 }
 
 // line 14: v_i = A n_i (gather version; c_spmv_win is the staged one)
@@ -134,11 +229,15 @@ __global__ void __launch_bounds__(256) c_spmvB(CsrOp A, Vecs V, Scal* __restrict
 }
 
 // lines 17-21
+template <bool NRM>
 __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                 Dd* __restrict__ part, Hist h) {
+  constexpr int K = NRM ? 9 : 5;
   if (sc->done) return;
   const double al = sc->alpha, om = sc->omega;
-  Dd acc[5] = {dd_zero(), dd_zero(), dd_zero(), dd_zero(), dd_zero()};
+  Dd acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   ROW_LOOP {
     const double dj = A.dinv[j];
     const double wc = V.w0[j], zc = V.z0[j];
@@ -148,30 +247,38 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
     const double u = V.k[j] - al * V.l[j];
     const double q = V.r[j] - al * sj;
     const double y = wc - al * zc;
-    const double xn = (V.x[j] + al * V.g[j]) + om * u;
+    const double xj = V.x[j];
+    const double xn = (xj + al * V.g[j]) + om * u;
     const double rn = q - om * y;
     const double kn = u - om * (m - al * n);
     const double wn = y - om * (t - al * v);
     const double rhj = V.rh[j];
     dd_fma(acc[0], rhj, rn);
-    dd_fma(acc[1], rhj, wn);
-    dd_fma(acc[2], rhj, sj);
-    dd_fma(acc[3], rhj, zc);
-    dd_fma(acc[4], rn, rn);
+    dd_fma(acc[1 % K], rhj, wn);
+    dd_fma(acc[2 % K], rhj, sj);
+    dd_fma(acc[3 % K], rhj, zc);
+    dd_fma(acc[4 % K], rn, rn);
+    if (NRM) {  // x_i, u_i, n_i, v_i
+      c_nrm(acc[5 % K], xj); c_nrm(acc[6 % K], u); c_nrm(acc[7 % K], n);
+      c_nrm(acc[8 % K], v);
+    }
     V.x[j] = xn;
     V.r[j] = rn;
     V.k[j] = kn;
     V.w0[j] = wn;
     V.mv[j] = dj * wn;  // m_{i+1} = M^-1 w_{i+1} (line 22)
   }
-  Dd tot[5];
-  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0)
+  Dd tot[K];
+  if (dd_grid_reduce<K>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0)
     publish<F_SWEEPC>(sc, h, tot);
 }
 
 // eq:rr: r := b - A x; k := M^-1 r; s := A g; l := M^-1 s
-__global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__ sc) {
+template <bool NRM>
+__global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                             Dd* __restrict__ part, Hist h) {
   if (sc->done || !sc->rr_fire) return;
+  Dd acc[4] = {dd_zero(), dd_zero(), dd_zero(), dd_zero()};
   ROW_LOOP {
     const double dj = A.dinv[j];
     const double rj = V.b[j] - ell_row<false>(A, V.x, j);
@@ -180,14 +287,26 @@ __global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__
     V.k[j] = dj * rj;
     V.s[j] = sj;
     V.l[j] = dj * sj;
+    if (NRM) {  // replaced x_{i+1}, k_{i+1}, s_i, l_i
+      c_nrm(acc[0], V.x[j]); c_nrm(acc[1], dj * rj); c_nrm(acc[2], sj); c_nrm(acc[3], dj * sj);
+    }
+  }
+  if (NRM) {
+    Dd tot[4];
+    if (dd_grid_reduce<4>(acc, part, &sc->counter[T_RR1], tot) && threadIdx.x == 0)
+      publish<F_RR1>(sc, h, tot);
   }
 }
 
 // w := A k; z := A l (into zrr); line-21 dots on the replaced vectors
+template <bool NRM>
 __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                              Dd* __restrict__ part, Hist h) {
+  constexpr int K = NRM ? 6 : 5;
   if (sc->done || !sc->rr_fire) return;
-  Dd acc[5] = {dd_zero(), dd_zero(), dd_zero(), dd_zero(), dd_zero()};
+  Dd acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   ROW_LOOP {
     const double wn = ell_row<true>(A, V.r, j);
     const double zr = ell_row<true>(A, V.s, j);
@@ -196,13 +315,14 @@ __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__
     V.zrr[j] = zr;
     const double rhj = V.rh[j], rc = V.r[j];
     dd_fma(acc[0], rhj, rc);
-    dd_fma(acc[1], rhj, wn);
-    dd_fma(acc[2], rhj, V.s[j]);
-    dd_fma(acc[3], rhj, zr);
-    dd_fma(acc[4], rc, rc);
+    dd_fma(acc[1 % K], rhj, wn);
+    dd_fma(acc[2 % K], rhj, V.s[j]);
+    dd_fma(acc[3 % K], rhj, zr);
+    dd_fma(acc[4 % K], rc, rc);
+    if (NRM) c_nrm(acc[5 % K], zr);  // replaced z_i
   }
-  Dd tot[5];
-  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_RR2], tot) && threadIdx.x == 0)
+  Dd tot[K];
+  if (dd_grid_reduce<K>(acc, part, &sc->counter[T_RR2], tot) && threadIdx.x == 0)
     publish<F_RR2>(sc, h, tot);
 }
 
@@ -252,17 +372,20 @@ __device__ __forceinline__ void win_issue(double* ring, const double* __restrict
   }
 }
 
-template <int WHICH>  // 0: v = A n (line 14), 1: t = A m (line 23)
+template <int WHICH>  // SpmvMode: input, output and epilogue of the step
 __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __restrict__ sc,
-                                                     WinGeo w) {
-  if (sc->done) return;
-  const double* __restrict__ u = WHICH == 0 ? V.nv : V.mv;
-  double* __restrict__ y = WHICH == 0 ? V.z1 : V.w1;
+                                                     WinGeo w, Dd* __restrict__ part, Hist h) {
+  constexpr int K = SpmvK<WHICH>::K > 0 ? SpmvK<WHICH>::K : 1;
+  if (WHICH != SP_PCW0 && sc->done) return;
+  const double al = sc->alpha;
+  const double* __restrict__ u = spmv_in<WHICH>(V);
+  Dd dacc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) dacc[k] = dd_zero();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   double* ring = reinterpret_cast<double*>(smem_raw + 64);
-  const int64_t R0 = (int64_t)blockIdx.x * w.rows_cta;
-  if (R0 >= A.n) return;
+  const int64_t R0 = (int64_t)blockIdx.x * w.rows_cta;  // < A.n: grid = ceil(n / rows_cta)
   const int64_t R1 = (R0 + w.rows_cta) < A.n ? (R0 + w.rows_cta) : A.n;
   const int nsteps = (int)((R1 - R0 + WTB - 1) / WTB);
   if (threadIdx.x == 0) {
@@ -303,12 +426,87 @@ __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __re
         const int c = __ldcs(A.col + (int64_t)p * A.n + j);
         acc = acc + __ldcs(A.val + (int64_t)p * A.n + j) * ring[(c + w.off) & (WRS - 1)];
       }
-      __stcs(y + j, acc);
+      spmv_epi<WHICH, K>(A, V, j, acc, al, dacc);
     }
     __syncthreads();  // step s done: its oldest chunk may be overwritten
     if (threadIdx.x == 0 && s + 2 < nsteps)
       win_issue(ring, u, j0 + 2 * WTB + w.bw, j0 + 3 * WTB + w.bw, w, &bar[b]);
   }
+  spmv_fin<WHICH>(sc, h, part, dacc);
+}
+
+// ---------------------------------------------------------------------------
+// Classic BiCGStab (Alg. 1) on CSR: the element-wise steps around the
+// SpMVs SP_CLS / SP_CLY.  Buffers: p -> g, M^-1 p -> mv, M^-1 q -> nv, y -> z1.
+// l.17 of the previous iteration (i = 0: beta = omega = 0 and p = s = 0, so
+// p_0 = r_0): p := r + beta (p - omega s); the SpMV operand mv := M^-1 p (l.4)
+__global__ void __launch_bounds__(256) c_cl_p(CsrOp A, Vecs V, Scal* __restrict__ sc) {
+  if (sc->done) return;
+  const double be = sc->beta, om = sc->omega;
+  ROW_LOOP {
+    const double p = V.r[j] + be * (V.g[j] - om * V.s[j]);
+    V.g[j] = p;
+    V.mv[j] = A.dinv[j] * p;
+  }
+}
+
+// l.8-9: q := r - alpha s; the SpMV operand nv := u = M^-1 q
+__global__ void __launch_bounds__(256) c_cl_u(CsrOp A, Vecs V, Scal* __restrict__ sc) {
+  if (sc->done) return;
+  const double al = sc->alpha;
+  ROW_LOOP { V.nv[j] = A.dinv[j] * (V.r[j] - al * V.s[j]); }
+}
+
+// l.13-15: x := (x + alpha g) + omega u; r := q - omega y; (r^0, r), ||r||^2
+__global__ void __launch_bounds__(256) c_cl_x(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                              Dd* __restrict__ part, Hist h) {
+  if (sc->done) return;
+  const double al = sc->alpha, om = sc->omega;
+  Dd acc[2] = {dd_zero(), dd_zero()};
+  ROW_LOOP {
+    const double q = V.r[j] - al * V.s[j];
+    const double xn = (V.x[j] + al * V.mv[j]) + om * V.nv[j];
+    const double rn = q - om * V.z1[j];
+    V.x[j] = xn;
+    V.r[j] = rn;
+    dd_fma(acc[0], V.rh[j], rn);
+    dd_fma(acc[1], rn, rn);
+  }
+  Dd tot[2];
+  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_CL3], tot) && threadIdx.x == 0)
+    publish<F_CL3>(sc, h, tot);
+}
+
+// p-CG iteration (reading A19) after n_i = A m_i (SP_PCN): buffers z -> z0,
+// q -> l, s, p -> g, x, r, u -> k, w -> w0, n -> z1, m -> mv (written for the
+// next SpMV); the next iteration's (r,u), (w,u), ||r||^2
+__global__ void __launch_bounds__(256) c_pc(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                            Dd* __restrict__ part, Hist h) {
+  if (sc->done) return;
+  const double al = sc->alpha, be = sc->beta;
+  Dd acc[3] = {dd_zero(), dd_zero(), dd_zero()};
+  ROW_LOOP {
+    const double dj = A.dinv[j];
+    const double wj = V.w0[j], uj = V.k[j];
+    const double mj = dj * wj;
+    const double zn = V.z1[j] + be * V.z0[j];
+    const double qn = mj + be * V.l[j];
+    const double sn = wj + be * V.s[j];
+    const double pn = uj + be * V.g[j];
+    const double xn = V.x[j] + al * pn;
+    const double rn = V.r[j] - al * sn;
+    const double un = uj - al * qn;
+    const double wn = wj - al * zn;
+    V.z0[j] = zn; V.l[j] = qn; V.s[j] = sn; V.g[j] = pn;
+    V.x[j] = xn; V.r[j] = rn; V.k[j] = un; V.w0[j] = wn;
+    V.mv[j] = dj * wn;
+    dd_fma(acc[0], rn, un);
+    dd_fma(acc[1], wn, un);
+    dd_fma(acc[2], rn, rn);
+  }
+  Dd tot[3];
+  if (dd_grid_reduce<3>(acc, part, &sc->counter[T_PC], tot) && threadIdx.x == 0)
+    publish<F_PC>(sc, h, tot);
 }
 
 __global__ void __launch_bounds__(256) c_gap(CsrOp A, Vecs V, Scal* __restrict__ sc,

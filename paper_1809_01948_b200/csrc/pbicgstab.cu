@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -232,7 +233,9 @@ Members members(pbicg_ctx* h) {
 // ---------------------------------------------------------------------------
 // Kernel launches (one rank)
 enum Phase { PH_INIT1, PH_INIT2, PH_SWEEPA, PH_SPMVB, PH_SWEEPC, PH_RR1, PH_RR2, PH_SPMVD, PH_GAP,
-             PH_CL1, PH_CL2, PH_CL3, PH_PC, PH_PCI1, PH_PCI2 };
+             PH_CL1, PH_CL2, PH_CL3, PH_PC, PH_PCI1, PH_PCI2,
+             // CSR comparison solvers: element-wise steps and SpMVs with epilogues
+             PH_CCP, PH_SP_CLS, PH_CCU, PH_SP_CLY, PH_CCX, PH_SP_PCW0, PH_SP_PCN, PH_CPC };
 
 template <int DIM, int MODE>
 void launch_tile(pbicg_ctx* h) {
@@ -306,12 +309,45 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
   }
 }
 
+template <int M>
+void launch_spmv(pbicg_ctx* h) {
+  if (h->win_ok)
+    c_spmv_win<M><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(h->csr, h->V, h->scal, h->wg, h->part,
+                                                             h->hist);
+  else
+    c_spmv_g<M><<<h->grid[K_SPMVB], h->block, 0, h->stream>>>(h->csr, h->V, h->scal, h->part,
+                                                              h->hist);
+}
+
 void launch_csr(pbicg_ctx* h, Phase p) {
   const CsrOp& A = h->csr;
   switch (p) {
+    case PH_CCP: {
+      LaunchScope ls(h, K_CL1);
+      c_cl_p<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+    } break;
+    case PH_SP_CLS: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_CLS>(h); } break;
+    case PH_CCU: {
+      LaunchScope ls(h, K_CL2);
+      c_cl_u<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+    } break;
+    case PH_SP_CLY: { LaunchScope ls(h, K_SPMVD); launch_spmv<SP_CLY>(h); } break;
+    case PH_CCX: {
+      LaunchScope ls(h, K_CL3);
+      c_cl_x<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_SP_PCW0: { LaunchScope ls(h, K_INIT); launch_spmv<SP_PCW0>(h); } break;
+    case PH_SP_PCN: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_PCN>(h); } break;
+    case PH_CPC: {
+      LaunchScope ls(h, K_PC);
+      c_pc<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+    } break;
     case PH_INIT1: {
       LaunchScope ls(h, K_INIT);
-      c_init1<<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->auto_rr)
+        c_init1<true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else
+        c_init1<false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_INIT2: {
       LaunchScope ls(h, K_INIT);
@@ -319,31 +355,45 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SWEEPA: {
       LaunchScope ls(h, K_SWEEPA);
-      c_sweepA<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->auto_rr)
+        c_sweepA<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else
+        c_sweepA<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SPMVB: {
       LaunchScope ls(h, K_SPMVB);
       if (h->win_ok)
-        c_spmv_win<0><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg);
+        c_spmv_win<SP_V><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg,
+                                                                    h->part, h->hist);
       else
         c_spmvB<<<h->grid[K_SPMVB], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
     case PH_SWEEPC: {
       LaunchScope ls(h, K_SWEEPC);
-      c_sweepC<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->auto_rr)
+        c_sweepC<true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else
+        c_sweepC<false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_RR1: {
       LaunchScope ls(h, K_RR1);
-      c_rr1<<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      if (h->auto_rr)
+        c_rr1<true><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else
+        c_rr1<false><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_RR2: {
       LaunchScope ls(h, K_RR2);
-      c_rr2<<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->auto_rr)
+        c_rr2<true><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else
+        c_rr2<false><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SPMVD: {
       LaunchScope ls(h, K_SPMVD);
       if (h->win_ok)
-        c_spmv_win<1><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg);
+        c_spmv_win<SP_T><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg,
+                                                                    h->part, h->hist);
       else
         c_spmvD<<<h->grid[K_SPMVD], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
@@ -497,6 +547,43 @@ const VecSel SZRR = [](pbicg_ctx* h) { return h->V.zrr; };
 
 // Alg. 1 (method 1) on the stencil: p_i, s_i, r_i double-buffered by parity
 // (tile_sweeps.cuh TM_CL*): r in {r, k}, p in {g, l}, s in {s, zrr}
+// CSR: p in g, M^-1 p in mv, M^-1 q in nv, y in z1 (csr_kernels.cuh c_cl_*)
+const VecSel SNVv = [](pbicg_ctx* h) { return h->V.nv; };
+const VecSel SMVv = [](pbicg_ctx* h) { return h->V.mv; };
+
+void enq_iter_classic_csr(const Members& G) {
+  const bool dist = G[0]->nranks > 1;
+  each(G, PH_CCP);  // l.17 (previous i) + l.4: p_i, M^-1 p_i
+  if (dist) comm_halo(G, {SMVv});
+  each(G, PH_SP_CLS);  // l.5-6: s_i, (r^0, s_i) -> alpha
+  reduce_fin(G, F_CL1);
+  each(G, PH_CCU);  // l.8-9: u = M^-1 (r - alpha s)
+  if (dist) comm_halo(G, {SNVv});
+  each(G, PH_SP_CLY);  // l.10-11: y, (q,y), (y,y) -> omega
+  reduce_fin(G, F_CL2);
+  each(G, PH_CCX);  // l.13-16: x, r, (r^0,r), ||r|| -> beta
+  reduce_fin(G, F_CL3);
+}
+
+// p-CG on CSR, software-pipelined: iteration i enqueues the SpMV of iteration
+// i+1 (n_{i+1} = A m_{i+1}) between its reduction's fork and join, so on P ranks
+// the all-reduce of {(r,u),(w,u),||r||} overlaps that SpMV -- the point of p-CG
+void enq_iter_pipecg_csr(const Members& G) {
+  pbicg_ctx* h0 = G[0];
+  const bool dist = h0->nranks > 1;
+  each(G, PH_CPC);
+  if (!dist) {
+    each(G, PH_SP_PCN);
+    return;
+  }
+  if (h0->overlap) fork_reduce(G);
+  else comm_reduce(G, false);
+  comm_halo(G, {SMVv});
+  each(G, PH_SP_PCN);
+  if (h0->overlap) join_reduce(G);
+  each_fin(G, F_PC);
+}
+
 void enq_init_classic(const Members& G) {
   const bool dist = G[0]->nranks > 1;
   if (dist) comm_halo(G, {SX});
@@ -523,6 +610,17 @@ void enq_iter_classic(const Members& G, int par) {
 // p-CG (method 2): one kernel and one reduction per iteration
 void enq_init_pipecg(const Members& G) {
   const bool dist = G[0]->nranks > 1;
+  if (G[0]->kind == KIND_CSR) {
+    if (dist) comm_halo(G, {SX});
+    each(G, PH_INIT1);  // r0, u0 (k); ||r0||, ||b|| (F_INIT1, method 2)
+    reduce_fin(G, F_INIT1);
+    if (dist) comm_halo(G, {SK});
+    each(G, PH_SP_PCW0);  // w0 = A u0, m0; (r0,u0), (w0,u0) -> alpha_0
+    reduce_fin(G, F_PINIT2);
+    if (dist) comm_halo(G, {SMVv});
+    each(G, PH_SP_PCN);  // n_0 = A m_0
+    return;
+  }
   if (dist) comm_halo(G, {SX});
   each(G, PH_PCI1);  // r0, u0; ||r0||, ||b|| (F_INIT1, method 2)
   reduce_fin(G, F_INIT1);
@@ -579,8 +677,14 @@ void enq_iter(const Members& G, bool with_rr, int par) {
   pbicg_ctx* h0 = G[0];
   const bool dist = h0->nranks > 1;
   if (h0->method != M_PBICGSTAB) {
-    if (h0->method == M_BICGSTAB) enq_iter_classic(G, par);
-    else enq_iter_pipecg(G, par);
+    if (h0->kind == KIND_CSR) {
+      if (h0->method == M_BICGSTAB) enq_iter_classic_csr(G);
+      else enq_iter_pipecg_csr(G);
+    } else if (h0->method == M_BICGSTAB) {
+      enq_iter_classic(G, par);
+    } else {
+      enq_iter_pipecg(G, par);
+    }
     enq_gap(G);
     return;
   }
@@ -646,6 +750,7 @@ void enq_iter(const Members& G, bool with_rr, int par) {
     if (with_rr) {
       if (dist) comm_halo(G, {SX, SG});
       each(G, PH_RR1);
+      if (h0->auto_rr) reduce_fin(G, F_RR1);  // norms of the replaced vectors
       if (dist) comm_halo(G, {SR, SS});
       each(G, PH_RR2);
       reduce_fin(G, F_RR2);
@@ -779,6 +884,10 @@ void setup_tile(pbicg_ctx* h) {
   int64_t TY = dim == 3 ? (tpmax / g.nx) : 1;
   if (TY < 1) TY = 1;
   if (TY > lines) TY = lines;
+  if (const char* e = getenv("PBICG_TILE_TY")) {  // tuning experiments only
+    const long v = strtol(e, nullptr, 10);
+    if (v >= 1 && v < TY) TY = v;
+  }
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
   const size_t reserve = 4096;  // static shared memory of the block reductions
@@ -817,6 +926,10 @@ void setup_tile(pbicg_ctx* h) {
       best_n = nch;
     }
     if (units > 64LL * grid) break;
+  }
+  if (const char* e = getenv("PBICG_TILE_NCHUNKS")) {  // tuning experiments only
+    const long v = strtol(e, nullptr, 10);
+    if (v >= 1 && v <= g.nol) best_n = v;
   }
   t.chunk = (int32_t)((g.nol + best_n - 1) / best_n);
   t.nchunks = (int32_t)((g.nol + t.chunk - 1) / t.chunk);
@@ -1098,9 +1211,43 @@ pbicg_status validate_csr(const pbicg_csr* op, int nranks, std::vector<double>* 
   return PBICG_OK;
 }
 
+// Automated-replacement constants of a CSR operator given ALL its row blocks in
+// order (reading A29): ||A|| <= sqrt(||A||_1 ||A||_inf), row sums in stored
+// (ascending column) order, column sums in ascending row order -- the same
+// doubles as oracle.c orc_anorm_bound; mu = max row length; ||M^-1|| = max |1/a_jj|.
+void csr_bound_consts(const pbicg_csr* ops, int nops, double* nA, double* muN, double* mutN) {
+  const int64_t N = ops[0].n_global;
+  std::vector<double> col((size_t)N, 0.0);
+  double rmax = 0.0, cmax = 0.0, mi = 0.0;
+  int64_t mu = 0;
+  for (int r = 0; r < nops; ++r) {
+    const pbicg_csr& op = ops[r];
+    for (int64_t i = 0; i < op.n_local; ++i) {
+      double rs = 0.0;
+      const int64_t p0 = op.row_ptr[i], p1 = op.row_ptr[i + 1];
+      if (p1 - p0 > mu) mu = p1 - p0;
+      for (int64_t p = p0; p < p1; ++p) {
+        rs = rs + std::fabs(op.val[p]);
+        col[(size_t)op.col[p]] = col[(size_t)op.col[p]] + std::fabs(op.val[p]);
+        if (op.col[p] == op.row_begin + i && std::fabs(1.0 / op.val[p]) > mi)
+          mi = std::fabs(1.0 / op.val[p]);
+      }
+      if (rs > rmax) rmax = rs;
+    }
+  }
+  for (double c : col) cmax = c > cmax ? c : cmax;
+  *nA = std::sqrt(cmax * rmax);
+  *muN = (double)mu * std::sqrt((double)N);
+  *mutN = 1.0 * std::sqrt((double)N) * mi;
+}
+
 pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<double>& dinv,
                        int64_t width, bool uniform) {
   h->kind = KIND_CSR;
+  if (h->nranks == 1) {  // multi-rank: the loopback group sets them (NCCL ranks: not available)
+    csr_bound_consts(op, 1, &h->ar_nA, &h->ar_muN, &h->ar_mutN);
+    h->ar_ok = true;
+  }
   const int64_t n = op->n_local;
   const int64_t* rp = op->row_ptr;
   h->n_global = op->n_global;
@@ -1139,13 +1286,14 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
   h->csr.len = uniform ? nullptr : (const int32_t*)pl;
   h->csr.dinv = h->dinv_g;
   const int64_t blocks = (n + h->block - 1) / h->block;
-  h->grid[K_INIT] = occ_grid(h, c_init1, blocks);
-  h->grid[K_SWEEPA] = occ_grid(h, c_sweepA, blocks);
-  h->grid[K_SWEEPC] = occ_grid(h, c_sweepC, blocks);
+  // (the NRM variants reuse these grids: grid-stride loops, last-CTA reductions)
+  h->grid[K_INIT] = occ_grid(h, c_init1<false>, blocks);
+  h->grid[K_SWEEPA] = occ_grid(h, c_sweepA<false>, blocks);
+  h->grid[K_SWEEPC] = occ_grid(h, c_sweepC<false>, blocks);
   h->grid[K_SPMVB] = occ_grid(h, c_spmvB, blocks);
   h->grid[K_SPMVD] = occ_grid(h, c_spmvD, blocks);
-  h->grid[K_RR1] = occ_grid(h, c_rr1, blocks);
-  h->grid[K_RR2] = occ_grid(h, c_rr2, blocks);
+  h->grid[K_RR1] = occ_grid(h, c_rr1<false>, blocks);
+  h->grid[K_RR2] = occ_grid(h, c_rr2<false>, blocks);
   h->grid[K_GAP] = occ_grid(h, c_gap, blocks);
   h->grid[K_APPLY] = occ_grid(h, c_apply, blocks);
   ST(gvec(h, &h->V.nv));
@@ -1167,11 +1315,14 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     per = ((per + WTB - 1) / WTB) * WTB;
     w.rows_cta = (int32_t)per;
     h->win_grid = (int)((n + per - 1) / per);
-    cudaError_t e1 = cudaFuncSetAttribute(c_spmv_win<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          WIN_SMEM);
-    cudaError_t e2 = cudaFuncSetAttribute(c_spmv_win<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          WIN_SMEM);
-    h->win_ok = e1 == cudaSuccess && e2 == cudaSuccess;
+    const cudaFuncAttribute SM = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaFuncSetAttribute(c_spmv_win<SP_V>, SM, WIN_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_T>, SM, WIN_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_CLS>, SM, WIN_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_CLY>, SM, WIN_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_PCW0>, SM, WIN_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_PCN>, SM, WIN_SMEM);
+    h->win_ok = e == cudaSuccess;
     cudaGetLastError();
   }
   return alloc_common(h);
@@ -1475,6 +1626,16 @@ pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec
     comm_halo(grp->m, {[](pbicg_ctx* c) { return c->dinv_g; }});
     if (cudaStreamSynchronize(s) != cudaSuccess) st = fail(nullptr, PBICG_ECUDA, "dinv halo");
   }
+  if (!st) {
+    double nA = 0, muN = 0, mutN = 0;
+    csr_bound_consts(ops, nranks, &nA, &muN, &mutN);
+    for (pbicg_ctx* m : grp->m) {
+      m->ar_nA = nA;
+      m->ar_muN = muN;
+      m->ar_mutN = mutN;
+      m->ar_ok = true;
+    }
+  }
   if (st) {
     Members m = grp->m;
     for (auto it = m.rbegin(); it != m.rend(); ++it) destroy_one(*it);
@@ -1523,20 +1684,20 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       m->tile_on = value != 0;
       destroy_graphs(m);
     } else if (k == "rr_auto") {
-      if (value != 0 && (m->kind != KIND_STENCIL || !m->tile_ok || !m->ar_ok ||
-                         m->method != M_PBICGSTAB))
+      if (value != 0 && (m->method != M_PBICGSTAB || !m->ar_ok ||
+                         (m->kind == KIND_STENCIL && !m->tile_ok)))
         return fail(h, PBICG_EINVAL,
-                    "rr_auto needs method 0 on a stencil operator with nx <= 1024 (TMA tile "
-                    "kernels)");
+                    "rr_auto needs method 0 and a stencil with nx <= 1024 (TMA tile kernels) or "
+                    "a CSR operator on one process (bound constants need every row)");
       m->auto_rr = value != 0;
       destroy_graphs(m);
     } else if (k == "method") {
       if (value != M_PBICGSTAB && m->auto_rr)
         return fail(h, PBICG_EINVAL, "switch rr_auto off before selecting method 1 or 2");
       if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "method must be 0, 1 or 2");
-      if (value != M_PBICGSTAB && (m->kind != KIND_STENCIL || !m->tile_ok))
+      if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && !m->tile_ok)
         return fail(h, PBICG_EINVAL,
-                    "methods 1 (BiCGStab) and 2 (p-CG) need a stencil operator with nx <= 1024 "
+                    "methods 1 (BiCGStab) and 2 (p-CG) on a stencil need nx <= 1024 "
                     "(TMA tile kernels)");
       m->method = (int)value;
       destroy_graphs(m);
@@ -1701,11 +1862,19 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     const double slots = (double)h->csr.width;  // ELL width
     const double mat = 12.0 * slots * N;        // val (8) + col (4) per slot
     if (n == "sweepA") b = 15 * 8 * N;  // read k,g,l,w,s,z,t,v,r,dinv; write g,s,l,z,n
+    else if (h->method == M_BICGSTAB && n == "spmvB") b = mat + 3 * 8 * N;  // mv in; s out; r^
+    else if (h->method == M_BICGSTAB && n == "spmvD") b = mat + 4 * 8 * N;  // nv in; y out; r, s
     else if (n == "spmvB" || n == "spmvD" || n == "apply") b = mat + 2 * 8 * N;  // n|m in, out
     else if (n == "sweepC") b = 17 * 8 * N;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w,m
     else if (n == "rr1") b = 2 * mat + 8 * 8 * N;
     else if (n == "rr2") b = 2 * mat + 7 * 8 * N;
     else if (n == "gap") b = mat + 3 * 8 * N;
+    else if (n == "iteration" && h->method == M_BICGSTAB) b = 2 * mat + 2 * 8 * N + 24 * 8 * N;
+    else if (n == "iteration" && h->method == M_PIPECG) b = mat + 21 * 8 * N;
+    else if (n == "cl1") b = 6 * 8 * N;   // c_cl_p: read r,p,s,dinv; write p, M^-1 p
+    else if (n == "cl2") b = 4 * 8 * N;   // c_cl_u: read r,s,dinv; write M^-1 q
+    else if (n == "cl3") b = 9 * 8 * N;   // c_cl_x: read x,mv,nv,r,s,y,r^; write x,r
+    else if (n == "pcg") b = 19 * 8 * N;  // c_pc: read n,z,q,s,p,x,r,u,w,dinv; write 9
     else if (n == "iteration") b = 2 * mat + 36 * 8 * N;
   }
   *bytes = b;

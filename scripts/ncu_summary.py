@@ -7,18 +7,27 @@ import argparse
 import csv
 import json
 
-ALG = {  # algorithmic bytes per row
-    "sweepA": 88, "sweepC": 104, "rr1": 56, "rr2": 40, "gap": 24, "init1": 40, "init2": 32,
+import re
+
+ALG = {  # algorithmic bytes per row: passes x 8 B
+    "sweepA": 88, "sweepC": 104, "rr1": 56, "rr2": 40, "gap": 24, "init1": 40, "init2": 24,
+    "cl1": 48, "cl2": 16, "cl3": 56, "pcg": 128, "pcinit1": 32, "pcinit2": 16,
 }
+# t_tile<DIM, MODE, VEC>: MODE numbering of tile_sweeps.cuh TileMode
+MODES = ["sweepA", "sweepC", "rr1", "rr2", "gap", "init1", "init2", "cl1", "cl2", "cl3", "pcg",
+         "pcinit1", "pcinit2", "sweepA", "sweepC", "rr1", "rr2", "init1"]
 
 
 def kernel_key(name: str):
-    if "t_sweep<3, 0" in name or "t_sweep<2, 0" in name or "k_sweepA" in name:
+    m = re.search(r"t_tile<\d, (\d+), ", name)
+    if m:
+        return MODES[int(m.group(1))]
+    if "k_sweepA" in name:
         return "sweepA"
-    if "t_sweep<3, 1" in name or "t_sweep<2, 1" in name or "k_sweepC" in name:
+    if "k_sweepC" in name:
         return "sweepC"
     for k in ("rr1", "rr2", "gap", "init1", "init2"):
-        if f"k_{k}" in name or f"t_{k}" in name:
+        if f"k_{k}" in name:
             return k
     return None
 

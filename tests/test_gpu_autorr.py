@@ -118,10 +118,47 @@ def test_auto_rr_errors(S, orc):
     solver.set_option("method", 1)
     with pytest.raises(PbicgError):
         solver.set_option("rr_auto", 1)
-    P = problems.csr_band(5000, nnz_row=9, band=50, seed=1)
-    cs = S.csr(P.n, P.row_ptr, P.col, P.val)
+    wide = S.stencil(2, 1500, 4, 1, problems.cfg2_coef())  # line kernels: no bound norms
     with pytest.raises(PbicgError):
-        cs.set_option("rr_auto", 1)
+        wide.set_option("rr_auto", 1)
+
+
+@pytest.mark.parametrize("band", [300, 6000])  # window / gather SpMV
+def test_auto_rr_csr(S, orc, band):
+    P = problems.csr_band(6000, nnz_row=27, band=band, seed=3)
+    solver = S.csr(P.n, P.row_ptr, P.col, P.val)
+    A = orc.csr(P.row_ptr, P.col, P.val)
+    xs = problems.x_star(P.n, 0)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    solver.set_option("bench", 1)
+    solver.set_option("rr_auto", 1)
+    res = solver.solve(b_d, tol=0.0, maxit=60, gap=True)
+    fr, rrl = solver.rr_info(res.iters)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=60, bench=True, auto_rr=True)
+    check_auto(res, fr, rrl, ref, xs)
+
+
+def test_auto_rr_csr_loopback(S, orc):
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    A0 = orc.stencil_csr(2, 64, 192, 1, problems.cfg2_coef())  # CSR with stencil structure
+    n, P = A0.n, 2
+    rp, ci, va = A0.rp, A0.ci.astype(np.int32), A0.va
+    cuts = [0, n // 2, n]
+    blocks = [(cuts[r], rp[cuts[r]:cuts[r + 1] + 1] - rp[cuts[r]], ci[rp[cuts[r]]:rp[cuts[r + 1]]],
+               va[rp[cuts[r]]:rp[cuts[r + 1]]]) for r in range(P)]
+    G = LoopbackGroup.csr(blocks, n)
+    G.set_option("bench", 1)
+    G.set_option("rr_auto", 1)
+    xs = problems.x_star(n, 0)
+    b = orc.spmv(A0, xs)
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=0.0, maxit=250, gap=True)
+    fr, rrl = G.ranks[0].rr_info(res.iters)
+    ref = orc.pbicgstab(A0, b, tol=0.0, maxit=250, bench=True, auto_rr=True)
+    assert len(ref.rr_iters) >= 1
+    check_auto(res, fr, rrl, ref, xs)
+    G.close()
 
 
 @pytest.mark.parametrize("P", [2, 3])

@@ -136,11 +136,7 @@ def test_degenerate_and_errors(S, orc):
         assert (r.iters, r.outcome) == (ref.iters, ref.outcome)
         assert np.array_equal(r.rnorm, ref.rnorm)
         assert np.array_equal(r.x.cpu().numpy(), ref.x)
-    # CSR handles and nx > 1024 reject methods 1/2 (tile kernels only)
-    P = problems.csr_band(5000, nnz_row=9, band=50, seed=1)
-    cs = S.csr(P.n, P.row_ptr, P.col, P.val)
-    with pytest.raises(PbicgError):
-        cs.set_option("method", 1)
+    # stencils with nx > 1024 reject methods 1/2 (tile kernels only)
     wide = S.stencil(2, 1500, 4, 1, problems.cfg2_coef())
     with pytest.raises(PbicgError):
         wide.set_option("method", 2)
@@ -178,3 +174,83 @@ def test_classic_fullsize_cfg3_first_iterations(S, orc):
     res = solver.solve(b_d, tol=0.0, maxit=3, gap=True)
     ref = orc.bicgstab(A, b, tol=0.0, maxit=3, bench=True)
     check_parity(res, ref, xs)
+
+
+def _csr_case(S, orc, spd, band, n=20000, seed=1):
+    """CSR band matrix; spd => symmetrised (A + A^T)/2 with the dominant diagonal
+    kept (p-CG needs SPD)."""
+    P = problems.csr_band(n, nnz_row=27, band=band, seed=seed)
+    rp, ci, va = P.row_ptr, P.col, P.val
+    if spd:
+        import scipy.sparse as sp
+        M = sp.csr_matrix((va, ci, rp), shape=(n, n))
+        M = ((M + M.T) * 0.5).tocsr()
+        M.sort_indices()
+        d = np.asarray(abs(M).sum(axis=1)).ravel()
+        M.setdiag(0)
+        M.eliminate_zeros()
+        M = (M + sp.diags(1.2 * np.asarray(abs(M).sum(axis=1)).ravel() + 1.0)).tocsr()
+        M.sort_indices()
+        rp, ci, va = M.indptr.astype(np.int64), M.indices.astype(np.int32), M.data
+    solver = S.csr(n, rp, ci, va)
+    A = orc.csr(rp, ci, va)
+    xs = problems.x_star(n, 0)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    return solver, A, xs, b, b_d, (rp, ci, va)
+
+
+@pytest.mark.parametrize("band", [500, 6000])  # window SpMV / gather SpMV
+@pytest.mark.parametrize("method", [1, 2])
+def test_methods_csr_parity(S, orc, method, band):
+    solver, A, xs, b, b_d, _ = _csr_case(S, orc, method == 2, band)
+    solver.set_option("method", method)
+    res = solver.solve(b_d, tol=1e-12, maxit=200, gap=True)
+    ref = ref_of(orc, method, A, b, tol=1e-12, maxit=200)
+    assert res.outcome == ref.outcome
+    check_parity(res, ref, xs)
+
+
+def test_methods_csr_ragged_rows_bench(S, orc):
+    """Stencil written out as CSR (3-5 entries per row), 300 fixed iterations."""
+    A0 = orc.stencil_csr(2, 23, 19, 1, problems.poisson2d_coef())
+    solver = S.csr(A0.n, A0.rp, A0.ci.astype(np.int32), A0.va)
+    xs = problems.x_star(A0.n, 1)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A0, xs)
+    solver.set_option("bench", 1)
+    for method in (1, 2):
+        solver.set_option("method", method)
+        res = solver.solve(b_d, tol=0.0, maxit=300, gap=True)
+        ref = ref_of(orc, method, A0, b, tol=0.0, maxit=300, bench=True)
+        check_parity(res, ref, xs, bitwise=False)
+        k = np.nonzero(ref.rnorm < 1e-16 * ref.rnorm[0])[0]
+        k = int(k[0]) if k.size else ref.iters + 1
+        assert np.array_equal(res.rnorm[:k], ref.rnorm[:k])
+
+
+@pytest.mark.parametrize("P", [2, 3])
+@pytest.mark.parametrize("method", [1, 2])
+def test_methods_csr_loopback(S, orc, P, method):
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    n = 3 * 8192
+    solver, A, xs, b, b_d, (rp, ci, va) = _csr_case(S, orc, method == 2, 1000, n=n)
+    solver.close()
+    cuts = [n * r // P for r in range(P + 1)]
+    blocks = []
+    for r in range(P):
+        lo, hi = cuts[r], cuts[r + 1]
+        blocks.append((lo, rp[lo:hi + 1] - rp[lo], ci[rp[lo]:rp[hi]], va[rp[lo]:rp[hi]]))
+    G = LoopbackGroup.csr(blocks, n)
+    G.set_option("method", method)
+    overlap_runs = []
+    for ov in (1, 0):
+        G.set_option("overlap", ov)
+        bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+        res = G.solve(bs, tol=1e-12, maxit=150, gap=True)
+        ref = ref_of(orc, method, A, b, tol=1e-12, maxit=150)
+        check_parity(res, ref, xs)
+        overlap_runs.append(res)
+    assert np.array_equal(overlap_runs[0].rnorm, overlap_runs[1].rnorm)
+    G.close()
