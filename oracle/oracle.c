@@ -104,9 +104,125 @@ int orc_jacobi_dinv(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
   return 0;
 }
 
-/* v := M^{-1} u, pointwise fl(dinv_j * u_j). */
-static void prec(int64_t n, const double* dinv, const double* u, double* v) {
-  for (int64_t j = 0; j < n; ++j) v[j] = dinv[j] * u[j];
+/* ------------------------------------------------------------------------- */
+/* Preconditioner M^{-1} (reading A33).  flags bits 8-15 =  */
+/* block size b: b <= 1 is Jacobi (A3), M^{-1} u = fl(dinv_j * u_j); b >= 2 is   */
+/* block Jacobi with the b x b diagonal blocks of A over rows [kb, (k+1)b)      */
+/* ("block preconditioners"): the blocks are inverted once by plain      */
+/* Gauss-Jordan elimination without pivoting and applied as                    */
+/* (M^{-1}u)_i = sum_k inv_ik u_{kb+k}, ascending k from +0.0.                  */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t n;
+  int b;
+  double* inv; /* b = 1: dinv[n]; else row-major [n][b]: row i of its block's inverse */
+} Prec;
+
+#define ORC_BLOCK(flags) (((flags) >> 8) & 0xff)
+
+/* Gauss-Jordan inverse of the dense b x b matrix a (row-major, destroyed) into e.
+ * Returns -1 on a zero pivot. */
+int orc_gauss_jordan(int b, double* a, double* e) {
+  for (int r = 0; r < b; ++r)
+    for (int c = 0; c < b; ++c) e[r * b + c] = (r == c) ? 1.0 : 0.0;
+  for (int p = 0; p < b; ++p) {
+    const double piv = a[p * b + p];
+    if (piv == 0.0 || !isfinite(piv)) return -1;
+    const double f = 1.0 / piv;
+    for (int c = 0; c < b; ++c) {
+      a[p * b + c] = a[p * b + c] * f;
+      e[p * b + c] = e[p * b + c] * f;
+    }
+    for (int r = 0; r < b; ++r) {
+      if (r == p) continue;
+      const double g = a[r * b + p];
+      for (int c = 0; c < b; ++c) {
+        a[r * b + c] = a[r * b + c] - g * a[p * b + c];
+        e[r * b + c] = e[r * b + c] - g * e[p * b + c];
+      }
+    }
+  }
+  return 0;
+}
+
+static int prec_make(int32_t flags, int64_t n, const int64_t* rp, const int64_t* ci,
+                     const double* va, Prec* P) {
+  const int b = ORC_BLOCK(flags) > 1 ? ORC_BLOCK(flags) : 1;
+  P->n = n;
+  P->b = b;
+  P->inv = (double*)calloc((size_t)(n > 0 ? n : 1) * (size_t)b, sizeof(double));
+  if (b == 1) {
+    if (orc_jacobi_dinv(n, rp, ci, va, P->inv) != 0) { free(P->inv); return -1; }
+    return 0;
+  }
+  if (n % b != 0) { free(P->inv); return -1; }
+  double* a = (double*)calloc((size_t)b * b, sizeof(double));
+  double* e = (double*)calloc((size_t)b * b, sizeof(double));
+  for (int64_t k0 = 0; k0 < n; k0 += b) {
+    for (int q = 0; q < b * b; ++q) a[q] = 0.0;
+    for (int r = 0; r < b; ++r)
+      for (int64_t p = rp[k0 + r]; p < rp[k0 + r + 1]; ++p)
+        if (ci[p] >= k0 && ci[p] < k0 + b) a[r * b + (ci[p] - k0)] = va[p];
+    if (orc_gauss_jordan(b, a, e) != 0) { free(a); free(e); free(P->inv); return -1; }
+    for (int r = 0; r < b; ++r)
+      for (int c = 0; c < b; ++c) P->inv[(size_t)(k0 + r) * b + c] = e[r * b + c];
+  }
+  free(a);
+  free(e);
+  return 0;
+}
+
+/* v := M^{-1} u */
+static void pprec(const Prec* P, const double* u, double* v) {
+  const int b = P->b;
+  if (b == 1) {
+    for (int64_t j = 0; j < P->n; ++j) v[j] = P->inv[j] * u[j];
+    return;
+  }
+  for (int64_t j = 0; j < P->n; ++j) {
+    const int64_t k0 = j - j % b;
+    double acc = 0.0;
+    for (int k = 0; k < b; ++k) acc = acc + P->inv[(size_t)j * b + k] * u[k0 + k];
+    v[j] = acc;
+  }
+}
+
+/* ||M^{-1}||_2 <= max over blocks of sqrt(||B^-1||_1 ||B^-1||_inf) (b = 1: max |dinv|),
+ * with row / column sums in ascending order (reading A29 for M^{-1}). */
+static double prec_norm_bound(const Prec* P) {
+  const int b = P->b;
+  double mx = 0.0;
+  if (b == 1) {
+    for (int64_t j = 0; j < P->n; ++j)
+      if (fabs(P->inv[j]) > mx) mx = fabs(P->inv[j]);
+    return mx;
+  }
+  for (int64_t k0 = 0; k0 < P->n; k0 += b) {
+    double rmax = 0.0, cmax = 0.0;
+    for (int r = 0; r < b; ++r) {
+      double rs = 0.0;
+      for (int c = 0; c < b; ++c) rs = rs + fabs(P->inv[(size_t)(k0 + r) * b + c]);
+      if (rs > rmax) rmax = rs;
+    }
+    for (int c = 0; c < b; ++c) {
+      double cs = 0.0;
+      for (int r = 0; r < b; ++r) cs = cs + fabs(P->inv[(size_t)(k0 + r) * b + c]);
+      if (cs > cmax) cmax = cs;
+    }
+    const double nb = sqrt(cmax * rmax);
+    if (nb > mx) mx = nb;
+  }
+  return mx;
+}
+
+/* v := M^{-1} u for tests (flags as the solvers'); -1 if M cannot be formed. */
+int orc_prec_apply(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+                   int32_t flags, const double* u, double* v) {
+  Prec P;
+  if (prec_make(flags, n, rp, ci, va, &P) != 0) return -1;
+  pprec(&P, u, v);
+  free(P.inv);
+  return 0;
 }
 
 /* Constant-coefficient 5-point (dim=2) / 7-point (dim=3) stencil written out
@@ -226,8 +342,8 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
                   double* sc_trace, double* vec_trace, double* bound_trace,
                   int32_t* rr_list, int32_t* n_rr) {
   if (n < 0 || maxit < 0 || rr_period < 0) return -2;
-  double* dinv = vec(n);
-  if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
+  Prec P;
+  if (prec_make(flags, n, rp, ci, va, &P) != 0) return -1;
   double *r = vec(n), *rh = vec(n), *k = vec(n), *w = vec(n), *m = vec(n), *t = vec(n);
   double *g = vec(n), *s = vec(n), *l = vec(n), *z = vec(n), *nn = vec(n), *v = vec(n);
   double *q = vec(n), *u = vec(n), *y = vec(n), *tmp = vec(n);
@@ -239,9 +355,9 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
   orc_spmv(n, rp, ci, va, x, tmp);
   for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
   memcpy(rh, r, (size_t)n * sizeof(double)); /* A2: shadow residual r^ := r0 */
-  prec(n, dinv, r, k);
+  pprec(&P, r, k);
   orc_spmv(n, rp, ci, va, k, w);
-  prec(n, dinv, w, m);
+  pprec(&P, w, m);
   /* line 3: t0 := A m0; alpha0 := (r0,r0)/(r0,w0); beta0 := 0 */
   orc_spmv(n, rp, ci, va, m, t);
   double rho = dotf(flags, n, rh, r);
@@ -258,16 +374,14 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
   int rr_next = 0, nrr = 0;
   if (fauto) {
     int64_t mu = 0;
-    double mi = 0.0;
-    for (int64_t j = 0; j < n; ++j) {
+    const double mi = prec_norm_bound(&P); /* ||M^-1|| (A29) */
+    for (int64_t j = 0; j < n; ++j)
       if (rp[j + 1] - rp[j] > mu) mu = rp[j + 1] - rp[j];
-      if (fabs(dinv[j]) > mi) mi = fabs(dinv[j]);
-    }
     ar.eps = ldexp(1.0, -53);
     ar.tau = sqrt(ar.eps);
     ar.nA = orc_anorm_bound(n, rp, ci, va);
     ar.muN = (double)mu * sqrt((double)n);
-    ar.mutN = 1.0 * sqrt((double)n) * mi;
+    ar.mutN = (double)P.b * sqrt((double)n) * mi; /* mu~ = b nonzeros per row of M^-1 */
     ar.f = ((ar.muN + 1.0) * ar.nA * nrm2(n, x) + nb) * ar.eps;  /* P:262 */
     ar.f_prev = ar.f;
     ar.Dw = ar.muN * ar.nA * nrm2(n, k) * ar.eps;                 /* P:281 */
@@ -322,7 +436,7 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     double qy = dotf(flags, n, q, y);
     double yy = dotf(flags, n, y, y);
     /* lines 13-14: n := M^-1 z; v := A n */
-    prec(n, dinv, z, nn);
+    pprec(&P, z, nn);
     orc_spmv(n, rp, ci, va, nn, v);
     if (vec_trace) {
       double* T = vec_trace + (size_t)i * NTRACE * (size_t)n;
@@ -380,10 +494,10 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     if (fire) {
       orc_spmv(n, rp, ci, va, x, tmp);
       for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
-      prec(n, dinv, r, k);
+      pprec(&P, r, k);
       orc_spmv(n, rp, ci, va, k, w);
       orc_spmv(n, rp, ci, va, g, s);
-      prec(n, dinv, s, l);
+      pprec(&P, s, l);
       orc_spmv(n, rp, ci, va, l, z);
       if (fauto) {
         /* gaps of the explicit recomputation (reading A31) */
@@ -402,7 +516,7 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     double dz = dotf(flags, n, rh, z);
     rhist[i + 1] = sqrt(dotf(flags, n, r, r));
     /* lines 22-23: m := M^-1 w; t := A m */
-    prec(n, dinv, w, m);
+    pprec(&P, w, m);
     orc_spmv(n, rp, ci, va, m, t);
     if (fgap) gaphist[i + 1] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
     iters = i + 1;
@@ -444,7 +558,7 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
   *iters_out = iters;
   *outcome_out = outcome;
   if (n_rr) *n_rr = nrr;
-  free(dinv); free(r); free(rh); free(k); free(w); free(m); free(t); free(g); free(s);
+  free(P.inv); free(r); free(rh); free(k); free(w); free(m); free(t); free(g); free(s);
   free(l); free(z); free(nn); free(v); free(q); free(u); free(y); free(tmp);
   return 0;
 }
@@ -459,8 +573,8 @@ int orc_bicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double* 
                  double* x, double* rhist, double* gaphist, int32_t* iters_out,
                  int32_t* outcome_out, double* sc_trace) {
   if (n < 0 || maxit < 0) return -2;
-  double* dinv = vec(n);
-  if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
+  Prec P;
+  if (prec_make(flags, n, rp, ci, va, &P) != 0) return -1;
   double *r = vec(n), *rh = vec(n), *p = vec(n), *g = vec(n), *s = vec(n), *q = vec(n);
   double *u = vec(n), *y = vec(n), *tmp = vec(n);
   int fgap = (flags & ORC_GAP) && gaphist;
@@ -478,12 +592,12 @@ int orc_bicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double* 
   int done = 0;
   if (rhist[0] <= tol * nb && !(flags & ORC_BENCH)) { outcome = OUT_CONVERGED; done = 1; }
   for (int32_t i = 0; i < maxit && !done; ++i) {
-    prec(n, dinv, p, g);                   /* line 4 */
+    pprec(&P, p, g);                   /* line 4 */
     orc_spmv(n, rp, ci, va, g, s);         /* line 5 */
     double rs = dotf(flags, n, rh, s);     /* line 6 */
     double alpha = rho / rs;               /* line 7 */
     for (int64_t j = 0; j < n; ++j) q[j] = r[j] - alpha * s[j]; /* line 8 */
-    prec(n, dinv, q, u);                   /* line 9 */
+    pprec(&P, q, u);                   /* line 9 */
     orc_spmv(n, rp, ci, va, u, y);         /* line 10 */
     double qy = dotf(flags, n, q, y);      /* line 11 */
     double yy = dotf(flags, n, y, y);
@@ -507,7 +621,7 @@ int orc_bicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double* 
   }
   *iters_out = iters;
   *outcome_out = outcome;
-  free(dinv); free(r); free(rh); free(p); free(g); free(s); free(q); free(u); free(y); free(tmp);
+  free(P.inv); free(r); free(rh); free(p); free(g); free(s); free(q); free(u); free(y); free(tmp);
   return 0;
 }
 
@@ -519,14 +633,14 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
             const double* b, const double* x0, double tol, int32_t maxit, int32_t flags,
             double* x, double* rhist, double* gaphist, int32_t* iters_out,
             int32_t* outcome_out) {
-  double* dinv = vec(n);
-  if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
+  Prec P;
+  if (prec_make(flags, n, rp, ci, va, &P) != 0) return -1;
   double *r = vec(n), *u = vec(n), *p = vec(n), *s = vec(n), *tmp = vec(n);
   int fgap = (flags & ORC_GAP) && gaphist;
   memcpy(x, x0, (size_t)n * sizeof(double));
   orc_spmv(n, rp, ci, va, x, tmp);
   for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
-  prec(n, dinv, r, u);
+  pprec(&P, r, u);
   memcpy(p, u, (size_t)n * sizeof(double));
   double gam = dotf(flags, n, r, u);
   double nb = sqrt(dotf(flags, n, b, b));
@@ -539,7 +653,7 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
     orc_spmv(n, rp, ci, va, p, s);
     double alpha = gam / dotf(flags, n, p, s);
     for (int64_t j = 0; j < n; ++j) { x[j] = x[j] + alpha * p[j]; r[j] = r[j] - alpha * s[j]; }
-    prec(n, dinv, r, u);
+    pprec(&P, r, u);
     double gam1 = dotf(flags, n, r, u);
     rhist[i + 1] = sqrt(dotf(flags, n, r, r));
     if (fgap) gaphist[i + 1] = res_gap(flags, n, rp, ci, va, b, x, r, tmp);
@@ -552,7 +666,7 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
   }
   *iters_out = iters;
   *outcome_out = outcome;
-  free(dinv); free(r); free(u); free(p); free(s); free(tmp);
+  free(P.inv); free(r); free(u); free(p); free(s); free(tmp);
   return 0;
 }
 
@@ -567,15 +681,15 @@ int orc_pipecg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va
                const double* b, const double* x0, double tol, int32_t maxit, int32_t flags,
                double* x, double* rhist, double* gaphist, int32_t* iters_out,
                int32_t* outcome_out) {
-  double* dinv = vec(n);
-  if (orc_jacobi_dinv(n, rp, ci, va, dinv) != 0) { free(dinv); return -1; }
+  Prec P;
+  if (prec_make(flags, n, rp, ci, va, &P) != 0) return -1;
   double *r = vec(n), *u = vec(n), *w = vec(n), *m = vec(n), *nn = vec(n);
   double *z = vec(n), *q = vec(n), *s = vec(n), *p = vec(n), *tmp = vec(n);
   int fgap = (flags & ORC_GAP) && gaphist;
   memcpy(x, x0, (size_t)n * sizeof(double));
   orc_spmv(n, rp, ci, va, x, tmp);
   for (int64_t j = 0; j < n; ++j) r[j] = b[j] - tmp[j];
-  prec(n, dinv, r, u);
+  pprec(&P, r, u);
   orc_spmv(n, rp, ci, va, u, w);
   double nb = sqrt(dotf(flags, n, b, b));
   rhist[0] = sqrt(dotf(flags, n, r, r));
@@ -587,7 +701,7 @@ int orc_pipecg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va
   for (int32_t i = 0; i < maxit && !done; ++i) {
     double gam = dotf(flags, n, r, u);
     double del = dotf(flags, n, w, u);
-    prec(n, dinv, w, m);
+    pprec(&P, w, m);
     orc_spmv(n, rp, ci, va, m, nn);
     double beta, alpha;
     if (i == 0) { beta = 0.0; alpha = gam / del; }
@@ -612,7 +726,7 @@ int orc_pipecg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va
   }
   *iters_out = iters;
   *outcome_out = outcome;
-  free(dinv); free(r); free(u); free(w); free(m); free(nn); free(z); free(q); free(s); free(p);
+  free(P.inv); free(r); free(u); free(w); free(m); free(nn); free(z); free(q); free(s); free(p);
   free(tmp);
   return 0;
 }

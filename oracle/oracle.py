@@ -59,6 +59,10 @@ def lib():
                                     P, P, P]
         L.orc_anorm_bound.restype = f64
         L.orc_anorm_bound.argtypes = [i64, P, P, P]
+        L.orc_prec_apply.restype = ctypes.c_int
+        L.orc_prec_apply.argtypes = [i64, P, P, P, i32, P, P]
+        L.orc_gauss_jordan.restype = ctypes.c_int
+        L.orc_gauss_jordan.argtypes = [ctypes.c_int, P, P]
         L.orc_bicgstab.restype = ctypes.c_int
         L.orc_bicgstab.argtypes = [i64, P, P, P, P, P, f64, i32, i32, P, P, P, P, P, P]
         for name in ("orc_pcg", "orc_pipecg"):
@@ -180,13 +184,22 @@ def _run(fn, A: CSR, b, x0, tol, maxit, flags, extra=(), want_sc=False, want_tra
                   None if rl is None else [int(v) for v in rl[:nrr.value]])
 
 
+def _blk(block: int) -> int:
+    """flags bits 8-15: block size of the block-Jacobi preconditioner (1 = Jacobi)."""
+    if not 1 <= block <= 255:
+        raise ValueError("block size must be in 1..255")
+    return (block if block > 1 else 0) << 8
+
+
 def pbicgstab(A: CSR, b, x0=None, tol=0.0, maxit=100, rr_period=0, bench=False,
               plain_dot=False, gap=True, want_scalars=False, want_trace=False,
-              auto_rr=False) -> Result:
+              auto_rr=False, block=1) -> Result:
     """Alg. 2 with periodic replacement or, with auto_rr, the
     automated replacement of P:609-623 (bound f^r_i history in .bounds, replacement
-    iterations in .rr_iters), and the gap history."""
-    flags = (BENCH if bench else 0) | (PLAIN_DOT if plain_dot else 0) | (AUTO_RR if auto_rr else 0)
+    iterations in .rr_iters), and the gap history.  block > 1: block-Jacobi
+    preconditioner with block x block diagonal blocks (reading A33)."""
+    flags = ((BENCH if bench else 0) | (PLAIN_DOT if plain_dot else 0) |
+             (AUTO_RR if auto_rr else 0) | _blk(block))
     return _run("orc_pbicgstab", A, b, x0, tol, maxit, flags, extra=(int(rr_period),),
                 want_sc=want_scalars, want_trace=want_trace, gap=gap, want_bounds=auto_rr)
 
@@ -197,15 +210,34 @@ def anorm_bound(A: CSR) -> float:
 
 
 def bicgstab(A: CSR, b, x0=None, tol=0.0, maxit=100, bench=False, plain_dot=False, gap=True,
-             want_scalars=False) -> Result:
+             want_scalars=False, block=1) -> Result:
     """Alg. 1 (P:66-91)."""
-    flags = (BENCH if bench else 0) | (PLAIN_DOT if plain_dot else 0)
+    flags = (BENCH if bench else 0) | (PLAIN_DOT if plain_dot else 0) | _blk(block)
     return _run("orc_bicgstab", A, b, x0, tol, maxit, flags, want_sc=want_scalars, gap=gap)
 
 
-def pcg(A: CSR, b, x0=None, tol=0.0, maxit=100, bench=False, gap=True) -> Result:
-    return _run("orc_pcg", A, b, x0, tol, maxit, BENCH if bench else 0, gap=gap)
+def pcg(A: CSR, b, x0=None, tol=0.0, maxit=100, bench=False, gap=True, block=1) -> Result:
+    return _run("orc_pcg", A, b, x0, tol, maxit, (BENCH if bench else 0) | _blk(block), gap=gap)
 
 
-def pipecg(A: CSR, b, x0=None, tol=0.0, maxit=100, bench=False, gap=True) -> Result:
-    return _run("orc_pipecg", A, b, x0, tol, maxit, BENCH if bench else 0, gap=gap)
+def pipecg(A: CSR, b, x0=None, tol=0.0, maxit=100, bench=False, gap=True, block=1) -> Result:
+    return _run("orc_pipecg", A, b, x0, tol, maxit, (BENCH if bench else 0) | _blk(block),
+                gap=gap)
+
+
+def prec_apply(A: CSR, u, block=1) -> np.ndarray:
+    """M^{-1} u with the oracle's preconditioner (Jacobi or block Jacobi, A3 / A33)."""
+    u = _f64(u)
+    v = np.zeros(A.n)
+    if lib().orc_prec_apply(A.n, _p(A.rp), _p(A.ci), _p(A.va), _blk(block), _p(u), _p(v)) != 0:
+        raise ValueError("preconditioner undefined (zero pivot / block size)")
+    return v
+
+
+def gauss_jordan(B) -> np.ndarray:
+    """The oracle's Gauss-Jordan inverse of a small dense matrix (no pivoting)."""
+    a = np.ascontiguousarray(B, dtype=np.float64).copy()
+    e = np.zeros_like(a)
+    if lib().orc_gauss_jordan(a.shape[0], _p(a), _p(e)) != 0:
+        raise ValueError("zero pivot")
+    return e

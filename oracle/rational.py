@@ -53,7 +53,11 @@ def add(x: Vec, y: Vec) -> Vec:
     return [a + b for a, b in zip(x, y)]
 
 
-def prec(dinv: Vec, v: Vec) -> Vec:
+def prec(dinv, v: Vec) -> Vec:
+    """M^{-1} v: diag(dinv) (Jacobi, a vector) or a dense matrix M^{-1} (a list of
+    rows, e.g. the block-diagonal inverse of block Jacobi, reading A33)."""
+    if dinv and isinstance(dinv[0], list):
+        return matvec(dinv, v)
     return [d * a for d, a in zip(dinv, v)]
 
 

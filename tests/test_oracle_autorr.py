@@ -175,3 +175,21 @@ def test_auto_rr_off_is_unchanged(orc):
     r0 = orc.pbicgstab(A, b, tol=0.0, maxit=6, bench=True)
     assert r1.rr_iters == []
     assert np.array_equal(r1.rnorm, r0.rnorm) and np.array_equal(r1.x, r0.x)
+
+
+def test_bounds_dominate_exact_gaps_block_jacobi(orc):
+    """Same dominance with the block-Jacobi preconditioner (mu~ = b, ||M^-1|| bound
+    over the inverse blocks, reading A33)."""
+    A = orc.stencil_csr(2, 8, 5, 1, problems.cfg2_coef())
+    xs = problems.x_star(A.n, seed=2)
+    b = orc.spmv(A, xs)
+    res = orc.pbicgstab(A, b, tol=0.0, maxit=14, bench=True, want_trace=True, auto_rr=True,
+                        block=4)
+    Af = R.fmat(A.dense())
+    bf = R.fvec(b)
+    idx = {nm: j for j, nm in enumerate(NAMES)}
+    V = lambda i, nm: R.fvec(res.trace[i, idx[nm]])
+    for i in range(res.iters):
+        x, r, k, w = V(i, "x"), V(i, "r"), V(i, "k"), V(i, "w")
+        assert nrm(R.sub(R.sub(bf, R.matvec(Af, x)), r)) <= res.bounds[i, 0]
+        assert nrm(R.sub(R.matvec(Af, k), w)) <= res.bounds[i, 1]
