@@ -216,7 +216,7 @@ def setup_solver(args, cfg, st, rank, world, dev, stream):
     if world == 1:
         if isinstance(st, CsrShape):
             M = csr_matrix(cfg)
-            return Solver.csr(st.n, M.row_ptr, M.col, M.val, stream=stream)
+            return Solver.csr(st.n, M.row_ptr, M.col, M.val, stream=stream, block=args.block)
         return Solver.stencil(st.dim, st.nx, st.ny, st.nz, method_coef(args, st), stream=stream)
     ids = [binding.nccl_unique_id(), binding.nccl_unique_id()] if rank == 0 else [None, None]
     torch.distributed.broadcast_object_list(ids, src=0)
@@ -226,7 +226,8 @@ def setup_solver(args, cfg, st, rank, world, dev, stream):
         lo, hi = st.n * rank // world, st.n * (rank + 1) // world
         rp = M.row_ptr[lo:hi + 1] - M.row_ptr[lo]
         sl = slice(int(M.row_ptr[lo]), int(M.row_ptr[hi]))
-        return Solver.csr(st.n, rp, M.col[sl], M.val[sl], row_begin=lo, stream=stream, dist=dist)
+        return Solver.csr(st.n, rp, M.col[sl], M.val[sl], row_begin=lo, stream=stream, dist=dist,
+                          block=args.block)
     return Solver.stencil(st.dim, st.nx, st.ny, st.nz, method_coef(args, st), stream=stream,
                           dist=dist)
 
@@ -349,6 +350,7 @@ def run_ours(args, rank, world):
                    "grid": [st.nx, st.ny, st.nz] if st.dim else "csr 27 nnz/row, band 4096",
                    "maxit_per_step": maxit, "rr_period": rr, "gap_tracking": gap,
                    "rr_auto": bool(args.rr_auto),
+                   "preconditioner": "jacobi" if args.block == 1 else f"block-jacobi {args.block}",
                    "method": args.method,
                    "schedule": SCHEDULES[args.method] if st.dim else
                                "split 4-phase (CSR as ELL), reduction #1 overlapped",
@@ -415,6 +417,8 @@ def main():
     ap.add_argument("--method", choices=["pbicgstab", "bicgstab", "pipecg"], default="pbicgstab",
                     help="solver: p-BiCGStab (the headline), classic BiCGStab or p-CG")
     ap.add_argument("--gap", type=int, default=0)
+    ap.add_argument("--block", type=int, default=1,
+                    help="CSR configs: block-Jacobi block size (1 = Jacobi)")
     ap.add_argument("--rr-auto", type=int, default=0,
                     help="automated residual replacement (bound f^r + eq:criterion) instead of "
                          "the periodic schedule")

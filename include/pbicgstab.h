@@ -49,7 +49,19 @@ typedef enum {
   PBICG_BREAKDOWN = 2  /* non-finite or zero scalar denominator (A9); x = last finite iterate */
 } pbicg_outcome;
 
-typedef enum { PBICG_PREC_JACOBI = 1 } pbicg_prec; /* M = diag(A), dinv_j = 1/a_jj (A3) */
+/* Preconditioner M (reading A3 / A33):
+ *   PBICG_PREC_JACOBI        M = diag(A), applied as fl(dinv_j v_j), dinv_j = 1/a_jj
+ *   PBICG_PREC_BJ(b)         block Jacobi ("block preconditioners"; SURVEY
+ *                            NEXT-4), b in {2,4,8,16,32}: M = the b x b diagonal blocks
+ *                            of A over rows [kb, (k+1)b) (global numbering), each
+ *                            inverted once by Gauss-Jordan elimination without
+ *                            pivoting; (M^-1 v)_i = sum_k inv_ik v_{kb+k}, ascending k.
+ *                            CSR operators only (stencils: EINVAL); every rank's
+ *                            row_begin and n_local must be multiples of b; a zero
+ *                            pivot is EINVAL.  Costs b-1 extra doubles per row read
+ *                            in each kernel that applies M^-1. */
+typedef enum { PBICG_PREC_JACOBI = 1, PBICG_PREC_BLOCK_JACOBI = 0x100 } pbicg_prec;
+#define PBICG_PREC_BJ(b) ((pbicg_prec)(PBICG_PREC_BLOCK_JACOBI | (b)))
 
 /* Matrix-free constant-coefficient stencil (Table 1 shapes).
  *   dim = 2: 5-point on an nx x ny grid (nz ignored, treated as 1)

@@ -17,6 +17,7 @@ NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",            # no FMA contraction anywhere (reading A4)
+    "-Xcompiler", "-ffp-contract=off",  # host-side constants (block inverses, bounds) too
     "-Xcompiler", "-fPIC", "-shared",
     "-diag-suppress", "177",
 ]

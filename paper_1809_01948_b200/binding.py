@@ -20,6 +20,11 @@ OUTCOMES = {0: "converged", 1: "maxit", 2: "breakdown"}
 KERNELS = ["init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap", "apply", "fin",
            "cl1", "cl2", "cl3", "pcg"]
 # option "method": 0 p-BiCGStab (Alg. 2), 1 classic BiCGStab (Alg. 1), 2 p-CG (reading A19)
+
+
+def prec_code(block: int) -> int:
+    """pbicg_prec value: 1 = Jacobi, PBICG_PREC_BJ(b) = 0x100 | b (block Jacobi, CSR)."""
+    return 1 if block == 1 else 0x100 | int(block)
 METHODS = {"pbicgstab": 0, "bicgstab": 1, "pipecg": 2}
 
 
@@ -180,15 +185,16 @@ class Solver:
         return cls(h)
 
     @classmethod
-    def csr(cls, n_global: int, row_ptr, col, val, row_begin: int = 0, stream=None, dist=None):
+    def csr(cls, n_global: int, row_ptr, col, val, row_begin: int = 0, stream=None, dist=None,
+            block: int = 1):
         rp = np.ascontiguousarray(row_ptr, dtype=np.int64)
         ci = np.ascontiguousarray(col, dtype=np.int32)
         va = np.ascontiguousarray(val, dtype=np.float64)
         c = _Csr(n_global, row_begin, len(rp) - 1, rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
         h = ctypes.c_void_p()
         d = ctypes.byref(dist) if dist is not None else None
-        _check(lib().pbicgstab_create_csr(ctypes.byref(c), 1, d, _stream_ptr(stream),
-                                          ctypes.byref(h)))
+        _check(lib().pbicgstab_create_csr(ctypes.byref(c), prec_code(block), d,
+                                          _stream_ptr(stream), ctypes.byref(h)))
         return cls(h)
 
     # -- API ------------------------------------------------------------------
@@ -303,7 +309,7 @@ class LoopbackGroup:
         return cls(hs)
 
     @classmethod
-    def csr(cls, blocks, n_global: int, stream=None):
+    def csr(cls, blocks, n_global: int, stream=None, block: int = 1):
         """blocks: list of (row_begin, row_ptr, col, val) per rank, contiguous."""
         keep = []
         arr = (_Csr * len(blocks))()
@@ -314,7 +320,8 @@ class LoopbackGroup:
             keep += [rp, ci, va]
             arr[r] = _Csr(n_global, rb, len(rp) - 1, rp.ctypes.data, ci.ctypes.data, va.ctypes.data)
         hs = (ctypes.c_void_p * len(blocks))()
-        _check(lib().pbicgstab_create_csr_loopback(arr, 1, len(blocks), _stream_ptr(stream), hs))
+        _check(lib().pbicgstab_create_csr_loopback(arr, prec_code(block), len(blocks),
+                                                   _stream_ptr(stream), hs))
         return cls(hs)
 
     def set_option(self, key, value):

@@ -25,7 +25,27 @@ struct CsrOp {
   const double* val;     // [width][n]
   const int32_t* len;    // [n] row lengths, or nullptr when every row has `width` entries
   const double* dinv;    // [n + 2H] ghosted Jacobi inverse diagonal (A3)
+  int32_t bj;            // preconditioner block size: 1 Jacobi, 2..32 block Jacobi (A33)
+  const double* binv;    // bj > 1: [n][bj] row j of its block's inverse (row-major)
 };
+
+// M^{-1} applied to the value v of row j (reading A3 / A33).  Jacobi: fl(dinv_j v).
+// Block Jacobi: the bj rows of a block are bj consecutive lanes of one warp
+// (blocks are aligned and n_local % bj == 0), so the block's values are read by
+// shuffles and (M^{-1}v)_j = sum_k binv_jk v_{kb+k}, ascending k from +0.0 -- the
+// oracle's order.  Every lane of the warp must call it (warp-uniform loops, WROW_LOOP).
+__device__ __forceinline__ double prec_row(const CsrOp& A, int64_t j, bool in, double v) {
+  if (A.bj == 1) return in ? A.dinv[j] * v : 0.0;
+  const int lane = threadIdx.x & 31;
+  const int base = lane & ~(A.bj - 1);
+  const double* __restrict__ row = A.binv + (in ? j : 0) * A.bj;
+  double acc = 0.0;
+  for (int k = 0; k < A.bj; ++k) {
+    const double vk = __shfl_sync(0xffffffffu, v, base + k);
+    acc = acc + (in ? __ldg(row + k) : 0.0) * vk;
+  }
+  return acc;
+}
 
 // fl(A v)_j or fl(A M^-1 v)_j, summed left to right in stored (ascending
 // column) order from +0.0 (A5).  Slots are processed in groups of ELL_U with all
@@ -62,6 +82,15 @@ __device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restri
 
 #define ROW_LOOP for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < A.n; \
                       j += (int64_t)gridDim.x * blockDim.x)
+// warp-uniform variant for steps that apply M^{-1} (prec_row shuffles): the whole
+// warp iterates while any lane has a row; `in` marks the lanes that do
+// (every prec_row call sits in converged code: loads/stores are predicated on `in`)
+#define WROW_LOOP                                                                     \
+  for (int64_t j0_ = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31; \
+       j0_ < A.n; j0_ += (int64_t)gridDim.x * blockDim.x) {                          \
+    const int64_t j = j0_ + (threadIdx.x & 31);                                       \
+    const bool in = j < A.n;
+#define WROW_END }
 
 // NRM (automated replacement): the step's reduction also carries the
 // sums of squares of the vectors the bound f^r needs (plain fp64, reading A30)
@@ -74,20 +103,22 @@ __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict
   Dd acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
-  ROW_LOOP {
-    const double bj = V.b[j];
-    const double rj = bj - ell_row<false>(A, V.x, j);
-    const double kj = A.dinv[j] * rj;
-    V.r[j] = rj;
-    V.rh[j] = rj;
-    V.k[j] = kj;
-    dd_fma(acc[0], rj, rj);
-    dd_fma(acc[1], bj, bj);
-    if (NRM) {
-      c_nrm(acc[2 % K], V.x[j]);
-      c_nrm(acc[3 % K], kj);
+  WROW_LOOP
+    const double bj = in ? V.b[j] : 0.0;
+    const double rj = in ? bj - ell_row<false>(A, V.x, j) : 0.0;
+    const double kj = prec_row(A, j, in, rj);  // k0 := M^-1 r0
+    if (in) {
+      V.r[j] = rj;
+      V.rh[j] = rj;
+      V.k[j] = kj;
+      dd_fma(acc[0], rj, rj);
+      dd_fma(acc[1], bj, bj);
+      if (NRM) {
+        c_nrm(acc[2 % K], V.x[j]);
+        c_nrm(acc[3 % K], kj);
+      }
     }
-  }
+  WROW_END
   Dd tot[K];
   if (dd_grid_reduce<K>(acc, part, &sc->counter[T_INIT1], tot) && threadIdx.x == 0)
     publish<F_INIT1>(sc, h, tot);
@@ -96,12 +127,15 @@ __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict
 __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                Dd* __restrict__ part, Hist h) {
   Dd acc[1] = {dd_zero()};
-  ROW_LOOP {
-    const double wj = ell_row<true>(A, V.r, j);  // w0 = A M^-1 r0 = A k0
-    V.w0[j] = wj;
-    V.mv[j] = A.dinv[j] * wj;                     // m0 = M^-1 w0 (line 2)
-    dd_fma(acc[0], V.rh[j], wj);
-  }
+  WROW_LOOP
+    const double wj = in ? ell_row<false>(A, V.k, j) : 0.0;  // w0 = A k0 = A M^-1 r0
+    const double mj = prec_row(A, j, in, wj);                // m0 = M^-1 w0 (line 2)
+    if (in) {
+      V.w0[j] = wj;
+      V.mv[j] = mj;
+      dd_fma(acc[0], V.rh[j], wj);
+    }
+  WROW_END
   Dd tot[1];
   if (dd_grid_reduce<1>(acc, part, &sc->counter[T_INIT2], tot) && threadIdx.x == 0)
     publish<F_INIT2>(sc, h, tot);
@@ -118,33 +152,36 @@ __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restric
   Dd acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
-  ROW_LOOP {
-    const double dj = A.dinv[j];
-    const double wc = V.w0[j], zc = V.z0[j];
-    const double zo = rr ? V.zrr[j] : zc;
-    const double m = dj * wc, n = dj * zc;
-    const double t = V.w1[j], v = V.z1[j];
-    const double lj = V.l[j];
-    const double gn = V.k[j] + be * (V.g[j] - om * lj);
-    const double sn = wc + be * (V.s[j] - om * zo);
-    const double ln = m + be * (lj - om * n);
-    const double zn = t + be * (zo - om * v);
-    const double q = V.r[j] - al * sn;
-    const double y = wc - al * zn;
-    dd_fma(acc[0], q, y);
-    dd_fma(acc[1], y, y);
-    if (NRM) {  // k, w, m, t, g, s, l, z, q, y of iteration i
-      c_nrm(acc[2 % K], V.k[j]); c_nrm(acc[3 % K], wc); c_nrm(acc[4 % K], m);
-      c_nrm(acc[5 % K], t); c_nrm(acc[6 % K], gn); c_nrm(acc[7 % K], sn);
-      c_nrm(acc[8 % K], ln); c_nrm(acc[9 % K], zn); c_nrm(acc[10 % K], q);
-      c_nrm(acc[11 % K], y);
+  WROW_LOOP
+    const double wc = in ? V.w0[j] : 0.0, zc = in ? V.z0[j] : 0.0;
+    const double m = prec_row(A, j, in, wc), n = prec_row(A, j, in, zc);  // m_i, n_{i-1}
+    double zn = 0.0;
+    if (in) {
+      const double zo = rr ? V.zrr[j] : zc;
+      const double t = V.w1[j], v = V.z1[j];
+      const double lj = V.l[j];
+      const double gn = V.k[j] + be * (V.g[j] - om * lj);
+      const double sn = wc + be * (V.s[j] - om * zo);
+      const double ln = m + be * (lj - om * n);
+      zn = t + be * (zo - om * v);
+      const double q = V.r[j] - al * sn;
+      const double y = wc - al * zn;
+      dd_fma(acc[0], q, y);
+      dd_fma(acc[1], y, y);
+      if (NRM) {  // k, w, m, t, g, s, l, z, q, y of iteration i
+        c_nrm(acc[2 % K], V.k[j]); c_nrm(acc[3 % K], wc); c_nrm(acc[4 % K], m);
+        c_nrm(acc[5 % K], t); c_nrm(acc[6 % K], gn); c_nrm(acc[7 % K], sn);
+        c_nrm(acc[8 % K], ln); c_nrm(acc[9 % K], zn); c_nrm(acc[10 % K], q);
+        c_nrm(acc[11 % K], y);
+      }
+      V.g[j] = gn;
+      V.s[j] = sn;
+      V.l[j] = ln;
+      V.z0[j] = zn;
     }
-    V.g[j] = gn;
-    V.s[j] = sn;
-    V.l[j] = ln;
-    V.z0[j] = zn;
-    V.nv[j] = dj * zn;  // n_i = M^-1 z_i (line 13)
-  }
+    const double nj = prec_row(A, j, in, zn);  // n_i = M^-1 z_i (line 13)
+    if (in) V.nv[j] = nj;
+  WROW_END
   Dd tot[K];
   if (dd_grid_reduce<K>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
     publish<F_SWEEPA>(sc, h, tot);
@@ -186,8 +223,7 @@ __device__ __forceinline__ void spmv_epi(const CsrOp& A, const Vecs& V, int64_t 
     dd_fma(acc[0], q, y);
     dd_fma(acc[1 % K], y, y);
   } else if (M == SP_PCW0) {
-    V.w0[j] = y;
-    V.mv[j] = A.dinv[j] * y;
+    V.w0[j] = y;  // m0 = M^-1 w0 follows in c_prec_mv (warp-uniform M^-1)
     const double u = V.k[j];
     dd_fma(acc[0], V.r[j], u);
     dd_fma(acc[1 % K], y, u);
@@ -238,10 +274,11 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
   Dd acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
-  ROW_LOOP {
-    const double dj = A.dinv[j];
-    const double wc = V.w0[j], zc = V.z0[j];
-    const double m = dj * wc, n = dj * zc;
+  WROW_LOOP
+    const double wc = in ? V.w0[j] : 0.0, zc = in ? V.z0[j] : 0.0;
+    const double m = prec_row(A, j, in, wc), n = prec_row(A, j, in, zc);  // m_i, n_i
+    double wn = 0.0;
+    if (in) {
     const double t = V.w1[j], v = V.z1[j];
     const double sj = V.s[j];
     const double u = V.k[j] - al * V.l[j];
@@ -251,7 +288,7 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
     const double xn = (xj + al * V.g[j]) + om * u;
     const double rn = q - om * y;
     const double kn = u - om * (m - al * n);
-    const double wn = y - om * (t - al * v);
+    wn = y - om * (t - al * v);
     const double rhj = V.rh[j];
     dd_fma(acc[0], rhj, rn);
     dd_fma(acc[1 % K], rhj, wn);
@@ -266,8 +303,10 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
     V.r[j] = rn;
     V.k[j] = kn;
     V.w0[j] = wn;
-    V.mv[j] = dj * wn;  // m_{i+1} = M^-1 w_{i+1} (line 22)
-  }
+    }
+    const double mn = prec_row(A, j, in, wn);  // m_{i+1} = M^-1 w_{i+1} (line 22)
+    if (in) V.mv[j] = mn;
+  WROW_END
   Dd tot[K];
   if (dd_grid_reduce<K>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0)
     publish<F_SWEEPC>(sc, h, tot);
@@ -279,18 +318,20 @@ __global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__
                                              Dd* __restrict__ part, Hist h) {
   if (sc->done || !sc->rr_fire) return;
   Dd acc[4] = {dd_zero(), dd_zero(), dd_zero(), dd_zero()};
-  ROW_LOOP {
-    const double dj = A.dinv[j];
-    const double rj = V.b[j] - ell_row<false>(A, V.x, j);
-    const double sj = ell_row<false>(A, V.g, j);
-    V.r[j] = rj;
-    V.k[j] = dj * rj;
-    V.s[j] = sj;
-    V.l[j] = dj * sj;
-    if (NRM) {  // replaced x_{i+1}, k_{i+1}, s_i, l_i
-      c_nrm(acc[0], V.x[j]); c_nrm(acc[1], dj * rj); c_nrm(acc[2], sj); c_nrm(acc[3], dj * sj);
+  WROW_LOOP
+    const double rj = in ? V.b[j] - ell_row<false>(A, V.x, j) : 0.0;
+    const double sj = in ? ell_row<false>(A, V.g, j) : 0.0;
+    const double kj = prec_row(A, j, in, rj), lj = prec_row(A, j, in, sj);
+    if (in) {
+      V.r[j] = rj;
+      V.k[j] = kj;
+      V.s[j] = sj;
+      V.l[j] = lj;
+      if (NRM) {  // replaced x_{i+1}, k_{i+1}, s_i, l_i
+        c_nrm(acc[0], V.x[j]); c_nrm(acc[1], kj); c_nrm(acc[2], sj); c_nrm(acc[3], lj);
+      }
     }
-  }
+  WROW_END
   if (NRM) {
     Dd tot[4];
     if (dd_grid_reduce<4>(acc, part, &sc->counter[T_RR1], tot) && threadIdx.x == 0)
@@ -307,20 +348,23 @@ __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__
   Dd acc[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
-  ROW_LOOP {
-    const double wn = ell_row<true>(A, V.r, j);
-    const double zr = ell_row<true>(A, V.s, j);
-    V.w0[j] = wn;
-    V.mv[j] = A.dinv[j] * wn;  // m_{i+1} follows the replaced w (A27)
-    V.zrr[j] = zr;
-    const double rhj = V.rh[j], rc = V.r[j];
-    dd_fma(acc[0], rhj, rc);
-    dd_fma(acc[1 % K], rhj, wn);
-    dd_fma(acc[2 % K], rhj, V.s[j]);
-    dd_fma(acc[3 % K], rhj, zr);
-    dd_fma(acc[4 % K], rc, rc);
-    if (NRM) c_nrm(acc[5 % K], zr);  // replaced z_i
-  }
+  WROW_LOOP
+    const double wn = in ? ell_row<false>(A, V.k, j) : 0.0;  // w := A k = A M^-1 r
+    const double zr = in ? ell_row<false>(A, V.l, j) : 0.0;  // z := A l = A M^-1 s
+    const double mn = prec_row(A, j, in, wn);  // m_{i+1} follows the replaced w (A27)
+    if (in) {
+      V.w0[j] = wn;
+      V.mv[j] = mn;
+      V.zrr[j] = zr;
+      const double rhj = V.rh[j], rc = V.r[j];
+      dd_fma(acc[0], rhj, rc);
+      dd_fma(acc[1 % K], rhj, wn);
+      dd_fma(acc[2 % K], rhj, V.s[j]);
+      dd_fma(acc[3 % K], rhj, zr);
+      dd_fma(acc[4 % K], rc, rc);
+      if (NRM) c_nrm(acc[5 % K], zr);  // replaced z_i
+    }
+  WROW_END
   Dd tot[K];
   if (dd_grid_reduce<K>(acc, part, &sc->counter[T_RR2], tot) && threadIdx.x == 0)
     publish<F_RR2>(sc, h, tot);
@@ -435,6 +479,14 @@ __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __re
   spmv_fin<WHICH>(sc, h, part, dacc);
 }
 
+// mv := M^-1 w0 (p-CG init, after SP_PCW0)
+__global__ void __launch_bounds__(256) c_prec_mv(CsrOp A, Vecs V) {
+  WROW_LOOP
+    const double m = prec_row(A, j, in, in ? V.w0[j] : 0.0);
+    if (in) V.mv[j] = m;
+  WROW_END
+}
+
 // ---------------------------------------------------------------------------
 // Classic BiCGStab (Alg. 1) on CSR: the element-wise steps around the
 // SpMVs SP_CLS / SP_CLY.  Buffers: p -> g, M^-1 p -> mv, M^-1 q -> nv, y -> z1.
@@ -443,18 +495,24 @@ __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __re
 __global__ void __launch_bounds__(256) c_cl_p(CsrOp A, Vecs V, Scal* __restrict__ sc) {
   if (sc->done) return;
   const double be = sc->beta, om = sc->omega;
-  ROW_LOOP {
-    const double p = V.r[j] + be * (V.g[j] - om * V.s[j]);
-    V.g[j] = p;
-    V.mv[j] = A.dinv[j] * p;
-  }
+  WROW_LOOP
+    const double p = in ? V.r[j] + be * (V.g[j] - om * V.s[j]) : 0.0;
+    const double g = prec_row(A, j, in, p);
+    if (in) {
+      V.g[j] = p;
+      V.mv[j] = g;
+    }
+  WROW_END
 }
 
 // l.8-9: q := r - alpha s; the SpMV operand nv := u = M^-1 q
 __global__ void __launch_bounds__(256) c_cl_u(CsrOp A, Vecs V, Scal* __restrict__ sc) {
   if (sc->done) return;
   const double al = sc->alpha;
-  ROW_LOOP { V.nv[j] = A.dinv[j] * (V.r[j] - al * V.s[j]); }
+  WROW_LOOP
+    const double u = prec_row(A, j, in, in ? V.r[j] - al * V.s[j] : 0.0);
+    if (in) V.nv[j] = u;
+  WROW_END
 }
 
 // l.13-15: x := (x + alpha g) + omega u; r := q - omega y; (r^0, r), ||r||^2
@@ -485,10 +543,12 @@ __global__ void __launch_bounds__(256) c_pc(CsrOp A, Vecs V, Scal* __restrict__ 
   if (sc->done) return;
   const double al = sc->alpha, be = sc->beta;
   Dd acc[3] = {dd_zero(), dd_zero(), dd_zero()};
-  ROW_LOOP {
-    const double dj = A.dinv[j];
-    const double wj = V.w0[j], uj = V.k[j];
-    const double mj = dj * wj;
+  WROW_LOOP
+    const double wj = in ? V.w0[j] : 0.0;
+    const double mj = prec_row(A, j, in, wj);
+    double wn = 0.0;
+    if (in) {
+    const double uj = V.k[j];
     const double zn = V.z1[j] + be * V.z0[j];
     const double qn = mj + be * V.l[j];
     const double sn = wj + be * V.s[j];
@@ -496,14 +556,16 @@ __global__ void __launch_bounds__(256) c_pc(CsrOp A, Vecs V, Scal* __restrict__ 
     const double xn = V.x[j] + al * pn;
     const double rn = V.r[j] - al * sn;
     const double un = uj - al * qn;
-    const double wn = wj - al * zn;
+    wn = wj - al * zn;
     V.z0[j] = zn; V.l[j] = qn; V.s[j] = sn; V.g[j] = pn;
     V.x[j] = xn; V.r[j] = rn; V.k[j] = un; V.w0[j] = wn;
-    V.mv[j] = dj * wn;
     dd_fma(acc[0], rn, un);
     dd_fma(acc[1], wn, un);
     dd_fma(acc[2], rn, rn);
-  }
+    }
+    const double mn = prec_row(A, j, in, wn);
+    if (in) V.mv[j] = mn;
+  WROW_END
   Dd tot[3];
   if (dd_grid_reduce<3>(acc, part, &sc->counter[T_PC], tot) && threadIdx.x == 0)
     publish<F_PC>(sc, h, tot);

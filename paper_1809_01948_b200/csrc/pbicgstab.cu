@@ -235,7 +235,8 @@ Members members(pbicg_ctx* h) {
 enum Phase { PH_INIT1, PH_INIT2, PH_SWEEPA, PH_SPMVB, PH_SWEEPC, PH_RR1, PH_RR2, PH_SPMVD, PH_GAP,
              PH_CL1, PH_CL2, PH_CL3, PH_PC, PH_PCI1, PH_PCI2,
              // CSR comparison solvers: element-wise steps and SpMVs with epilogues
-             PH_CCP, PH_SP_CLS, PH_CCU, PH_SP_CLY, PH_CCX, PH_SP_PCW0, PH_SP_PCN, PH_CPC };
+             PH_CCP, PH_SP_CLS, PH_CCU, PH_SP_CLY, PH_CCX, PH_SP_PCW0, PH_SP_PCN, PH_CPC,
+             PH_PRECMV };
 
 template <int DIM, int MODE>
 void launch_tile(pbicg_ctx* h) {
@@ -338,6 +339,10 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SP_PCW0: { LaunchScope ls(h, K_INIT); launch_spmv<SP_PCW0>(h); } break;
     case PH_SP_PCN: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_PCN>(h); } break;
+    case PH_PRECMV: {
+      LaunchScope ls(h, K_INIT);
+      c_prec_mv<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V);
+    } break;
     case PH_CPC: {
       LaunchScope ls(h, K_PC);
       c_pc<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
@@ -615,8 +620,9 @@ void enq_init_pipecg(const Members& G) {
     each(G, PH_INIT1);  // r0, u0 (k); ||r0||, ||b|| (F_INIT1, method 2)
     reduce_fin(G, F_INIT1);
     if (dist) comm_halo(G, {SK});
-    each(G, PH_SP_PCW0);  // w0 = A u0, m0; (r0,u0), (w0,u0) -> alpha_0
+    each(G, PH_SP_PCW0);  // w0 = A u0; (r0,u0), (w0,u0) -> alpha_0
     reduce_fin(G, F_PINIT2);
+    each(G, PH_PRECMV);   // m0 = M^-1 w0
     if (dist) comm_halo(G, {SMVv});
     each(G, PH_SP_PCN);  // n_0 = A m_0
     return;
@@ -657,7 +663,7 @@ void enq_init(const Members& G) {
   if (dist) comm_halo(G, {SX});
   each(G, PH_INIT1);
   reduce_fin(G, F_INIT1);
-  if (dist) comm_halo(G, {SR});
+  if (dist) comm_halo(G, {h0->kind == KIND_CSR ? SK : SR});  // CSR: w0 = A k0
   each(G, PH_INIT2);
   reduce_fin(G, F_INIT2);
   if (h0->kind == KIND_CSR) {  // t_0 = A m_0 (line 3)
@@ -751,7 +757,7 @@ void enq_iter(const Members& G, bool with_rr, int par) {
       if (dist) comm_halo(G, {SX, SG});
       each(G, PH_RR1);
       if (h0->auto_rr) reduce_fin(G, F_RR1);  // norms of the replaced vectors
-      if (dist) comm_halo(G, {SR, SS});
+      if (dist) comm_halo(G, {SK, SL});         // w := A k, z := A l
       each(G, PH_RR2);
       reduce_fin(G, F_RR2);
     }
@@ -1211,11 +1217,62 @@ pbicg_status validate_csr(const pbicg_csr* op, int nranks, std::vector<double>* 
   return PBICG_OK;
 }
 
+// Block Jacobi (reading A33): the bj x bj diagonal blocks of this rank's rows
+// (rows [k bj, (k+1) bj), aligned globally), each inverted by plain Gauss-Jordan
+// elimination without pivoting -- the same operations, in the same order, as
+// oracle.c orc_gauss_jordan -- stored row-major as binv[i * bj + c].
+pbicg_status block_inverse(const pbicg_csr* op, int bj, std::vector<double>* binv) {
+  const int64_t n = op->n_local;
+  binv->assign((size_t)n * bj, 0.0);
+  std::vector<double> a((size_t)bj * bj), e((size_t)bj * bj);
+  for (int64_t k0 = 0; k0 < n; k0 += bj) {
+    std::fill(a.begin(), a.end(), 0.0);
+    for (int r = 0; r < bj; ++r)
+      for (int64_t p = op->row_ptr[k0 + r]; p < op->row_ptr[k0 + r + 1]; ++p) {
+        const int64_t c = op->col[p] - op->row_begin - k0;
+        if (c >= 0 && c < bj) a[(size_t)r * bj + c] = op->val[p];
+      }
+    for (int r = 0; r < bj; ++r)
+      for (int c = 0; c < bj; ++c) e[(size_t)r * bj + c] = (r == c) ? 1.0 : 0.0;
+    for (int p = 0; p < bj; ++p) {
+      const double piv = a[(size_t)p * bj + p];
+      if (piv == 0.0 || !std::isfinite(piv))
+        return fail(nullptr, PBICG_EINVAL, "block Jacobi: zero pivot in a diagonal block");
+      const double f = 1.0 / piv;
+      for (int c = 0; c < bj; ++c) {
+        a[(size_t)p * bj + c] = a[(size_t)p * bj + c] * f;
+        e[(size_t)p * bj + c] = e[(size_t)p * bj + c] * f;
+      }
+      for (int r = 0; r < bj; ++r) {
+        if (r == p) continue;
+        const double g = a[(size_t)r * bj + p];
+        for (int c = 0; c < bj; ++c) {
+          a[(size_t)r * bj + c] = a[(size_t)r * bj + c] - g * a[(size_t)p * bj + c];
+          e[(size_t)r * bj + c] = e[(size_t)r * bj + c] - g * e[(size_t)p * bj + c];
+        }
+      }
+    }
+    for (int r = 0; r < bj; ++r)
+      for (int c = 0; c < bj; ++c) (*binv)[(size_t)(k0 + r) * bj + c] = e[(size_t)r * bj + c];
+  }
+  return PBICG_OK;
+}
+
+// preconditioner block size from the ABI value: 1 Jacobi, b for PBICG_PREC_BJ(b)
+int prec_block(int prec) {
+  if (prec == PBICG_PREC_JACOBI) return 1;
+  const int b = prec & 0xff;
+  if ((prec & ~0xff) == PBICG_PREC_BLOCK_JACOBI && (b == 2 || b == 4 || b == 8 || b == 16 || b == 32))
+    return b;
+  return 0;
+}
+
 // Automated-replacement constants of a CSR operator given ALL its row blocks in
 // order (reading A29): ||A|| <= sqrt(||A||_1 ||A||_inf), row sums in stored
 // (ascending column) order, column sums in ascending row order -- the same
 // doubles as oracle.c orc_anorm_bound; mu = max row length; ||M^-1|| = max |1/a_jj|.
-void csr_bound_consts(const pbicg_csr* ops, int nops, double* nA, double* muN, double* mutN) {
+void csr_bound_consts(const pbicg_csr* ops, int nops, int bj, double* nA, double* muN,
+                      double* mutN) {
   const int64_t N = ops[0].n_global;
   std::vector<double> col((size_t)N, 0.0);
   double rmax = 0.0, cmax = 0.0, mi = 0.0;
@@ -1236,16 +1293,49 @@ void csr_bound_consts(const pbicg_csr* ops, int nops, double* nA, double* muN, d
     }
   }
   for (double c : col) cmax = c > cmax ? c : cmax;
+  if (bj > 1) {  // ||M^-1|| <= max over blocks sqrt(||B^-1||_1 ||B^-1||_inf) (oracle prec_norm_bound)
+    mi = 0.0;
+    std::vector<double> inv;
+    for (int r = 0; r < nops; ++r) {
+      if (block_inverse(&ops[r], bj, &inv) != PBICG_OK) continue;
+      for (int64_t k0 = 0; k0 < ops[r].n_local; k0 += bj) {
+        double rm = 0.0, cm = 0.0;
+        for (int a = 0; a < bj; ++a) {
+          double rs = 0.0;
+          for (int c = 0; c < bj; ++c) rs = rs + std::fabs(inv[(size_t)(k0 + a) * bj + c]);
+          if (rs > rm) rm = rs;
+        }
+        for (int c = 0; c < bj; ++c) {
+          double cs = 0.0;
+          for (int a = 0; a < bj; ++a) cs = cs + std::fabs(inv[(size_t)(k0 + a) * bj + c]);
+          if (cs > cm) cm = cs;
+        }
+        const double nbk = std::sqrt(cm * rm);
+        if (nbk > mi) mi = nbk;
+      }
+    }
+  }
   *nA = std::sqrt(cmax * rmax);
   *muN = (double)mu * std::sqrt((double)N);
-  *mutN = 1.0 * std::sqrt((double)N) * mi;
+  *mutN = (double)bj * std::sqrt((double)N) * mi;
 }
 
 pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<double>& dinv,
-                       int64_t width, bool uniform) {
+                       int64_t width, bool uniform, int bj) {
   h->kind = KIND_CSR;
+  if (bj > 1) {
+    if (op->n_local % bj != 0 || op->row_begin % bj != 0)
+      return fail(h, PBICG_EINVAL, "block Jacobi: rank rows must be whole aligned blocks");
+    std::vector<double> inv;
+    ST(block_inverse(op, bj, &inv));
+    void* pb = nullptr;
+    ST(dalloc(h, &pb, inv.size() * sizeof(double)));
+    CU(cudaMemcpy(pb, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    h->csr.binv = (const double*)pb;
+  }
+  h->csr.bj = bj;
   if (h->nranks == 1) {  // multi-rank: the loopback group sets them (NCCL ranks: not available)
-    csr_bound_consts(op, 1, &h->ar_nA, &h->ar_muN, &h->ar_mutN);
+    csr_bound_consts(op, 1, bj, &h->ar_nA, &h->ar_muN, &h->ar_mutN);
     h->ar_ok = true;
   }
   const int64_t n = op->n_local;
@@ -1524,7 +1614,9 @@ pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pb
                                   void* cuda_stream, pbicg_handle* out) {
   if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
   *out = nullptr;
-  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+  const int bj = prec_block(prec);
+  if (!bj)
+    return fail(nullptr, PBICG_EINVAL, "prec must be PBICG_PREC_JACOBI or PBICG_PREC_BJ(2..32)");
   const int nranks = dist ? dist->nranks : 1;
   if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
     return fail(nullptr, PBICG_EINVAL, "inconsistent nranks/rank");
@@ -1537,7 +1629,7 @@ pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pb
   h->rank = dist ? dist->rank : 0;
   pbicg_status st = common_setup(h, cuda_stream);
   if (!st && nranks > 1) st = nccl_setup(h, dist);
-  if (!st) st = build_csr(h, op, dinv, width, uniform);
+  if (!st) st = build_csr(h, op, dinv, width, uniform, bj);
   if (!st && nranks > 1) {  // dinv ghosts, once (collective)
     comm_halo(Members{h}, {[](pbicg_ctx* c) { return c->dinv_g; }});
     cudaError_t e = cudaStreamSynchronize(h->stream);
@@ -1589,7 +1681,9 @@ pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_pr
 pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec, int32_t nranks,
                                            void* cuda_stream, pbicg_handle* out) {
   if (!out || !ops || nranks < 1) return fail(nullptr, PBICG_EINVAL, "bad argument");
-  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+  const int bj = prec_block(prec);
+  if (!bj)
+    return fail(nullptr, PBICG_EINVAL, "prec must be PBICG_PREC_JACOBI or PBICG_PREC_BJ(2..32)");
   for (int r = 0; r < nranks; ++r) out[r] = nullptr;
   std::vector<std::vector<double>> dinv(nranks);
   std::vector<int64_t> width(nranks);
@@ -1619,7 +1713,7 @@ pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec
     grp->alive++;
     st = common_setup(h, s);
     if (r == 0) h->own_stream = own;
-    if (!st) st = build_csr(h, &ops[r], dinv[r], width[r], uni[r] != 0);
+    if (!st) st = build_csr(h, &ops[r], dinv[r], width[r], uni[r] != 0, bj);
     if (st) g_create_err = h->err;
   }
   if (!st) {
@@ -1628,7 +1722,7 @@ pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec
   }
   if (!st) {
     double nA = 0, muN = 0, mutN = 0;
-    csr_bound_consts(ops, nranks, &nA, &muN, &mutN);
+    csr_bound_consts(ops, nranks, prec_block(prec), &nA, &muN, &mutN);
     for (pbicg_ctx* m : grp->m) {
       m->ar_nA = nA;
       m->ar_muN = muN;
@@ -1861,11 +1955,14 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
   } else {
     const double slots = (double)h->csr.width;  // ELL width
     const double mat = 12.0 * slots * N;        // val (8) + col (4) per slot
-    if (n == "sweepA") b = 15 * 8 * N;  // read k,g,l,w,s,z,t,v,r,dinv; write g,s,l,z,n
+    // block Jacobi: each kernel applying M^-1 reads its rows of the block inverse
+    // instead of dinv (bj doubles instead of 1 per row)
+    const double pb = h->csr.bj > 1 ? (h->csr.bj - 1) * 8.0 * N : 0.0;
+    if (n == "sweepA") b = 15 * 8 * N + pb;  // read k,g,l,w,s,z,t,v,r,dinv; write g,s,l,z,n
     else if (h->method == M_BICGSTAB && n == "spmvB") b = mat + 3 * 8 * N;  // mv in; s out; r^
     else if (h->method == M_BICGSTAB && n == "spmvD") b = mat + 4 * 8 * N;  // nv in; y out; r, s
     else if (n == "spmvB" || n == "spmvD" || n == "apply") b = mat + 2 * 8 * N;  // n|m in, out
-    else if (n == "sweepC") b = 17 * 8 * N;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w,m
+    else if (n == "sweepC") b = 17 * 8 * N + pb;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w,m
     else if (n == "rr1") b = 2 * mat + 8 * 8 * N;
     else if (n == "rr2") b = 2 * mat + 7 * 8 * N;
     else if (n == "gap") b = mat + 3 * 8 * N;
@@ -1875,7 +1972,7 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "cl2") b = 4 * 8 * N;   // c_cl_u: read r,s,dinv; write M^-1 q
     else if (n == "cl3") b = 9 * 8 * N;   // c_cl_x: read x,mv,nv,r,s,y,r^; write x,r
     else if (n == "pcg") b = 19 * 8 * N;  // c_pc: read n,z,q,s,p,x,r,u,w,dinv; write 9
-    else if (n == "iteration") b = 2 * mat + 36 * 8 * N;
+    else if (n == "iteration") b = 2 * mat + 36 * 8 * N + 2 * pb;
   }
   *bytes = b;
   return PBICG_OK;

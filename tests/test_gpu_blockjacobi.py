@@ -1,0 +1,114 @@
+"""GPU parity of the block-Jacobi preconditioner (reading A33)
+on CSR operators, against the oracle: the library inverts the diagonal blocks
+with its own Gauss-Jordan (same textbook operations as the oracle's) and applies
+them with warp shuffles, so the runs are expected bitwise equal.
+"""
+import numpy as np
+import pytest
+
+from paper_1809_01948_b200 import problems
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from test_gpu_parity import check_parity  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_1809_01948_b200 import Solver
+    assert torch.cuda.is_available()
+    return Solver
+
+
+def case(S, orc, A, block, seed=0):
+    solver = S.csr(A.n, A.rp, A.ci.astype(np.int32), A.va, block=block)
+    xs = problems.x_star(A.n, seed)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    return solver, xs, b, b_d
+
+
+def band(n, bw, seed):
+    P = problems.csr_band(n, nnz_row=27, band=bw, seed=seed)
+    from oracle import oracle as o
+    return o.csr(P.row_ptr, P.col, P.val)
+
+
+@pytest.mark.parametrize("block", [1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("bw", [300, 6000])  # window SpMV / gather SpMV
+def test_bj_pbicgstab_parity(S, orc, block, bw):
+    A = band(8192, bw, 1)
+    solver, xs, b, b_d = case(S, orc, A, block)
+    for rr in (0, 3):
+        res = solver.solve(b_d, tol=1e-12, maxit=100, rr_period=rr, gap=True)
+        ref = orc.pbicgstab(A, b, tol=1e-12, maxit=100, rr_period=rr, block=block)
+        assert res.outcome == ref.outcome
+        check_parity(res, ref, xs)
+
+
+@pytest.mark.parametrize("block", [4, 8])
+def test_bj_stencil_as_csr_all_methods(S, orc, block):
+    """A 2D Poisson stencil written out as CSR (ragged rows): block Jacobi speeds
+    up every solver; p-BiCGStab, classic BiCGStab and p-CG bitwise vs the oracle."""
+    A = orc.stencil_csr(2, 40, 30, 1, problems.poisson2d_coef())
+    solver, xs, b, b_d = case(S, orc, A, block)
+    for method, ref in ((0, orc.pbicgstab(A, b, tol=1e-10, maxit=500, block=block)),
+                        (1, orc.bicgstab(A, b, tol=1e-10, maxit=500, block=block)),
+                        (2, orc.pipecg(A, b, tol=1e-10, maxit=500, block=block))):
+        solver.set_option("method", method)
+        res = solver.solve(b_d, tol=1e-10, maxit=500, gap=True)
+        assert res.outcome == ref.outcome == "converged"
+        check_parity(res, ref, xs)
+        jac = {0: orc.pbicgstab, 1: orc.bicgstab, 2: orc.pipecg}[method](A, b, tol=1e-10, maxit=500)
+        assert res.iters < jac.iters
+
+
+def test_bj_auto_rr(S, orc):
+    A = orc.stencil_csr(2, 64, 64, 1, problems.cfg2_coef())
+    solver, xs, b, b_d = case(S, orc, A, 4)
+    solver.set_option("bench", 1)
+    solver.set_option("rr_auto", 1)
+    res = solver.solve(b_d, tol=0.0, maxit=200, gap=True)
+    fr, rrl = solver.rr_info(res.iters)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=200, bench=True, auto_rr=True, block=4)
+    from test_gpu_autorr import check_auto
+    check_auto(res, fr, rrl, ref, xs)
+
+
+@pytest.mark.parametrize("method", [0, 1, 2])
+def test_bj_loopback(S, orc, method):
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    A = orc.stencil_csr(2, 64, 192, 1, problems.poisson2d_coef())
+    n, P, blk = A.n, 3, 8
+    rp, ci, va = A.rp, A.ci.astype(np.int32), A.va
+    cuts = [0, 4096, 8192, n]
+    blocks = [(cuts[r], rp[cuts[r]:cuts[r + 1] + 1] - rp[cuts[r]], ci[rp[cuts[r]]:rp[cuts[r + 1]]],
+               va[rp[cuts[r]]:rp[cuts[r + 1]]]) for r in range(P)]
+    G = LoopbackGroup.csr(blocks, n, block=blk)
+    G.set_option("method", method)
+    xs = problems.x_star(n, 0)
+    b = orc.spmv(A, xs)
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=1e-10, maxit=400, rr_period=0, gap=True)
+    ref = {0: orc.pbicgstab, 1: orc.bicgstab, 2: orc.pipecg}[method](A, b, tol=1e-10, maxit=400,
+                                                                      block=blk)
+    check_parity(res, ref, xs)
+    G.close()
+
+
+def test_bj_errors(S, orc):
+    from paper_1809_01948_b200.binding import PbicgError
+    A = orc.stencil_csr(2, 10, 9, 1, problems.poisson2d_coef())  # n = 90
+    with pytest.raises(PbicgError):  # n not a multiple of b
+        S.csr(A.n, A.rp, A.ci.astype(np.int32), A.va, block=4)
+    with pytest.raises(PbicgError):  # unsupported block size
+        S.csr(A.n, A.rp, A.ci.astype(np.int32), A.va, block=3)
+    with pytest.raises(PbicgError):  # stencils: Jacobi only
+        from paper_1809_01948_b200 import binding
+        import ctypes
+        st = binding._Stencil(2, 8, 8, 1, (ctypes.c_double * 7)(4, -1, -1, -1, -1, 0, 0))
+        h = ctypes.c_void_p()
+        binding._check(binding.lib().pbicgstab_create_stencil(ctypes.byref(st), 0x104, None, None,
+                                                              ctypes.byref(h)))
