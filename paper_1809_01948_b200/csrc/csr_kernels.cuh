@@ -34,15 +34,21 @@ struct CsrOp {
 // (blocks are aligned and n_local % bj == 0), so the block's values are read by
 // shuffles and (M^{-1}v)_j = sum_k binv_jk v_{kb+k}, ascending k from +0.0 -- the
 // oracle's order.  Every lane of the warp must call it (warp-uniform loops, WROW_LOOP).
-__device__ __forceinline__ double prec_row(const CsrOp& A, int64_t j, bool in, double v) {
-  if (A.bj == 1) return in ? A.dinv[j] * v : 0.0;
+// BJ = false: Jacobi with dj = dinv_j preloaded by the caller (0 on idle lanes).
+template <bool BJ>
+__device__ __forceinline__ double prec_row(const CsrOp& A, int64_t j, bool in, double v,
+                                          double dj) {
+  if (!BJ) return dj * v;
   const int lane = threadIdx.x & 31;
   const int base = lane & ~(A.bj - 1);
-  const double* __restrict__ row = A.binv + (in ? j : 0) * A.bj;
+  const double* __restrict__ row = A.binv + (in ? j : 0) * A.bj;  // 16-byte aligned (bj even)
   double acc = 0.0;
-  for (int k = 0; k < A.bj; ++k) {
-    const double vk = __shfl_sync(0xffffffffu, v, base + k);
-    acc = acc + (in ? __ldg(row + k) : 0.0) * vk;
+  for (int k = 0; k < A.bj; k += 2) {
+    const double2 rw = in ? __ldg(reinterpret_cast<const double2*>(row + k)) : make_double2(0.0, 0.0);
+    const double v0 = __shfl_sync(0xffffffffu, v, base + k);
+    const double v1 = __shfl_sync(0xffffffffu, v, base + k + 1);
+    acc = acc + rw.x * v0;
+    acc = acc + rw.y * v1;
   }
   return acc;
 }
@@ -89,14 +95,15 @@ __device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restri
   for (int64_t j0_ = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~(int64_t)31; \
        j0_ < A.n; j0_ += (int64_t)gridDim.x * blockDim.x) {                          \
     const int64_t j = j0_ + (threadIdx.x & 31);                                       \
-    const bool in = j < A.n;
+    const bool in = j < A.n;                                                          \
+    const double dj = (!BJ && in) ? A.dinv[j] : 0.0; /* Jacobi: dinv_j, loaded once */
 #define WROW_END }
 
 // NRM (automated replacement): the step's reduction also carries the
 // sums of squares of the vectors the bound f^r needs (plain fp64, reading A30)
 __device__ __forceinline__ void c_nrm(Dd& a, double v) { a.hi = a.hi + v * v; }
 
-template <bool NRM>
+template <bool NRM, bool BJ>
 __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                Dd* __restrict__ part, Hist h) {
   constexpr int K = NRM ? 4 : 2;
@@ -106,7 +113,7 @@ __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict
   WROW_LOOP
     const double bj = in ? V.b[j] : 0.0;
     const double rj = in ? bj - ell_row<false>(A, V.x, j) : 0.0;
-    const double kj = prec_row(A, j, in, rj);  // k0 := M^-1 r0
+    const double kj = prec_row<BJ>(A, j, in, rj, dj);  // k0 := M^-1 r0
     if (in) {
       V.r[j] = rj;
       V.rh[j] = rj;
@@ -124,12 +131,13 @@ __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict
     publish<F_INIT1>(sc, h, tot);
 }
 
+template <bool BJ>
 __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                Dd* __restrict__ part, Hist h) {
   Dd acc[1] = {dd_zero()};
   WROW_LOOP
     const double wj = in ? ell_row<false>(A, V.k, j) : 0.0;  // w0 = A k0 = A M^-1 r0
-    const double mj = prec_row(A, j, in, wj);                // m0 = M^-1 w0 (line 2)
+    const double mj = prec_row<BJ>(A, j, in, wj, dj);            // m0 = M^-1 w0 (line 2)
     if (in) {
       V.w0[j] = wj;
       V.mv[j] = mj;
@@ -142,7 +150,7 @@ __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict
 }
 
 // lines 5-12 with stored t_i, v_{i-1}; n_{i-1} = M^-1 z_{i-1} (pre-replacement, A26)
-template <bool NRM>
+template <bool NRM, bool BJ>
 __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                 Dd* __restrict__ part, Hist h) {
   constexpr int K = NRM ? 12 : 2;
@@ -154,7 +162,7 @@ __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restric
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   WROW_LOOP
     const double wc = in ? V.w0[j] : 0.0, zc = in ? V.z0[j] : 0.0;
-    const double m = prec_row(A, j, in, wc), n = prec_row(A, j, in, zc);  // m_i, n_{i-1}
+    const double m = prec_row<BJ>(A, j, in, wc, dj), n = prec_row<BJ>(A, j, in, zc, dj);  // m_i, n_{i-1}
     double zn = 0.0;
     if (in) {
       const double zo = rr ? V.zrr[j] : zc;
@@ -179,7 +187,7 @@ __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restric
       V.l[j] = ln;
       V.z0[j] = zn;
     }
-    const double nj = prec_row(A, j, in, zn);  // n_i = M^-1 z_i (line 13)
+    const double nj = prec_row<BJ>(A, j, in, zn, dj);  // n_i = M^-1 z_i (line 13)
     if (in) V.nv[j] = nj;
   WROW_END
   Dd tot[K];
@@ -265,7 +273,7 @@ __global__ void __launch_bounds__(256) c_spmvB(CsrOp A, Vecs V, Scal* __restrict
 }
 
 // lines 17-21
-template <bool NRM>
+template <bool NRM, bool BJ>
 __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                 Dd* __restrict__ part, Hist h) {
   constexpr int K = NRM ? 9 : 5;
@@ -276,7 +284,7 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   WROW_LOOP
     const double wc = in ? V.w0[j] : 0.0, zc = in ? V.z0[j] : 0.0;
-    const double m = prec_row(A, j, in, wc), n = prec_row(A, j, in, zc);  // m_i, n_i
+    const double m = prec_row<BJ>(A, j, in, wc, dj), n = prec_row<BJ>(A, j, in, zc, dj);  // m_i, n_i
     double wn = 0.0;
     if (in) {
     const double t = V.w1[j], v = V.z1[j];
@@ -304,7 +312,7 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
     V.k[j] = kn;
     V.w0[j] = wn;
     }
-    const double mn = prec_row(A, j, in, wn);  // m_{i+1} = M^-1 w_{i+1} (line 22)
+    const double mn = prec_row<BJ>(A, j, in, wn, dj);  // m_{i+1} = M^-1 w_{i+1} (line 22)
     if (in) V.mv[j] = mn;
   WROW_END
   Dd tot[K];
@@ -313,7 +321,7 @@ __global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restric
 }
 
 // eq:rr: r := b - A x; k := M^-1 r; s := A g; l := M^-1 s
-template <bool NRM>
+template <bool NRM, bool BJ>
 __global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                              Dd* __restrict__ part, Hist h) {
   if (sc->done || !sc->rr_fire) return;
@@ -321,7 +329,7 @@ __global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__
   WROW_LOOP
     const double rj = in ? V.b[j] - ell_row<false>(A, V.x, j) : 0.0;
     const double sj = in ? ell_row<false>(A, V.g, j) : 0.0;
-    const double kj = prec_row(A, j, in, rj), lj = prec_row(A, j, in, sj);
+    const double kj = prec_row<BJ>(A, j, in, rj, dj), lj = prec_row<BJ>(A, j, in, sj, dj);
     if (in) {
       V.r[j] = rj;
       V.k[j] = kj;
@@ -340,7 +348,7 @@ __global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__
 }
 
 // w := A k; z := A l (into zrr); line-21 dots on the replaced vectors
-template <bool NRM>
+template <bool NRM, bool BJ>
 __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                              Dd* __restrict__ part, Hist h) {
   constexpr int K = NRM ? 6 : 5;
@@ -351,7 +359,7 @@ __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__
   WROW_LOOP
     const double wn = in ? ell_row<false>(A, V.k, j) : 0.0;  // w := A k = A M^-1 r
     const double zr = in ? ell_row<false>(A, V.l, j) : 0.0;  // z := A l = A M^-1 s
-    const double mn = prec_row(A, j, in, wn);  // m_{i+1} follows the replaced w (A27)
+    const double mn = prec_row<BJ>(A, j, in, wn, dj);  // m_{i+1} follows the replaced w (A27)
     if (in) {
       V.w0[j] = wn;
       V.mv[j] = mn;
@@ -480,9 +488,10 @@ __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __re
 }
 
 // mv := M^-1 w0 (p-CG init, after SP_PCW0)
+template <bool BJ>
 __global__ void __launch_bounds__(256) c_prec_mv(CsrOp A, Vecs V) {
   WROW_LOOP
-    const double m = prec_row(A, j, in, in ? V.w0[j] : 0.0);
+    const double m = prec_row<BJ>(A, j, in, in ? V.w0[j] : 0.0, dj);
     if (in) V.mv[j] = m;
   WROW_END
 }
@@ -492,12 +501,13 @@ __global__ void __launch_bounds__(256) c_prec_mv(CsrOp A, Vecs V) {
 // SpMVs SP_CLS / SP_CLY.  Buffers: p -> g, M^-1 p -> mv, M^-1 q -> nv, y -> z1.
 // l.17 of the previous iteration (i = 0: beta = omega = 0 and p = s = 0, so
 // p_0 = r_0): p := r + beta (p - omega s); the SpMV operand mv := M^-1 p (l.4)
+template <bool BJ>
 __global__ void __launch_bounds__(256) c_cl_p(CsrOp A, Vecs V, Scal* __restrict__ sc) {
   if (sc->done) return;
   const double be = sc->beta, om = sc->omega;
   WROW_LOOP
     const double p = in ? V.r[j] + be * (V.g[j] - om * V.s[j]) : 0.0;
-    const double g = prec_row(A, j, in, p);
+    const double g = prec_row<BJ>(A, j, in, p, dj);
     if (in) {
       V.g[j] = p;
       V.mv[j] = g;
@@ -506,11 +516,12 @@ __global__ void __launch_bounds__(256) c_cl_p(CsrOp A, Vecs V, Scal* __restrict_
 }
 
 // l.8-9: q := r - alpha s; the SpMV operand nv := u = M^-1 q
+template <bool BJ>
 __global__ void __launch_bounds__(256) c_cl_u(CsrOp A, Vecs V, Scal* __restrict__ sc) {
   if (sc->done) return;
   const double al = sc->alpha;
   WROW_LOOP
-    const double u = prec_row(A, j, in, in ? V.r[j] - al * V.s[j] : 0.0);
+    const double u = prec_row<BJ>(A, j, in, in ? V.r[j] - al * V.s[j] : 0.0, dj);
     if (in) V.nv[j] = u;
   WROW_END
 }
@@ -538,6 +549,7 @@ __global__ void __launch_bounds__(256) c_cl_x(CsrOp A, Vecs V, Scal* __restrict_
 // p-CG iteration (reading A19) after n_i = A m_i (SP_PCN): buffers z -> z0,
 // q -> l, s, p -> g, x, r, u -> k, w -> w0, n -> z1, m -> mv (written for the
 // next SpMV); the next iteration's (r,u), (w,u), ||r||^2
+template <bool BJ>
 __global__ void __launch_bounds__(256) c_pc(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                             Dd* __restrict__ part, Hist h) {
   if (sc->done) return;
@@ -545,7 +557,7 @@ __global__ void __launch_bounds__(256) c_pc(CsrOp A, Vecs V, Scal* __restrict__ 
   Dd acc[3] = {dd_zero(), dd_zero(), dd_zero()};
   WROW_LOOP
     const double wj = in ? V.w0[j] : 0.0;
-    const double mj = prec_row(A, j, in, wj);
+    const double mj = prec_row<BJ>(A, j, in, wj, dj);
     double wn = 0.0;
     if (in) {
     const double uj = V.k[j];
@@ -563,7 +575,7 @@ __global__ void __launch_bounds__(256) c_pc(CsrOp A, Vecs V, Scal* __restrict__ 
     dd_fma(acc[1], wn, un);
     dd_fma(acc[2], rn, rn);
     }
-    const double mn = prec_row(A, j, in, wn);
+    const double mn = prec_row<BJ>(A, j, in, wn, dj);
     if (in) V.mv[j] = mn;
   WROW_END
   Dd tot[3];

@@ -325,12 +325,14 @@ void launch_csr(pbicg_ctx* h, Phase p) {
   switch (p) {
     case PH_CCP: {
       LaunchScope ls(h, K_CL1);
-      c_cl_p<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      if (h->csr.bj > 1) c_cl_p<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      else c_cl_p<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
     case PH_SP_CLS: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_CLS>(h); } break;
     case PH_CCU: {
       LaunchScope ls(h, K_CL2);
-      c_cl_u<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      if (h->csr.bj > 1) c_cl_u<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      else c_cl_u<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
     case PH_SP_CLY: { LaunchScope ls(h, K_SPMVD); launch_spmv<SP_CLY>(h); } break;
     case PH_CCX: {
@@ -341,29 +343,38 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     case PH_SP_PCN: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_PCN>(h); } break;
     case PH_PRECMV: {
       LaunchScope ls(h, K_INIT);
-      c_prec_mv<<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V);
+      if (h->csr.bj > 1) c_prec_mv<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V);
+      else c_prec_mv<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V);
     } break;
     case PH_CPC: {
       LaunchScope ls(h, K_PC);
-      c_pc<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->csr.bj > 1) c_pc<true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else c_pc<false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_INIT1: {
       LaunchScope ls(h, K_INIT);
-      if (h->auto_rr)
-        c_init1<true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else
-        c_init1<false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->csr.bj > 1) {
+        if (h->auto_rr) c_init1<true, true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_init1<false, true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      } else {
+        if (h->auto_rr) c_init1<true, false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_init1<false, false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      }
     } break;
     case PH_INIT2: {
       LaunchScope ls(h, K_INIT);
-      c_init2<<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->csr.bj > 1) c_init2<true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else c_init2<false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SWEEPA: {
       LaunchScope ls(h, K_SWEEPA);
-      if (h->auto_rr)
-        c_sweepA<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else
-        c_sweepA<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->csr.bj > 1) {
+        if (h->auto_rr) c_sweepA<true, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_sweepA<false, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      } else {
+        if (h->auto_rr) c_sweepA<true, false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_sweepA<false, false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      }
     } break;
     case PH_SPMVB: {
       LaunchScope ls(h, K_SPMVB);
@@ -375,24 +386,33 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SWEEPC: {
       LaunchScope ls(h, K_SWEEPC);
-      if (h->auto_rr)
-        c_sweepC<true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else
-        c_sweepC<false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->csr.bj > 1) {
+        if (h->auto_rr) c_sweepC<true, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_sweepC<false, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      } else {
+        if (h->auto_rr) c_sweepC<true, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_sweepC<false, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      }
     } break;
     case PH_RR1: {
       LaunchScope ls(h, K_RR1);
-      if (h->auto_rr)
-        c_rr1<true><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else
-        c_rr1<false><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->csr.bj > 1) {
+        if (h->auto_rr) c_rr1<true, true><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_rr1<false, true><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      } else {
+        if (h->auto_rr) c_rr1<true, false><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_rr1<false, false><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      }
     } break;
     case PH_RR2: {
       LaunchScope ls(h, K_RR2);
-      if (h->auto_rr)
-        c_rr2<true><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else
-        c_rr2<false><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->csr.bj > 1) {
+        if (h->auto_rr) c_rr2<true, true><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_rr2<false, true><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      } else {
+        if (h->auto_rr) c_rr2<true, false><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_rr2<false, false><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      }
     } break;
     case PH_SPMVD: {
       LaunchScope ls(h, K_SPMVD);
@@ -1377,13 +1397,13 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
   h->csr.dinv = h->dinv_g;
   const int64_t blocks = (n + h->block - 1) / h->block;
   // (the NRM variants reuse these grids: grid-stride loops, last-CTA reductions)
-  h->grid[K_INIT] = occ_grid(h, c_init1<false>, blocks);
-  h->grid[K_SWEEPA] = occ_grid(h, c_sweepA<false>, blocks);
-  h->grid[K_SWEEPC] = occ_grid(h, c_sweepC<false>, blocks);
+  h->grid[K_INIT] = occ_grid(h, c_init1<false, false>, blocks);
+  h->grid[K_SWEEPA] = occ_grid(h, c_sweepA<false, false>, blocks);
+  h->grid[K_SWEEPC] = occ_grid(h, c_sweepC<false, false>, blocks);
   h->grid[K_SPMVB] = occ_grid(h, c_spmvB, blocks);
   h->grid[K_SPMVD] = occ_grid(h, c_spmvD, blocks);
-  h->grid[K_RR1] = occ_grid(h, c_rr1<false>, blocks);
-  h->grid[K_RR2] = occ_grid(h, c_rr2<false>, blocks);
+  h->grid[K_RR1] = occ_grid(h, c_rr1<false, false>, blocks);
+  h->grid[K_RR2] = occ_grid(h, c_rr2<false, false>, blocks);
   h->grid[K_GAP] = occ_grid(h, c_gap, blocks);
   h->grid[K_APPLY] = occ_grid(h, c_apply, blocks);
   ST(gvec(h, &h->V.nv));
