@@ -361,7 +361,11 @@ def run_ours(args, rank, world):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
-                     "iteration_frac": (it_bytes * value / world / 1e9) / peak},
+                     "iteration_frac": (it_bytes * value / world / 1e9) / peak,
+                     # SURVEY 8(d)'s model of the 4-phase schedule (256 B/row stencil,
+                     # 944 B/row CSR): the fused schedule moves fewer bytes, so > 1
+                     "iteration_frac_4phase_model": ((256 if st.dim else 944) * st.n * value / 1e9)
+                                                    / peak if args.method == "pbicgstab" else None},
         "kernels": per_kernel,
         "gpu_launches": launches,
         "e2e": {"value": e2e_iters / (e2e_ms / 1000.0), "unit": UNIT,
