@@ -364,8 +364,9 @@ def run_ours(args, rank, world):
                      "iteration_frac": (it_bytes * value / world / 1e9) / peak,
                      # SURVEY 8(d)'s model of the 4-phase schedule (256 B/row stencil,
                      # 944 B/row CSR): the fused schedule moves fewer bytes, so > 1
-                     "iteration_frac_4phase_model": ((256 if st.dim else 944) * st.n * value / 1e9)
-                                                    / peak if args.method == "pbicgstab" else None},
+                     "iteration_frac_4phase_model": ((256 if st.dim else 944) * st.n * value / world
+                                                     / 1e9) / peak
+                                                    if args.method == "pbicgstab" else None},
         "kernels": per_kernel,
         "gpu_launches": launches,
         "e2e": {"value": e2e_iters / (e2e_ms / 1000.0), "unit": UNIT,
