@@ -1,0 +1,115 @@
+"""Seeded randomised parity sweep (GPU vs oracle) over the option space: random
+grid shapes (2D/3D, odd and even nx, tiny extents), random diagonally dominant
+coefficient sets, random solver / replacement / graph / tile / loopback-rank
+choices and random CSR band matrices with Jacobi or block Jacobi.  Every case
+must meet the north-star bars, and -- above the noise floor -- be bitwise equal.
+"""
+import numpy as np
+import pytest
+
+from paper_1809_01948_b200 import problems
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from test_gpu_parity import check_parity  # noqa: E402
+
+N_CASES = 24
+
+
+def rand_coef(rng, dim, spd):
+    off = -rng.uniform(0.2, 2.0, 6)
+    if dim == 2:
+        off[4:] = 0.0
+    if spd:  # symmetric: -x = +x, -y = +y, -z = +z
+        off[1], off[3], off[5] = off[0], off[2], off[4]
+    c0 = np.abs(off).sum() * rng.uniform(1.0, 1.5)
+    return [float(c0)] + [float(o) for o in off]
+
+
+def bitwise_above_floor(res, ref):
+    k = np.nonzero(ref.rnorm < 1e-16 * ref.rnorm[0])[0]
+    k = int(k[0]) if k.size else min(res.iters, ref.iters) + 1
+    assert np.array_equal(res.rnorm[:k], ref.rnorm[:k])
+
+
+@pytest.mark.parametrize("seed", range(N_CASES))
+def test_fuzz_stencil(orc, seed):
+    from paper_1809_01948_b200 import Solver
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    rng = np.random.default_rng(1000 + seed)
+    dim = int(rng.choice([2, 3]))
+    nx = int(rng.integers(1, 70))
+    ny = int(rng.integers(1, 40))
+    nz = int(rng.integers(1, 25)) if dim == 3 else 1
+    method = int(rng.choice([0, 0, 1, 2]))
+    coef = rand_coef(rng, dim, spd=(method == 2))
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, seed)
+    b = orc.spmv(A, xs)
+    auto = method == 0 and bool(rng.integers(0, 2))
+    rr = int(rng.choice([0, 2, 5, 9])) if method == 0 and not auto else 0
+    maxit = int(rng.integers(5, 80))
+    tol = float(rng.choice([0.0, 1e-8, 1e-11]))
+    outer = nz if dim == 3 else ny
+    P = int(rng.choice([1, 1, 2, 3])) if outer >= 3 else 1
+    if P == 1:
+        S = Solver.stencil(dim, nx, ny, nz, coef)
+        S.set_option("graphs", int(rng.integers(0, 2)))
+        if not auto and method == 0:
+            S.set_option("tile", int(rng.integers(0, 2)))
+        S.set_option("method", method)
+        S.set_option("rr_auto", int(auto))
+        S.set_option("bench", int(tol == 0.0))
+        b_d = S.apply(torch.from_numpy(xs).cuda())
+        assert np.array_equal(b_d.cpu().numpy(), b)
+        res = S.solve(b_d, tol=tol, maxit=maxit, rr_period=rr, gap=True)
+    else:
+        S = LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
+        S.set_option("method", method)
+        S.set_option("rr_auto", int(auto))
+        S.set_option("bench", int(tol == 0.0))
+        bs = S.apply(S.split(torch.from_numpy(xs).cuda()))
+        res = S.solve(bs, tol=tol, maxit=maxit, rr_period=rr, gap=True)
+    kw = dict(tol=tol, maxit=maxit, bench=tol == 0.0)
+    if method == 0:
+        ref = orc.pbicgstab(A, b, rr_period=rr, auto_rr=auto, **kw)
+    elif method == 1:
+        ref = orc.bicgstab(A, b, **kw)
+    else:
+        ref = orc.pipecg(A, b, **kw)
+    assert res.outcome == ref.outcome, (res.outcome, ref.outcome)
+    check_parity(res, ref, xs, bitwise=False)
+    bitwise_above_floor(res, ref)
+    S.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_fuzz_csr(orc, seed):
+    from paper_1809_01948_b200 import Solver
+    rng = np.random.default_rng(2000 + seed)
+    block = int(rng.choice([1, 1, 2, 4, 8, 16, 32]))
+    n = int(rng.integers(64, 400)) * 32
+    bw = int(rng.choice([8, 100, 1000, 5000]))
+    nnz = int(rng.integers(3, 28))
+    M = problems.csr_band(n, nnz_row=min(nnz, bw + 1), band=bw, seed=seed)  # edge rows: bw candidates
+    A = orc.csr(M.row_ptr, M.col, M.val)
+    S = Solver.csr(n, M.row_ptr, M.col, M.val, block=block)
+    method = int(rng.choice([0, 0, 1]))
+    S.set_option("method", method)
+    auto = method == 0 and bool(rng.integers(0, 2))
+    S.set_option("rr_auto", int(auto))
+    rr = int(rng.choice([0, 2, 5])) if method == 0 and not auto else 0
+    xs = problems.x_star(n, seed)
+    b_d = S.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    res = S.solve(b_d, tol=1e-12, maxit=60, rr_period=rr, gap=True)
+    if method == 0:
+        ref = orc.pbicgstab(A, b, tol=1e-12, maxit=60, rr_period=rr, auto_rr=auto, block=block)
+    else:
+        ref = orc.bicgstab(A, b, tol=1e-12, maxit=60, block=block)
+    assert res.outcome == ref.outcome
+    check_parity(res, ref, xs, bitwise=False)
+    bitwise_above_floor(res, ref)
+    S.close()
