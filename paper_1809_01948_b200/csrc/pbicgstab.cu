@@ -916,7 +916,7 @@ void setup_tile(pbicg_ctx* h) {
   }
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
-  const size_t reserve = 4096;  // static shared memory of the block reductions
+  const size_t reserve = 8192;  // static shared memory of the block reductions (K <= 16 pairs)
   for (; TY >= 1; --TY) {
     t.nx = g.nx;
     t.ny = lines;

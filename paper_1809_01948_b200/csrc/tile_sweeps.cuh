@@ -58,7 +58,7 @@ template <> struct BaseOf<TM_INIT1N> { enum { v = TM_INIT1 }; };
 // (DER), whether the operand enters as A M^-1 v (PREC) or A v, the maximum number
 // of streamed vectors, outputs, dot products
 template <int M> struct TileTraits;
-template <> struct TileTraits<TM_A> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 6, NOUT = 4, K = 2 }; };
+template <> struct TileTraits<TM_A> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 5, NOUT = 4, K = 2 }; };
 template <> struct TileTraits<TM_C> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 7, NOUT = 4, K = 5 }; };
 template <> struct TileTraits<TM_RR1> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 0 }; };
 template <> struct TileTraits<TM_RR2> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 5 }; };
@@ -73,7 +73,15 @@ template <> struct TileTraits<TM_PCI1> { enum { NSV = 1, DER = 0, PREC = 0, NSTR
 template <> struct TileTraits<TM_PCI2> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 2 }; };
 // + norms: A: k, w, m, t, g, s, l, z, q, y; C: x, u, n, v; RR1: x, k, s, l; RR2: z;
 // INIT1: x0, k0
-template <> struct TileTraits<TM_AN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 6, NOUT = 4, K = 12 }; };
+template <> struct TileTraits<TM_AN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 5, NOUT = 4, K = 12 }; };
+
+// Depth of the streamed-vector ring (planes in shared memory: the current one +
+// SD-1 in flight).  Sweep A streams only 5 vectors, so it fits a third slot and
+// keeps two planes of them in flight -- the bytes in flight its 13-pass budget
+// needs to run at the copy rate when the power cap lowers the SM clock.
+template <int M> struct StreamDepth { enum { v = 2 }; };
+template <> struct StreamDepth<TM_A> { enum { v = 3 }; };
+template <> struct StreamDepth<TM_AN> { enum { v = 3 }; };
 template <> struct TileTraits<TM_CN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 7, NOUT = 4, K = 9 }; };
 template <> struct TileTraits<TM_RR1N> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 4 }; };
 template <> struct TileTraits<TM_RR2N> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 6 }; };
@@ -257,12 +265,13 @@ __device__ __forceinline__ void stencil_pair_der(const TileGeo& g, int nx, const
 // Per-row arithmetic of each mode.  S = stream slot at this row, st = stride;
 // c0/c1 = the stencil operands' centre values, t0/t1 = their stencil products.
 template <int MODE, int K, int NOUTC, bool NRM>
-__device__ __forceinline__ void row_update(const double* S, int st, bool rr, double c0, double c1,
+__device__ __forceinline__ void row_update(const double* S, int st, bool rr, const double* zrr_g,
+                                           double c0, double c1,
                                            double t0, double t1, double al, double be, double om,
                                            double dinv, Dd* acc, double* o) {
   if (MODE == TM_A) {  // c0 = w_i, c1 = z_{i-1}; t0 = t_i, t1 = v_{i-1}
     const double kj = S[0], gj = S[st], lj = S[2 * st], sj = S[3 * st], rj = S[4 * st];
-    const double zoc = rr ? S[5 * st] : c1;    // replaced z_{i-1} (A26)
+    const double zoc = rr ? __ldg(zrr_g) : c1; // replaced z_{i-1} (A26), read from global
     const double m = dinv * c0;                // m_i
     const double nn = dinv * c1;               // n_{i-1}
     o[0] = kj + be * (gj - om * lj);           // line 5: g
@@ -402,6 +411,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   constexpr int NOUT = T::NOUT > 0 ? T::NOUT : 1;
   constexpr int K = T::K > 0 ? T::K : 1;
   constexpr bool PREC = T::PREC != 0;
+  constexpr int SD = StreamDepth<MODE_>::v;  // stream ring depth; stencil barriers follow
   static_assert(K <= RED_K, "partials buffer holds RED_K pairs per CTA");
   if (MODE == TM_A || MODE == TM_C || MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3 ||
       MODE == TM_PC) {
@@ -412,9 +422,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     if (sc->gap_iter >= sc->iter) return;
   }
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);  // [0,1] streams, [2..4] stencil
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);  // [0,SD) streams, [SD,SD+3) stencil
   double* st = reinterpret_cast<double*>(smem_raw + 64);
-  double* sv = st + 2 * NST * g.st_stride;
+  double* sv = st + SD * NST * g.st_stride;
   const int tid = threadIdx.x;
   const int nx = (int)g.nx;
   const int sts = g.st_stride, svs = g.sv_stride;
@@ -430,9 +440,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     svp[0] = (it & 1) ? V.w1 : V.w0;                 // w_i
     svp[1] = (it & 1) ? V.z0 : V.z1;                 // z_{i-1} pre-replacement
     stp[0] = V.k; stp[1 % NSTR_MAX] = V.g; stp[2 % NSTR_MAX] = V.l; stp[3 % NSTR_MAX] = V.s;
-    stp[4 % NSTR_MAX] = V.r;
-    stp[NSTR_MAX - 1] = V.zrr;                       // z_{i-1} replaced (A26)
-    nstr = rr ? 6 : 5;
+    stp[4 % NSTR_MAX] = V.r;                         // (replaced z_{i-1}: global load, A26)
     outp[0] = V.g; outp[1 % NOUT] = V.s; outp[2 % NOUT] = V.l;
     outp[3 % NOUT] = (it & 1) ? V.z1 : V.z0;         // z_i
   } else if (MODE == TM_C) {
@@ -501,11 +509,11 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     outp[0] = V.w0;
   }
   if (tid == 0) {
-    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < SD + 3; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
   __syncthreads();
-  uint32_t ph = 0;        // parity bits: bit s (streams 0,1), bit 2+s (stencil 0..2)
+  uint32_t ph = 0;        // parity bits: bit s (streams 0..SD-1), bit SD+s (stencil 0..2)
   int svc = 0, stc = 0;   // ring counters (slots filled so far)
   Dd acc[K];
 #pragma unroll
@@ -548,17 +556,19 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       for (int m = 0; m < 3 && m < nsv; ++m) {
         const int s = (svc + m) % 3;
         stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, (z0 - 1 + m) * g.pxy + toff - g.halo,
-              TP + 2 * g.halo, &bar[2 + s]);
+              TP + 2 * g.halo, &bar[SD + s]);
       }
       if (HAS_STR) {
-        const int s = stc % 2;
-        stage(st + (size_t)s * NST * sts, sts, stp, nstr, z0 * g.pxy + toff, TP, &bar[s]);
+        for (int m = 0; m < SD - 1 && m < nst; ++m) {  // planes z0 .. z0+SD-2
+          const int s = (stc + m) % SD;
+          stage(st + (size_t)s * NST * sts, sts, stp, nstr, (z0 + m) * g.pxy + toff, TP, &bar[s]);
+        }
       }
     }
     {  // plane z0-1 -> registers
       const int s = svc % 3;
-      mbar_wait(&bar[2 + s], (ph >> (2 + s)) & 1u);
-      ph ^= 1u << (2 + s);
+      mbar_wait(&bar[SD + s], (ph >> (SD + s)) & 1u);
+      ph ^= 1u << (SD + s);
       const double* b0p = sv + (size_t)s * NSV * svs +
                           align_off(svp[0] + (z0 - 1) * g.pxy + toff - g.halo) + g.halo + r;
       if (act) {
@@ -570,8 +580,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         }
       }
       const int s1 = (svc + 1) % 3;  // plane z0
-      mbar_wait(&bar[2 + s1], (ph >> (2 + s1)) & 1u);
-      ph ^= 1u << (2 + s1);
+      mbar_wait(&bar[SD + s1], (ph >> (SD + s1)) & 1u);
+      ph ^= 1u << (SD + s1);
     }
     for (int n = 0; n < nst; ++n) {
       const int64_t z = z0 + n;
@@ -580,17 +590,17 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         if (n + 3 < nsv) {  // plane z+2
           const int s = (svc + n + 3) % 3;
           stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, (z + 2) * g.pxy + toff - g.halo,
-                TP + 2 * g.halo, &bar[2 + s]);
+                TP + 2 * g.halo, &bar[SD + s]);
         }
-        if (HAS_STR && n + 1 < nst) {  // streams z+1
-          const int s = (stc + n + 1) % 2;
-          stage(st + (size_t)s * NST * sts, sts, stp, nstr, (z + 1) * g.pxy + toff, TP,
+        if (HAS_STR && n + SD - 1 < nst) {  // streams z+SD-1 into the slot step n-1 freed
+          const int s = (stc + n + SD - 1) % SD;
+          stage(st + (size_t)s * NST * sts, sts, stp, nstr, (z + SD - 1) * g.pxy + toff, TP,
                 &bar[s]);
         }
       }
-      const int s_z = (svc + n + 1) % 3, s_z1 = (svc + n + 2) % 3, s_st = (stc + n) % 2;
-      mbar_wait(&bar[2 + s_z1], (ph >> (2 + s_z1)) & 1u);
-      ph ^= 1u << (2 + s_z1);
+      const int s_z = (svc + n + 1) % 3, s_z1 = (svc + n + 2) % 3, s_st = (stc + n) % SD;
+      mbar_wait(&bar[SD + s_z1], (ph >> (SD + s_z1)) & 1u);
+      ph ^= 1u << (SD + s_z1);
       if (HAS_STR) {
         mbar_wait(&bar[s_st], (ph >> s_st) & 1u);
         ph ^= 1u << s_st;
@@ -636,12 +646,13 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       double o0[NOUT], o1[NOUT];
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) o0[k] = o1[k] = 0.0;
-      row_update<MODE, K, NOUT, NRM>(S0, sts, rr, c[0][0], c[1][0], t[0][0], t[1][0], al, be, om,
-                                g.dinv, acc, o0);
-      if (valid1)
-        row_update<MODE, K, NOUT, NRM>(HAS_STR ? S0 + 1 : nullptr, sts, rr, c[0][1], c[1][1], t[0][1],
-                                  t[1][1], al, be, om, g.dinv, acc, o1);
       const int64_t gi = z * g.pxy + toff + r;
+      row_update<MODE, K, NOUT, NRM>(S0, sts, rr, V.zrr + gi, c[0][0], c[1][0], t[0][0], t[1][0],
+                                     al, be, om, g.dinv, acc, o0);
+      if (valid1)
+        row_update<MODE, K, NOUT, NRM>(HAS_STR ? S0 + 1 : nullptr, sts, rr, V.zrr + gi + 1,
+                                       c[0][1], c[1][1], t[0][1], t[1][1], al, be, om, g.dinv,
+                                       acc, o1);
       if (T::NOUT > 0) {
 #pragma unroll
         for (int k = 0; k < NOUT; ++k) st2<VEC>(outp[k] + gi, o0[k], o1[k], valid1);
@@ -649,7 +660,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     }
     __syncthreads();  // unit done: every slot is free
     svc = (svc + nsv) % 3;
-    stc = (stc + nst) % 2;
+    stc = (stc + nst) % SD;
   }
   if (T::K > 0) {
     Dd tot[K];
@@ -678,7 +689,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
 // host-side helper: shared-memory bytes of a t_tile<., MODE, .> launch
 template <int M>
 inline size_t tile_smem_bytes_t(const TileGeo& g) {
-  return 64 + sizeof(double) * ((size_t)2 * TileTraits<M>::NSTR * g.st_stride +
+  return 64 + sizeof(double) * ((size_t)StreamDepth<M>::v * TileTraits<M>::NSTR * g.st_stride +
                                 (size_t)3 * TileTraits<M>::NSV * g.sv_stride);
 }
 
