@@ -82,6 +82,7 @@ template <> struct TileTraits<TM_AN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR =
 template <int M> struct StreamDepth { enum { v = 2 }; };
 template <> struct StreamDepth<TM_A> { enum { v = 3 }; };
 template <> struct StreamDepth<TM_AN> { enum { v = 3 }; };
+template <> struct StreamDepth<TM_CL3> { enum { v = 3 }; };  // measured: CL3 +4%; CL1, PC: no gain
 template <> struct TileTraits<TM_CN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 7, NOUT = 4, K = 9 }; };
 template <> struct TileTraits<TM_RR1N> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 4 }; };
 template <> struct TileTraits<TM_RR2N> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 6 }; };
