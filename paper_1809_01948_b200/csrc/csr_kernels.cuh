@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(256) c_spmvB(CsrOp A, Vecs V, Scal* __restrict
 
 // lines 17-21
 template <bool NRM, bool BJ>
-__global__ void __launch_bounds__(256) c_sweepC(CsrOp A, Vecs V, Scal* __restrict__ sc,
+// (256, 3): <= 85 registers keep 3 CTAs per SM for the block-Jacobi instance too
+__global__ void __launch_bounds__(256, 3) c_sweepC(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                 Dd* __restrict__ part, Hist h) {
   constexpr int K = NRM ? 9 : 5;
   if (sc->done) return;

@@ -34,9 +34,9 @@ thread_local std::string g_create_err;
 constexpr int WIN_SMEM = 64 + WRS * (int)sizeof(double);
 
 enum Kname { K_INIT = 0, K_SWEEPA, K_SWEEPC, K_SPMVB, K_SPMVD, K_RR1, K_RR2, K_GAP, K_APPLY, K_FIN,
-             K_CL1, K_CL2, K_CL3, K_PC, K_N };
-const char* kname_str[K_N] = {"init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2",
-                              "gap",  "apply",  "fin",    "cl1",   "cl2",   "cl3", "pcg"};
+             K_CL1, K_CL2, K_CL3, K_PC, K_PREC, K_N };
+const char* kname_str[K_N] = {"init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap",
+                              "apply", "fin", "cl1", "cl2", "cl3", "pcg", "prec"};
 
 // solver selected with option "method"
 enum Method { M_PBICGSTAB = 0, M_BICGSTAB = 1, M_PIPECG = 2 };
@@ -385,13 +385,15 @@ void launch_csr(pbicg_ctx* h, Phase p) {
         c_spmvB<<<h->grid[K_SPMVB], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
     case PH_SWEEPC: {
-      LaunchScope ls(h, K_SWEEPC);
-      if (h->csr.bj > 1) {
-        if (h->auto_rr) c_sweepC<true, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_sweepC<false, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      } else {
-        if (h->auto_rr) c_sweepC<true, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_sweepC<false, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      {
+        LaunchScope ls(h, K_SWEEPC);
+        if (h->csr.bj > 1) {
+          if (h->auto_rr) c_sweepC<true, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          else c_sweepC<false, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        } else {
+          if (h->auto_rr) c_sweepC<true, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          else c_sweepC<false, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        }
       }
     } break;
     case PH_RR1: {
@@ -1992,6 +1994,7 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "cl2") b = 4 * 8 * N;   // c_cl_u: read r,s,dinv; write M^-1 q
     else if (n == "cl3") b = 9 * 8 * N;   // c_cl_x: read x,mv,nv,r,s,y,r^; write x,r
     else if (n == "pcg") b = 19 * 8 * N;  // c_pc: read n,z,q,s,p,x,r,u,w,dinv; write 9
+    else if (n == "prec") b = 2 * 8 * N + pb + 8 * N;  // block Jacobi m = M^-1 w: w, binv rows; m
     else if (n == "iteration") b = 2 * mat + 36 * 8 * N + 2 * pb;
   }
   *bytes = b;

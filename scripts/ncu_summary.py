@@ -12,6 +12,9 @@ import re
 ALG = {  # algorithmic bytes per row: passes x 8 B
     "sweepA": 88, "sweepC": 104, "rr1": 56, "rr2": 40, "gap": 24, "init1": 40, "init2": 24,
     "cl1": 48, "cl2": 16, "cl3": 56, "pcg": 128, "pcinit1": 32, "pcinit2": 16,
+    # CSR at 27 nnz/row (ELL val 8 + col 4 per slot = 324 B/row), Jacobi
+    "csr_sweepA": 120, "csr_sweepC": 136, "csr_spmvB": 340, "csr_spmvD": 340,
+    "csr_init1": 372, "csr_init2": 364, "csr_apply": 340,
 }
 # t_tile<DIM, MODE, VEC>: MODE numbering of tile_sweeps.cuh TileMode
 MODES = ["sweepA", "sweepC", "rr1", "rr2", "gap", "init1", "init2", "cl1", "cl2", "cl3", "pcg",
@@ -22,6 +25,11 @@ def kernel_key(name: str):
     m = re.search(r"t_tile<\d, (\d+), ", name)
     if m:
         return MODES[int(m.group(1))]
+    for k, v in (("c_sweepA", "csr_sweepA"), ("c_sweepC", "csr_sweepC"), ("c_spmv_win<0>", "csr_spmvB"),
+                 ("c_spmv_win<1>", "csr_spmvD"), ("c_init1", "csr_init1"), ("c_init2", "csr_init2"),
+                 ("c_apply", "csr_apply")):
+        if name.startswith(k):
+            return v
     if "k_sweepA" in name:
         return "sweepA"
     if "k_sweepC" in name:
@@ -39,11 +47,17 @@ def main():
     ap.add_argument("--n", type=int, default=512 ** 3)
     ap.add_argument("--traffic", default=None)
     ap.add_argument("--title", default="ncu --set full summary")
-    ap.add_argument("--peak", type=float, default=6539.2)
+    ap.add_argument("--peak", type=float, default=6550.4)
+    ap.add_argument("--prec-extra", type=float, default=0.0,
+                    help="extra bytes/row of each CSR sweep (block Jacobi: (b-1)*8)")
     a = ap.parse_args()
     rows = list(csv.reader(open(a.raw)))
-    hdr, data = rows[0], rows[2:]
+    hdr, units, data = rows[0], rows[1], rows[2:]
     g = lambda d, k: d[hdr.index(k)] if k in hdr else ""
+    scale = {"byte": 1e-9, "Kbyte": 1e-6, "Mbyte": 1e-3, "Gbyte": 1.0, "Tbyte": 1e3,
+             "ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s": 1e3}
+    # per-column units row: convert bytes to GB and times to ms
+    gu = lambda d, k: float(g(d, k)) * scale.get(units[hdr.index(k)], 1.0)
     md = [f"# {a.title}", "",
           f"N = {a.n} rows; algorithmic bytes per row from DESIGN.md §7; peak {a.peak} GB/s "
           "(MEASURED_PEAKS.json hbm_gbs).", "",
@@ -53,9 +67,9 @@ def main():
     for d in data:
         name = g(d, "Kernel Name").replace("void ", "").split("(")[0]
         key = kernel_key(name)
-        t = float(g(d, "gpu__time_duration.sum"))
-        tot = float(g(d, "dram__bytes_read.sum")) + float(g(d, "dram__bytes_write.sum"))
-        alg = ALG.get(key, 0) * a.n / 1e9
+        t = gu(d, "gpu__time_duration.sum")
+        tot = gu(d, "dram__bytes_read.sum") + gu(d, "dram__bytes_write.sum")
+        alg = (ALG.get(key, 0) + (a.prec_extra if key in ("csr_sweepA", "csr_sweepC") else 0)) * a.n / 1e9
         bw = tot / t * 1e3
         md.append(f"| `{name}` | {t:.3f} | {tot:.3f} | {tot / alg if alg else float('nan'):.3f} | "
                   f"{bw:.0f} | {100 * bw / a.peak:.1f} | "

@@ -17,11 +17,12 @@ ap.add_argument("--rr", type=int, default=2)
 ap.add_argument("--gap", type=int, default=0)
 ap.add_argument("--method", type=int, default=0)
 ap.add_argument("--rr-auto", type=int, default=0)
+ap.add_argument("--block", type=int, default=1)
 a = ap.parse_args()
 cfg = problems.configs()[a.config]
 if cfg.kind == "csr":
     M = problems.csr_band(cfg.csr_n, nnz_row=27, band=4096, seed=1)
-    S = Solver.csr(M.n, M.row_ptr, M.col, M.val)
+    S = Solver.csr(M.n, M.row_ptr, M.col, M.val, block=a.block)
     n = M.n
 else:
     st = cfg.stencil
