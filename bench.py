@@ -217,7 +217,8 @@ def setup_solver(args, cfg, st, rank, world, dev, stream):
         if isinstance(st, CsrShape):
             M = csr_matrix(cfg)
             return Solver.csr(st.n, M.row_ptr, M.col, M.val, stream=stream, block=args.block)
-        return Solver.stencil(st.dim, st.nx, st.ny, st.nz, method_coef(args, st), stream=stream)
+        return Solver.stencil(st.dim, st.nx, st.ny, st.nz, method_coef(args, st), stream=stream,
+                              block=args.block)
     ids = [binding.nccl_unique_id(), binding.nccl_unique_id()] if rank == 0 else [None, None]
     torch.distributed.broadcast_object_list(ids, src=0)
     dist = binding.make_dist(world, rank, ids[0], ids[1])
@@ -229,7 +230,7 @@ def setup_solver(args, cfg, st, rank, world, dev, stream):
         return Solver.csr(st.n, rp, M.col[sl], M.val[sl], row_begin=lo, stream=stream, dist=dist,
                           block=args.block)
     return Solver.stencil(st.dim, st.nx, st.ny, st.nz, method_coef(args, st), stream=stream,
-                          dist=dist)
+                          dist=dist, block=args.block)
 
 
 def run_ours(args, rank, world):
@@ -423,7 +424,7 @@ def main():
                     help="solver: p-BiCGStab (the headline), classic BiCGStab or p-CG")
     ap.add_argument("--gap", type=int, default=0)
     ap.add_argument("--block", type=int, default=1,
-                    help="CSR configs: block-Jacobi block size (1 = Jacobi)")
+                    help="block-Jacobi block size (1 = Jacobi; CSR 2..32, stencils 2|4|8)")
     ap.add_argument("--rr-auto", type=int, default=0,
                     help="automated residual replacement (bound f^r + eq:criterion) instead of "
                          "the periodic schedule")

@@ -176,12 +176,13 @@ class Solver:
 
     # -- construction -----------------------------------------------------
     @classmethod
-    def stencil(cls, dim: int, nx: int, ny: int, nz: int, coef, stream=None, dist=None):
+    def stencil(cls, dim: int, nx: int, ny: int, nz: int, coef, stream=None, dist=None,
+                block: int = 1):
         st = _Stencil(dim, nx, ny, nz if dim == 3 else 1, (ctypes.c_double * 7)(*[float(c) for c in coef]))
         h = ctypes.c_void_p()
         d = ctypes.byref(dist) if dist is not None else None
-        _check(lib().pbicgstab_create_stencil(ctypes.byref(st), 1, d, _stream_ptr(stream),
-                                              ctypes.byref(h)))
+        _check(lib().pbicgstab_create_stencil(ctypes.byref(st), prec_code(block), d,
+                                              _stream_ptr(stream), ctypes.byref(h)))
         return cls(h)
 
     @classmethod
@@ -300,11 +301,12 @@ class LoopbackGroup:
         self.ranks = [Solver(ctypes.c_void_p(h)) for h in handles]
 
     @classmethod
-    def stencil(cls, nranks: int, dim: int, nx: int, ny: int, nz: int, coef, stream=None):
+    def stencil(cls, nranks: int, dim: int, nx: int, ny: int, nz: int, coef, stream=None,
+                block: int = 1):
         st = _Stencil(dim, nx, ny, nz if dim == 3 else 1,
                       (ctypes.c_double * 7)(*[float(c) for c in coef]))
         hs = (ctypes.c_void_p * nranks)()
-        _check(lib().pbicgstab_create_stencil_loopback(ctypes.byref(st), 1, nranks,
+        _check(lib().pbicgstab_create_stencil_loopback(ctypes.byref(st), prec_code(block), nranks,
                                                        _stream_ptr(stream), hs))
         return cls(hs)
 

@@ -41,6 +41,14 @@ const char* kname_str[K_N] = {"init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1
 // solver selected with option "method"
 enum Method { M_PBICGSTAB = 0, M_BICGSTAB = 1, M_PIPECG = 2 };
 
+// tile modes that have a block-Jacobi instance (p-BiCGStab + automated replacement;
+// the raw-stencil gap kernel needs none; the comparison solvers use Jacobi only)
+constexpr bool bj_mode(int m) {
+  return m == TM_A || m == TM_C || m == TM_RR1 || m == TM_RR2 || m == TM_INIT1 ||
+         m == TM_INIT2 || m == TM_AN || m == TM_CN || m == TM_RR1N || m == TM_RR2N ||
+         m == TM_INIT1N;
+}
+
 struct TimedLaunch {
   int k;
   cudaEvent_t e0, e1;
@@ -243,6 +251,13 @@ void launch_tile(pbicg_ctx* h) {
   const int per_sm = h->tile_occ[MODE] > 0 ? h->tile_occ[MODE] : 1;
   const int cap = h->num_sm * per_sm;
   const int grid = h->tg.units < cap ? h->tg.units : cap;
+  if constexpr (bj_mode(MODE)) {  // block Jacobi (nx % bj == 0 => paired 16-byte path)
+    if (h->tg.bj > 1) {
+      t_tile<DIM, MODE, true, true><<<grid, TNT, h->tile_smem[MODE], h->stream>>>(
+          h->tg, h->V, h->scal, h->part, h->hist);
+      return;
+    }
+  }
   if (h->tile_vec)
     t_tile<DIM, MODE, true><<<grid, TNT, h->tile_smem[MODE], h->stream>>>(h->tg, h->V, h->scal,
                                                                           h->part, h->hist);
@@ -870,6 +885,14 @@ cudaError_t set_tile_attr(pbicg_ctx* h) {
   if (e == cudaSuccess)
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, t_tile<DIM, MODE, true>, TNT,
                                                   h->tile_smem[MODE]);
+  if constexpr (bj_mode(MODE)) {
+    if (e == cudaSuccess && h->tg.bj > 1) {
+      e = cudaFuncSetAttribute(t_tile<DIM, MODE, true, true>, A, (int)h->tile_smem[MODE]);
+      if (e == cudaSuccess)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, t_tile<DIM, MODE, true, true>, TNT,
+                                                      h->tile_smem[MODE]);
+    }
+  }
   h->tile_occ[MODE] = occ < 1 ? 1 : occ;
   return e;
 }
@@ -1141,11 +1164,69 @@ void stencil_bound_consts(pbicg_ctx* h, const pbicg_stencil* op) {
   h->ar_nA = std::sqrt(cmax * rmax);
   h->ar_muN = (double)mu * std::sqrt(n);
   h->ar_mutN = 1.0 * std::sqrt(n) * std::fabs(1.0 / c[0]);
+  const int bj = h->tg.bj;
+  if (bj > 1) {  // ||M^-1|| <= sqrt(||B^-1||_1 ||B^-1||_inf) of the common block (A29, A33)
+    double rm = 0.0, cm = 0.0;
+    for (int a = 0; a < bj; ++a) {
+      double rs = 0.0;
+      for (int q = 0; q < bj; ++q) rs = rs + std::fabs(h->tg.bi[a * bj + q]);
+      if (rs > rm) rm = rs;
+    }
+    for (int q = 0; q < bj; ++q) {
+      double cs = 0.0;
+      for (int a = 0; a < bj; ++a) cs = cs + std::fabs(h->tg.bi[a * bj + q]);
+      if (cs > cm) cm = cs;
+    }
+    h->ar_mutN = (double)bj * std::sqrt(n) * std::sqrt(cm * rm);
+  }
   h->ar_ok = true;
 }
 
-pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op) {
+// the common bj x bj block of a constant-coefficient stencil along x (row i: coef[1]
+// at column i-1, coef[0] at i, coef[2] at i+1), inverted by the same Gauss-Jordan as
+// block_inverse / oracle.c (reading A33)
+pbicg_status stencil_block_inverse(const pbicg_stencil* op, int bj, double* bi) {
+  std::vector<double> a((size_t)bj * bj, 0.0), e((size_t)bj * bj);
+  for (int r = 0; r < bj; ++r) {
+    if (r > 0) a[(size_t)r * bj + r - 1] = op->coef[1];
+    a[(size_t)r * bj + r] = op->coef[0];
+    if (r + 1 < bj) a[(size_t)r * bj + r + 1] = op->coef[2];
+  }
+  for (int r = 0; r < bj; ++r)
+    for (int c = 0; c < bj; ++c) e[(size_t)r * bj + c] = (r == c) ? 1.0 : 0.0;
+  for (int p = 0; p < bj; ++p) {
+    const double piv = a[(size_t)p * bj + p];
+    if (piv == 0.0 || !std::isfinite(piv))
+      return fail(nullptr, PBICG_EINVAL, "block Jacobi: zero pivot in the stencil block");
+    const double f = 1.0 / piv;
+    for (int c = 0; c < bj; ++c) {
+      a[(size_t)p * bj + c] = a[(size_t)p * bj + c] * f;
+      e[(size_t)p * bj + c] = e[(size_t)p * bj + c] * f;
+    }
+    for (int r = 0; r < bj; ++r) {
+      if (r == p) continue;
+      const double g = a[(size_t)r * bj + p];
+      for (int c = 0; c < bj; ++c) {
+        a[(size_t)r * bj + c] = a[(size_t)r * bj + c] - g * a[(size_t)p * bj + c];
+        e[(size_t)r * bj + c] = e[(size_t)r * bj + c] - g * e[(size_t)p * bj + c];
+      }
+    }
+  }
+  for (size_t q = 0; q < e.size(); ++q) bi[q] = e[q];
+  return PBICG_OK;
+}
+
+pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
   h->kind = KIND_STENCIL;
+  h->tg.bj = 1;
+  if (bj > 1) {
+    if (op->nx % bj != 0)
+      return fail(h, PBICG_EINVAL, "block Jacobi on a stencil needs nx % b == 0");
+    if (op->nx > 1024)
+      return fail(h, PBICG_EINVAL, "block Jacobi on a stencil needs nx <= 1024 (tile kernels)");
+    ST(stencil_block_inverse(op, bj, h->tg.bi));
+    h->tg.bj = bj;
+  }
   stencil_bound_consts(h, op);
   h->dim = op->dim;
   const int64_t nz = op->dim == 3 ? op->nz : 1;
@@ -1190,6 +1271,8 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op) {
     h->grid[K_APPLY] = occ_grid(h, k_apply<2>, L);
   }
   setup_tile(h);
+  if (bj > 1 && !h->tile_ok)
+    return fail(h, PBICG_EINVAL, "block Jacobi on a stencil needs the TMA tile kernels");
   return alloc_common(h);
 }
 
@@ -1612,7 +1695,10 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
                                       pbicg_handle* out) {
   if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
   *out = nullptr;
-  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+  const int bj = prec_block(prec);
+  if (!bj || bj > 8)
+    return fail(nullptr, PBICG_EINVAL,
+                "stencil prec must be PBICG_PREC_JACOBI or PBICG_PREC_BJ(2|4|8)");
   const int nranks = dist ? dist->nranks : 1;
   if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
     return fail(nullptr, PBICG_EINVAL, "inconsistent nranks/rank");
@@ -1622,7 +1708,7 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
   h->rank = dist ? dist->rank : 0;
   pbicg_status st = common_setup(h, cuda_stream);
   if (!st && nranks > 1) st = nccl_setup(h, dist);
-  if (!st) st = build_stencil(h, op);
+  if (!st) st = build_stencil(h, op, bj);
   if (st) {
     g_create_err = h->err;
     destroy_one(h);
@@ -1670,7 +1756,10 @@ pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_pr
                                                int32_t nranks, void* cuda_stream,
                                                pbicg_handle* out) {
   if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
-  if (prec != PBICG_PREC_JACOBI) return fail(nullptr, PBICG_EINVAL, "only Jacobi is supported");
+  const int bj = prec_block(prec);
+  if (!bj || bj > 8)
+    return fail(nullptr, PBICG_EINVAL,
+                "stencil prec must be PBICG_PREC_JACOBI or PBICG_PREC_BJ(2|4|8)");
   ST(validate_stencil(op, nranks));
   for (int r = 0; r < nranks; ++r) out[r] = nullptr;
   cudaStream_t s;
@@ -1688,7 +1777,7 @@ pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_pr
     grp->alive++;
     st = common_setup(h, s);
     if (r == 0) h->own_stream = own;
-    if (!st) st = build_stencil(h, op);
+    if (!st) st = build_stencil(h, op, bj);
     if (st) g_create_err = h->err;
   }
   if (st) {
@@ -1797,6 +1886,8 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       m->overlap = value != 0 && (m->comm != COMM_NCCL || m->nccl_red != m->nccl_halo);
       destroy_graphs(m);
     } else if (k == "tile") {
+      if (value == 0 && m->kind == KIND_STENCIL && m->tg.bj > 1)
+        return fail(h, PBICG_EINVAL, "block Jacobi on a stencil runs on the tile kernels only");
       m->tile_on = value != 0;
       destroy_graphs(m);
     } else if (k == "rr_auto") {
@@ -1811,6 +1902,8 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       if (value != M_PBICGSTAB && m->auto_rr)
         return fail(h, PBICG_EINVAL, "switch rr_auto off before selecting method 1 or 2");
       if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "method must be 0, 1 or 2");
+      if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && m->tg.bj > 1)
+        return fail(h, PBICG_EINVAL, "methods 1 and 2 on a stencil use the Jacobi preconditioner");
       if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && !m->tile_ok)
         return fail(h, PBICG_EINVAL,
                     "methods 1 (BiCGStab) and 2 (p-CG) on a stencil need nx <= 1024 "

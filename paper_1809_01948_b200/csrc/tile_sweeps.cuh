@@ -101,6 +101,8 @@ struct TileGeo {
   int32_t halo;       // rows staged before the tile start (3D: nx + 2; 2D: 2)
   double c[7];
   double dinv;
+  int32_t bj;         // preconditioner: 1 Jacobi; 2, 4, 8 block Jacobi along x (reading A33)
+  double bi[64];      // bj > 1: the (common) bj x bj inverse block, row-major
 };
 
 __device__ __forceinline__ int align_off(const double* p) {
@@ -194,6 +196,95 @@ __device__ __forceinline__ void stencil_pair(const TileGeo& g, int nx, const dou
   t1 = a;
 }
 
+// ---------------------------------------------------------------------------
+// Block Jacobi on the stencil path (reading A33): blocks of bj consecutive x
+// points (nx % bj == 0), all with the same bj x bj matrix (constant coefficients,
+// the -x/+x legs inside a block always exist), so one inverse g.bi serves every
+// block.  (M^-1 v)_i = sum_k bi[i][k] v_k, ascending k from +0.0 (the oracle's order).
+// bj_row: position i of the block whose element 0 is at P.
+__device__ __forceinline__ double bj_row(const TileGeo& g, int i, const double* P) {
+  const int b = g.bj;
+  double acc = 0.0;
+  for (int k = 0; k < b; ++k) acc = acc + g.bi[i * b + k] * P[k];
+  return acc;
+}
+
+// both rows of the pair (positions i0, i0+1) from one pass over the block
+__device__ __forceinline__ void bj_pair(const TileGeo& g, int i0, const double* P, double& a,
+                                        double& c) {
+  const int b = g.bj;
+  double x = 0.0, y = 0.0;
+  for (int k = 0; k < b; ++k) {
+    const double v = P[k];
+    x = x + g.bi[i0 * b + k] * v;
+    y = y + g.bi[(i0 + 1) * b + k] * v;
+  }
+  a = x;
+  c = y;
+}
+
+// stencil_pair with M^-1 = block Jacobi: raw centre pair (c0, c1), preconditioned
+// centre pair (pc0, pc1) and fl(A M^-1 v) for the row pair (r, r+1); i0 = x % bj
+// of row r (even).  zm0/zm1 are the PRECONDITIONED values of plane z-1.  Legs as
+// in stencil_pair (A5); a dropped leg's value may be read past the line but is
+// never added.
+template <int DIM, bool VEC, bool INTERIOR>
+__device__ __forceinline__ void stencil_pair_bj(const TileGeo& g, int nx, int i0, const double* W,
+                                                const double* W1, double zm0, double zm1,
+                                                unsigned b0, unsigned b1, double& c0, double& c1,
+                                                double& pc0, double& pc1, double& t0, double& t1) {
+  const int b = g.bj;
+  const double* blk = W - i0;  // element 0 of this pair's block
+  ld2<VEC>(W, c0, c1);
+  bj_pair(g, i0, blk, pc0, pc1);
+  const double pm = i0 == 0 ? bj_row(g, b - 1, blk - b) : bj_row(g, i0 - 1, blk);
+  const double p2 = i0 + 2 == b ? bj_row(g, 0, blk + b) : bj_row(g, i0 + 2, blk);
+  double ym0 = 0.0, ym1 = 0.0, yp0 = 0.0, yp1 = 0.0, zp0, zp1;
+  if (DIM == 3) {
+    bj_pair(g, i0, blk - nx, ym0, ym1);
+    bj_pair(g, i0, blk + nx, yp0, yp1);
+  }
+  bj_pair(g, i0, W1 - i0, zp0, zp1);
+  const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
+  double a = 0.0;
+  a = leg<INTERIOR>(b0, 1u, a, czm * zm0);
+  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * ym0);
+  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * pm);
+  a = a + g.c[0] * pc0;
+  a = leg<INTERIOR>(b0, 8u, a, g.c[2] * pc1);
+  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * yp0);
+  a = leg<INTERIOR>(b0, 32u, a, czp * zp0);
+  t0 = a;
+  a = 0.0;
+  a = leg<INTERIOR>(b1, 1u, a, czm * zm1);
+  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * ym1);
+  a = leg<INTERIOR>(b1, 4u, a, g.c[1] * pc0);
+  a = a + g.c[0] * pc1;
+  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * p2);
+  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * yp1);
+  a = leg<INTERIOR>(b1, 32u, a, czp * zp1);
+  t1 = a;
+}
+
+// (M^-1 v) for the pair of row values (v0, v1) held by this thread when the block's
+// other values sit in the neighbouring lanes (RR1 / INIT1 form r = b - A x per row)
+__device__ __forceinline__ void bj_pair_shfl(const TileGeo& g, unsigned mask, int i0, double v0,
+                                             double v1, double& o0, double& o1) {
+  const int b = g.bj;
+  const int base = (threadIdx.x & 31) - i0 / 2;  // lane holding block elements 0, 1
+  double a = 0.0, c = 0.0;
+  for (int k = 0; k < b; k += 2) {
+    const double e0 = __shfl_sync(mask, v0, base + k / 2);
+    const double e1 = __shfl_sync(mask, v1, base + k / 2);
+    a = a + g.bi[i0 * b + k] * e0;
+    a = a + g.bi[i0 * b + k + 1] * e1;
+    c = c + g.bi[(i0 + 1) * b + k] * e0;
+    c = c + g.bi[(i0 + 1) * b + k + 1] * e1;
+  }
+  o0 = a;
+  o1 = c;
+}
+
 // The derived operand of a DERIVED mode from the staged values v[0..NSV-1] of
 // one element (same expression, same order as the oracle's stored vector).
 template <int MODE>
@@ -265,16 +356,16 @@ __device__ __forceinline__ void stencil_pair_der(const TileGeo& g, int nx, const
 
 // Per-row arithmetic of each mode.  S = stream slot at this row, st = stride;
 // c0/c1 = the stencil operands' centre values, t0/t1 = their stencil products.
-template <int MODE, int K, int NOUTC, bool NRM>
+template <int MODE, int K, int NOUTC, bool NRM, bool BJ>
 __device__ __forceinline__ void row_update(const double* S, int st, bool rr, const double* zrr_g,
-                                           double c0, double c1,
+                                           double pc0, double pc1, double c0, double c1,
                                            double t0, double t1, double al, double be, double om,
                                            double dinv, Dd* acc, double* o) {
   if (MODE == TM_A) {  // c0 = w_i, c1 = z_{i-1}; t0 = t_i, t1 = v_{i-1}
     const double kj = S[0], gj = S[st], lj = S[2 * st], sj = S[3 * st], rj = S[4 * st];
     const double zoc = rr ? __ldg(zrr_g) : c1; // replaced z_{i-1} (A26), read from global
-    const double m = dinv * c0;                // m_i
-    const double nn = dinv * c1;               // n_{i-1}
+    const double m = BJ ? pc0 : dinv * c0;     // m_i
+    const double nn = BJ ? pc1 : dinv * c1;    // n_{i-1}
     o[0] = kj + be * (gj - om * lj);           // line 5: g
     o[1] = c0 + be * (sj - om * zoc);          // line 6: s
     o[2] = m + be * (lj - om * nn);            // line 7: l
@@ -292,8 +383,8 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
   } else if (MODE == TM_C) {  // c0 = w_i, c1 = z_i; t0 = t_i, t1 = v_i
     const double xj = S[0], gj = S[st], kj = S[2 * st], lj = S[3 * st], rj = S[4 * st];
     const double sj = S[5 * st], rhj = S[6 * st];
-    const double m = dinv * c0;                // m_i
-    const double nn = dinv * c1;               // n_i (line 13)
+    const double m = BJ ? pc0 : dinv * c0;     // m_i
+    const double nn = BJ ? pc1 : dinv * c1;    // n_i (line 13)
     const double uu = kj - al * lj;            // line 10
     const double qq = rj - al * sj;            // line 9
     const double yy = c0 - al * c1;            // line 11
@@ -316,9 +407,12 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
     o[1] = dinv * rj;                          // k := M^-1 r
     o[2] = t1;                                 // s := A g
     o[3] = dinv * t1;                          // l := M^-1 s
-    if (NRM) {
-      nrm_add(acc[0], c0); nrm_add(acc[1 % K], o[1]); nrm_add(acc[2 % K], o[2]);
-      nrm_add(acc[3 % K], o[3]);
+    if (NRM) {  // (block Jacobi: k, l norms after the shuffle in t_tile)
+      nrm_add(acc[0], c0); nrm_add(acc[2 % K], o[2]);
+      if (!BJ) {
+        nrm_add(acc[1 % K], o[1]);
+        nrm_add(acc[3 % K], o[3]);
+      }
     }
   } else if (MODE == TM_RR2) {  // c = r, s; t0 = A M^-1 r = A k, t1 = A M^-1 s = A l
     const double rhj = S[0];
@@ -343,7 +437,7 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
     dd_fma(acc[1 % K], bj, bj);
     if (NRM) {
       nrm_add(acc[2 % K], c0);
-      nrm_add(acc[3 % K], o[2]);
+      if (!BJ) nrm_add(acc[3 % K], o[2]);
     }
   } else if (MODE == TM_INIT2) {  // c = r0; t0 = A M^-1 r0 = A k0
     o[0] = t0;                                 // w0
@@ -398,7 +492,7 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
 // Generic tile kernel.  VEC: every staged range and every vector is 16-byte
 // aligned (nx even) -> paired loads and stores.  One row pair per thread:
 // TP <= 2 * TNT.
-template <int DIM, int MODE_, bool VEC>
+template <int DIM, int MODE_, bool VEC, bool BJ = false>
 __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
                                                  Dd* __restrict__ part, Hist h) {
   using T = TileTraits<MODE_>;
@@ -412,6 +506,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   constexpr int NOUT = T::NOUT > 0 ? T::NOUT : 1;
   constexpr int K = T::K > 0 ? T::K : 1;
   constexpr bool PREC = T::PREC != 0;
+  constexpr bool BJP = BJ && PREC && !DER;  // stencil operands enter as A (block M)^-1 v
   constexpr int SD = StreamDepth<MODE_>::v;  // stream ring depth; stencil barriers follow
   static_assert(K <= RED_K, "partials buffer holds RED_K pairs per CTA");
   if (MODE == TM_A || MODE == TM_C || MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3 ||
@@ -547,6 +642,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         if (gy1 < g.ny - 1) b1 |= 16u;
       }
     }
+    const unsigned amask = __ballot_sync(0xffffffffu, act);  // blocks are all-in or all-out
+    const int i0 = BJ ? (r % nx) % g.bj : 0;                  // row r's position in its block
     const unsigned xy_all = DIM == 3 ? 30u : 12u;
     const bool xy_int = __all_sync(0xffffffffu, !act || ((b0 & xy_all) == xy_all &&
                                                          (b1 & xy_all) == xy_all));
@@ -575,6 +672,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       if (act) {
         if (DER) {
           derive_pair<VEC, NSV, MODE>(b0p, svs, al, be, om, m1[0][0], m1[0][1]);
+        } else if (BJP) {  // the -z leg takes M^-1 of plane z0-1
+#pragma unroll
+          for (int v = 0; v < NSO; ++v) bj_pair(g, i0, b0p + v * svs - i0, m1[v][0], m1[v][1]);
         } else {
 #pragma unroll
           for (int v = 0; v < NSO; ++v) ld2<VEC>(b0p + v * svs, m1[v][0], m1[v][1]);
@@ -617,7 +717,22 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       const bool zin = (g.o0 + z) > 0 && (g.o0 + z) < g.nog - 1;
       const unsigned zb = ((g.o0 + z) > 0 ? 1u : 0u) | ((g.o0 + z) < g.nog - 1 ? 32u : 0u);
       double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-      if (DER) {
+      double pc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // block Jacobi: M^-1 of the centre pair
+      if (BJP) {
+        if (xy_int && zin) {
+#pragma unroll
+          for (int v = 0; v < NSO; ++v)
+            stencil_pair_bj<DIM, VEC, true>(g, nx, i0, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                            m1[v][1], 0u, 0u, c[v][0], c[v][1], pc[v][0],
+                                            pc[v][1], t[v][0], t[v][1]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < NSO; ++v)
+            stencil_pair_bj<DIM, VEC, false>(g, nx, i0, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                             m1[v][1], b0 | zb, b1 | zb, c[v][0], c[v][1],
+                                             pc[v][0], pc[v][1], t[v][0], t[v][1]);
+        }
+      } else if (DER) {
         if (xy_int && zin)
           stencil_pair_der<DIM, VEC, true, PREC, NSV, MODE>(g, nx, Wz, svs, Wz1, m1[0][0],
                                                             m1[0][1], 0u, 0u, al, be, om, c[0][0],
@@ -641,19 +756,36 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       }
 #pragma unroll
       for (int v = 0; v < NSO; ++v) {
-        m1[v][0] = c[v][0];
-        m1[v][1] = c[v][1];
+        m1[v][0] = BJP ? pc[v][0] : c[v][0];
+        m1[v][1] = BJP ? pc[v][1] : c[v][1];
       }
       double o0[NOUT], o1[NOUT];
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) o0[k] = o1[k] = 0.0;
       const int64_t gi = z * g.pxy + toff + r;
-      row_update<MODE, K, NOUT, NRM>(S0, sts, rr, V.zrr + gi, c[0][0], c[1][0], t[0][0], t[1][0],
-                                     al, be, om, g.dinv, acc, o0);
+      row_update<MODE, K, NOUT, NRM, BJ>(S0, sts, rr, V.zrr + gi, pc[0][0], pc[1 % NSO][0],
+                                         c[0][0], c[1][0], t[0][0], t[1][0], al, be, om, g.dinv,
+                                         acc, o0);
       if (valid1)
-        row_update<MODE, K, NOUT, NRM>(HAS_STR ? S0 + 1 : nullptr, sts, rr, V.zrr + gi + 1,
-                                       c[0][1], c[1][1], t[0][1], t[1][1], al, be, om, g.dinv,
-                                       acc, o1);
+        row_update<MODE, K, NOUT, NRM, BJ>(HAS_STR ? S0 + 1 : nullptr, sts, rr, V.zrr + gi + 1,
+                                           pc[0][1], pc[1 % NSO][1], c[0][1], c[1][1], t[0][1],
+                                           t[1][1], al, be, om, g.dinv, acc, o1);
+      if (BJ && (MODE == TM_RR1 || MODE == TM_INIT1)) {
+        // k := M^-1 r (and l := M^-1 s): the block's r values sit in neighbouring lanes
+        const int ko = MODE == TM_RR1 ? 1 : 2;
+        bj_pair_shfl(g, amask, i0, o0[0], o1[0], o0[ko % NOUT], o1[ko % NOUT]);
+        if (MODE == TM_RR1) bj_pair_shfl(g, amask, i0, o0[2 % NOUT], o1[2 % NOUT], o0[3 % NOUT],
+                                         o1[3 % NOUT]);
+        if (NRM) {
+          const int kn = MODE == TM_RR1 ? 1 : 3;
+          nrm_add(acc[kn % K], o0[ko % NOUT]);
+          nrm_add(acc[kn % K], o1[ko % NOUT]);
+          if (MODE == TM_RR1) {
+            nrm_add(acc[3 % K], o0[3 % NOUT]);
+            nrm_add(acc[3 % K], o1[3 % NOUT]);
+          }
+        }
+      }
       if (T::NOUT > 0) {
 #pragma unroll
         for (int k = 0; k < NOUT; ++k) st2<VEC>(outp[k] + gi, o0[k], o1[k], valid1);
@@ -690,8 +822,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
 // host-side helper: shared-memory bytes of a t_tile<., MODE, .> launch
 template <int M>
 inline size_t tile_smem_bytes_t(const TileGeo& g) {
+  // + 16 doubles of slack: block-Jacobi reads of a dropped leg may run past the last slot
   return 64 + sizeof(double) * ((size_t)StreamDepth<M>::v * TileTraits<M>::NSTR * g.st_stride +
-                                (size_t)3 * TileTraits<M>::NSV * g.sv_stride);
+                                (size_t)3 * TileTraits<M>::NSV * g.sv_stride + 16);
 }
 
 inline size_t tile_smem_bytes(const TileGeo& g, int mode) {

@@ -1,5 +1,5 @@
 """GPU parity of the block-Jacobi preconditioner (reading A33)
-on CSR operators, against the oracle: the library inverts the diagonal blocks
+on CSR operators and matrix-free stencils, against the oracle: the library inverts the diagonal blocks
 with its own Gauss-Jordan (same textbook operations as the oracle's) and applies
 them with warp shuffles, so the runs are expected bitwise equal.
 """
@@ -98,6 +98,68 @@ def test_bj_loopback(S, orc, method):
     G.close()
 
 
+STENCILS = [(2, 64, 48, 1, "cd2"), (2, 40, 30, 1, "poisson"), (3, 16, 12, 10, "cd3"),
+            (3, 64, 64, 64, "cd3"), (3, 8, 5, 7, "cd3")]
+
+
+@pytest.mark.parametrize("block", [2, 4, 8])
+@pytest.mark.parametrize("shape", STENCILS)
+def test_bj_stencil_parity(S, orc, block, shape):
+    """Matrix-free stencils with x-aligned blocks: tile kernels apply the common
+    inverse block from shared memory (stencil legs) and by lane shuffles (k, l in
+    the replacement / init steps); bitwise vs the oracle's CSR form."""
+    from test_gpu_parity import coef_of
+    dim, nx, ny, nz, kind = shape
+    if nx % block:
+        pytest.skip("nx % b != 0")
+    coef = coef_of(kind)
+    solver = S.stencil(dim, nx, ny, nz, coef, block=block)
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 0)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    for rr in (0, 5):
+        res = solver.solve(b_d, tol=1e-11, maxit=150, rr_period=rr, gap=True)
+        ref = orc.pbicgstab(A, b, tol=1e-11, maxit=150, rr_period=rr, block=block)
+        assert res.outcome == ref.outcome
+        check_parity(res, ref, xs)
+    solver.set_option("bench", 1)
+    solver.set_option("rr_auto", 1)
+    res = solver.solve(b_d, tol=0.0, maxit=120, gap=True)
+    fr, rrl = solver.rr_info(res.iters)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=120, bench=True, auto_rr=True, block=block)
+    from test_gpu_autorr import check_auto
+    check_auto(res, fr, rrl, ref, xs)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_bj_stencil_loopback(S, orc, P):
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    dim, nx, ny, nz, blk = 3, 24, 10, 9, 4
+    coef = problems.cfg34_coef()
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 0)
+    b = orc.spmv(A, xs)
+    G = LoopbackGroup.stencil(P, dim, nx, ny, nz, coef, block=blk)
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=1e-11, maxit=200, rr_period=7, gap=True)
+    ref = orc.pbicgstab(A, b, tol=1e-11, maxit=200, rr_period=7, block=blk)
+    check_parity(res, ref, xs)
+    G.close()
+
+
+def test_bj_stencil_cfg3_fullsize_first_iterations(S, orc):
+    st = problems.configs()["cfg3"].stencil
+    solver = S.stencil(st.dim, st.nx, st.ny, st.nz, st.coef, block=4)
+    A = orc.stencil_csr(st.dim, st.nx, st.ny, st.nz, st.coef)
+    xs = problems.x_star(A.n, 0)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    res = solver.solve(b_d, tol=0.0, maxit=3, rr_period=2, gap=True)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=3, rr_period=2, block=4)
+    check_parity(res, ref, xs)
+
+
 def test_bj_errors(S, orc):
     from paper_1809_01948_b200.binding import PbicgError
     A = orc.stencil_csr(2, 10, 9, 1, problems.poisson2d_coef())  # n = 90
@@ -105,10 +167,12 @@ def test_bj_errors(S, orc):
         S.csr(A.n, A.rp, A.ci.astype(np.int32), A.va, block=4)
     with pytest.raises(PbicgError):  # unsupported block size
         S.csr(A.n, A.rp, A.ci.astype(np.int32), A.va, block=3)
-    with pytest.raises(PbicgError):  # stencils: Jacobi only
-        from paper_1809_01948_b200 import binding
-        import ctypes
-        st = binding._Stencil(2, 8, 8, 1, (ctypes.c_double * 7)(4, -1, -1, -1, -1, 0, 0))
-        h = ctypes.c_void_p()
-        binding._check(binding.lib().pbicgstab_create_stencil(ctypes.byref(st), 0x104, None, None,
-                                                              ctypes.byref(h)))
+    with pytest.raises(PbicgError):  # stencil: nx % b != 0
+        S.stencil(2, 10, 8, 1, problems.poisson2d_coef(), block=4)
+    with pytest.raises(PbicgError):  # stencil: b <= 8
+        S.stencil(2, 32, 8, 1, problems.poisson2d_coef(), block=16)
+    st = S.stencil(2, 32, 8, 1, problems.poisson2d_coef(), block=4)
+    with pytest.raises(PbicgError):  # comparison solvers use Jacobi
+        st.set_option("method", 1)
+    with pytest.raises(PbicgError):  # line kernels have no block Jacobi
+        st.set_option("tile", 0)
