@@ -26,6 +26,7 @@
 #include "csr_kernels.cuh"
 #include "nccl_dyn.h"
 #include "stencil_kernels.cuh"
+#include "tile_bj.h"
 #include "tile_sweeps.cuh"
 
 namespace {
@@ -251,11 +252,13 @@ void launch_tile(pbicg_ctx* h) {
   const int per_sm = h->tile_occ[MODE] > 0 ? h->tile_occ[MODE] : 1;
   const int cap = h->num_sm * per_sm;
   const int grid = h->tg.units < cap ? h->tg.units : cap;
-  if constexpr (bj_mode(MODE)) {  // block Jacobi (nx % bj == 0 => paired 16-byte path)
-    if (h->tg.bj > 1) {
-      t_tile<DIM, MODE, true, true><<<grid, TNT, h->tile_smem[MODE], h->stream>>>(
-          h->tg, h->V, h->scal, h->part, h->hist);
-      return;
+  if constexpr (bj_mode(MODE)) {  // block Jacobi instances live in tile_bj.cu
+    const size_t sm = h->tile_smem[MODE];
+    switch (h->tg.bj) {
+      case 2: tile_bj_launch_2(DIM, MODE, grid, sm, h->stream, h->tg, h->V, h->scal, h->part, h->hist); return;
+      case 4: tile_bj_launch_4(DIM, MODE, grid, sm, h->stream, h->tg, h->V, h->scal, h->part, h->hist); return;
+      case 8: tile_bj_launch_8(DIM, MODE, grid, sm, h->stream, h->tg, h->V, h->scal, h->part, h->hist); return;
+      default: break;
     }
   }
   if (h->tile_vec)
@@ -887,10 +890,10 @@ cudaError_t set_tile_attr(pbicg_ctx* h) {
                                                   h->tile_smem[MODE]);
   if constexpr (bj_mode(MODE)) {
     if (e == cudaSuccess && h->tg.bj > 1) {
-      e = cudaFuncSetAttribute(t_tile<DIM, MODE, true, true>, A, (int)h->tile_smem[MODE]);
-      if (e == cudaSuccess)
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, t_tile<DIM, MODE, true, true>, TNT,
-                                                      h->tile_smem[MODE]);
+      const int sm = (int)h->tile_smem[MODE];
+      if (h->tg.bj == 2) e = tile_bj_attr_2(DIM, MODE, sm, &occ);
+      else if (h->tg.bj == 4) e = tile_bj_attr_4(DIM, MODE, sm, &occ);
+      else e = tile_bj_attr_8(DIM, MODE, sm, &occ);
     }
   }
   h->tile_occ[MODE] = occ < 1 ? 1 : occ;

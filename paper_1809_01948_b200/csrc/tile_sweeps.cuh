@@ -201,55 +201,84 @@ __device__ __forceinline__ void stencil_pair(const TileGeo& g, int nx, const dou
 // points (nx % bj == 0), all with the same bj x bj matrix (constant coefficients,
 // the -x/+x legs inside a block always exist), so one inverse g.bi serves every
 // block.  (M^-1 v)_i = sum_k bi[i][k] v_k, ascending k from +0.0 (the oracle's order).
-// bj_row: position i of the block whose element 0 is at P.
-__device__ __forceinline__ double bj_row(const TileGeo& g, int i, const double* P) {
-  const int b = g.bj;
+// B: the block size as a template constant (2, 4, 8); bi: the inverse block staged
+// in shared memory (row-major B x B); rows are picked by the thread's position.
+template <int B>
+__device__ __forceinline__ double bj_row(const double* bi, int i, const double* P) {
   double acc = 0.0;
-  for (int k = 0; k < b; ++k) acc = acc + g.bi[i * b + k] * P[k];
+#pragma unroll
+  for (int k = 0; k < B; ++k) acc = acc + bi[i * B + k] * P[k];
   return acc;
 }
 
-// both rows of the pair (positions i0, i0+1) from one pass over the block
-__device__ __forceinline__ void bj_pair(const TileGeo& g, int i0, const double* P, double& a,
+// rows i0, i0+1 of the block at P (loaded once)
+template <int B, bool VEC>
+__device__ __forceinline__ void bj_pair(const double* bi, int i0, const double* P, double& a,
                                         double& c) {
-  const int b = g.bj;
+  double v[B];
+#pragma unroll
+  for (int k = 0; k < B; k += 2) ld2<VEC>(P + k, v[k], v[k + 1]);
   double x = 0.0, y = 0.0;
-  for (int k = 0; k < b; ++k) {
-    const double v = P[k];
-    x = x + g.bi[i0 * b + k] * v;
-    y = y + g.bi[(i0 + 1) * b + k] * v;
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    x = x + bi[i0 * B + k] * v[k];
+    y = y + bi[(i0 + 1) * B + k] * v[k];
   }
   a = x;
   c = y;
 }
 
 // stencil_pair with M^-1 = block Jacobi: raw centre pair (c0, c1), preconditioned
-// centre pair (pc0, pc1) and fl(A M^-1 v) for the row pair (r, r+1); i0 = x % bj
+// centre pair (pc0, pc1) and fl(A M^-1 v) for the row pair (r, r+1); i0 = x % B
 // of row r (even).  zm0/zm1 are the PRECONDITIONED values of plane z-1.  Legs as
 // in stencil_pair (A5); a dropped leg's value may be read past the line but is
 // never added.
-template <int DIM, bool VEC, bool INTERIOR>
-__device__ __forceinline__ void stencil_pair_bj(const TileGeo& g, int nx, int i0, const double* W,
-                                                const double* W1, double zm0, double zm1,
-                                                unsigned b0, unsigned b1, double& c0, double& c1,
-                                                double& pc0, double& pc1, double& t0, double& t1) {
-  const int b = g.bj;
-  const double* blk = W - i0;  // element 0 of this pair's block
-  ld2<VEC>(W, c0, c1);
-  bj_pair(g, i0, blk, pc0, pc1);
-  const double pm = i0 == 0 ? bj_row(g, b - 1, blk - b) : bj_row(g, i0 - 1, blk);
-  const double p2 = i0 + 2 == b ? bj_row(g, 0, blk + b) : bj_row(g, i0 + 2, blk);
+template <int DIM, bool VEC, bool INTERIOR, int B>
+__device__ __forceinline__ void stencil_pair_bj(const TileGeo& g, const double* bi, int nx, int i0,
+                                                const double* W, const double* W1, double zm0,
+                                                double zm1, unsigned b0, unsigned b1, double& c0,
+                                                double& c1, double& pc0, double& pc1, double& t0,
+                                                double& t1) {
+  const double* blk = W - i0;  // element 0 of this pair's block (16-byte aligned: i0, B even)
+  double v[B];
+#pragma unroll
+  for (int k = 0; k < B; k += 2) ld2<VEC>(blk + k, v[k], v[k + 1]);
+  c0 = v[0];
+  c1 = v[1];
+  if (B > 2) {  // the raw centre pair sits at i0, i0+1 of the block
+    ld2<VEC>(W, c0, c1);
+  }
+  double x0 = 0.0, x1 = 0.0, xm = 0.0, xp = 0.0;
+#pragma unroll
+  for (int k = 0; k < B; ++k) {
+    x0 = x0 + bi[i0 * B + k] * v[k];
+    x1 = x1 + bi[(i0 + 1) * B + k] * v[k];
+  }
+  pc0 = x0;
+  pc1 = x1;
+  if (i0 > 0) {  // x-1 inside this block
+#pragma unroll
+    for (int k = 0; k < B; ++k) xm = xm + bi[(i0 - 1) * B + k] * v[k];
+  } else {
+    xm = bj_row<B>(bi, B - 1, blk - B);
+  }
+  if (i0 + 2 < B) {  // x+2 inside this block
+#pragma unroll
+    for (int k = 0; k < B; ++k) xp = xp + bi[(i0 + 2) * B + k] * v[k];
+  } else {
+    xp = bj_row<B>(bi, 0, blk + B);
+  }
   double ym0 = 0.0, ym1 = 0.0, yp0 = 0.0, yp1 = 0.0, zp0, zp1;
   if (DIM == 3) {
-    bj_pair(g, i0, blk - nx, ym0, ym1);
-    bj_pair(g, i0, blk + nx, yp0, yp1);
+    bj_pair<B, VEC>(bi, i0, blk - nx, ym0, ym1);
+    bj_pair<B, VEC>(bi, i0, blk + nx, yp0, yp1);
   }
-  bj_pair(g, i0, W1 - i0, zp0, zp1);
+  bj_pair<B, VEC>(bi, i0, W1 - i0, zp0, zp1);
   const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
   double a = 0.0;
   a = leg<INTERIOR>(b0, 1u, a, czm * zm0);
   if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * ym0);
-  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * pm);
+  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * xm);
   a = a + g.c[0] * pc0;
   a = leg<INTERIOR>(b0, 8u, a, g.c[2] * pc1);
   if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * yp0);
@@ -260,7 +289,7 @@ __device__ __forceinline__ void stencil_pair_bj(const TileGeo& g, int nx, int i0
   if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * ym1);
   a = leg<INTERIOR>(b1, 4u, a, g.c[1] * pc0);
   a = a + g.c[0] * pc1;
-  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * p2);
+  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * xp);
   if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * yp1);
   a = leg<INTERIOR>(b1, 32u, a, czp * zp1);
   t1 = a;
@@ -268,18 +297,19 @@ __device__ __forceinline__ void stencil_pair_bj(const TileGeo& g, int nx, int i0
 
 // (M^-1 v) for the pair of row values (v0, v1) held by this thread when the block's
 // other values sit in the neighbouring lanes (RR1 / INIT1 form r = b - A x per row)
-__device__ __forceinline__ void bj_pair_shfl(const TileGeo& g, unsigned mask, int i0, double v0,
+template <int B>
+__device__ __forceinline__ void bj_pair_shfl(const double* bi, unsigned mask, int i0, double v0,
                                              double v1, double& o0, double& o1) {
-  const int b = g.bj;
   const int base = (threadIdx.x & 31) - i0 / 2;  // lane holding block elements 0, 1
   double a = 0.0, c = 0.0;
-  for (int k = 0; k < b; k += 2) {
+#pragma unroll
+  for (int k = 0; k < B; k += 2) {
     const double e0 = __shfl_sync(mask, v0, base + k / 2);
     const double e1 = __shfl_sync(mask, v1, base + k / 2);
-    a = a + g.bi[i0 * b + k] * e0;
-    a = a + g.bi[i0 * b + k + 1] * e1;
-    c = c + g.bi[(i0 + 1) * b + k] * e0;
-    c = c + g.bi[(i0 + 1) * b + k + 1] * e1;
+    a = a + bi[i0 * B + k] * e0;
+    a = a + bi[i0 * B + k + 1] * e1;
+    c = c + bi[(i0 + 1) * B + k] * e0;
+    c = c + bi[(i0 + 1) * B + k + 1] * e1;
   }
   o0 = a;
   o1 = c;
@@ -492,7 +522,7 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
 // Generic tile kernel.  VEC: every staged range and every vector is 16-byte
 // aligned (nx even) -> paired loads and stores.  One row pair per thread:
 // TP <= 2 * TNT.
-template <int DIM, int MODE_, bool VEC, bool BJ = false>
+template <int DIM, int MODE_, bool VEC, int BJ = 0>  // BJ: block-Jacobi block size (0 Jacobi)
 __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
                                                  Dd* __restrict__ part, Hist h) {
   using T = TileTraits<MODE_>;
@@ -506,7 +536,12 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   constexpr int NOUT = T::NOUT > 0 ? T::NOUT : 1;
   constexpr int K = T::K > 0 ? T::K : 1;
   constexpr bool PREC = T::PREC != 0;
-  constexpr bool BJP = BJ && PREC && !DER;  // stencil operands enter as A (block M)^-1 v
+  constexpr bool BJP = BJ > 0 && PREC && !DER;  // stencil operands enter as A (block M)^-1 v
+  constexpr int BB = BJ > 0 ? BJ : 2;          // block size for the helpers' array extents
+  __shared__ double s_bi[64];                  // the inverse block (row-major BB x BB)
+  if (BJ > 0) {
+    for (int q = threadIdx.x; q < BB * BB; q += blockDim.x) s_bi[q] = g.bi[q];
+  }
   constexpr int SD = StreamDepth<MODE_>::v;  // stream ring depth; stencil barriers follow
   static_assert(K <= RED_K, "partials buffer holds RED_K pairs per CTA");
   if (MODE == TM_A || MODE == TM_C || MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3 ||
@@ -643,7 +678,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       }
     }
     const unsigned amask = __ballot_sync(0xffffffffu, act);  // blocks are all-in or all-out
-    const int i0 = BJ ? (r % nx) % g.bj : 0;                  // row r's position in its block
+    const int i0 = BJ > 0 ? (r % nx) % BB : 0;                // row r's position in its block
     const unsigned xy_all = DIM == 3 ? 30u : 12u;
     const bool xy_int = __all_sync(0xffffffffu, !act || ((b0 & xy_all) == xy_all &&
                                                          (b1 & xy_all) == xy_all));
@@ -674,7 +709,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
           derive_pair<VEC, NSV, MODE>(b0p, svs, al, be, om, m1[0][0], m1[0][1]);
         } else if (BJP) {  // the -z leg takes M^-1 of plane z0-1
 #pragma unroll
-          for (int v = 0; v < NSO; ++v) bj_pair(g, i0, b0p + v * svs - i0, m1[v][0], m1[v][1]);
+          for (int v = 0; v < NSO; ++v)
+            bj_pair<BB, VEC>(s_bi, i0, b0p + v * svs - i0, m1[v][0], m1[v][1]);
         } else {
 #pragma unroll
           for (int v = 0; v < NSO; ++v) ld2<VEC>(b0p + v * svs, m1[v][0], m1[v][1]);
@@ -722,15 +758,15 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         if (xy_int && zin) {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair_bj<DIM, VEC, true>(g, nx, i0, Wz + v * svs, Wz1 + v * svs, m1[v][0],
-                                            m1[v][1], 0u, 0u, c[v][0], c[v][1], pc[v][0],
-                                            pc[v][1], t[v][0], t[v][1]);
+            stencil_pair_bj<DIM, VEC, true, BB>(g, s_bi, nx, i0, Wz + v * svs, Wz1 + v * svs,
+                                                m1[v][0], m1[v][1], 0u, 0u, c[v][0], c[v][1],
+                                                pc[v][0], pc[v][1], t[v][0], t[v][1]);
         } else {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair_bj<DIM, VEC, false>(g, nx, i0, Wz + v * svs, Wz1 + v * svs, m1[v][0],
-                                             m1[v][1], b0 | zb, b1 | zb, c[v][0], c[v][1],
-                                             pc[v][0], pc[v][1], t[v][0], t[v][1]);
+            stencil_pair_bj<DIM, VEC, false, BB>(g, s_bi, nx, i0, Wz + v * svs, Wz1 + v * svs,
+                                                 m1[v][0], m1[v][1], b0 | zb, b1 | zb, c[v][0],
+                                                 c[v][1], pc[v][0], pc[v][1], t[v][0], t[v][1]);
         }
       } else if (DER) {
         if (xy_int && zin)
@@ -763,19 +799,20 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) o0[k] = o1[k] = 0.0;
       const int64_t gi = z * g.pxy + toff + r;
-      row_update<MODE, K, NOUT, NRM, BJ>(S0, sts, rr, V.zrr + gi, pc[0][0], pc[1 % NSO][0],
+      row_update<MODE, K, NOUT, NRM, (BJ > 0)>(S0, sts, rr, V.zrr + gi, pc[0][0], pc[1 % NSO][0],
                                          c[0][0], c[1][0], t[0][0], t[1][0], al, be, om, g.dinv,
                                          acc, o0);
       if (valid1)
-        row_update<MODE, K, NOUT, NRM, BJ>(HAS_STR ? S0 + 1 : nullptr, sts, rr, V.zrr + gi + 1,
+        row_update<MODE, K, NOUT, NRM, (BJ > 0)>(HAS_STR ? S0 + 1 : nullptr, sts, rr, V.zrr + gi + 1,
                                            pc[0][1], pc[1 % NSO][1], c[0][1], c[1][1], t[0][1],
                                            t[1][1], al, be, om, g.dinv, acc, o1);
-      if (BJ && (MODE == TM_RR1 || MODE == TM_INIT1)) {
+      if (BJ > 0 && (MODE == TM_RR1 || MODE == TM_INIT1)) {
         // k := M^-1 r (and l := M^-1 s): the block's r values sit in neighbouring lanes
         const int ko = MODE == TM_RR1 ? 1 : 2;
-        bj_pair_shfl(g, amask, i0, o0[0], o1[0], o0[ko % NOUT], o1[ko % NOUT]);
-        if (MODE == TM_RR1) bj_pair_shfl(g, amask, i0, o0[2 % NOUT], o1[2 % NOUT], o0[3 % NOUT],
-                                         o1[3 % NOUT]);
+        bj_pair_shfl<BB>(s_bi, amask, i0, o0[0], o1[0], o0[ko % NOUT], o1[ko % NOUT]);
+        if (MODE == TM_RR1)
+          bj_pair_shfl<BB>(s_bi, amask, i0, o0[2 % NOUT], o1[2 % NOUT], o0[3 % NOUT],
+                           o1[3 % NOUT]);
         if (NRM) {
           const int kn = MODE == TM_RR1 ? 1 : 3;
           nrm_add(acc[kn % K], o0[ko % NOUT]);
