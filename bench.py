@@ -261,6 +261,8 @@ def run_ours(args, rank, world):
     S.set_option("bench", 1)
     S.set_option("graphs", 1)
     S.set_option("overlap", args.overlap)
+    if world > 1:
+        S.set_option("transport", args.transport)  # collective: every rank sets it
     gap = bool(args.gap)
 
     def step():
@@ -358,7 +360,8 @@ def run_ours(args, rank, world):
                    "l2": "inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9),
                    "parallelism": f"z-slab x{world}" + (" (NCCL halo + rank-row all-gather)"
                                                         if world > 1 else ""),
-                   "overlap": bool(args.overlap) if world > 1 else None},
+                   "overlap": bool(args.overlap) if world > 1 else None,
+                   "transport": (["nccl", "peer-memory"][args.transport] if world > 1 else None)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
@@ -399,6 +402,7 @@ def run_loopback(args):
     del xs
     G.set_option("bench", 1)
     G.set_option("overlap", args.overlap)
+    G.set_option("transport", args.transport)
     for _ in range(args.warmup):
         G.solve(bs, tol=0.0, maxit=maxit, rr_period=rr, gap=bool(args.gap))
     torch.cuda.synchronize()
@@ -428,6 +432,8 @@ def main():
     ap.add_argument("--rr-auto", type=int, default=0,
                     help="automated residual replacement (bound f^r + eq:criterion) instead of "
                          "the periodic schedule")
+    ap.add_argument("--transport", type=int, default=0,
+                    help="P > 1 reductions: 0 NCCL all-reduce, 1 peer-memory stores + flags")
     ap.add_argument("--overlap", type=int, default=1,
                     help="P > 1: dot-product reductions overlap the halo exchange / SpMV (1) "
                          "or block the compute stream (0)")

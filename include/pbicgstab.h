@@ -168,6 +168,13 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *                paper's p-CG comparison, reconstructed: DESIGN.md A19).
  *                Methods 1 and 2 need a stencil operator with nx <= 1024 and
  *                rr_period = 0 (EINVAL otherwise)
+ *   "transport"  multi-rank reductions: 0 (default) NCCL all-reduce of the zero-padded
+ *                rank rows (loopback: device copies); 1 peer memory -- the last CTA of
+ *                each reducing kernel stores its rank's Dot2 pairs into every rank's
+ *                receive buffer over NVLink (CUDA IPC mappings exchanged once with an
+ *                NCCL all-gather) and raises a flag; the finalize kernel waits for the
+ *                P flags.  No collective launch per reduction.  Collective option for
+ *                NCCL ranks (all call it with the same value); <= 8 ranks
  *   "rr_auto"    1 => automated residual replacement: the run-time bound
  *                f^r_i on the residual gap (eq:DDr_bound) is propagated on the device
  *                and iteration i replaces when f_{i-1} <= sqrt(eps)||r_{i-1}|| and

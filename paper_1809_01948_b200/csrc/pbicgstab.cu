@@ -107,6 +107,14 @@ struct pbicg_ctx {
   double ar_nA = 0, ar_muN = 0, ar_mutN = 0;  // bound constants (reading A29)
   bool ar_ok = false;                        // constants known for this operator
   int32_t last_iters = -1;                   // iterations of the last solve
+  // peer-memory reduction transport (option "transport" 1; state.cuh publish/k_fin)
+  int p2p = 0;
+  Dd* p2p_buf = nullptr;                     // own receive buffer [2][nranks][RED_K]
+  unsigned long long* p2p_flags = nullptr;   // own flags [nranks]
+  unsigned long long* p2p_ep = nullptr;      // own epoch counter
+  std::vector<Dd*> p2p_recv_tab;             // every rank's buffer, in this address space
+  std::vector<unsigned long long*> p2p_flag_tab;
+  std::vector<void*> ipc_opened;             // peer mappings to close
   int32_t last_nrr = 0;                      // replacements of the last solve
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
   std::vector<TimedLaunch> pending;
@@ -497,6 +505,7 @@ using VecSel = std::function<double*(pbicg_ctx*)>;
 void comm_reduce(const Members& G, bool on_side) {
   pbicg_ctx* h0 = G[0];
   if (h0->nranks == 1) return;
+  if (h0->p2p) return;  // the producing kernels already stored into every rank's buffer
   if (h0->comm == COMM_NCCL) {
     pbicg_ctx* h = h0;
     cudaStream_t s = on_side ? h->side : h->stream;
@@ -1065,6 +1074,73 @@ pbicg_status entry_sync(pbicg_ctx* h) {
   return PBICG_OK;
 }
 
+// Buffers of the peer-memory transport for one rank (zeroed flags and epoch).
+pbicg_status p2p_alloc(pbicg_ctx* h) {
+  if (h->p2p_buf) return PBICG_OK;
+  void *b = nullptr, *f = nullptr, *e = nullptr;
+  ST(dalloc(h, &b, (size_t)2 * h->nranks * RED_K * sizeof(Dd)));
+  ST(dalloc(h, &f, (size_t)h->nranks * sizeof(unsigned long long)));
+  ST(dalloc(h, &e, sizeof(unsigned long long)));
+  CU(cudaMemset(b, 0, (size_t)2 * h->nranks * RED_K * sizeof(Dd)));
+  CU(cudaMemset(f, 0, (size_t)h->nranks * sizeof(unsigned long long)));
+  CU(cudaMemset(e, 0, sizeof(unsigned long long)));
+  h->p2p_buf = (Dd*)b;
+  h->p2p_flags = (unsigned long long*)f;
+  h->p2p_ep = (unsigned long long*)e;
+  return PBICG_OK;
+}
+
+// Peer tables: loopback members share one address space; NCCL ranks exchange
+// CUDA IPC handles of their buffers with an all-gather (collective, once).
+pbicg_status p2p_setup(const Members& G) {
+  pbicg_ctx* h = G[0];
+  if (h->nranks > P2P_MAXR)
+    return fail(h, PBICG_EINVAL, "transport 1 (peer memory) supports up to 8 ranks");
+  if (h->comm == COMM_LOOP) {
+    for (pbicg_ctx* m : G) ST(p2p_alloc(m));
+    for (pbicg_ctx* m : G) {
+      m->p2p_recv_tab.clear();
+      m->p2p_flag_tab.clear();
+      for (pbicg_ctx* q : G) {
+        m->p2p_recv_tab.push_back(q->p2p_buf);
+        m->p2p_flag_tab.push_back(q->p2p_flags);
+      }
+    }
+    return PBICG_OK;
+  }
+  if (h->comm != COMM_NCCL) return fail(h, PBICG_ESTATE, "transport 1 needs several ranks");
+  if (!h->p2p_recv_tab.empty()) return PBICG_OK;
+  ST(p2p_alloc(h));
+  const int P = h->nranks;
+  cudaIpcMemHandle_t mine[2];
+  CU(cudaIpcGetMemHandle(&mine[0], h->p2p_buf));
+  CU(cudaIpcGetMemHandle(&mine[1], h->p2p_flags));
+  const size_t hb = sizeof(mine);
+  void *dsend = nullptr, *drecv = nullptr;
+  ST(dalloc(h, &dsend, hb));
+  ST(dalloc(h, &drecv, hb * P));
+  CU(cudaMemcpy(dsend, mine, hb, cudaMemcpyHostToDevice));
+  NC(nccl_api().AllGather(dsend, drecv, hb, ncclChar, h->nccl_halo, h->stream));
+  std::vector<cudaIpcMemHandle_t> all((size_t)2 * P);
+  CU(cudaStreamSynchronize(h->stream));
+  CU(cudaMemcpy(all.data(), drecv, hb * P, cudaMemcpyDeviceToHost));
+  for (int q = 0; q < P; ++q) {
+    if (q == h->rank) {
+      h->p2p_recv_tab.push_back(h->p2p_buf);
+      h->p2p_flag_tab.push_back(h->p2p_flags);
+      continue;
+    }
+    void *pb = nullptr, *pf = nullptr;
+    CU(cudaIpcOpenMemHandle(&pb, all[(size_t)2 * q], cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_opened.push_back(pb);
+    CU(cudaIpcOpenMemHandle(&pf, all[(size_t)2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
+    h->ipc_opened.push_back(pf);
+    h->p2p_recv_tab.push_back((Dd*)pb);
+    h->p2p_flag_tab.push_back((unsigned long long*)pf);
+  }
+  return PBICG_OK;
+}
+
 pbicg_status nccl_setup(pbicg_ctx* h, const pbicg_dist* d) {
   auto& api = nccl_api();
   if (!api.ok) return fail(h, PBICG_ESTATE, api.err);
@@ -1531,6 +1607,7 @@ void destroy_one(pbicg_ctx* h) {
   collect_timing(h);
   destroy_graphs(h);
   for (cudaEvent_t e : h->ev_pool) cudaEventDestroy(e);
+  for (void* p : h->ipc_opened) cudaIpcCloseMemHandle(p);
   for (void* p : h->allocs) cudaFree(p);
   if (h->scal_host) cudaFreeHost(h->scal_host);
   cudaEvent_t evs[] = {h->ev_entry, h->ev_poll[0], h->ev_poll[1], h->ev_fork, h->ev_join};
@@ -1608,6 +1685,14 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
     s0.rr_period = rr_period;
     s0.method = m->method;
     s0.auto_rr = m->auto_rr;
+    s0.p2p = m->p2p;
+    if (m->p2p) {
+      s0.p2p_epoch = m->p2p_ep;
+      for (int q = 0; q < m->nranks; ++q) {
+        s0.p2p_recv[q] = m->p2p_recv_tab[q];
+        s0.p2p_flag[q] = m->p2p_flag_tab[q];
+      }
+    }
     s0.ar_nA = m->ar_nA;
     s0.ar_muN = m->ar_muN;
     s0.ar_mutN = m->ar_mutN;
@@ -1878,6 +1963,18 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
 pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value) {
   if (!h || !key) return fail(h, PBICG_EINVAL, "NULL argument");
   std::string k(key);
+  if (k == "transport") {  // collective for NCCL ranks; applies to every loopback member
+    if (value < 0 || value > 1) return fail(h, PBICG_EINVAL, "transport must be 0 or 1");
+    if (value == 1) {
+      if (h->nranks == 1) return fail(h, PBICG_EINVAL, "transport 1 needs several ranks");
+      ST(p2p_setup(members(h)));
+    }
+    for (pbicg_ctx* m : members(h)) {
+      m->p2p = (int)value;
+      destroy_graphs(m);
+    }
+    return PBICG_OK;
+  }
   for (pbicg_ctx* m : members(h)) {
     if (k == "bench") {
       m->bench = value != 0;

@@ -19,6 +19,7 @@
 #define OUT_MAXIT 1
 #define OUT_BREAKDOWN 2
 #define RED_K 16  // dot slots per rank in the reduction buffers
+#define P2P_MAXR 8  // ranks of the peer-memory transport (one NVSwitch domain of B200s)
 
 struct Scal {
   double alpha, beta, omega, rho;  // alpha_i, beta_i, omega (latest), (r0, r_i)
@@ -50,6 +51,14 @@ struct Scal {
   int32_t nranks, rank;
   Dd* red_send;                    // [nranks][RED_K]: only row `rank` is ever written
   Dd* red_recv;                    // [nranks][RED_K]: all rows after the exchange
+  // peer-memory transport (option "transport" 1): the last CTA of a reducing kernel
+  // stores its rank's pairs into row `rank` of EVERY rank's p2p_recv[q] (NVLink
+  // stores; double-buffered by epoch parity) and raises p2p_flag[q][rank] = epoch;
+  // the finalize kernel waits for all P flags -- no collective launch at all
+  int32_t p2p;
+  unsigned long long* p2p_epoch;   // own counter (device, persists across solves)
+  Dd* p2p_recv[P2P_MAXR];          // rank q's receive buffer [2][nranks][RED_K]
+  unsigned long long* p2p_flag[P2P_MAXR];  // rank q's flags [nranks]
   unsigned int counter[16];        // last-CTA tickets, one per kernel kind
 };
 
@@ -336,9 +345,31 @@ __device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot) {
 
 // Tail of every reducing kernel (thread 0 of the last CTA): finish on one rank,
 // publish the rank's partial pairs on several.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 template <int F, int K>
 __device__ __forceinline__ void publish(Scal* sc, Hist h, const Dd (&tot)[K]) {
-  if (sc->nranks > 1) {
+  if (sc->nranks > 1 && sc->p2p) {
+    // every rank performs the same reductions in the same order: the epoch numbers
+    // them identically on all ranks
+    const unsigned long long e = *sc->p2p_epoch + 1;
+    *sc->p2p_epoch = e;
+    const int P = sc->nranks;
+    const size_t off = ((size_t)(e & 1) * P + sc->rank) * RED_K;
+    for (int q = 0; q < P; ++q) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) sc->p2p_recv[q][off + k] = tot[k];
+    }
+    __threadfence_system();
+    for (int q = 0; q < P; ++q) st_release_sys(sc->p2p_flag[q] + sc->rank, e);
+  } else if (sc->nranks > 1) {
     Dd* row = sc->red_send + (size_t)sc->rank * RED_K;
 #pragma unroll
     for (int k = 0; k < K; ++k) row[k] = tot[k];
@@ -358,12 +389,26 @@ __global__ void k_fin(Scal* __restrict__ sc, Hist h) {
   } else if (F != F_INIT1 && F != F_INIT2) {
     if (sc->done) return;
   }
+  const Dd* rows = sc->red_recv;
+  if (sc->p2p) {  // wait for every rank's pairs of this epoch (written by their kernels)
+    const unsigned long long e = *sc->p2p_epoch;
+    const unsigned long long* flag = sc->p2p_flag[sc->rank];
+    for (int r = 0; r < sc->nranks; ++r)
+      while (ld_acquire_sys(flag + r) < e) __nanosleep(32);
+    rows = sc->p2p_recv[sc->rank] + (size_t)(e & 1) * sc->nranks * RED_K;
+  }
   Dd tot[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) tot[k] = dd_zero();
   for (int r = 0; r < sc->nranks; ++r) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) tot[k] = dd_add(tot[k], sc->red_recv[(size_t)r * RED_K + k]);
+    for (int k = 0; k < K; ++k) {
+      const Dd* q = rows + (size_t)r * RED_K + k;
+      Dd v;
+      v.hi = __ldcv(&q->hi);  // peers wrote it over NVLink: bypass L1
+      v.lo = __ldcv(&q->lo);
+      tot[k] = dd_add(tot[k], v);
+    }
   }
   fin_step<F>(sc, h, tot);
 }

@@ -113,3 +113,63 @@ def test_partition_is_balanced_slabs(B):
     rb = [s.row_begin for s in G.ranks]
     assert nl == [400, 400, 300] and rb == [0, 400, 800]
     G.close()
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("case", ["stencil", "stencil_auto", "stencil_bj", "classic", "pipecg",
+                                  "csr", "csr_pipecg"])
+def test_peer_memory_transport(B, orc, P, case):
+    """option transport=1: the producing kernels store their rank's Dot2 pairs into
+    every rank's receive buffer and the finalize kernels wait on per-rank flags
+    (no collective launch).  Results are those of the copy transport (and the
+    oracle), bitwise, over repeated solves (the epoch counter persists)."""
+    coef = problems.cfg34_coef()
+    spd = [6.0, -1, -1, -1, -1, -1, -1]
+    if case.startswith("csr"):
+        n = 4096 * P
+        M = problems.csr_band(n, nnz_row=15, band=900, seed=3)
+        rp, ci, va = M.row_ptr, M.col, M.val
+        if case == "csr_pipecg":
+            A0 = orc.stencil_csr(2, 64, n // 64, 1, problems.poisson2d_coef())
+            rp, ci, va = A0.rp, A0.ci.astype(np.int32), A0.va
+        A = orc.csr(rp, ci, va)
+        cuts = [n * r // P for r in range(P + 1)]
+        blocks = [(cuts[r], rp[cuts[r]:cuts[r + 1] + 1] - rp[cuts[r]], ci[rp[cuts[r]]:rp[cuts[r + 1]]],
+                   va[rp[cuts[r]]:rp[cuts[r + 1]]]) for r in range(P)]
+        make = lambda: B.LoopbackGroup.csr(blocks, n)
+    else:
+        dim, nx, ny, nz = 3, 24, 10, 13
+        cf = spd if case == "pipecg" else coef
+        A = orc.stencil_csr(dim, nx, ny, nz, cf)
+        blk = 4 if case == "stencil_bj" else 1
+        make = lambda: B.LoopbackGroup.stencil(P, dim, nx, ny, nz, cf, block=blk)
+    method = {"classic": 1, "pipecg": 2, "csr_pipecg": 2}.get(case, 0)
+    auto = case == "stencil_auto"
+    rr = 0 if (method or auto) else 4
+    xs = problems.x_star(A.n, 0)
+    b = orc.spmv(A, xs)
+    out = []
+    for transport in (0, 1):
+        G = make()
+        G.set_option("method", method)
+        G.set_option("rr_auto", int(auto))
+        G.set_option("bench", 1)
+        G.set_option("transport", transport)
+        bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+        for rep in range(2):  # the epoch counter carries over between solves
+            res = G.solve(bs, tol=0.0, maxit=60, rr_period=rr, gap=True)
+        out.append(res)
+        G.close()
+    kw = dict(tol=0.0, maxit=60, bench=True)
+    if method == 1:
+        ref = orc.bicgstab(A, b, **kw)
+    elif method == 2:
+        ref = orc.pipecg(A, b, **kw)
+    else:
+        ref = orc.pbicgstab(A, b, rr_period=rr, auto_rr=auto, block=4 if case == "stencil_bj" else 1,
+                            **kw)
+    for res in out:
+        _parity(res, ref, xs, bitwise=False)
+    assert np.array_equal(out[0].rnorm, out[1].rnorm)
+    assert np.array_equal(out[0].x.cpu().numpy(), out[1].x.cpu().numpy())
+    assert np.array_equal(out[0].gap, out[1].gap)
