@@ -261,6 +261,8 @@ def run_ours(args, rank, world):
     S.set_option("bench", 1)
     S.set_option("graphs", 1)
     S.set_option("overlap", args.overlap)
+    if args.schedule:
+        S.set_option("schedule", args.schedule)
     if world > 1:
         S.set_option("transport", args.transport)  # collective: every rank sets it
     gap = bool(args.gap)
@@ -355,8 +357,10 @@ def run_ours(args, rank, world):
                    "rr_auto": bool(args.rr_auto),
                    "preconditioner": "jacobi" if args.block == 1 else f"block-jacobi {args.block}",
                    "method": args.method,
-                   "schedule": SCHEDULES[args.method] if st.dim else
-                               "split 4-phase (CSR as ELL), reduction #1 overlapped",
+                   "schedule": (("split 4-phase (stencil), stand-alone TMA SpMVs the reductions "
+                                 "hide behind" if args.schedule == 2 else SCHEDULES[args.method])
+                                if st.dim else
+                                "split 4-phase (CSR as ELL), reduction #1 overlapped"),
                    "l2": "inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9),
                    "parallelism": f"z-slab x{world}" + (" (NCCL halo + rank-row all-gather)"
                                                         if world > 1 else ""),
@@ -403,6 +407,8 @@ def run_loopback(args):
     G.set_option("bench", 1)
     G.set_option("overlap", args.overlap)
     G.set_option("transport", args.transport)
+    if args.schedule:
+        G.set_option("schedule", args.schedule)
     for _ in range(args.warmup):
         G.solve(bs, tol=0.0, maxit=maxit, rr_period=rr, gap=bool(args.gap))
     torch.cuda.synchronize()
@@ -432,6 +438,9 @@ def main():
     ap.add_argument("--rr-auto", type=int, default=0,
                     help="automated residual replacement (bound f^r + eq:criterion) instead of "
                          "the periodic schedule")
+    ap.add_argument("--schedule", type=int, default=0,
+                    help="stencil p-BiCGStab: 0 auto (fused), 1 fused 2-sweep, 2 the paper's split "
+                         "4-phase pipeline")
     ap.add_argument("--transport", type=int, default=0,
                     help="P > 1 reductions: 0 NCCL all-reduce, 1 peer-memory stores + flags")
     ap.add_argument("--overlap", type=int, default=1,

@@ -253,7 +253,9 @@ enum Phase { PH_INIT1, PH_INIT2, PH_SWEEPA, PH_SPMVB, PH_SWEEPC, PH_RR1, PH_RR2,
              PH_CL1, PH_CL2, PH_CL3, PH_PC, PH_PCI1, PH_PCI2,
              // CSR comparison solvers: element-wise steps and SpMVs with epilogues
              PH_CCP, PH_SP_CLS, PH_CCU, PH_SP_CLY, PH_CCX, PH_SP_PCW0, PH_SP_PCN, PH_CPC,
-             PH_PRECMV };
+             PH_PRECMV,
+             // stencil split schedule (option schedule 2)
+             PH_SWEEPA2, PH_SWEEPC2, PH_SPB, PH_SPD };
 
 template <int DIM, int MODE>
 void launch_tile(pbicg_ctx* h) {
@@ -331,6 +333,16 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
     case PH_PC: { LaunchScope ls(h, K_PC); launch_tile<DIM, TM_PC>(h); } break;
     case PH_PCI1: { LaunchScope ls(h, K_INIT); launch_tile<DIM, TM_PCI1>(h); } break;
     case PH_PCI2: { LaunchScope ls(h, K_INIT); launch_tile<DIM, TM_PCI2>(h); } break;
+    case PH_SWEEPA2: {
+      LaunchScope ls(h, K_SWEEPA);
+      k_sweepA2<DIM><<<h->grid[K_PREC], 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_SWEEPC2: {
+      LaunchScope ls(h, K_SWEEPC);
+      k_sweepC2<DIM><<<h->grid[K_PREC], 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+    } break;
+    case PH_SPB: { LaunchScope ls(h, K_SPMVB); launch_tile<DIM, TM_SPB>(h); } break;
+    case PH_SPD: { LaunchScope ls(h, K_SPMVD); launch_tile<DIM, TM_SPD>(h); } break;
     default:
       break;
   }
@@ -718,8 +730,9 @@ void enq_init(const Members& G) {
   if (h0->kind == KIND_CSR) {  // t_0 = A m_0 (line 3)
     if (dist) comm_halo(G, {SMV});
     each(G, PH_SPMVD);
-  } else if (dist) {
-    comm_halo(G, {SW0});  // w_0 is read with the stencil
+  } else {
+    if (dist) comm_halo(G, {SW0});  // w_0 is read with the stencil
+    if (h0->schedule == 2) each(G, PH_SPD);  // split schedule: t_0 stored
   }
   if (h0->gap_on) {
     each(G, PH_GAP);
@@ -741,6 +754,44 @@ void enq_iter(const Members& G, bool with_rr, int par) {
       enq_iter_pipecg(G, par);
     }
     enq_gap(G);
+    return;
+  }
+  if (h0->kind == KIND_STENCIL && h0->schedule == 2) {
+    // split 4-phase schedule (the paper's): each reduction hides behind the
+    // halo exchange + stand-alone SpMV of the vector the next phase needs
+    const bool ov = dist && h0->overlap;
+    each(G, PH_SWEEPA2);  // lines 5-12 with stored t_i, v_{i-1}
+    if (ov) fork_reduce(G);
+    else if (dist) comm_reduce(G, false);
+    if (dist) comm_halo(G, {par ? SZ1 : SZ0});
+    each(G, PH_SPB);  // lines 13-14: v_i = A M^-1 z_i
+    if (ov) join_reduce(G);
+    each_fin(G, F_SWEEPA);
+    each(G, PH_SWEEPC2);  // lines 16-21
+    if (ov && !with_rr) {  // reduction #2 || halo w_{i+1} + SpMV_D (no replacement possible)
+      fork_reduce(G);
+      comm_halo(G, {par ? SW0 : SW1});
+      each(G, PH_SPD);  // lines 22-23 (harmless if this iteration converged)
+      join_reduce(G);
+      each_fin(G, F_SWEEPC);
+    } else {
+      reduce_fin(G, F_SWEEPC);
+      if (with_rr) {  // eq:rr after line 20
+        if (dist) comm_halo(G, {SX, SG});
+        each(G, PH_RR1);
+        if (h0->auto_rr) reduce_fin(G, F_RR1);
+        if (dist) comm_halo(G, {SR, SS});
+        each(G, PH_RR2);
+        reduce_fin(G, F_RR2);
+      }
+      if (dist) comm_halo(G, {par ? SW0 : SW1});
+      each(G, PH_SPD);  // t_{i+1} from the (replaced) w_{i+1} (A27)
+    }
+    if (h0->gap_on) {
+      if (dist) comm_halo(G, {SX});
+      each(G, PH_GAP);
+      reduce_fin(G, F_GAP);
+    }
     return;
   }
   if (h0->kind == KIND_STENCIL) {
@@ -929,6 +980,8 @@ cudaError_t set_tile_attrs(pbicg_ctx* h) {
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_RR1N>(h);
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_RR2N>(h);
   if (e == cudaSuccess) e = set_tile_attr<DIM, TM_INIT1N>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_SPB>(h);
+  if (e == cudaSuccess) e = set_tile_attr<DIM, TM_SPD>(h);
   return e;
 }
 
@@ -1340,6 +1393,8 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
     h->grid[K_RR2] = occ_grid(h, k_rr2<3>, L);
     h->grid[K_GAP] = occ_grid(h, k_gap<3>, L);
     h->grid[K_APPLY] = occ_grid(h, k_apply<3>, L);
+    { const int b0 = h->block; h->block = 256;
+      h->grid[K_PREC] = occ_grid(h, k_sweepC2<3>, (h->n_local + 255) / 256); h->block = b0; }
   } else {
     h->grid[K_INIT] = occ_grid(h, k_init1<2>, L);
     h->grid[K_SWEEPA] = occ_grid(h, k_sweepA<2>, L);
@@ -1348,6 +1403,8 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
     h->grid[K_RR2] = occ_grid(h, k_rr2<2>, L);
     h->grid[K_GAP] = occ_grid(h, k_gap<2>, L);
     h->grid[K_APPLY] = occ_grid(h, k_apply<2>, L);
+    { const int b0 = h->block; h->block = 256;
+      h->grid[K_PREC] = occ_grid(h, k_sweepC2<2>, (h->n_local + 255) / 256); h->block = b0; }
   }
   setup_tile(h);
   if (bj > 1 && !h->tile_ok)
@@ -1992,7 +2049,7 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       destroy_graphs(m);
     } else if (k == "rr_auto") {
       if (value != 0 && (m->method != M_PBICGSTAB || !m->ar_ok ||
-                         (m->kind == KIND_STENCIL && !m->tile_ok)))
+                         (m->kind == KIND_STENCIL && (!m->tile_ok || m->schedule == 2))))
         return fail(h, PBICG_EINVAL,
                     "rr_auto needs method 0 and a stencil with nx <= 1024 (TMA tile kernels) or "
                     "a CSR operator on one process (bound constants need every row)");
@@ -2002,6 +2059,8 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       if (value != M_PBICGSTAB && m->auto_rr)
         return fail(h, PBICG_EINVAL, "switch rr_auto off before selecting method 1 or 2");
       if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "method must be 0, 1 or 2");
+      if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && m->schedule == 2)
+        return fail(h, PBICG_EINVAL, "methods 1 and 2 run their own schedules (set schedule 0)");
       if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && m->tg.bj > 1)
         return fail(h, PBICG_EINVAL, "methods 1 and 2 on a stencil use the Jacobi preconditioner");
       if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && !m->tile_ok)
@@ -2012,11 +2071,19 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       destroy_graphs(m);
     } else if (k == "schedule") {
       if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "schedule must be 0, 1 or 2");
-      if (value == 2 && m->kind == KIND_STENCIL)
-        return fail(h, PBICG_EINVAL, "split schedule is not built for stencils in this version");
+      if (value == 2 && m->kind == KIND_STENCIL) {
+        if (!m->tile_ok || m->tg.bj > 1 || m->auto_rr || m->method != M_PBICGSTAB)
+          return fail(h, PBICG_EINVAL,
+                      "split stencil schedule: Jacobi, nx <= 1024, method 0, rr_auto off");
+        if (!m->V.tv) {
+          ST(gvec(m, &m->V.tv));
+          ST(gvec(m, &m->V.vv));
+        }
+      }
       if (value == 1 && m->kind == KIND_CSR)
         return fail(h, PBICG_EINVAL, "fused schedule is stencil-only");
       m->schedule = (int)value;
+      destroy_graphs(m);
     } else {
       return fail(h, PBICG_EINVAL, "unknown option '" + k + "'");
     }
@@ -2152,7 +2219,17 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
   std::string n(name);
   const double N = (double)h->n_local;
   double b = 0;
-  if (h->kind == KIND_STENCIL) {
+  if (h->kind == KIND_STENCIL && h->schedule == 2) {
+    // split schedule (SURVEY 8(a)'s 32 passes)
+    if (n == "sweepA") b = 13 * 8 * N;       // read k,g,l,s,r,w,z,t,v; write g,s,l,z
+    else if (n == "sweepC") b = 15 * 8 * N;  // read x,g,k,l,r,s,r^,w,z,t,v; write x,r,k,w
+    else if (n == "spmvB" || n == "spmvD") b = 2 * 8 * N;
+    else if (n == "rr1") b = 7 * 8 * N;
+    else if (n == "rr2") b = 5 * 8 * N;
+    else if (n == "gap") b = 3 * 8 * N;
+    else if (n == "apply") b = 2 * 8 * N;
+    else if (n == "iteration") b = 32 * 8 * N;
+  } else if (h->kind == KIND_STENCIL) {
     // fused schedule: every vector read / written once per launch
     if (n == "cl1") b = 6 * 8 * N;        // Alg. 1: read r,p,s,r^; write p,s
     else if (n == "cl2") b = 2 * 8 * N;   // read r,s

@@ -34,6 +34,7 @@ struct Scal {
   int32_t gap_iter;                // last iteration whose gap was written
   int32_t bench, rr_period;
   int32_t method;                  // 0 p-BiCGStab (Alg. 2), 1 BiCGStab (Alg. 1), 2 p-CG
+  int32_t spd_par;                 // split stencil schedule: buffer parity of the w SpMV_D reads
   double g_old, a_old;             // p-CG: gamma_{i-1}, alpha_{i-1}
   // automated residual replacement (oracle.c orc_pbicgstab, ORC_AUTO_RR)
   int32_t auto_rr;                 // option rr_auto

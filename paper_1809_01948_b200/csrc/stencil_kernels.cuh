@@ -34,6 +34,7 @@ struct Vecs {
   double *x, *r, *rh, *k, *g, *s, *l, *b;
   double *w0, *w1, *z0, *z1, *zrr;
   double *nv, *mv;  // CSR path: n = M^-1 z and m = M^-1 w, inputs of the window SpMVs
+  double *tv, *vv;  // stencil split schedule: stored t_i = A M^-1 w_i, v_i = A M^-1 z_i
 };
 
 template <int DIM>
@@ -299,4 +300,93 @@ __global__ void __launch_bounds__(256) k_apply(Geo g, const double* __restrict__
   const double xc = xin[j];
   yout[j] = apply_row<DIM, false>(xin, j, xc, g, NBR);
   STENCIL_LOOP_END
+}
+
+// ---------------------------------------------------------------------------
+// Split 4-phase schedule on a stencil (option schedule 2; the paper's own
+// pipeline): the SpMVs of lines 13-14 and 22-23 are separate tile kernels
+// (TM_SPB / TM_SPD) that the two global reductions hide behind on P ranks; these
+// two point-wise sweeps read the stored t_i, v_{i-1} / v_i.  Same operations in the
+// same order as the fused sweeps (tile_sweeps.cuh row_update), so bitwise equal.
+// Buffers follow the fused convention: w_i in {w0, w1}[i & 1], z_i in {z0, z1}[i & 1].
+template <int DIM>
+__global__ void __launch_bounds__(256) k_sweepA2(Geo g, Vecs V, Scal* __restrict__ sc,
+                                                 Dd* __restrict__ part, Hist h) {
+  if (sc->done) return;
+  const int it = sc->iter;
+  const double al = sc->alpha, be = sc->beta, om = sc->omega;
+  const bool rr = sc->use_rr != 0;
+  const double* __restrict__ w = (it & 1) ? V.w1 : V.w0;   // w_i
+  const double* __restrict__ zn = (it & 1) ? V.z0 : V.z1;  // z_{i-1} pre-replacement
+  double* __restrict__ zw = (it & 1) ? V.z1 : V.z0;        // z_i
+  const double dinv = g.dinv;
+  const int64_t n = g.nlines * g.nx;
+  Dd acc[2] = {dd_zero(), dd_zero()};
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double c0 = w[j], c1 = zn[j];
+    const double zoc = rr ? V.zrr[j] : c1;
+    const double t0 = V.tv[j], t1 = V.vv[j];                 // t_i, v_{i-1}
+    const double kj = V.k[j], gj = V.g[j], lj = V.l[j], sj = V.s[j], rj = V.r[j];
+    const double m = dinv * c0, nn = dinv * c1;
+    const double gn = kj + be * (gj - om * lj);                // line 5
+    const double sn = c0 + be * (sj - om * zoc);               // line 6
+    const double ln = m + be * (lj - om * nn);                 // line 7
+    const double zz = t0 + be * (zoc - om * t1);               // line 8
+    const double qq = rj - al * sn;                            // line 9
+    const double yy = c0 - al * zz;                            // line 11
+    dd_fma(acc[0], qq, yy);                                    // line 12
+    dd_fma(acc[1], yy, yy);
+    V.g[j] = gn;
+    V.s[j] = sn;
+    V.l[j] = ln;
+    zw[j] = zz;
+  }
+  Dd tot[2];
+  if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
+    publish<F_SWEEPA>(sc, h, tot);
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_sweepC2(Geo g, Vecs V, Scal* __restrict__ sc,
+                                                 Dd* __restrict__ part, Hist h) {
+  if (sc->done) return;
+  const int it = sc->iter;
+  const double al = sc->alpha, om = sc->omega;
+  const double* __restrict__ w = (it & 1) ? V.w1 : V.w0;  // w_i
+  double* __restrict__ ww = (it & 1) ? V.w0 : V.w1;       // w_{i+1}
+  const double* __restrict__ z = (it & 1) ? V.z1 : V.z0;  // z_i
+  const double dinv = g.dinv;
+  const int64_t n = g.nlines * g.nx;
+  Dd acc[5] = {dd_zero(), dd_zero(), dd_zero(), dd_zero(), dd_zero()};
+  // SpMV_D may run before the finalize step advances iter (P ranks, overlap): tell it
+  // where w_{i+1} is
+  if (blockIdx.x == 0 && threadIdx.x == 0) sc->spd_par = (it + 1) & 1;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const double c0 = w[j], c1 = z[j];
+    const double t0 = V.tv[j], t1 = V.vv[j];                  // t_i, v_i
+    const double xj = V.x[j], gj = V.g[j], kj = V.k[j], lj = V.l[j], rj = V.r[j];
+    const double sj = V.s[j], rhj = V.rh[j];
+    const double m = dinv * c0, nn = dinv * c1;
+    const double uu = kj - al * lj;                             // line 10
+    const double qq = rj - al * sj;                             // line 9
+    const double yy = c0 - al * c1;                             // line 11
+    const double xn = (xj + al * gj) + om * uu;                 // line 17
+    const double rn = qq - om * yy;                             // line 18
+    const double kn = uu - om * (m - al * nn);                  // line 19
+    const double wn = yy - om * (t0 - al * t1);                 // line 20
+    dd_fma(acc[0], rhj, rn);                                    // line 21
+    dd_fma(acc[1], rhj, wn);
+    dd_fma(acc[2], rhj, sj);
+    dd_fma(acc[3], rhj, c1);
+    dd_fma(acc[4], rn, rn);
+    V.x[j] = xn;
+    V.r[j] = rn;
+    V.k[j] = kn;
+    ww[j] = wn;
+  }
+  Dd tot[5];
+  if (dd_grid_reduce<5>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0)
+    publish<F_SWEEPC>(sc, h, tot);
 }

@@ -45,7 +45,9 @@ enum TileMode { TM_A = 0, TM_C, TM_RR1, TM_RR2, TM_GAP, TM_INIT1, TM_INIT2,
                 TM_CL1, TM_CL2, TM_CL3, TM_PC, TM_PCI1, TM_PCI2,
                 // the same steps plus the vector norms of the automated-replacement
                 // bound f^r: sums of squares ride the step's reduction
-                TM_AN, TM_CN, TM_RR1N, TM_RR2N, TM_INIT1N, TM_N };
+                TM_AN, TM_CN, TM_RR1N, TM_RR2N, TM_INIT1N,
+                // split schedule (option schedule 2): the stand-alone SpMVs
+                TM_SPB, TM_SPD, TM_N };
 
 template <int M> struct BaseOf { enum { v = M }; };
 template <> struct BaseOf<TM_AN> { enum { v = TM_A }; };
@@ -87,6 +89,8 @@ template <> struct TileTraits<TM_CN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR =
 template <> struct TileTraits<TM_RR1N> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 4 }; };
 template <> struct TileTraits<TM_RR2N> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 6 }; };
 template <> struct TileTraits<TM_INIT1N> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 1, NOUT = 3, K = 4 }; };
+template <> struct TileTraits<TM_SPB> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 0 }; };
+template <> struct TileTraits<TM_SPD> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 0 }; };
 
 // sum of squares for a bound norm (plain fp64 per thread; reading A30)
 __device__ __forceinline__ void nrm_add(Dd& a, double v) { a.hi = a.hi + v * v; }
@@ -511,6 +515,8 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
     o[1 % NOUTC] = dinv * rj;                  // u0 := M^-1 r0
     dd_fma(acc[0], rj, rj);
     dd_fma(acc[1 % K], bj, bj);
+  } else if (MODE == TM_SPB || MODE == TM_SPD) {  // lines 13-14 / 22-23: v_i / t_{i+1}
+    o[0] = t0;
   } else if (MODE == TM_PCI2) {  // c = r0; t0 = A M^-1 r0 = A u0
     const double uj = dinv * c0;               // u0 (same value as stored)
     o[0] = t0;                                 // w0
@@ -545,7 +551,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   constexpr int SD = StreamDepth<MODE_>::v;  // stream ring depth; stencil barriers follow
   static_assert(K <= RED_K, "partials buffer holds RED_K pairs per CTA");
   if (MODE == TM_A || MODE == TM_C || MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3 ||
-      MODE == TM_PC) {
+      MODE == TM_PC || MODE == TM_SPB || MODE == TM_SPD) {
     if (sc->done) return;
   } else if (MODE == TM_RR1 || MODE == TM_RR2) {
     if (sc->done || !sc->rr_fire) return;
@@ -627,6 +633,12 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     svp[0] = V.x;
     stp[0] = V.b;
     outp[0] = V.r; outp[1 % NOUT] = V.k;              // r0, u0
+  } else if (MODE == TM_SPB) {  // v_i = A M^-1 z_i (z_i as sweep A wrote it)
+    svp[0] = (it & 1) ? V.z1 : V.z0;
+    outp[0] = V.vv;
+  } else if (MODE == TM_SPD) {  // t_{i+1} = A M^-1 w_{i+1} (buffer named by sweep C2)
+    svp[0] = sc->spd_par ? V.w1 : V.w0;
+    outp[0] = V.tv;
   } else if (MODE == TM_PCI2) {
     svp[0] = V.r;
     outp[0] = V.w0;
@@ -883,6 +895,8 @@ inline size_t tile_smem_bytes(const TileGeo& g, int mode) {
     case TM_RR1N: return tile_smem_bytes_t<TM_RR1N>(g);
     case TM_RR2N: return tile_smem_bytes_t<TM_RR2N>(g);
     case TM_INIT1N: return tile_smem_bytes_t<TM_INIT1N>(g);
+    case TM_SPB: return tile_smem_bytes_t<TM_SPB>(g);
+    case TM_SPD: return tile_smem_bytes_t<TM_SPD>(g);
     default: return tile_smem_bytes_t<TM_PCI2>(g);
   }
 }

@@ -173,3 +173,30 @@ def test_peer_memory_transport(B, orc, P, case):
     assert np.array_equal(out[0].rnorm, out[1].rnorm)
     assert np.array_equal(out[0].x.cpu().numpy(), out[1].x.cpu().numpy())
     assert np.array_equal(out[0].gap, out[1].gap)
+
+
+@pytest.mark.parametrize("P", [1, 2, 3])
+@pytest.mark.parametrize("overlap", [1, 0])
+def test_split_stencil_schedule(B, orc, P, overlap):
+    """option schedule=2 on a stencil: the paper's 4-phase pipeline (stand-alone
+    SpMVs the reductions hide behind) gives the fused schedule's results bitwise,
+    with periodic replacement, on 1 and P emulated ranks, overlap on and off."""
+    dim, nx, ny, nz = 3, 20, 11, 12
+    coef = problems.cfg34_coef()
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 0)
+    b = orc.spmv(A, xs)
+    ref = orc.pbicgstab(A, b, tol=1e-11, maxit=150, rr_period=6)
+    if P == 1:
+        S = B.Solver.stencil(dim, nx, ny, nz, coef)
+        S.set_option("schedule", 2)
+        b_d = S.apply(torch.from_numpy(xs).cuda())
+        res = S.solve(b_d, tol=1e-11, maxit=150, rr_period=6, gap=True)
+    else:
+        S = B.LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
+        S.set_option("schedule", 2)
+        S.set_option("overlap", overlap)
+        bs = S.apply(S.split(torch.from_numpy(xs).cuda()))
+        res = S.solve(bs, tol=1e-11, maxit=150, rr_period=6, gap=True)
+    _parity(res, ref, xs)
+    S.close()
