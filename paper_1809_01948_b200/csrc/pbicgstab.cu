@@ -107,6 +107,7 @@ struct pbicg_ctx {
   double ar_nA = 0, ar_muN = 0, ar_mutN = 0;  // bound constants (reading A29)
   bool ar_ok = false;                        // constants known for this operator
   int32_t last_iters = -1;                   // iterations of the last solve
+  int grid_a2 = 0, grid_c2 = 0;              // split stencil schedule sweeps (occupancy grids)
   // peer-memory reduction transport (option "transport" 1; state.cuh publish/k_fin)
   int p2p = 0;
   Dd* p2p_buf = nullptr;                     // own receive buffer [2][nranks][RED_K]
@@ -335,11 +336,11 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
     case PH_PCI2: { LaunchScope ls(h, K_INIT); launch_tile<DIM, TM_PCI2>(h); } break;
     case PH_SWEEPA2: {
       LaunchScope ls(h, K_SWEEPA);
-      k_sweepA2<DIM><<<h->grid[K_PREC], 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+      k_sweepA2<DIM><<<h->grid_a2, 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SWEEPC2: {
       LaunchScope ls(h, K_SWEEPC);
-      k_sweepC2<DIM><<<h->grid[K_PREC], 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+      k_sweepC2<DIM><<<h->grid_c2, 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SPB: { LaunchScope ls(h, K_SPMVB); launch_tile<DIM, TM_SPB>(h); } break;
     case PH_SPD: { LaunchScope ls(h, K_SPMVD); launch_tile<DIM, TM_SPD>(h); } break;
@@ -1394,7 +1395,8 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
     h->grid[K_GAP] = occ_grid(h, k_gap<3>, L);
     h->grid[K_APPLY] = occ_grid(h, k_apply<3>, L);
     { const int b0 = h->block; h->block = 256;
-      h->grid[K_PREC] = occ_grid(h, k_sweepC2<3>, (h->n_local + 255) / 256); h->block = b0; }
+      h->grid_a2 = occ_grid(h, k_sweepA2<3>, (h->n_local + 255) / 256);
+      h->grid_c2 = occ_grid(h, k_sweepC2<3>, (h->n_local + 255) / 256); h->block = b0; }
   } else {
     h->grid[K_INIT] = occ_grid(h, k_init1<2>, L);
     h->grid[K_SWEEPA] = occ_grid(h, k_sweepA<2>, L);
@@ -1404,7 +1406,8 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
     h->grid[K_GAP] = occ_grid(h, k_gap<2>, L);
     h->grid[K_APPLY] = occ_grid(h, k_apply<2>, L);
     { const int b0 = h->block; h->block = 256;
-      h->grid[K_PREC] = occ_grid(h, k_sweepC2<2>, (h->n_local + 255) / 256); h->block = b0; }
+      h->grid_a2 = occ_grid(h, k_sweepA2<2>, (h->n_local + 255) / 256);
+      h->grid_c2 = occ_grid(h, k_sweepC2<2>, (h->n_local + 255) / 256); h->block = b0; }
   }
   setup_tile(h);
   if (bj > 1 && !h->tile_ok)

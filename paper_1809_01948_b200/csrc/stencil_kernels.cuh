@@ -324,10 +324,11 @@ __global__ void __launch_bounds__(256) k_sweepA2(Geo g, Vecs V, Scal* __restrict
   Dd acc[2] = {dd_zero(), dd_zero()};
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
        j += (int64_t)gridDim.x * blockDim.x) {
-    const double c0 = w[j], c1 = zn[j];
-    const double zoc = rr ? V.zrr[j] : c1;
-    const double t0 = V.tv[j], t1 = V.vv[j];                 // t_i, v_{i-1}
-    const double kj = V.k[j], gj = V.g[j], lj = V.l[j], sj = V.s[j], rj = V.r[j];
+    const double c0 = __ldcs(w + j), c1 = __ldcs(zn + j);
+    const double zoc = rr ? __ldcs(V.zrr + j) : c1;
+    const double t0 = __ldcs(V.tv + j), t1 = __ldcs(V.vv + j);  // t_i, v_{i-1}
+    const double kj = __ldcs(V.k + j), gj = __ldcs(V.g + j), lj = __ldcs(V.l + j);
+    const double sj = __ldcs(V.s + j), rj = __ldcs(V.r + j);
     const double m = dinv * c0, nn = dinv * c1;
     const double gn = kj + be * (gj - om * lj);                // line 5
     const double sn = c0 + be * (sj - om * zoc);               // line 6
@@ -337,10 +338,10 @@ __global__ void __launch_bounds__(256) k_sweepA2(Geo g, Vecs V, Scal* __restrict
     const double yy = c0 - al * zz;                            // line 11
     dd_fma(acc[0], qq, yy);                                    // line 12
     dd_fma(acc[1], yy, yy);
-    V.g[j] = gn;
-    V.s[j] = sn;
-    V.l[j] = ln;
-    zw[j] = zz;
+    __stcs(V.g + j, gn);
+    __stcs(V.s + j, sn);
+    __stcs(V.l + j, ln);
+    __stcs(zw + j, zz);
   }
   Dd tot[2];
   if (dd_grid_reduce<2>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
