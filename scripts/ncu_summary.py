@@ -15,10 +15,12 @@ ALG = {  # algorithmic bytes per row: passes x 8 B
     # CSR at 27 nnz/row (ELL val 8 + col 4 per slot = 324 B/row), Jacobi
     "csr_sweepA": 120, "csr_sweepC": 136, "csr_spmvB": 340, "csr_spmvD": 340,
     "csr_init1": 372, "csr_init2": 364, "csr_apply": 340,
+    # split stencil schedule: stand-alone SpMV (2 passes), point-wise sweeps
+    "spmv": 16, "split_sweepA": 104, "split_sweepC": 120,
 }
 # t_tile<DIM, MODE, VEC>: MODE numbering of tile_sweeps.cuh TileMode
 MODES = ["sweepA", "sweepC", "rr1", "rr2", "gap", "init1", "init2", "cl1", "cl2", "cl3", "pcg",
-         "pcinit1", "pcinit2", "sweepA", "sweepC", "rr1", "rr2", "init1"]
+         "pcinit1", "pcinit2", "sweepA", "sweepC", "rr1", "rr2", "init1", "spmv", "spmv"]
 
 
 def kernel_key(name: str):
@@ -30,6 +32,10 @@ def kernel_key(name: str):
                  ("c_apply", "csr_apply")):
         if name.startswith(k):
             return v
+    if name.startswith("k_sweepA2"):
+        return "split_sweepA"
+    if name.startswith("k_sweepC2"):
+        return "split_sweepC"
     if "k_sweepA" in name:
         return "sweepA"
     if "k_sweepC" in name:
