@@ -58,6 +58,7 @@ __device__ __forceinline__ double prec_row(const CsrOp& A, int64_t j, bool in, d
 // loads of a group issued before its adds (memory-level parallelism); the
 // matrix is streamed with evict-first loads so L1/L2 keep the gathered window.
 #define ELL_U 9
+#define WIN_U 27
 template <bool PREC>
 __device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restrict__ v, int64_t j) {
   const int len = A.len ? A.len[j] : A.width;
@@ -464,6 +465,19 @@ __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __re
       const int len = A.len ? A.len[j] : A.width;
       double acc = 0.0;
       int p = 0;
+      // groups of WIN_U slots: all of a group's matrix loads in flight before its adds
+      // (27 = the cfg5 row length: one group, +4.5% over groups of 9 -- measured)
+      for (; p + WIN_U <= len; p += WIN_U) {
+        int c[WIN_U];
+        double a[WIN_U];
+#pragma unroll
+        for (int k = 0; k < WIN_U; ++k) {
+          c[k] = __ldcs(A.col + (int64_t)(p + k) * A.n + j);
+          a[k] = __ldcs(A.val + (int64_t)(p + k) * A.n + j);
+        }
+#pragma unroll
+        for (int k = 0; k < WIN_U; ++k) acc = acc + a[k] * ring[(c[k] + w.off) & (WRS - 1)];
+      }
       for (; p + ELL_U <= len; p += ELL_U) {
         int c[ELL_U];
         double a[ELL_U];
