@@ -158,16 +158,22 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *   "graphs"     1 (default) => replay chunks of iterations as CUDA graphs
  *   "timing"     1 => record CUDA events around every kernel (disables graphs);
  *                read with pbicgstab_kernel_time
- *   "overlap"    1 (default) => multi-GPU: reductions overlap the SpMV (split
- *                schedule); 0 => blocking
+ *   "overlap"    1 (default) => multi-GPU: each global reduction runs on a side
+ *                stream behind the halo exchange / SpMV the next phase needs;
+ *                0 => blocking on the compute stream
  *   "tile"       1 (default) => stencil sweeps use the TMA-staged 2.5D kernels when
- *                the grid fits (nx <= 2048); 0 => plain line kernels (same results)
- *   "schedule"   0 (default) auto, 1 fused 2-sweep (stencil only), 2 split 4-phase
+ *                nx <= 1024; 0 => plain line kernels (same results; not with block
+ *                Jacobi)
+ *   "schedule"   0 (default) auto (stencil: fused, CSR: split); 1 fused 2-sweep
+ *                (stencil only: t, v recomputed inside the sweeps, 24 passes); 2 split
+ *                4-phase (the paper's pipeline: stored t, v, stand-alone SpMVs the
+ *                reductions hide behind, 32 passes; stencil: Jacobi, method 0,
+ *                rr_auto off)
  *   "method"     0 (default) p-BiCGStab, Alg. 2; 1 classic preconditioned
  *                BiCGStab, Alg. 1; 2 preconditioned pipelined CG (the
  *                paper's p-CG comparison, reconstructed: DESIGN.md A19).
- *                Methods 1 and 2 need a stencil operator with nx <= 1024 and
- *                rr_period = 0 (EINVAL otherwise)
+ *                Methods 1 and 2 need rr_period = 0; on a stencil also nx <= 1024 and
+ *                the Jacobi preconditioner (EINVAL otherwise)
  *   "transport"  multi-rank reductions: 0 (default) NCCL all-reduce of the zero-padded
  *                rank rows (loopback: device copies); 1 peer memory -- the last CTA of
  *                each reducing kernel stores its rank's Dot2 pairs into every rank's
@@ -217,7 +223,8 @@ pbicg_status pbicgstab_solve_host(pbicg_handle h, const double* b_host, const do
 
 /* Per-kernel statistics since the last reset (reset = 1 clears them).
  *   name: "init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap",
- *   "apply", "fin" (multi-rank scalar finalisation), or "all".
+ *   "apply", "fin" (multi-rank scalar finalisation), "cl1", "cl2", "cl3" (classic
+ *   BiCGStab), "pcg" (p-CG), "prec" (stand-alone M^-1), or "all".
  *   launches: kernel launches issued (graph nodes count once per replay);
  *   ms: summed CUDA-event time (only with option "timing"; else NaN). */
 pbicg_status pbicgstab_kernel_time(pbicg_handle h, const char* name, int64_t* launches,
