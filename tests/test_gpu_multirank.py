@@ -41,11 +41,12 @@ def _parity(res, ref, xs, bitwise=True):
 
 @pytest.mark.parametrize("P", [2, 3, 4])
 @pytest.mark.parametrize("dim,nx,ny,nz", [(3, 24, 20, 17), (2, 64, 37, 1), (3, 13, 7, 9)])
-@pytest.mark.parametrize("tile", [1, 0])
-def test_loopback_stencil_matches_oracle(B, orc, P, dim, nx, ny, nz, tile):
+@pytest.mark.parametrize("tile,overlap", [(1, 1), (0, 1), (1, 0)])
+def test_loopback_stencil_matches_oracle(B, orc, P, dim, nx, ny, nz, tile, overlap):
     coef = problems.cfg34_coef() if dim == 3 else problems.cfg2_coef()
     G = B.LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
     G.set_option("tile", tile)
+    G.set_option("overlap", overlap)  # reductions behind the halo exchange, or blocking
     A = orc.stencil_csr(dim, nx, ny, nz, coef)
     xs = problems.x_star(A.n, 0)
     b = orc.spmv(A, xs)

@@ -124,6 +124,15 @@ def test_cfg1_qualitative_paper_claims(orc):
     assert err(prr) < 1e-2 * err(p)
 
 
+def test_replacement_can_delay_convergence(orc):
+    """explicitly recomputed vectors are not orthogonal to the Krylov
+    basis built so far, so frequent replacement delays convergence."""
+    A, xs, b = _stencil(orc, 2, 128, 128, 1, problems.cfg2_coef())
+    its = {rr: orc.pbicgstab(A, b, tol=1e-10, maxit=5000, rr_period=rr, gap=False).iters
+           for rr in (0, 50, 20)}
+    assert its[0] < its[50] < its[20]
+
+
 def test_identity_system_one_iteration(orc):
     """A = I: r1 = 0 after one iteration (y0 = 0 => omega := 0 guard, A9)."""
     n = 10
