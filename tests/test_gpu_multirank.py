@@ -117,8 +117,8 @@ def test_partition_is_balanced_slabs(B):
 
 
 @pytest.mark.parametrize("P", [2, 3, 4])
-@pytest.mark.parametrize("case", ["stencil", "stencil_auto", "stencil_bj", "classic", "pipecg",
-                                  "csr", "csr_pipecg"])
+@pytest.mark.parametrize("case", ["stencil", "stencil_auto", "stencil_bj", "stencil_split",
+                                  "classic", "pipecg", "csr", "csr_pipecg"])
 def test_peer_memory_transport(B, orc, P, case):
     """option transport=1: the producing kernels store their rank's Dot2 pairs into
     every rank's receive buffer and the finalize kernels wait on per-rank flags
@@ -156,6 +156,8 @@ def test_peer_memory_transport(B, orc, P, case):
         G.set_option("rr_auto", int(auto))
         G.set_option("bench", 1)
         G.set_option("transport", transport)
+        if case == "stencil_split":
+            G.set_option("schedule", 2)
         bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
         for rep in range(2):  # the epoch counter carries over between solves
             res = G.solve(bs, tol=0.0, maxit=60, rr_period=rr, gap=True)
