@@ -25,7 +25,8 @@ NVCC_FLAGS = [
 # translation units: the host driver (+ Jacobi kernels) and the block-Jacobi tile
 # instances, one object per block size, compiled in parallel and linked into one .so
 UNITS = [("pbicgstab.cu", []), ("tile_bj.cu", ["-DPBICG_BJ_B=2"]),
-         ("tile_bj.cu", ["-DPBICG_BJ_B=4"]), ("tile_bj.cu", ["-DPBICG_BJ_B=8"])]
+         ("tile_bj.cu", ["-DPBICG_BJ_B=4"]), ("tile_bj.cu", ["-DPBICG_BJ_B=8"]),
+         ("tile_seg.cu", [])]
 
 
 def sources() -> list[str]:

@@ -27,6 +27,7 @@
 #include "nccl_dyn.h"
 #include "stencil_kernels.cuh"
 #include "tile_bj.h"
+#include "tile_seg.h"
 #include "tile_sweeps.cuh"
 
 namespace {
@@ -76,6 +77,7 @@ struct pbicg_ctx {
   TileGeo tg{};
   bool tile_ok = false;  // TMA 2.5D sweeps eligible for this operator
   bool tile_vec = false; // ... with 16-byte aligned pairs (nx even)
+  bool tile_seg = false; // ... as x-segmented tiles (nx > 1024; instances in tile_seg.cu)
   int tile_on = 1;       // option "tile"
   size_t tile_smem[TM_N] = {0};
   int tile_occ[TM_N] = {0};  // resident CTAs per SM of each tile kernel
@@ -263,6 +265,11 @@ void launch_tile(pbicg_ctx* h) {
   const int per_sm = h->tile_occ[MODE] > 0 ? h->tile_occ[MODE] : 1;
   const int cap = h->num_sm * per_sm;
   const int grid = h->tg.units < cap ? h->tg.units : cap;
+  if (h->tile_seg) {  // x-segmented instances live in tile_seg.cu
+    tile_seg_launch(DIM, MODE, grid, h->tile_smem[MODE], h->stream, h->tg, h->V, h->scal,
+                    h->part, h->hist);
+    return;
+  }
   if constexpr (bj_mode(MODE)) {  // block Jacobi instances live in tile_bj.cu
     const size_t sm = h->tile_smem[MODE];
     switch (h->tg.bj) {
@@ -941,6 +948,12 @@ pbicg_status ensure_hist(pbicg_ctx* h, int64_t need) {
 template <int DIM, int MODE>
 cudaError_t set_tile_attr(pbicg_ctx* h) {
   const cudaFuncAttribute A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  if (h->tile_seg) {
+    int occ = 1;
+    const cudaError_t e = tile_seg_attr(DIM, MODE, (int)h->tile_smem[MODE], &occ);
+    h->tile_occ[MODE] = occ < 1 ? 1 : occ;
+    return e;
+  }
   cudaError_t e = cudaFuncSetAttribute(t_tile<DIM, MODE, true>, A, (int)h->tile_smem[MODE]);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(t_tile<DIM, MODE, false>, A, (int)h->tile_smem[MODE]);
@@ -993,41 +1006,75 @@ void setup_tile(pbicg_ctx* h) {
   const Geo& g = h->geo;
   TileGeo& t = h->tg;
   h->tile_ok = false;
+  h->tile_seg = false;
   const int dim = h->dim;
   const int64_t tpmax = 2LL * TNT;  // one row pair per thread
-  if (g.nx > tpmax) return;
-  h->tile_vec = (g.nx % 2) == 0;  // then every staged range / vector is 16-byte aligned
-  const int64_t lines = dim == 3 ? g.ny : 1;
-  int64_t TY = dim == 3 ? (tpmax / g.nx) : 1;
-  if (TY < 1) TY = 1;
-  if (TY > lines) TY = lines;
-  if (const char* e = getenv("PBICG_TILE_TY")) {  // tuning experiments only
-    const long v = strtol(e, nullptr, 10);
-    if (v >= 1 && v < TY) TY = v;
-  }
   int max_smem = 0;
   cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
   const size_t reserve = 8192;  // static shared memory of the block reductions (K <= 16 pairs)
-  for (; TY >= 1; --TY) {
-    t.nx = g.nx;
-    t.ny = lines;
-    t.nol = g.nol;
-    t.o0 = g.o0;
-    t.nog = g.nog;
-    t.pxy = g.pxy;
-    t.TY = (int32_t)TY;
-    t.halo = (int32_t)(dim == 3 ? g.nx + 2 : 2);
-    const int64_t TP = TY * g.nx;
-    t.st_stride = (int32_t)((TP + 2 + 1) & ~1LL);
-    t.sv_stride = (int32_t)((TP + 2 * t.halo + 2 + 1) & ~1LL);
-    size_t worst = 0;
-    for (int m = 0; m < TM_N; ++m) worst = tile_smem_bytes(t, m) > worst ? tile_smem_bytes(t, m) : worst;
-    if (worst + reserve <= (size_t)max_smem) break;
+  const int64_t lines = dim == 3 ? g.ny : 1;
+  t.nx = g.nx;
+  t.ny = lines;
+  t.nol = g.nol;
+  t.o0 = g.o0;
+  t.nog = g.nog;
+  t.pxy = g.pxy;
+  t.sx = (int32_t)g.nx;
+  t.nseg = 1;
+  t.lstride = (int32_t)g.nx;
+  int64_t nseg = 1;
+  if (g.nx > tpmax) {
+    // x-segmented tiles (tile_seg.cu): TY lines x sx columns, sx the widest multiple of
+    // 16 (<= 512) whose worst-mode shared memory fits; odd nx keeps the line kernels
+    if (g.nx % 2 != 0) return;
+    const int64_t TYs = dim == 3 ? (lines < 2 ? lines : 2) : 1;
+    int64_t SX = 512;
+    for (; SX >= 64; SX -= 16) {
+      t.TY = (int32_t)TYs;
+      t.sx = (int32_t)SX;
+      t.lstride = (int32_t)(SX + 2 * SEG_HX);
+      t.halo = 0;
+      t.st_stride = (int32_t)(TYs * SX);
+      t.sv_stride = (int32_t)((dim == 3 ? TYs + 2 : 1) * t.lstride + 2);
+      size_t worst = 0;
+      for (int m = 0; m < TM_N; ++m)
+        worst = tile_smem_bytes(t, m) > worst ? tile_smem_bytes(t, m) : worst;
+      if (worst + reserve <= (size_t)max_smem) break;
+    }
+    if (SX < 64) return;
+    nseg = (g.nx + SX - 1) / SX;
+    t.nseg = (int32_t)nseg;
+    h->tile_seg = true;
+    h->tile_vec = true;
+    for (int i = 0; i < 7; ++i) t.c[i] = g.c[i];
+    t.dinv = g.dinv;
+    t.ncols = (int32_t)(((lines + TYs - 1) / TYs) * nseg);
   }
-  if (TY < 1) return;
-  for (int i = 0; i < 7; ++i) t.c[i] = g.c[i];
-  t.dinv = g.dinv;
-  t.ncols = (int32_t)((lines + TY - 1) / TY);
+  if (!h->tile_seg) {  // full-line tiles: TY lines of nx
+    int64_t TY = dim == 3 ? (tpmax / g.nx) : 1;
+    if (TY < 1) TY = 1;
+    if (TY > lines) TY = lines;
+    if (const char* e = getenv("PBICG_TILE_TY")) {  // tuning experiments only
+      const long v = strtol(e, nullptr, 10);
+      if (v >= 1 && v < TY) TY = v;
+    }
+    h->tile_vec = (g.nx % 2) == 0;  // 16-byte aligned pairs / ranges
+    for (; TY >= 1; --TY) {
+      t.TY = (int32_t)TY;
+      t.halo = (int32_t)(dim == 3 ? g.nx + 2 : 2);
+      const int64_t TP = TY * g.nx;
+      t.st_stride = (int32_t)((TP + 2 + 1) & ~1LL);
+      t.sv_stride = (int32_t)((TP + 2 * t.halo + 2 + 1) & ~1LL);
+      size_t worst = 0;
+      for (int m = 0; m < TM_N; ++m)
+        worst = tile_smem_bytes(t, m) > worst ? tile_smem_bytes(t, m) : worst;
+      if (worst + reserve <= (size_t)max_smem) break;
+    }
+    if (TY < 1) return;
+    for (int i = 0; i < 7; ++i) t.c[i] = g.c[i];
+    t.dinv = g.dinv;
+    t.ncols = (int32_t)((lines + TY - 1) / TY);
+  }
   // chunk count: minimise rounds * (chunk + 2 prologue planes) per CTA
   const int grid = h->num_sm;
   int64_t best_n = 1;
@@ -1380,7 +1427,9 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
   h->n_global = op->nx * op->ny * nz;
   h->n_local = g.pxy * g.nol;
   h->row_begin = g.o0 * g.pxy;
-  h->H = g.pxy + g.nx + 4;  // ghost plane + staging slack of the tile kernels
+  // ghost plane + staging slack of the tile kernels (segmented tiles stage line y-1,
+  // column x-SEG_HX of plane -1: pxy + nx + 8 before, pxy + nx + 6 after)
+  h->H = g.pxy + g.nx + 2 * SEG_HX;
   h->halo_n = g.pxy;
   h->block = 256;
   if (g.nx < 256) h->block = (int)(((g.nx + 31) / 32) * 32);

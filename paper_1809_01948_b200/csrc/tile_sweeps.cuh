@@ -107,7 +107,29 @@ struct TileGeo {
   double dinv;
   int32_t bj;         // preconditioner: 1 Jacobi; 2, 4, 8 block Jacobi along x (reading A33)
   double bi[64];      // bj > 1: the (common) bj x bj inverse block, row-major
+  // x-segmented tiles (grids with nx > 1024, nx even): a tile is TY lines x sx columns
+  int32_t sx;         // segment width (even); == nx when lines are not segmented
+  int32_t nseg;       // segments per line
+  int32_t lstride;    // shared-memory stride of a staged stencil line segment (sx + 16)
 };
+
+// halo columns staged on each side of a segment (>= 2 for the x legs; 8 keeps every
+// staged line 16-byte aligned for any even x0)
+#define SEG_HX 8
+
+// stage `n` vectors' line segments: nl lines of len doubles starting at element e0
+// (line stride nx in global memory, ls in shared memory); every range is 16-byte
+// aligned by construction (nx, e0, len even)
+__device__ __forceinline__ void stage_lines(double* dst, int stride, const double* const* src,
+                                            int n, int64_t e0, int64_t nx, int nl, int len,
+                                            int ls, uint64_t* bar) {
+  const uint32_t bytes = (uint32_t)len * 8u;
+  mbar_arrive_expect_tx(bar, bytes * (uint32_t)(n * nl));
+  for (int v = 0; v < n; ++v)
+    for (int l = 0; l < nl; ++l)
+      bulk_g2s(dst + (size_t)v * stride + (size_t)l * ls, src[v] + e0 + (int64_t)l * nx, bytes,
+               bar);
+}
 
 __device__ __forceinline__ int align_off(const double* p) {
   return (int)(((uintptr_t)p & 15u) >> 3);
@@ -528,7 +550,8 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
 // Generic tile kernel.  VEC: every staged range and every vector is 16-byte
 // aligned (nx even) -> paired loads and stores.  One row pair per thread:
 // TP <= 2 * TNT.
-template <int DIM, int MODE_, bool VEC, int BJ = 0>  // BJ: block-Jacobi block size (0 Jacobi)
+// BJ: block-Jacobi block size (0 Jacobi); SEG: x-segmented tiles (nx > 1024)
+template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false>
 __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
                                                  Dd* __restrict__ part, Hist h) {
   using T = TileTraits<MODE_>;
@@ -665,9 +688,16 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
 
   for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
     const int col = u % g.ncols, q = u / g.ncols;
-    const int64_t y0 = (int64_t)col * g.TY;
+    // SEG: col = ycol * nseg + segment; x0s/sxc = the segment's first column / width
+    const int ycol = SEG ? col / g.nseg : col;
+    const int x0s = SEG ? (col % g.nseg) * g.sx : 0;
+    const int sxc = SEG ? (nx - x0s < g.sx ? nx - x0s : g.sx) : nx;
+    const int64_t y0 = (int64_t)ycol * g.TY;
     const int tyc = (int)((g.ny - y0) < g.TY ? (g.ny - y0) : g.TY);
-    const int TP = tyc * nx;
+    const int TP = tyc * sxc;
+    const int ly = r / sxc, cx = r % sxc;         // this row pair's line / column in the tile
+    const int ls = SEG ? g.lstride : nx;          // y stride of the staged stencil planes
+    const int nlines = DIM == 3 ? tyc + 2 : 1;    // SEG: staged lines per stencil plane
     const int64_t z0 = (int64_t)q * g.chunk;
     const int64_t z1 = (z0 + g.chunk) < g.nol ? (z0 + g.chunk) : g.nol;
     const int nst = (int)(z1 - z0), nsv = nst + 2;
@@ -676,8 +706,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     const bool act = r < TP, valid1 = r + 1 < TP;
     unsigned b0 = 0, b1 = 0;
     {
-      const int x0 = r % nx, x1 = (r + 1) % nx;
-      const int64_t gy0 = y0 + r / nx, gy1 = y0 + (r + 1) / nx;
+      const int x0 = SEG ? x0s + cx : r % nx, x1 = SEG ? x0s + cx + 1 : (r + 1) % nx;
+      const int64_t gy0 = SEG ? y0 + ly : y0 + r / nx, gy1 = SEG ? y0 + ly : y0 + (r + 1) / nx;
       if (x0 > 0) b0 |= 4u;
       if (x0 < nx - 1) b0 |= 8u;
       if (x1 > 0) b1 |= 4u;
@@ -690,32 +720,47 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       }
     }
     const unsigned amask = __ballot_sync(0xffffffffu, act);  // blocks are all-in or all-out
-    const int i0 = BJ > 0 ? (r % nx) % BB : 0;                // row r's position in its block
+    const int i0 = BJ > 0 ? ((SEG ? x0s + cx : r % nx) % BB) : 0;  // position in its block
     const unsigned xy_all = DIM == 3 ? 30u : 12u;
     const bool xy_int = __all_sync(0xffffffffu, !act || ((b0 & xy_all) == xy_all &&
                                                          (b1 & xy_all) == xy_all));
     double m1[NSO][2];  // plane z-1 centre values per stencil operand
 #pragma unroll
     for (int v = 0; v < NSO; ++v) m1[v][0] = m1[v][1] = 0.0;
-    if (tid == 0) {
-      for (int m = 0; m < 3 && m < nsv; ++m) {
-        const int s = (svc + m) % 3;
-        stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, (z0 - 1 + m) * g.pxy + toff - g.halo,
+    // SEG: element index of (line y0 - 1 (3D) / the line (2D), column x0s - SEG_HX)
+    const int64_t sv_e0 = SEG ? (DIM == 3 ? (y0 - 1) * g.nx : 0) + x0s - SEG_HX : 0;
+    const int64_t st_e0 = SEG ? (DIM == 3 ? y0 * g.nx : 0) + x0s : 0;
+    auto stage_sv = [&](int s, int64_t zp) {  // stencil plane zp into ring slot s
+      if (SEG)
+        stage_lines(sv + (size_t)s * NSV * svs, svs, svp, NSV, zp * g.pxy + sv_e0, g.nx, nlines,
+                    sxc + 2 * SEG_HX, ls, &bar[SD + s]);
+      else
+        stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, zp * g.pxy + toff - g.halo,
               TP + 2 * g.halo, &bar[SD + s]);
-      }
+    };
+    auto stage_st = [&](int s, int64_t zp) {  // streamed vectors of plane zp into slot s
+      if (SEG)
+        stage_lines(st + (size_t)s * NST * sts, sts, stp, nstr, zp * g.pxy + st_e0, g.nx, tyc,
+                    sxc, g.sx, &bar[s]);
+      else
+        stage(st + (size_t)s * NST * sts, sts, stp, nstr, zp * g.pxy + toff, TP, &bar[s]);
+    };
+    // this row pair's offset in a stencil slot / a stream slot
+    auto sv_off = [&](int64_t zp) -> int {
+      return SEG ? (ly + (DIM == 3 ? 1 : 0)) * ls + SEG_HX + cx
+                 : align_off(svp[0] + zp * g.pxy + toff - g.halo) + g.halo + r;
+    };
+    if (tid == 0) {
+      for (int m = 0; m < 3 && m < nsv; ++m) stage_sv((svc + m) % 3, z0 - 1 + m);
       if (HAS_STR) {
-        for (int m = 0; m < SD - 1 && m < nst; ++m) {  // planes z0 .. z0+SD-2
-          const int s = (stc + m) % SD;
-          stage(st + (size_t)s * NST * sts, sts, stp, nstr, (z0 + m) * g.pxy + toff, TP, &bar[s]);
-        }
+        for (int m = 0; m < SD - 1 && m < nst; ++m) stage_st((stc + m) % SD, z0 + m);
       }
     }
     {  // plane z0-1 -> registers
       const int s = svc % 3;
       mbar_wait(&bar[SD + s], (ph >> (SD + s)) & 1u);
       ph ^= 1u << (SD + s);
-      const double* b0p = sv + (size_t)s * NSV * svs +
-                          align_off(svp[0] + (z0 - 1) * g.pxy + toff - g.halo) + g.halo + r;
+      const double* b0p = sv + (size_t)s * NSV * svs + sv_off(z0 - 1);
       if (act) {
         if (DER) {
           derive_pair<VEC, NSV, MODE>(b0p, svs, al, be, om, m1[0][0], m1[0][1]);
@@ -736,16 +781,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       const int64_t z = z0 + n;
       __syncthreads();  // step n-1 done: its plane-(z-1) slot and stream slot are free
       if (tid == 0) {
-        if (n + 3 < nsv) {  // plane z+2
-          const int s = (svc + n + 3) % 3;
-          stage(sv + (size_t)s * NSV * svs, svs, svp, NSV, (z + 2) * g.pxy + toff - g.halo,
-                TP + 2 * g.halo, &bar[SD + s]);
-        }
-        if (HAS_STR && n + SD - 1 < nst) {  // streams z+SD-1 into the slot step n-1 freed
-          const int s = (stc + n + SD - 1) % SD;
-          stage(st + (size_t)s * NST * sts, sts, stp, nstr, (z + SD - 1) * g.pxy + toff, TP,
-                &bar[s]);
-        }
+        if (n + 3 < nsv) stage_sv((svc + n + 3) % 3, z + 2);  // plane z+2
+        if (HAS_STR && n + SD - 1 < nst)  // streams z+SD-1 into the slot step n-1 freed
+          stage_st((stc + n + SD - 1) % SD, z + SD - 1);
       }
       const int s_z = (svc + n + 1) % 3, s_z1 = (svc + n + 2) % 3, s_st = (stc + n) % SD;
       mbar_wait(&bar[SD + s_z1], (ph >> (SD + s_z1)) & 1u);
@@ -755,13 +793,12 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         ph ^= 1u << s_st;
       }
       if (!act) continue;
-      const int oz = align_off(svp[0] + z * g.pxy + toff - g.halo) + g.halo;
-      const int oz1 = align_off(svp[0] + (z + 1) * g.pxy + toff - g.halo) + g.halo;
-      const double* Wz = sv + (size_t)s_z * NSV * svs + oz + r;
-      const double* Wz1 = sv + (size_t)s_z1 * NSV * svs + oz1 + r;
-      const double* S0 = HAS_STR ? st + (size_t)s_st * NST * sts +
-                                       align_off(stp[0] + z * g.pxy + toff) + r
-                                 : nullptr;
+      const double* Wz = sv + (size_t)s_z * NSV * svs + sv_off(z);
+      const double* Wz1 = sv + (size_t)s_z1 * NSV * svs + sv_off(z + 1);
+      const double* S0 = !HAS_STR ? nullptr
+                         : SEG    ? st + (size_t)s_st * NST * sts + ly * g.sx + cx
+                                  : st + (size_t)s_st * NST * sts +
+                                        align_off(stp[0] + z * g.pxy + toff) + r;
       const bool zin = (g.o0 + z) > 0 && (g.o0 + z) < g.nog - 1;
       const unsigned zb = ((g.o0 + z) > 0 ? 1u : 0u) | ((g.o0 + z) < g.nog - 1 ? 32u : 0u);
       double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -770,35 +807,35 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         if (xy_int && zin) {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair_bj<DIM, VEC, true, BB>(g, s_bi, nx, i0, Wz + v * svs, Wz1 + v * svs,
+            stencil_pair_bj<DIM, VEC, true, BB>(g, s_bi, ls, i0, Wz + v * svs, Wz1 + v * svs,
                                                 m1[v][0], m1[v][1], 0u, 0u, c[v][0], c[v][1],
                                                 pc[v][0], pc[v][1], t[v][0], t[v][1]);
         } else {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair_bj<DIM, VEC, false, BB>(g, s_bi, nx, i0, Wz + v * svs, Wz1 + v * svs,
+            stencil_pair_bj<DIM, VEC, false, BB>(g, s_bi, ls, i0, Wz + v * svs, Wz1 + v * svs,
                                                  m1[v][0], m1[v][1], b0 | zb, b1 | zb, c[v][0],
                                                  c[v][1], pc[v][0], pc[v][1], t[v][0], t[v][1]);
         }
       } else if (DER) {
         if (xy_int && zin)
-          stencil_pair_der<DIM, VEC, true, PREC, NSV, MODE>(g, nx, Wz, svs, Wz1, m1[0][0],
+          stencil_pair_der<DIM, VEC, true, PREC, NSV, MODE>(g, ls, Wz, svs, Wz1, m1[0][0],
                                                             m1[0][1], 0u, 0u, al, be, om, c[0][0],
                                                             c[0][1], t[0][0], t[0][1]);
         else
-          stencil_pair_der<DIM, VEC, false, PREC, NSV, MODE>(g, nx, Wz, svs, Wz1, m1[0][0],
+          stencil_pair_der<DIM, VEC, false, PREC, NSV, MODE>(g, ls, Wz, svs, Wz1, m1[0][0],
                                                              m1[0][1], b0 | zb, b1 | zb, al, be,
                                                              om, c[0][0], c[0][1], t[0][0],
                                                              t[0][1]);
       } else if (xy_int && zin) {
 #pragma unroll
         for (int v = 0; v < NSO; ++v)
-          stencil_pair<DIM, VEC, true, PREC>(g, nx, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+          stencil_pair<DIM, VEC, true, PREC>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
                                              m1[v][1], 0u, 0u, c[v][0], c[v][1], t[v][0], t[v][1]);
       } else {
 #pragma unroll
         for (int v = 0; v < NSO; ++v)
-          stencil_pair<DIM, VEC, false, PREC>(g, nx, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+          stencil_pair<DIM, VEC, false, PREC>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
                                               m1[v][1], b0 | zb, b1 | zb, c[v][0], c[v][1],
                                               t[v][0], t[v][1]);
       }
@@ -810,7 +847,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       double o0[NOUT], o1[NOUT];
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) o0[k] = o1[k] = 0.0;
-      const int64_t gi = z * g.pxy + toff + r;
+      const int64_t gi = SEG ? z * g.pxy + (DIM == 3 ? (y0 + ly) * g.nx : 0) + x0s + cx
+                             : z * g.pxy + toff + r;
       row_update<MODE, K, NOUT, NRM, (BJ > 0)>(S0, sts, rr, V.zrr + gi, pc[0][0], pc[1 % NSO][0],
                                          c[0][0], c[1][0], t[0][0], t[1][0], al, be, om, g.dinv,
                                          acc, o0);

@@ -118,7 +118,7 @@ def test_auto_rr_errors(S, orc):
     solver.set_option("method", 1)
     with pytest.raises(PbicgError):
         solver.set_option("rr_auto", 1)
-    wide = S.stencil(2, 1500, 4, 1, problems.cfg2_coef())  # line kernels: no bound norms
+    wide = S.stencil(2, 1501, 4, 1, problems.cfg2_coef())  # odd nx > 1024: line kernels
     with pytest.raises(PbicgError):
         wide.set_option("rr_auto", 1)
 

@@ -113,3 +113,32 @@ def test_fuzz_csr(orc, seed):
     check_parity(res, ref, xs, bitwise=False)
     bitwise_above_floor(res, ref)
     S.close()
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_fuzz_wide_grids(orc, seed):
+    """nx > 1024 (x-segmented tiles for even nx, line kernels for odd nx), random
+    solver / replacement options, bitwise above the noise floor."""
+    from paper_1809_01948_b200 import Solver
+    rng = np.random.default_rng(3000 + seed)
+    dim = int(rng.choice([2, 3]))
+    nx = int(rng.integers(1025, 2400))
+    ny = int(rng.integers(1, 12))
+    nz = int(rng.integers(1, 6)) if dim == 3 else 1
+    method = int(rng.choice([0, 0, 1])) if nx % 2 == 0 else 0
+    coef = rand_coef(rng, dim, spd=False)
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, seed)
+    b = orc.spmv(A, xs)
+    S = Solver.stencil(dim, nx, ny, nz, coef)
+    S.set_option("method", method)
+    rr = int(rng.choice([0, 3, 6])) if method == 0 else 0
+    b_d = S.apply(torch.from_numpy(xs).cuda())
+    assert np.array_equal(b_d.cpu().numpy(), b)
+    res = S.solve(b_d, tol=1e-11, maxit=60, rr_period=rr, gap=True)
+    ref = (orc.pbicgstab(A, b, tol=1e-11, maxit=60, rr_period=rr) if method == 0
+           else orc.bicgstab(A, b, tol=1e-11, maxit=60))
+    assert res.outcome == ref.outcome
+    check_parity(res, ref, xs, bitwise=False)
+    bitwise_above_floor(res, ref)
+    S.close()

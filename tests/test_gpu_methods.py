@@ -137,7 +137,7 @@ def test_degenerate_and_errors(S, orc):
         assert np.array_equal(r.rnorm, ref.rnorm)
         assert np.array_equal(r.x.cpu().numpy(), ref.x)
     # stencils with nx > 1024 reject methods 1/2 (tile kernels only)
-    wide = S.stencil(2, 1500, 4, 1, problems.cfg2_coef())
+    wide = S.stencil(2, 1501, 4, 1, problems.cfg2_coef())  # odd nx > 1024: line kernels only
     with pytest.raises(PbicgError):
         wide.set_option("method", 2)
 

@@ -224,3 +224,30 @@ def test_csr_wide_band_uses_gather_path(S, orc):
     res = solver.solve(b_d, tol=1e-12, maxit=100, rr_period=4)
     ref = orc.pbicgstab(A, b, tol=1e-12, maxit=100, rr_period=4)
     check_parity(res, ref, xs)
+
+
+@pytest.mark.parametrize("dim,nx,ny,nz,kind", [
+    (2, 1500, 40, 1, "cd2"), (2, 4096, 24, 1, "poisson"), (2, 2050, 9, 1, "cd2"),
+    (3, 1100, 5, 6, "cd3"), (3, 2048, 3, 4, "cd3"), (3, 1026, 1, 5, "cd3")])
+def test_segmented_tiles(S, orc, dim, nx, ny, nz, kind):
+    """nx > 1024 (even): x-segmented TMA tiles (line segments with halo columns,
+    ragged last segment); every solver and automated replacement, bitwise."""
+    solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of(kind))
+    res = solver.solve(b_d, tol=1e-11, maxit=120, rr_period=7, gap=True)
+    ref = orc.pbicgstab(A, b, tol=1e-11, maxit=120, rr_period=7)
+    check_parity(res, ref, xs)
+    solver.set_option("bench", 1)
+    solver.set_option("rr_auto", 1)
+    res = solver.solve(b_d, tol=0.0, maxit=40, gap=True)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=40, bench=True, auto_rr=True)
+    check_parity(res, ref, xs, bitwise=False)
+    assert np.array_equal(res.rnorm, ref.rnorm)
+    solver.set_option("rr_auto", 0)
+    solver.set_option("bench", 0)
+    solver.set_option("method", 1)
+    res = solver.solve(b_d, tol=1e-11, maxit=120, gap=True)
+    check_parity(res, orc.bicgstab(A, b, tol=1e-11, maxit=120), xs)
+    solver.set_option("method", 0)
+    solver.set_option("schedule", 2)
+    res = solver.solve(b_d, tol=1e-11, maxit=120, rr_period=7, gap=True)
+    check_parity(res, orc.pbicgstab(A, b, tol=1e-11, maxit=120, rr_period=7), xs)
