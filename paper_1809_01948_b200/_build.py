@@ -26,7 +26,8 @@ NVCC_FLAGS = [
 # instances, one object per block size, compiled in parallel and linked into one .so
 UNITS = [("pbicgstab.cu", []), ("tile_bj.cu", ["-DPBICG_BJ_B=2"]),
          ("tile_bj.cu", ["-DPBICG_BJ_B=4"]), ("tile_bj.cu", ["-DPBICG_BJ_B=8"]),
-         ("tile_seg.cu", [])]
+         ("tile_seg.cu", []), ("tile_jac.cu", ["-DPBICG_VEC=1"]),
+         ("tile_jac.cu", ["-DPBICG_VEC=0"])]
 
 
 def sources() -> list[str]:

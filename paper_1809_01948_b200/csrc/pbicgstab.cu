@@ -27,6 +27,7 @@
 #include "nccl_dyn.h"
 #include "stencil_kernels.cuh"
 #include "tile_bj.h"
+#include "tile_jac.h"
 #include "tile_seg.h"
 #include "tile_sweeps.cuh"
 
@@ -279,12 +280,13 @@ void launch_tile(pbicg_ctx* h) {
       default: break;
     }
   }
+  // Jacobi instances live in tile_jac.cu (one object per pairing mode)
   if (h->tile_vec)
-    t_tile<DIM, MODE, true><<<grid, TNT, h->tile_smem[MODE], h->stream>>>(h->tg, h->V, h->scal,
-                                                                          h->part, h->hist);
+    tile_jac_launch_1(DIM, MODE, grid, h->tile_smem[MODE], h->stream, h->tg, h->V, h->scal,
+                      h->part, h->hist);
   else
-    t_tile<DIM, MODE, false><<<grid, TNT, h->tile_smem[MODE], h->stream>>>(h->tg, h->V, h->scal,
-                                                                           h->part, h->hist);
+    tile_jac_launch_0(DIM, MODE, grid, h->tile_smem[MODE], h->stream, h->tg, h->V, h->scal,
+                      h->part, h->hist);
 }
 
 template <int DIM>
@@ -954,14 +956,11 @@ cudaError_t set_tile_attr(pbicg_ctx* h) {
     h->tile_occ[MODE] = occ < 1 ? 1 : occ;
     return e;
   }
-  cudaError_t e = cudaFuncSetAttribute(t_tile<DIM, MODE, true>, A, (int)h->tile_smem[MODE]);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(t_tile<DIM, MODE, false>, A, (int)h->tile_smem[MODE]);
   // light modes (few streams) fit 2 CTAs per SM: twice the bytes in flight
-  int occ = 1;
-  if (e == cudaSuccess)
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, t_tile<DIM, MODE, true>, TNT,
-                                                  h->tile_smem[MODE]);
+  int occ = 1, occ0 = 1;
+  cudaError_t e = tile_jac_attr_1(DIM, MODE, (int)h->tile_smem[MODE], &occ);
+  if (e == cudaSuccess) e = tile_jac_attr_0(DIM, MODE, (int)h->tile_smem[MODE], &occ0);
+  (void)A;
   if constexpr (bj_mode(MODE)) {
     if (e == cudaSuccess && h->tg.bj > 1) {
       const int sm = (int)h->tile_smem[MODE];
