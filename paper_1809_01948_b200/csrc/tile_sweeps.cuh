@@ -410,6 +410,50 @@ __device__ __forceinline__ void stencil_pair_der(const TileGeo& g, int nx, const
   t1 = a;
 }
 
+// Transform stage (XF) of the block-Jacobi modes with large blocks: once a
+// stencil plane has landed in its slot, the CTA replaces each staged operand v
+// by fl(M^-1 v), so every element is preconditioned once per plane instead of
+// once per leg that reads it (up to 7 times in 3D).  Same expression, same order
+// as bj_row (ascending k from +0.0), hence the same bits.  base: the slot; span:
+// staged elements; every element this thread owns sits at the same block
+// position ib (TNT % B == 0), bir = row ib of the inverse block.  The caller
+// has read the raw centre values it needs; the barrier after each operand's
+// reads orders them (and the block reads) before the in-place writes.
+#define XF_E 7  // elements per thread: span <= off + TP + 2 halo <= 1 + 1024 + 2 * 1026
+template <int NSO, int BB>
+__device__ __forceinline__ void xform_slot(double* base, int svs, int span, int ib,
+                                           const double* bir) {
+  {  // one operand at a time: XF_E results in registers, then in-place writes
+#pragma unroll
+    for (int v = 0; v < NSO; ++v) {
+      double o[XF_E];
+#pragma unroll
+      for (int k = 0; k < XF_E; ++k) {
+        const int e = threadIdx.x + k * TNT;
+        o[k] = 0.0;
+        if (e < span) {
+          const double* P = base + v * svs + e - ib;  // the block, 16-byte aligned
+          double a = 0.0;
+#pragma unroll
+          for (int q = 0; q < BB; q += 2) {
+            const double2 w = *reinterpret_cast<const double2*>(P + q);
+            a = a + bir[q] * w.x;
+            a = a + bir[q + 1] * w.y;
+          }
+          o[k] = a;
+        }
+      }
+      __syncthreads();  // every read of operand v (and the callers' centre reads) done
+#pragma unroll
+      for (int k = 0; k < XF_E; ++k) {
+        const int e = threadIdx.x + k * TNT;
+        if (e < span) base[v * svs + e] = o[k];
+      }
+    }
+  }
+  __syncthreads();
+}
+
 // Per-row arithmetic of each mode.  S = stream slot at this row, st = stride;
 // c0/c1 = the stencil operands' centre values, t0/t1 = their stencil products.
 template <int MODE, int K, int NOUTC, bool NRM, bool BJ>
@@ -567,6 +611,11 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   constexpr bool PREC = T::PREC != 0;
   constexpr bool BJP = BJ > 0 && PREC && !DER;  // stencil operands enter as A (block M)^-1 v
   constexpr int BB = BJ > 0 ? BJ : 2;          // block size for the helpers' array extents
+  // transform stage (xform_slot): measured on cfg4, it pays only where the per-leg
+  // preconditioner work is large -- block Jacobi b = 8: 89 -> 153 it/s; b = 4: 177 ->
+  // 174, b = 2: 226 -> 198, derived (classic BiCGStab): 292 -> 246 (its two extra CTA
+  // barriers per plane step cost more than the legs' recomputation)
+  constexpr bool XF = BJP && BB >= 8;
   __shared__ double s_bi[64];                  // the inverse block (row-major BB x BB)
   if (BJ > 0) {
     for (int q = threadIdx.x; q < BB * BB; q += blockDim.x) s_bi[q] = g.bi[q];
@@ -725,8 +774,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     const bool xy_int = __all_sync(0xffffffffu, !act || ((b0 & xy_all) == xy_all &&
                                                          (b1 & xy_all) == xy_all));
     double m1[NSO][2];  // plane z-1 centre values per stencil operand
+    double cr[NSO][2];  // XF: raw (DERIVED: derived) centre values of plane z
 #pragma unroll
-    for (int v = 0; v < NSO; ++v) m1[v][0] = m1[v][1] = 0.0;
+    for (int v = 0; v < NSO; ++v) m1[v][0] = m1[v][1] = cr[v][0] = cr[v][1] = 0.0;
     // SEG: element index of (line y0 - 1 (3D) / the line (2D), column x0s - SEG_HX)
     const int64_t sv_e0 = SEG ? (DIM == 3 ? (y0 - 1) * g.nx : 0) + x0s - SEG_HX : 0;
     const int64_t st_e0 = SEG ? (DIM == 3 ? y0 * g.nx : 0) + x0s : 0;
@@ -749,6 +799,24 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     auto sv_off = [&](int64_t zp) -> int {
       return SEG ? (ly + (DIM == 3 ? 1 : 0)) * ls + SEG_HX + cx
                  : align_off(svp[0] + zp * g.pxy + toff - g.halo) + g.halo + r;
+    };
+    // XF: this thread's block position (constant over the unit: TNT, nx, toff and the
+    // plane stride are multiples of BB) and its row of the inverse block
+    const int xf_ib = (BJP && !SEG) ? ((tid - align_off(svp[0] + toff - g.halo) - g.halo) & (BB - 1)) : 0;
+    double bir[BB];
+#pragma unroll
+    for (int q = 0; q < BB; ++q) bir[q] = BJP ? s_bi[xf_ib * BB + q] : 0.0;
+    // XF: read plane zp's centre values (raw / derived) into cc, then transform its slot
+    auto xf_plane = [&](int s, int64_t zp, double (&cc)[NSO][2]) {
+      double* base = sv + (size_t)s * NSV * svs;
+      if (act) {
+        const double* P = base + sv_off(zp);
+#pragma unroll
+        for (int v = 0; v < NSO; ++v) ld2<VEC>(P + v * svs, cc[v][0], cc[v][1]);
+      }
+      const int span = SEG ? nlines * ls
+                           : align_off(svp[0] + zp * g.pxy + toff - g.halo) + TP + 2 * g.halo;
+      xform_slot<NSO, BB>(base, svs, span, xf_ib, bir);
     };
     if (tid == 0) {
       for (int m = 0; m < 3 && m < nsv; ++m) stage_sv((svc + m) % 3, z0 - 1 + m);
@@ -776,6 +844,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       const int s1 = (svc + 1) % 3;  // plane z0
       mbar_wait(&bar[SD + s1], (ph >> (SD + s1)) & 1u);
       ph ^= 1u << (SD + s1);
+      if (XF) xf_plane(s1, z0, cr);
     }
     for (int n = 0; n < nst; ++n) {
       const int64_t z = z0 + n;
@@ -792,6 +861,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         mbar_wait(&bar[s_st], (ph >> s_st) & 1u);
         ph ^= 1u << s_st;
       }
+      double cn[NSO][2];  // XF: raw centre values of plane z+1 (next step's cr)
+      if (XF) xf_plane(s_z1, z + 1, cn);
       if (!act) continue;
       const double* Wz = sv + (size_t)s_z * NSV * svs + sv_off(z);
       const double* Wz1 = sv + (size_t)s_z1 * NSV * svs + sv_off(z + 1);
@@ -803,7 +874,28 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       const unsigned zb = ((g.o0 + z) > 0 ? 1u : 0u) | ((g.o0 + z) < g.nog - 1 ? 32u : 0u);
       double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
       double pc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // block Jacobi: M^-1 of the centre pair
-      if (BJP) {
+      if (XF) {  // planes z, z+1 hold the transformed operands: plain stencil
+        if (xy_int && zin) {
+#pragma unroll
+          for (int v = 0; v < NSO; ++v)
+            stencil_pair<DIM, VEC, true, false>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                                m1[v][1], 0u, 0u, pc[v][0], pc[v][1], t[v][0],
+                                                t[v][1]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < NSO; ++v)
+            stencil_pair<DIM, VEC, false, false>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                                 m1[v][1], b0 | zb, b1 | zb, pc[v][0], pc[v][1],
+                                                 t[v][0], t[v][1]);
+        }
+#pragma unroll
+        for (int v = 0; v < NSO; ++v) {
+          c[v][0] = cr[v][0];
+          c[v][1] = cr[v][1];
+          cr[v][0] = cn[v][0];
+          cr[v][1] = cn[v][1];
+        }
+      } else if (BJP) {
         if (xy_int && zin) {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
@@ -841,8 +933,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       }
 #pragma unroll
       for (int v = 0; v < NSO; ++v) {
-        m1[v][0] = BJP ? pc[v][0] : c[v][0];
-        m1[v][1] = BJP ? pc[v][1] : c[v][1];
+        m1[v][0] = (BJP || XF) ? pc[v][0] : c[v][0];
+        m1[v][1] = (BJP || XF) ? pc[v][1] : c[v][1];
       }
       double o0[NOUT], o1[NOUT];
 #pragma unroll
