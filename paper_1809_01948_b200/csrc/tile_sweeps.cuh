@@ -410,48 +410,90 @@ __device__ __forceinline__ void stencil_pair_der(const TileGeo& g, int nx, const
   t1 = a;
 }
 
-// Transform stage (XF) of the block-Jacobi modes with large blocks: once a
-// stencil plane has landed in its slot, the CTA replaces each staged operand v
-// by fl(M^-1 v), so every element is preconditioned once per plane instead of
-// once per leg that reads it (up to 7 times in 3D).  Same expression, same order
-// as bj_row (ascending k from +0.0), hence the same bits.  base: the slot; span:
-// staged elements; every element this thread owns sits at the same block
-// position ib (TNT % B == 0), bir = row ib of the inverse block.  The caller
-// has read the raw centre values it needs; the barrier after each operand's
-// reads orders them (and the block reads) before the in-place writes.
-#define XF_E 7  // elements per thread: span <= off + TP + 2 halo <= 1 + 1024 + 2 * 1026
-template <int NSO, int BB>
-__device__ __forceinline__ void xform_slot(double* base, int svs, int span, int ib,
-                                           const double* bir) {
-  {  // one operand at a time: XF_E results in registers, then in-place writes
+// Transform stage (XF) of the block-Jacobi modes.  When plane z+1 lands in its
+// slot, each thread overwrites its own row pair -- and a share of the halo
+// pairs -- of every staged operand v with fl(M^-1 v), the values the stencil
+// legs take.  Every element is then preconditioned once per plane instead of
+// once per leg that reads it (up to 7 times in 3D), with the same expression and
+// order as bj_pair, hence the same bits.  Plane z+1
+// is read by nobody else during step n (its +z leg uses the own pair, kept in
+// registers), so the writes need no CTA barrier: the next step's barrier orders
+// them before the neighbour reads.  A block-Jacobi block spans B/2 consecutive
+// pairs owned by consecutive lanes of one warp (pairs are block-aligned), so a
+// __syncwarp separates the block reads from the in-place writes.
+#define XF_H 3  // halo pairs per thread: <= (2 halo + off + B) / 2 / TNT + 1
+
+// transformed values of the element pair at slot element e; block Jacobi: every
+// pair a thread transforms sits at its block position ib (pairs are block-aligned,
+// TNT % B == 0), so rows ib, ib+1 of the inverse block come from registers (b0, b1)
+template <bool VEC, int NSO, int BB>
+__device__ __forceinline__ void xf_pair(const double* base, int svs, int e, int ib,
+                                        const double* b0, const double* b1, double (&o)[NSO][2]) {
+  {
 #pragma unroll
     for (int v = 0; v < NSO; ++v) {
-      double o[XF_E];
+      const double* P = base + v * svs + e - ib;
+      double x = 0.0, y = 0.0;
 #pragma unroll
-      for (int k = 0; k < XF_E; ++k) {
-        const int e = threadIdx.x + k * TNT;
-        o[k] = 0.0;
-        if (e < span) {
-          const double* P = base + v * svs + e - ib;  // the block, 16-byte aligned
-          double a = 0.0;
-#pragma unroll
-          for (int q = 0; q < BB; q += 2) {
-            const double2 w = *reinterpret_cast<const double2*>(P + q);
-            a = a + bir[q] * w.x;
-            a = a + bir[q + 1] * w.y;
-          }
-          o[k] = a;
-        }
+      for (int k = 0; k < BB; k += 2) {
+        double w0, w1;
+        ld2<VEC>(P + k, w0, w1);
+        x = x + b0[k] * w0;
+        x = x + b0[k + 1] * w1;
+        y = y + b1[k] * w0;
+        y = y + b1[k + 1] * w1;
       }
-      __syncthreads();  // every read of operand v (and the callers' centre reads) done
-#pragma unroll
-      for (int k = 0; k < XF_E; ++k) {
-        const int e = threadIdx.x + k * TNT;
-        if (e < span) base[v * svs + e] = o[k];
-      }
+      o[v][0] = x;
+      o[v][1] = y;
     }
   }
-  __syncthreads();
+}
+
+template <bool VEC, int NSO>
+__device__ __forceinline__ void xf_store(double* base, int svs, int e, const double (&o)[NSO][2]) {
+#pragma unroll
+  for (int v = 0; v < NSO; ++v) {
+    if (VEC) {
+      *reinterpret_cast<double2*>(base + v * svs + e) = make_double2(o[v][0], o[v][1]);
+    } else {
+      base[v * svs + e] = o[v][0];
+      base[v * svs + e + 1] = o[v][1];
+    }
+  }
+}
+
+// stencil_pair on transformed planes: the centre pair (p0, p1), the z-1 and z+1
+// pairs come from registers, the x and y legs from the transformed plane at W
+template <int DIM, bool VEC, bool INTERIOR>
+__device__ __forceinline__ void stencil_pair_xf(const TileGeo& g, int nx, const double* W,
+                                                double p0, double p1, double zm0, double zm1,
+                                                double zp0, double zp1, unsigned b0,
+                                                unsigned b1, double& t0, double& t1) {
+  const double pm = W[-1], p2 = W[2];
+  double ym0 = 0.0, ym1 = 0.0, yp0 = 0.0, yp1 = 0.0;
+  if (DIM == 3) {
+    ld2<VEC>(W - nx, ym0, ym1);
+    ld2<VEC>(W + nx, yp0, yp1);
+  }
+  const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
+  double a = 0.0;
+  a = leg<INTERIOR>(b0, 1u, a, czm * zm0);
+  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * ym0);
+  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * pm);
+  a = a + g.c[0] * p0;
+  a = leg<INTERIOR>(b0, 8u, a, g.c[2] * p1);
+  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * yp0);
+  a = leg<INTERIOR>(b0, 32u, a, czp * zp0);
+  t0 = a;
+  a = 0.0;
+  a = leg<INTERIOR>(b1, 1u, a, czm * zm1);
+  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * ym1);
+  a = leg<INTERIOR>(b1, 4u, a, g.c[1] * p0);
+  a = a + g.c[0] * p1;
+  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * p2);
+  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * yp1);
+  a = leg<INTERIOR>(b1, 32u, a, czp * zp1);
+  t1 = a;
 }
 
 // Per-row arithmetic of each mode.  S = stream slot at this row, st = stride;
@@ -611,11 +653,11 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   constexpr bool PREC = T::PREC != 0;
   constexpr bool BJP = BJ > 0 && PREC && !DER;  // stencil operands enter as A (block M)^-1 v
   constexpr int BB = BJ > 0 ? BJ : 2;          // block size for the helpers' array extents
-  // transform stage (xform_slot): measured on cfg4, it pays only where the per-leg
-  // preconditioner work is large -- block Jacobi b = 8: 89 -> 153 it/s; b = 4: 177 ->
-  // 174, b = 2: 226 -> 198, derived (classic BiCGStab): 292 -> 246 (its two extra CTA
-  // barriers per plane step cost more than the legs' recomputation)
-  constexpr bool XF = BJP && BB >= 8;
+  // transform stage (xf_pair) for block Jacobi b >= 4.  Measured on cfg4 (it/s, per-leg
+  // form -> transform): b = 8: 89 -> 162, b = 4: 177 -> 197; b = 2: 226 -> 210 and the
+  // derived operands of classic BiCGStab: 292 -> 276, so those keep the per-leg form
+  // (their per-leg work is one or two flops; the transform's halo pairs and stores cost more)
+  constexpr bool XF = BJP && BB >= 4;
   __shared__ double s_bi[64];                  // the inverse block (row-major BB x BB)
   if (BJ > 0) {
     for (int q = threadIdx.x; q < BB * BB; q += blockDim.x) s_bi[q] = g.bi[q];
@@ -774,9 +816,11 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     const bool xy_int = __all_sync(0xffffffffu, !act || ((b0 & xy_all) == xy_all &&
                                                          (b1 & xy_all) == xy_all));
     double m1[NSO][2];  // plane z-1 centre values per stencil operand
-    double cr[NSO][2];  // XF: raw (DERIVED: derived) centre values of plane z
+    double cr[NSO][2];  // XF: raw centre pair of plane z
+    double tr[NSO][2];  // XF: transformed centre pair of plane z
 #pragma unroll
-    for (int v = 0; v < NSO; ++v) m1[v][0] = m1[v][1] = cr[v][0] = cr[v][1] = 0.0;
+    for (int v = 0; v < NSO; ++v)
+      m1[v][0] = m1[v][1] = cr[v][0] = cr[v][1] = tr[v][0] = tr[v][1] = 0.0;
     // SEG: element index of (line y0 - 1 (3D) / the line (2D), column x0s - SEG_HX)
     const int64_t sv_e0 = SEG ? (DIM == 3 ? (y0 - 1) * g.nx : 0) + x0s - SEG_HX : 0;
     const int64_t st_e0 = SEG ? (DIM == 3 ? y0 * g.nx : 0) + x0s : 0;
@@ -800,23 +844,49 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       return SEG ? (ly + (DIM == 3 ? 1 : 0)) * ls + SEG_HX + cx
                  : align_off(svp[0] + zp * g.pxy + toff - g.halo) + g.halo + r;
     };
-    // XF: this thread's block position (constant over the unit: TNT, nx, toff and the
-    // plane stride are multiples of BB) and its row of the inverse block
-    const int xf_ib = (BJP && !SEG) ? ((tid - align_off(svp[0] + toff - g.halo) - g.halo) & (BB - 1)) : 0;
-    double bir[BB];
+    // XF: transform plane zp in slot s (own pair + a share of the halo pairs);
+    // returns the own pair raw (craw) and transformed (ctr).  Full-line tiles only
+    // (block Jacobi needs nx % b == 0 <= 1024).  Every pair this thread transforms
+    // sits at block position i0, so rows i0, i0+1 of the inverse block are registers.
+    static_assert(!(XF && SEG), "the transform stage runs on full-line tiles");
+    double bir0[BB], bir1[BB];
 #pragma unroll
-    for (int q = 0; q < BB; ++q) bir[q] = BJP ? s_bi[xf_ib * BB + q] : 0.0;
-    // XF: read plane zp's centre values (raw / derived) into cc, then transform its slot
-    auto xf_plane = [&](int s, int64_t zp, double (&cc)[NSO][2]) {
+    for (int q = 0; q < BB; ++q) {
+      bir0[q] = XF ? s_bi[i0 * BB + q] : 0.0;
+      bir1[q] = XF ? s_bi[(i0 + 1) * BB + q] : 0.0;
+    }
+    auto xf_plane = [&](int s, int64_t zp, double (&craw)[NSO][2], double (&ctr)[NSO][2]) {
       double* base = sv + (size_t)s * NSV * svs;
+      // E0: slot element of tile row 0.  Halo pairs h: nb (a multiple of the pairs per
+      // block, so blocks stay inside a warp) end at E0, the rest start at the tile's end.
+      const int E0 = align_off(svp[0] + zp * g.pxy + toff - g.halo) + g.halo;
+      const int TPe = TP + (TP & 1);
+      constexpr int BP = BB / 2;
+      const int nb = ((E0 + 1) / 2 + BP - 1) / BP * BP;
+      const int H = nb + (g.halo - (TP & 1) + 1) / 2;
       if (act) {
-        const double* P = base + sv_off(zp);
+        const int e = sv_off(zp);
 #pragma unroll
-        for (int v = 0; v < NSO; ++v) ld2<VEC>(P + v * svs, cc[v][0], cc[v][1]);
+        for (int v = 0; v < NSO; ++v) ld2<VEC>(base + v * svs + e, craw[v][0], craw[v][1]);
+        xf_pair<VEC, NSO, BB>(base, svs, e, i0, bir0, bir1, ctr);
       }
-      const int span = SEG ? nlines * ls
-                           : align_off(svp[0] + zp * g.pxy + toff - g.halo) + TP + 2 * g.halo;
-      xform_slot<NSO, BB>(base, svs, span, xf_ib, bir);
+      // one operand and one halo pair at a time (registers); per pair the warp's
+      // block reads precede its in-place writes (__syncwarp)
+#pragma unroll
+      for (int v = 0; v < NSO; ++v) {
+        double* bv = base + v * svs;
+#pragma unroll
+        for (int k = 0; k < XF_H; ++k) {
+          const int h = tid + k * TNT;
+          int e = h < nb ? E0 - 2 * (nb - h) : E0 + TPe + 2 * (h - nb);
+          if (h >= H || e < 0 || e + 1 >= svs) e = -1;
+          double o[1][2] = {{0.0, 0.0}};
+          if (e >= 0) xf_pair<VEC, 1, BB>(bv, svs, e, i0, bir0, bir1, o);
+          __syncwarp();
+          if (k == 0 && act) xf_store<VEC, 1>(bv, svs, sv_off(zp), {{ctr[v][0], ctr[v][1]}});
+          if (e >= 0) xf_store<VEC, 1>(bv, svs, e, o);
+        }
+      }
     };
     if (tid == 0) {
       for (int m = 0; m < 3 && m < nsv; ++m) stage_sv((svc + m) % 3, z0 - 1 + m);
@@ -844,7 +914,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       const int s1 = (svc + 1) % 3;  // plane z0
       mbar_wait(&bar[SD + s1], (ph >> (SD + s1)) & 1u);
       ph ^= 1u << (SD + s1);
-      if (XF) xf_plane(s1, z0, cr);
+      if (XF) xf_plane(s1, z0, cr, tr);  // ordered before step 0's reads by its barrier
     }
     for (int n = 0; n < nst; ++n) {
       const int64_t z = z0 + n;
@@ -861,8 +931,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         mbar_wait(&bar[s_st], (ph >> s_st) & 1u);
         ph ^= 1u << s_st;
       }
-      double cn[NSO][2];  // XF: raw centre values of plane z+1 (next step's cr)
-      if (XF) xf_plane(s_z1, z + 1, cn);
+      double cn[NSO][2], tn[NSO][2];  // XF: own pair of plane z+1, raw / transformed
+      if (XF) xf_plane(s_z1, z + 1, cn, tn);
       if (!act) continue;
       const double* Wz = sv + (size_t)s_z * NSV * svs + sv_off(z);
       const double* Wz1 = sv + (size_t)s_z1 * NSV * svs + sv_off(z + 1);
@@ -874,26 +944,30 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       const unsigned zb = ((g.o0 + z) > 0 ? 1u : 0u) | ((g.o0 + z) < g.nog - 1 ? 32u : 0u);
       double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
       double pc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // block Jacobi: M^-1 of the centre pair
-      if (XF) {  // planes z, z+1 hold the transformed operands: plain stencil
+      if (XF) {  // plane z holds the transformed operands; centre, z+-1 from registers
         if (xy_int && zin) {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair<DIM, VEC, true, false>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
-                                                m1[v][1], 0u, 0u, pc[v][0], pc[v][1], t[v][0],
-                                                t[v][1]);
+            stencil_pair_xf<DIM, VEC, true>(g, ls, Wz + v * svs, tr[v][0], tr[v][1], m1[v][0],
+                                            m1[v][1], tn[v][0], tn[v][1], 0u, 0u, t[v][0],
+                                            t[v][1]);
         } else {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair<DIM, VEC, false, false>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
-                                                 m1[v][1], b0 | zb, b1 | zb, pc[v][0], pc[v][1],
-                                                 t[v][0], t[v][1]);
+            stencil_pair_xf<DIM, VEC, false>(g, ls, Wz + v * svs, tr[v][0], tr[v][1], m1[v][0],
+                                             m1[v][1], tn[v][0], tn[v][1], b0 | zb, b1 | zb,
+                                             t[v][0], t[v][1]);
         }
 #pragma unroll
         for (int v = 0; v < NSO; ++v) {
           c[v][0] = cr[v][0];
           c[v][1] = cr[v][1];
+          pc[v][0] = tr[v][0];
+          pc[v][1] = tr[v][1];
           cr[v][0] = cn[v][0];
           cr[v][1] = cn[v][1];
+          tr[v][0] = tn[v][0];
+          tr[v][1] = tn[v][1];
         }
       } else if (BJP) {
         if (xy_int && zin) {
