@@ -47,12 +47,14 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def ncu_traffic(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary."""
+def ncu_traffic(config: str, kernel: str):
+    """dram bytes per launch of `kernel` on `config` from the committed ncu --set full
+    summaries (profiles/ncu_traffic.json; captured with the Jacobi preconditioner,
+    the default schedule and periodic replacement)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(p))
-        return d[kernel]["dram_bytes_per_launch"]
+        return d[config][kernel]["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -345,7 +347,9 @@ def run_ours(args, rank, world):
     kb = per_kernel[dom]["bytes"]
     achieved = kb / k_avg_s / 1e9
     it_bytes = S.kernel_bytes("iteration") * world  # all ranks' algorithmic bytes per iteration
-    traffic = ncu_traffic(dom) if (world == 1 and cfg.name == "cfg4") else None
+    profiled = (world == 1 and args.block == 1 and not args.rr_auto and args.schedule == 0
+                and not args.loopback)
+    traffic = ncu_traffic(cfg.name, dom) if profiled else None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,

@@ -1,7 +1,7 @@
 """Summarise an `ncu --page raw --csv` export into profiles/: a markdown table and
 the per-kernel DRAM traffic JSON bench.py reads for roofline.traffic.
 
-usage: python scripts/ncu_summary.py RAW.csv OUT.md [--n ROWS] [--traffic profiles/ncu_traffic.json]
+usage: python scripts/ncu_summary.py RAW.csv OUT.md [--n ROWS] [--traffic profiles/ncu_traffic.json --config cfg4]
 """
 import argparse
 import csv
@@ -52,6 +52,7 @@ def main():
     ap.add_argument("out")
     ap.add_argument("--n", type=int, default=512 ** 3)
     ap.add_argument("--traffic", default=None)
+    ap.add_argument("--config", default="cfg4", help="section of the traffic JSON")
     ap.add_argument("--title", default="ncu --set full summary")
     ap.add_argument("--peak", type=float, default=6550.4)
     ap.add_argument("--prec-extra", type=float, default=0.0,
@@ -89,8 +90,13 @@ def main():
                             "kernel": name, "source": a.out}
     open(a.out, "w").write("\n".join(md) + "\n")
     print("\n".join(md))
-    if a.traffic:
-        json.dump(traffic, open(a.traffic, "w"), indent=1)
+    if a.traffic:  # merge into the config's section
+        try:
+            allt = json.load(open(a.traffic))
+        except (OSError, ValueError):
+            allt = {}
+        allt.setdefault(a.config, {}).update(traffic)
+        json.dump(allt, open(a.traffic, "w"), indent=1)
 
 
 if __name__ == "__main__":
