@@ -78,7 +78,8 @@ struct pbicg_ctx {
   TileGeo tg{};
   bool tile_ok = false;  // TMA 2.5D sweeps eligible for this operator
   bool tile_vec = false; // ... with 16-byte aligned pairs (nx even)
-  bool tile_seg = false; // ... as x-segmented tiles (nx > 1024; instances in tile_seg.cu)
+  bool tile_seg = false; // ... as x-segmented tiles (nx > 1024, or 3D planes too wide for
+                         // full-line tiles; instances in tile_seg.cu)
   int tile_on = 1;       // option "tile"
   size_t tile_smem[TM_N] = {0};
   int tile_occ[TM_N] = {0};  // resident CTAs per SM of each tile kernel
@@ -1022,7 +1023,25 @@ void setup_tile(pbicg_ctx* h) {
   t.nseg = 1;
   t.lstride = (int32_t)g.nx;
   int64_t nseg = 1;
-  if (g.nx > tpmax) {
+  // full-line tiles need nx <= 2 TNT and (3D) a plane of TY >= 1 lines plus two halo
+  // lines per staged vector in shared memory (3D: nx <= ~850 for the widest mode, sweep A)
+  bool full = g.nx <= tpmax;
+  if (full) {
+    int64_t TY = dim == 3 ? (tpmax / g.nx) : 1;
+    if (TY > lines) TY = lines;
+    t.TY = (int32_t)(TY < 1 ? 1 : TY);
+    for (; t.TY >= 1; --t.TY) {
+      const int64_t TP = t.TY * g.nx, hl = dim == 3 ? g.nx + 2 : 2;
+      t.st_stride = (int32_t)((TP + 2 + 1) & ~1LL);
+      t.sv_stride = (int32_t)((TP + 2 * hl + 2 + 1) & ~1LL);
+      size_t worst = 0;
+      for (int m = 0; m < TM_N; ++m)
+        worst = tile_smem_bytes(t, m) > worst ? tile_smem_bytes(t, m) : worst;
+      if (worst + reserve <= (size_t)max_smem) break;
+    }
+    full = t.TY >= 1;
+  }
+  if (!full) {
     // x-segmented tiles (tile_seg.cu): TY lines x sx columns, sx the widest multiple of
     // 16 (<= 512) whose worst-mode shared memory fits; odd nx keeps the line kernels
     if (g.nx % 2 != 0) return;
@@ -1458,8 +1477,10 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
       h->grid_c2 = occ_grid(h, k_sweepC2<2>, (h->n_local + 255) / 256); h->block = b0; }
   }
   setup_tile(h);
-  if (bj > 1 && !h->tile_ok)
-    return fail(h, PBICG_EINVAL, "block Jacobi on a stencil needs the TMA tile kernels");
+  if (bj > 1 && (!h->tile_ok || h->tile_seg))
+    return fail(h, PBICG_EINVAL,
+                "block Jacobi on a stencil needs full-line TMA tiles (2D: nx <= 1024, "
+                "3D: nx <= ~850)");
   return alloc_common(h);
 }
 

@@ -99,7 +99,11 @@ def test_bj_loopback(S, orc, method):
 
 
 STENCILS = [(2, 64, 48, 1, "cd2"), (2, 40, 30, 1, "poisson"), (3, 16, 12, 10, "cd3"),
-            (3, 64, 64, 64, "cd3"), (3, 8, 5, 7, "cd3")]
+            (3, 64, 64, 64, "cd3"), (3, 8, 5, 7, "cd3"),
+            # one-line tiles with the widest halos that fit (3D nx = 840: the transform
+            # stage's halo pairs take two rounds of the CTA), a tile of one block per line
+            (3, 840, 3, 4, "cd3"), (3, 520, 5, 4, "cd3"), (2, 1024, 6, 1, "cd2"),
+            (2, 8, 40, 1, "cd2")]
 
 
 @pytest.mark.parametrize("block", [2, 4, 8])
@@ -171,6 +175,10 @@ def test_bj_errors(S, orc):
         S.stencil(2, 10, 8, 1, problems.poisson2d_coef(), block=4)
     with pytest.raises(PbicgError):  # stencil: b <= 8
         S.stencil(2, 32, 8, 1, problems.poisson2d_coef(), block=16)
+    with pytest.raises(PbicgError):  # x-segmented tiles (nx > 1024) have no block Jacobi
+        S.stencil(2, 2048, 4, 1, problems.poisson2d_coef(), block=4)
+    with pytest.raises(PbicgError):  # 3D planes too wide for full-line tiles: segmented
+        S.stencil(3, 1024, 3, 4, problems.cfg34_coef(), block=4)
     st = S.stencil(2, 32, 8, 1, problems.poisson2d_coef(), block=4)
     with pytest.raises(PbicgError):  # comparison solvers use Jacobi
         st.set_option("method", 1)

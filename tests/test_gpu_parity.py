@@ -228,10 +228,12 @@ def test_csr_wide_band_uses_gather_path(S, orc):
 
 @pytest.mark.parametrize("dim,nx,ny,nz,kind", [
     (2, 1500, 40, 1, "cd2"), (2, 4096, 24, 1, "poisson"), (2, 2050, 9, 1, "cd2"),
-    (3, 1100, 5, 6, "cd3"), (3, 2048, 3, 4, "cd3"), (3, 1026, 1, 5, "cd3")])
+    (3, 1100, 5, 6, "cd3"), (3, 2048, 3, 4, "cd3"), (3, 1026, 1, 5, "cd3"),
+    (3, 1000, 5, 4, "cd3"), (3, 900, 2, 3, "cd3")])
 def test_segmented_tiles(S, orc, dim, nx, ny, nz, kind):
-    """nx > 1024 (even): x-segmented TMA tiles (line segments with halo columns,
-    ragged last segment); every solver and automated replacement, bitwise."""
+    """nx > 1024 (even), or 3D planes too wide for full-line tiles (nx > ~850):
+    x-segmented TMA tiles (line segments with halo columns, ragged last segment);
+    every solver and automated replacement, bitwise."""
     solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of(kind))
     res = solver.solve(b_d, tol=1e-11, maxit=120, rr_period=7, gap=True)
     ref = orc.pbicgstab(A, b, tol=1e-11, maxit=120, rr_period=7)
