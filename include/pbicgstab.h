@@ -161,9 +161,14 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *   "overlap"    1 (default) => multi-GPU: each global reduction runs on a side
  *                stream behind the halo exchange / SpMV the next phase needs;
  *                0 => blocking on the compute stream
- *   "tile"       1 (default) => stencil sweeps use the TMA-staged 2.5D kernels when
- *                nx <= 1024; 0 => plain line kernels (same results; not with block
- *                Jacobi)
+ *   "tile"       1 (default) => stencil sweeps use the TMA-staged 2.5D kernels
+ *                (full-line tiles; x-segmented tiles for even nx > 1024 and 3D nx >
+ *                ~850; odd nx beyond those keeps the line kernels); 0 => plain line
+ *                kernels (same results; not with block Jacobi)
+ *   "pdl"        1 => launch the tile kernels with programmatic dependent launch:
+ *                the next sweep's CTAs are scheduled as the previous sweep's CTAs
+ *                retire (griddepcontrol); same results.  Default 0: measured +1-15%
+ *                without CUDA graphs, within +-2% with them
  *   "schedule"   0 (default) auto (stencil: fused, CSR: split); 1 fused 2-sweep
  *                (stencil only: t, v recomputed inside the sweeps, 24 passes); 2 split
  *                4-phase (the paper's pipeline: stored t, v, stand-alone SpMVs the
@@ -184,8 +189,9 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *   "rr_auto"    1 => automated residual replacement: the run-time bound
  *                f^r_i on the residual gap (eq:DDr_bound) is propagated on the device
  *                and iteration i replaces when f_{i-1} <= sqrt(eps)||r_{i-1}|| and
- *                f_i > sqrt(eps)||r_i|| (eq:criterion).  Needs method 0, a stencil
- *                operator with nx <= 1024 and rr_period = 0 in pbicgstab_solve
+ *                f_i > sqrt(eps)||r_i|| (eq:criterion).  Needs method 0, the tile
+ *                kernels on a stencil (not odd nx > 1024) and rr_period = 0 in
+ *                pbicgstab_solve
  * Errors: EINVAL for an unknown key or bad value. */
 pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value);
 

@@ -2111,6 +2111,9 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       m->use_graphs = value != 0;
     } else if (k == "timing") {
       m->timing = value != 0;
+    } else if (k == "pdl") {  // programmatic dependent launch of the tile kernels
+      m->tg.pdl = value != 0;
+      destroy_graphs(m);
     } else if (k == "overlap") {
       m->overlap = value != 0 && (m->comm != COMM_NCCL || m->nccl_red != m->nccl_halo);
       destroy_graphs(m);
@@ -2123,7 +2126,7 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       if (value != 0 && (m->method != M_PBICGSTAB || !m->ar_ok ||
                          (m->kind == KIND_STENCIL && (!m->tile_ok || m->schedule == 2))))
         return fail(h, PBICG_EINVAL,
-                    "rr_auto needs method 0 and a stencil with nx <= 1024 (TMA tile kernels) or "
+                    "rr_auto needs method 0 and a stencil on the TMA tile kernels (not odd nx > 1024) or "
                     "a CSR operator on one process (bound constants need every row)");
       m->auto_rr = value != 0;
       destroy_graphs(m);

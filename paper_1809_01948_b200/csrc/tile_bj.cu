@@ -16,7 +16,7 @@ namespace {
 template <int DIM, int MODE>
 void launch_one(int grid, size_t smem, cudaStream_t s, const TileGeo& g, const Vecs& V, Scal* sc,
                 Dd* part, Hist h) {
-  t_tile<DIM, MODE, true, PBICG_BJ_B><<<grid, TNT, smem, s>>>(g, V, sc, part, h);
+  tile_launch(t_tile<DIM, MODE, true, PBICG_BJ_B>, grid, smem, s, g, V, sc, part, h);
 }
 
 template <int DIM, int MODE>

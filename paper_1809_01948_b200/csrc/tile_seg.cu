@@ -12,7 +12,7 @@ namespace {
 template <int DIM, int MODE>
 void launch_one(int grid, size_t smem, cudaStream_t s, const TileGeo& g, const Vecs& V, Scal* sc,
                 Dd* part, Hist h) {
-  t_tile<DIM, MODE, true, 0, true><<<grid, TNT, smem, s>>>(g, V, sc, part, h);
+  tile_launch(t_tile<DIM, MODE, true, 0, true>, grid, smem, s, g, V, sc, part, h);
 }
 
 template <int DIM, int MODE>

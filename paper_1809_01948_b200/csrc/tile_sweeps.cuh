@@ -111,6 +111,7 @@ struct TileGeo {
   int32_t sx;         // segment width (even); == nx when lines are not segmented
   int32_t nseg;       // segments per line
   int32_t lstride;    // shared-memory stride of a staged stencil line segment (sx + 16)
+  int32_t pdl;        // launch with programmatic dependent launch (option "pdl")
 };
 
 // halo columns staged on each side of a segment (>= 2 for the x legs; 8 keeps every
@@ -662,6 +663,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   if (BJ > 0) {
     for (int q = threadIdx.x; q < BB * BB; q += blockDim.x) s_bi[q] = g.bi[q];
   }
+  // PDL (tile_launch): nothing above reads the previous kernel's results; wait for it
+  // to complete (a no-op without PDL)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr int SD = StreamDepth<MODE_>::v;  // stream ring depth; stencil barriers follow
   static_assert(K <= RED_K, "partials buffer holds RED_K pairs per CTA");
   if (MODE == TM_A || MODE == TM_C || MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3 ||
@@ -1048,6 +1052,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     svc = (svc + nsv) % 3;
     stc = (stc + nst) % SD;
   }
+  // PDL: this CTA's sweep is done; the next kernel may be scheduled (it still waits
+  // for this grid's completion, the grid reduction included, before reading anything)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (T::K > 0) {
     Dd tot[K];
     const int slot = MODE == TM_A ? T_SWEEPA : MODE == TM_C ? T_SWEEPC : MODE == TM_RR2 ? T_RR2
@@ -1103,4 +1110,28 @@ inline size_t tile_smem_bytes(const TileGeo& g, int mode) {
     case TM_SPD: return tile_smem_bytes_t<TM_SPD>(g);
     default: return tile_smem_bytes_t<TM_PCI2>(g);
   }
+}
+
+// Host launch of a tile kernel.  With g.pdl the launch carries programmatic stream
+// serialization (PDL): the grid may be scheduled while the previous kernel of the
+// stream is still draining; t_tile's griddepcontrol.wait holds every read of that
+// kernel's results until it has completed and its writes are visible.
+template <typename... A>
+inline void tile_launch(void (*kern)(A...), int grid, size_t smem, cudaStream_t s,
+                        const TileGeo& g, const Vecs& V, Scal* sc, Dd* part, Hist h) {
+  if (!g.pdl) {
+    kern<<<grid, TNT, smem, s>>>(g, V, sc, part, h);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(TNT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, g, V, sc, part, h);
 }

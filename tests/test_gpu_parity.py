@@ -253,3 +253,20 @@ def test_segmented_tiles(S, orc, dim, nx, ny, nz, kind):
     solver.set_option("schedule", 2)
     res = solver.solve(b_d, tol=1e-11, maxit=120, rr_period=7, gap=True)
     check_parity(res, orc.pbicgstab(A, b, tol=1e-11, maxit=120, rr_period=7), xs)
+
+
+@pytest.mark.parametrize("graphs", [0, 1])
+def test_pdl_launch(S, orc, graphs):
+    """Option pdl (programmatic dependent launch of the tile kernels): every sweep
+    still reads its predecessor's results only after griddepcontrol.wait, so the
+    iterates are the same bits, with and without CUDA graphs, with replacement,
+    gap tracking and automated replacement."""
+    solver, A, xs, b, b_d = stencil_case(S, orc, 3, 40, 33, 29, coef_of("cd3"))
+    solver.set_option("pdl", 1)
+    solver.set_option("graphs", graphs)
+    res = solver.solve(b_d, tol=1e-12, maxit=200, rr_period=9, gap=True)
+    check_parity(res, orc.pbicgstab(A, b, tol=1e-12, maxit=200, rr_period=9), xs)
+    solver.set_option("method", 1)
+    res = solver.solve(b_d, tol=1e-12, maxit=200, gap=True)
+    check_parity(res, orc.bicgstab(A, b, tol=1e-12, maxit=200), xs)
+
