@@ -165,6 +165,9 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *                (full-line tiles; x-segmented tiles for even nx > 1024 and 3D nx >
  *                ~850; odd nx beyond those keeps the line kernels); 0 => plain line
  *                kernels (same results; not with block Jacobi)
+ *   "csr_tma"    1 (default) => CSR with the Jacobi preconditioner: sweeps A and C
+ *                stream their vectors through shared memory with bulk copies
+ *                (c_sweep_tma); 0 => per-row global loads (same results)
  *   "pdl"        1 => launch the tile kernels with programmatic dependent launch:
  *                the next sweep's CTAs are scheduled as the previous sweep's CTAs
  *                retire (griddepcontrol); same results.  Default 0: measured +1-15%

@@ -322,6 +322,164 @@ __global__ void __launch_bounds__(256, 3) c_sweepC(CsrOp A, Vecs V, Scal* __rest
     publish<F_SWEEPC>(sc, h, tot);
 }
 
+// ---------------------------------------------------------------------------
+// TMA-staged sweeps (Jacobi): the same row arithmetic as c_sweepA / c_sweepC, with
+// every input vector streamed into shared memory as CST_R-row chunks by bulk copies
+// (cp.async.bulk + mbarrier, a two-stage ring: one chunk in flight while the other
+// is computed), two rows per thread (16-byte shared loads, 16-byte streaming
+// stores).  Chunks go to CTAs round-robin (static, deterministic); one CTA per SM.
+#define CST_R 1024   // rows per chunk
+#define CST_T 512    // threads per CTA (a row pair each)
+#define CST_NIN 12   // input vectors staged per chunk (max over the two sweeps)
+constexpr size_t kCstSmem = 64 + 2 * (size_t)CST_NIN * CST_R * sizeof(double);
+
+template <int SW, bool NRM>  // SW 0: sweep A (lines 5-12), 1: sweep C (lines 17-21)
+__global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                                        Dd* __restrict__ part, Hist h) {
+  constexpr int K = SW == 0 ? (NRM ? 12 : 2) : (NRM ? 9 : 5);
+  if (sc->done) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  double* buf = reinterpret_cast<double*>(smem_raw + 64);
+  const int tid = threadIdx.x;
+  const double al = sc->alpha, be = sc->beta, om = sc->omega;
+  const bool rr = SW == 0 && sc->use_rr != 0;
+  // staged inputs, in this order
+  //   A: w, z (pre-replacement), t, v, l, k, g, s, r, dinv [, replaced z]
+  //   C: w, z, t, v, s, k, l, r, x, g, r^0, dinv
+  const double* in[CST_NIN];
+  int nin;
+  if (SW == 0) {
+    const double* a[11] = {V.w0, V.z0, V.w1, V.z1, V.l, V.k, V.g, V.s, V.r, A.dinv, V.zrr};
+    nin = rr ? 11 : 10;
+#pragma unroll
+    for (int v = 0; v < 11; ++v) in[v] = a[v];
+    in[11] = nullptr;
+  } else {
+    const double* a[12] = {V.w0, V.z0, V.w1, V.z1, V.s, V.k, V.l, V.r, V.x, V.g, V.rh, A.dinv};
+    nin = 12;
+#pragma unroll
+    for (int v = 0; v < 12; ++v) in[v] = a[v];
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t nch = (A.n + CST_R - 1) / CST_R;
+  auto stage = [&](int slot, int64_t c) {
+    const int64_t j0 = c * CST_R;
+    const int64_t rows = (A.n - j0) < CST_R ? (A.n - j0) : CST_R;
+    const uint32_t bytes = (uint32_t)((rows * 8 + 15) & ~15LL);  // vectors carry 2 slack rows
+    mbar_arrive_expect_tx(&bar[slot], bytes * (uint32_t)nin);
+#pragma unroll
+    for (int v = 0; v < CST_NIN; ++v)  // unrolled: `in` stays in registers
+      if (v < nin)
+        bulk_g2s(buf + ((size_t)slot * CST_NIN + v) * CST_R, in[v] + j0, bytes, &bar[slot]);
+  };
+  Dd acc[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k] = dd_zero();
+  if (tid == 0 && (int64_t)blockIdx.x < nch) stage(0, blockIdx.x);
+  uint32_t ph = 0;
+  int slot = 0;
+  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, slot ^= 1) {
+    // the other slot was released by the previous chunk's closing barrier
+    if (tid == 0 && c + gridDim.x < nch) stage(slot ^ 1, c + gridDim.x);
+    mbar_wait(&bar[slot], (ph >> slot) & 1u);
+    ph ^= 1u << slot;
+    const int64_t j = c * CST_R + 2 * tid;
+    if (j < A.n) {
+      const bool valid1 = j + 1 < A.n;
+      const double* B = buf + (size_t)slot * CST_NIN * CST_R + 2 * tid;
+      double x0[CST_NIN], x1[CST_NIN];
+#pragma unroll
+      for (int v = 0; v < CST_NIN; ++v) {
+        if (v < nin) {
+          const double2 q = *reinterpret_cast<const double2*>(B + (size_t)v * CST_R);
+          x0[v] = q.x;
+          x1[v] = q.y;
+        } else {
+          x0[v] = x1[v] = 0.0;
+        }
+      }
+      double o0[5], o1[5];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double* xv = e == 0 ? x0 : x1;
+        double* o = e == 0 ? o0 : o1;
+        if (e == 1 && !valid1) break;
+        if (SW == 0) {  // identical expressions to c_sweepA
+          const double wc = xv[0], zc = xv[1], t = xv[2], v = xv[3], lj = xv[4];
+          const double dj = xv[9];
+          const double m = dj * wc, n = dj * zc;  // m_i, n_{i-1}
+          const double zo = rr ? xv[10] : zc;
+          const double gn = xv[5] + be * (xv[6] - om * lj);
+          const double sn = wc + be * (xv[7] - om * zo);
+          const double ln = m + be * (lj - om * n);
+          const double zn = t + be * (zo - om * v);
+          const double q = xv[8] - al * sn;
+          const double y = wc - al * zn;
+          dd_fma(acc[0], q, y);
+          dd_fma(acc[1 % K], y, y);
+          if (NRM) {
+            c_nrm(acc[2 % K], xv[5]); c_nrm(acc[3 % K], wc); c_nrm(acc[4 % K], m);
+            c_nrm(acc[5 % K], t); c_nrm(acc[6 % K], gn); c_nrm(acc[7 % K], sn);
+            c_nrm(acc[8 % K], ln); c_nrm(acc[9 % K], zn); c_nrm(acc[10 % K], q);
+            c_nrm(acc[11 % K], y);
+          }
+          o[0] = gn; o[1] = sn; o[2] = ln; o[3] = zn; o[4] = dj * zn;  // n_i (line 13)
+        } else {  // identical expressions to c_sweepC
+          const double wc = xv[0], zc = xv[1], t = xv[2], v = xv[3], sj = xv[4];
+          const double dj = xv[11];
+          const double m = dj * wc, n = dj * zc;  // m_i, n_i
+          const double u = xv[5] - al * xv[6];
+          const double q = xv[7] - al * sj;
+          const double y = wc - al * zc;
+          const double xj = xv[8];
+          const double xn = (xj + al * xv[9]) + om * u;
+          const double rn = q - om * y;
+          const double kn = u - om * (m - al * n);
+          const double wn = y - om * (t - al * v);
+          const double rhj = xv[10];
+          dd_fma(acc[0], rhj, rn);
+          dd_fma(acc[1 % K], rhj, wn);
+          dd_fma(acc[2 % K], rhj, sj);
+          dd_fma(acc[3 % K], rhj, zc);
+          dd_fma(acc[4 % K], rn, rn);
+          if (NRM) {
+            c_nrm(acc[5 % K], xj); c_nrm(acc[6 % K], u); c_nrm(acc[7 % K], n);
+            c_nrm(acc[8 % K], v);
+          }
+          o[0] = xn; o[1] = rn; o[2] = kn; o[3] = wn; o[4] = dj * wn;  // m_{i+1} (line 22)
+        }
+      }
+      double* out[5];
+      if (SW == 0) {
+        out[0] = V.g; out[1] = V.s; out[2] = V.l; out[3] = V.z0; out[4] = V.nv;
+      } else {
+        out[0] = V.x; out[1] = V.r; out[2] = V.k; out[3] = V.w0; out[4] = V.mv;
+      }
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        if (valid1) {
+          __stcs(reinterpret_cast<double2*>(out[k] + j), make_double2(o0[k], o1[k]));
+        } else {
+          __stcs(out[k] + j, o0[k]);
+        }
+      }
+    }
+    __syncthreads();  // this slot is free for the chunk after next
+  }
+  Dd tot[K];
+  if (dd_grid_reduce<K>(acc, part, &sc->counter[SW == 0 ? T_SWEEPA : T_SWEEPC], tot) &&
+      threadIdx.x == 0) {
+    if (SW == 0) publish<F_SWEEPA>(sc, h, tot);
+    else publish<F_SWEEPC>(sc, h, tot);
+  }
+}
+
 // eq:rr: r := b - A x; k := M^-1 r; s := A g; l := M^-1 s
 template <bool NRM, bool BJ>
 __global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__ sc,

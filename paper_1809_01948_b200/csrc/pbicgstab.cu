@@ -87,6 +87,9 @@ struct pbicg_ctx {
   WinGeo wg{};
   bool win_ok = false;  // banded CSR: window SpMV (c_spmv_win) eligible
   int win_grid = 0;
+  bool cst_ok = false;  // CSR: TMA-staged sweeps (c_sweep_tma) eligible (Jacobi)
+  bool cst_on = true;   // option "csr_tma"
+  int cst_grid = 0;
   std::vector<void*> allocs;
   Vecs V{};
   double* xtmp = nullptr;    // ghosted scratch (apply input, host-solve staging)
@@ -420,6 +423,9 @@ void launch_csr(pbicg_ctx* h, Phase p) {
       if (h->csr.bj > 1) {
         if (h->auto_rr) c_sweepA<true, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
         else c_sweepA<false, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      } else if (h->cst_ok && h->cst_on) {
+        if (h->auto_rr) c_sweep_tma<0, true><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        else c_sweep_tma<0, false><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
       } else {
         if (h->auto_rr) c_sweepA<true, false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
         else c_sweepA<false, false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
@@ -439,6 +445,9 @@ void launch_csr(pbicg_ctx* h, Phase p) {
         if (h->csr.bj > 1) {
           if (h->auto_rr) c_sweepC<true, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
           else c_sweepC<false, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        } else if (h->cst_ok && h->cst_on) {
+          if (h->auto_rr) c_sweep_tma<1, true><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          else c_sweep_tma<1, false><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
         } else {
           if (h->auto_rr) c_sweepC<true, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
           else c_sweepC<false, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
@@ -1728,6 +1737,17 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     h->win_ok = e == cudaSuccess;
     cudaGetLastError();
   }
+  if (h->csr.bj <= 1) {  // TMA-staged sweeps: one CTA per SM, two-stage chunk ring
+    const auto SM = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaFuncSetAttribute(c_sweep_tma<0, false>, SM, (int)kCstSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<0, true>, SM, (int)kCstSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, false>, SM, (int)kCstSmem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, true>, SM, (int)kCstSmem);
+    const int64_t nch = (n + CST_R - 1) / CST_R;
+    h->cst_grid = (int)(nch < h->num_sm ? nch : h->num_sm);
+    h->cst_ok = e == cudaSuccess && h->H % 2 == 0;  // 16-byte aligned row pairs
+    cudaGetLastError();
+  }
   return alloc_common(h);
 }
 
@@ -2111,6 +2131,9 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       m->use_graphs = value != 0;
     } else if (k == "timing") {
       m->timing = value != 0;
+    } else if (k == "csr_tma") {  // CSR: TMA-staged sweeps (1, default) or per-row loads
+      m->cst_on = value != 0;
+      destroy_graphs(m);
     } else if (k == "pdl") {  // programmatic dependent launch of the tile kernels
       m->tg.pdl = value != 0;
       destroy_graphs(m);
