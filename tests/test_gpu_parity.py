@@ -270,3 +270,34 @@ def test_pdl_launch(S, orc, graphs):
     res = solver.solve(b_d, tol=1e-12, maxit=200, gap=True)
     check_parity(res, orc.bicgstab(A, b, tol=1e-12, maxit=200), xs)
 
+
+@pytest.mark.parametrize("n", [2, 77, 1023, 5001, 20000])
+def test_csr_tma_sweeps_ragged(S, orc, n):
+    """CSR sweeps A/C through the TMA chunk ring (option csr_tma, default) and through
+    per-row loads: both bitwise vs the oracle for row counts below one chunk, odd (a
+    last half pair) and spanning several chunks per CTA, with periodic and automated
+    replacement."""
+    P = problems.csr_band(n, nnz_row=min(9, n), band=max(n - 1, 1) if n < 60 else 50, seed=n)
+    A = orc.csr(P.row_ptr, P.col, P.val)
+    xs = problems.x_star(n, 1)
+    b = orc.spmv(A, xs)
+    for tma in (1, 0):
+        solver = S.csr(n, P.row_ptr, P.col, P.val)
+        solver.set_option("csr_tma", tma)
+        b_d = solver.apply(torch.from_numpy(xs).cuda())
+        assert np.array_equal(b_d.cpu().numpy(), b)
+        res = solver.solve(b_d, tol=1e-12, maxit=80, rr_period=6, gap=True)
+        check_parity(res, orc.pbicgstab(A, b, tol=1e-12, maxit=80, rr_period=6), xs)
+        if n < 64:  # converges in <= n steps; no long noise-floor run
+            solver.close()
+            continue
+        solver.set_option("bench", 1)
+        solver.set_option("rr_auto", 1)
+        res = solver.solve(b_d, tol=0.0, maxit=30, gap=True)
+        ref = orc.pbicgstab(A, b, tol=0.0, maxit=30, bench=True, auto_rr=True)
+        check_parity(res, ref, xs, bitwise=False)
+        k = np.nonzero(ref.rnorm < 1e-16 * ref.rnorm[0])[0]
+        k = int(k[0]) if k.size else ref.iters + 1
+        assert np.array_equal(res.rnorm[:k], ref.rnorm[:k])
+        solver.close()
+
