@@ -27,7 +27,8 @@ def kernel_key(name: str):
     m = re.search(r"t_tile<\d, (\d+), ", name)
     if m:
         return MODES[int(m.group(1))]
-    for k, v in (("c_sweepA", "csr_sweepA"), ("c_sweepC", "csr_sweepC"), ("c_spmv_win<0>", "csr_spmvB"),
+    for k, v in (("c_sweep_tma<0", "csr_sweepA"), ("c_sweep_tma<1", "csr_sweepC"),
+                 ("c_sweepA", "csr_sweepA"), ("c_sweepC", "csr_sweepC"), ("c_spmv_win<0>", "csr_spmvB"),
                  ("c_spmv_win<1>", "csr_spmvD"), ("c_init1", "csr_init1"), ("c_init2", "csr_init2"),
                  ("c_apply", "csr_apply")):
         if name.startswith(k):
