@@ -27,6 +27,11 @@ struct CsrOp {
   const double* dinv;    // [n + 2H] ghosted Jacobi inverse diagonal (A3)
   int32_t bj;            // preconditioner block size: 1 Jacobi, 2..32 block Jacobi (A33)
   const double* binv;    // bj > 1: [n][bj] row j of its block's inverse (row-major)
+  // window SpMV operands, sliced ELL (SELL-32): rows in slices of 32 (one warp), slot k
+  // of the slice's 32 rows contiguous -- element (j, k) at ((j / 32) width + k) 32 + j % 32,
+  // so every load of a row's slots is the row's base + an immediate k * 32 elements
+  const double* sval;    // values (padding 0)
+  const int16_t* sdcol;  // column - row (|.| <= half bandwidth <= (WRS - 3 WTB) / 2)
 };
 
 // M^{-1} applied to the value v of row j (reading A3 / A33).  Jacobi: fl(dinv_j v).
@@ -621,35 +626,40 @@ __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __re
       const int64_t j = j0 + threadIdx.x + q * WNT;
       if (j >= R1) break;
       const int len = A.len ? A.len[j] : A.width;
+      const int rb = (int)((j + w.off) & (WRS - 1));  // ring position of row j's own column
+      const size_t sb = ((size_t)(j >> 5) * A.width) * 32 + (j & 31);  // slot 0 (SELL-32)
+      const double* __restrict__ av = A.sval + sb;    // advanced by whole groups, so
+      const int16_t* __restrict__ ac = A.sdcol + sb;  // every load is base + immediate
       double acc = 0.0;
       int p = 0;
       // groups of WIN_U slots: all of a group's matrix loads in flight before its adds
-      // (27 = the cfg5 row length: one group, +4.5% over groups of 9 -- measured)
-      for (; p + WIN_U <= len; p += WIN_U) {
+      // (27 = the cfg5 row length: one group, +4.5% over groups of 9 -- measured).
+      // Column = j + delta (int16), ring position (rb + delta) mod WRS.
+      for (; p + WIN_U <= len; p += WIN_U, av += WIN_U * 32, ac += WIN_U * 32) {
         int c[WIN_U];
         double a[WIN_U];
 #pragma unroll
         for (int k = 0; k < WIN_U; ++k) {
-          c[k] = __ldcs(A.col + (int64_t)(p + k) * A.n + j);
-          a[k] = __ldcs(A.val + (int64_t)(p + k) * A.n + j);
+          c[k] = __ldcs(ac + k * 32);
+          a[k] = __ldcs(av + k * 32);
         }
 #pragma unroll
-        for (int k = 0; k < WIN_U; ++k) acc = acc + a[k] * ring[(c[k] + w.off) & (WRS - 1)];
+        for (int k = 0; k < WIN_U; ++k) acc = acc + a[k] * ring[(rb + c[k]) & (WRS - 1)];
       }
-      for (; p + ELL_U <= len; p += ELL_U) {
+      for (; p + ELL_U <= len; p += ELL_U, av += ELL_U * 32, ac += ELL_U * 32) {
         int c[ELL_U];
         double a[ELL_U];
 #pragma unroll
         for (int k = 0; k < ELL_U; ++k) {
-          c[k] = __ldcs(A.col + (int64_t)(p + k) * A.n + j);
-          a[k] = __ldcs(A.val + (int64_t)(p + k) * A.n + j);
+          c[k] = __ldcs(ac + k * 32);
+          a[k] = __ldcs(av + k * 32);
         }
 #pragma unroll
-        for (int k = 0; k < ELL_U; ++k) acc = acc + a[k] * ring[(c[k] + w.off) & (WRS - 1)];
+        for (int k = 0; k < ELL_U; ++k) acc = acc + a[k] * ring[(rb + c[k]) & (WRS - 1)];
       }
-      for (; p < len; ++p) {
-        const int c = __ldcs(A.col + (int64_t)p * A.n + j);
-        acc = acc + __ldcs(A.val + (int64_t)p * A.n + j) * ring[(c + w.off) & (WRS - 1)];
+      for (; p < len; ++p, av += 32, ac += 32) {
+        const int c = __ldcs(ac);
+        acc = acc + __ldcs(av) * ring[(rb + c) & (WRS - 1)];
       }
       spmv_epi<WHICH, K>(A, V, j, acc, al, dacc);
     }

@@ -1718,6 +1718,24 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
       bw = d < 0 ? (-d > bw ? -d : bw) : (d > bw ? d : bw);
     }
   if (3LL * WTB + 2 * bw <= WRS) {
+    // the window SpMV's operands as sliced ELL (SELL-32) with 16-bit column offsets
+    // (|col - row| <= bw < 2^15): 10 bytes per slot, immediate-offset loads
+    const int64_t ns = (n + 31) / 32;
+    std::vector<double> sval((size_t)ns * width * 32, 0.0);
+    std::vector<int16_t> sdcol((size_t)ns * width * 32, 0);
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t q = 0; q < width; ++q) {
+        const size_t e = ((size_t)(i / 32) * width + q) * 32 + (i % 32);
+        sval[e] = eval[(size_t)q * n + i];
+        sdcol[e] = (int16_t)(ecol[(size_t)q * n + i] - i);
+      }
+    void *psv = nullptr, *psd = nullptr;
+    ST(dalloc(h, &psv, sval.size() * sizeof(double)));
+    ST(dalloc(h, &psd, sdcol.size() * sizeof(int16_t)));
+    CU(cudaMemcpy(psv, sval.data(), sval.size() * sizeof(double), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(psd, sdcol.data(), sdcol.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+    h->csr.sval = (const double*)psv;
+    h->csr.sdcol = (const int16_t*)psd;
     WinGeo& w = h->wg;
     w.bw = (int32_t)bw;
     w.lo = -h->H;
@@ -2345,25 +2363,28 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
   } else {
     const double slots = (double)h->csr.width;  // ELL width
     const double mat = 12.0 * slots * N;        // val (8) + col (4) per slot
+    // the iteration's SpMVs: window kernel with 16-bit column offsets when banded
+    const double matw = h->win_ok ? 10.0 * slots * N : mat;
     // block Jacobi: each kernel applying M^-1 reads its rows of the block inverse
     // instead of dinv (bj doubles instead of 1 per row)
     const double pb = h->csr.bj > 1 ? (h->csr.bj - 1) * 8.0 * N : 0.0;
     if (n == "sweepA") b = 15 * 8 * N + pb;  // read k,g,l,w,s,z,t,v,r,dinv; write g,s,l,z,n
-    else if (h->method == M_BICGSTAB && n == "spmvB") b = mat + 3 * 8 * N;  // mv in; s out; r^
-    else if (h->method == M_BICGSTAB && n == "spmvD") b = mat + 4 * 8 * N;  // nv in; y out; r, s
-    else if (n == "spmvB" || n == "spmvD" || n == "apply") b = mat + 2 * 8 * N;  // n|m in, out
+    else if (h->method == M_BICGSTAB && n == "spmvB") b = matw + 3 * 8 * N;  // mv in; s out; r^
+    else if (h->method == M_BICGSTAB && n == "spmvD") b = matw + 4 * 8 * N;  // nv in; y out; r, s
+    else if (n == "spmvB" || n == "spmvD") b = matw + 2 * 8 * N;  // n|m in, out
+    else if (n == "apply") b = mat + 2 * 8 * N;
     else if (n == "sweepC") b = 17 * 8 * N + pb;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w,m
     else if (n == "rr1") b = 2 * mat + 8 * 8 * N;
     else if (n == "rr2") b = 2 * mat + 7 * 8 * N;
     else if (n == "gap") b = mat + 3 * 8 * N;
-    else if (n == "iteration" && h->method == M_BICGSTAB) b = 2 * mat + 2 * 8 * N + 24 * 8 * N;
-    else if (n == "iteration" && h->method == M_PIPECG) b = mat + 21 * 8 * N;
+    else if (n == "iteration" && h->method == M_BICGSTAB) b = 2 * matw + 2 * 8 * N + 24 * 8 * N;
+    else if (n == "iteration" && h->method == M_PIPECG) b = matw + 21 * 8 * N;
     else if (n == "cl1") b = 6 * 8 * N;   // c_cl_p: read r,p,s,dinv; write p, M^-1 p
     else if (n == "cl2") b = 4 * 8 * N;   // c_cl_u: read r,s,dinv; write M^-1 q
     else if (n == "cl3") b = 9 * 8 * N;   // c_cl_x: read x,mv,nv,r,s,y,r^; write x,r
     else if (n == "pcg") b = 19 * 8 * N;  // c_pc: read n,z,q,s,p,x,r,u,w,dinv; write 9
     else if (n == "prec") b = 2 * 8 * N + pb + 8 * N;  // block Jacobi m = M^-1 w: w, binv rows; m
-    else if (n == "iteration") b = 2 * mat + 36 * 8 * N + 2 * pb;
+    else if (n == "iteration") b = 2 * matw + 36 * 8 * N + 2 * pb;
   }
   *bytes = b;
   return PBICG_OK;

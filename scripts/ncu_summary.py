@@ -12,8 +12,9 @@ import re
 ALG = {  # algorithmic bytes per row: passes x 8 B
     "sweepA": 88, "sweepC": 104, "rr1": 56, "rr2": 40, "gap": 24, "init1": 40, "init2": 24,
     "cl1": 48, "cl2": 16, "cl3": 56, "pcg": 128, "pcinit1": 32, "pcinit2": 16,
-    # CSR at 27 nnz/row (ELL val 8 + col 4 per slot = 324 B/row), Jacobi
-    "csr_sweepA": 120, "csr_sweepC": 136, "csr_spmvB": 340, "csr_spmvD": 340,
+    # CSR at 27 nnz/row, Jacobi: window SpMV SELL-32 val 8 + int16 offset 2 per slot
+    # (270 B/row); the int32 column-major ELL (12 per slot) for init / apply
+    "csr_sweepA": 120, "csr_sweepC": 136, "csr_spmvB": 286, "csr_spmvD": 286,
     "csr_init1": 372, "csr_init2": 364, "csr_apply": 340,
     # split stencil schedule: stand-alone SpMV (2 passes), point-wise sweeps
     "spmv": 16, "split_sweepA": 104, "split_sweepC": 120,
