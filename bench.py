@@ -382,7 +382,14 @@ def run_ours(args, rank, world):
                                  "hide behind" if args.schedule == 2 else SCHEDULES[args.method])
                                 if st.dim else
                                 "split 4-phase (CSR as ELL), reduction #1 overlapped"),
-                   "l2": "inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9),
+                   "l2": ("inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9)
+                          if 14 * 8 * n > 4 * 126e6 else
+                          "working set %.0f MB, about the 126 MB L2: not flushed (this "
+                          "config is L2-resident by construction)" % (14 * 8 * n / 1e6)),
+                   "timed_region": ("CUDA events around every kernel on the solver stream "
+                                    "(graphs off: per-kernel durations for the roofline); "
+                                    "e2e runs with CUDA graphs" if args.kernel_timing else
+                                    "CUDA graphs, no per-kernel events"),
                    "parallelism": f"z-slab x{world}" + (" (NCCL halo + rank-row all-gather)"
                                                         if world > 1 else ""),
                    "overlap": bool(args.overlap) if world > 1 else None,
