@@ -338,7 +338,11 @@ __global__ void __launch_bounds__(256, 3) c_sweepC(CsrOp A, Vecs V, Scal* __rest
 #define CST_NIN 12   // input vectors staged per chunk (max over the two sweeps)
 constexpr size_t kCstSmem = 64 + 2 * (size_t)CST_NIN * CST_R * sizeof(double);
 
-template <int SW, bool NRM>  // SW 0: sweep A (lines 5-12), 1: sweep C (lines 17-21)
+// BJ (block Jacobi, A33): dinv is not staged; (M^-1 v)_j = sum_k binv_jk v_{block+k},
+// ascending k from +0.0 (prec_row's order).  Blocks are aligned (b | CST_R) and a
+// block's rows are the row pairs of b/2 consecutive lanes of one warp, so its values
+// come by shuffles from those lanes' registers (old and new z, w alike).
+template <int SW, bool NRM, bool BJ>  // SW 0: sweep A (lines 5-12), 1: sweep C (lines 17-21)
 __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                         Dd* __restrict__ part, Hist h) {
   constexpr int K = SW == 0 ? (NRM ? 12 : 2) : (NRM ? 9 : 5);
@@ -349,20 +353,20 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
   const int tid = threadIdx.x;
   const double al = sc->alpha, be = sc->beta, om = sc->omega;
   const bool rr = SW == 0 && sc->use_rr != 0;
-  // staged inputs, in this order
-  //   A: w, z (pre-replacement), t, v, l, k, g, s, r, dinv [, replaced z]
+  // staged inputs, fixed slots (a bit of `mask` per staged vector)
+  //   A: w, z (pre-replacement), t, v, l, k, g, s, r, dinv, replaced z
   //   C: w, z, t, v, s, k, l, r, x, g, r^0, dinv
   const double* in[CST_NIN];
-  int nin;
+  unsigned mask;
   if (SW == 0) {
     const double* a[11] = {V.w0, V.z0, V.w1, V.z1, V.l, V.k, V.g, V.s, V.r, A.dinv, V.zrr};
-    nin = rr ? 11 : 10;
+    mask = (BJ ? 0x1FFu : 0x3FFu) | (rr ? 0x400u : 0u);
 #pragma unroll
     for (int v = 0; v < 11; ++v) in[v] = a[v];
     in[11] = nullptr;
   } else {
     const double* a[12] = {V.w0, V.z0, V.w1, V.z1, V.s, V.k, V.l, V.r, V.x, V.g, V.rh, A.dinv};
-    nin = 12;
+    mask = BJ ? 0x7FFu : 0xFFFu;
 #pragma unroll
     for (int v = 0; v < 12; ++v) in[v] = a[v];
   }
@@ -377,11 +381,32 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
     const int64_t j0 = c * CST_R;
     const int64_t rows = (A.n - j0) < CST_R ? (A.n - j0) : CST_R;
     const uint32_t bytes = (uint32_t)((rows * 8 + 15) & ~15LL);  // vectors carry 2 slack rows
-    mbar_arrive_expect_tx(&bar[slot], bytes * (uint32_t)nin);
+    mbar_arrive_expect_tx(&bar[slot], bytes * (uint32_t)__popc(mask));
 #pragma unroll
     for (int v = 0; v < CST_NIN; ++v)  // unrolled: `in` stays in registers
-      if (v < nin)
+      if ((mask >> v) & 1u)
         bulk_g2s(buf + ((size_t)slot * CST_NIN + v) * CST_R, in[v] + j0, bytes, &bar[slot]);
+  };
+  // block Jacobi: M^-1 of the vector whose rows j, j+1 this thread holds (v0, v1); every
+  // lane of the warp calls it (shuffles), idle lanes with zeros
+  auto bjpair = [&](double v0, double v1, int64_t j, bool act, double& o0, double& o1) {
+    const int lane = tid & 31;
+    const int base = lane & ~(A.bj / 2 - 1);  // lane holding the block's rows 0, 1
+    const double* __restrict__ r0 = A.binv + (act ? j : 0) * A.bj;  // 16-byte aligned rows
+    const double* __restrict__ r1 = r0 + A.bj;
+    double a = 0.0, c = 0.0;
+    for (int k = 0; k < A.bj; k += 2) {
+      const double e0 = __shfl_sync(0xffffffffu, v0, base + k / 2);
+      const double e1 = __shfl_sync(0xffffffffu, v1, base + k / 2);
+      const double2 p = act ? __ldg(reinterpret_cast<const double2*>(r0 + k)) : make_double2(0, 0);
+      const double2 q = act ? __ldg(reinterpret_cast<const double2*>(r1 + k)) : make_double2(0, 0);
+      a = a + p.x * e0;
+      a = a + p.y * e1;
+      c = c + q.x * e0;
+      c = c + q.y * e1;
+    }
+    o0 = a;
+    o1 = c;
   };
   Dd acc[K];
 #pragma unroll
@@ -395,21 +420,29 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
     mbar_wait(&bar[slot], (ph >> slot) & 1u);
     ph ^= 1u << slot;
     const int64_t j = c * CST_R + 2 * tid;
-    if (j < A.n) {
-      const bool valid1 = j + 1 < A.n;
-      const double* B = buf + (size_t)slot * CST_NIN * CST_R + 2 * tid;
-      double x0[CST_NIN], x1[CST_NIN];
+    const bool act = j < A.n;  // (block Jacobi: n % b == 0, blocks all-in or all-out)
+    const bool valid1 = j + 1 < A.n;
+    const double* B = buf + (size_t)slot * CST_NIN * CST_R;
+    double x0[CST_NIN], x1[CST_NIN];
 #pragma unroll
-      for (int v = 0; v < CST_NIN; ++v) {
-        if (v < nin) {
-          const double2 q = *reinterpret_cast<const double2*>(B + (size_t)v * CST_R);
-          x0[v] = q.x;
-          x1[v] = q.y;
-        } else {
-          x0[v] = x1[v] = 0.0;
-        }
+    for (int v = 0; v < CST_NIN; ++v) {
+      if (act && ((mask >> v) & 1u)) {
+        const double2 q = *reinterpret_cast<const double2*>(B + (size_t)v * CST_R + 2 * tid);
+        x0[v] = q.x;
+        x1[v] = q.y;
+      } else {
+        x0[v] = x1[v] = 0.0;
       }
-      double o0[5], o1[5];
+    }
+    // M^-1 of w and z (block Jacobi: by shuffles; n % b == 0, so an active thread's
+    // second row is valid)
+    double mw[2] = {0.0, 0.0}, nz[2] = {0.0, 0.0};
+    if (BJ) {
+      bjpair(x0[0], x1[0], j, act, mw[0], mw[1]);
+      bjpair(x0[1], x1[1], j, act, nz[0], nz[1]);
+    }
+    double o0[5] = {0, 0, 0, 0, 0}, o1[5] = {0, 0, 0, 0, 0};
+    if (act) {
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         const double* xv = e == 0 ? x0 : x1;
@@ -418,7 +451,7 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
         if (SW == 0) {  // identical expressions to c_sweepA
           const double wc = xv[0], zc = xv[1], t = xv[2], v = xv[3], lj = xv[4];
           const double dj = xv[9];
-          const double m = dj * wc, n = dj * zc;  // m_i, n_{i-1}
+          const double m = BJ ? mw[e] : dj * wc, n = BJ ? nz[e] : dj * zc;  // m_i, n_{i-1}
           const double zo = rr ? xv[10] : zc;
           const double gn = xv[5] + be * (xv[6] - om * lj);
           const double sn = wc + be * (xv[7] - om * zo);
@@ -434,11 +467,12 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
             c_nrm(acc[8 % K], ln); c_nrm(acc[9 % K], zn); c_nrm(acc[10 % K], q);
             c_nrm(acc[11 % K], y);
           }
-          o[0] = gn; o[1] = sn; o[2] = ln; o[3] = zn; o[4] = dj * zn;  // n_i (line 13)
+          o[0] = gn; o[1] = sn; o[2] = ln; o[3] = zn;
+          o[4] = BJ ? 0.0 : dj * zn;  // n_i (line 13); block Jacobi below
         } else {  // identical expressions to c_sweepC
           const double wc = xv[0], zc = xv[1], t = xv[2], v = xv[3], sj = xv[4];
           const double dj = xv[11];
-          const double m = dj * wc, n = dj * zc;  // m_i, n_i
+          const double m = BJ ? mw[e] : dj * wc, n = BJ ? nz[e] : dj * zc;  // m_i, n_i
           const double u = xv[5] - al * xv[6];
           const double q = xv[7] - al * sj;
           const double y = wc - al * zc;
@@ -457,9 +491,13 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
             c_nrm(acc[5 % K], xj); c_nrm(acc[6 % K], u); c_nrm(acc[7 % K], n);
             c_nrm(acc[8 % K], v);
           }
-          o[0] = xn; o[1] = rn; o[2] = kn; o[3] = wn; o[4] = dj * wn;  // m_{i+1} (line 22)
+          o[0] = xn; o[1] = rn; o[2] = kn; o[3] = wn;
+          o[4] = BJ ? 0.0 : dj * wn;  // m_{i+1} (line 22); block Jacobi below
         }
       }
+    }
+    if (BJ) bjpair(o0[3], o1[3], j, act, o0[4], o1[4]);  // M^-1 of the new z (A) / w (C)
+    if (act) {
       double* out[5];
       if (SW == 0) {
         out[0] = V.g; out[1] = V.s; out[2] = V.l; out[3] = V.z0; out[4] = V.nv;

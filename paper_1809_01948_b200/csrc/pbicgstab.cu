@@ -420,12 +420,18 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SWEEPA: {
       LaunchScope ls(h, K_SWEEPA);
-      if (h->csr.bj > 1) {
+      if (h->cst_ok && h->cst_on && h->csr.bj <= 4) {  // TMA chunk ring (Jacobi, b <= 4)
+        const int g = h->cst_grid;
+        if (h->csr.bj > 1) {
+          if (h->auto_rr) c_sweep_tma<0, true, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          else c_sweep_tma<0, false, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        } else {
+          if (h->auto_rr) c_sweep_tma<0, true, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          else c_sweep_tma<0, false, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        }
+      } else if (h->csr.bj > 1) {
         if (h->auto_rr) c_sweepA<true, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
         else c_sweepA<false, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      } else if (h->cst_ok && h->cst_on) {
-        if (h->auto_rr) c_sweep_tma<0, true><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_sweep_tma<0, false><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
       } else {
         if (h->auto_rr) c_sweepA<true, false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
         else c_sweepA<false, false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
@@ -442,12 +448,18 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     case PH_SWEEPC: {
       {
         LaunchScope ls(h, K_SWEEPC);
-        if (h->csr.bj > 1) {
+        if (h->cst_ok && h->cst_on && h->csr.bj <= 4) {  // TMA chunk ring (Jacobi, b <= 4)
+          const int g = h->cst_grid;
+          if (h->csr.bj > 1) {
+            if (h->auto_rr) c_sweep_tma<1, true, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+            else c_sweep_tma<1, false, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          } else {
+            if (h->auto_rr) c_sweep_tma<1, true, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+            else c_sweep_tma<1, false, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          }
+        } else if (h->csr.bj > 1) {
           if (h->auto_rr) c_sweepC<true, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
           else c_sweepC<false, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        } else if (h->cst_ok && h->cst_on) {
-          if (h->auto_rr) c_sweep_tma<1, true><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-          else c_sweep_tma<1, false><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
         } else {
           if (h->auto_rr) c_sweepC<true, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
           else c_sweepC<false, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
@@ -1755,12 +1767,21 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     h->win_ok = e == cudaSuccess;
     cudaGetLastError();
   }
-  if (h->csr.bj <= 1) {  // TMA-staged sweeps: one CTA per SM, two-stage chunk ring
+  // TMA-staged sweeps: one CTA per SM, two-stage chunk ring.  Block Jacobi b <= 4 only:
+  // measured on cfg5 (it/s, per-row kernel -> TMA ring) b = 2: 781 -> 834, b = 4: 757 ->
+  // 761, b = 8: 673 -> 570 (the per-thread gathers of two b-wide inverse rows lack the
+  // per-row kernel's 24 warps per SM of memory parallelism), b = 16, 32 likewise slower
+  if (h->csr.bj <= 4) {
     const auto SM = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    cudaError_t e = cudaFuncSetAttribute(c_sweep_tma<0, false>, SM, (int)kCstSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<0, true>, SM, (int)kCstSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, false>, SM, (int)kCstSmem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, true>, SM, (int)kCstSmem);
+    const int sm = (int)kCstSmem;
+    cudaError_t e = cudaFuncSetAttribute(c_sweep_tma<0, false, false>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<0, true, false>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, false, false>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, true, false>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<0, false, true>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<0, true, true>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, false, true>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, true, true>, SM, sm);
     const int64_t nch = (n + CST_R - 1) / CST_R;
     h->cst_grid = (int)(nch < h->num_sm ? nch : h->num_sm);
     h->cst_ok = e == cudaSuccess && h->H % 2 == 0;  // 16-byte aligned row pairs

@@ -891,6 +891,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
           if (e >= 0) xf_store<VEC, 1>(bv, svs, e, o);
         }
       }
+      fence_proxy_async_smem();  // the slot is re-staged by TMA after a later barrier
     };
     if (tid == 0) {
       for (int m = 0; m < 3 && m < nsv; ++m) stage_sv((svc + m) % 3, z0 - 1 + m);

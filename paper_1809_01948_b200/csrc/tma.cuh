@@ -58,3 +58,10 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+
+// Order this thread's generic-proxy shared-memory writes before later async-proxy
+// (TMA) accesses of the same bytes: executed by the writers, then a CTA barrier, then
+// the bulk copy that reuses the buffer.
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
