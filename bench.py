@@ -269,8 +269,7 @@ def run_ours(args, rank, world):
     S.set_option("overlap", args.overlap)
     if args.schedule:
         S.set_option("schedule", args.schedule)
-    if isinstance(st, CsrShape):
-        S.set_option("csr_tma", args.csr_tma)
+    S.set_option("csr_tma", args.csr_tma)  # CSR sweeps / the stencil split schedule's sweeps
     if world > 1:
         S.set_option("transport", args.transport)  # collective: every rank sets it
     gap = bool(args.gap)
@@ -475,7 +474,8 @@ def main():
                     help="P > 1: dot-product reductions overlap the halo exchange / SpMV (1) "
                          "or block the compute stream (0)")
     ap.add_argument("--csr-tma", type=int, default=1,
-                    help="CSR: TMA-staged sweeps (1, default) or per-row loads (0)")
+                    help="point-wise sweeps (CSR; stencil --schedule 2) on the TMA chunk ring "
+                         "(1, default) or per-row loads (0)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--kernel-timing", type=int, default=1,
                     help="1: CUDA events around every kernel in the timed region (graphs off); "

@@ -342,11 +342,18 @@ constexpr size_t kCstSmem = 64 + 2 * (size_t)CST_NIN * CST_R * sizeof(double);
 // ascending k from +0.0 (prec_row's order).  Blocks are aligned (b | CST_R) and a
 // block's rows are the row pairs of b/2 consecutive lanes of one warp, so its values
 // come by shuffles from those lanes' registers (old and new z, w alike).
-template <int SW, bool NRM, bool BJ>  // SW 0: sweep A (lines 5-12), 1: sweep C (lines 17-21)
+// STS: the stencil split schedule (option schedule 2; k_sweepA2 / k_sweepC2's steps):
+// scalar dinv (dsc), w and z double-buffered by iteration parity, t, v in tv, vv, and no
+// M^-1 output (the stand-alone tile SpMVs apply the Jacobi scaling per leg).
+template <int SW, bool NRM, bool BJ, bool STS = false>  // SW 0: sweep A (l. 5-12), 1: C (l. 17-21)
 __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* __restrict__ sc,
-                                                        Dd* __restrict__ part, Hist h) {
+                                                        Dd* __restrict__ part, Hist h,
+                                                        double dsc) {
   constexpr int K = SW == 0 ? (NRM ? 12 : 2) : (NRM ? 9 : 5);
+  constexpr int NOUT = STS ? 4 : 5;
+  static_assert(!(STS && (BJ || NRM)), "split stencil sweeps: Jacobi, no bound norms");
   if (sc->done) return;
+  const int it = sc->iter;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
   double* buf = reinterpret_cast<double*>(smem_raw + 64);
@@ -358,17 +365,27 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
   //   C: w, z, t, v, s, k, l, r, x, g, r^0, dinv
   const double* in[CST_NIN];
   unsigned mask;
+  const bool odd = (it & 1) != 0;
   if (SW == 0) {
-    const double* a[11] = {V.w0, V.z0, V.w1, V.z1, V.l, V.k, V.g, V.s, V.r, A.dinv, V.zrr};
-    mask = (BJ ? 0x1FFu : 0x3FFu) | (rr ? 0x400u : 0u);
+    const double* wv = STS ? (odd ? V.w1 : V.w0) : V.w0;  // w_i
+    const double* zv = STS ? (odd ? V.z0 : V.z1) : V.z0;  // z_{i-1} pre-replacement
+    const double* a[11] = {wv, zv, STS ? V.tv : V.w1, STS ? V.vv : V.z1, V.l, V.k, V.g, V.s,
+                           V.r, A.dinv, V.zrr};
+    mask = (BJ || STS ? 0x1FFu : 0x3FFu) | (rr ? 0x400u : 0u);
 #pragma unroll
     for (int v = 0; v < 11; ++v) in[v] = a[v];
     in[11] = nullptr;
   } else {
-    const double* a[12] = {V.w0, V.z0, V.w1, V.z1, V.s, V.k, V.l, V.r, V.x, V.g, V.rh, A.dinv};
-    mask = BJ ? 0x7FFu : 0xFFFu;
+    const double* wv = STS ? (odd ? V.w1 : V.w0) : V.w0;  // w_i
+    const double* zv = STS ? (odd ? V.z1 : V.z0) : V.z0;  // z_i
+    const double* a[12] = {wv, zv, STS ? V.tv : V.w1, STS ? V.vv : V.z1, V.s, V.k, V.l, V.r,
+                           V.x, V.g, V.rh, A.dinv};
+    mask = BJ || STS ? 0x7FFu : 0xFFFu;
 #pragma unroll
     for (int v = 0; v < 12; ++v) in[v] = a[v];
+    // SpMV_D may run before the finalize step advances iter (P ranks, overlap): tell it
+    // where w_{i+1} is
+    if (STS && blockIdx.x == 0 && tid == 0) sc->spd_par = (it + 1) & 1;
   }
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -450,7 +467,7 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
         if (e == 1 && !valid1) break;
         if (SW == 0) {  // identical expressions to c_sweepA
           const double wc = xv[0], zc = xv[1], t = xv[2], v = xv[3], lj = xv[4];
-          const double dj = xv[9];
+          const double dj = STS ? dsc : xv[9];
           const double m = BJ ? mw[e] : dj * wc, n = BJ ? nz[e] : dj * zc;  // m_i, n_{i-1}
           const double zo = rr ? xv[10] : zc;
           const double gn = xv[5] + be * (xv[6] - om * lj);
@@ -471,7 +488,7 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
           o[4] = BJ ? 0.0 : dj * zn;  // n_i (line 13); block Jacobi below
         } else {  // identical expressions to c_sweepC
           const double wc = xv[0], zc = xv[1], t = xv[2], v = xv[3], sj = xv[4];
-          const double dj = xv[11];
+          const double dj = STS ? dsc : xv[11];
           const double m = BJ ? mw[e] : dj * wc, n = BJ ? nz[e] : dj * zc;  // m_i, n_i
           const double u = xv[5] - al * xv[6];
           const double q = xv[7] - al * sj;
@@ -500,12 +517,16 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
     if (act) {
       double* out[5];
       if (SW == 0) {
-        out[0] = V.g; out[1] = V.s; out[2] = V.l; out[3] = V.z0; out[4] = V.nv;
+        out[0] = V.g; out[1] = V.s; out[2] = V.l;
+        out[3] = STS ? (odd ? V.z1 : V.z0) : V.z0;  // z_i
+        out[4] = V.nv;
       } else {
-        out[0] = V.x; out[1] = V.r; out[2] = V.k; out[3] = V.w0; out[4] = V.mv;
+        out[0] = V.x; out[1] = V.r; out[2] = V.k;
+        out[3] = STS ? (odd ? V.w0 : V.w1) : V.w0;  // w_{i+1}
+        out[4] = V.mv;
       }
 #pragma unroll
-      for (int k = 0; k < 5; ++k) {
+      for (int k = 0; k < NOUT; ++k) {
         if (valid1) {
           __stcs(reinterpret_cast<double2*>(out[k] + j), make_double2(o0[k], o1[k]));
         } else {

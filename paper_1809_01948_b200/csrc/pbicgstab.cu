@@ -349,11 +349,19 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
     case PH_PCI2: { LaunchScope ls(h, K_INIT); launch_tile<DIM, TM_PCI2>(h); } break;
     case PH_SWEEPA2: {
       LaunchScope ls(h, K_SWEEPA);
-      k_sweepA2<DIM><<<h->grid_a2, 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+      if (h->cst_ok && h->cst_on)  // TMA chunk ring (option csr_tma covers it too)
+        c_sweep_tma<0, false, false, true><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(
+            h->csr, h->V, h->scal, h->part, h->hist, g.dinv);
+      else
+        k_sweepA2<DIM><<<h->grid_a2, 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SWEEPC2: {
       LaunchScope ls(h, K_SWEEPC);
-      k_sweepC2<DIM><<<h->grid_c2, 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
+      if (h->cst_ok && h->cst_on)
+        c_sweep_tma<1, false, false, true><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(
+            h->csr, h->V, h->scal, h->part, h->hist, g.dinv);
+      else
+        k_sweepC2<DIM><<<h->grid_c2, 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SPB: { LaunchScope ls(h, K_SPMVB); launch_tile<DIM, TM_SPB>(h); } break;
     case PH_SPD: { LaunchScope ls(h, K_SPMVD); launch_tile<DIM, TM_SPD>(h); } break;
@@ -423,11 +431,11 @@ void launch_csr(pbicg_ctx* h, Phase p) {
       if (h->cst_ok && h->cst_on && h->csr.bj <= 4) {  // TMA chunk ring (Jacobi, b <= 4)
         const int g = h->cst_grid;
         if (h->csr.bj > 1) {
-          if (h->auto_rr) c_sweep_tma<0, true, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-          else c_sweep_tma<0, false, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          if (h->auto_rr) c_sweep_tma<0, true, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
+          else c_sweep_tma<0, false, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
         } else {
-          if (h->auto_rr) c_sweep_tma<0, true, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-          else c_sweep_tma<0, false, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+          if (h->auto_rr) c_sweep_tma<0, true, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
+          else c_sweep_tma<0, false, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
         }
       } else if (h->csr.bj > 1) {
         if (h->auto_rr) c_sweepA<true, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
@@ -451,11 +459,11 @@ void launch_csr(pbicg_ctx* h, Phase p) {
         if (h->cst_ok && h->cst_on && h->csr.bj <= 4) {  // TMA chunk ring (Jacobi, b <= 4)
           const int g = h->cst_grid;
           if (h->csr.bj > 1) {
-            if (h->auto_rr) c_sweep_tma<1, true, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-            else c_sweep_tma<1, false, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+            if (h->auto_rr) c_sweep_tma<1, true, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
+            else c_sweep_tma<1, false, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
           } else {
-            if (h->auto_rr) c_sweep_tma<1, true, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-            else c_sweep_tma<1, false, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+            if (h->auto_rr) c_sweep_tma<1, true, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
+            else c_sweep_tma<1, false, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
           }
         } else if (h->csr.bj > 1) {
           if (h->auto_rr) c_sweepC<true, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
@@ -1496,6 +1504,18 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
     { const int b0 = h->block; h->block = 256;
       h->grid_a2 = occ_grid(h, k_sweepA2<2>, (h->n_local + 255) / 256);
       h->grid_c2 = occ_grid(h, k_sweepC2<2>, (h->n_local + 255) / 256); h->block = b0; }
+  }
+  {  // split schedule (option schedule 2): point-wise sweeps on the TMA chunk ring
+    const auto SM = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e = cudaFuncSetAttribute(c_sweep_tma<0, false, false, true>, SM, (int)kCstSmem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(c_sweep_tma<1, false, false, true>, SM, (int)kCstSmem);
+    h->csr.n = h->n_local;  // the kernel's row count (no matrix on a stencil handle)
+    h->csr.bj = 1;
+    const int64_t nch = (h->n_local + CST_R - 1) / CST_R;
+    h->cst_grid = (int)(nch < h->num_sm ? nch : h->num_sm);
+    h->cst_ok = e == cudaSuccess && h->H % 2 == 0;  // 16-byte aligned row pairs
+    cudaGetLastError();
   }
   setup_tile(h);
   if (bj > 1 && (!h->tile_ok || h->tile_seg))

@@ -301,3 +301,20 @@ def test_csr_tma_sweeps_ragged(S, orc, n):
         assert np.array_equal(res.rnorm[:k], ref.rnorm[:k])
         solver.close()
 
+
+@pytest.mark.parametrize("dim,nx,ny,nz,kind", [
+    (3, 20, 11, 12, "cd3"),   # ghost offset even: point-wise sweeps on the TMA chunk ring
+    (3, 9, 6, 7, "cd3"),      # nx (ny + 1) odd: 16-byte misaligned rows -> line kernels
+    (2, 333, 41, 1, "cd2"), (3, 64, 32, 40, "cd3")])
+def test_split_schedule_sweep_paths(S, orc, dim, nx, ny, nz, kind):
+    """Option schedule 2 (the paper's split pipeline): sweeps A/C through the TMA chunk
+    ring (csr_tma 1, where the rows are 16-byte aligned) and through the line kernels
+    (csr_tma 0) give the oracle's iterates bitwise, with periodic replacement."""
+    solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of(kind))
+    solver.set_option("schedule", 2)
+    ref = orc.pbicgstab(A, b, tol=1e-11, maxit=150, rr_period=7)
+    for tma in (1, 0):
+        solver.set_option("csr_tma", tma)
+        res = solver.solve(b_d, tol=1e-11, maxit=150, rr_period=7, gap=True)
+        check_parity(res, ref, xs)
+
