@@ -187,7 +187,10 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *                each reducing kernel stores its rank's Dot2 pairs into every rank's
  *                receive buffer over NVLink (CUDA IPC mappings exchanged once with an
  *                NCCL all-gather) and raises a flag; the finalize kernel waits for the
- *                P flags.  No collective launch per reduction.  Collective option for
+ *                P flags.  No collective launch per reduction.  Stencil, fused
+ *                schedule: sweeps A and C also store their boundary planes of z_i and
+ *                w_{i+1} into the neighbours' ghost planes (published by the same
+ *                flags), so no halo exchange is enqueued for them.  Collective option for
  *                NCCL ranks (all call it with the same value); <= 8 ranks
  *   "rr_auto"    1 => automated residual replacement: the run-time bound
  *                f^r_i on the residual gap (eq:DDr_bound) is propagated on the device

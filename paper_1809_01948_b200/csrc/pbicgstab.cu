@@ -123,6 +123,11 @@ struct pbicg_ctx {
   std::vector<Dd*> p2p_recv_tab;             // every rank's buffer, in this address space
   std::vector<unsigned long long*> p2p_flag_tab;
   std::vector<void*> ipc_opened;             // peer mappings to close
+  // transport 1, fused schedule: neighbours' ghost planes of w0, w1, z0, z1 ([q][0]:
+  // the lower neighbour's upper ghost, [q][1]: the upper neighbour's lower ghost)
+  double* peer_ghost[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr},
+                              {nullptr, nullptr}};
+  int64_t halo_ops = 0;  // halo exchanges enqueued (copies / NCCL groups), for tests
   int32_t last_nrr = 0;                      // replacements of the last solve
   std::map<std::tuple<int, int, int>, cudaGraphExec_t> graphs;
   std::vector<TimedLaunch> pending;
@@ -573,10 +578,16 @@ void comm_reduce(const Members& G, bool on_side) {
   }
 }
 
+// the fused schedule's z / w halos travel inside the tile sweeps (transport 1)
+bool fused_halo(const pbicg_ctx* h) {
+  return h->p2p && h->kind == KIND_STENCIL && h->tile_ok && h->tile_on && h->schedule != 2;
+}
+
 // nearest-neighbour ghost exchange of halo_n rows per side for each vector
 void comm_halo(const Members& G, std::initializer_list<VecSel> sels) {
   pbicg_ctx* h0 = G[0];
   if (h0->nranks == 1) return;
+  h0->halo_ops++;
   if (h0->comm == COMM_NCCL) {
     pbicg_ctx* h = h0;
     auto& api = nccl_api();
@@ -847,7 +858,8 @@ void enq_iter(const Members& G, bool with_rr, int par) {
       } else {
         comm_reduce(G, false);
       }
-      comm_halo(G, {par ? SZ1 : SZ0});  // z_i for sweep C's stencil
+      // z_i for sweep C's stencil (transport 1: sweep A stored it in the neighbours)
+      if (!fused_halo(h0)) comm_halo(G, {par ? SZ1 : SZ0});
       if (ov) join_reduce(G);
       each_fin(G, F_SWEEPA);
     }
@@ -855,7 +867,7 @@ void enq_iter(const Members& G, bool with_rr, int par) {
     if (dist && !with_rr && h0->overlap) {
       // reduction #2 || halo of w_{i+1} (no replacement can rewrite w this iteration)
       fork_reduce(G);
-      comm_halo(G, {par ? SW0 : SW1});
+      if (!fused_halo(h0)) comm_halo(G, {par ? SW0 : SW1});
       join_reduce(G);
       each_fin(G, F_SWEEPC);
       if (h0->gap_on) {
@@ -874,7 +886,8 @@ void enq_iter(const Members& G, bool with_rr, int par) {
       each(G, PH_RR2);
       reduce_fin(G, F_RR2);
     }
-    if (dist) comm_halo(G, {par ? SW0 : SW1});  // w_{i+1}
+    // w_{i+1} (transport 1: stored by sweep C in the neighbours unless replaced)
+    if (dist && (with_rr || !fused_halo(h0))) comm_halo(G, {par ? SW0 : SW1});
   } else {
     // split 4-phase schedule; reduction #1 overlaps the halo + spmv_B
     each(G, PH_SWEEPA);
@@ -1223,6 +1236,10 @@ pbicg_status entry_sync(pbicg_ctx* h) {
 }
 
 // Buffers of the peer-memory transport for one rank (zeroed flags and epoch).
+double* ghost_vec(pbicg_ctx* h, int q) {  // 0 w0, 1 w1, 2 z0, 3 z1
+  return q == 0 ? h->V.w0 : q == 1 ? h->V.w1 : q == 2 ? h->V.z0 : h->V.z1;
+}
+
 pbicg_status p2p_alloc(pbicg_ctx* h) {
   if (h->p2p_buf) return PBICG_OK;
   void *b = nullptr, *f = nullptr, *e = nullptr;
@@ -1246,12 +1263,18 @@ pbicg_status p2p_setup(const Members& G) {
     return fail(h, PBICG_EINVAL, "transport 1 (peer memory) supports up to 8 ranks");
   if (h->comm == COMM_LOOP) {
     for (pbicg_ctx* m : G) ST(p2p_alloc(m));
-    for (pbicg_ctx* m : G) {
+    for (size_t r = 0; r < G.size(); ++r) {
+      pbicg_ctx* m = G[r];
       m->p2p_recv_tab.clear();
       m->p2p_flag_tab.clear();
       for (pbicg_ctx* q : G) {
         m->p2p_recv_tab.push_back(q->p2p_buf);
         m->p2p_flag_tab.push_back(q->p2p_flags);
+      }
+      for (int q = 0; q < 4; ++q) {
+        m->peer_ghost[q][0] = r > 0 ? ghost_vec(G[r - 1], q) + G[r - 1]->n_local : nullptr;
+        m->peer_ghost[q][1] = r + 1 < G.size() ? ghost_vec(G[r + 1], q) - G[r + 1]->halo_n
+                                               : nullptr;
       }
     }
     return PBICG_OK;
@@ -1260,16 +1283,25 @@ pbicg_status p2p_setup(const Members& G) {
   if (!h->p2p_recv_tab.empty()) return PBICG_OK;
   ST(p2p_alloc(h));
   const int P = h->nranks;
-  cudaIpcMemHandle_t mine[2];
-  CU(cudaIpcGetMemHandle(&mine[0], h->p2p_buf));
-  CU(cudaIpcGetMemHandle(&mine[1], h->p2p_flags));
-  const size_t hb = sizeof(mine);
+  // per rank: the reduction buffer and flags, the allocations of w0, w1, z0, z1 (ghost
+  // planes written by the neighbours' sweeps), and the geometry to address them
+  struct Blob {
+    cudaIpcMemHandle_t buf, flags, vec[4];
+    int64_t n_local, halo_n, H;
+  } mine{};
+  CU(cudaIpcGetMemHandle(&mine.buf, h->p2p_buf));
+  CU(cudaIpcGetMemHandle(&mine.flags, h->p2p_flags));
+  for (int q = 0; q < 4; ++q) CU(cudaIpcGetMemHandle(&mine.vec[q], ghost_vec(h, q) - h->H));
+  mine.n_local = h->n_local;
+  mine.halo_n = h->halo_n;
+  mine.H = h->H;
+  const size_t hb = sizeof(Blob);
   void *dsend = nullptr, *drecv = nullptr;
   ST(dalloc(h, &dsend, hb));
   ST(dalloc(h, &drecv, hb * P));
-  CU(cudaMemcpy(dsend, mine, hb, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(dsend, &mine, hb, cudaMemcpyHostToDevice));
   NC(nccl_api().AllGather(dsend, drecv, hb, ncclChar, h->nccl_halo, h->stream));
-  std::vector<cudaIpcMemHandle_t> all((size_t)2 * P);
+  std::vector<Blob> all((size_t)P);
   CU(cudaStreamSynchronize(h->stream));
   CU(cudaMemcpy(all.data(), drecv, hb * P, cudaMemcpyDeviceToHost));
   for (int q = 0; q < P; ++q) {
@@ -1279,15 +1311,35 @@ pbicg_status p2p_setup(const Members& G) {
       continue;
     }
     void *pb = nullptr, *pf = nullptr;
-    CU(cudaIpcOpenMemHandle(&pb, all[(size_t)2 * q], cudaIpcMemLazyEnablePeerAccess));
+    CU(cudaIpcOpenMemHandle(&pb, all[q].buf, cudaIpcMemLazyEnablePeerAccess));
     h->ipc_opened.push_back(pb);
-    CU(cudaIpcOpenMemHandle(&pf, all[(size_t)2 * q + 1], cudaIpcMemLazyEnablePeerAccess));
+    CU(cudaIpcOpenMemHandle(&pf, all[q].flags, cudaIpcMemLazyEnablePeerAccess));
     h->ipc_opened.push_back(pf);
     h->p2p_recv_tab.push_back((Dd*)pb);
     h->p2p_flag_tab.push_back((unsigned long long*)pf);
+    if (h->kind == KIND_STENCIL && (q == h->rank - 1 || q == h->rank + 1)) {
+      const int side = q == h->rank - 1 ? 0 : 1;
+      for (int v = 0; v < 4; ++v) {
+        void* pv = nullptr;
+        CU(cudaIpcOpenMemHandle(&pv, all[q].vec[v], cudaIpcMemLazyEnablePeerAccess));
+        h->ipc_opened.push_back(pv);
+        double* row0 = (double*)pv + all[q].H;  // the peer's local row 0
+        h->peer_ghost[v][side] = side == 0 ? row0 + all[q].n_local : row0 - all[q].halo_n;
+      }
+    }
   }
   return PBICG_OK;
 }
+
+// point the tile sweeps' ghost stores at the neighbours (transport 1) or nowhere
+void set_peer_halo(pbicg_ctx* h, bool on) {
+  for (int b = 0; b < 2; ++b)
+    for (int sd = 0; sd < 2; ++sd) {
+      h->V.hw[b][sd] = on ? h->peer_ghost[b][sd] : nullptr;      // w0, w1
+      h->V.hz[b][sd] = on ? h->peer_ghost[2 + b][sd] : nullptr;  // z0, z1
+    }
+}
+
 
 pbicg_status nccl_setup(pbicg_ctx* h, const pbicg_dist* d) {
   auto& api = nccl_api();
@@ -2179,6 +2231,7 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
     }
     for (pbicg_ctx* m : members(h)) {
       m->p2p = (int)value;
+      set_peer_halo(m, value == 1);
       destroy_graphs(m);
     }
     return PBICG_OK;
@@ -2349,6 +2402,12 @@ pbicg_status pbicgstab_kernel_time(pbicg_handle h, const char* name, int64_t* la
                                    int32_t reset) {
   if (!h || !name) return fail(h, PBICG_EINVAL, "NULL argument");
   std::string n(name);
+  if (n == "halo") {  // halo exchanges enqueued (not kernels of this library)
+    if (launches) *launches = h->halo_ops;
+    if (ms) *ms = NAN;
+    if (reset) h->halo_ops = 0;
+    return PBICG_OK;
+  }
   int64_t L = 0;
   double t = 0;
   bool found = false;

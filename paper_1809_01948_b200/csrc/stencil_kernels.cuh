@@ -35,6 +35,12 @@ struct Vecs {
   double *w0, *w1, *z0, *z1, *zrr;
   double *nv, *mv;  // CSR path: n = M^-1 z and m = M^-1 w, inputs of the window SpMVs
   double *tv, *vv;  // stencil split schedule: stored t_i = A M^-1 w_i, v_i = A M^-1 z_i
+  // peer-memory transport (option transport 1), fused schedule: where sweep A stores its
+  // first / last plane of z (hz[b]: buffer z_b) and sweep C of w (hw[b]: buffer w_b) in
+  // the lower ([0]: its upper ghost plane) and upper ([1]: its lower ghost plane)
+  // neighbours' memory; nullptr = no neighbour / no fused halo
+  double* hz[2][2];
+  double* hw[2][2];
 };
 
 template <int DIM>

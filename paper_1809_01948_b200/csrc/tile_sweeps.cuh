@@ -780,6 +780,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
 #pragma unroll
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   const int r = 2 * tid;  // this thread's row pair within the tile
+  bool remote = false;    // this thread stored into a peer's ghost plane
 
   for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
     const int col = u % g.ncols, q = u / g.ncols;
@@ -1048,6 +1049,21 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
 #pragma unroll
         for (int k = 0; k < NOUT; ++k) st2<VEC>(outp[k] + gi, o0[k], o1[k], valid1);
       }
+      if (MODE == TM_A || MODE == TM_C) {
+        // peer-memory transport: the slab's first / last plane of z_i (sweep A) or
+        // w_{i+1} (sweep C) also goes straight into the neighbour's ghost plane over
+        // NVLink; the reduction flags this kernel raises publish it (fence below)
+        double* const* hh = MODE == TM_A ? V.hz[it & 1] : V.hw[(it & 1) ^ 1];
+        const int64_t po = gi - z * g.pxy;  // offset within the plane
+        if (z == 0 && hh[0]) {
+          st2<VEC>(hh[0] + po, o0[3 % NOUT], o1[3 % NOUT], valid1);
+          remote = true;
+        }
+        if (z == g.nol - 1 && hh[1]) {
+          st2<VEC>(hh[1] + po, o0[3 % NOUT], o1[3 % NOUT], valid1);
+          remote = true;
+        }
+      }
     }
     __syncthreads();  // unit done: every slot is free
     svc = (svc + nsv) % 3;
@@ -1056,6 +1072,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   // PDL: this CTA's sweep is done; the next kernel may be scheduled (it still waits
   // for this grid's completion, the grid reduction included, before reading anything)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // remote ghost stores visible system-wide before this CTA's ticket: the last CTA's
+  // release of the reduction flag then publishes them with the partials
+  if (remote) __threadfence_system();
   if (T::K > 0) {
     Dd tot[K];
     const int slot = MODE == TM_A ? T_SWEEPA : MODE == TM_C ? T_SWEEPC : MODE == TM_RR2 ? T_RR2

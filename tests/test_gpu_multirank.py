@@ -203,3 +203,44 @@ def test_split_stencil_schedule(B, orc, P, overlap):
         res = S.solve(bs, tol=1e-11, maxit=150, rr_period=6, gap=True)
     _parity(res, ref, xs)
     S.close()
+
+
+@pytest.mark.parametrize("shape,P", [((3, 24, 13, 14), 2), ((3, 24, 13, 14), 3),
+                                     ((3, 1100, 3, 3), 3),   # x-segmented tiles, 1 plane/rank
+                                     ((2, 40, 30, 1), 4)])
+@pytest.mark.parametrize("overlap", [1, 0])
+def test_peer_halo_fused_into_sweeps(B, orc, shape, P, overlap):
+    """transport 1, fused schedule: sweep A stores its boundary planes of z_i and sweep C
+    of w_{i+1} straight into the neighbours' ghost planes (peer memory; loopback members
+    share the address space), so the iteration enqueues no z / w halo exchange -- only
+    replacement iterations (w replaced after the sweep) and the gap still exchange.
+    Iterates bitwise equal to transport 0 and to the oracle above the noise floor."""
+    dim, nx, ny, nz = shape
+    coef = problems.cfg34_coef() if dim == 3 else problems.cfg2_coef()
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 0)
+    b = orc.spmv(A, xs)
+    maxit, rr = 60, 7
+    out, halos = [], []
+    for transport in (0, 1):
+        G = B.LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
+        G.set_option("bench", 1)
+        G.set_option("overlap", overlap)
+        G.set_option("transport", transport)
+        bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+        G.ranks[0].kernel_time("halo", reset=True)
+        res = G.solve(bs, tol=0.0, maxit=maxit, rr_period=rr, gap=False)
+        halos.append(G.ranks[0].kernel_time("halo")[0])
+        out.append(res)
+        G.close()
+    assert np.array_equal(out[0].rnorm, out[1].rnorm)
+    assert np.array_equal(out[0].x.cpu().numpy(), out[1].x.cpu().numpy())
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=maxit, rr_period=rr, bench=True, gap=False)
+    _parity(out[1], ref, xs, bitwise=False)
+    k = np.nonzero(ref.rnorm < 1e-16 * ref.rnorm[0])[0]
+    k = int(k[0]) if k.size else maxit + 1
+    assert np.array_equal(out[1].rnorm[:k], ref.rnorm[:k])
+    # two exchanges per iteration fewer, except the w halo of replacement iterations
+    n_rr = maxit // rr
+    assert halos[0] - halos[1] == 2 * maxit - n_rr, halos
+
