@@ -952,24 +952,34 @@ pbicg_status run_chunk(const Members& G, int L, int P) {
   auto it = h->graphs.find(key);
   // the enqueue pass below (capture or, for cached graphs, counted separately)
   // establishes how many launches one replay contains
-  CU(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  // A capture that fails (e.g. a communication library that cannot be captured on
+  // this system) is not fatal: the handle's members drop to direct enqueue, which is
+  // the same sequence of launches, and this chunk runs that way.
+  auto no_graphs = [&](cudaGraph_t g) {
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+    for (size_t q = 0; q < G.size(); ++q) {  // the failed capture counted its launches
+      G[q]->use_graphs = 0;
+      for (int k = 0; k < K_N; ++k) G[q]->launches[k] = before[q][k];
+    }
+    enq_chunk(G, L, P);
+    CU(cudaGetLastError());
+    return PBICG_OK;
+  };
+  if (cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+    return no_graphs(nullptr);
   enq_chunk(G, L, P);
   cudaGraph_t g = nullptr;
   cudaError_t ce = cudaStreamEndCapture(h->stream, &g);
-  if (ce != cudaSuccess)
-    return fail(h, PBICG_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+  if (ce != cudaSuccess) return no_graphs(g);
   if (it == h->graphs.end()) {
     cudaGraphExec_t ge = nullptr;
     ce = cudaGraphInstantiate(&ge, g, 0);
-    if (ce != cudaSuccess) {
-      cudaGraphDestroy(g);
-      return fail(h, PBICG_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
-    }
+    if (ce != cudaSuccess) return no_graphs(g);
     it = h->graphs.emplace(key, ge).first;
   }
   cudaGraphDestroy(g);
   CU(cudaGraphLaunch(it->second, h->stream));
-  (void)before;
   return PBICG_OK;
 }
 
