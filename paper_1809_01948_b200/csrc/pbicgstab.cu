@@ -509,7 +509,11 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     case PH_GAP: {
       LaunchScope ls(h, K_GAP);
-      c_gap<<<h->grid[K_GAP], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->win_ok)  // window SpMV over the SELL-32 matrix, gap epilogue
+        c_spmv_win<SP_GAP><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg,
+                                                                      h->part, h->hist);
+      else
+        c_gap<<<h->grid[K_GAP], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     default:
       break;
@@ -1846,6 +1850,7 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_CLY>, SM, WIN_SMEM);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_PCW0>, SM, WIN_SMEM);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_PCN>, SM, WIN_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_GAP>, SM, WIN_SMEM);
     h->win_ok = e == cudaSuccess;
     cudaGetLastError();
   }
@@ -2486,7 +2491,7 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "sweepC") b = 17 * 8 * N + pb;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w,m
     else if (n == "rr1") b = 2 * mat + 8 * 8 * N;
     else if (n == "rr2") b = 2 * mat + 7 * 8 * N;
-    else if (n == "gap") b = mat + 3 * 8 * N;
+    else if (n == "gap") b = matw + 3 * 8 * N;
     else if (n == "iteration" && h->method == M_BICGSTAB) b = 2 * matw + 2 * 8 * N + 24 * 8 * N;
     else if (n == "iteration" && h->method == M_PIPECG) b = matw + 21 * 8 * N;
     else if (n == "cl1") b = 6 * 8 * N;   // c_cl_p: read r,p,s,dinv; write p, M^-1 p
