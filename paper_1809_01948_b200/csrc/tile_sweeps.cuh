@@ -85,6 +85,12 @@ template <int M> struct StreamDepth { enum { v = 2 }; };
 template <> struct StreamDepth<TM_A> { enum { v = 3 }; };
 template <> struct StreamDepth<TM_AN> { enum { v = 3 }; };
 template <> struct StreamDepth<TM_CL3> { enum { v = 3 }; };  // measured: CL3 +4%; CL1, PC: no gain
+// Depth of the stencil-plane ring (planes z, z+1 resident, the rest in flight).  The
+// stand-alone SpMV tiles of the split schedule stream nothing else and do little work
+// per plane: a 6-slot ring keeps four planes in flight per CTA.
+template <int M> struct SvDepth { enum { v = 3 }; };
+template <> struct SvDepth<TM_SPB> { enum { v = 6 }; };
+template <> struct SvDepth<TM_SPD> { enum { v = 6 }; };
 template <> struct TileTraits<TM_CN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 7, NOUT = 4, K = 9 }; };
 template <> struct TileTraits<TM_RR1N> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 4 }; };
 template <> struct TileTraits<TM_RR2N> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 6 }; };
@@ -667,6 +673,8 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   // to complete (a no-op without PDL)
   asm volatile("griddepcontrol.wait;" ::: "memory");
   constexpr int SD = StreamDepth<MODE_>::v;  // stream ring depth; stencil barriers follow
+  constexpr int SVR = SvDepth<MODE_>::v;      // stencil-plane ring depth
+  static_assert(SD + SVR <= 8, "the mbarriers fit the 64-byte shared-memory header");
   static_assert(K <= RED_K, "partials buffer holds RED_K pairs per CTA");
   if (MODE == TM_A || MODE == TM_C || MODE == TM_CL1 || MODE == TM_CL2 || MODE == TM_CL3 ||
       MODE == TM_PC || MODE == TM_SPB || MODE == TM_SPD) {
@@ -770,7 +778,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     outp[0] = V.w0;
   }
   if (tid == 0) {
-    for (int i = 0; i < SD + 3; ++i) mbar_init(&bar[i], 1);
+    for (int i = 0; i < SD + SVR; ++i) mbar_init(&bar[i], 1);
     fence_barrier_init();
   }
   __syncthreads();
@@ -895,13 +903,13 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       fence_proxy_async_smem();  // the slot is re-staged by TMA after a later barrier
     };
     if (tid == 0) {
-      for (int m = 0; m < 3 && m < nsv; ++m) stage_sv((svc + m) % 3, z0 - 1 + m);
+      for (int m = 0; m < SVR && m < nsv; ++m) stage_sv((svc + m) % SVR, z0 - 1 + m);
       if (HAS_STR) {
         for (int m = 0; m < SD - 1 && m < nst; ++m) stage_st((stc + m) % SD, z0 + m);
       }
     }
     {  // plane z0-1 -> registers
-      const int s = svc % 3;
+      const int s = svc % SVR;
       mbar_wait(&bar[SD + s], (ph >> (SD + s)) & 1u);
       ph ^= 1u << (SD + s);
       const double* b0p = sv + (size_t)s * NSV * svs + sv_off(z0 - 1);
@@ -917,7 +925,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
           for (int v = 0; v < NSO; ++v) ld2<VEC>(b0p + v * svs, m1[v][0], m1[v][1]);
         }
       }
-      const int s1 = (svc + 1) % 3;  // plane z0
+      const int s1 = (svc + 1) % SVR;  // plane z0
       mbar_wait(&bar[SD + s1], (ph >> (SD + s1)) & 1u);
       ph ^= 1u << (SD + s1);
       if (XF) xf_plane(s1, z0, cr, tr);  // ordered before step 0's reads by its barrier
@@ -926,11 +934,11 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       const int64_t z = z0 + n;
       __syncthreads();  // step n-1 done: its plane-(z-1) slot and stream slot are free
       if (tid == 0) {
-        if (n + 3 < nsv) stage_sv((svc + n + 3) % 3, z + 2);  // plane z+2
+        if (n + SVR < nsv) stage_sv((svc + n + SVR) % SVR, z + SVR - 1);  // plane z+SVR-1
         if (HAS_STR && n + SD - 1 < nst)  // streams z+SD-1 into the slot step n-1 freed
           stage_st((stc + n + SD - 1) % SD, z + SD - 1);
       }
-      const int s_z = (svc + n + 1) % 3, s_z1 = (svc + n + 2) % 3, s_st = (stc + n) % SD;
+      const int s_z = (svc + n + 1) % SVR, s_z1 = (svc + n + 2) % SVR, s_st = (stc + n) % SD;
       mbar_wait(&bar[SD + s_z1], (ph >> (SD + s_z1)) & 1u);
       ph ^= 1u << (SD + s_z1);
       if (HAS_STR) {
@@ -1066,7 +1074,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       }
     }
     __syncthreads();  // unit done: every slot is free
-    svc = (svc + nsv) % 3;
+    svc = (svc + nsv) % SVR;
     stc = (stc + nst) % SD;
   }
   // PDL: this CTA's sweep is done; the next kernel may be scheduled (it still waits
@@ -1104,7 +1112,7 @@ template <int M>
 inline size_t tile_smem_bytes_t(const TileGeo& g) {
   // + 16 doubles of slack: block-Jacobi reads of a dropped leg may run past the last slot
   return 64 + sizeof(double) * ((size_t)StreamDepth<M>::v * TileTraits<M>::NSTR * g.st_stride +
-                                (size_t)3 * TileTraits<M>::NSV * g.sv_stride + 16);
+                                (size_t)SvDepth<M>::v * TileTraits<M>::NSV * g.sv_stride + 16);
 }
 
 inline size_t tile_smem_bytes(const TileGeo& g, int mode) {
