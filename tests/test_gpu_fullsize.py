@@ -62,3 +62,41 @@ def test_cfg5_full_size_solve(orc):
     ref = orc.pbicgstab(A, b, tol=cfg.tol, maxit=cfg.maxit, rr_period=cfg.rr_period)
     assert ref.outcome == "converged"
     _compare(res, ref, xs)
+
+
+def test_cfg5_full_size_block_jacobi_and_gap(orc):
+    """cfg5 at full size with block Jacobi b = 2 (the TMA chunk-ring sweeps with
+    shuffle-gathered blocks) in bench mode, replacement every 3 iterations and the
+    window-SpMV gap kernel: 8 iterations bitwise."""
+    from paper_1809_01948_b200 import Solver
+    cfg = problems.configs()["cfg5"]
+    M = problems.csr_band(cfg.csr_n, nnz_row=27, band=4096, seed=1)
+    S = Solver.csr(M.n, M.row_ptr, M.col, M.val, block=2)
+    xs = problems.x_star(M.n, 0)
+    b_d = S.apply(torch.from_numpy(xs).cuda())
+    S.set_option("bench", 1)
+    res = S.solve(b_d, tol=0.0, maxit=8, rr_period=3, gap=True)
+    A = orc.csr(M.row_ptr, M.col, M.val)
+    b = orc.spmv(A, xs)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=8, rr_period=3, bench=True, block=2)
+    _compare(res, ref, xs)
+
+
+def test_cfg4_full_size_split_schedule(orc):
+    """cfg4 at full size on the paper's split schedule (option schedule 2: TMA
+    chunk-ring point-wise sweeps, stand-alone SpMV tiles with the 6-slot ring):
+    3 iterations with a replacement, bitwise."""
+    from paper_1809_01948_b200 import Solver
+    st = problems.configs()["cfg4"].stencil
+    S = Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef)
+    xs = problems.x_star(st.n, 0)
+    b_d = S.apply(torch.from_numpy(xs).cuda())
+    S.set_option("bench", 1)
+    S.set_option("schedule", 2)
+    res = S.solve(b_d, tol=0.0, maxit=3, rr_period=2, gap=False)
+    del b_d
+    A = orc.stencil_csr(st.dim, st.nx, st.ny, st.nz, st.coef)
+    b = orc.spmv(A, xs)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=3, rr_period=2, bench=True, gap=False)
+    _compare(res, ref, xs)
+
