@@ -10,8 +10,13 @@
 //     mbarriers, so ~100 KB per SM is in flight while the CTA computes;
 //   * the stencil operands (w and z in the sweeps; x, g / r, s in the
 //     replacement; x or r in init and gap) are staged as planes with one halo
-//     line on each side (a 3-slot ring: z, z+1 resident, z+2 in flight); the -z
-//     leg comes from registers (the previous step's centre values);
+//     line on each side (a ring of SvDepth slots, 3 by default: z, z+1 resident,
+//     z+2 in flight); the -z leg comes from registers (the previous step's centre
+//     values);
+//   * block Jacobi b >= 4: a transform stage overwrites each landed plane with
+//     M^-1 v once (xf_pair), then a plain stencil runs;
+//   * peer-memory transport: sweeps A / C also store their slab's boundary planes
+//     into the neighbours' ghost planes (Vecs::hz / hw);
 //   * one row pair per thread; 16-byte shared loads / global streaming stores
 //     when nx is even; a warp-uniform interior path drops the boundary selects.
 // Per row the kernels touch DRAM exactly once per vector (tile halos hit L2).
