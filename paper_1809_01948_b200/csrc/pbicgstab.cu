@@ -1815,6 +1815,9 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
       const int64_t d = op->col[q] - (op->row_begin + i);
       bw = d < 0 ? (-d > bw ? -d : bw) : (d > bw ? d : bw);
     }
+  // the window's first element R0 - bw must be 16-byte aligned for the bulk copies:
+  // round the half bandwidth up to even (rows of an odd band just stage one more column)
+  bw = (bw + 1) & ~(int64_t)1;
   if (3LL * WTB + 2 * bw <= WRS) {
     // the window SpMV's operands as sliced ELL (SELL-32) with 16-bit column offsets
     // (|col - row| <= bw < 2^15): 10 bytes per slot, immediate-offset loads

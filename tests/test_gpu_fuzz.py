@@ -4,6 +4,8 @@ coefficient sets, random solver / replacement / graph / tile / loopback-rank
 choices and random CSR band matrices with Jacobi or block Jacobi.  Every case
 must meet the north-star bars, and -- above the noise floor -- be bitwise equal.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -14,7 +16,9 @@ pytestmark = pytest.mark.gpu
 
 from test_gpu_parity import check_parity  # noqa: E402
 
-N_CASES = 24
+# PBICG_FUZZ_SCALE=k runs k times the cases (a wider sweep than the default suite)
+SCALE = int(os.environ.get("PBICG_FUZZ_SCALE", "1"))
+N_CASES = 24 * SCALE
 
 
 def rand_coef(rng, dim, spd):
@@ -57,7 +61,11 @@ def test_fuzz_stencil(orc, seed):
         S = Solver.stencil(dim, nx, ny, nz, coef)
         S.set_option("graphs", int(rng.integers(0, 2)))
         if not auto and method == 0:
-            S.set_option("tile", int(rng.integers(0, 2)))
+            tile = int(rng.integers(0, 2))
+            S.set_option("tile", tile)
+            if tile and rng.integers(0, 3) == 0:  # the paper's split schedule
+                S.set_option("schedule", 2)
+        S.set_option("pdl", int(rng.integers(0, 2)))
         S.set_option("method", method)
         S.set_option("rr_auto", int(auto))
         S.set_option("bench", int(tol == 0.0))
@@ -66,6 +74,7 @@ def test_fuzz_stencil(orc, seed):
         res = S.solve(b_d, tol=tol, maxit=maxit, rr_period=rr, gap=True)
     else:
         S = LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
+        S.set_option("transport", int(rng.integers(0, 2)))
         S.set_option("method", method)
         S.set_option("rr_auto", int(auto))
         S.set_option("bench", int(tol == 0.0))
@@ -84,7 +93,7 @@ def test_fuzz_stencil(orc, seed):
     S.close()
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(12 * SCALE))
 def test_fuzz_csr(orc, seed):
     from paper_1809_01948_b200 import Solver
     rng = np.random.default_rng(2000 + seed)
@@ -95,6 +104,7 @@ def test_fuzz_csr(orc, seed):
     M = problems.csr_band(n, nnz_row=min(nnz, bw + 1), band=bw, seed=seed)  # edge rows: bw candidates
     A = orc.csr(M.row_ptr, M.col, M.val)
     S = Solver.csr(n, M.row_ptr, M.col, M.val, block=block)
+    S.set_option("csr_tma", int(rng.integers(0, 2)))
     method = int(rng.choice([0, 0, 1]))
     S.set_option("method", method)
     auto = method == 0 and bool(rng.integers(0, 2))
@@ -115,7 +125,7 @@ def test_fuzz_csr(orc, seed):
     S.close()
 
 
-@pytest.mark.parametrize("seed", range(8))
+@pytest.mark.parametrize("seed", range(8 * SCALE))
 def test_fuzz_wide_grids(orc, seed):
     """nx > 1024 (x-segmented tiles for even nx, line kernels for odd nx), random
     solver / replacement options, bitwise above the noise floor."""

@@ -318,3 +318,36 @@ def test_split_schedule_sweep_paths(S, orc, dim, nx, ny, nz, kind):
         res = solver.solve(b_d, tol=1e-11, maxit=150, rr_period=7, gap=True)
         check_parity(res, ref, xs)
 
+
+@pytest.mark.parametrize("bw", [1, 7, 1001, 5119])
+def test_csr_odd_bandwidth(S, orc, bw):
+    """A band whose half width is odd: the window SpMV rounds it up to even so the
+    operand window's bulk copies stay 16-byte aligned (regression: an odd width made
+    the first copy start 8 bytes off and the launch failed with a misaligned address)."""
+    n = 4096 + 64
+    rows, cols, vals = [], [], []
+    rng = np.random.default_rng(bw)
+    for i in range(n):
+        js = sorted({j for j in (i - bw, i - 1, i + 1, i + bw) if 0 <= j < n and j != i})
+        off = rng.uniform(-1, 1, len(js))
+        d = 1.2 * np.abs(off).sum() + 1.0
+        row = sorted([(j, v) for j, v in zip(js, off)] + [(i, d)])
+        rows.append(len(row))
+        cols += [c for c, _ in row]
+        vals += [v for _, v in row]
+    rp = np.concatenate([[0], np.cumsum(rows)]).astype(np.int64)
+    col = np.array(cols, dtype=np.int32)
+    val = np.array(vals, dtype=np.float64)
+    A = orc.csr(rp, col, val)
+    xs = problems.x_star(n, 2)
+    b = orc.spmv(A, xs)
+    for method in (0, 1):
+        solver = S.csr(n, rp, col, val)
+        solver.set_option("method", method)
+        b_d = solver.apply(torch.from_numpy(xs).cuda())
+        assert np.array_equal(b_d.cpu().numpy(), b)
+        res = solver.solve(b_d, tol=1e-12, maxit=100, gap=True)
+        ref = (orc.pbicgstab if method == 0 else orc.bicgstab)(A, b, tol=1e-12, maxit=100)
+        check_parity(res, ref, xs)
+        solver.close()
+
