@@ -152,3 +152,82 @@ def test_fuzz_wide_grids(orc, seed):
     check_parity(res, ref, xs, bitwise=False)
     bitwise_above_floor(res, ref)
     S.close()
+
+
+@pytest.mark.parametrize("seed", range(8 * SCALE))
+def test_fuzz_csr_loopback(orc, seed):
+    """Random CSR band matrices split over P emulated ranks at random row cuts (each
+    rank >= PBICG_CSR_HALO rows, any parity), Jacobi or block Jacobi, random solver,
+    transport, TMA sweeps on/off and replacement."""
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    rng = np.random.default_rng(4000 + seed)
+    P = int(rng.choice([2, 3]))
+    block = int(rng.choice([1, 1, 2, 4, 8]))
+    halo = 4096
+    sizes = [int(rng.integers(halo, halo + 3000)) for _ in range(P)]
+    sizes = [sz - sz % block for sz in sizes]
+    n = sum(sizes)
+    bw = int(rng.choice([8, 100, 1001, 4000]))
+    M = problems.csr_band(n, nnz_row=min(int(rng.integers(3, 28)), bw + 1), band=bw,
+                          seed=seed)
+    A = orc.csr(M.row_ptr, M.col, M.val)
+    cuts = np.concatenate([[0], np.cumsum(sizes)])
+    blocks = [(int(cuts[r]), M.row_ptr[cuts[r]:cuts[r + 1] + 1] - M.row_ptr[cuts[r]],
+               M.col[M.row_ptr[cuts[r]]:M.row_ptr[cuts[r + 1]]],
+               M.val[M.row_ptr[cuts[r]]:M.row_ptr[cuts[r + 1]]]) for r in range(P)]
+    G = LoopbackGroup.csr(blocks, n, block=block)
+    method = int(rng.choice([0, 0, 1]))
+    G.set_option("method", method)
+    G.set_option("transport", int(rng.integers(0, 2)))
+    G.set_option("csr_tma", int(rng.integers(0, 2)))
+    G.set_option("overlap", int(rng.integers(0, 2)))
+    rr = int(rng.choice([0, 3, 7])) if method == 0 else 0
+    xs = problems.x_star(n, seed)
+    b = orc.spmv(A, xs)
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=1e-12, maxit=60, rr_period=rr, gap=True)
+    if method == 0:
+        ref = orc.pbicgstab(A, b, tol=1e-12, maxit=60, rr_period=rr, block=block)
+    else:
+        ref = orc.bicgstab(A, b, tol=1e-12, maxit=60, block=block)
+    assert res.outcome == ref.outcome
+    check_parity(res, ref, xs, bitwise=False)
+    bitwise_above_floor(res, ref)
+    G.close()
+
+
+@pytest.mark.parametrize("seed", range(8 * SCALE))
+def test_fuzz_stencil_block_jacobi(orc, seed):
+    """Random stencils with x-aligned block Jacobi b = 2 / 4 / 8 (per-leg form and
+    the transform stage), 1 or P emulated ranks, random transport and replacement."""
+    from paper_1809_01948_b200 import Solver
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    rng = np.random.default_rng(5000 + seed)
+    block = int(rng.choice([2, 4, 8]))
+    dim = int(rng.choice([2, 3]))
+    nx = block * int(rng.integers(1, 840 // block if dim == 3 else 1024 // block))
+    ny = int(rng.integers(1, 30 if dim == 3 else 60))
+    nz = int(rng.integers(1, 12)) if dim == 3 else 1
+    coef = rand_coef(rng, dim, spd=False)
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    if A.n > 400000:
+        pytest.skip("oracle size")
+    xs = problems.x_star(A.n, seed)
+    b = orc.spmv(A, xs)
+    outer = nz if dim == 3 else ny
+    P = int(rng.choice([1, 2, 3])) if outer >= 3 else 1
+    rr = int(rng.choice([0, 4, 9]))
+    if P == 1:
+        S = Solver.stencil(dim, nx, ny, nz, coef, block=block)
+        bs = S.apply(torch.from_numpy(xs).cuda())
+    else:
+        S = LoopbackGroup.stencil(P, dim, nx, ny, nz, coef, block=block)
+        S.set_option("transport", int(rng.integers(0, 2)))
+        bs = S.apply(S.split(torch.from_numpy(xs).cuda()))
+    res = S.solve(bs, tol=1e-11, maxit=60, rr_period=rr, gap=True)
+    ref = orc.pbicgstab(A, b, tol=1e-11, maxit=60, rr_period=rr, block=block)
+    assert res.outcome == ref.outcome
+    check_parity(res, ref, xs, bitwise=False)
+    bitwise_above_floor(res, ref)
+    S.close()
+
