@@ -71,7 +71,14 @@ def test_fuzz_stencil(orc, seed):
         S.set_option("bench", int(tol == 0.0))
         b_d = S.apply(torch.from_numpy(xs).cuda())
         assert np.array_equal(b_d.cpu().numpy(), b)
-        res = S.solve(b_d, tol=tol, maxit=maxit, rr_period=rr, gap=True)
+        if rng.integers(0, 2):  # a nonzero initial guess
+            x0 = rng.uniform(-1, 1, A.n)
+            x0_kw = dict(x0=x0)
+            res = S.solve(b_d, x0=torch.from_numpy(x0).cuda(), tol=tol, maxit=maxit,
+                          rr_period=rr, gap=True)
+        else:
+            x0_kw = {}
+            res = S.solve(b_d, tol=tol, maxit=maxit, rr_period=rr, gap=True)
     else:
         S = LoopbackGroup.stencil(P, dim, nx, ny, nz, coef)
         S.set_option("transport", int(rng.integers(0, 2)))
@@ -80,7 +87,8 @@ def test_fuzz_stencil(orc, seed):
         S.set_option("bench", int(tol == 0.0))
         bs = S.apply(S.split(torch.from_numpy(xs).cuda()))
         res = S.solve(bs, tol=tol, maxit=maxit, rr_period=rr, gap=True)
-    kw = dict(tol=tol, maxit=maxit, bench=tol == 0.0)
+        x0_kw = {}
+    kw = dict(tol=tol, maxit=maxit, bench=tol == 0.0, **x0_kw)
     if method == 0:
         ref = orc.pbicgstab(A, b, rr_period=rr, auto_rr=auto, **kw)
     elif method == 1:
