@@ -189,13 +189,16 @@ def test_fuzz_csr_loopback(orc, seed):
     G.set_option("transport", int(rng.integers(0, 2)))
     G.set_option("csr_tma", int(rng.integers(0, 2)))
     G.set_option("overlap", int(rng.integers(0, 2)))
-    rr = int(rng.choice([0, 3, 7])) if method == 0 else 0
+    auto = method == 0 and bool(rng.integers(0, 2))
+    G.set_option("rr_auto", int(auto))
+    rr = int(rng.choice([0, 3, 7])) if method == 0 and not auto else 0
     xs = problems.x_star(n, seed)
     b = orc.spmv(A, xs)
     bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
     res = G.solve(bs, tol=1e-12, maxit=60, rr_period=rr, gap=True)
     if method == 0:
-        ref = orc.pbicgstab(A, b, tol=1e-12, maxit=60, rr_period=rr, block=block)
+        ref = orc.pbicgstab(A, b, tol=1e-12, maxit=60, rr_period=rr, block=block,
+                            auto_rr=auto)
     else:
         ref = orc.bicgstab(A, b, tol=1e-12, maxit=60, block=block)
     assert res.outcome == ref.outcome
