@@ -213,17 +213,22 @@ enum SpmvMode {
   SP_PCW0,    // p-CG init: w0 = A u0 [k]; m0 = M^-1 w0; (r0,u0), (w0,u0)
   SP_PCN,     // p-CG: n_i = A m_i [mv]
   SP_GAP,     // eq:res_gap: ||(b - A x) - r|| [x]
+  SP_I1,      // Alg. 2 line 2 (Jacobi): r0 = b - A x0, r^0 = r0, k0 = M^-1 r0; (r0,r0), (b,b) [x]
+  SP_I2,      // Alg. 2 line 3 (Jacobi): w0 = A k0, m0 = M^-1 w0; (r^0, w0) [k]
   SP_N
 };
 template <int M> struct SpmvK { enum { K = 0 }; };
 template <> struct SpmvK<SP_GAP> { enum { K = 1 }; };
+template <> struct SpmvK<SP_I1> { enum { K = 2 }; };
+template <> struct SpmvK<SP_I2> { enum { K = 1 }; };
 template <> struct SpmvK<SP_CLS> { enum { K = 1 }; };
 template <> struct SpmvK<SP_CLY> { enum { K = 2 }; };
 template <> struct SpmvK<SP_PCW0> { enum { K = 2 }; };
 
 template <int M>
 __device__ __forceinline__ const double* spmv_in(const Vecs& V) {
-  return (M == SP_V || M == SP_CLY) ? V.nv : M == SP_PCW0 ? V.k : M == SP_GAP ? V.x : V.mv;
+  return (M == SP_V || M == SP_CLY) ? V.nv : (M == SP_PCW0 || M == SP_I2) ? V.k
+       : (M == SP_GAP || M == SP_I1) ? V.x : V.mv;
 }
 
 template <int M, int K>
@@ -241,6 +246,18 @@ __device__ __forceinline__ void spmv_epi(const CsrOp& A, const Vecs& V, int64_t 
   } else if (M == SP_GAP) {
     const double d = (V.b[j] - y) - V.r[j];  // c_gap's expression
     dd_fma(acc[0], d, d);
+  } else if (M == SP_I1) {  // c_init1's expressions (Jacobi)
+    const double bj = V.b[j];
+    const double rj = bj - y;
+    V.r[j] = rj;
+    V.rh[j] = rj;
+    V.k[j] = A.dinv[j] * rj;
+    dd_fma(acc[0], rj, rj);
+    dd_fma(acc[1 % K], bj, bj);
+  } else if (M == SP_I2) {  // c_init2's expressions (Jacobi)
+    V.w0[j] = y;
+    V.mv[j] = A.dinv[j] * y;
+    dd_fma(acc[0], V.rh[j], y);
   } else if (M == SP_PCW0) {
     V.w0[j] = y;  // m0 = M^-1 w0 follows in c_prec_mv (warp-uniform M^-1)
     const double u = V.k[j];
@@ -254,11 +271,14 @@ __device__ __forceinline__ void spmv_fin(Scal* sc, Hist h, Dd* part, Dd (&acc)[S
   constexpr int K = SpmvK<M>::K > 0 ? SpmvK<M>::K : 1;
   if (SpmvK<M>::K == 0) return;
   Dd tot[K];
-  const int slot = M == SP_CLS ? T_CL1 : M == SP_CLY ? T_CL2 : M == SP_GAP ? T_GAP : T_PCI2;
+  const int slot = M == SP_CLS ? T_CL1 : M == SP_CLY ? T_CL2 : M == SP_GAP ? T_GAP
+                 : M == SP_I1 ? T_INIT1 : M == SP_I2 ? T_INIT2 : T_PCI2;
   if (dd_grid_reduce<K>(acc, part, &sc->counter[slot], tot) && threadIdx.x == 0) {
     if (M == SP_CLS) publish<F_CL1>(sc, h, tot);
     else if (M == SP_CLY) publish<F_CL2>(sc, h, tot);
     else if (M == SP_GAP) publish<F_GAP>(sc, h, tot);
+    else if (M == SP_I1) publish<F_INIT1>(sc, h, tot);
+    else if (M == SP_I2) publish<F_INIT2>(sc, h, tot);
     else publish<F_PINIT2>(sc, h, tot);
   }
 }
@@ -658,7 +678,8 @@ template <int WHICH>  // SpmvMode: input, output and epilogue of the step
 __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                      WinGeo w, Dd* __restrict__ part, Hist h) {
   constexpr int K = SpmvK<WHICH>::K > 0 ? SpmvK<WHICH>::K : 1;
-  if (WHICH == SP_GAP ? sc->gap_iter >= sc->iter : (WHICH != SP_PCW0 && sc->done)) return;
+  constexpr bool INIT = WHICH == SP_PCW0 || WHICH == SP_I1 || WHICH == SP_I2;
+  if (WHICH == SP_GAP ? sc->gap_iter >= sc->iter : (!INIT && sc->done)) return;
   const double al = sc->alpha;
   const double* __restrict__ u = spmv_in<WHICH>(V);
   Dd dacc[K];

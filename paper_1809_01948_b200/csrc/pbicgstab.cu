@@ -421,6 +421,9 @@ void launch_csr(pbicg_ctx* h, Phase p) {
       if (h->csr.bj > 1) {
         if (h->auto_rr) c_init1<true, true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
         else c_init1<false, true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      } else if (h->win_ok && !h->auto_rr) {  // window SpMV over the SELL-32 matrix
+        c_spmv_win<SP_I1><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg,
+                                                                     h->part, h->hist);
       } else {
         if (h->auto_rr) c_init1<true, false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
         else c_init1<false, false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
@@ -429,6 +432,9 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     case PH_INIT2: {
       LaunchScope ls(h, K_INIT);
       if (h->csr.bj > 1) c_init2<true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else if (h->win_ok)
+        c_spmv_win<SP_I2><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg,
+                                                                     h->part, h->hist);
       else c_init2<false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SWEEPA: {
@@ -1854,6 +1860,8 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_PCW0>, SM, WIN_SMEM);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_PCN>, SM, WIN_SMEM);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_GAP>, SM, WIN_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_I1>, SM, WIN_SMEM);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_spmv_win<SP_I2>, SM, WIN_SMEM);
     h->win_ok = e == cudaSuccess;
     cudaGetLastError();
   }
