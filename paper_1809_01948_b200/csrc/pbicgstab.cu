@@ -1353,6 +1353,7 @@ pbicg_status p2p_setup(const Members& G) {
 
 // point the tile sweeps' ghost stores at the neighbours (transport 1) or nowhere
 void set_peer_halo(pbicg_ctx* h, bool on) {
+  h->tg.peer = on && h->kind == KIND_STENCIL;
   for (int b = 0; b < 2; ++b)
     for (int sd = 0; sd < 2; ++sd) {
       h->V.hw[b][sd] = on ? h->peer_ghost[b][sd] : nullptr;      // w0, w1

@@ -17,6 +17,12 @@ constexpr bool kVec = PBICG_VEC != 0;
 template <int DIM, int MODE>
 void launch_one(int grid, size_t smem, cudaStream_t s, const TileGeo& g, const Vecs& V, Scal* sc,
                 Dd* part, Hist h) {
+  if constexpr (HasPeer<MODE>::v) {
+    if (g.peer) {  // peer-memory transport: the instance that stores the boundary planes
+      tile_launch(t_tile<DIM, MODE, kVec, 0, false, true>, grid, smem, s, g, V, sc, part, h);
+      return;
+    }
+  }
   tile_launch(t_tile<DIM, MODE, kVec>, grid, smem, s, g, V, sc, part, h);
 }
 
@@ -24,6 +30,10 @@ template <int DIM, int MODE>
 cudaError_t attr_one(int smem, int* occ) {
   cudaError_t e = cudaFuncSetAttribute(t_tile<DIM, MODE, kVec>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if constexpr (HasPeer<MODE>::v) {
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(t_tile<DIM, MODE, kVec, 0, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  }
   if (e == cudaSuccess)
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, t_tile<DIM, MODE, kVec>, TNT, smem);
   return e;

@@ -123,6 +123,7 @@ struct TileGeo {
   int32_t nseg;       // segments per line
   int32_t lstride;    // shared-memory stride of a staged stencil line segment (sx + 16)
   int32_t pdl;        // launch with programmatic dependent launch (option "pdl")
+  int32_t peer;       // sweeps A / C store their boundary planes in the neighbours (Vecs::hz/hw)
 };
 
 // halo columns staged on each side of a segment (>= 2 for the x legs; 8 keeps every
@@ -649,7 +650,34 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
 // aligned (nx even) -> paired loads and stores.  One row pair per thread:
 // TP <= 2 * TNT.
 // BJ: block-Jacobi block size (0 Jacobi); SEG: x-segmented tiles (nx > 1024)
-template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false>
+// Peer-memory transport (Vecs::hz / hw): copy this thread's row pair of the slab's
+// first / last plane of z_i (sweep A) or w_{i+1} (sweep C) -- stored by the same thread
+// earlier in the unit -- into the neighbours' ghost planes.  Out of line: it runs at the
+// end of the (at most two) boundary units and stays out of the step loop's registers.
+template <bool VEC>
+__device__ __noinline__ bool peer_put(double* hp_lo, double* hp_hi, const double* own,
+                                      int64_t pxy, int64_t nol, int64_t z0, int64_t z1,
+                                      int64_t po, bool valid1) {
+  bool stored = false;
+  for (int sd = 0; sd < 2; ++sd) {
+    double* const hp = sd == 0 ? hp_lo : hp_hi;
+    const int64_t zb = sd == 0 ? 0 : nol - 1;
+    if (!hp || zb < z0 || zb >= z1) continue;
+    const double a = own[zb * pxy + po];
+    const double c = valid1 ? own[zb * pxy + po + 1] : 0.0;
+    st2<VEC>(hp + po, a, c, valid1);
+    stored = true;
+  }
+  return stored;
+}
+
+// PEER: the instance the peer-memory transport launches (tile_launch picks it when
+// TileGeo::peer): sweeps A / C also store their boundary planes in the neighbours.  A
+// template flag so the default instances carry no trace of it (measured: even an
+// untaken runtime branch cost sweep A 0.5-1.3%).
+template <int M> struct HasPeer { enum { v = BaseOf<M>::v == TM_A || BaseOf<M>::v == TM_C }; };
+
+template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false, bool PEER = false>
 __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
                                                  Dd* __restrict__ part, Hist h) {
   using T = TileTraits<MODE_>;
@@ -794,6 +822,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   const int r = 2 * tid;  // this thread's row pair within the tile
   bool remote = false;    // this thread stored into a peer's ghost plane
+  // peer ghost planes of this sweep's z_i (A) / w_{i+1} (C): only a uniform flag stays
+  // live across the loop; the pointers are resolved in the (boundary-plane) branch
+  constexpr bool peer = PEER && (MODE == TM_A || MODE == TM_C);
 
   for (int u = blockIdx.x; u < g.units; u += gridDim.x) {
     const int col = u % g.ncols, q = u / g.ncols;
@@ -1062,21 +1093,19 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
 #pragma unroll
         for (int k = 0; k < NOUT; ++k) st2<VEC>(outp[k] + gi, o0[k], o1[k], valid1);
       }
-      if (MODE == TM_A || MODE == TM_C) {
-        // peer-memory transport: the slab's first / last plane of z_i (sweep A) or
-        // w_{i+1} (sweep C) also goes straight into the neighbour's ghost plane over
-        // NVLink; the reduction flags this kernel raises publish it (fence below)
-        double* const* hh = MODE == TM_A ? V.hz[it & 1] : V.hw[(it & 1) ^ 1];
-        const int64_t po = gi - z * g.pxy;  // offset within the plane
-        if (z == 0 && hh[0]) {
-          st2<VEC>(hh[0] + po, o0[3 % NOUT], o1[3 % NOUT], valid1);
-          remote = true;
-        }
-        if (z == g.nol - 1 && hh[1]) {
-          st2<VEC>(hh[1] + po, o0[3 % NOUT], o1[3 % NOUT], valid1);
-          remote = true;
-        }
-      }
+    }
+    if ((MODE == TM_A || MODE == TM_C) && peer && act && (z0 == 0 || z1 == g.nol)) {
+      // peer-memory transport: the slab's first / last plane of z_i (sweep A) or w_{i+1}
+      // (sweep C), which this thread stored during the unit, also goes straight into the
+      // neighbour's ghost plane over NVLink; the reduction flags this kernel raises
+      // publish it (fence below)
+      const int64_t po = SEG ? (DIM == 3 ? (y0 + ly) * g.nx : 0) + x0s + cx : toff + r;
+      const bool odd = (it & 1) != 0;
+      double* const hp_lo = MODE == TM_A ? (odd ? V.hz[1][0] : V.hz[0][0])
+                                         : (odd ? V.hw[0][0] : V.hw[1][0]);
+      double* const hp_hi = MODE == TM_A ? (odd ? V.hz[1][1] : V.hz[0][1])
+                                         : (odd ? V.hw[0][1] : V.hw[1][1]);
+      remote |= peer_put<VEC>(hp_lo, hp_hi, outp[3 % NOUT], g.pxy, g.nol, z0, z1, po, valid1);
     }
     __syncthreads();  // unit done: every slot is free
     svc = (svc + nsv) % SVR;
