@@ -188,6 +188,13 @@ __device__ __forceinline__ double leg(unsigned b, unsigned bit, double acc, doub
   return (INTERIOR || (b & bit)) ? acc + term : acc;
 }
 
+// the same with a mask of the legs that may be dropped (DROP: boundary bits checked;
+// legs outside it are always present for the warp)
+template <unsigned DROP>
+__device__ __forceinline__ double legm(unsigned b, unsigned bit, double acc, double term) {
+  return ((DROP & bit) == 0u || (b & bit)) ? acc + term : acc;
+}
+
 template <bool PREC>
 __device__ __forceinline__ double pre(double d, double v) {
   return PREC ? d * v : v;
@@ -199,7 +206,7 @@ __device__ __forceinline__ double pre(double d, double v) {
 // right from +0.0; with PREC every leg is fl(c * fl(dinv * v)), exactly the
 // oracle's "n := M^-1 z; v := A n".  Products shared by the two rows are formed
 // once (same values).  bnd bits: 1 zm, 2 ym, 4 xm, 8 xp, 16 yp, 32 zp.
-template <int DIM, bool VEC, bool INTERIOR, bool PREC>
+template <int DIM, bool VEC, unsigned DROP, bool PREC>
 __device__ __forceinline__ void stencil_pair(const TileGeo& g, int nx, const double* W,
                                              const double* W1, double zm0, double zm1,
                                              unsigned b0, unsigned b1, double& c0, double& c1,
@@ -216,22 +223,22 @@ __device__ __forceinline__ void stencil_pair(const TileGeo& g, int nx, const dou
   ld2<VEC>(W1, zp0, zp1);
   const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
   double a = 0.0;
-  a = leg<INTERIOR>(b0, 1u, a, czm * pre<PREC>(d, zm0));
-  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * pre<PREC>(d, ym0));
-  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * pm);
+  a = legm<DROP>(b0, 1u, a, czm * pre<PREC>(d, zm0));
+  if (DIM == 3) a = legm<DROP>(b0, 2u, a, g.c[3] * pre<PREC>(d, ym0));
+  a = legm<DROP>(b0, 4u, a, g.c[1] * pm);
   a = a + g.c[0] * p0;
-  a = leg<INTERIOR>(b0, 8u, a, g.c[2] * p1);
-  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * pre<PREC>(d, yp0));
-  a = leg<INTERIOR>(b0, 32u, a, czp * pre<PREC>(d, zp0));
+  a = legm<DROP>(b0, 8u, a, g.c[2] * p1);
+  if (DIM == 3) a = legm<DROP>(b0, 16u, a, g.c[4] * pre<PREC>(d, yp0));
+  a = legm<DROP>(b0, 32u, a, czp * pre<PREC>(d, zp0));
   t0 = a;
   a = 0.0;
-  a = leg<INTERIOR>(b1, 1u, a, czm * pre<PREC>(d, zm1));
-  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * pre<PREC>(d, ym1));
-  a = leg<INTERIOR>(b1, 4u, a, g.c[1] * p0);
+  a = legm<DROP>(b1, 1u, a, czm * pre<PREC>(d, zm1));
+  if (DIM == 3) a = legm<DROP>(b1, 2u, a, g.c[3] * pre<PREC>(d, ym1));
+  a = legm<DROP>(b1, 4u, a, g.c[1] * p0);
   a = a + g.c[0] * p1;
-  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * p2);
-  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * pre<PREC>(d, yp1));
-  a = leg<INTERIOR>(b1, 32u, a, czp * pre<PREC>(d, zp1));
+  a = legm<DROP>(b1, 8u, a, g.c[2] * p2);
+  if (DIM == 3) a = legm<DROP>(b1, 16u, a, g.c[4] * pre<PREC>(d, yp1));
+  a = legm<DROP>(b1, 32u, a, czp * pre<PREC>(d, zp1));
   t1 = a;
 }
 
@@ -864,6 +871,9 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
     const unsigned xy_all = DIM == 3 ? 30u : 12u;
     const bool xy_int = __all_sync(0xffffffffu, !act || ((b0 & xy_all) == xy_all &&
                                                          (b1 & xy_all) == xy_all));
+    const unsigned y_all = DIM == 3 ? 18u : 0u;  // in-plane y legs (3D)
+    const bool yz_int = __all_sync(0xffffffffu, !act || ((b0 & y_all) == y_all &&
+                                                         (b1 & y_all) == y_all));
     double m1[NSO][2];  // plane z-1 centre values per stencil operand
     double cr[NSO][2];  // XF: raw centre pair of plane z
     double tr[NSO][2];  // XF: transformed centre pair of plane z
@@ -1046,14 +1056,20 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       } else if (xy_int && zin) {
 #pragma unroll
         for (int v = 0; v < NSO; ++v)
-          stencil_pair<DIM, VEC, true, PREC>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
-                                             m1[v][1], 0u, 0u, c[v][0], c[v][1], t[v][0], t[v][1]);
+          stencil_pair<DIM, VEC, 0u, PREC>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                           m1[v][1], 0u, 0u, c[v][0], c[v][1], t[v][0], t[v][1]);
+      } else if (yz_int && zin) {  // a warp holding a line's first / last x: x legs only
+#pragma unroll
+        for (int v = 0; v < NSO; ++v)
+          stencil_pair<DIM, VEC, 12u, PREC>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                            m1[v][1], b0, b1, c[v][0], c[v][1], t[v][0],
+                                            t[v][1]);
       } else {
 #pragma unroll
         for (int v = 0; v < NSO; ++v)
-          stencil_pair<DIM, VEC, false, PREC>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
-                                              m1[v][1], b0 | zb, b1 | zb, c[v][0], c[v][1],
-                                              t[v][0], t[v][1]);
+          stencil_pair<DIM, VEC, 63u, PREC>(g, ls, Wz + v * svs, Wz1 + v * svs, m1[v][0],
+                                            m1[v][1], b0 | zb, b1 | zb, c[v][0], c[v][1],
+                                            t[v][0], t[v][1]);
       }
 #pragma unroll
       for (int v = 0; v < NSO; ++v) {
