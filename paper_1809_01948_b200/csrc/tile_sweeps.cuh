@@ -392,7 +392,7 @@ __device__ __forceinline__ double derive_one(const double* P, int svs, double al
 // of staged vector 0 (vector k at W + k * svs), W1 likewise for plane z+1; zm0/zm1
 // are the derived values of plane z-1.  Returns the derived centre pair (c0, c1)
 // and fl(A M^-1 op) (PREC) or fl(A op) for the row pair, legs as in stencil_pair.
-template <int DIM, bool VEC, bool INTERIOR, bool PREC, int NSV, int MODE>
+template <int DIM, bool VEC, unsigned DROP, bool PREC, int NSV, int MODE>
 __device__ __forceinline__ void stencil_pair_der(const TileGeo& g, int nx, const double* W,
                                                  int svs, const double* W1, double zm0,
                                                  double zm1, unsigned b0, unsigned b1,
@@ -411,22 +411,22 @@ __device__ __forceinline__ void stencil_pair_der(const TileGeo& g, int nx, const
   derive_pair<VEC, NSV, MODE>(W1, svs, al, be, om, zp0, zp1);
   const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
   double a = 0.0;
-  a = leg<INTERIOR>(b0, 1u, a, czm * pre<PREC>(d, zm0));
-  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * pre<PREC>(d, ym0));
-  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * pm);
+  a = legm<DROP>(b0, 1u, a, czm * pre<PREC>(d, zm0));
+  if (DIM == 3) a = legm<DROP>(b0, 2u, a, g.c[3] * pre<PREC>(d, ym0));
+  a = legm<DROP>(b0, 4u, a, g.c[1] * pm);
   a = a + g.c[0] * p0;
-  a = leg<INTERIOR>(b0, 8u, a, g.c[2] * p1);
-  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * pre<PREC>(d, yp0));
-  a = leg<INTERIOR>(b0, 32u, a, czp * pre<PREC>(d, zp0));
+  a = legm<DROP>(b0, 8u, a, g.c[2] * p1);
+  if (DIM == 3) a = legm<DROP>(b0, 16u, a, g.c[4] * pre<PREC>(d, yp0));
+  a = legm<DROP>(b0, 32u, a, czp * pre<PREC>(d, zp0));
   t0 = a;
   a = 0.0;
-  a = leg<INTERIOR>(b1, 1u, a, czm * pre<PREC>(d, zm1));
-  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * pre<PREC>(d, ym1));
-  a = leg<INTERIOR>(b1, 4u, a, g.c[1] * p0);
+  a = legm<DROP>(b1, 1u, a, czm * pre<PREC>(d, zm1));
+  if (DIM == 3) a = legm<DROP>(b1, 2u, a, g.c[3] * pre<PREC>(d, ym1));
+  a = legm<DROP>(b1, 4u, a, g.c[1] * p0);
   a = a + g.c[0] * p1;
-  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * p2);
-  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * pre<PREC>(d, yp1));
-  a = leg<INTERIOR>(b1, 32u, a, czp * pre<PREC>(d, zp1));
+  a = legm<DROP>(b1, 8u, a, g.c[2] * p2);
+  if (DIM == 3) a = legm<DROP>(b1, 16u, a, g.c[4] * pre<PREC>(d, yp1));
+  a = legm<DROP>(b1, 32u, a, czp * pre<PREC>(d, zp1));
   t1 = a;
 }
 
@@ -484,7 +484,7 @@ __device__ __forceinline__ void xf_store(double* base, int svs, int e, const dou
 
 // stencil_pair on transformed planes: the centre pair (p0, p1), the z-1 and z+1
 // pairs come from registers, the x and y legs from the transformed plane at W
-template <int DIM, bool VEC, bool INTERIOR>
+template <int DIM, bool VEC, unsigned DROP>
 __device__ __forceinline__ void stencil_pair_xf(const TileGeo& g, int nx, const double* W,
                                                 double p0, double p1, double zm0, double zm1,
                                                 double zp0, double zp1, unsigned b0,
@@ -497,22 +497,22 @@ __device__ __forceinline__ void stencil_pair_xf(const TileGeo& g, int nx, const 
   }
   const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
   double a = 0.0;
-  a = leg<INTERIOR>(b0, 1u, a, czm * zm0);
-  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * ym0);
-  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * pm);
+  a = legm<DROP>(b0, 1u, a, czm * zm0);
+  if (DIM == 3) a = legm<DROP>(b0, 2u, a, g.c[3] * ym0);
+  a = legm<DROP>(b0, 4u, a, g.c[1] * pm);
   a = a + g.c[0] * p0;
-  a = leg<INTERIOR>(b0, 8u, a, g.c[2] * p1);
-  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * yp0);
-  a = leg<INTERIOR>(b0, 32u, a, czp * zp0);
+  a = legm<DROP>(b0, 8u, a, g.c[2] * p1);
+  if (DIM == 3) a = legm<DROP>(b0, 16u, a, g.c[4] * yp0);
+  a = legm<DROP>(b0, 32u, a, czp * zp0);
   t0 = a;
   a = 0.0;
-  a = leg<INTERIOR>(b1, 1u, a, czm * zm1);
-  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * ym1);
-  a = leg<INTERIOR>(b1, 4u, a, g.c[1] * p0);
+  a = legm<DROP>(b1, 1u, a, czm * zm1);
+  if (DIM == 3) a = legm<DROP>(b1, 2u, a, g.c[3] * ym1);
+  a = legm<DROP>(b1, 4u, a, g.c[1] * p0);
   a = a + g.c[0] * p1;
-  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * p2);
-  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * yp1);
-  a = leg<INTERIOR>(b1, 32u, a, czp * zp1);
+  a = legm<DROP>(b1, 8u, a, g.c[2] * p2);
+  if (DIM == 3) a = legm<DROP>(b1, 16u, a, g.c[4] * yp1);
+  a = legm<DROP>(b1, 32u, a, czp * zp1);
   t1 = a;
 }
 
@@ -1008,13 +1008,19 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         if (xy_int && zin) {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair_xf<DIM, VEC, true>(g, ls, Wz + v * svs, tr[v][0], tr[v][1], m1[v][0],
+            stencil_pair_xf<DIM, VEC, 0u>(g, ls, Wz + v * svs, tr[v][0], tr[v][1], m1[v][0],
                                             m1[v][1], tn[v][0], tn[v][1], 0u, 0u, t[v][0],
                                             t[v][1]);
+        } else if (yz_int && zin) {  // x legs only
+#pragma unroll
+          for (int v = 0; v < NSO; ++v)
+            stencil_pair_xf<DIM, VEC, 12u>(g, ls, Wz + v * svs, tr[v][0], tr[v][1], m1[v][0],
+                                             m1[v][1], tn[v][0], tn[v][1], b0, b1, t[v][0],
+                                             t[v][1]);
         } else {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair_xf<DIM, VEC, false>(g, ls, Wz + v * svs, tr[v][0], tr[v][1], m1[v][0],
+            stencil_pair_xf<DIM, VEC, 63u>(g, ls, Wz + v * svs, tr[v][0], tr[v][1], m1[v][0],
                                              m1[v][1], tn[v][0], tn[v][1], b0 | zb, b1 | zb,
                                              t[v][0], t[v][1]);
         }
@@ -1045,11 +1051,15 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         }
       } else if (DER) {
         if (xy_int && zin)
-          stencil_pair_der<DIM, VEC, true, PREC, NSV, MODE>(g, ls, Wz, svs, Wz1, m1[0][0],
+          stencil_pair_der<DIM, VEC, 0u, PREC, NSV, MODE>(g, ls, Wz, svs, Wz1, m1[0][0],
                                                             m1[0][1], 0u, 0u, al, be, om, c[0][0],
                                                             c[0][1], t[0][0], t[0][1]);
+        else if (yz_int && zin)  // x legs only
+          stencil_pair_der<DIM, VEC, 12u, PREC, NSV, MODE>(g, ls, Wz, svs, Wz1, m1[0][0],
+                                                             m1[0][1], b0, b1, al, be, om,
+                                                             c[0][0], c[0][1], t[0][0], t[0][1]);
         else
-          stencil_pair_der<DIM, VEC, false, PREC, NSV, MODE>(g, ls, Wz, svs, Wz1, m1[0][0],
+          stencil_pair_der<DIM, VEC, 63u, PREC, NSV, MODE>(g, ls, Wz, svs, Wz1, m1[0][0],
                                                              m1[0][1], b0 | zb, b1 | zb, al, be,
                                                              om, c[0][0], c[0][1], t[0][0],
                                                              t[0][1]);
