@@ -976,15 +976,34 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       ph ^= 1u << (SD + s1);
       if (XF) xf_plane(s1, z0, cr, tr);  // ordered before step 0's reads by its barrier
     }
+    // ring slots of step n, advanced incrementally (no modulo per step): the slot plane
+    // z+SVR-1 is staged into, planes z and z+1, the stream slot and the stream slot
+    // being refilled; the 16-byte phase of a plane's first staged element flips per
+    // plane only when the plane stride is odd
+    int k_new = svc % SVR, k_z = (svc + 1) % SVR, k_z1 = (svc + 2) % SVR;
+    int k_st = stc % SD, k_stn = (stc + SD - 1) % SD;
+    const int pstep = (int)(g.pxy & 1);
+    const int ao_sv0 = SEG ? 0 : align_off(svp[0] + z0 * g.pxy + toff - g.halo);
+    const int ao_st0 = (SEG || !HAS_STR) ? 0 : align_off(stp[0] + z0 * g.pxy + toff);
+    const int64_t gin = SEG ? (DIM == 3 ? (y0 + ly) * g.nx : 0) + x0s + cx : toff + r;
+    int64_t gz = z0 * g.pxy;  // z * pxy
     for (int n = 0; n < nst; ++n) {
       const int64_t z = z0 + n;
+      if (n > 0) {
+        k_new = k_new + 1 == SVR ? 0 : k_new + 1;
+        k_z = k_z + 1 == SVR ? 0 : k_z + 1;
+        k_z1 = k_z1 + 1 == SVR ? 0 : k_z1 + 1;
+        k_st = k_st + 1 == SD ? 0 : k_st + 1;
+        k_stn = k_stn + 1 == SD ? 0 : k_stn + 1;
+        gz += g.pxy;
+      }
       __syncthreads();  // step n-1 done: its plane-(z-1) slot and stream slot are free
       if (tid == 0) {
-        if (n + SVR < nsv) stage_sv((svc + n + SVR) % SVR, z + SVR - 1);  // plane z+SVR-1
+        if (n + SVR < nsv) stage_sv(k_new, z + SVR - 1);  // plane z+SVR-1
         if (HAS_STR && n + SD - 1 < nst)  // streams z+SD-1 into the slot step n-1 freed
-          stage_st((stc + n + SD - 1) % SD, z + SD - 1);
+          stage_st(k_stn, z + SD - 1);
       }
-      const int s_z = (svc + n + 1) % SVR, s_z1 = (svc + n + 2) % SVR, s_st = (stc + n) % SD;
+      const int s_z = k_z, s_z1 = k_z1, s_st = k_st;
       mbar_wait(&bar[SD + s_z1], (ph >> (SD + s_z1)) & 1u);
       ph ^= 1u << (SD + s_z1);
       if (HAS_STR) {
@@ -994,12 +1013,15 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       double cn[NSO][2], tn[NSO][2];  // XF: own pair of plane z+1, raw / transformed
       if (XF) xf_plane(s_z1, z + 1, cn, tn);
       if (!act) continue;
-      const double* Wz = sv + (size_t)s_z * NSV * svs + sv_off(z);
-      const double* Wz1 = sv + (size_t)s_z1 * NSV * svs + sv_off(z + 1);
+      // plane offsets: sv_off / align_off without re-deriving them from addresses
+      const int ov_z = SEG ? (ly + (DIM == 3 ? 1 : 0)) * ls + SEG_HX + cx
+                           : (ao_sv0 ^ (n & pstep)) + g.halo + r;
+      const int ov_z1 = SEG ? ov_z : (ao_sv0 ^ ((n + 1) & pstep)) + g.halo + r;
+      const double* Wz = sv + (size_t)s_z * NSV * svs + ov_z;
+      const double* Wz1 = sv + (size_t)s_z1 * NSV * svs + ov_z1;
       const double* S0 = !HAS_STR ? nullptr
                          : SEG    ? st + (size_t)s_st * NST * sts + ly * g.sx + cx
-                                  : st + (size_t)s_st * NST * sts +
-                                        align_off(stp[0] + z * g.pxy + toff) + r;
+                                  : st + (size_t)s_st * NST * sts + (ao_st0 ^ (n & pstep)) + r;
       const bool zin = (g.o0 + z) > 0 && (g.o0 + z) < g.nog - 1;
       const unsigned zb = ((g.o0 + z) > 0 ? 1u : 0u) | ((g.o0 + z) < g.nog - 1 ? 32u : 0u);
       double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, t[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
@@ -1089,8 +1111,7 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       double o0[NOUT], o1[NOUT];
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) o0[k] = o1[k] = 0.0;
-      const int64_t gi = SEG ? z * g.pxy + (DIM == 3 ? (y0 + ly) * g.nx : 0) + x0s + cx
-                             : z * g.pxy + toff + r;
+      const int64_t gi = gz + gin;
       row_update<MODE, K, NOUT, NRM, (BJ > 0)>(S0, sts, rr, V.zrr + gi, pc[0][0], pc[1 % NSO][0],
                                          c[0][0], c[1][0], t[0][0], t[1][0], al, be, om, g.dinv,
                                          acc, o0);
