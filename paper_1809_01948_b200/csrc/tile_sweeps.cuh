@@ -279,7 +279,7 @@ __device__ __forceinline__ void bj_pair(const double* bi, int i0, const double* 
 // of row r (even).  zm0/zm1 are the PRECONDITIONED values of plane z-1.  Legs as
 // in stencil_pair (A5); a dropped leg's value may be read past the line but is
 // never added.
-template <int DIM, bool VEC, bool INTERIOR, int B>
+template <int DIM, bool VEC, unsigned DROP, int B>
 __device__ __forceinline__ void stencil_pair_bj(const TileGeo& g, const double* bi, int nx, int i0,
                                                 const double* W, const double* W1, double zm0,
                                                 double zm1, unsigned b0, unsigned b1, double& c0,
@@ -322,22 +322,22 @@ __device__ __forceinline__ void stencil_pair_bj(const TileGeo& g, const double* 
   bj_pair<B, VEC>(bi, i0, W1 - i0, zp0, zp1);
   const double czm = g.c[DIM == 3 ? 5 : 3], czp = g.c[DIM == 3 ? 6 : 4];
   double a = 0.0;
-  a = leg<INTERIOR>(b0, 1u, a, czm * zm0);
-  if (DIM == 3) a = leg<INTERIOR>(b0, 2u, a, g.c[3] * ym0);
-  a = leg<INTERIOR>(b0, 4u, a, g.c[1] * xm);
+  a = legm<DROP>(b0, 1u, a, czm * zm0);
+  if (DIM == 3) a = legm<DROP>(b0, 2u, a, g.c[3] * ym0);
+  a = legm<DROP>(b0, 4u, a, g.c[1] * xm);
   a = a + g.c[0] * pc0;
-  a = leg<INTERIOR>(b0, 8u, a, g.c[2] * pc1);
-  if (DIM == 3) a = leg<INTERIOR>(b0, 16u, a, g.c[4] * yp0);
-  a = leg<INTERIOR>(b0, 32u, a, czp * zp0);
+  a = legm<DROP>(b0, 8u, a, g.c[2] * pc1);
+  if (DIM == 3) a = legm<DROP>(b0, 16u, a, g.c[4] * yp0);
+  a = legm<DROP>(b0, 32u, a, czp * zp0);
   t0 = a;
   a = 0.0;
-  a = leg<INTERIOR>(b1, 1u, a, czm * zm1);
-  if (DIM == 3) a = leg<INTERIOR>(b1, 2u, a, g.c[3] * ym1);
-  a = leg<INTERIOR>(b1, 4u, a, g.c[1] * pc0);
+  a = legm<DROP>(b1, 1u, a, czm * zm1);
+  if (DIM == 3) a = legm<DROP>(b1, 2u, a, g.c[3] * ym1);
+  a = legm<DROP>(b1, 4u, a, g.c[1] * pc0);
   a = a + g.c[0] * pc1;
-  a = leg<INTERIOR>(b1, 8u, a, g.c[2] * xp);
-  if (DIM == 3) a = leg<INTERIOR>(b1, 16u, a, g.c[4] * yp1);
-  a = leg<INTERIOR>(b1, 32u, a, czp * zp1);
+  a = legm<DROP>(b1, 8u, a, g.c[2] * xp);
+  if (DIM == 3) a = legm<DROP>(b1, 16u, a, g.c[4] * yp1);
+  a = legm<DROP>(b1, 32u, a, czp * zp1);
   t1 = a;
 }
 
@@ -1061,13 +1061,19 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
         if (xy_int && zin) {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair_bj<DIM, VEC, true, BB>(g, s_bi, ls, i0, Wz + v * svs, Wz1 + v * svs,
-                                                m1[v][0], m1[v][1], 0u, 0u, c[v][0], c[v][1],
-                                                pc[v][0], pc[v][1], t[v][0], t[v][1]);
+            stencil_pair_bj<DIM, VEC, 0u, BB>(g, s_bi, ls, i0, Wz + v * svs, Wz1 + v * svs,
+                                              m1[v][0], m1[v][1], 0u, 0u, c[v][0], c[v][1],
+                                              pc[v][0], pc[v][1], t[v][0], t[v][1]);
+        } else if (yz_int && zin) {  // x legs only
+#pragma unroll
+          for (int v = 0; v < NSO; ++v)
+            stencil_pair_bj<DIM, VEC, 12u, BB>(g, s_bi, ls, i0, Wz + v * svs, Wz1 + v * svs,
+                                               m1[v][0], m1[v][1], b0, b1, c[v][0], c[v][1],
+                                               pc[v][0], pc[v][1], t[v][0], t[v][1]);
         } else {
 #pragma unroll
           for (int v = 0; v < NSO; ++v)
-            stencil_pair_bj<DIM, VEC, false, BB>(g, s_bi, ls, i0, Wz + v * svs, Wz1 + v * svs,
+            stencil_pair_bj<DIM, VEC, 63u, BB>(g, s_bi, ls, i0, Wz + v * svs, Wz1 + v * svs,
                                                  m1[v][0], m1[v][1], b0 | zb, b1 | zb, c[v][0],
                                                  c[v][1], pc[v][0], pc[v][1], t[v][0], t[v][1]);
         }
