@@ -815,6 +815,107 @@ __global__ void __launch_bounds__(256) c_cl_x(CsrOp A, Vecs V, Scal* __restrict_
     publish<F_CL3>(sc, h, tot);
 }
 
+// Classic BiCGStab's point-wise steps (Jacobi) on the same TMA chunk ring as the
+// p-BiCGStab sweeps: the expressions of c_cl_p / c_cl_u / c_cl_x, a row pair per thread.
+//   ST 0 (l.17): p := r + beta (p - omega s), mv := M^-1 p      in: r, p(g), s, dinv
+//   ST 1 (l.8-9): nv := M^-1 (r - alpha s)                       in: r, s, dinv
+//   ST 2 (l.13-15): x, r; (r^0, r), ||r||^2                       in: r, s, x, mv, nv, y(z1), r^0
+template <int ST>
+__global__ void __launch_bounds__(CST_T, 1) c_cl_tma(CsrOp A, Vecs V, Scal* __restrict__ sc,
+                                                     Dd* __restrict__ part, Hist h) {
+  constexpr int NIN = ST == 0 ? 4 : ST == 1 ? 3 : 7;
+  if (sc->done) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw);
+  double* buf = reinterpret_cast<double*>(smem_raw + 64);
+  const int tid = threadIdx.x;
+  const double al = sc->alpha, be = sc->beta, om = sc->omega;
+  const double* in[7];
+  if (ST == 0) {
+    in[0] = V.r; in[1] = V.g; in[2] = V.s; in[3] = A.dinv;
+  } else if (ST == 1) {
+    in[0] = V.r; in[1] = V.s; in[2] = A.dinv;
+  } else {
+    in[0] = V.r; in[1] = V.s; in[2] = V.x; in[3] = V.mv; in[4] = V.nv; in[5] = V.z1;
+    in[6] = V.rh;
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_barrier_init();
+  }
+  __syncthreads();
+  const int64_t nch = (A.n + CST_R - 1) / CST_R;
+  auto stage = [&](int slot, int64_t c) {
+    const int64_t j0 = c * CST_R;
+    const int64_t rows = (A.n - j0) < CST_R ? (A.n - j0) : CST_R;
+    const uint32_t bytes = (uint32_t)((rows * 8 + 15) & ~15LL);  // vectors carry 2 slack rows
+    mbar_arrive_expect_tx(&bar[slot], bytes * (uint32_t)NIN);
+#pragma unroll
+    for (int v = 0; v < NIN; ++v)
+      bulk_g2s(buf + ((size_t)slot * CST_NIN + v) * CST_R, in[v] + j0, bytes, &bar[slot]);
+  };
+  Dd acc[2] = {dd_zero(), dd_zero()};
+  if (tid == 0 && (int64_t)blockIdx.x < nch) stage(0, blockIdx.x);
+  uint32_t ph = 0;
+  int slot = 0;
+  for (int64_t c = blockIdx.x; c < nch; c += gridDim.x, slot ^= 1) {
+    if (tid == 0 && c + gridDim.x < nch) stage(slot ^ 1, c + gridDim.x);
+    mbar_wait(&bar[slot], (ph >> slot) & 1u);
+    ph ^= 1u << slot;
+    const int64_t j = c * CST_R + 2 * tid;
+    if (j < A.n) {
+      const bool valid1 = j + 1 < A.n;
+      const double* B = buf + (size_t)slot * CST_NIN * CST_R + 2 * tid;
+      double x0[NIN], x1[NIN];
+#pragma unroll
+      for (int v = 0; v < NIN; ++v) {
+        const double2 q = *reinterpret_cast<const double2*>(B + (size_t)v * CST_R);
+        x0[v] = q.x;
+        x1[v] = q.y;
+      }
+      double o0[2] = {0.0, 0.0}, o1[2] = {0.0, 0.0};
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const double* xv = e == 0 ? x0 : x1;
+        double* o = e == 0 ? o0 : o1;
+        if (e == 1 && !valid1) break;
+        if (ST == 0) {  // c_cl_p
+          const double pn = xv[0] + be * (xv[1] - om * xv[2]);
+          o[0] = pn;
+          o[1] = xv[3] * pn;
+        } else if (ST == 1) {  // c_cl_u
+          o[0] = xv[2] * (xv[0] - al * xv[1]);
+        } else {  // c_cl_x
+          const double q = xv[0] - al * xv[1];
+          const double xn = (xv[2] + al * xv[3]) + om * xv[4];
+          const double rn = q - om * xv[5];
+          o[0] = xn;
+          o[1] = rn;
+          dd_fma(acc[0], xv[6], rn);
+          dd_fma(acc[1], rn, rn);
+        }
+      }
+      double* out[2];
+      if (ST == 0) { out[0] = V.g; out[1] = V.mv; }
+      else if (ST == 1) { out[0] = V.nv; out[1] = V.nv; }
+      else { out[0] = V.x; out[1] = V.r; }
+      constexpr int NOUT = ST == 1 ? 1 : 2;
+#pragma unroll
+      for (int k = 0; k < NOUT; ++k) {
+        if (valid1) __stcs(reinterpret_cast<double2*>(out[k] + j), make_double2(o0[k], o1[k]));
+        else __stcs(out[k] + j, o0[k]);
+      }
+    }
+    __syncthreads();  // this slot is free for the chunk after next
+  }
+  if (ST == 2) {
+    Dd tot[2];
+    if (dd_grid_reduce<2>(acc, part, &sc->counter[T_CL3], tot) && threadIdx.x == 0)
+      publish<F_CL3>(sc, h, tot);
+  }
+}
+
 // p-CG iteration (reading A19) after n_i = A m_i (SP_PCN): buffers z -> z0,
 // q -> l, s, p -> g, x, r, u -> k, w -> w0, n -> z1, m -> mv (written for the
 // next SpMV); the next iteration's (r,u), (w,u), ||r||^2

@@ -390,19 +390,26 @@ void launch_csr(pbicg_ctx* h, Phase p) {
   switch (p) {
     case PH_CCP: {
       LaunchScope ls(h, K_CL1);
-      if (h->csr.bj > 1) c_cl_p<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      const bool ring = h->csr.bj <= 1 && h->cst_ok && h->cst_on;  // TMA chunk ring
+      if (ring) c_cl_tma<0><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else if (h->csr.bj > 1) c_cl_p<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
       else c_cl_p<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
     case PH_SP_CLS: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_CLS>(h); } break;
     case PH_CCU: {
       LaunchScope ls(h, K_CL2);
-      if (h->csr.bj > 1) c_cl_u<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      const bool ring = h->csr.bj <= 1 && h->cst_ok && h->cst_on;
+      if (ring) c_cl_tma<1><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else if (h->csr.bj > 1) c_cl_u<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
       else c_cl_u<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
     case PH_SP_CLY: { LaunchScope ls(h, K_SPMVD); launch_spmv<SP_CLY>(h); } break;
     case PH_CCX: {
       LaunchScope ls(h, K_CL3);
-      c_cl_x<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      if (h->cst_ok && h->cst_on)  // no M^-1 here: the ring serves every preconditioner
+        c_cl_tma<2><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else
+        c_cl_x<<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
     } break;
     case PH_SP_PCW0: { LaunchScope ls(h, K_INIT); launch_spmv<SP_PCW0>(h); } break;
     case PH_SP_PCN: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_PCN>(h); } break;
@@ -1881,6 +1888,9 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<0, true, true>, SM, sm);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, false, true>, SM, sm);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(c_sweep_tma<1, true, true>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_cl_tma<0>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_cl_tma<1>, SM, sm);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(c_cl_tma<2>, SM, sm);
     const int64_t nch = (n + CST_R - 1) / CST_R;
     h->cst_grid = (int)(nch < h->num_sm ? nch : h->num_sm);
     h->cst_ok = e == cudaSuccess && h->H % 2 == 0;  // 16-byte aligned row pairs
