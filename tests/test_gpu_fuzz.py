@@ -32,7 +32,11 @@ def rand_coef(rng, dim, spd):
 
 
 def bitwise_above_floor(res, ref):
-    k = np.nonzero(ref.rnorm < 1e-16 * ref.rnorm[0])[0]
+    """Bitwise while ||r_i|| >= 1e-14 ||r_0|| (~90 eps; DESIGN.md 'parity rule at the
+    noise floor'): a stagnating recursive residual plateaus a few eps sqrt(n) above
+    1e-16 (case stencil[2366]: 800 rows, flat at 1.02e-15), where it is accumulated
+    rounding and Dot2 of noise vectors depends on the summation order."""
+    k = np.nonzero(ref.rnorm < 1e-14 * ref.rnorm[0])[0]
     k = int(k[0]) if k.size else min(res.iters, ref.iters) + 1
     assert np.array_equal(res.rnorm[:k], ref.rnorm[:k])
 
