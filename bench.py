@@ -135,9 +135,45 @@ def csr_matrix(cfg):
     return _CSR_CACHE[cfg.name]
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+class PinnedCore:
+    """Pin the calling thread to one core (the oracle is single-threaded) for the
+    duration of the sample, like `taskset -c <core>`; restores the old mask."""
+
+    def __enter__(self):
+        self.old = None
+        self.core = None
+        try:
+            self.old = os.sched_getaffinity(0)
+            self.core = max(self.old)  # the highest core: away from the driver threads
+            os.sched_setaffinity(0, {self.core})
+        except (AttributeError, OSError):
+            self.old = None
+        return self
+
+    def __exit__(self, *a):
+        if self.old is not None:
+            os.sched_setaffinity(0, self.old)
+
+
 def oracle_sample(st, maxit_sample: int, nz_sample: int, cfg=None, method="pbicgstab"):
-    """Time the oracle (1 core) on an nx*ny*nz_sample slab of the workload
+    """Time the oracle (1 core, pinned) on an nx*ny*nz_sample slab of the workload
     (CSR: the full matrix for maxit_sample iterations)."""
+    with PinnedCore():
+        return _oracle_sample(st, maxit_sample, nz_sample, cfg, method)
+
+
+def _oracle_sample(st, maxit_sample, nz_sample, cfg, method):
     from oracle import oracle as orc
     solve = {"pbicgstab": orc.pbicgstab, "bicgstab": orc.bicgstab, "pipecg": orc.pipecg}[method]
     if isinstance(st, CsrShape):
@@ -200,7 +236,8 @@ def run_reference(args, rank, world):
             "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": n_full,
                                             "maxit": maxit, "rr_period": rr},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu": cpu_model(),
+                             "pinning": "sched_setaffinity to one core (taskset -c)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -413,6 +450,7 @@ def run_ours(args, rank, world):
         rows_per_s, n_s, its, t = oracle_sample(st, 6 if st.dim else 3, 64, cfg, args.method)
         line["cpu_baseline"] = {
             "value": rows_per_s / st.n, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu": cpu_model(), "pinning": "sched_setaffinity to one core (taskset -c)",
             "sample": f"oracle {args.method} (C, 1 core) on {sample_desc(st, cfg)} "
                       f"({n_s} rows), {its} iterations in {t:.1f} s, scaled by rows to {st.n}"}
     print(json.dumps(line), flush=True)
@@ -448,6 +486,29 @@ def run_loopback(args):
                       "iterations_per_s": args.steps * maxit / dt, "iters": r.iters}), flush=True)
     G.close()
     return 0
+
+
+def relaunch_under_torchrun(n: int) -> int:
+    """`bench.py --gpus N` started without torchrun: re-exec this command as N ranks
+    (one process per GPU, NCCL over NVLink) exactly as the driver launches it;
+    rank 0 prints the JSON line.  NCCL's own log level is left to the caller."""
+    import socket
+    try:
+        import torch
+        have = torch.cuda.device_count()
+    except Exception:
+        have = 0
+    if have < n:
+        print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}", file=sys.stderr)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -488,9 +549,10 @@ def main():
         args.warmup = 3
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if args.gpus != world and args.impl == "ours":
-        print(f"note: --gpus {args.gpus} but WORLD_SIZE={world}; launch with torchrun for N>1",
-              file=sys.stderr)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_under_torchrun(args.gpus)
+    if args.gpus != world:
+        print(f"note: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if args.loopback:

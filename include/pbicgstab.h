@@ -56,10 +56,12 @@ typedef enum {
  *                            of A over rows [kb, (k+1)b) (global numbering), each
  *                            inverted once by Gauss-Jordan elimination without
  *                            pivoting; (M^-1 v)_i = sum_k inv_ik v_{kb+k}, ascending k.
- *                            CSR operators only (stencils: EINVAL); every rank's
- *                            row_begin and n_local must be multiples of b; a zero
- *                            pivot is EINVAL.  Costs b-1 extra doubles per row read
- *                            in each kernel that applies M^-1. */
+ *                            CSR: b in {2,4,8,16,32}, every rank's row_begin and
+ *                            n_local multiples of b, all three methods.  Stencils:
+ *                            b in {2,4,8}, nx % b == 0, full-line TMA tiles (nx <=
+ *                            1024 in 2D, ~850 in 3D), method 0 only (EINVAL
+ *                            otherwise).  A zero pivot is EINVAL.  Costs b-1 extra
+ *                            doubles per row read in each kernel that applies M^-1. */
 typedef enum { PBICG_PREC_JACOBI = 1, PBICG_PREC_BLOCK_JACOBI = 0x100 } pbicg_prec;
 #define PBICG_PREC_BJ(b) ((pbicg_prec)(PBICG_PREC_BLOCK_JACOBI | (b)))
 
@@ -97,6 +99,13 @@ typedef struct {
 /* Multi-GPU description (one process per GPU).  NULL => single GPU.
  * nccl_id_halo / nccl_id_red: 128-byte ncclUniqueId blobs from
  * pbicgstab_get_unique_id() on rank 0, broadcast to all ranks by the caller.
+ * nccl_id_red may be NULL (one communicator; the reductions then block the compute
+ * stream: option "overlap" is forced to 0).  The reduction communicator is created
+ * with ncclCommInitRankConfig and maxCTAs = 2 (tiny payloads), its side stream with
+ * the highest stream priority.  nranks == 1 WITH an nccl_id_halo creates a one-rank
+ * NCCL job that runs the multi-rank schedule (rank-row all-reduce, empty halo
+ * groups, finalize kernels, peer-memory transport) -- bitwise equal to the plain
+ * single-GPU path; nranks == 1 with a NULL id is the plain single-GPU path.
  * Stencils are split into contiguous z-slabs (3D) / y-slabs (2D) chosen by the
  * library (pbicgstab_local_rows reports them); CSR uses the caller's rows. */
 typedef struct {
@@ -105,10 +114,14 @@ typedef struct {
   const void* nccl_id_red;
 } pbicg_dist;
 
-/* Create a solver for a stencil operator.  `cuda_stream` (cudaStream_t or NULL
- * for the legacy default stream) is the stream every kernel of this handle is
- * launched on.  Allocates the device workspace (12 fp64 vectors of n_local rows
- * plus ghost planes).  Errors: EINVAL (dim not 2/3, nx/ny/nz < 1, coef[0] == 0,
+/* Create a solver for a stencil operator.  `cuda_stream` is the cudaStream_t every
+ * kernel and copy of this handle is enqueued on; NULL => the handle creates (and
+ * owns) a private cudaStreamNonBlocking stream, and every entry point that reads
+ * caller memory first orders that stream after the legacy default stream (event
+ * record on stream 0 + wait), so data written there before the call is visible.
+ * Create-time uploads run on the handle's stream and finish before create returns.
+ * Allocates the device workspace (14 fp64 vectors of n_local rows plus ghost
+ * planes).  Errors: EINVAL (dim not 2/3, nx/ny/nz < 1, coef[0] == 0,
  * nranks/rank inconsistent), ECUDA, ENOMEM, ENCCL. */
 pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
                                       const pbicg_dist* dist, void* cuda_stream,

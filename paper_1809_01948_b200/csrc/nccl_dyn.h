@@ -14,6 +14,8 @@ struct NcclApi {
   std::string err;
   ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  // optional (NCCL >= 2.14): communicator limits (maxCTAs of the reduction comm)
+  ncclResult_t (*CommInitRankConfig)(ncclComm_t*, int, ncclUniqueId, int, ncclConfig_t*) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
@@ -57,6 +59,8 @@ inline NcclApi& nccl_api() {
   NCCL_SYM(GroupEnd, "ncclGroupEnd");
   NCCL_SYM(GetErrorString, "ncclGetErrorString");
 #undef NCCL_SYM
+  api.CommInitRankConfig = reinterpret_cast<decltype(api.CommInitRankConfig)>(
+      dlsym(lib, "ncclCommInitRankConfig"));
   api.ok = true;
   return api;
 }

@@ -104,6 +104,7 @@ struct pbicg_ctx {
   int grid[16] = {0};
   // distribution
   int nranks = 1, rank = 0;
+  bool dist = false;  // rank-row exchange path: nranks > 1, or an NCCL communicator of 1 rank
   int comm = COMM_NONE;
   ncclComm_t nccl_halo = nullptr, nccl_red = nullptr;
   pbicg_group* group = nullptr;
@@ -198,6 +199,17 @@ pbicg_status gvec(pbicg_ctx* h, double** out) {
   ST(dalloc(h, &p, n * sizeof(double)));
   CU(cudaMemsetAsync(p, 0, n * sizeof(double), h->stream));
   *out = (double*)p + h->H;
+  return PBICG_OK;
+}
+
+// Create-time host->device upload.  Every create-time write goes through the
+// handle's stream (a cudaStreamNonBlocking stream when the caller passes NULL),
+// and the stream is drained before the call returns: a plain cudaMemcpy runs on
+// the legacy default stream, which is NOT ordered against that stream, so it
+// could land before gvec()'s zero-fill of the same buffer (dinv_g).
+pbicg_status upload(pbicg_ctx* h, void* dst, const void* src, size_t bytes) {
+  CU(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
   return PBICG_OK;
 }
 
@@ -578,7 +590,7 @@ using VecSel = std::function<double*(pbicg_ctx*)>;
 // the owner's is zero in red_send, so the sum adds exact zeros)
 void comm_reduce(const Members& G, bool on_side) {
   pbicg_ctx* h0 = G[0];
-  if (h0->nranks == 1) return;
+  if (!h0->dist) return;
   if (h0->p2p) return;  // the producing kernels already stored into every rank's buffer
   if (h0->comm == COMM_NCCL) {
     pbicg_ctx* h = h0;
@@ -603,7 +615,7 @@ bool fused_halo(const pbicg_ctx* h) {
 // nearest-neighbour ghost exchange of halo_n rows per side for each vector
 void comm_halo(const Members& G, std::initializer_list<VecSel> sels) {
   pbicg_ctx* h0 = G[0];
-  if (h0->nranks == 1) return;
+  if (!h0->dist) return;
   h0->halo_ops++;
   if (h0->comm == COMM_NCCL) {
     pbicg_ctx* h = h0;
@@ -656,11 +668,11 @@ void each(const Members& G, Phase p) {
   for (pbicg_ctx* h : G) launch(h, p);
 }
 void each_fin(const Members& G, int f) {
-  if (G[0]->nranks == 1) return;
+  if (!G[0]->dist) return;
   for (pbicg_ctx* h : G) launch_fin(h, f);
 }
 void reduce_fin(const Members& G, int f) {
-  if (G[0]->nranks == 1) return;
+  if (!G[0]->dist) return;
   comm_reduce(G, false);
   each_fin(G, f);
 }
@@ -686,7 +698,7 @@ const VecSel SNVv = [](pbicg_ctx* h) { return h->V.nv; };
 const VecSel SMVv = [](pbicg_ctx* h) { return h->V.mv; };
 
 void enq_iter_classic_csr(const Members& G) {
-  const bool dist = G[0]->nranks > 1;
+  const bool dist = G[0]->dist;
   each(G, PH_CCP);  // l.17 (previous i) + l.4: p_i, M^-1 p_i
   if (dist) comm_halo(G, {SMVv});
   each(G, PH_SP_CLS);  // l.5-6: s_i, (r^0, s_i) -> alpha
@@ -704,7 +716,7 @@ void enq_iter_classic_csr(const Members& G) {
 // the all-reduce of {(r,u),(w,u),||r||} overlaps that SpMV -- the point of p-CG
 void enq_iter_pipecg_csr(const Members& G) {
   pbicg_ctx* h0 = G[0];
-  const bool dist = h0->nranks > 1;
+  const bool dist = h0->dist;
   each(G, PH_CPC);
   if (!dist) {
     each(G, PH_SP_PCN);
@@ -719,7 +731,7 @@ void enq_iter_pipecg_csr(const Members& G) {
 }
 
 void enq_init_classic(const Members& G) {
-  const bool dist = G[0]->nranks > 1;
+  const bool dist = G[0]->dist;
   if (dist) comm_halo(G, {SX});
   each(G, PH_INIT1);  // r0 := b - A x0, r^0 := r0; rho_0, ||b|| (F_INIT1, method 1)
   reduce_fin(G, F_INIT1);
@@ -727,7 +739,7 @@ void enq_init_classic(const Members& G) {
 }
 
 void enq_iter_classic(const Members& G, int par) {
-  const bool dist = G[0]->nranks > 1;
+  const bool dist = G[0]->dist;
   each(G, PH_CL1);  // l.17 (previous i) + l.4-6: p_i, s_i, (r^0, s_i)
   if (dist) {
     comm_reduce(G, false);
@@ -743,7 +755,7 @@ void enq_iter_classic(const Members& G, int par) {
 
 // p-CG (method 2): one kernel and one reduction per iteration
 void enq_init_pipecg(const Members& G) {
-  const bool dist = G[0]->nranks > 1;
+  const bool dist = G[0]->dist;
   if (G[0]->kind == KIND_CSR) {
     if (dist) comm_halo(G, {SX});
     each(G, PH_INIT1);  // r0, u0 (k); ||r0||, ||b|| (F_INIT1, method 2)
@@ -766,7 +778,7 @@ void enq_init_pipecg(const Members& G) {
 }
 
 void enq_iter_pipecg(const Members& G, int par) {
-  const bool dist = G[0]->nranks > 1;
+  const bool dist = G[0]->dist;
   each(G, PH_PC);
   reduce_fin(G, F_PC);
   if (dist) comm_halo(G, {par ? SW0 : SW1});  // w_{i+1}
@@ -774,7 +786,7 @@ void enq_iter_pipecg(const Members& G, int par) {
 
 void enq_gap(const Members& G) {
   if (!G[0]->gap_on) return;
-  if (G[0]->nranks > 1) comm_halo(G, {SX});
+  if (G[0]->dist) comm_halo(G, {SX});
   each(G, PH_GAP);
   reduce_fin(G, F_GAP);
 }
@@ -782,7 +794,7 @@ void enq_gap(const Members& G) {
 // Alg. 2 lines 2-3 [+ gap of iteration 0]
 void enq_init(const Members& G) {
   pbicg_ctx* h0 = G[0];
-  const bool dist = h0->nranks > 1;
+  const bool dist = h0->dist;
   if (h0->method != M_PBICGSTAB) {
     if (h0->method == M_BICGSTAB) enq_init_classic(G);
     else enq_init_pipecg(G);
@@ -811,7 +823,7 @@ void enq_init(const Members& G) {
 // one iteration i (par = i & 1 selects the double-buffered w and z)
 void enq_iter(const Members& G, bool with_rr, int par) {
   pbicg_ctx* h0 = G[0];
-  const bool dist = h0->nranks > 1;
+  const bool dist = h0->dist;
   if (h0->method != M_PBICGSTAB) {
     if (h0->kind == KIND_CSR) {
       if (h0->method == M_BICGSTAB) enq_iter_classic_csr(G);
@@ -1209,7 +1221,9 @@ pbicg_status common_setup(pbicg_ctx* h, void* cuda_stream) {
     CU(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
     h->own_stream = true;
   }
-  CU(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+  int prio_lo = 0, prio_hi = 0;  // the reduction side stream: highest priority
+  CU(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CU(cudaStreamCreateWithPriority(&h->side, cudaStreamNonBlocking, prio_hi));
   CU(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_poll[0], cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&h->ev_poll[1], cudaEventDisableTiming));
@@ -1246,6 +1260,7 @@ pbicg_status alloc_common(pbicg_ctx* h) {
   memset(&s, 0, sizeof(s));
   s.nranks = h->nranks;
   s.rank = h->rank;
+  s.dist = h->dist;
   s.red_send = h->red_send;
   s.red_recv = h->red_recv;
   CU(cudaMemcpyAsync(h->scal, &s, sizeof(Scal), cudaMemcpyHostToDevice, h->stream));
@@ -1273,9 +1288,10 @@ pbicg_status p2p_alloc(pbicg_ctx* h) {
   ST(dalloc(h, &b, (size_t)2 * h->nranks * RED_K * sizeof(Dd)));
   ST(dalloc(h, &f, (size_t)h->nranks * sizeof(unsigned long long)));
   ST(dalloc(h, &e, sizeof(unsigned long long)));
-  CU(cudaMemset(b, 0, (size_t)2 * h->nranks * RED_K * sizeof(Dd)));
-  CU(cudaMemset(f, 0, (size_t)h->nranks * sizeof(unsigned long long)));
-  CU(cudaMemset(e, 0, sizeof(unsigned long long)));
+  CU(cudaMemsetAsync(b, 0, (size_t)2 * h->nranks * RED_K * sizeof(Dd), h->stream));
+  CU(cudaMemsetAsync(f, 0, (size_t)h->nranks * sizeof(unsigned long long), h->stream));
+  CU(cudaMemsetAsync(e, 0, sizeof(unsigned long long), h->stream));
+  CU(cudaStreamSynchronize(h->stream));
   h->p2p_buf = (Dd*)b;
   h->p2p_flags = (unsigned long long*)f;
   h->p2p_ep = (unsigned long long*)e;
@@ -1326,7 +1342,7 @@ pbicg_status p2p_setup(const Members& G) {
   void *dsend = nullptr, *drecv = nullptr;
   ST(dalloc(h, &dsend, hb));
   ST(dalloc(h, &drecv, hb * P));
-  CU(cudaMemcpy(dsend, &mine, hb, cudaMemcpyHostToDevice));
+  ST(upload(h, dsend, &mine, hb));
   NC(nccl_api().AllGather(dsend, drecv, hb, ncclChar, h->nccl_halo, h->stream));
   std::vector<Blob> all((size_t)P);
   CU(cudaStreamSynchronize(h->stream));
@@ -1369,6 +1385,14 @@ void set_peer_halo(pbicg_ctx* h, bool on) {
 }
 
 
+// NCCL communicators: the halo communicator with NCCL's defaults, the reduction
+// communicator (payload 32-256 B per rank) limited to NCCL_RED_MAX_CTAS CTAs so the
+// all-reduce on the side stream takes as few SMs as possible from the concurrent
+// sweep / SpMV; the side stream has the device's highest priority.
+// A pbicg_dist of ONE rank with an id is a real one-rank NCCL job: the same
+// rank-row exchange and finalize kernels run (tests exercise the NCCL calls, graph
+// capture of NCCL nodes and the peer-memory setup on one GPU).
+#define NCCL_RED_MAX_CTAS 2
 pbicg_status nccl_setup(pbicg_ctx* h, const pbicg_dist* d) {
   auto& api = nccl_api();
   if (!api.ok) return fail(h, PBICG_ESTATE, api.err);
@@ -1378,12 +1402,20 @@ pbicg_status nccl_setup(pbicg_ctx* h, const pbicg_dist* d) {
   NC(api.CommInitRank(&h->nccl_halo, d->nranks, id, d->rank));
   if (d->nccl_id_red) {
     memcpy(&id, d->nccl_id_red, sizeof(id));
-    NC(api.CommInitRank(&h->nccl_red, d->nranks, id, d->rank));
+    if (api.CommInitRankConfig) {
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.minCTAs = 1;
+      cfg.maxCTAs = NCCL_RED_MAX_CTAS;
+      NC(api.CommInitRankConfig(&h->nccl_red, d->nranks, id, d->rank, &cfg));
+    } else {
+      NC(api.CommInitRank(&h->nccl_red, d->nranks, id, d->rank));
+    }
   } else {
     h->nccl_red = h->nccl_halo;
     h->overlap = 0;  // one communicator: its operations must stay on one stream
   }
   h->comm = COMM_NCCL;
+  h->dist = true;
   return PBICG_OK;
 }
 
@@ -1764,7 +1796,7 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     ST(block_inverse(op, bj, &inv));
     void* pb = nullptr;
     ST(dalloc(h, &pb, inv.size() * sizeof(double)));
-    CU(cudaMemcpy(pb, inv.data(), inv.size() * sizeof(double), cudaMemcpyHostToDevice));
+    ST(upload(h, pb, inv.data(), inv.size() * sizeof(double)));
     h->csr.binv = (const double*)pb;
   }
   h->csr.bj = bj;
@@ -1797,12 +1829,12 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
   ST(dalloc(h, &pc, ecol.size() * sizeof(int32_t)));
   ST(dalloc(h, &pv, eval.size() * sizeof(double)));
   if (!uniform) ST(dalloc(h, &pl, (size_t)n * sizeof(int32_t)));
-  CU(cudaMemcpy(pc, ecol.data(), ecol.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(pv, eval.data(), eval.size() * sizeof(double), cudaMemcpyHostToDevice));
+  ST(upload(h, pc, ecol.data(), ecol.size() * sizeof(int32_t)));
+  ST(upload(h, pv, eval.data(), eval.size() * sizeof(double)));
   if (!uniform)
-    CU(cudaMemcpy(pl, elen.data(), (size_t)n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    ST(upload(h, pl, elen.data(), (size_t)n * sizeof(int32_t)));
   ST(gvec(h, &h->dinv_g));
-  CU(cudaMemcpy(h->dinv_g, dinv.data(), (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
+  ST(upload(h, h->dinv_g, dinv.data(), (size_t)n * sizeof(double)));
   h->csr.n = n;
   h->csr.width = (int32_t)width;
   h->csr.col = (const int32_t*)pc;
@@ -1847,8 +1879,8 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     void *psv = nullptr, *psd = nullptr;
     ST(dalloc(h, &psv, sval.size() * sizeof(double)));
     ST(dalloc(h, &psd, sdcol.size() * sizeof(int16_t)));
-    CU(cudaMemcpy(psv, sval.data(), sval.size() * sizeof(double), cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(psd, sdcol.data(), sdcol.size() * sizeof(int16_t), cudaMemcpyHostToDevice));
+    ST(upload(h, psv, sval.data(), sval.size() * sizeof(double)));
+    ST(upload(h, psd, sdcol.data(), sdcol.size() * sizeof(int16_t)));
     h->csr.sval = (const double*)psv;
     h->csr.sdcol = (const int16_t*)psd;
     WinGeo& w = h->wg;
@@ -1997,6 +2029,7 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
     s0.ar_tau = std::sqrt(s0.ar_eps);
     s0.nranks = m->nranks;
     s0.rank = m->rank;
+    s0.dist = m->dist;
     s0.red_send = m->red_send;
     s0.red_recv = m->red_recv;
     m->scal_host[0] = s0;
@@ -2092,7 +2125,7 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
   h->nranks = nranks;
   h->rank = dist ? dist->rank : 0;
   pbicg_status st = common_setup(h, cuda_stream);
-  if (!st && nranks > 1) st = nccl_setup(h, dist);
+  if (!st && (nranks > 1 || (dist && dist->nccl_id_halo))) st = nccl_setup(h, dist);
   if (!st) st = build_stencil(h, op, bj);
   if (st) {
     g_create_err = h->err;
@@ -2121,9 +2154,9 @@ pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pb
   h->nranks = nranks;
   h->rank = dist ? dist->rank : 0;
   pbicg_status st = common_setup(h, cuda_stream);
-  if (!st && nranks > 1) st = nccl_setup(h, dist);
+  if (!st && (nranks > 1 || (dist && dist->nccl_id_halo))) st = nccl_setup(h, dist);
   if (!st) st = build_csr(h, op, dinv, width, uniform, bj);
-  if (!st && nranks > 1) {  // dinv ghosts, once (collective)
+  if (!st && h->dist) {  // dinv ghosts, once (collective)
     comm_halo(Members{h}, {[](pbicg_ctx* c) { return c->dinv_g; }});
     cudaError_t e = cudaStreamSynchronize(h->stream);
     if (e != cudaSuccess) st = fail(h, PBICG_ECUDA, cudaGetErrorString(e));
@@ -2157,6 +2190,7 @@ pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_pr
     h->nranks = nranks;
     h->rank = r;
     h->comm = COMM_LOOP;
+    h->dist = nranks > 1;
     h->group = grp;
     grp->m.push_back(h);
     grp->alive++;
@@ -2204,6 +2238,7 @@ pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec
     h->nranks = nranks;
     h->rank = r;
     h->comm = COMM_LOOP;
+    h->dist = nranks > 1;
     h->group = grp;
     grp->m.push_back(h);
     grp->alive++;
@@ -2263,7 +2298,8 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
   if (k == "transport") {  // collective for NCCL ranks; applies to every loopback member
     if (value < 0 || value > 1) return fail(h, PBICG_EINVAL, "transport must be 0 or 1");
     if (value == 1) {
-      if (h->nranks == 1) return fail(h, PBICG_EINVAL, "transport 1 needs several ranks");
+      if (!h->dist)
+        return fail(h, PBICG_EINVAL, "transport 1 needs several ranks (or an NCCL communicator)");
       ST(p2p_setup(members(h)));
     }
     for (pbicg_ctx* m : members(h)) {
@@ -2496,6 +2532,7 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "rr2") b = 5 * 8 * N;      // read r,s,r^; write w,z
     else if (n == "gap") b = 3 * 8 * N;
     else if (n == "apply") b = 2 * 8 * N;
+    else if (n == "init") b = 4 * 8 * N;     // mean of init1 (x,b -> r,r^,k) and init2 (r,r^ -> w)
     else if (n == "iteration") b = 24 * 8 * N;
   } else {
     const double slots = (double)h->csr.width;  // ELL width
@@ -2510,6 +2547,7 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (h->method == M_BICGSTAB && n == "spmvD") b = matw + 4 * 8 * N;  // nv in; y out; r, s
     else if (n == "spmvB" || n == "spmvD") b = matw + 2 * 8 * N;  // n|m in, out
     else if (n == "apply") b = mat + 2 * 8 * N;
+    else if (n == "init") b = matw + 4 * 8 * N;  // mean of the two init SpMVs (x0 -> r,r^,k; k -> w,m)
     else if (n == "sweepC") b = 17 * 8 * N + pb;  // read x,g,k,l,r,s,w,z,t,v,r^,dinv; write x,r,k,w,m
     else if (n == "rr1") b = 2 * mat + 8 * 8 * N;
     else if (n == "rr2") b = 2 * mat + 7 * 8 * N;

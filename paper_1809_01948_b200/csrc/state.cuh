@@ -50,6 +50,8 @@ struct Scal {
   double nP_[6];                   // previous iteration: g, s, l, z, n, v
   double nX0, nK0;                 // init: ||x_0||, ||k_0||
   int32_t nranks, rank;
+  int32_t dist;                    // rank-row exchange + finalize kernel (nranks > 1, or an
+                                   // NCCL communicator of one rank)
   Dd* red_send;                    // [nranks][RED_K]: only row `rank` is ever written
   Dd* red_recv;                    // [nranks][RED_K]: all rows after the exchange
   // peer-memory transport (option "transport" 1): the last CTA of a reducing kernel
@@ -357,7 +359,7 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 template <int F, int K>
 __device__ __forceinline__ void publish(Scal* sc, Hist h, const Dd (&tot)[K]) {
-  if (sc->nranks > 1 && sc->p2p) {
+  if (sc->dist && sc->p2p) {
     // every rank performs the same reductions in the same order: the epoch numbers
     // them identically on all ranks
     const unsigned long long e = *sc->p2p_epoch + 1;
@@ -370,7 +372,7 @@ __device__ __forceinline__ void publish(Scal* sc, Hist h, const Dd (&tot)[K]) {
     }
     __threadfence_system();
     for (int q = 0; q < P; ++q) st_release_sys(sc->p2p_flag[q] + sc->rank, e);
-  } else if (sc->nranks > 1) {
+  } else if (sc->dist) {
     Dd* row = sc->red_send + (size_t)sc->rank * RED_K;
 #pragma unroll
     for (int k = 0; k < K; ++k) row[k] = tot[k];
