@@ -36,6 +36,7 @@
 #define ORC_PLAIN_DOT 2  /* plain left-to-right dot instead of Dot2 (diagnostic) */
 #define ORC_GAP 4        /* compute the residual gap history */
 #define ORC_AUTO_RR 8    /* automated replacement: bound f^r_i (eq:DDr_bound) + eq:criterion */
+#define ORC_ILU0 16      /* preconditioner ILU(0) (= ICC(0) for symmetric A), reading A34 */
 
 #define OUT_CONVERGED 0
 #define OUT_MAXIT 1
@@ -116,7 +117,64 @@ typedef struct {
   int64_t n;
   int b;
   double* inv; /* b = 1: dinv[n]; else row-major [n][b]: row i of its block's inverse */
+  /* ILU(0) (b = 0): the factors on the pattern of the preconditioner matrix */
+  const int64_t* rp;
+  const int64_t* ci;
+  double* lu;   /* strictly lower part: multipliers l_ik; upper part: u_ij; diagonal: u_ii */
 } Prec;
+
+/* ------------------------------------------------------------------------- */
+/* ILU(0) / ICC(0) (Table 1 "Precond." ICC(0); "incomplete Cholesky  */
+/* preconditioner with zero fill-in"; reading A34).  */
+/* The incomplete factorisation with the sparsity pattern of A (no fill):        */
+/* Saad's IKJ variant of Gaussian elimination restricted to the pattern --       */
+/*   for i = 0..n-1:                                                             */
+/*     for k < i with (i,k) in NZ, ascending:  a_ik := a_ik * uinv_k             */
+/*       for j > k with (k,j) in NZ, ascending: if (i,j) in NZ:                  */
+/*                                               a_ij := a_ij - a_ik * a_kj      */
+/*     uinv_i := 1 / a_ii                                                        */
+/* giving M = L U (L unit lower triangular with the multipliers l_ik, U upper    */
+/* with u_ij); for symmetric A this M is the incomplete Cholesky (ICC(0)) M =     */
+/* L~ L~^T in root-free form (L~ = L diag(u)^{1/2}).  The pivots are applied as   */
+/* reciprocals (uinv, as the Jacobi dinv of A3).  M^{-1} v: forward              */
+/* y_i = v_i - sum_{k<i} l_ik y_k, then backward x_i = (y_i - sum_{j>i} u_ij x_j) */
+/* * uinv_i, every row summed in ascending column order (A5).  Returns -1 on a   */
+/* missing or zero pivot. */
+int orc_ilu0_factor(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
+                    double* lu, double* uinv) {
+  for (int64_t p = 0; p < rp[n]; ++p) lu[p] = va[p];
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t p = rp[i]; p < rp[i + 1] && ci[p] < i; ++p) {
+      const int64_t k = ci[p];
+      lu[p] = lu[p] * uinv[k];
+      for (int64_t q = rp[k]; q < rp[k + 1]; ++q) {
+        if (ci[q] <= k) continue;
+        for (int64_t p2 = rp[i]; p2 < rp[i + 1]; ++p2)
+          if (ci[p2] == ci[q]) { lu[p2] = lu[p2] - lu[p] * lu[q]; break; }
+      }
+    }
+    double d = 0.0;
+    int found = 0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p)
+      if (ci[p] == i) { d = lu[p]; found = 1; }
+    if (!found || d == 0.0 || !isfinite(d)) return -1;
+    uinv[i] = 1.0 / d;
+  }
+  return 0;
+}
+
+/* The matrix whose ILU(0) defines M (NULL: A itself).  Test infrastructure sets it
+ * to the block-diagonal part of A over the ranks' row blocks for the multi-rank
+ * reading of A34 (each rank factorises its own diagonal block). */
+static int64_t g_pm_n = -1;
+static const int64_t *g_pm_rp = 0, *g_pm_ci = 0;
+static const double* g_pm_va = 0;
+void orc_set_prec_matrix(int64_t n, const int64_t* rp, const int64_t* ci, const double* va) {
+  g_pm_n = rp ? n : -1;
+  g_pm_rp = rp;
+  g_pm_ci = ci;
+  g_pm_va = va;
+}
 
 #define ORC_BLOCK(flags) (((flags) >> 8) & 0xff)
 
@@ -150,6 +208,19 @@ static int prec_make(int32_t flags, int64_t n, const int64_t* rp, const int64_t*
   const int b = ORC_BLOCK(flags) > 1 ? ORC_BLOCK(flags) : 1;
   P->n = n;
   P->b = b;
+  P->lu = 0;
+  if (flags & ORC_ILU0) {
+    if (g_pm_rp && g_pm_n == n) { rp = g_pm_rp; ci = g_pm_ci; va = g_pm_va; }
+    P->b = 0;
+    P->rp = rp;
+    P->ci = ci;
+    P->inv = (double*)calloc((size_t)(n > 0 ? n : 1), sizeof(double));
+    P->lu = (double*)calloc((size_t)(rp[n] > 0 ? rp[n] : 1), sizeof(double));
+    if (orc_ilu0_factor(n, rp, ci, va, P->lu, P->inv) != 0) {
+      free(P->lu); free(P->inv); P->lu = 0; return -1;
+    }
+    return 0;
+  }
   P->inv = (double*)calloc((size_t)(n > 0 ? n : 1) * (size_t)b, sizeof(double));
   if (b == 1) {
     if (orc_jacobi_dinv(n, rp, ci, va, P->inv) != 0) { free(P->inv); return -1; }
@@ -175,6 +246,21 @@ static int prec_make(int32_t flags, int64_t n, const int64_t* rp, const int64_t*
 /* v := M^{-1} u */
 static void pprec(const Prec* P, const double* u, double* v) {
   const int b = P->b;
+  if (b == 0) { /* ILU(0): forward then backward substitution (A34) */
+    for (int64_t i = 0; i < P->n; ++i) {
+      double acc = u[i];
+      for (int64_t p = P->rp[i]; p < P->rp[i + 1] && P->ci[p] < i; ++p)
+        acc = acc - P->lu[p] * v[P->ci[p]];
+      v[i] = acc;
+    }
+    for (int64_t i = P->n - 1; i >= 0; --i) {
+      double acc = v[i];
+      for (int64_t p = P->rp[i]; p < P->rp[i + 1]; ++p)
+        if (P->ci[p] > i) acc = acc - P->lu[p] * v[P->ci[p]];
+      v[i] = acc * P->inv[i];
+    }
+    return;
+  }
   if (b == 1) {
     for (int64_t j = 0; j < P->n; ++j) v[j] = P->inv[j] * u[j];
     return;
@@ -215,13 +301,18 @@ static double prec_norm_bound(const Prec* P) {
   return mx;
 }
 
+static void prec_free(Prec* P) {
+  free(P->inv);
+  if (P->lu) free(P->lu);
+}
+
 /* v := M^{-1} u for tests (flags as the solvers'); -1 if M cannot be formed. */
 int orc_prec_apply(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
                    int32_t flags, const double* u, double* v) {
   Prec P;
   if (prec_make(flags, n, rp, ci, va, &P) != 0) return -1;
   pprec(&P, u, v);
-  free(P.inv);
+  prec_free(&P);
   return 0;
 }
 
@@ -342,6 +433,8 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
                   double* sc_trace, double* vec_trace, double* bound_trace,
                   int32_t* rr_list, int32_t* n_rr) {
   if (n < 0 || maxit < 0 || rr_period < 0) return -2;
+  /* the run-time bound needs mu~ and ||M^-1|| (A29); not defined here for ILU(0) */
+  if ((flags & ORC_AUTO_RR) && (flags & ORC_ILU0)) return -3;
   Prec P;
   if (prec_make(flags, n, rp, ci, va, &P) != 0) return -1;
   double *r = vec(n), *rh = vec(n), *k = vec(n), *w = vec(n), *m = vec(n), *t = vec(n);
@@ -558,7 +651,7 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
   *iters_out = iters;
   *outcome_out = outcome;
   if (n_rr) *n_rr = nrr;
-  free(P.inv); free(r); free(rh); free(k); free(w); free(m); free(t); free(g); free(s);
+  prec_free(&P); free(r); free(rh); free(k); free(w); free(m); free(t); free(g); free(s);
   free(l); free(z); free(nn); free(v); free(q); free(u); free(y); free(tmp);
   return 0;
 }
@@ -621,7 +714,7 @@ int orc_bicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double* 
   }
   *iters_out = iters;
   *outcome_out = outcome;
-  free(P.inv); free(r); free(rh); free(p); free(g); free(s); free(q); free(u); free(y); free(tmp);
+  prec_free(&P); free(r); free(rh); free(p); free(g); free(s); free(q); free(u); free(y); free(tmp);
   return 0;
 }
 
@@ -666,7 +759,7 @@ int orc_pcg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va,
   }
   *iters_out = iters;
   *outcome_out = outcome;
-  free(P.inv); free(r); free(u); free(p); free(s); free(tmp);
+  prec_free(&P); free(r); free(u); free(p); free(s); free(tmp);
   return 0;
 }
 
@@ -726,7 +819,7 @@ int orc_pipecg(int64_t n, const int64_t* rp, const int64_t* ci, const double* va
   }
   *iters_out = iters;
   *outcome_out = outcome;
-  free(P.inv); free(r); free(u); free(w); free(m); free(nn); free(z); free(q); free(s); free(p);
+  prec_free(&P); free(r); free(u); free(w); free(m); free(nn); free(z); free(q); free(s); free(p);
   free(tmp);
   return 0;
 }

@@ -21,6 +21,7 @@ BENCH = 1
 PLAIN_DOT = 2
 GAP = 4
 AUTO_RR = 8
+ILU0 = 16
 NTRACE = 15
 TRACE_NAMES = ["x", "r", "k", "w", "m", "t", "g", "s", "l", "z", "q", "u", "y", "n", "v"]
 OUTCOMES = {0: "converged", 1: "maxit", 2: "breakdown"}
@@ -61,6 +62,10 @@ def lib():
         L.orc_anorm_bound.argtypes = [i64, P, P, P]
         L.orc_prec_apply.restype = ctypes.c_int
         L.orc_prec_apply.argtypes = [i64, P, P, P, i32, P, P]
+        L.orc_ilu0_factor.restype = ctypes.c_int
+        L.orc_ilu0_factor.argtypes = [i64, P, P, P, P, P]
+        L.orc_set_prec_matrix.restype = None
+        L.orc_set_prec_matrix.argtypes = [i64, P, P, P]
         L.orc_gauss_jordan.restype = ctypes.c_int
         L.orc_gauss_jordan.argtypes = [ctypes.c_int, P, P]
         L.orc_bicgstab.restype = ctypes.c_int
@@ -184,11 +189,49 @@ def _run(fn, A: CSR, b, x0, tol, maxit, flags, extra=(), want_sc=False, want_tra
                   None if rl is None else [int(v) for v in rl[:nrr.value]])
 
 
-def _blk(block: int) -> int:
-    """flags bits 8-15: block size of the block-Jacobi preconditioner (1 = Jacobi)."""
+def _blk(block) -> int:
+    """Preconditioner flags: an int = block size of the block-Jacobi preconditioner in
+    bits 8-15 (1 = Jacobi); "ilu0" / "icc0" = ILU(0) (ICC(0) for symmetric A, A34)."""
+    if block in ("ilu0", "icc0"):
+        return ILU0
     if not 1 <= block <= 255:
         raise ValueError("block size must be in 1..255")
     return (block if block > 1 else 0) << 8
+
+
+class prec_matrix:
+    """Context manager: the matrix whose ILU(0) defines M (default A itself), e.g.
+    block_diagonal(A, cuts) for the multi-rank reading of A34."""
+
+    def __init__(self, Mtx: "CSR | None"):
+        self.M = Mtx
+
+    def __enter__(self):
+        if self.M is not None:
+            lib().orc_set_prec_matrix(self.M.n, _p(self.M.rp), _p(self.M.ci), _p(self.M.va))
+        return self
+
+    def __exit__(self, *a):
+        lib().orc_set_prec_matrix(-1, None, None, None)
+
+
+def block_diagonal(A: "CSR", cuts) -> "CSR":
+    """A with every entry coupling two different row blocks [cuts[r], cuts[r+1]) dropped."""
+    part = np.searchsorted(np.asarray(cuts[1:], np.int64), np.arange(A.n), side="right")
+    rows = np.repeat(np.arange(A.n), np.diff(A.rp))
+    keep = part[rows] == part[A.ci]
+    rp = np.concatenate([[0], np.cumsum(np.bincount(rows[keep], minlength=A.n))]).astype(np.int64)
+    return CSR(A.n, rp, A.ci[keep].copy(), A.va[keep].copy())
+
+
+def ilu0_factor(A: "CSR"):
+    """The oracle's ILU(0) factors on A's pattern: (lu values aligned with A.ci:
+    multipliers l_ik below the diagonal, u_ij on and above it; uinv = 1/u_ii)."""
+    lu = np.zeros(len(A.va))
+    uinv = np.zeros(A.n)
+    if lib().orc_ilu0_factor(A.n, _p(A.rp), _p(A.ci), _p(A.va), _p(lu), _p(uinv)) != 0:
+        raise ValueError("ILU(0): missing or zero pivot")
+    return lu, uinv
 
 
 def pbicgstab(A: CSR, b, x0=None, tol=0.0, maxit=100, rr_period=0, bench=False,
