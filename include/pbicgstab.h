@@ -49,7 +49,7 @@ typedef enum {
   PBICG_BREAKDOWN = 2  /* non-finite or zero scalar denominator (A9); x = last finite iterate */
 } pbicg_outcome;
 
-/* Preconditioner M (reading A3 / A33):
+/* Preconditioner M (reading A3 / A33 / A34):
  *   PBICG_PREC_JACOBI        M = diag(A), applied as fl(dinv_j v_j), dinv_j = 1/a_jj
  *   PBICG_PREC_BJ(b)         block Jacobi ("block preconditioners"; SURVEY
  *                            NEXT-4), b in {2,4,8,16,32}: M = the b x b diagonal blocks
@@ -61,8 +61,29 @@ typedef enum {
  *                            b in {2,4,8}, nx % b == 0, full-line TMA tiles (nx <=
  *                            1024 in 2D, ~850 in 3D), method 0 only (EINVAL
  *                            otherwise).  A zero pivot is EINVAL.  Costs b-1 extra
- *                            doubles per row read in each kernel that applies M^-1. */
-typedef enum { PBICG_PREC_JACOBI = 1, PBICG_PREC_BLOCK_JACOBI = 0x100 } pbicg_prec;
+ *                            doubles per row read in each kernel that applies M^-1.
+ *   PBICG_PREC_ILU0          ILU(0): the incomplete LU factorisation with the sparsity
+ *                            pattern of A (zero fill-in; Saad's IKJ variant restricted to
+ *                            the pattern, pivots applied as reciprocals), M = L U;
+ *                            M^-1 v by forward then backward substitution, every row in
+ *                            ascending column order (reading A34).  Factorised once on
+ *                            the host at create; applied by the library's wavefront
+ *                            kernels (stencils: pipelined line wavefront; CSR: level-
+ *                            ordered rows).  Multi-rank: each rank factorises its own
+ *                            diagonal block (couplings to other ranks dropped from M).
+ *                            All three methods; no automated replacement (EINVAL).
+ *   PBICG_PREC_ICC0          ICC(0) (Table 1 "Precond."): for a
+ *                            symmetric A (stencil: coef[1]==coef[2], coef[3]==coef[4],
+ *                            coef[5]==coef[6]; CSR: each rank's diagonal block symmetric,
+ *                            else EINVAL) the incomplete Cholesky factorisation with zero
+ *                            fill-in, in root-free form: the same M and the same
+ *                            arithmetic as PBICG_PREC_ILU0. */
+typedef enum {
+  PBICG_PREC_JACOBI = 1,
+  PBICG_PREC_ILU0 = 2,
+  PBICG_PREC_ICC0 = 3,
+  PBICG_PREC_BLOCK_JACOBI = 0x100
+} pbicg_prec;
 #define PBICG_PREC_BJ(b) ((pbicg_prec)(PBICG_PREC_BLOCK_JACOBI | (b)))
 
 /* Matrix-free constant-coefficient stencil (Table 1 shapes).
@@ -267,6 +288,17 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
  * ESTATE before the first solve. */
 pbicg_status pbicgstab_rr_info(pbicg_handle h, double* fr_hist, int32_t* rr_iters, int32_t cap,
                                int32_t* n_rr);
+
+/* Parity diagnostics: the scalars of the last p-BiCGStab solve on h
+ * (rank 0's handle for a loopback group), per iteration i < min(iters, cap):
+ * out[9i..9i+8] = alpha_i, beta_i, omega_i, rho_i = (r^0, r_i), then the raw Dot2
+ * results (q_i, y_i), (y_i, y_i) (line 12) and (r^0, w_{i+1}), (r^0, s_i), (r^0, z_i)
+ * (line 21, of the replaced vectors after a replacement) -- the layout of the oracle's
+ * scalar trace, so the first iteration and dot where a run leaves the oracle, and by
+ * how many ulps, can be named.  Rows of iterations that stopped
+ * before omega_i was formed are unspecified.  EINVAL for methods 1 / 2, ESTATE
+ * before the first solve. */
+pbicg_status pbicgstab_scalar_trace(pbicg_handle h, double* out, int32_t cap);
 
 /* ncclUniqueId blob (128 bytes) for multi-GPU creation; ESTATE without NCCL. */
 pbicg_status pbicgstab_get_unique_id(void* out128);

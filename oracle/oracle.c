@@ -37,6 +37,7 @@
 #define ORC_GAP 4        /* compute the residual gap history */
 #define ORC_AUTO_RR 8    /* automated replacement: bound f^r_i (eq:DDr_bound) + eq:criterion */
 #define ORC_ILU0 16      /* preconditioner ILU(0) (= ICC(0) for symmetric A), reading A34 */
+#define ORC_SCW 9        /* doubles per iteration of orc_pbicgstab's scalar trace */
 
 #define OUT_CONVERGED 0
 #define OUT_MAXIT 1
@@ -393,7 +394,9 @@ static double res_gap(int flags, int64_t n, const int64_t* rp, const int64_t* ci
 /* r_0), A7 (stop when ||r_i|| <= tol*||b||), A8 ((r,r) added to reduction 2),*/
 /* A9 (breakdown guards), A10-A12 (replacement placement/schedule/sqrt(eps)  */
 /* stop, latched), A26 (n_i, v_i are not replaced).                           */
-/* sc_trace (optional): per iteration i: alpha_i, beta_i, omega_i, rho_i.     */
+/* sc_trace (optional): per iteration i, ORC_SCW = 9 doubles: alpha_i, beta_i,  */
+/* omega_i, rho_i, then the raw dots (q,y), (y,y) of line 12 and (r0,w), (r0,s), */
+/* (r0,z) of line 21 (after a replacement: of the replaced vectors).           */
 /* ------------------------------------------------------------------------- */
 /* Automated residual replacement, flag ORC_AUTO_RR.  The run-time
  * bound f^r_i on ||Delta^r_i|| (eq:DDr_bound P:613-616) is propagated by the
@@ -500,7 +503,7 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
       const double* src[6] = {x, r, k, w, m, t};
       for (int a = 0; a < 6; ++a) memcpy(T + (size_t)a * n, src[a], (size_t)n * sizeof(double));
     }
-    if (sc_trace) { sc_trace[4 * i + 0] = alpha; sc_trace[4 * i + 1] = beta; sc_trace[4 * i + 3] = rho; }
+    if (sc_trace) { sc_trace[ORC_SCW * i + 0] = alpha; sc_trace[ORC_SCW * i + 1] = beta; sc_trace[ORC_SCW * i + 3] = rho; }
     /* norms of the previous iteration's g, s, l, z, n, v (zero at i = 0, A1;
      * after a replacement s, l, z are the replaced vectors, n, v are not, A26)
      * and of this iteration's x, k, w, m, t, for the bound f^r */
@@ -539,7 +542,11 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     }
     /* line 16: omega := (q,y)/(y,y); A9: (y,y) = 0 => omega := 0 */
     omega = (yy == 0.0) ? 0.0 : qy / yy;
-    if (sc_trace) sc_trace[4 * i + 2] = omega;
+    if (sc_trace) {
+      sc_trace[ORC_SCW * i + 2] = omega;
+      sc_trace[ORC_SCW * i + 4] = qy;
+      sc_trace[ORC_SCW * i + 5] = yy;
+    }
     if (!isfinite(omega)) { outcome = OUT_BREAKDOWN; iters = i; done = 1; break; }
     /* bound recursion of iteration i, before x, r, k, w move on */
     double nG = 0, nS = 0, nL = 0, nZ = 0, nQ = 0, nU = 0, nY = 0, nN = 0, nV = 0;
@@ -608,6 +615,11 @@ int orc_pbicgstab(int64_t n, const int64_t* rp, const int64_t* ci, const double*
     double ds = dotf(flags, n, rh, s);
     double dz = dotf(flags, n, rh, z);
     rhist[i + 1] = sqrt(dotf(flags, n, r, r));
+    if (sc_trace) {
+      sc_trace[ORC_SCW * i + 6] = dw;
+      sc_trace[ORC_SCW * i + 7] = ds;
+      sc_trace[ORC_SCW * i + 8] = dz;
+    }
     /* lines 22-23: m := M^-1 w; t := A m */
     pprec(&P, w, m);
     orc_spmv(n, rp, ci, va, m, t);

@@ -169,7 +169,8 @@ def _run(fn, A: CSR, b, x0, tol, maxit, flags, extra=(), want_sc=False, want_tra
             int(flags), _p(x), _p(rh), _p(gh), ctypes.byref(it), ctypes.byref(oc)]
     sc = tr = None
     if fn in ("orc_pbicgstab", "orc_bicgstab"):
-        sc = np.full((maxit + 1, 4), np.nan) if want_sc else None
+        # p-BiCGStab: alpha, beta, omega, rho + the raw dots (q,y), (y,y), (r0,w), (r0,s), (r0,z)
+        sc = np.full((maxit + 1, 9 if fn == "orc_pbicgstab" else 4), np.nan) if want_sc else None
         args.append(_p(sc))
     bt = rl = None
     nrr = ctypes.c_int32(0)

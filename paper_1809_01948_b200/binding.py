@@ -22,8 +22,11 @@ KERNELS = ["init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap", "a
 # option "method": 0 p-BiCGStab (Alg. 2), 1 classic BiCGStab (Alg. 1), 2 p-CG (reading A19)
 
 
-def prec_code(block: int) -> int:
-    """pbicg_prec value: 1 = Jacobi, PBICG_PREC_BJ(b) = 0x100 | b (block Jacobi, CSR)."""
+def prec_code(block) -> int:
+    """pbicg_prec value: 1 = Jacobi, PBICG_PREC_BJ(b) = 0x100 | b (block Jacobi),
+    "ilu0" = PBICG_PREC_ILU0 (2), "icc0" = PBICG_PREC_ICC0 (3) (reading A34)."""
+    if block in ("ilu0", "icc0"):
+        return 2 if block == "ilu0" else 3
     return 1 if block == 1 else 0x100 | int(block)
 METHODS = {"pbicgstab": 0, "bicgstab": 1, "pipecg": 2}
 
@@ -55,6 +58,7 @@ SYMBOLS = ["pbicgstab_create_stencil", "pbicgstab_create_csr", "pbicgstab_create
            "pbicgstab_local_rows", "pbicgstab_stencil_partition",
            "pbicgstab_set_option", "pbicgstab_apply", "pbicgstab_solve", "pbicgstab_solve_host",
            "pbicgstab_kernel_time", "pbicgstab_kernel_bytes", "pbicgstab_rr_info",
+           "pbicgstab_scalar_trace",
            "pbicgstab_get_unique_id",
            "pbicgstab_last_error", "pbicgstab_destroy"]
 
@@ -98,6 +102,7 @@ def lib(build: bool = True):
                                         ctypes.POINTER(f64), i32]
     L.pbicgstab_kernel_bytes.argtypes = [P, ctypes.c_char_p, ctypes.POINTER(f64)]
     L.pbicgstab_rr_info.argtypes = [P, P, P, i32, ctypes.POINTER(i32)]
+    L.pbicgstab_scalar_trace.argtypes = [P, P, i32]
     L.pbicgstab_get_unique_id.argtypes = [P]
     L.pbicgstab_last_error.argtypes = [P]
     L.pbicgstab_last_error.restype = ctypes.c_char_p
@@ -260,6 +265,14 @@ class Solver:
                                        rl.ctypes.data_as(ctypes.c_void_p), cap,
                                        ctypes.byref(n)), self._h)
         return fr, [int(v) for v in rl[:min(n.value, cap)]]
+
+    def scalar_trace(self, iters: int) -> np.ndarray:
+        """[iters, 9]: alpha_i, beta_i, omega_i, rho_i, (q,y), (y,y), (r0,w), (r0,s), (r0,z)
+        of the last p-BiCGStab solve (pbicgstab_scalar_trace; the oracle's `scalars`)."""
+        out = np.full((max(iters, 1), 9), np.nan)
+        _check(lib().pbicgstab_scalar_trace(self._h, out.ctypes.data_as(ctypes.c_void_p),
+                                            int(iters)), self._h)
+        return out[:iters]
 
     def kernel_time(self, name: str = "all", reset: bool = False) -> tuple[int, float]:
         n, ms = ctypes.c_int64(), ctypes.c_double()

@@ -34,6 +34,14 @@ struct CsrOp {
   const int16_t* sdcol;  // column - row (|.| <= half bandwidth <= (WRS - 3 WTB) / 2)
 };
 
+// Preconditioner kinds of the per-row kernels' PK template parameter: Jacobi and
+// block Jacobi are applied inside the kernels (prec_row); with ILU(0) (reading A34)
+// the preconditioned vectors k, l, m, n (and classic BiCGStab's M^-1 p, M^-1 q) are
+// produced by the k_ilu_* sweeps between the kernels, which read them from memory.
+#define PK_JAC 0
+#define PK_BJ 1
+#define PK_ILU 2
+
 // M^{-1} applied to the value v of row j (reading A3 / A33).  Jacobi: fl(dinv_j v).
 // Block Jacobi: the bj rows of a block are bj consecutive lanes of one warp
 // (blocks are aligned and n_local % bj == 0), so the block's values are read by
@@ -109,9 +117,10 @@ __device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restri
 // sums of squares of the vectors the bound f^r needs (plain fp64, reading A30)
 __device__ __forceinline__ void c_nrm(Dd& a, double v) { a.hi = a.hi + v * v; }
 
-template <bool NRM, bool BJ>
+template <bool NRM, int PK>
 __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                Dd* __restrict__ part, Hist h) {
+  constexpr bool BJ = PK == PK_BJ;
   constexpr int K = NRM ? 4 : 2;
   Dd acc[K];
 #pragma unroll
@@ -119,11 +128,12 @@ __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict
   WROW_LOOP
     const double bj = in ? V.b[j] : 0.0;
     const double rj = in ? bj - ell_row<false>(A, V.x, j) : 0.0;
-    const double kj = prec_row<BJ>(A, j, in, rj, dj);  // k0 := M^-1 r0
+    // k0 := M^-1 r0 (ILU(0): k_ilu_* after this kernel)
+    const double kj = PK == PK_ILU ? 0.0 : prec_row<BJ>(A, j, in, rj, dj);
     if (in) {
       V.r[j] = rj;
       V.rh[j] = rj;
-      V.k[j] = kj;
+      if (PK != PK_ILU) V.k[j] = kj;
       dd_fma(acc[0], rj, rj);
       dd_fma(acc[1], bj, bj);
       if (NRM) {
@@ -137,16 +147,18 @@ __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict
     publish<F_INIT1>(sc, h, tot);
 }
 
-template <bool BJ>
+template <int PK>
 __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                Dd* __restrict__ part, Hist h) {
+  constexpr bool BJ = PK == PK_BJ;
   Dd acc[1] = {dd_zero()};
   WROW_LOOP
     const double wj = in ? ell_row<false>(A, V.k, j) : 0.0;  // w0 = A k0 = A M^-1 r0
-    const double mj = prec_row<BJ>(A, j, in, wj, dj);            // m0 = M^-1 w0 (line 2)
+    // m0 = M^-1 w0 (line 2; ILU(0): k_ilu_* after this kernel)
+    const double mj = PK == PK_ILU ? 0.0 : prec_row<BJ>(A, j, in, wj, dj);
     if (in) {
       V.w0[j] = wj;
-      V.mv[j] = mj;
+      if (PK != PK_ILU) V.mv[j] = mj;
       dd_fma(acc[0], V.rh[j], wj);
     }
   WROW_END
@@ -156,9 +168,10 @@ __global__ void __launch_bounds__(256) c_init2(CsrOp A, Vecs V, Scal* __restrict
 }
 
 // lines 5-12 with stored t_i, v_{i-1}; n_{i-1} = M^-1 z_{i-1} (pre-replacement, A26)
-template <bool NRM, bool BJ>
+template <bool NRM, int PK>
 __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                 Dd* __restrict__ part, Hist h) {
+  constexpr bool BJ = PK == PK_BJ;
   constexpr int K = NRM ? 12 : 2;
   if (sc->done) return;
   const double al = sc->alpha, be = sc->beta, om = sc->omega;
@@ -168,7 +181,9 @@ __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restric
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   WROW_LOOP
     const double wc = in ? V.w0[j] : 0.0, zc = in ? V.z0[j] : 0.0;
-    const double m = prec_row<BJ>(A, j, in, wc, dj), n = prec_row<BJ>(A, j, in, zc, dj);  // m_i, n_{i-1}
+    // m_i, n_{i-1} (ILU(0): as stored by k_ilu_*; nv still holds the pre-replacement n, A26)
+    const double m = PK == PK_ILU ? (in ? V.mv[j] : 0.0) : prec_row<BJ>(A, j, in, wc, dj);
+    const double n = PK == PK_ILU ? (in ? V.nv[j] : 0.0) : prec_row<BJ>(A, j, in, zc, dj);
     double zn = 0.0;
     if (in) {
       const double zo = rr ? V.zrr[j] : zc;
@@ -193,8 +208,10 @@ __global__ void __launch_bounds__(256) c_sweepA(CsrOp A, Vecs V, Scal* __restric
       V.l[j] = ln;
       V.z0[j] = zn;
     }
-    const double nj = prec_row<BJ>(A, j, in, zn, dj);  // n_i = M^-1 z_i (line 13)
-    if (in) V.nv[j] = nj;
+    if (PK != PK_ILU) {
+      const double nj = prec_row<BJ>(A, j, in, zn, dj);  // n_i = M^-1 z_i (line 13)
+      if (in) V.nv[j] = nj;
+    }
   WROW_END
   Dd tot[K];
   if (dd_grid_reduce<K>(acc, part, &sc->counter[T_SWEEPA], tot) && threadIdx.x == 0)
@@ -305,10 +322,11 @@ __global__ void __launch_bounds__(256) c_spmvB(CsrOp A, Vecs V, Scal* __restrict
 }
 
 // lines 17-21
-template <bool NRM, bool BJ>
+template <bool NRM, int PK>
 // (256, 3): <= 85 registers keep 3 CTAs per SM for the block-Jacobi instance too
 __global__ void __launch_bounds__(256, 3) c_sweepC(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                                 Dd* __restrict__ part, Hist h) {
+  constexpr bool BJ = PK == PK_BJ;
   constexpr int K = NRM ? 9 : 5;
   if (sc->done) return;
   const double al = sc->alpha, om = sc->omega;
@@ -317,7 +335,9 @@ __global__ void __launch_bounds__(256, 3) c_sweepC(CsrOp A, Vecs V, Scal* __rest
   for (int k = 0; k < K; ++k) acc[k] = dd_zero();
   WROW_LOOP
     const double wc = in ? V.w0[j] : 0.0, zc = in ? V.z0[j] : 0.0;
-    const double m = prec_row<BJ>(A, j, in, wc, dj), n = prec_row<BJ>(A, j, in, zc, dj);  // m_i, n_i
+    // m_i, n_i (ILU(0): as stored by k_ilu_*)
+    const double m = PK == PK_ILU ? (in ? V.mv[j] : 0.0) : prec_row<BJ>(A, j, in, wc, dj);
+    const double n = PK == PK_ILU ? (in ? V.nv[j] : 0.0) : prec_row<BJ>(A, j, in, zc, dj);
     double wn = 0.0;
     if (in) {
     const double t = V.w1[j], v = V.z1[j];
@@ -345,8 +365,10 @@ __global__ void __launch_bounds__(256, 3) c_sweepC(CsrOp A, Vecs V, Scal* __rest
     V.k[j] = kn;
     V.w0[j] = wn;
     }
-    const double mn = prec_row<BJ>(A, j, in, wn, dj);  // m_{i+1} = M^-1 w_{i+1} (line 22)
-    if (in) V.mv[j] = mn;
+    if (PK != PK_ILU) {
+      const double mn = prec_row<BJ>(A, j, in, wn, dj);  // m_{i+1} = M^-1 w_{i+1} (line 22)
+      if (in) V.mv[j] = mn;
+    }
   WROW_END
   Dd tot[K];
   if (dd_grid_reduce<K>(acc, part, &sc->counter[T_SWEEPC], tot) && threadIdx.x == 0)
@@ -571,20 +593,25 @@ __global__ void __launch_bounds__(CST_T, 1) c_sweep_tma(CsrOp A, Vecs V, Scal* _
 }
 
 // eq:rr: r := b - A x; k := M^-1 r; s := A g; l := M^-1 s
-template <bool NRM, bool BJ>
+template <bool NRM, int PK>
 __global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                              Dd* __restrict__ part, Hist h) {
+  constexpr bool BJ = PK == PK_BJ;
   if (sc->done || !sc->rr_fire) return;
   Dd acc[4] = {dd_zero(), dd_zero(), dd_zero(), dd_zero()};
   WROW_LOOP
     const double rj = in ? V.b[j] - ell_row<false>(A, V.x, j) : 0.0;
     const double sj = in ? ell_row<false>(A, V.g, j) : 0.0;
-    const double kj = prec_row<BJ>(A, j, in, rj, dj), lj = prec_row<BJ>(A, j, in, sj, dj);
+    // k := M^-1 r, l := M^-1 s (ILU(0): k_ilu_* after this kernel)
+    const double kj = PK == PK_ILU ? 0.0 : prec_row<BJ>(A, j, in, rj, dj);
+    const double lj = PK == PK_ILU ? 0.0 : prec_row<BJ>(A, j, in, sj, dj);
     if (in) {
       V.r[j] = rj;
-      V.k[j] = kj;
       V.s[j] = sj;
-      V.l[j] = lj;
+      if (PK != PK_ILU) {
+        V.k[j] = kj;
+        V.l[j] = lj;
+      }
       if (NRM) {  // replaced x_{i+1}, k_{i+1}, s_i, l_i
         c_nrm(acc[0], V.x[j]); c_nrm(acc[1], kj); c_nrm(acc[2], sj); c_nrm(acc[3], lj);
       }
@@ -598,9 +625,10 @@ __global__ void __launch_bounds__(256) c_rr1(CsrOp A, Vecs V, Scal* __restrict__
 }
 
 // w := A k; z := A l (into zrr); line-21 dots on the replaced vectors
-template <bool NRM, bool BJ>
+template <bool NRM, int PK>
 __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                              Dd* __restrict__ part, Hist h) {
+  constexpr bool BJ = PK == PK_BJ;
   constexpr int K = NRM ? 6 : 5;
   if (sc->done || !sc->rr_fire) return;
   Dd acc[K];
@@ -609,10 +637,11 @@ __global__ void __launch_bounds__(256) c_rr2(CsrOp A, Vecs V, Scal* __restrict__
   WROW_LOOP
     const double wn = in ? ell_row<false>(A, V.k, j) : 0.0;  // w := A k = A M^-1 r
     const double zr = in ? ell_row<false>(A, V.l, j) : 0.0;  // z := A l = A M^-1 s
-    const double mn = prec_row<BJ>(A, j, in, wn, dj);  // m_{i+1} follows the replaced w (A27)
+    // m_{i+1} follows the replaced w (A27; ILU(0): k_ilu_* after this kernel)
+    const double mn = PK == PK_ILU ? 0.0 : prec_row<BJ>(A, j, in, wn, dj);
     if (in) {
       V.w0[j] = wn;
-      V.mv[j] = mn;
+      if (PK != PK_ILU) V.mv[j] = mn;
       V.zrr[j] = zr;
       const double rhj = V.rh[j], rc = V.r[j];
       dd_fma(acc[0], rhj, rc);
@@ -757,8 +786,9 @@ __global__ void __launch_bounds__(WNT, 1) c_spmv_win(CsrOp A, Vecs V, Scal* __re
 }
 
 // mv := M^-1 w0 (p-CG init, after SP_PCW0)
-template <bool BJ>
+template <int PK>
 __global__ void __launch_bounds__(256) c_prec_mv(CsrOp A, Vecs V) {
+  constexpr bool BJ = PK == PK_BJ;
   WROW_LOOP
     const double m = prec_row<BJ>(A, j, in, in ? V.w0[j] : 0.0, dj);
     if (in) V.mv[j] = m;
@@ -770,28 +800,35 @@ __global__ void __launch_bounds__(256) c_prec_mv(CsrOp A, Vecs V) {
 // SpMVs SP_CLS / SP_CLY.  Buffers: p -> g, M^-1 p -> mv, M^-1 q -> nv, y -> z1.
 // l.17 of the previous iteration (i = 0: beta = omega = 0 and p = s = 0, so
 // p_0 = r_0): p := r + beta (p - omega s); the SpMV operand mv := M^-1 p (l.4)
-template <bool BJ>
+template <int PK>
 __global__ void __launch_bounds__(256) c_cl_p(CsrOp A, Vecs V, Scal* __restrict__ sc) {
+  constexpr bool BJ = PK == PK_BJ;
   if (sc->done) return;
   const double be = sc->beta, om = sc->omega;
   WROW_LOOP
     const double p = in ? V.r[j] + be * (V.g[j] - om * V.s[j]) : 0.0;
-    const double g = prec_row<BJ>(A, j, in, p, dj);
+    const double g = PK == PK_ILU ? 0.0 : prec_row<BJ>(A, j, in, p, dj);
     if (in) {
       V.g[j] = p;
-      V.mv[j] = g;
+      if (PK != PK_ILU) V.mv[j] = g;  // ILU(0): mv := M^-1 p by k_ilu_* (from g)
     }
   WROW_END
 }
 
 // l.8-9: q := r - alpha s; the SpMV operand nv := u = M^-1 q
-template <bool BJ>
+template <int PK>
 __global__ void __launch_bounds__(256) c_cl_u(CsrOp A, Vecs V, Scal* __restrict__ sc) {
+  constexpr bool BJ = PK == PK_BJ;
   if (sc->done) return;
   const double al = sc->alpha;
   WROW_LOOP
-    const double u = prec_row<BJ>(A, j, in, in ? V.r[j] - al * V.s[j] : 0.0, dj);
-    if (in) V.nv[j] = u;
+    const double q = in ? V.r[j] - al * V.s[j] : 0.0;
+    if (PK == PK_ILU) {  // q stored in z0; nv := M^-1 q by k_ilu_*
+      if (in) V.z0[j] = q;
+    } else {
+      const double u = prec_row<BJ>(A, j, in, q, dj);
+      if (in) V.nv[j] = u;
+    }
   WROW_END
 }
 
@@ -919,15 +956,17 @@ __global__ void __launch_bounds__(CST_T, 1) c_cl_tma(CsrOp A, Vecs V, Scal* __re
 // p-CG iteration (reading A19) after n_i = A m_i (SP_PCN): buffers z -> z0,
 // q -> l, s, p -> g, x, r, u -> k, w -> w0, n -> z1, m -> mv (written for the
 // next SpMV); the next iteration's (r,u), (w,u), ||r||^2
-template <bool BJ>
+template <int PK>
 __global__ void __launch_bounds__(256) c_pc(CsrOp A, Vecs V, Scal* __restrict__ sc,
                                             Dd* __restrict__ part, Hist h) {
+  constexpr bool BJ = PK == PK_BJ;
   if (sc->done) return;
   const double al = sc->alpha, be = sc->beta;
   Dd acc[3] = {dd_zero(), dd_zero(), dd_zero()};
   WROW_LOOP
     const double wj = in ? V.w0[j] : 0.0;
-    const double mj = prec_row<BJ>(A, j, in, wj, dj);
+    // m_i = M^-1 w_i (ILU(0): as stored by k_ilu_*)
+    const double mj = PK == PK_ILU ? (in ? V.mv[j] : 0.0) : prec_row<BJ>(A, j, in, wj, dj);
     double wn = 0.0;
     if (in) {
     const double uj = V.k[j];
@@ -945,8 +984,10 @@ __global__ void __launch_bounds__(256) c_pc(CsrOp A, Vecs V, Scal* __restrict__ 
     dd_fma(acc[1], wn, un);
     dd_fma(acc[2], rn, rn);
     }
-    const double mn = prec_row<BJ>(A, j, in, wn, dj);
-    if (in) V.mv[j] = mn;
+    if (PK != PK_ILU) {
+      const double mn = prec_row<BJ>(A, j, in, wn, dj);
+      if (in) V.mv[j] = mn;
+    }
   WROW_END
   Dd tot[3];
   if (dd_grid_reduce<3>(acc, part, &sc->counter[T_PC], tot) && threadIdx.x == 0)

@@ -11,6 +11,7 @@
 // stencil_kernels.cuh / tile_sweeps.cuh / csr_kernels.cuh.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <cmath>
@@ -24,6 +25,7 @@
 
 #include "../../include/pbicgstab.h"
 #include "csr_kernels.cuh"
+#include "ilu_kernels.cuh"
 #include "nccl_dyn.h"
 #include "stencil_kernels.cuh"
 #include "tile_bj.h"
@@ -89,6 +91,11 @@ struct pbicg_ctx {
   int win_grid = 0;
   bool cst_ok = false;  // CSR: TMA-staged sweeps (c_sweep_tma) eligible (Jacobi)
   bool cst_on = true;   // option "csr_tma"
+  // ILU(0) / ICC(0) preconditioner (reading A34): factors of this rank's diagonal block
+  int ilu = 0;          // 1 ILU(0), 2 ICC(0) (symmetric A)
+  bool ilu_st = false;  // stencil wavefront kernels (else the general CSR level-order kernel)
+  IluOp ilu_op{};
+  int ilu_grid = 0;
   int cst_grid = 0;
   std::vector<void*> allocs;
   Vecs V{};
@@ -397,23 +404,70 @@ void launch_spmv(pbicg_ctx* h) {
                                                               h->hist);
 }
 
+// preconditioner kind of the per-row CSR kernels (csr_kernels.cuh PK_*)
+int pk_of(const pbicg_ctx* h) { return h->ilu ? PK_ILU : (h->csr.bj > 1 ? PK_BJ : PK_JAC); }
+
+// the per-row kernels, one instance per preconditioner kind (NRM: automated replacement,
+// never with ILU(0))
+template <int PK>
+void launch_csr_rows(pbicg_ctx* h, Phase p) {
+  const CsrOp& A = h->csr;
+  const bool nrm = PK != PK_ILU && h->auto_rr;
+  cudaStream_t st = h->stream;
+  switch (p) {
+    case PH_CCP: c_cl_p<PK><<<h->grid[K_SWEEPA], h->block, 0, st>>>(A, h->V, h->scal); break;
+    case PH_CCU: c_cl_u<PK><<<h->grid[K_SWEEPA], h->block, 0, st>>>(A, h->V, h->scal); break;
+    case PH_PRECMV: c_prec_mv<PK><<<h->grid[K_SWEEPA], h->block, 0, st>>>(A, h->V); break;
+    case PH_CPC: c_pc<PK><<<h->grid[K_SWEEPC], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist); break;
+    case PH_INIT1:
+      if (nrm) c_init1<true, PK><<<h->grid[K_INIT], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      else c_init1<false, PK><<<h->grid[K_INIT], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      break;
+    case PH_INIT2: c_init2<PK><<<h->grid[K_INIT], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist); break;
+    case PH_SWEEPA:
+      if (nrm) c_sweepA<true, PK><<<h->grid[K_SWEEPA], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      else c_sweepA<false, PK><<<h->grid[K_SWEEPA], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      break;
+    case PH_SWEEPC:
+      if (nrm) c_sweepC<true, PK><<<h->grid[K_SWEEPC], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      else c_sweepC<false, PK><<<h->grid[K_SWEEPC], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      break;
+    case PH_RR1:
+      if (nrm) c_rr1<true, PK><<<h->grid[K_RR1], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      else c_rr1<false, PK><<<h->grid[K_RR1], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      break;
+    case PH_RR2:
+      if (nrm) c_rr2<true, PK><<<h->grid[K_RR2], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      else c_rr2<false, PK><<<h->grid[K_RR2], h->block, 0, st>>>(A, h->V, h->scal, h->part, h->hist);
+      break;
+    default:
+      break;
+  }
+}
+
+void launch_rows(pbicg_ctx* h, Phase p) {
+  switch (pk_of(h)) {
+    case PK_ILU: launch_csr_rows<PK_ILU>(h, p); break;
+    case PK_BJ: launch_csr_rows<PK_BJ>(h, p); break;
+    default: launch_csr_rows<PK_JAC>(h, p); break;
+  }
+}
+
 void launch_csr(pbicg_ctx* h, Phase p) {
   const CsrOp& A = h->csr;
+  // the TMA chunk-ring sweeps apply Jacobi (and block Jacobi b <= 4) themselves
+  const bool ring = !h->ilu && h->cst_ok && h->cst_on;
   switch (p) {
     case PH_CCP: {
       LaunchScope ls(h, K_CL1);
-      const bool ring = h->csr.bj <= 1 && h->cst_ok && h->cst_on;  // TMA chunk ring
-      if (ring) c_cl_tma<0><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else if (h->csr.bj > 1) c_cl_p<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
-      else c_cl_p<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      if (ring && h->csr.bj <= 1) c_cl_tma<0><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else launch_rows(h, p);
     } break;
     case PH_SP_CLS: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_CLS>(h); } break;
     case PH_CCU: {
       LaunchScope ls(h, K_CL2);
-      const bool ring = h->csr.bj <= 1 && h->cst_ok && h->cst_on;
-      if (ring) c_cl_tma<1><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else if (h->csr.bj > 1) c_cl_u<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
-      else c_cl_u<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal);
+      if (ring && h->csr.bj <= 1) c_cl_tma<1><<<h->cst_grid, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else launch_rows(h, p);
     } break;
     case PH_SP_CLY: { LaunchScope ls(h, K_SPMVD); launch_spmv<SP_CLY>(h); } break;
     case PH_CCX: {
@@ -425,54 +479,40 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SP_PCW0: { LaunchScope ls(h, K_INIT); launch_spmv<SP_PCW0>(h); } break;
     case PH_SP_PCN: { LaunchScope ls(h, K_SPMVB); launch_spmv<SP_PCN>(h); } break;
-    case PH_PRECMV: {
-      LaunchScope ls(h, K_INIT);
-      if (h->csr.bj > 1) c_prec_mv<true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V);
-      else c_prec_mv<false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V);
-    } break;
-    case PH_CPC: {
-      LaunchScope ls(h, K_PC);
-      if (h->csr.bj > 1) c_pc<true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else c_pc<false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-    } break;
+    case PH_PRECMV: { LaunchScope ls(h, K_INIT); launch_rows(h, p); } break;
+    case PH_CPC: { LaunchScope ls(h, K_PC); launch_rows(h, p); } break;
     case PH_INIT1: {
       LaunchScope ls(h, K_INIT);
-      if (h->csr.bj > 1) {
-        if (h->auto_rr) c_init1<true, true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_init1<false, true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      } else if (h->win_ok && !h->auto_rr) {  // window SpMV over the SELL-32 matrix
+      if (h->csr.bj <= 1 && !h->ilu && h->win_ok && !h->auto_rr)  // window SpMV, SELL-32
         c_spmv_win<SP_I1><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg,
                                                                      h->part, h->hist);
-      } else {
-        if (h->auto_rr) c_init1<true, false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_init1<false, false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      }
+      else launch_rows(h, p);
     } break;
     case PH_INIT2: {
       LaunchScope ls(h, K_INIT);
-      if (h->csr.bj > 1) c_init2<true><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      else if (h->win_ok)
+      if (h->csr.bj <= 1 && !h->ilu && h->win_ok)
         c_spmv_win<SP_I2><<<h->win_grid, WNT, WIN_SMEM, h->stream>>>(A, h->V, h->scal, h->wg,
                                                                      h->part, h->hist);
-      else c_init2<false><<<h->grid[K_INIT], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+      else launch_rows(h, p);
     } break;
-    case PH_SWEEPA: {
-      LaunchScope ls(h, K_SWEEPA);
-      if (h->cst_ok && h->cst_on && h->csr.bj <= 4) {  // TMA chunk ring (Jacobi, b <= 4)
+    case PH_SWEEPA:
+    case PH_SWEEPC: {
+      const int SW = p == PH_SWEEPA ? 0 : 1;
+      LaunchScope ls(h, SW == 0 ? K_SWEEPA : K_SWEEPC);
+      if (ring && h->csr.bj <= 4) {  // TMA chunk ring (Jacobi, b <= 4)
         const int g = h->cst_grid;
-        if (h->csr.bj > 1) {
-          if (h->auto_rr) c_sweep_tma<0, true, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
-          else c_sweep_tma<0, false, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
+        const bool bj = h->csr.bj > 1, nrm = h->auto_rr != 0;
+#define CST_L(S, N, B) c_sweep_tma<S, N, B><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0)
+        if (SW == 0) {
+          if (bj) { if (nrm) CST_L(0, true, true); else CST_L(0, false, true); }
+          else { if (nrm) CST_L(0, true, false); else CST_L(0, false, false); }
         } else {
-          if (h->auto_rr) c_sweep_tma<0, true, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
-          else c_sweep_tma<0, false, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
+          if (bj) { if (nrm) CST_L(1, true, true); else CST_L(1, false, true); }
+          else { if (nrm) CST_L(1, true, false); else CST_L(1, false, false); }
         }
-      } else if (h->csr.bj > 1) {
-        if (h->auto_rr) c_sweepA<true, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_sweepA<false, true><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+#undef CST_L
       } else {
-        if (h->auto_rr) c_sweepA<true, false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_sweepA<false, false><<<h->grid[K_SWEEPA], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
+        launch_rows(h, p);
       }
     } break;
     case PH_SPMVB: {
@@ -483,47 +523,8 @@ void launch_csr(pbicg_ctx* h, Phase p) {
       else
         c_spmvB<<<h->grid[K_SPMVB], h->block, 0, h->stream>>>(A, h->V, h->scal);
     } break;
-    case PH_SWEEPC: {
-      {
-        LaunchScope ls(h, K_SWEEPC);
-        if (h->cst_ok && h->cst_on && h->csr.bj <= 4) {  // TMA chunk ring (Jacobi, b <= 4)
-          const int g = h->cst_grid;
-          if (h->csr.bj > 1) {
-            if (h->auto_rr) c_sweep_tma<1, true, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
-            else c_sweep_tma<1, false, true><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
-          } else {
-            if (h->auto_rr) c_sweep_tma<1, true, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
-            else c_sweep_tma<1, false, false><<<g, CST_T, kCstSmem, h->stream>>>(A, h->V, h->scal, h->part, h->hist, 0.0);
-          }
-        } else if (h->csr.bj > 1) {
-          if (h->auto_rr) c_sweepC<true, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-          else c_sweepC<false, true><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        } else {
-          if (h->auto_rr) c_sweepC<true, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-          else c_sweepC<false, false><<<h->grid[K_SWEEPC], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        }
-      }
-    } break;
-    case PH_RR1: {
-      LaunchScope ls(h, K_RR1);
-      if (h->csr.bj > 1) {
-        if (h->auto_rr) c_rr1<true, true><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_rr1<false, true><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      } else {
-        if (h->auto_rr) c_rr1<true, false><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_rr1<false, false><<<h->grid[K_RR1], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      }
-    } break;
-    case PH_RR2: {
-      LaunchScope ls(h, K_RR2);
-      if (h->csr.bj > 1) {
-        if (h->auto_rr) c_rr2<true, true><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_rr2<false, true><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      } else {
-        if (h->auto_rr) c_rr2<true, false><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-        else c_rr2<false, false><<<h->grid[K_RR2], h->block, 0, h->stream>>>(A, h->V, h->scal, h->part, h->hist);
-      }
-    } break;
+    case PH_RR1: { LaunchScope ls(h, K_RR1); launch_rows(h, p); } break;
+    case PH_RR2: { LaunchScope ls(h, K_RR2); launch_rows(h, p); } break;
     case PH_SPMVD: {
       LaunchScope ls(h, K_SPMVD);
       if (h->win_ok)
@@ -542,6 +543,26 @@ void launch_csr(pbicg_ctx* h, Phase p) {
     } break;
     default:
       break;
+  }
+}
+
+// ILU(0) application out := M^{-1} in (ilu_kernels.cuh; reading A34): forward then
+// backward sweep, gated like the step it follows (1: skip when done, 2: only in a
+// replacement iteration)
+void launch_ilu(pbicg_ctx* h, const double* in, double* out, int gate) {
+  LaunchScope ls(h, K_PREC);
+  const IluOp& P = h->ilu_op;
+  if (h->ilu_st) {
+    if (P.dim == 3) {
+      k_ilu_st<3, false><<<h->ilu_grid, ILU_T, 0, h->stream>>>(P, h->scal, gate, in, out);
+      k_ilu_st<3, true><<<h->ilu_grid, ILU_T, 0, h->stream>>>(P, h->scal, gate, in, out);
+    } else {
+      k_ilu_st<2, false><<<h->ilu_grid, ILU_T, 0, h->stream>>>(P, h->scal, gate, in, out);
+      k_ilu_st<2, true><<<h->ilu_grid, ILU_T, 0, h->stream>>>(P, h->scal, gate, in, out);
+    }
+  } else {
+    k_ilu_csr<false><<<h->ilu_grid, 256, 0, h->stream>>>(P, h->scal, gate, in, out);
+    k_ilu_csr<true><<<h->ilu_grid, 256, 0, h->stream>>>(P, h->scal, gate, in, out);
   }
 }
 
@@ -667,6 +688,12 @@ void join_reduce(const Members& G) { cudaStreamWaitEvent(G[0]->stream, G[0]->ev_
 void each(const Members& G, Phase p) {
   for (pbicg_ctx* h : G) launch(h, p);
 }
+// ILU(0) handles: out := M^{-1} in on every member (each rank its own block, A34);
+// a no-op for the point-wise preconditioners, which the kernels apply themselves
+void each_ilu(const Members& G, const VecSel& in, const VecSel& out, int gate) {
+  if (!G[0]->ilu) return;
+  for (pbicg_ctx* h : G) launch_ilu(h, in(h), out(h), gate);
+}
 void each_fin(const Members& G, int f) {
   if (!G[0]->dist) return;
   for (pbicg_ctx* h : G) launch_fin(h, f);
@@ -700,10 +727,12 @@ const VecSel SMVv = [](pbicg_ctx* h) { return h->V.mv; };
 void enq_iter_classic_csr(const Members& G) {
   const bool dist = G[0]->dist;
   each(G, PH_CCP);  // l.17 (previous i) + l.4: p_i, M^-1 p_i
+  each_ilu(G, SG, SMVv, 1);  // ILU(0): M^-1 p_i
   if (dist) comm_halo(G, {SMVv});
   each(G, PH_SP_CLS);  // l.5-6: s_i, (r^0, s_i) -> alpha
   reduce_fin(G, F_CL1);
   each(G, PH_CCU);  // l.8-9: u = M^-1 (r - alpha s)
+  each_ilu(G, SZ0, SNVv, 1);  // ILU(0): q_i was stored in z0
   if (dist) comm_halo(G, {SNVv});
   each(G, PH_SP_CLY);  // l.10-11: y, (q,y), (y,y) -> omega
   reduce_fin(G, F_CL2);
@@ -719,11 +748,13 @@ void enq_iter_pipecg_csr(const Members& G) {
   const bool dist = h0->dist;
   each(G, PH_CPC);
   if (!dist) {
+    each_ilu(G, SW0, SMVv, 1);  // ILU(0): m_{i+1} = M^-1 w_{i+1}
     each(G, PH_SP_PCN);
     return;
   }
   if (h0->overlap) fork_reduce(G);
   else comm_reduce(G, false);
+  each_ilu(G, SW0, SMVv, 1);  // overlaps the reduction with the SpMV
   comm_halo(G, {SMVv});
   each(G, PH_SP_PCN);
   if (h0->overlap) join_reduce(G);
@@ -759,11 +790,13 @@ void enq_init_pipecg(const Members& G) {
   if (G[0]->kind == KIND_CSR) {
     if (dist) comm_halo(G, {SX});
     each(G, PH_INIT1);  // r0, u0 (k); ||r0||, ||b|| (F_INIT1, method 2)
+    each_ilu(G, SR, SK, 0);  // ILU(0): u0 = M^-1 r0
     reduce_fin(G, F_INIT1);
     if (dist) comm_halo(G, {SK});
     each(G, PH_SP_PCW0);  // w0 = A u0; (r0,u0), (w0,u0) -> alpha_0
     reduce_fin(G, F_PINIT2);
-    each(G, PH_PRECMV);   // m0 = M^-1 w0
+    if (G[0]->ilu) each_ilu(G, SW0, SMVv, 0);
+    else each(G, PH_PRECMV);   // m0 = M^-1 w0
     if (dist) comm_halo(G, {SMVv});
     each(G, PH_SP_PCN);  // n_0 = A m_0
     return;
@@ -803,9 +836,11 @@ void enq_init(const Members& G) {
   }
   if (dist) comm_halo(G, {SX});
   each(G, PH_INIT1);
+  each_ilu(G, SR, SK, 0);  // ILU(0): k0 = M^-1 r0
   reduce_fin(G, F_INIT1);
   if (dist) comm_halo(G, {h0->kind == KIND_CSR ? SK : SR});  // CSR: w0 = A k0
   each(G, PH_INIT2);
+  each_ilu(G, SW0, SMV, 0);  // ILU(0): m0 = M^-1 w0
   reduce_fin(G, F_INIT2);
   if (h0->kind == KIND_CSR) {  // t_0 = A m_0 (line 3)
     if (dist) comm_halo(G, {SMV});
@@ -918,33 +953,42 @@ void enq_iter(const Members& G, bool with_rr, int par) {
     // w_{i+1} (transport 1: stored by sweep C in the neighbours unless replaced)
     if (dist && (with_rr || !fused_halo(h0))) comm_halo(G, {par ? SW0 : SW1});
   } else {
-    // split 4-phase schedule; reduction #1 overlaps the halo + spmv_B
+    // split 4-phase schedule: reduction #1 overlaps M^-1 z (ILU(0)), the halo
+    // and spmv_B; reduction #2 overlaps M^-1 w, the halo and spmv_D when this
+    // iteration cannot replace
     each(G, PH_SWEEPA);
     const bool ov = dist && h0->overlap;
-    if (ov) {
-      cudaEventRecord(h0->ev_fork, h0->stream);
-      cudaStreamWaitEvent(h0->side, h0->ev_fork, 0);
-      comm_reduce(G, true);
-      cudaEventRecord(h0->ev_join, h0->side);
-    } else if (dist) {
-      comm_reduce(G, false);
-    }
+    if (ov) fork_reduce(G);
+    else if (dist) comm_reduce(G, false);
+    each_ilu(G, SZ0, SNV, 1);  // ILU(0): n_i = M^-1 z_i (line 13)
     if (dist) comm_halo(G, {SNV});  // n_i ghosts for v_i = A n_i
     each(G, PH_SPMVB);  // lines 13-14
-    if (ov) cudaStreamWaitEvent(h0->stream, h0->ev_join, 0);
+    if (ov) join_reduce(G);
     each_fin(G, F_SWEEPA);
     each(G, PH_SWEEPC);
-    reduce_fin(G, F_SWEEPC);
-    if (with_rr) {
-      if (dist) comm_halo(G, {SX, SG});
-      each(G, PH_RR1);
-      if (h0->auto_rr) reduce_fin(G, F_RR1);  // norms of the replaced vectors
-      if (dist) comm_halo(G, {SK, SL});         // w := A k, z := A l
-      each(G, PH_RR2);
-      reduce_fin(G, F_RR2);
+    if (ov && !with_rr) {
+      fork_reduce(G);
+      each_ilu(G, SW0, SMV, 1);  // ILU(0): m_{i+1} = M^-1 w_{i+1} (line 22)
+      comm_halo(G, {SMV});
+      each(G, PH_SPMVD);  // lines 22-23 (harmless if this iteration converged)
+      join_reduce(G);
+      each_fin(G, F_SWEEPC);
+    } else {
+      reduce_fin(G, F_SWEEPC);
+      if (with_rr) {
+        if (dist) comm_halo(G, {SX, SG});
+        each(G, PH_RR1);
+        each_ilu(G, SR, SK, 2);  // ILU(0): k := M^-1 r, l := M^-1 s (eq:rr)
+        each_ilu(G, SS, SL, 2);
+        if (h0->auto_rr) reduce_fin(G, F_RR1);  // norms of the replaced vectors
+        if (dist) comm_halo(G, {SK, SL});         // w := A k, z := A l
+        each(G, PH_RR2);
+        reduce_fin(G, F_RR2);
+      }
+      each_ilu(G, SW0, SMV, 1);  // ILU(0): m_{i+1} from the (replaced) w (A27)
+      if (dist) comm_halo(G, {SMV});  // m_{i+1} ghosts
+      each(G, PH_SPMVD);  // lines 22-23
     }
-    if (dist) comm_halo(G, {SMV});  // m_{i+1} ghosts
-    each(G, PH_SPMVD);  // lines 22-23
   }
   if (h0->gap_on) {
     if (dist) comm_halo(G, {SX});
@@ -1016,15 +1060,17 @@ pbicg_status ensure_hist(pbicg_ctx* h, int64_t need) {
   if (need <= h->hist_cap) return PBICG_OK;
   destroy_graphs(h);  // graphs captured the old pointers
   int64_t cap = need < 1024 ? 1024 : need;
-  void *a = nullptr, *b = nullptr, *c = nullptr, *d = nullptr;
+  void *a = nullptr, *b = nullptr, *c = nullptr, *d = nullptr, *e = nullptr;
   ST(dalloc(h, &a, (size_t)cap * sizeof(double)));
   ST(dalloc(h, &b, (size_t)cap * sizeof(double)));
   ST(dalloc(h, &c, (size_t)cap * sizeof(double)));
   ST(dalloc(h, &d, (size_t)cap * sizeof(int32_t)));
+  ST(dalloc(h, &e, (size_t)cap * SC_W * sizeof(double)));
   h->hist.rnorm = (double*)a;
   h->hist.gap = (double*)b;
   h->hist.fr = (double*)c;
   h->hist.rrl = (int32_t*)d;
+  h->hist.sc = (double*)e;
   h->hist_cap = cap;
   return PBICG_OK;
 }
@@ -1639,18 +1685,18 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
 
 // ---------------------------- CSR construction --------------------------------
 pbicg_status validate_csr(const pbicg_csr* op, int nranks, std::vector<double>* dinv,
-                          int64_t* width, bool* uniform) {
+                          int64_t* width, bool* uniform, int64_t halo = PBICG_CSR_HALO) {
   if (!op || !op->row_ptr || (op->n_local > 0 && (!op->col || !op->val)))
     return fail(nullptr, PBICG_EINVAL, "NULL argument");
   const int64_t n = op->n_local;
   if (op->n_global < 1 || n < 1 || op->row_begin < 0 || op->row_begin + n > op->n_global)
     return fail(nullptr, PBICG_EINVAL, "bad row range");
   if (op->n_global > INT32_MAX) return fail(nullptr, PBICG_EINVAL, "n_global must fit int32");
-  const int64_t H = nranks > 1 ? PBICG_CSR_HALO : 0;
+  const int64_t H = nranks > 1 ? halo : 0;
   if (nranks == 1 && (op->row_begin != 0 || n != op->n_global))
     return fail(nullptr, PBICG_EINVAL, "single rank: the rank must own all rows");
   if (nranks > 1 && n < H)
-    return fail(nullptr, PBICG_EINVAL, "multi-rank CSR: every rank needs >= PBICG_CSR_HALO rows");
+    return fail(nullptr, PBICG_EINVAL, "multi-rank CSR: every rank needs >= halo (PBICG_CSR_HALO) rows");
   const int64_t lo = op->row_begin - H, hi = op->row_begin + n + H;
   const int64_t* rp = op->row_ptr;
   *width = 0;
@@ -1786,9 +1832,13 @@ void csr_bound_consts(const pbicg_csr* ops, int nops, int bj, double* nA, double
   *mutN = (double)bj * std::sqrt((double)N) * mi;
 }
 
+pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* st);
+
 pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<double>& dinv,
-                       int64_t width, bool uniform, int bj) {
+                       int64_t width, bool uniform, int bj, int ilu = 0,
+                       const pbicg_stencil* st = nullptr, int64_t halo = PBICG_CSR_HALO) {
   h->kind = KIND_CSR;
+  h->ilu = ilu;
   if (bj > 1) {
     if (op->n_local % bj != 0 || op->row_begin % bj != 0)
       return fail(h, PBICG_EINVAL, "block Jacobi: rank rows must be whole aligned blocks");
@@ -1809,7 +1859,7 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
   h->n_global = op->n_global;
   h->n_local = n;
   h->row_begin = op->row_begin;
-  h->H = h->nranks > 1 ? PBICG_CSR_HALO : 0;
+  h->H = h->nranks > 1 ? halo : 0;
   h->halo_n = h->H;
   h->block = 256;
   // column-major ELL in stored row order; padding slots are never read (len[])
@@ -1843,13 +1893,13 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
   h->csr.dinv = h->dinv_g;
   const int64_t blocks = (n + h->block - 1) / h->block;
   // (the NRM variants reuse these grids: grid-stride loops, last-CTA reductions)
-  h->grid[K_INIT] = occ_grid(h, c_init1<false, false>, blocks);
-  h->grid[K_SWEEPA] = occ_grid(h, c_sweepA<false, false>, blocks);
-  h->grid[K_SWEEPC] = occ_grid(h, c_sweepC<false, false>, blocks);
+  h->grid[K_INIT] = occ_grid(h, c_init1<false, PK_JAC>, blocks);
+  h->grid[K_SWEEPA] = occ_grid(h, c_sweepA<false, PK_JAC>, blocks);
+  h->grid[K_SWEEPC] = occ_grid(h, c_sweepC<false, PK_JAC>, blocks);
   h->grid[K_SPMVB] = occ_grid(h, c_spmvB, blocks);
   h->grid[K_SPMVD] = occ_grid(h, c_spmvD, blocks);
-  h->grid[K_RR1] = occ_grid(h, c_rr1<false, false>, blocks);
-  h->grid[K_RR2] = occ_grid(h, c_rr2<false, false>, blocks);
+  h->grid[K_RR1] = occ_grid(h, c_rr1<false, PK_JAC>, blocks);
+  h->grid[K_RR2] = occ_grid(h, c_rr2<false, PK_JAC>, blocks);
   h->grid[K_GAP] = occ_grid(h, c_gap, blocks);
   h->grid[K_APPLY] = occ_grid(h, c_apply, blocks);
   ST(gvec(h, &h->V.nv));
@@ -1928,7 +1978,263 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
     h->cst_ok = e == cudaSuccess && h->H % 2 == 0;  // 16-byte aligned row pairs
     cudaGetLastError();
   }
-  return alloc_common(h);
+  ST(alloc_common(h));
+  if (ilu) ST(ilu_setup(h, op, st));
+  return PBICG_OK;
+}
+
+// ------------------------------ ILU(0) / ICC(0) ---------------------------------
+// ILU(0) of this rank's diagonal block (reading A34): Saad's IKJ Gaussian elimination
+// restricted to the pattern (columns of other ranks dropped), pivots as reciprocals --
+// the same operations in the same order as oracle.c orc_ilu0_factor (a row's entries
+// are located through a scatter map instead of a search: same arithmetic).
+// lu[p] (p indexes op's entries) = l_ik below the diagonal, u_ij on / above it.
+pbicg_status ilu0_host(const pbicg_csr* op, std::vector<double>* lu, std::vector<double>* uinv) {
+  const int64_t n = op->n_local, rb = op->row_begin, p0 = op->row_ptr[0];
+  const int64_t* rp = op->row_ptr;
+  const int64_t nnz = rp[n] - p0;
+  lu->assign(op->val, op->val + nnz);
+  uinv->assign((size_t)n, 0.0);
+  std::vector<int64_t> pos((size_t)n, -1);
+  double* L = lu->data();
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = op->col[p] - rb;
+      if (c >= 0 && c < n) pos[(size_t)c] = p - p0;
+    }
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t k = op->col[p] - rb;
+      if (k < 0) continue;
+      if (k >= i) break;
+      const int64_t pk = p - p0;
+      L[pk] = L[pk] * (*uinv)[(size_t)k];
+      for (int64_t q = rp[k]; q < rp[k + 1]; ++q) {
+        const int64_t j = op->col[q] - rb;
+        if (j <= k || j >= n) continue;
+        const int64_t pj = pos[(size_t)j];
+        if (pj >= 0) L[pj] = L[pj] - L[pk] * L[q - p0];
+      }
+    }
+    const int64_t pd = pos[(size_t)i];
+    if (pd < 0 || L[pd] == 0.0 || !std::isfinite(L[pd]))
+      return fail(nullptr, PBICG_EINVAL, "ILU(0): zero or non-finite pivot in row " +
+                                             std::to_string(rb + i));
+    (*uinv)[(size_t)i] = 1.0 / L[pd];
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = op->col[p] - rb;
+      if (c >= 0 && c < n) pos[(size_t)c] = -1;
+    }
+  }
+  return PBICG_OK;
+}
+
+// ICC(0) needs a symmetric diagonal block (the block M is built from)
+bool block_symmetric(const pbicg_csr* op) {
+  const int64_t n = op->n_local, rb = op->row_begin;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t p = op->row_ptr[i]; p < op->row_ptr[i + 1]; ++p) {
+      const int64_t c = op->col[p] - rb;
+      if (c < 0 || c >= n) continue;
+      const int32_t* b = op->col + op->row_ptr[c];
+      const int32_t* e = op->col + op->row_ptr[c + 1];
+      const int32_t* f = std::lower_bound(b, e, (int32_t)(rb + i));
+      if (f == e || *f != rb + i || op->val[op->row_ptr[c] + (f - b)] != op->val[p]) return false;
+    }
+  return true;
+}
+
+pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* st) {
+  std::vector<double> lu, uinv;
+  ST(ilu0_host(op, &lu, &uinv));
+  const int64_t n = op->n_local, rb = op->row_begin, p0 = op->row_ptr[0];
+  const int64_t* rp = op->row_ptr;
+  IluOp& P = h->ilu_op;
+  void* pu = nullptr;
+  ST(dalloc(h, &pu, (size_t)n * sizeof(double)));
+  ST(upload(h, pu, uinv.data(), (size_t)n * sizeof(double)));
+  P.uinv = (const double*)pu;
+  void* pc = nullptr;
+  ST(dalloc(h, &pc, 8 * sizeof(unsigned int)));
+  CU(cudaMemsetAsync(pc, 0, 8 * sizeof(unsigned int), h->stream));
+  P.ctr = (unsigned int*)pc;
+  P.n = n;
+  // stencil: the wavefront kernels recompute l_ik = fl(c_leg uinv_k) and u_ij = c_leg;
+  // confirm the factors are exactly that (no fill interaction on a 5/7-point stencil)
+  bool st_ok = st != nullptr;
+  if (st_ok) {
+    const double* c = st->coef;
+    for (int64_t i = 0; i < n && st_ok; ++i)
+      for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+        const int64_t k = op->col[p] - rb;
+        if (k < 0 || k >= n || k == i) continue;
+        const int64_t d = i - k;  // > 0: lower leg
+        const int leg = d == 1 ? 1 : d == -1 ? 2 : d == st->nx ? 3 : d == -st->nx ? 4
+                        : d > 0 ? 5 : 6;
+        const double want = d > 0 ? c[leg] * uinv[(size_t)k] : c[leg];
+        if (lu[(size_t)(p - p0)] != want) { st_ok = false; break; }
+      }
+  }
+  h->ilu_st = st_ok;
+  if (st_ok) {
+    const Geo& g = h->geo;  // set by the stencil create path
+    P.dim = st->dim;
+    P.nx = st->nx;
+    P.cxm = st->coef[1];
+    P.cxp = st->coef[2];
+    P.cam = st->coef[3];
+    P.cap = st->coef[4];
+    if (st->dim == 3) {
+      P.na = st->ny;
+      P.nb = g.nol;
+      P.sa = st->nx;
+      P.sb = st->nx * st->ny;
+      P.cbm = st->coef[5];
+      P.cbp = st->coef[6];
+      P.TA = (int32_t)(st->ny < 16 ? st->ny : 16);
+      const int64_t tb = ILU_T / P.TA;
+      P.TB = (int32_t)(g.nol < tb ? g.nol : tb);
+    } else {
+      P.na = g.nol;
+      P.nb = 1;
+      P.sa = st->nx;
+      P.sb = 0;
+      P.cbm = P.cbp = 0.0;
+      P.TA = (int32_t)(g.nol < ILU_T ? g.nol : ILU_T);
+      P.TB = 1;
+    }
+    P.nta = (int32_t)((P.na + P.TA - 1) / P.TA);
+    P.ntb = (int32_t)((P.nb + P.TB - 1) / P.TB);
+    P.ntiles = P.nta * P.ntb;
+    std::vector<int32_t> order;  // diagonals of the tile grid, then A
+    for (int32_t d = 0; d <= P.nta + P.ntb - 2; ++d)
+      for (int32_t A = 0; A < P.nta; ++A) {
+        const int32_t B = d - A;
+        if (B >= 0 && B < P.ntb) order.push_back(A + P.nta * B);
+      }
+    void *po = nullptr, *pf = nullptr, *pb = nullptr;
+    ST(dalloc(h, &po, order.size() * sizeof(int32_t)));
+    ST(upload(h, po, order.data(), order.size() * sizeof(int32_t)));
+    ST(dalloc(h, &pf, (size_t)P.ntiles * sizeof(unsigned long long)));
+    ST(dalloc(h, &pb, (size_t)P.ntiles * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(pf, 0, (size_t)P.ntiles * sizeof(unsigned long long), h->stream));
+    CU(cudaMemsetAsync(pb, 0, (size_t)P.ntiles * sizeof(unsigned long long), h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    P.order = (const int32_t*)po;
+    P.prog_f = (unsigned long long*)pf;
+    P.prog_b = (unsigned long long*)pb;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_st<3, false>, ILU_T, 0);
+    const int64_t cap = (int64_t)(occ < 1 ? 1 : occ) * h->num_sm;
+    h->ilu_grid = (int)(P.ntiles < cap ? P.ntiles : cap);
+    return PBICG_OK;
+  }
+  // general CSR: strictly lower / upper parts as column-major ELL, level orders
+  std::vector<int32_t> nl((size_t)n, 0), nu((size_t)n, 0), lev((size_t)n, 0), levb((size_t)n, 0);
+  int32_t wl = 0, wu = 0, nlev = 0, nlevb = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    int32_t l = 0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = op->col[p] - rb;
+      if (c < 0 || c >= n || c == i) continue;
+      if (c < i) { nl[(size_t)i]++; l = std::max(l, lev[(size_t)c] + 1); }
+      else nu[(size_t)i]++;
+    }
+    lev[(size_t)i] = l;
+    nlev = std::max(nlev, l + 1);
+    wl = std::max(wl, nl[(size_t)i]);
+    wu = std::max(wu, nu[(size_t)i]);
+  }
+  for (int64_t i = n - 1; i >= 0; --i) {
+    int32_t l = 0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = op->col[p] - rb;
+      if (c > i && c < n) l = std::max(l, levb[(size_t)c] + 1);
+    }
+    levb[(size_t)i] = l;
+    nlevb = std::max(nlevb, l + 1);
+  }
+  std::vector<int32_t> lcol((size_t)wl * n, -1), ucol((size_t)wu * n, -1);
+  std::vector<double> lval((size_t)wl * n, 0.0), uval((size_t)wu * n, 0.0);
+  for (int64_t i = 0; i < n; ++i) {
+    int32_t a = 0, b = 0;
+    for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+      const int64_t c = op->col[p] - rb;
+      if (c < 0 || c >= n || c == i) continue;
+      if (c < i) {
+        lcol[(size_t)a * n + i] = (int32_t)c;
+        lval[(size_t)a * n + i] = lu[(size_t)(p - p0)];
+        a++;
+      } else {
+        ucol[(size_t)b * n + i] = (int32_t)c;
+        uval[(size_t)b * n + i] = lu[(size_t)(p - p0)];
+        b++;
+      }
+    }
+  }
+  // counting sort by level (forward: ascending rows within a level; backward: descending)
+  std::vector<int64_t> cnt((size_t)nlev + 1, 0), cntb((size_t)nlevb + 1, 0);
+  for (int64_t i = 0; i < n; ++i) { cnt[(size_t)lev[(size_t)i] + 1]++; cntb[(size_t)levb[(size_t)i] + 1]++; }
+  for (size_t k = 1; k < cnt.size(); ++k) cnt[k] += cnt[k - 1];
+  for (size_t k = 1; k < cntb.size(); ++k) cntb[k] += cntb[k - 1];
+  std::vector<int32_t> ford((size_t)n), bord((size_t)n);
+  for (int64_t i = 0; i < n; ++i) ford[(size_t)cnt[(size_t)lev[(size_t)i]]++] = (int32_t)i;
+  for (int64_t i = n - 1; i >= 0; --i) bord[(size_t)cntb[(size_t)levb[(size_t)i]]++] = (int32_t)i;
+  auto up = [&](const void* src, size_t bytes, void** dst) -> pbicg_status {
+    ST(dalloc(h, dst, bytes));
+    if (bytes) ST(upload(h, *dst, src, bytes));
+    return PBICG_OK;
+  };
+  void *a1, *a2, *a3, *a4, *a5, *a6, *a7;
+  ST(up(lcol.data(), lcol.size() * sizeof(int32_t), &a1));
+  ST(up(lval.data(), lval.size() * sizeof(double), &a2));
+  ST(up(ucol.data(), ucol.size() * sizeof(int32_t), &a3));
+  ST(up(uval.data(), uval.size() * sizeof(double), &a4));
+  ST(up(ford.data(), ford.size() * sizeof(int32_t), &a5));
+  ST(up(bord.data(), bord.size() * sizeof(int32_t), &a6));
+  ST(dalloc(h, &a7, (size_t)n * sizeof(unsigned int)));
+  CU(cudaMemsetAsync(a7, 0, (size_t)n * sizeof(unsigned int), h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  P.wl = wl;
+  P.wu = wu;
+  P.lcol = (const int32_t*)a1;
+  P.lval = (const double*)a2;
+  P.ucol = (const int32_t*)a3;
+  P.uval = (const double*)a4;
+  P.ford = (const int32_t*)a5;
+  P.bord = (const int32_t*)a6;
+  P.rflag = (unsigned int*)a7;
+  P.ntiles = nlev;  // (diagnostic: level count)
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_csr<false>, 256, 0);
+  const int64_t cap = (int64_t)(occ < 1 ? 1 : occ) * h->num_sm;
+  const int64_t need = (n + 255) / 256;
+  h->ilu_grid = (int)(need < cap ? (need < 1 ? 1 : need) : cap);
+  return PBICG_OK;
+}
+
+// stencil rows of this rank written out as CSR (global columns, ascending; Dirichlet
+// legs dropped) for the ILU(0) handles, which run the CSR schedule
+void stencil_rows_csr(const pbicg_stencil* op, int64_t row_begin, int64_t n_local,
+                      std::vector<int64_t>* rp, std::vector<int32_t>* ci, std::vector<double>* va) {
+  const int64_t nx = op->nx, ny = op->ny, nz = op->dim == 3 ? op->nz : 1;
+  const int64_t pxy = nx * ny;
+  const double* c = op->coef;
+  rp->assign((size_t)n_local + 1, 0);
+  ci->clear();
+  va->clear();
+  for (int64_t r = 0; r < n_local; ++r) {
+    const int64_t row = row_begin + r;
+    const int64_t x = row % nx, y = (row / nx) % ny, z = row / pxy;
+    auto put = [&](int64_t col, double v) { ci->push_back((int32_t)col); va->push_back(v); };
+    if (op->dim == 3 && z > 0) put(row - pxy, c[5]);
+    if (y > 0) put(row - nx, c[3]);
+    if (x > 0) put(row - 1, c[1]);
+    put(row, c[0]);
+    if (x < nx - 1) put(row + 1, c[2]);
+    if (y < ny - 1) put(row + nx, c[4]);
+    if (op->dim == 3 && z < nz - 1) put(row + pxy, c[6]);
+    (*rp)[(size_t)r + 1] = (int64_t)ci->size();
+  }
 }
 
 void destroy_one(pbicg_ctx* h) {
@@ -2001,9 +2307,10 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
     CU(cudaMemcpyAsync(m->V.b, io[r].b, nb, cudaMemcpyDeviceToDevice, m->stream));
     CU(cudaMemcpyAsync(m->V.x, io[r].x0, nb, cudaMemcpyDeviceToDevice, m->stream));
     // A1: g, s, l, z_{-1} (and the spare buffers) start at zero
-    double* zs[] = {m->V.g, m->V.s, m->V.l, m->V.z0, m->V.z1, m->V.zrr};
+    // (ILU(0): n_{-1} = M^-1 z_{-1} = 0 is read from nv by the first sweep A)
+    double* zs[] = {m->V.g, m->V.s, m->V.l, m->V.z0, m->V.z1, m->V.zrr, m->ilu ? m->V.nv : nullptr};
     for (double* v : zs)
-      CU(cudaMemsetAsync(v - m->H, 0, nb + 2 * m->H * sizeof(double), m->stream));
+      if (v) CU(cudaMemsetAsync(v - m->H, 0, nb + 2 * m->H * sizeof(double), m->stream));
     Scal s0;
     memset(&s0, 0, sizeof(s0));
     s0.tol = tol;
@@ -2092,6 +2399,45 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
   return PBICG_OK;
 }
 
+// 0: not an incomplete factorisation; 1: ILU(0); 2: ICC(0) (reading A34)
+int prec_ilu(int prec) {
+  return prec == PBICG_PREC_ILU0 ? 1 : prec == PBICG_PREC_ICC0 ? 2 : 0;
+}
+
+// An ILU(0) / ICC(0) stencil handle runs the CSR schedule (stored n = M^-1 z and
+// m = M^-1 w, the paper's split schedule) on the stencil written out as CSR for this
+// rank's slab (ghost band = one plane / line), with the stencil wavefront kernels for
+// M^-1 (the factors are those of the slab's diagonal block).
+pbicg_status build_stencil_ilu(pbicg_ctx* h, const pbicg_stencil* op, int ilu) {
+  if (ilu == 2 && (op->coef[1] != op->coef[2] || op->coef[3] != op->coef[4] ||
+                   (op->dim == 3 && op->coef[5] != op->coef[6])))
+    return fail(h, PBICG_EINVAL, "ICC(0) needs a symmetric stencil (use PBICG_PREC_ILU0)");
+  const int64_t nz = op->dim == 3 ? op->nz : 1;
+  const int64_t outer = op->dim == 3 ? nz : op->ny;
+  const int64_t plane = op->dim == 3 ? op->nx * op->ny : op->nx;
+  Geo& g = h->geo;
+  g.nx = op->nx;
+  g.ny = op->ny;
+  g.nog = outer;
+  slab(outer, h->nranks, h->rank, &g.o0, &g.nol);
+  g.pxy = plane;
+  for (int i = 0; i < 7; ++i) g.c[i] = op->coef[i];
+  g.dinv = 1.0 / op->coef[0];
+  h->dim = op->dim;
+  std::vector<int64_t> rp;
+  std::vector<int32_t> ci;
+  std::vector<double> va;
+  const int64_t rb = g.o0 * plane, nl = g.nol * plane;
+  stencil_rows_csr(op, rb, nl, &rp, &ci, &va);
+  pbicg_csr c2{op->nx * op->ny * nz, rb, nl, rp.data(), ci.data(), va.data()};
+  std::vector<double> dinv;
+  int64_t width = 0;
+  bool uniform = true;
+  pbicg_status st = validate_csr(&c2, h->nranks, &dinv, &width, &uniform, plane);
+  if (st) return fail(h, st, g_create_err);
+  return build_csr(h, &c2, dinv, width, uniform, 1, ilu, op, plane);
+}
+
 // P handles sharing one stream (loopback transport)
 pbicg_group* new_group(void* cuda_stream, cudaStream_t* s, bool* own) {
   *s = (cudaStream_t)cuda_stream;
@@ -2113,10 +2459,11 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
                                       pbicg_handle* out) {
   if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
   *out = nullptr;
-  const int bj = prec_block(prec);
+  const int ilu = prec_ilu(prec);
+  const int bj = ilu ? 1 : prec_block(prec);
   if (!bj || bj > 8)
     return fail(nullptr, PBICG_EINVAL,
-                "stencil prec must be PBICG_PREC_JACOBI or PBICG_PREC_BJ(2|4|8)");
+                "stencil prec must be PBICG_PREC_JACOBI, _ILU0, _ICC0 or PBICG_PREC_BJ(2|4|8)");
   const int nranks = dist ? dist->nranks : 1;
   if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
     return fail(nullptr, PBICG_EINVAL, "inconsistent nranks/rank");
@@ -2126,7 +2473,12 @@ pbicg_status pbicgstab_create_stencil(const pbicg_stencil* op, pbicg_prec prec,
   h->rank = dist ? dist->rank : 0;
   pbicg_status st = common_setup(h, cuda_stream);
   if (!st && (nranks > 1 || (dist && dist->nccl_id_halo))) st = nccl_setup(h, dist);
-  if (!st) st = build_stencil(h, op, bj);
+  if (!st) st = ilu ? build_stencil_ilu(h, op, ilu) : build_stencil(h, op, bj);
+  if (!st && ilu && h->dist) {  // dinv ghosts of the CSR schedule, once (collective)
+    comm_halo(Members{h}, {[](pbicg_ctx* c) { return c->dinv_g; }});
+    cudaError_t e = cudaStreamSynchronize(h->stream);
+    if (e != cudaSuccess) st = fail(h, PBICG_ECUDA, cudaGetErrorString(e));
+  }
   if (st) {
     g_create_err = h->err;
     destroy_one(h);
@@ -2140,9 +2492,13 @@ pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pb
                                   void* cuda_stream, pbicg_handle* out) {
   if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
   *out = nullptr;
-  const int bj = prec_block(prec);
+  const int ilu = prec_ilu(prec);
+  const int bj = ilu ? 1 : prec_block(prec);
   if (!bj)
-    return fail(nullptr, PBICG_EINVAL, "prec must be PBICG_PREC_JACOBI or PBICG_PREC_BJ(2..32)");
+    return fail(nullptr, PBICG_EINVAL,
+                "prec must be PBICG_PREC_JACOBI, _ILU0, _ICC0 or PBICG_PREC_BJ(2..32)");
+  if (ilu == 2 && op && op->row_ptr && !block_symmetric(op))
+    return fail(nullptr, PBICG_EINVAL, "ICC(0) needs a symmetric (diagonal block of the) matrix");
   const int nranks = dist ? dist->nranks : 1;
   if (dist && (dist->nranks < 1 || dist->rank < 0 || dist->rank >= dist->nranks))
     return fail(nullptr, PBICG_EINVAL, "inconsistent nranks/rank");
@@ -2155,7 +2511,7 @@ pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pb
   h->rank = dist ? dist->rank : 0;
   pbicg_status st = common_setup(h, cuda_stream);
   if (!st && (nranks > 1 || (dist && dist->nccl_id_halo))) st = nccl_setup(h, dist);
-  if (!st) st = build_csr(h, op, dinv, width, uniform, bj);
+  if (!st) st = build_csr(h, op, dinv, width, uniform, bj, ilu);
   if (!st && h->dist) {  // dinv ghosts, once (collective)
     comm_halo(Members{h}, {[](pbicg_ctx* c) { return c->dinv_g; }});
     cudaError_t e = cudaStreamSynchronize(h->stream);
@@ -2174,10 +2530,11 @@ pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_pr
                                                int32_t nranks, void* cuda_stream,
                                                pbicg_handle* out) {
   if (!out) return fail(nullptr, PBICG_EINVAL, "NULL argument");
-  const int bj = prec_block(prec);
+  const int ilu = prec_ilu(prec);
+  const int bj = ilu ? 1 : prec_block(prec);
   if (!bj || bj > 8)
     return fail(nullptr, PBICG_EINVAL,
-                "stencil prec must be PBICG_PREC_JACOBI or PBICG_PREC_BJ(2|4|8)");
+                "stencil prec must be PBICG_PREC_JACOBI, _ILU0, _ICC0 or PBICG_PREC_BJ(2|4|8)");
   ST(validate_stencil(op, nranks));
   for (int r = 0; r < nranks; ++r) out[r] = nullptr;
   cudaStream_t s;
@@ -2196,8 +2553,12 @@ pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_pr
     grp->alive++;
     st = common_setup(h, s);
     if (r == 0) h->own_stream = own;
-    if (!st) st = build_stencil(h, op, bj);
+    if (!st) st = ilu ? build_stencil_ilu(h, op, ilu) : build_stencil(h, op, bj);
     if (st) g_create_err = h->err;
+  }
+  if (!st && ilu && nranks > 1) {  // dinv ghosts of the CSR schedule
+    comm_halo(grp->m, {[](pbicg_ctx* c) { return c->dinv_g; }});
+    if (cudaStreamSynchronize(s) != cudaSuccess) st = fail(nullptr, PBICG_ECUDA, "dinv halo");
   }
   if (st) {
     Members m = grp->m;
@@ -2211,9 +2572,11 @@ pbicg_status pbicgstab_create_stencil_loopback(const pbicg_stencil* op, pbicg_pr
 pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec, int32_t nranks,
                                            void* cuda_stream, pbicg_handle* out) {
   if (!out || !ops || nranks < 1) return fail(nullptr, PBICG_EINVAL, "bad argument");
-  const int bj = prec_block(prec);
+  const int ilu = prec_ilu(prec);
+  const int bj = ilu ? 1 : prec_block(prec);
   if (!bj)
-    return fail(nullptr, PBICG_EINVAL, "prec must be PBICG_PREC_JACOBI or PBICG_PREC_BJ(2..32)");
+    return fail(nullptr, PBICG_EINVAL,
+                "prec must be PBICG_PREC_JACOBI, _ILU0, _ICC0 or PBICG_PREC_BJ(2..32)");
   for (int r = 0; r < nranks; ++r) out[r] = nullptr;
   std::vector<std::vector<double>> dinv(nranks);
   std::vector<int64_t> width(nranks);
@@ -2244,7 +2607,9 @@ pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec
     grp->alive++;
     st = common_setup(h, s);
     if (r == 0) h->own_stream = own;
-    if (!st) st = build_csr(h, &ops[r], dinv[r], width[r], uni[r] != 0, bj);
+    if (!st && ilu == 2 && !block_symmetric(&ops[r]))
+      st = fail(h, PBICG_EINVAL, "ICC(0) needs symmetric diagonal blocks");
+    if (!st) st = build_csr(h, &ops[r], dinv[r], width[r], uni[r] != 0, bj, ilu);
     if (st) g_create_err = h->err;
   }
   if (!st) {
@@ -2253,7 +2618,7 @@ pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec
   }
   if (!st) {
     double nA = 0, muN = 0, mutN = 0;
-    csr_bound_consts(ops, nranks, prec_block(prec), &nA, &muN, &mutN);
+    csr_bound_consts(ops, nranks, bj, &nA, &muN, &mutN);
     for (pbicg_ctx* m : grp->m) {
       m->ar_nA = nA;
       m->ar_muN = muN;
@@ -2331,6 +2696,8 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       m->tile_on = value != 0;
       destroy_graphs(m);
     } else if (k == "rr_auto") {
+      if (value != 0 && m->ilu)
+        return fail(h, PBICG_EINVAL, "rr_auto is not defined for ILU(0) / ICC(0) (reading A34)");
       if (value != 0 && (m->method != M_PBICGSTAB || !m->ar_ok ||
                          (m->kind == KIND_STENCIL && (!m->tile_ok || m->schedule == 2))))
         return fail(h, PBICG_EINVAL,
@@ -2585,6 +2952,17 @@ pbicg_status pbicgstab_rr_info(pbicg_handle h, double* fr_hist, int32_t* rr_iter
     const int32_t c = n < cap ? n : cap;
     CU(cudaMemcpy(rr_iters, h->hist.rrl, (size_t)c * sizeof(int32_t), cudaMemcpyDeviceToHost));
   }
+  return PBICG_OK;
+}
+
+pbicg_status pbicgstab_scalar_trace(pbicg_handle h, double* out, int32_t cap) {
+  if (!h || !out || cap < 0) return fail(h, PBICG_EINVAL, "NULL argument");
+  if (h->last_iters < 0) return fail(h, PBICG_ESTATE, "no solve has completed on this handle");
+  if (h->comm == COMM_LOOP && h->group && h->group->m[0] != h)
+    return fail(h, PBICG_EINVAL, "loopback group: ask rank 0's handle");
+  if (h->method != M_PBICGSTAB) return fail(h, PBICG_EINVAL, "scalar trace: method 0 only");
+  const int32_t n = h->last_iters < cap ? h->last_iters : cap;
+  if (n > 0) CU(cudaMemcpy(out, h->hist.sc, (size_t)n * SC_W * sizeof(double), cudaMemcpyDeviceToHost));
   return PBICG_OK;
 }
 

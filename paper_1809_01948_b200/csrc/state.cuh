@@ -19,7 +19,8 @@
 #define OUT_MAXIT 1
 #define OUT_BREAKDOWN 2
 #define RED_K 16  // dot slots per rank in the reduction buffers
-#define P2P_MAXR 8  // ranks of the peer-memory transport (one NVSwitch domain of B200s)
+#define P2P_MAXR 8
+#define SC_W 9      // doubles per iteration of the scalar trace (Hist.sc)  // ranks of the peer-memory transport (one NVSwitch domain of B200s)
 
 struct Scal {
   double alpha, beta, omega, rho;  // alpha_i, beta_i, omega (latest), (r0, r_i)
@@ -77,6 +78,9 @@ struct Hist {
   double* gap;    // [maxit+1]
   double* fr;     // [maxit+1] run-time gap bound f^r_i (automated replacement)
   int32_t* rrl;   // [maxit] iterations i that replaced r_{i+1}
+  double* sc;     // [maxit][SC_W] p-BiCGStab scalars of iteration i: alpha_i, beta_i,
+                  // omega_i, rho_i, (q,y)_i, (y,y)_i, (r0,w), (r0,s), (r0,z) of line 21
+                  // (the oracle's sc_trace layout; parity diagnostics)
 };
 
 // ---------------------------------------------------------------------------
@@ -152,6 +156,12 @@ __device__ __forceinline__ void finalize_iteration(Scal* s, Hist h, double rho1,
   const int i = s->iter;
   const double hn = sqrt(rr);
   h.rnorm[i + 1] = hn;
+  {
+    double* t = h.sc + SC_W * (size_t)i;
+    t[6] = dw;
+    t[7] = ds;
+    t[8] = dz;
+  }
   s->iters = i + 1;
   s->iter = i + 1;
   if (hn < s->sqrt_eps * s->h0) s->rr_off = 1;
@@ -315,6 +325,15 @@ __device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot) {
     const double omn = (yy == 0.0) ? 0.0 : qy / yy;
     sc->omega = omn;
     sc->use_rr = 0;
+    {
+      double* t = h.sc + SC_W * (size_t)sc->iter;
+      t[0] = sc->alpha;
+      t[1] = sc->beta;
+      t[2] = omn;
+      t[3] = sc->rho;
+      t[4] = qy;
+      t[5] = yy;
+    }
     if (sc->auto_rr)
       for (int k = 0; k < 10; ++k) sc->nA_[k] = sqrt(dd_round(tot[2 + k]));
     if (!isfinite(omn)) {

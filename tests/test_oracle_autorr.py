@@ -91,7 +91,7 @@ def test_bound_dominates_exact_delta_recursion(orc):
     Dw = nrm(R.sub(Ax(V(0, "k")), V(0, "w")))
     Ds = Dz = 0.0
     for i in range(res.iters - 1):
-        al, be, om, _ = [F(float(a)) for a in res.scalars[i]]
+        al, be, om, _ = [F(float(a)) for a in res.scalars[i, :4]]
         om_prev = F(float(res.scalars[i - 1, 2])) if i > 0 else F(0)
         x, r, k, w = V(i, "x"), V(i, "r"), V(i, "k"), V(i, "w")
         g, s, l, z, q, u, y = (V(i, nm) for nm in "g s l z q u y".split())

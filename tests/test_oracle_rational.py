@@ -186,7 +186,7 @@ def test_local_errors_within_paper_bounds(orc):
     worst = 0.0
     zero = [F(0)] * n
     for i in range(iters - 1):
-        al, be, om, _ = [F(float(a)) for a in res.scalars[i]]
+        al, be, om, _ = [F(float(a)) for a in res.scalars[i, :4]]
         om_prev = F(float(res.scalars[i - 1, 2])) if i > 0 else F(0)
         k, w, m, t = V(i, "k"), V(i, "w"), V(i, "m"), V(i, "t")
         x, r = V(i, "x"), V(i, "r")
@@ -264,7 +264,7 @@ def test_gap_recurrences_exact(orc):
     zero = [F(0)] * n
     Ds_prev, Dz_prev = zero, zero
     for i in range(iters - 1):
-        al, be, om, _ = [F(float(a)) for a in res.scalars[i]]
+        al, be, om, _ = [F(float(a)) for a in res.scalars[i, :4]]
         om_prev = F(float(res.scalars[i - 1, 2])) if i > 0 else F(0)
         x, r, k, w = V(i, "x"), V(i, "r"), V(i, "k"), V(i, "w")
         g, s, l, z, q, u, y = (V(i, nm) for nm in "g s l z q u y".split())
