@@ -166,14 +166,14 @@ class PinnedCore:
             os.sched_setaffinity(0, self.old)
 
 
-def oracle_sample(st, maxit_sample: int, nz_sample: int, cfg=None, method="pbicgstab"):
+def oracle_sample(st, maxit_sample: int, nz_sample: int, cfg=None, method="pbicgstab", block=1):
     """Time the oracle (1 core, pinned) on an nx*ny*nz_sample slab of the workload
     (CSR: the full matrix for maxit_sample iterations)."""
     with PinnedCore():
-        return _oracle_sample(st, maxit_sample, nz_sample, cfg, method)
+        return _oracle_sample(st, maxit_sample, nz_sample, cfg, method, block)
 
 
-def _oracle_sample(st, maxit_sample, nz_sample, cfg, method):
+def _oracle_sample(st, maxit_sample, nz_sample, cfg, method, block):
     from oracle import oracle as orc
     solve = {"pbicgstab": orc.pbicgstab, "bicgstab": orc.bicgstab, "pipecg": orc.pipecg}[method]
     if isinstance(st, CsrShape):
@@ -182,10 +182,10 @@ def _oracle_sample(st, maxit_sample, nz_sample, cfg, method):
         xs = problems.x_star(A.n, 0)
         b = orc.spmv(A, xs)
         t0 = time.perf_counter()
-        solve(A, b, tol=0.0, maxit=0, bench=True, gap=False)
+        solve(A, b, tol=0.0, maxit=0, bench=True, gap=False, block=block)
         t_init = time.perf_counter() - t0
         t0 = time.perf_counter()
-        r = solve(A, b, tol=0.0, maxit=maxit_sample, bench=True, gap=False)
+        r = solve(A, b, tol=0.0, maxit=maxit_sample, bench=True, gap=False, block=block)
         t = time.perf_counter() - t0 - t_init
         return A.n * r.iters / t, A.n, r.iters, t
     nzs = min(nz_sample, st.nz if st.dim == 3 else st.ny)
@@ -197,10 +197,10 @@ def _oracle_sample(st, maxit_sample, nz_sample, cfg, method):
     xs = problems.x_star(A.n, 0)
     b = orc.spmv(A, xs)
     t0 = time.perf_counter()
-    solve(A, b, tol=0.0, maxit=0, bench=True, gap=False)
+    solve(A, b, tol=0.0, maxit=0, bench=True, gap=False, block=block)
     t_init = time.perf_counter() - t0
     t0 = time.perf_counter()
-    r = solve(A, b, tol=0.0, maxit=maxit_sample, bench=True, gap=False)
+    r = solve(A, b, tol=0.0, maxit=maxit_sample, bench=True, gap=False, block=block)
     t = time.perf_counter() - t0 - t_init
     rows_per_s = A.n * r.iters / t
     return rows_per_s, A.n, r.iters, t
@@ -358,7 +358,7 @@ def run_ours(args, rank, world):
     launches, _ = S.kernel_time("all")
     per_kernel = {}
     for k in ("sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap", "init", "apply", "fin",
-              "cl1", "cl2", "cl3", "pcg", "prec"):
+              "cl1", "cl2", "cl3", "pcg", "prec", "persist"):
         nk, tk = S.kernel_time(k)
         if nk:
             per_kernel[k] = {"launches": nk, "avg_ms": tk / nk if args.kernel_timing else None,
@@ -412,7 +412,9 @@ def run_ours(args, rank, world):
                    "maxit_per_step": maxit, "rr_period": rr, "gap_tracking": gap,
                    "rr_auto": bool(args.rr_auto),
                    **({"breakdown_at": breakdown_at} if breakdown_at else {}),
-                   "preconditioner": "jacobi" if args.block == 1 else f"block-jacobi {args.block}",
+                   "preconditioner": ("jacobi" if args.block == 1 else args.block.upper()
+                                      if isinstance(args.block, str) else
+                                      f"block-jacobi {args.block}"),
                    "method": args.method,
                    "schedule": (("split 4-phase (stencil), stand-alone TMA SpMVs the reductions "
                                  "hide behind" if args.schedule == 2 else SCHEDULES[args.method])
@@ -447,7 +449,8 @@ def run_ours(args, rank, world):
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and world == 1:
-        rows_per_s, n_s, its, t = oracle_sample(st, 6 if st.dim else 3, 64, cfg, args.method)
+        rows_per_s, n_s, its, t = oracle_sample(st, 6 if st.dim else 3, 64, cfg, args.method,
+                                                args.block)
         line["cpu_baseline"] = {
             "value": rows_per_s / st.n, "unit": UNIT, "cores": 1, "kind": "oracle",
             "cpu": cpu_model(), "pinning": "sched_setaffinity to one core (taskset -c)",
@@ -521,8 +524,9 @@ def main():
     ap.add_argument("--method", choices=["pbicgstab", "bicgstab", "pipecg"], default="pbicgstab",
                     help="solver: p-BiCGStab (the headline), classic BiCGStab or p-CG")
     ap.add_argument("--gap", type=int, default=0)
-    ap.add_argument("--block", type=int, default=1,
-                    help="block-Jacobi block size (1 = Jacobi; CSR 2..32, stencils 2|4|8)")
+    ap.add_argument("--block", type=lambda v: int(v) if v.isdigit() else v, default=1,
+                    help="preconditioner: block-Jacobi block size (1 = Jacobi; CSR 2..32, "
+                         "stencils 2|4|8), or ilu0 / icc0 (reading A34)")
     ap.add_argument("--rr-auto", type=int, default=0,
                     help="automated residual replacement (bound f^r + eq:criterion) instead of "
                          "the periodic schedule")

@@ -114,8 +114,8 @@ __device__ __forceinline__ double ell_row(const CsrOp& A, const double* __restri
 #define WROW_END }
 
 // NRM (automated replacement): the step's reduction also carries the
-// sums of squares of the vectors the bound f^r needs (plain fp64, reading A30)
-__device__ __forceinline__ void c_nrm(Dd& a, double v) { a.hi = a.hi + v * v; }
+// Dot2 sums of squares of the vectors the bound f^r needs (reading A30)
+__device__ __forceinline__ void c_nrm(Dd& a, double v) { dd_fma(a, v, v); }
 
 template <bool NRM, int PK>
 __global__ void __launch_bounds__(256) c_init1(CsrOp A, Vecs V, Scal* __restrict__ sc,

@@ -85,8 +85,8 @@ struct Hist {
 
 // ---------------------------------------------------------------------------
 // Automated replacement bookkeeping, one thread, same formulas and
-// operation order as oracle.c (the norms are the kernels' sums of squares, so
-// f^r agrees with the oracle to rounding, not bitwise; reading A30).
+// operation order as oracle.c; the norms are the kernels' Dot2 sums of squares
+// (reading A30), so f^r and the decisions are the oracle's bitwise.
 __device__ __forceinline__ void auto_step(Scal* s, Hist h, double R1) {
   const int i = s->iter;
   const double R = h.rnorm[i];

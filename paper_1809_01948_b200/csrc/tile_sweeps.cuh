@@ -39,10 +39,14 @@
 // never written to HBM; it is formed with the same operations as the oracle's
 // stored vector, hence bitwise equal.
 #pragma once
+#include <cooperative_groups.h>
+
 #include "dd.cuh"
 #include "state.cuh"
 #include "stencil_kernels.cuh"
 #include "tma.cuh"
+
+namespace cg = cooperative_groups;
 
 #define TNT 512  // threads per CTA
 
@@ -103,8 +107,9 @@ template <> struct TileTraits<TM_INIT1N> { enum { NSV = 1, DER = 0, PREC = 0, NS
 template <> struct TileTraits<TM_SPB> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 0 }; };
 template <> struct TileTraits<TM_SPD> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 0 }; };
 
-// sum of squares for a bound norm (plain fp64 per thread; reading A30)
-__device__ __forceinline__ void nrm_add(Dd& a, double v) { a.hi = a.hi + v * v; }
+// sum of squares for a bound norm: Dot2 (v, v) like every other dot (reading A30), so
+// the bound f^r and the replacement decisions are the oracle's bitwise
+__device__ __forceinline__ void nrm_add(Dd& a, double v) { dd_fma(a, v, v); }
 
 struct TileGeo {
   int64_t nx, ny;     // x extent; lines per plane (3D: ny, 2D: 1)
@@ -684,9 +689,11 @@ __device__ __noinline__ bool peer_put(double* hp_lo, double* hp_hi, const double
 // untaken runtime branch cost sweep A 0.5-1.3%).
 template <int M> struct HasPeer { enum { v = BaseOf<M>::v == TM_A || BaseOf<M>::v == TM_C }; };
 
+// The body of one tile step (a device function so the persistent iteration kernel
+// t_persist can run sweep A and sweep C back to back inside one launch).
 template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false, bool PEER = false>
-__global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
-                                                 Dd* __restrict__ part, Hist h) {
+__device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Scal* __restrict__ sc,
+                                            Dd* __restrict__ part, const Hist& h) {
   using T = TileTraits<MODE_>;
   constexpr int MODE = BaseOf<MODE_>::v;
   constexpr bool NRM = MODE_ != MODE;
@@ -1191,6 +1198,33 @@ __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __rest
       else if (MODE == TM_RR1) publish<F_RR1>(sc, h, tot);
       else publish<F_PINIT2>(sc, h, tot);
     }
+  }
+}
+
+template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false, bool PEER = false>
+__global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
+                                                 Dd* __restrict__ part, Hist h) {
+  t_tile_body<DIM, MODE_, VEC, BJ, SEG, PEER>(g, V, sc, part, h);
+}
+
+// Persistent iteration kernel (option "persist"; one rank, Jacobi, full-line tiles,
+// no replacement / gap in the stretch): L iterations of the fused schedule -- sweep
+// A, grid barrier, sweep C, grid barrier -- in ONE cooperative launch.  The scalars
+// the last CTA of each sweep forms (omega; beta, alpha, stop) are read by every CTA
+// after the barrier, exactly as the next kernel would read them, so the arithmetic
+// and its order are those of the two-kernel schedule (bitwise); what disappears is
+// the kernel boundary: launch, grid ramp-up and drain, twice per iteration (the
+// latency regime of small grids).
+template <int DIM, bool VEC>
+__global__ void __launch_bounds__(TNT, 1) t_persist(TileGeo g, Vecs V, Scal* __restrict__ sc,
+                                                    Dd* __restrict__ part, Hist h, int L) {
+  cg::grid_group grid = cg::this_grid();
+  for (int o = 0; o < L; ++o) {
+    if (*(volatile int32_t*)&sc->done) break;  // uniform: read after a grid barrier
+    t_tile_body<DIM, TM_A, VEC>(g, V, sc, part, h);
+    grid.sync();
+    t_tile_body<DIM, TM_C, VEC>(g, V, sc, part, h);
+    grid.sync();
   }
 }
 

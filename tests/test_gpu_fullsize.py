@@ -100,3 +100,41 @@ def test_cfg4_full_size_split_schedule(orc):
     ref = orc.pbicgstab(A, b, tol=0.0, maxit=3, rr_period=2, bench=True, gap=False)
     _compare(res, ref, xs)
 
+
+
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_converged_full_size_vs_golden(name):
+    """BASELINE cfg2 (2D 1024^2, tol 1e-10, ~2000 iterations) and cfg3 (3D 256^3,
+    tol 1e-10, replacement every 50, ~510 iterations) solved to convergence at full
+    size in bench.py's launch configuration (tile sweeps, CUDA graphs), against the
+    oracle's converged solve of the same inputs stored in tests/golden/fullsize_*.json
+    by scripts/make_golden_fullsize.py (which calls only oracle/).  The north-star
+    bars (||r_i|| within 1e-9 over the first 30, iterations +-2, error within 10x) and
+    the design target: bitwise ||r_i|| and gap histories over the whole solve and
+    bitwise x (sha256 of its bytes)."""
+    import hashlib
+    import json
+    import os
+    from paper_1809_01948_b200 import Solver
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", f"fullsize_{name}.json")))
+    cfg = problems.configs()[name]
+    st = cfg.stencil
+    assert g["n"] == st.n and g["tol"] == cfg.tol and g["rr_period"] == cfg.rr_period
+    S = Solver.stencil(st.dim, st.nx, st.ny, st.nz, st.coef)
+    xs = problems.x_star(st.n, g["x_star_seed"])
+    b_d = S.apply(torch.from_numpy(xs).cuda())
+    res = S.solve(b_d, tol=cfg.tol, maxit=cfg.maxit, rr_period=cfg.rr_period, gap=True)
+    rn = np.array([float.fromhex(h) for h in g["rnorm_hex"]])
+    gp = np.array([float.fromhex(h) for h in g["gap_hex"]])
+    k = min(30, g["iters"], res.iters)
+    assert np.max(np.abs(res.rnorm[:k + 1] / rn[:k + 1] - 1)) <= 1e-9
+    assert abs(res.iters - g["iters"]) <= 2 and res.outcome == g["outcome"]
+    x = res.x.cpu().numpy()
+    err = np.linalg.norm(x - xs) / np.linalg.norm(xs)
+    assert err <= 10 * g["err"]
+    assert res.iters == g["iters"]
+    assert np.array_equal(res.rnorm, rn), "rnorm history not bitwise"
+    assert np.array_equal(res.gap, gp), "gap history not bitwise"
+    assert hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest() == g["x_sha256"], \
+        "x not bitwise"
+    S.close()

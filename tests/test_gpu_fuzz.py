@@ -95,7 +95,10 @@ def test_fuzz_stencil(orc, seed):
     else:
         ref = orc.pipecg(A, b, **kw)
     assert res.outcome == ref.outcome, (res.outcome, ref.outcome)
-    noise_floor_parity(_rank0(S) if method == 0 else None, res, ref, xs, tag=f" stencil[{seed}]")
+    rerun = lambda m: orc.pbicgstab(A, b, rr_period=rr, auto_rr=auto, want_trace=True,
+                                    **dict(kw, maxit=m))
+    noise_floor_parity(_rank0(S) if method == 0 else None, res, ref, xs, tag=f" stencil[{seed}]",
+                       rerun=rerun)
     S.close()
 
 
@@ -127,7 +130,9 @@ def test_fuzz_csr(orc, seed):
     else:
         ref = orc.bicgstab(A, b, tol=1e-12, maxit=60, block=block)
     assert res.outcome == ref.outcome
-    noise_floor_parity(S if method == 0 else None, res, ref, xs, tag=f" csr[{seed}]")
+    rerun = lambda m: orc.pbicgstab(A, b, tol=1e-12, maxit=m, rr_period=rr, auto_rr=auto,
+                                    block=block, want_trace=True)
+    noise_floor_parity(S if method == 0 else None, res, ref, xs, tag=f" csr[{seed}]", rerun=rerun)
     S.close()
 
 
@@ -199,8 +204,10 @@ def test_fuzz_csr_loopback(orc, seed):
     else:
         ref = orc.bicgstab(A, b, tol=1e-12, maxit=60, block=block)
     assert res.outcome == ref.outcome
+    rerun = lambda m: orc.pbicgstab(A, b, tol=1e-12, maxit=m, rr_period=rr, block=block,
+                                    auto_rr=auto, want_trace=True)
     noise_floor_parity(G.ranks[0] if method == 0 else None, res, ref, xs,
-                       tag=f" csr_loopback[{seed}]")
+                       tag=f" csr_loopback[{seed}]", rerun=rerun)
     G.close()
 
 

@@ -98,7 +98,9 @@ def test_cfg1_icc0_three_solvers_500_iterations(orc):
             assert np.array_equal(res.rnorm, ref.rnorm) and np.array_equal(res.gap, ref.gap)
             assert np.array_equal(res.x.cpu().numpy(), ref.x)
             continue
-        noise_floor_parity(S, res, ref, xs, tag=f" cfg1 ICC(0) p-BiCGStab rr={rr}")
+        rerun = (lambda m, rr=rr: orc.pbicgstab(A, b, tol=0.0, maxit=m, bench=True, block="icc0",
+                                                rr_period=rr, want_trace=True))
+        noise_floor_parity(S, res, ref, xs, tag=f" cfg1 ICC(0) p-BiCGStab rr={rr}", rerun=rerun)
     S.close()
 
 
