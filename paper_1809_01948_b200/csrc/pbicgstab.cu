@@ -121,6 +121,7 @@ struct pbicg_ctx {
   pbicg_group* group = nullptr;
   // options
   int bench = 0, use_graphs = 1, timing = 0, overlap = 1, schedule = 0, gap_on = 0;
+  bool auto_split = false;  // schedule 0 picks the split schedule (NCCL ranks, small slabs)
   int method = M_PBICGSTAB;
   int auto_rr = 0;                           // option rr_auto
   double ar_nA = 0, ar_muN = 0, ar_mutN = 0;  // bound constants (reading A29)
@@ -632,9 +633,23 @@ void comm_reduce(const Members& G, bool on_side) {
   }
 }
 
+// Stencil schedule in force: 2 = the paper's split 4-phase schedule, else the fused
+// 2-sweep one.  schedule 0 (auto) picks split for NCCL ranks whose slab is small
+// enough that the two reductions the fused schedule can hide only behind a halo
+// exchange cost more than the split schedule's 8 extra passes (DESIGN.md section 2:
+// n_local < 2 t_red BW / 64 B = 3 M rows at t_red = 15 us, 6.5 TB/s -- a model, the
+// 1-GPU pool cannot measure it); never with the peer-memory transport (a few-us
+// reduction), block Jacobi, automated replacement or the comparison methods.
+bool split_sched(const pbicg_ctx* h) {
+  if (h->kind != KIND_STENCIL) return false;
+  if (h->schedule == 2) return true;
+  return h->schedule == 0 && h->auto_split && !h->p2p && h->method == M_PBICGSTAB &&
+         !h->auto_rr && h->tg.bj <= 1;
+}
+
 // the fused schedule's z / w halos travel inside the tile sweeps (transport 1)
 bool fused_halo(const pbicg_ctx* h) {
-  return h->p2p && h->kind == KIND_STENCIL && h->tile_ok && h->tile_on && h->schedule != 2;
+  return h->p2p && h->kind == KIND_STENCIL && h->tile_ok && h->tile_on && !split_sched(h);
 }
 
 // nearest-neighbour ghost exchange of halo_n rows per side for each vector
@@ -851,7 +866,7 @@ void enq_init(const Members& G) {
     each(G, PH_SPMVD);
   } else {
     if (dist) comm_halo(G, {SW0});  // w_0 is read with the stencil
-    if (h0->schedule == 2) each(G, PH_SPD);  // split schedule: t_0 stored
+    if (split_sched(h0)) each(G, PH_SPD);  // split schedule: t_0 stored
   }
   if (h0->gap_on) {
     each(G, PH_GAP);
@@ -875,7 +890,7 @@ void enq_iter(const Members& G, bool with_rr, int par) {
     enq_gap(G);
     return;
   }
-  if (h0->kind == KIND_STENCIL && h0->schedule == 2) {
+  if (split_sched(h0)) {
     // split 4-phase schedule (the paper's): each reduction hides behind the
     // halo exchange + stand-alone SpMV of the vector the next phase needs
     const bool ov = dist && h0->overlap;
@@ -1008,7 +1023,7 @@ bool persist_eligible(const Members& G) {
   const pbicg_ctx* h = G[0];
   return h->persist && h->persist_ok && G.size() == 1 && !h->dist && h->kind == KIND_STENCIL &&
          h->tile_ok && h->tile_on && h->method == M_PBICGSTAB && !h->auto_rr && !h->gap_on &&
-         h->schedule != 2 && !h->tg.pdl;
+         !split_sched(h) && !h->tg.pdl;
 }
 
 void launch_persist(pbicg_ctx* h, int L) {
@@ -1190,6 +1205,8 @@ void setup_tile(pbicg_ctx* h) {
   // full-line tiles need nx <= 2 TNT and (3D) a plane of TY >= 1 lines plus two halo
   // lines per staged vector in shared memory (3D: nx <= ~850 for the widest mode, sweep A)
   bool full = g.nx <= tpmax;
+  const char* force_seg = getenv("PBICG_TILE_SEG");  // tuning experiments only: x-segment width
+  if (force_seg && g.nx % 2 == 0) full = false;
   if (full) {
     int64_t TY = dim == 3 ? (tpmax / g.nx) : 1;
     if (TY > lines) TY = lines;
@@ -1211,6 +1228,10 @@ void setup_tile(pbicg_ctx* h) {
     if (g.nx % 2 != 0) return;
     const int64_t TYs = dim == 3 ? (lines < 2 ? lines : 2) : 1;
     int64_t SX = 512;
+    if (force_seg) {
+      const long v = strtol(force_seg, nullptr, 10);
+      if (v >= 64 && v <= 512 && v % 16 == 0) SX = v;
+    }
     for (; SX >= 64; SX -= 16) {
       t.TY = (int32_t)TYs;
       t.sx = (int32_t)SX;
@@ -1728,11 +1749,20 @@ pbicg_status build_stencil(pbicg_ctx* h, const pbicg_stencil* op, int bj) {
     cudaGetLastError();
   }
   setup_tile(h);
+  constexpr int64_t kSplitRows = 3000000;  // see split_sched
+  if (h->comm == COMM_NCCL && h->nranks > 1 && bj <= 1 && h->tile_ok && h->n_local < kSplitRows &&
+      !getenv("PBICG_NO_AUTO_SPLIT"))
+    h->auto_split = true;
   if (bj > 1 && (!h->tile_ok || h->tile_seg))
     return fail(h, PBICG_EINVAL,
                 "block Jacobi on a stencil needs full-line TMA tiles (2D: nx <= 1024, "
                 "3D: nx <= ~850)");
-  return alloc_common(h);
+  ST(alloc_common(h));
+  if (h->auto_split) {  // stored t, v of the split schedule
+    ST(gvec(h, &h->V.tv));
+    ST(gvec(h, &h->V.vv));
+  }
+  return PBICG_OK;
 }
 
 // ---------------------------- CSR construction --------------------------------
@@ -1835,6 +1865,30 @@ int prec_block(int prec) {
 // order (reading A29): ||A|| <= sqrt(||A||_1 ||A||_inf), row sums in stored
 // (ascending column) order, column sums in ascending row order -- the same
 // doubles as oracle.c orc_anorm_bound; mu = max row length; ||M^-1|| = max |1/a_jj|.
+// max over one rank's diagonal blocks of sqrt(||B^-1||_1 ||B^-1||_inf), row / column
+// sums in ascending order (oracle prec_norm_bound)
+double block_inv_norm_max(const pbicg_csr* op, int bj) {
+  std::vector<double> inv;
+  double mi = 0.0;
+  if (block_inverse(op, bj, &inv) != PBICG_OK) return 0.0;
+  for (int64_t k0 = 0; k0 < op->n_local; k0 += bj) {
+    double rm = 0.0, cm = 0.0;
+    for (int a = 0; a < bj; ++a) {
+      double rs = 0.0;
+      for (int c = 0; c < bj; ++c) rs = rs + std::fabs(inv[(size_t)(k0 + a) * bj + c]);
+      if (rs > rm) rm = rs;
+    }
+    for (int c = 0; c < bj; ++c) {
+      double cs = 0.0;
+      for (int a = 0; a < bj; ++a) cs = cs + std::fabs(inv[(size_t)(k0 + a) * bj + c]);
+      if (cs > cm) cm = cs;
+    }
+    const double nbk = std::sqrt(cm * rm);
+    if (nbk > mi) mi = nbk;
+  }
+  return mi;
+}
+
 void csr_bound_consts(const pbicg_csr* ops, int nops, int bj, double* nA, double* muN,
                       double* mutN) {
   const int64_t N = ops[0].n_global;
@@ -1859,24 +1913,9 @@ void csr_bound_consts(const pbicg_csr* ops, int nops, int bj, double* nA, double
   for (double c : col) cmax = c > cmax ? c : cmax;
   if (bj > 1) {  // ||M^-1|| <= max over blocks sqrt(||B^-1||_1 ||B^-1||_inf) (oracle prec_norm_bound)
     mi = 0.0;
-    std::vector<double> inv;
     for (int r = 0; r < nops; ++r) {
-      if (block_inverse(&ops[r], bj, &inv) != PBICG_OK) continue;
-      for (int64_t k0 = 0; k0 < ops[r].n_local; k0 += bj) {
-        double rm = 0.0, cm = 0.0;
-        for (int a = 0; a < bj; ++a) {
-          double rs = 0.0;
-          for (int c = 0; c < bj; ++c) rs = rs + std::fabs(inv[(size_t)(k0 + a) * bj + c]);
-          if (rs > rm) rm = rs;
-        }
-        for (int c = 0; c < bj; ++c) {
-          double cs = 0.0;
-          for (int a = 0; a < bj; ++a) cs = cs + std::fabs(inv[(size_t)(k0 + a) * bj + c]);
-          if (cs > cm) cm = cs;
-        }
-        const double nbk = std::sqrt(cm * rm);
-        if (nbk > mi) mi = nbk;
-      }
+      const double m = block_inv_norm_max(&ops[r], bj);
+      if (m > mi) mi = m;
     }
   }
   *nA = std::sqrt(cmax * rmax);
@@ -1885,6 +1924,62 @@ void csr_bound_consts(const pbicg_csr* ops, int nops, int bj, double* nA, double
 }
 
 pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* st);
+
+// The same constants computed rank by rank (multi-process CSR, reading A29): the
+// column sums are accumulated in ascending row order ACROSS ranks by passing a
+// window of partial column sums down the ranks -- rank r receives the sums of
+// ranks < r for columns [rb - H, rb + H) (the only columns ranks < r reach that r
+// reaches too; every rank holds >= H rows), adds its own rows, and hands
+// [re - H, re + H) to rank r + 1.  Column j's sum is final at the rank whose range
+// [rb - H, re - H) (the last rank: up to N) holds j, so the maximum over those
+// ranges, combined with the row-sum / mu / ||M^-1|| maxima by an exact max
+// all-reduce, is bitwise csr_bound_consts over all rows.  part = {max column sum,
+// max row sum, mu, ||M^-1|| bound} of this rank.
+void csr_bound_chain_step(const pbicg_csr* op, int bj, int64_t H, bool last,
+                          const double* win_in, double* win_out, double part[4]) {
+  const int64_t n = op->n_local, rb = op->row_begin;
+  std::vector<double> acc((size_t)(n + 2 * H), 0.0);  // columns [rb - H, rb + n + H)
+  if (win_in)
+    for (int64_t q = 0; q < 2 * H; ++q) acc[(size_t)q] = win_in[q];
+  double rmax = 0.0, mi = 0.0;
+  int64_t mu = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    double rs = 0.0;
+    const int64_t p0 = op->row_ptr[i], p1 = op->row_ptr[i + 1];
+    if (p1 - p0 > mu) mu = p1 - p0;
+    for (int64_t p = p0; p < p1; ++p) {
+      rs = rs + std::fabs(op->val[p]);
+      double& c = acc[(size_t)(op->col[p] - (rb - H))];
+      c = c + std::fabs(op->val[p]);
+      if (op->col[p] == rb + i && std::fabs(1.0 / op->val[p]) > mi) mi = std::fabs(1.0 / op->val[p]);
+    }
+    if (rs > rmax) rmax = rs;
+  }
+  if (bj > 1) mi = block_inv_norm_max(op, bj);  // ||M^-1|| over this rank's blocks
+  const int64_t fin = last ? n + H : n;  // final column range [rb - H, rb - H + fin)
+  double cmax = 0.0;
+  for (int64_t q = 0; q < fin; ++q) cmax = acc[(size_t)q] > cmax ? acc[(size_t)q] : cmax;
+  if (win_out)
+    for (int64_t q = 0; q < 2 * H; ++q) win_out[q] = acc[(size_t)(n + q)];
+  part[0] = cmax;
+  part[1] = rmax;
+  part[2] = (double)mu;
+  part[3] = mi;
+}
+
+void bound_consts_from_parts(const double* parts, int P, int64_t N, int bj, double* nA,
+                             double* muN, double* mutN) {
+  double c = 0, r = 0, mu = 0, mi = 0;
+  for (int q = 0; q < P; ++q) {
+    c = parts[4 * q] > c ? parts[4 * q] : c;
+    r = parts[4 * q + 1] > r ? parts[4 * q + 1] : r;
+    mu = parts[4 * q + 2] > mu ? parts[4 * q + 2] : mu;
+    mi = parts[4 * q + 3] > mi ? parts[4 * q + 3] : mi;
+  }
+  *nA = std::sqrt(c * r);
+  *muN = mu * std::sqrt((double)N);
+  *mutN = (double)bj * std::sqrt((double)N) * mi;
+}
 
 pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<double>& dinv,
                        int64_t width, bool uniform, int bj, int ilu = 0,
@@ -2451,6 +2546,38 @@ pbicg_status solve_members(const Members& G, const std::vector<SolveArgs>& io, d
   return PBICG_OK;
 }
 
+// NCCL ranks: the automated-replacement constants by the rank chain of
+// csr_bound_chain_step (window of partial column sums rank r -> r + 1 over the halo
+// communicator, then the exact all-gather of the four per-rank maxima)
+pbicg_status csr_bound_nccl(pbicg_ctx* h, const pbicg_csr* op, int bj) {
+  const int64_t H = h->H;
+  const int P = h->nranks, r = h->rank;
+  auto& api = nccl_api();
+  void *dwin = nullptr, *dparts = nullptr;
+  ST(dalloc(h, &dwin, (size_t)2 * H * sizeof(double)));
+  ST(dalloc(h, &dparts, (size_t)4 * P * sizeof(double)));
+  std::vector<double> win_in((size_t)2 * H), win_out((size_t)2 * H), parts((size_t)4 * P, 0.0);
+  if (r > 0) {
+    NC(api.Recv(dwin, (size_t)2 * H, ncclDouble, r - 1, h->nccl_halo, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+    CU(cudaMemcpy(win_in.data(), dwin, (size_t)2 * H * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  csr_bound_chain_step(op, bj, H, r == P - 1, r > 0 ? win_in.data() : nullptr,
+                       r + 1 < P ? win_out.data() : nullptr, &parts[(size_t)4 * r]);
+  if (r + 1 < P) {
+    ST(upload(h, dwin, win_out.data(), (size_t)2 * H * sizeof(double)));
+    NC(api.Send(dwin, (size_t)2 * H, ncclDouble, r + 1, h->nccl_halo, h->stream));
+    CU(cudaStreamSynchronize(h->stream));
+  }
+  ST(upload(h, dparts, parts.data(), parts.size() * sizeof(double)));  // zero but row r
+  NC(api.AllReduce(dparts, dparts, (size_t)4 * P, ncclDouble, ncclSum, h->nccl_halo, h->stream));
+  CU(cudaStreamSynchronize(h->stream));
+  CU(cudaMemcpy(parts.data(), dparts, parts.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  bound_consts_from_parts(parts.data(), P, op->n_global, bj, &h->ar_nA, &h->ar_muN, &h->ar_mutN);
+  h->ar_ok = true;
+  return PBICG_OK;
+}
+
 // 0: not an incomplete factorisation; 1: ILU(0); 2: ICC(0) (reading A34)
 int prec_ilu(int prec) {
   return prec == PBICG_PREC_ILU0 ? 1 : prec == PBICG_PREC_ICC0 ? 2 : 0;
@@ -2564,6 +2691,7 @@ pbicg_status pbicgstab_create_csr(const pbicg_csr* op, pbicg_prec prec, const pb
   pbicg_status st = common_setup(h, cuda_stream);
   if (!st && (nranks > 1 || (dist && dist->nccl_id_halo))) st = nccl_setup(h, dist);
   if (!st) st = build_csr(h, op, dinv, width, uniform, bj, ilu);
+  if (!st && h->comm == COMM_NCCL && nranks > 1 && !ilu) st = csr_bound_nccl(h, op, bj);
   if (!st && h->dist) {  // dinv ghosts, once (collective)
     comm_halo(Members{h}, {[](pbicg_ctx* c) { return c->dinv_g; }});
     cudaError_t e = cudaStreamSynchronize(h->stream);
@@ -2670,7 +2798,15 @@ pbicg_status pbicgstab_create_csr_loopback(const pbicg_csr* ops, pbicg_prec prec
   }
   if (!st) {
     double nA = 0, muN = 0, mutN = 0;
-    csr_bound_consts(ops, nranks, bj, &nA, &muN, &mutN);
+    // rank by rank, exactly as NCCL ranks do it (the window hand-over is a host copy)
+    const int64_t H = PBICG_CSR_HALO;
+    std::vector<double> parts((size_t)4 * nranks), win((size_t)2 * H), win2((size_t)2 * H);
+    for (int r = 0; r < nranks; ++r) {
+      csr_bound_chain_step(&ops[r], bj, H, r == nranks - 1, r > 0 ? win.data() : nullptr,
+                           r + 1 < nranks ? win2.data() : nullptr, &parts[(size_t)4 * r]);
+      win.swap(win2);
+    }
+    bound_consts_from_parts(parts.data(), nranks, ops[0].n_global, bj, &nA, &muN, &mutN);
     for (pbicg_ctx* m : grp->m) {
       m->ar_nA = nA;
       m->ar_muN = muN;
@@ -2756,8 +2892,8 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       if (value != 0 && (m->method != M_PBICGSTAB || !m->ar_ok ||
                          (m->kind == KIND_STENCIL && (!m->tile_ok || m->schedule == 2))))
         return fail(h, PBICG_EINVAL,
-                    "rr_auto needs method 0 and a stencil on the TMA tile kernels (not odd nx > 1024) or "
-                    "a CSR operator on one process (bound constants need every row)");
+                    "rr_auto needs method 0 and a stencil on the TMA tile kernels (not odd nx > 1024) "
+                    "or a CSR operator");
       m->auto_rr = value != 0;
       destroy_graphs(m);
     } else if (k == "method") {
@@ -2930,7 +3066,7 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
   std::string n(name);
   const double N = (double)h->n_local;
   double b = 0;
-  if (h->kind == KIND_STENCIL && h->schedule == 2) {
+  if (split_sched(h)) {
     // split schedule (SURVEY 8(a)'s 32 passes)
     if (n == "sweepA") b = 13 * 8 * N;       // read k,g,l,s,r,w,z,t,v; write g,s,l,z
     else if (n == "sweepC") b = 15 * 8 * N;  // read x,g,k,l,r,s,r^,w,z,t,v; write x,r,k,w

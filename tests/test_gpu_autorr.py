@@ -187,3 +187,31 @@ def test_auto_rr_fullsize_cfg3_first_iterations(S, orc):
     fr, rrl = solver.rr_info(res.iters)
     ref = orc.pbicgstab(A, b, tol=0.0, maxit=12, bench=True, auto_rr=True, gap=False)
     check_auto(res, fr, rrl, ref, xs)
+
+
+@pytest.mark.parametrize("block", [1, 2])
+def test_auto_rr_csr_loopback_band_chain(S, orc, block):
+    """Multi-rank CSR with rr_auto: the ||A|| bound's column sums are accumulated
+    rank by rank (window hand-over, csr_bound_chain_step -- the code NCCL ranks run),
+    with ranks of barely more than the halo so column sums span three ranks; the
+    constants, hence f^r and the decisions, must be the one-process oracle's bitwise."""
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    sizes = [4096 + 100, 4200, 4096 + 4]
+    n = sum(sizes)
+    M = problems.csr_band(n, nnz_row=9, band=4000, seed=12)
+    A = orc.csr(M.row_ptr, M.col, M.val)
+    cuts = np.concatenate([[0], np.cumsum(sizes)])
+    blocks = [(int(cuts[r]), M.row_ptr[cuts[r]:cuts[r + 1] + 1] - M.row_ptr[cuts[r]],
+               M.col[M.row_ptr[cuts[r]]:M.row_ptr[cuts[r + 1]]],
+               M.val[M.row_ptr[cuts[r]]:M.row_ptr[cuts[r + 1]]]) for r in range(3)]
+    G = LoopbackGroup.csr(blocks, n, block=block)
+    G.set_option("bench", 1)
+    G.set_option("rr_auto", 1)
+    xs = problems.x_star(n, 4)
+    b = orc.spmv(A, xs)
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=0.0, maxit=40, gap=True)
+    fr, rrl = G.ranks[0].rr_info(res.iters)
+    ref = orc.pbicgstab(A, b, tol=0.0, maxit=40, bench=True, auto_rr=True, block=block)
+    check_auto(res, fr, rrl, ref, xs)
+    G.close()
