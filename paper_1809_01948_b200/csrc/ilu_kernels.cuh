@@ -107,8 +107,26 @@ __device__ __forceinline__ void ilu_finish(unsigned int* ctr) {
   }
 }
 
+__device__ __forceinline__ void cp_async8(double* smem, const double* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+// dynamic shared memory of k_ilu_st: per thread, double-buffered, the ILU_K steps'
+// own operands (v or y, uinv), and for the tile-boundary threads the neighbouring
+// tile's values (a-side: threads ta = 0, indexed by tb; b-side: tb = 0, by ta; <= 32)
+#define ILU_BMAX 32
+constexpr size_t kIluSmem = sizeof(double) * (2 * ILU_K * 2 * ILU_T + 2 * 2 * ILU_K * 2 * ILU_BMAX);
+
 // Stencil ILU(0) sweep.  BWD = false: out := L^{-1} v; BWD = true: out := U^{-1} out
-// (in place; v unused).
+// (in place; v unused).  Operands are prefetched one block of ILU_K steps ahead
+// (own values by cp.async into shared memory; the neighbouring tiles' boundary values,
+// written during this kernel, by L2 loads into registers once that tile's progress
+// covers the next block, parked in shared memory at the end of the current block), so
+// a step costs shared-memory traffic, the row's arithmetic and one barrier.
 template <int DIM, bool BWD>
 __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
                                                   const double* __restrict__ v,
@@ -116,6 +134,10 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
   if (ilu_skip(sc, gate)) return;
   __shared__ double pub[2][2][ILU_T];  // [step parity][+a / +b consumer][thread]
   __shared__ int s_tile;
+  extern __shared__ __align__(16) double ilu_smem[];
+  double* pf = ilu_smem;                                   // [2][ILU_K][2][ILU_T]
+  double* pfa = ilu_smem + 2 * ILU_K * 2 * ILU_T;          // [2][ILU_K][2][ILU_BMAX]
+  double* pfb = pfa + 2 * ILU_K * 2 * ILU_BMAX;            // [2][ILU_K][2][ILU_BMAX]
   unsigned int* ctr = P.ctr + (BWD ? 4 : 0);
   unsigned long long* prog = BWD ? P.prog_b : P.prog_f;
   const unsigned long long ep = (unsigned long long)ilu_epoch(ctr) << 32;
@@ -142,6 +164,7 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
     const bool has_a = BWD ? (a + 1 < P.na) : (a > 0);
     const bool has_b = BWD ? (b + 1 < P.nb) : (b > 0);
     const bool own_a = ta > 0, own_b = tb > 0;  // neighbour line inside this tile
+    const bool bnd_a = valid && has_a && !own_a, bnd_b = valid && has_b && !own_b;
     // predecessor tiles (their progress gates the tile-boundary lines)
     const unsigned long long* pa = nullptr;
     const unsigned long long* pb = nullptr;
@@ -154,47 +177,111 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
     }
     const int64_t base = a * P.sa + b * P.sb;
     const int steps = (int)P.nx + na_t + nb_t - 2;
-    double prev = 0.0, uprev = 0.0;  // own value (and forward: its uinv) at x -/+ 1
-    for (int s0 = 0; s0 < steps; s0 += ILU_K) {
-      const int s1 = (s0 + ILU_K) < steps ? (s0 + ILU_K) : steps;
+    const int da = BWD ? (int)P.sa : -(int)P.sa;  // offset of the a / b dependency
+    const int64_t db = BWD ? P.sb : -P.sb;
+    auto row_of = [&](int s, int64_t& i) -> bool {  // row of step s; false if idle
+      const int xs = s - ta - tb;
+      if (!valid || xs < 0 || xs >= P.nx) return false;
+      i = base + (BWD ? P.nx - 1 - xs : xs);
+      return true;
+    };
+    auto wait_pred = [&](int upto) {  // predecessors' x-count >= min(nx, upto)
       if (tid == 0) {
         const unsigned long long need =
-            ep | (unsigned long long)((int64_t)s1 < P.nx ? s1 : P.nx);
+            ep | (unsigned long long)((int64_t)upto < P.nx ? upto : P.nx);
         if (pa) while (ld_acq_gpu(pa) < need) __nanosleep(20);
         if (pb) while (ld_acq_gpu(pb) < need) __nanosleep(20);
       }
       __syncthreads();
-      for (int s = s0; s < s1; ++s) {
-        const int xs = s - ta - tb;  // steps into this line
-        if (valid && xs >= 0 && xs < P.nx) {
-          const int64_t x = BWD ? P.nx - 1 - xs : xs;
-          const int64_t i = base + x;
+    };
+    // own operands of block [sb, sb + ILU_K) into buffer q (asynchronous copies)
+    auto fetch_own = [&](int sb, int q) {
+      for (int k = 0; k < ILU_K; ++k) {
+        int64_t i;
+        if (!row_of(sb + k, i)) continue;
+        double* d = pf + ((size_t)(q * ILU_K + k) * 2) * ILU_T + tid;
+        cp_async8(d, BWD ? out + i : v + i);
+        cp_async8(d + ILU_T, P.uinv + i);
+        if (!BWD) {  // the neighbours' pivots (static) ride along
+          if (bnd_a) cp_async8(pfa + ((size_t)(q * ILU_K + k) * 2 + 1) * ILU_BMAX + tb, P.uinv + i + da);
+          if (bnd_b) cp_async8(pfb + ((size_t)(q * ILU_K + k) * 2 + 1) * ILU_BMAX + ta, P.uinv + i + db);
+        }
+      }
+      cp_async_commit();
+    };
+    // the neighbouring tiles' values of block [sb, sb + ILU_K) (written in this kernel:
+    // L2 loads) -> registers; parked in buffer q by park_bnd
+    double ya[ILU_K], yb[ILU_K];
+    auto load_bnd = [&](int sb) {
+#pragma unroll
+      for (int k = 0; k < ILU_K; ++k) {
+        int64_t i;
+        ya[k] = yb[k] = 0.0;
+        if (!row_of(sb + k, i)) continue;
+        if (bnd_a) ya[k] = __ldcg(out + i + da);
+        if (bnd_b) yb[k] = __ldcg(out + i + db);
+      }
+    };
+    auto park_bnd = [&](int q) {
+#pragma unroll
+      for (int k = 0; k < ILU_K; ++k) {
+        if (bnd_a) pfa[((size_t)(q * ILU_K + k) * 2) * ILU_BMAX + tb] = ya[k];
+        if (bnd_b) pfb[((size_t)(q * ILU_K + k) * 2) * ILU_BMAX + ta] = yb[k];
+      }
+    };
+    double prev = 0.0, uprev = 0.0;  // own value (and forward: its uinv) at x -/+ 1
+    // prologue: block 0's operands
+    wait_pred(ILU_K);
+    fetch_own(0, 0);
+    load_bnd(0);
+    park_bnd(0);
+    int cur = 0;
+    for (int s0 = 0; s0 < steps; s0 += ILU_K) {
+      const int s1 = (s0 + ILU_K) < steps ? (s0 + ILU_K) : steps;
+      const bool more = s1 < steps;
+      if (more) {  // next block: predecessors far enough, then prefetch
+        wait_pred(s1 + ILU_K);
+        fetch_own(s1, cur ^ 1);
+        load_bnd(s1);
+      } else {
+        cp_async_commit();  // (empty group: keeps wait_group 1 meaningful)
+      }
+      cp_async_wait1();  // this block's own copies (this thread's) have landed
+      __syncthreads();   // ... and the parked boundary values of the previous block
+      for (int k = 0; k < ILU_K; ++k) {
+        const int s = s0 + k;
+        if (s >= s1) break;  // uniform
+        int64_t i;
+        if (row_of(s, i)) {
+          const int xs = s - ta - tb;
           const int q = (s - 1) & 1;
+          const double* d = pf + ((size_t)(cur * ILU_K + k) * 2) * ILU_T + tid;
+          const size_t ob = ((size_t)(cur * ILU_K + k) * 2) * ILU_BMAX;
           // ascending column order: forward -b, -a, -x; backward +x, +a, +b
-          double acc = BWD ? __ldcg(out + i) : __ldg(v + i);
+          double acc = d[0];
+          const double ui = d[ILU_T];
           if (!BWD) {
             if (has_b) {
               const double term = own_b ? pub[q][1][tid - P.TA]
-                                        : (cb * __ldg(P.uinv + i - P.sb)) * __ldcg(out + i - P.sb);
+                                        : (cb * pfb[ob + ILU_BMAX + ta]) * pfb[ob + ta];
               acc = acc - term;
             }
             if (has_a) {
               const double term = own_a ? pub[q][0][tid - 1]
-                                        : (ca * __ldg(P.uinv + i - P.sa)) * __ldcg(out + i - P.sa);
+                                        : (ca * pfa[ob + ILU_BMAX + tb]) * pfa[ob + tb];
               acc = acc - term;
             }
             if (xs > 0) acc = acc - (cx * uprev) * prev;
             out[i] = acc;
-            const double ui = __ldg(P.uinv + i);
             pub[s & 1][0][tid] = (ca * ui) * acc;  // the +a neighbour's -a term
             pub[s & 1][1][tid] = (cb * ui) * acc;  // the +b neighbour's -b term
             prev = acc;
             uprev = ui;
           } else {
             if (xs > 0) acc = acc - cx * prev;
-            if (has_a) acc = acc - (own_a ? pub[q][0][tid - 1] : ca * __ldcg(out + i + P.sa));
-            if (has_b) acc = acc - (own_b ? pub[q][1][tid - P.TA] : cb * __ldcg(out + i + P.sb));
-            const double xi = acc * __ldg(P.uinv + i);
+            if (has_a) acc = acc - (own_a ? pub[q][0][tid - 1] : ca * pfa[ob + tb]);
+            if (has_b) acc = acc - (own_b ? pub[q][1][tid - P.TA] : cb * pfb[ob + ta]);
+            const double xi = acc * ui;
             out[i] = xi;
             pub[s & 1][0][tid] = ca * xi;
             pub[s & 1][1][tid] = cb * xi;
@@ -203,6 +290,7 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
         }
         __syncthreads();
       }
+      if (more) park_bnd(cur ^ 1);  // the next block's boundary loads have landed by now
       if (tid == 0) {  // x-count every line of the tile has finished after step s1 - 1
         int64_t done = (int64_t)s1 - (na_t - 1) - (nb_t - 1);
         if (done < 0) done = 0;
@@ -210,7 +298,199 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
         __threadfence();
         st_rel_gpu(prog + tile, ep | (unsigned long long)done);
       }
+      cur ^= 1;
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  }
+  ilu_finish(ctr);
+}
+
+// 2D stencils: warp-decoupled line wavefront (k_ilu_2d).  A tile is 32 x I2_W
+// consecutive lines (y); warp w owns 32 of them, lane l one line, and at its local
+// step sigma lane l handles xs = sigma - l, so the -y (+y) term of lane l is lane
+// l - 1's previous-step result, one shuffle away.  Lane 0 takes it from warp w - 1's
+// lane 31 -- published into a shared-memory ring edge[w - 1] and handed over once
+// per block of I2_K steps (counter ecnt; econs gives the ring back-pressure) -- or,
+// for w = 0, from the previous tile (global memory after its progress flag).  No
+// CTA barrier per step; warps lag their predecessor by about 40 steps.  Own operands
+// are prefetched a block ahead into registers; steps are branch-free (selects,
+// predicated stores), and the warp is reconverged after the hand-over spins: a warp
+// left diverged takes the slow path of every shuffle (measured 5x slower per step).
+#define I2_W 8     // warps per CTA
+#define I2_K 8     // steps per prefetch block (and per edge hand-over)
+#define I2_R 128   // edge ring slots per warp
+
+__device__ __forceinline__ void st_global_pred(double* p, double v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}" ::"l"(p),
+      "d"(v), "r"((int)pred)
+      : "memory");
+}
+
+__device__ __forceinline__ double ld_vol_shared(const double* p) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];"
+               : "=d"(v)
+               : "r"((uint32_t)__cvta_generic_to_shared((const void*)p))
+               : "memory");
+  return v;
+}
+
+template <bool BWD>
+__global__ void __launch_bounds__(32 * I2_W) k_ilu_2d(IluOp P, Scal* __restrict__ sc, int gate,
+                                                      const double* __restrict__ v,
+                                                      double* __restrict__ out) {
+  if (ilu_skip(sc, gate)) return;
+  // warp w's lane 31 publishes its per-step results (the -y / +y term of warp w + 1's
+  // lane 0) into edge[w] and, once per block, the x-count in ecnt[w]; warp w + 1 reads
+  // a whole block of them at its block start (econs = what it has consumed)
+  __shared__ double edge[I2_W][I2_R];
+  __shared__ volatile int ecnt[I2_W], econs[I2_W];
+  __shared__ int s_tile;
+  unsigned int* ctr = P.ctr + (BWD ? 4 : 0);
+  unsigned long long* prog = BWD ? P.prog_b : P.prog_f;
+  const unsigned long long ep = (unsigned long long)ilu_epoch(ctr) << 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const double ca = BWD ? P.cap : P.cam, cx = BWD ? P.cxp : P.cxm;
+  const int nx = (int)P.nx;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = (int)atomicAdd(ctr, 1u);
+    if (threadIdx.x < I2_W) {
+      ecnt[threadIdx.x] = 0;
+      econs[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    const int t = s_tile;
+    if (t >= P.ntiles) break;
+    const int A = P.order[BWD ? P.ntiles - 1 - t : t];
+    const int64_t a0 = (int64_t)A * P.TA;
+    const int na_t = (int)((P.na - a0) < P.TA ? (P.na - a0) : P.TA);
+    const int ta = 32 * w + lane;
+    const bool valid = ta < na_t;
+    const int64_t a = a0 + (BWD ? na_t - 1 - ta : ta);
+    const bool has_a = BWD ? (a + 1 < P.na) : (a > 0);
+    const int64_t base = a * P.sa;
+    const int64_t da = BWD ? P.sa : -P.sa;
+    const int nvw = (na_t + 31) / 32;  // warps with lines
+    if (w < nvw) {
+      const int lmax = (na_t - 32 * w) < 32 ? (na_t - 32 * w - 1) : 31;  // last valid lane
+      const int wsteps = nx + lmax;
+      const bool glob = w == 0 && lane == 0 && has_a;   // dependency from the previous tile
+      const bool fring = w > 0 && lane == 0 && has_a;   // ... from warp w - 1
+      const bool tring = lane == 31 && w + 1 < nvw;     // lane 31 feeds warp w + 1
+      const bool last = ta == na_t - 1;                 // the tile's last line
+      const bool succ = BWD ? A > 0 : A + 1 < P.nta;    // ... is read by the next tile
+      const unsigned long long* pa = nullptr;
+      if (glob) pa = prog + (BWD ? A + 1 : A - 1);
+      // own operands of steps [sg0, sg0 + I2_K): registers, one block ahead
+      auto fetch = [&](int sg0, double (&o0)[I2_K], double (&o1)[I2_K]) {
+#pragma unroll
+        for (int k = 0; k < I2_K; ++k) {
+          const int xs = sg0 + k - lane;
+          const bool ok = valid && xs >= 0 && xs < nx;
+          const int64_t i = base + (BWD ? nx - 1 - xs : xs);
+          o0[k] = ok ? (BWD ? __ldcg(out + i) : __ldg(v + i)) : 0.0;
+          o1[k] = ok ? __ldg(P.uinv + i) : 0.0;
+        }
+      };
+      double up0[I2_K];  // lane 0: the -y / +y term of its block (other warp / other tile)
+      auto fetch_up = [&](int sg0) {
+#pragma unroll
+        for (int k = 0; k < I2_K; ++k) up0[k] = 0.0;
+        if (fring) {
+          const int need = (sg0 + I2_K) < nx ? (sg0 + I2_K) : nx;
+          while (ecnt[w - 1] < need) {
+          }
+#pragma unroll
+          for (int k = 0; k < I2_K; ++k)
+            if (sg0 + k < nx) up0[k] = ld_vol_shared(&edge[w - 1][(sg0 + k) & (I2_R - 1)]);
+          econs[w] = sg0 + I2_K;
+        } else if (glob) {
+          const unsigned long long need =
+              ep | (unsigned long long)((sg0 + I2_K) < nx ? (sg0 + I2_K) : nx);
+          while (ld_acq_gpu(pa) < need) __nanosleep(20);
+#pragma unroll
+          for (int k = 0; k < I2_K; ++k) {
+            const int xs = sg0 + k;
+            if (xs < nx) {
+              const int64_t i = base + (BWD ? nx - 1 - xs : xs);
+              up0[k] = BWD ? ca * __ldcg(out + i + da)
+                           : (ca * __ldg(P.uinv + i + da)) * __ldcg(out + i + da);
+            }
+          }
+        }
+      };
+      double c0[I2_K], c1[I2_K], n0[I2_K], n1[I2_K];
+      fetch(0, c0, c1);
+      double prev = 0.0, uprev = 0.0, pubprev = 0.0;
+      for (int sg0 = 0; sg0 < wsteps; sg0 += I2_K) {
+        const bool more = sg0 + I2_K < wsteps;
+        if (more) fetch(sg0 + I2_K, n0, n1);
+        if (tring) {  // ring back-pressure: warp w + 1 has consumed x < sg0 + I2_K - 31 - I2_R
+          while (econs[w + 1] < sg0 + I2_K - 31 - I2_R) {
+          }
+        }
+        fetch_up(sg0);
+        // reconverge after lane 0's / lane 31's spins: a warp left diverged would take
+        // the slow (WARPSYNC) path of every shuffle in the step loop (measured 5x slower)
+        __syncwarp();
+        // branch-free steps: every lane computes, selects keep the inactive ones inert
+#pragma unroll
+        for (int k = 0; k < I2_K; ++k) {
+          const int sg = sg0 + k;
+          const int xs = sg - lane;
+          const bool act = valid && xs >= 0 && xs < nx;
+          const double sh = __shfl_up_sync(0xffffffffu, pubprev, 1);  // lane l-1, step sg-1
+          const double up = lane == 0 ? up0[k] : sh;
+          double res, pub;
+          if (!BWD) {  // -y, -x (ascending column order)
+            double acc = c0[k];
+            const double t1 = acc - up;
+            acc = has_a ? t1 : acc;
+            const double t2 = acc - (cx * uprev) * prev;
+            acc = xs > 0 ? t2 : acc;
+            res = acc;
+            const double ui = c1[k];
+            pub = (ca * ui) * acc;  // the +y neighbour's -y term
+            prev = act ? acc : prev;
+            uprev = act ? ui : uprev;
+          } else {  // +x, +y
+            double acc = c0[k];
+            const double t1 = acc - cx * prev;
+            acc = xs > 0 ? t1 : acc;
+            const double t2 = acc - up;
+            acc = has_a ? t2 : acc;
+            res = acc * c1[k];
+            pub = ca * res;
+            prev = act ? res : prev;
+          }
+          {  // predicated store, no branch: the address is clamped for idle lanes
+            const int xc = xs < 0 ? 0 : (xs >= nx ? nx - 1 : xs);
+            st_global_pred(out + base + (BWD ? nx - 1 - xc : xc), res, act);
+          }
+          if (tring && act) edge[w][xs & (I2_R - 1)] = pub;
+          pubprev = act ? pub : 0.0;
+        }
+        if (tring) {  // lane 31's x-count after this block
+          __threadfence_block();
+          const int done = sg0 + I2_K - 31;
+          ecnt[w] = done < nx ? done : nx;
+        }
+        if (last && succ) {  // the successor tile reads only this line, stored by this
+          int done = sg0 + I2_K - lane;  // thread: its release store alone orders it
+          if (done > nx) done = nx;
+          if (done > 0) st_rel_gpu(prog + A, ep | (unsigned long long)done);
+        }
+        if (more) {
+#pragma unroll
+          for (int k = 0; k < I2_K; ++k) {
+            c0[k] = n0[k];
+            c1[k] = n1[k];
+          }
+        }
+      }
+    }
+    __syncthreads();
   }
   ilu_finish(ctr);
 }

@@ -559,11 +559,11 @@ void launch_ilu(pbicg_ctx* h, const double* in, double* out, int gate) {
   const IluOp& P = h->ilu_op;
   if (h->ilu_st) {
     if (P.dim == 3) {
-      k_ilu_st<3, false><<<h->ilu_grid, ILU_T, 0, h->stream>>>(P, h->scal, gate, in, out);
-      k_ilu_st<3, true><<<h->ilu_grid, ILU_T, 0, h->stream>>>(P, h->scal, gate, in, out);
+      k_ilu_st<3, false><<<h->ilu_grid, ILU_T, kIluSmem, h->stream>>>(P, h->scal, gate, in, out);
+      k_ilu_st<3, true><<<h->ilu_grid, ILU_T, kIluSmem, h->stream>>>(P, h->scal, gate, in, out);
     } else {
-      k_ilu_st<2, false><<<h->ilu_grid, ILU_T, 0, h->stream>>>(P, h->scal, gate, in, out);
-      k_ilu_st<2, true><<<h->ilu_grid, ILU_T, 0, h->stream>>>(P, h->scal, gate, in, out);
+      k_ilu_2d<false><<<h->ilu_grid, 32 * I2_W, 0, h->stream>>>(P, h->scal, gate, in, out);
+      k_ilu_2d<true><<<h->ilu_grid, 32 * I2_W, 0, h->stream>>>(P, h->scal, gate, in, out);
     }
   } else {
     k_ilu_csr<false><<<h->ilu_grid, 256, 0, h->stream>>>(P, h->scal, gate, in, out);
@@ -2238,7 +2238,8 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
       P.cbm = st->coef[5];
       P.cbp = st->coef[6];
       P.TA = (int32_t)(st->ny < 16 ? st->ny : 16);
-      const int64_t tb = ILU_T / P.TA;
+      int64_t tb = ILU_T / P.TA;
+      if (tb > ILU_BMAX) tb = ILU_BMAX;  // boundary-value slots per side
       P.TB = (int32_t)(g.nol < tb ? g.nol : tb);
     } else {
       P.na = g.nol;
@@ -2246,7 +2247,7 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
       P.sa = st->nx;
       P.sb = 0;
       P.cbm = P.cbp = 0.0;
-      P.TA = (int32_t)(g.nol < ILU_T ? g.nol : ILU_T);
+      P.TA = 32 * I2_W;  // k_ilu_2d: I2_W warps of 32 lines
       P.TB = 1;
     }
     P.nta = (int32_t)((P.na + P.TA - 1) / P.TA);
@@ -2269,8 +2270,16 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
     P.order = (const int32_t*)po;
     P.prog_f = (unsigned long long*)pf;
     P.prog_b = (unsigned long long*)pb;
+    const auto SMA = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    CU(cudaFuncSetAttribute(k_ilu_st<3, false>, SMA, (int)kIluSmem));
+    CU(cudaFuncSetAttribute(k_ilu_st<3, true>, SMA, (int)kIluSmem));
+    CU(cudaFuncSetAttribute(k_ilu_st<2, false>, SMA, (int)kIluSmem));
+    CU(cudaFuncSetAttribute(k_ilu_st<2, true>, SMA, (int)kIluSmem));
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_st<3, false>, ILU_T, 0);
+    if (P.dim == 3)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_st<3, false>, ILU_T, kIluSmem);
+    else
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_2d<false>, 32 * I2_W, 0);
     const int64_t cap = (int64_t)(occ < 1 ? 1 : occ) * h->num_sm;
     h->ilu_grid = (int)(P.ntiles < cap ? P.ntiles : cap);
     return PBICG_OK;
