@@ -491,7 +491,7 @@ def run_loopback(args):
     return 0
 
 
-def relaunch_under_torchrun(n: int) -> int:
+def relaunch_under_torchrun(n: int, need_gpus: bool = True) -> int:
     """`bench.py --gpus N` started without torchrun: re-exec this command as N ranks
     (one process per GPU, NCCL over NVLink) exactly as the driver launches it;
     rank 0 prints the JSON line.  NCCL's own log level is left to the caller."""
@@ -501,7 +501,7 @@ def relaunch_under_torchrun(n: int) -> int:
         have = torch.cuda.device_count()
     except Exception:
         have = 0
-    if have < n:
+    if need_gpus and have < n:
         print(f"bench.py: --gpus {n} needs {n} visible GPUs, found {have}", file=sys.stderr)
         return 2
     s = socket.socket()
@@ -554,7 +554,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        return relaunch_under_torchrun(args.gpus)
+        return relaunch_under_torchrun(args.gpus, need_gpus=args.impl == "ours")
     if args.gpus != world:
         print(f"note: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
     if args.impl == "reference":

@@ -107,3 +107,26 @@ def test_reference_arm_under_torchrun_two_ranks():
     import json
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["cores"] == 1
+
+
+def test_bench_relaunches_itself_under_torchrun():
+    """`bench.py --gpus 2` started WITHOUT torchrun relaunches itself as 2 ranks
+    (torch.distributed.run, 127.0.0.1); the reference arm needs no GPU, so on this CPU
+    box the relaunched job runs and rank 0 prints the one JSON line with n_gpus 2; the
+    GPU arm refuses cleanly when fewer GPUs are visible than requested."""
+    import json
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+           "--steps", "1", "--warmup", "0", "--config", "cfg3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["n_gpus"] == 2
+    import torch
+    if torch.cuda.device_count() < 2:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2"],
+                           capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+        assert r.returncode == 2 and "needs 2 visible GPUs" in r.stderr
