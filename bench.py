@@ -233,14 +233,40 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * statistics.median(secs),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": n_full,
-                                            "maxit": maxit, "rr_period": rr},
+            "data": "synthetic", "config": bench_config(args, cfg, st, maxit, rr, world),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": sample, "cpu": cpu_model(),
                              "pinning": "sched_setaffinity to one core (taskset -c)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def bench_config(args, cfg, st, maxit, rr, world):
+    """The workload description both arms print (identical config => comparable lines)."""
+    n = st.n // world  # rows per rank
+    return {"workload": f"{cfg.name}: {cfg.desc}", "n": st.n,
+            "grid": [st.nx, st.ny, st.nz] if st.dim else "csr 27 nnz/row, band 4096",
+            "maxit_per_step": maxit, "rr_period": rr, "gap_tracking": bool(args.gap),
+            "rr_auto": bool(args.rr_auto),
+            "preconditioner": ("jacobi" if args.block == 1 else args.block.upper()
+                               if isinstance(args.block, str) else f"block-jacobi {args.block}"),
+            "method": args.method,
+            "schedule": (("split 4-phase (stencil), stand-alone TMA SpMVs the reductions "
+                          "hide behind" if args.schedule == 2 else SCHEDULES[args.method])
+                         if st.dim else "split 4-phase (CSR as ELL), reduction #1 overlapped"),
+            "l2": ("inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9)
+                   if 14 * 8 * n > 4 * 126e6 else
+                   "working set %.0f MB, about the 126 MB L2: not flushed (this "
+                   "config is L2-resident by construction)" % (14 * 8 * n / 1e6)),
+            "timed_region": ("CUDA events around every kernel on the solver stream "
+                             "(graphs off: per-kernel durations for the roofline); "
+                             "e2e runs with CUDA graphs" if args.kernel_timing else
+                             "CUDA graphs, no per-kernel events"),
+            "parallelism": (f"z-slab x{world}" if st.dim else f"row-block x{world}") +
+                           (" (NCCL halo + rank-row all-gather)" if world > 1 else ""),
+            "overlap": bool(args.overlap) if world > 1 else None,
+            "transport": (["nccl", "peer-memory"][args.transport] if world > 1 else None)}
 
 
 def method_coef(args, st):
@@ -407,31 +433,8 @@ def run_ours(args, rank, world):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded x* ~ U[-1,1], b = A x* on device)",
-        "config": {"workload": f"{cfg.name}: {cfg.desc}", "n": st.n,
-                   "grid": [st.nx, st.ny, st.nz] if st.dim else "csr 27 nnz/row, band 4096",
-                   "maxit_per_step": maxit, "rr_period": rr, "gap_tracking": gap,
-                   "rr_auto": bool(args.rr_auto),
-                   **({"breakdown_at": breakdown_at} if breakdown_at else {}),
-                   "preconditioner": ("jacobi" if args.block == 1 else args.block.upper()
-                                      if isinstance(args.block, str) else
-                                      f"block-jacobi {args.block}"),
-                   "method": args.method,
-                   "schedule": (("split 4-phase (stencil), stand-alone TMA SpMVs the reductions "
-                                 "hide behind" if args.schedule == 2 else SCHEDULES[args.method])
-                                if st.dim else
-                                "split 4-phase (CSR as ELL), reduction #1 overlapped"),
-                   "l2": ("inputs larger than L2 (%.1f GB per GPU)" % (14 * 8 * n / 1e9)
-                          if 14 * 8 * n > 4 * 126e6 else
-                          "working set %.0f MB, about the 126 MB L2: not flushed (this "
-                          "config is L2-resident by construction)" % (14 * 8 * n / 1e6)),
-                   "timed_region": ("CUDA events around every kernel on the solver stream "
-                                    "(graphs off: per-kernel durations for the roofline); "
-                                    "e2e runs with CUDA graphs" if args.kernel_timing else
-                                    "CUDA graphs, no per-kernel events"),
-                   "parallelism": f"z-slab x{world}" + (" (NCCL halo + rank-row all-gather)"
-                                                        if world > 1 else ""),
-                   "overlap": bool(args.overlap) if world > 1 else None,
-                   "transport": (["nccl", "peer-memory"][args.transport] if world > 1 else None)},
+        "config": {**bench_config(args, cfg, st, maxit, rr, world),
+                   **({"breakdown_at": breakdown_at} if breakdown_at else {})},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
