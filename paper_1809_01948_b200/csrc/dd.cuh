@@ -58,24 +58,76 @@ __device__ __forceinline__ Dd dd_warp_reduce(Dd a) {
   return a;
 }
 
+template <int K> struct Pow2 { enum { v = K <= 1 ? 1 : K <= 2 ? 2 : K <= 4 ? 4 : K <= 8 ? 8 : 16 }; };
+template <int P> struct Log2 { enum { v = P <= 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : 4 }; };
+
+__device__ __forceinline__ Dd dd_shfl_xor(Dd a, int m) {
+  Dd b;
+  b.hi = __shfl_xor_sync(0xffffffffu, a.hi, m);
+  b.lo = __shfl_xor_sync(0xffffffffu, a.lo, m);
+  return b;
+}
+
+// K values per lane reduced over the warp by transposition: at the first log2(P)
+// levels (P = K rounded up to a power of two) each lane keeps half of its values and
+// trades the other half with its partner, so one shuffle-and-add serves two values
+// (9 combines per lane for K = 5 instead of 25); the remaining levels are a
+// butterfly.  Lane l ends with the total of value l >> (5 - log2 P).  Every value is
+// combined over exactly the pairs (i, i + off), off = 16, 8, ..., 1, of
+// dd_warp_reduce's tree, and (+) is commutative bitwise, so the totals are that
+// tree's bits.
+template <int K>
+__device__ __forceinline__ Dd dd_warp_reduce_multi(const Dd (&a)[K]) {
+  constexpr int P = Pow2<K>::v, LP = Log2<P>::v;
+  static_assert(K <= 16, "at most 16 values");
+  Dd v[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) v[j] = j < K ? a[j] : dd_zero();
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int o = 16 >> t;
+    if (t < LP) {
+      const int half = P >> (t + 1);
+      const bool up = (lane & o) != 0;
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const Dd send = up ? v[j] : v[j + half];
+        const Dd keep = up ? v[j + half] : v[j];
+        v[j] = dd_add(keep, dd_shfl_xor(send, o));
+      }
+    } else {
+      v[0] = dd_add(v[0], dd_shfl_xor(v[0], o));
+    }
+  }
+  return v[0];
+}
+
 // Block reduction of K partials; thread 0 returns the totals.  blockDim.x must
-// be a multiple of 32 and <= 1024.  Ends with a __syncthreads().
+// be a multiple of 32 and <= 1024.  Ends with a __syncthreads().  Per value the
+// tree is a warp tree (dd_warp_reduce's pairs) over the lanes, then one over the
+// warps' totals (zeros past the last warp).
 template <int K>
 __device__ __forceinline__ void dd_block_reduce(Dd (&acc)[K]) {
+  constexpr int S = 5 - Log2<Pow2<K>::v>::v;  // lane l holds value l >> S
   __shared__ Dd sh[K][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = blockDim.x >> 5;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    Dd v = dd_warp_reduce(acc[k]);
-    if (lane == 0) sh[k][warp] = v;
+  {
+    const Dd t = dd_warp_reduce_multi<K>(acc);
+    const int k = lane >> S;
+    if ((lane & ((1 << S) - 1)) == 0 && k < K) sh[k][warp] = t;
   }
   __syncthreads();
   if (warp == 0) {
+    Dd v[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = lane < nwarps ? sh[k][lane] : dd_zero();
+    const Dd t = dd_warp_reduce_multi<K>(v);
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      Dd v = lane < nwarps ? sh[k][lane] : dd_zero();
-      acc[k] = dd_warp_reduce(v);
+      acc[k].hi = __shfl_sync(0xffffffffu, t.hi, k << S);
+      acc[k].lo = __shfl_sync(0xffffffffu, t.lo, k << S);
     }
   }
   __syncthreads();

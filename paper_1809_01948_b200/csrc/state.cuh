@@ -83,6 +83,26 @@ struct Hist {
                   // (the oracle's sc_trace layout; parity diagnostics)
 };
 
+// The scalar state the end-of-iteration bookkeeping reads (fin_step F_SWEEPA /
+// F_SWEEPC / F_RR2), loaded in one batch of independent loads.  Every field is
+// written only by the scalar-forming step of an earlier kernel, so a copy taken
+// after a kernel's PDL wait is the state its own publish starts from; the tile
+// sweeps take it in their prologue (off the critical path) and the last CTA's
+// bookkeeping then issues only stores -- no chain of dependent global-memory
+// round trips behind the grid reduction (scripts/timeline.py: C's publish 1.5-3.2 us).
+struct Snap {
+  double alpha, beta, omega, rho, sqrt_eps, h0, tol_abs;
+  int32_t iter, bench, auto_rr, rr_next, rr_period, rr_off, n_rr, dist, p2p;
+};
+
+__device__ __forceinline__ void snap_load(Snap& p, const Scal* s) {
+  p.alpha = s->alpha; p.beta = s->beta; p.omega = s->omega; p.rho = s->rho;
+  p.sqrt_eps = s->sqrt_eps; p.h0 = s->h0; p.tol_abs = s->tol_abs;
+  p.iter = s->iter; p.bench = s->bench; p.auto_rr = s->auto_rr; p.rr_next = s->rr_next;
+  p.rr_period = s->rr_period; p.rr_off = s->rr_off; p.n_rr = s->n_rr;
+  p.dist = s->dist; p.p2p = s->p2p;
+}
+
 // ---------------------------------------------------------------------------
 // Automated replacement bookkeeping, one thread, same formulas and
 // operation order as oracle.c; the norms are the kernels' Dot2 sums of squares
@@ -151,9 +171,10 @@ __device__ __forceinline__ void auto_reset(Scal* s, Hist h, double R1, double nZ
 // Line 21-26 bookkeeping once the five dots of reduction #2 are
 // known: history, sqrt(eps) latch (A12), stop test (A7), beta_{i+1},
 // alpha_{i+1} (left to right as printed, A4), breakdown (A9).
-__device__ __forceinline__ void finalize_iteration(Scal* s, Hist h, double rho1, double dw,
-                                                   double ds, double dz, double rr) {
-  const int i = s->iter;
+// p: the state before this step (Snap).
+__device__ __forceinline__ void finalize_iteration(Scal* s, Hist h, const Snap& p, double rho1,
+                                                   double dw, double ds, double dz, double rr) {
+  const int i = p.iter;
   const double hn = sqrt(rr);
   h.rnorm[i + 1] = hn;
   {
@@ -164,14 +185,14 @@ __device__ __forceinline__ void finalize_iteration(Scal* s, Hist h, double rho1,
   }
   s->iters = i + 1;
   s->iter = i + 1;
-  if (hn < s->sqrt_eps * s->h0) s->rr_off = 1;
+  if (hn < p.sqrt_eps * p.h0) s->rr_off = 1;
   s->rr_fire = 0;
-  if (hn <= s->tol_abs && !s->bench) {
+  if (hn <= p.tol_abs && !p.bench) {
     s->done = 1;
     s->outcome = OUT_CONVERGED;
     return;
   }
-  const double alpha = s->alpha, omega = s->omega, rho = s->rho;
+  const double alpha = p.alpha, omega = p.omega, rho = p.rho;
   const double beta1 = ((alpha / omega) * rho1) / rho;
   const double den = (dw + beta1 * ds) - (beta1 * omega) * dz;
   const double alpha1 = rho1 / den;
@@ -186,14 +207,14 @@ __device__ __forceinline__ void finalize_iteration(Scal* s, Hist h, double rho1,
 }
 
 // Replacement decision for iteration i (A11: (i+1) mod P == 0; A12 latch).
-__device__ __forceinline__ bool rr_scheduled(const Scal* s) {
-  if (s->auto_rr) return s->rr_next != 0;  // eq:criterion
-  return s->rr_period > 0 && ((s->iter + 1) % s->rr_period) == 0 && !s->rr_off;
+__device__ __forceinline__ bool rr_scheduled(const Snap& s) {
+  if (s.auto_rr) return s.rr_next != 0;  // eq:criterion
+  return s.rr_period > 0 && ((s.iter + 1) % s.rr_period) == 0 && !s.rr_off;
 }
 
 // The scalar-forming steps, given the combined dot totals (one thread).
 template <int F>
-__device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot) {
+__device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot, const Snap& p) {
   if (F == F_INIT1) {
     sc->tmp0 = dd_round(tot[0]);  // (r0, r0) = (r^0, r0) = rho_0
     sc->tmp1 = dd_round(tot[1]);  // (b, b)
@@ -326,37 +347,38 @@ __device__ __forceinline__ void fin_step(Scal* sc, Hist h, const Dd* tot) {
     sc->omega = omn;
     sc->use_rr = 0;
     {
-      double* t = h.sc + SC_W * (size_t)sc->iter;
-      t[0] = sc->alpha;
-      t[1] = sc->beta;
+      double* t = h.sc + SC_W * (size_t)p.iter;
+      t[0] = p.alpha;
+      t[1] = p.beta;
       t[2] = omn;
-      t[3] = sc->rho;
+      t[3] = p.rho;
       t[4] = qy;
       t[5] = yy;
     }
-    if (sc->auto_rr)
+    if (p.auto_rr)
       for (int k = 0; k < 10; ++k) sc->nA_[k] = sqrt(dd_round(tot[2 + k]));
     if (!isfinite(omn)) {
       sc->done = 1;
       sc->outcome = OUT_BREAKDOWN;
-      sc->iters = sc->iter;
+      sc->iters = p.iter;
     }
   } else if (F == F_SWEEPC) {
-    if (sc->auto_rr)
+    if (p.auto_rr)
       for (int k = 0; k < 4; ++k) sc->nC_[k] = sqrt(dd_round(tot[5 + k]));
-    if (rr_scheduled(sc)) {
+    if (rr_scheduled(p)) {
       sc->rr_fire = 1;  // the line-21 dots are recomputed after the replacement
-      h.rrl[sc->n_rr++] = sc->iter;
+      h.rrl[p.n_rr] = p.iter;
+      sc->n_rr = p.n_rr + 1;
     } else {
-      if (sc->auto_rr) auto_step(sc, h, sqrt(dd_round(tot[4])));
-      finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
+      if (p.auto_rr) auto_step(sc, h, sqrt(dd_round(tot[4])));
+      finalize_iteration(sc, h, p, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
                          dd_round(tot[3]), dd_round(tot[4]));
     }
   } else if (F == F_RR1) {  // norms of the replaced x_{i+1}, k_{i+1}, s_i, l_i
     for (int k = 0; k < 4; ++k) sc->nR_[k] = sqrt(dd_round(tot[k]));
   } else if (F == F_RR2) {
-    if (sc->auto_rr) auto_reset(sc, h, sqrt(dd_round(tot[4])), sqrt(dd_round(tot[5])));
-    finalize_iteration(sc, h, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
+    if (p.auto_rr) auto_reset(sc, h, sqrt(dd_round(tot[4])), sqrt(dd_round(tot[5])));
+    finalize_iteration(sc, h, p, dd_round(tot[0]), dd_round(tot[1]), dd_round(tot[2]),
                        dd_round(tot[3]), dd_round(tot[4]));
     sc->use_rr = 1;
   } else if (F == F_GAP) {
@@ -376,9 +398,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   return v;
 }
 
+// pre: the kernel's prologue copy of the state (Snap), or null to load it here
 template <int F, int K>
-__device__ __forceinline__ void publish(Scal* sc, Hist h, const Dd (&tot)[K]) {
-  if (sc->dist && sc->p2p) {
+__device__ __forceinline__ void publish(Scal* sc, Hist h, const Dd (&tot)[K],
+                                        const Snap* pre = nullptr) {
+  Snap p;
+  if (pre) p = *pre;
+  else snap_load(p, sc);
+  if (p.dist && p.p2p) {
     // every rank performs the same reductions in the same order: the epoch numbers
     // them identically on all ranks
     const unsigned long long e = *sc->p2p_epoch + 1;
@@ -391,12 +418,12 @@ __device__ __forceinline__ void publish(Scal* sc, Hist h, const Dd (&tot)[K]) {
     }
     __threadfence_system();
     for (int q = 0; q < P; ++q) st_release_sys(sc->p2p_flag[q] + sc->rank, e);
-  } else if (sc->dist) {
+  } else if (p.dist) {
     Dd* row = sc->red_send + (size_t)sc->rank * RED_K;
 #pragma unroll
     for (int k = 0; k < K; ++k) row[k] = tot[k];
   } else {
-    fin_step<F>(sc, h, tot);
+    fin_step<F>(sc, h, tot, p);
   }
 }
 
@@ -432,5 +459,7 @@ __global__ void k_fin(Scal* __restrict__ sc, Hist h) {
       tot[k] = dd_add(tot[k], v);
     }
   }
-  fin_step<F>(sc, h, tot);
+  Snap p;
+  snap_load(p, sc);
+  fin_step<F>(sc, h, tot, p);
 }

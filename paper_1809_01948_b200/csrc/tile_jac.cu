@@ -109,3 +109,15 @@ cudaError_t JAC_CAT(tile_persist_launch_, PBICG_VEC)(int dim, int grid, size_t s
   return dim == 3 ? cudaLaunchKernelEx(&cfg, t_persist<3, kVec>, g, V, sc, part, h, L)
                   : cudaLaunchKernelEx(&cfg, t_persist<2, kVec>, g, V, sc, part, h, L);
 }
+
+#if defined(PBICG_TIMELINE) && PBICG_VEC
+// timeline variant only: point the instrumentation at a device buffer (records, count)
+extern "C" int pbicg_timeline_set(void* buf, void* cnt, unsigned cap) {
+  TlRec* b = (TlRec*)buf;
+  unsigned* c = (unsigned*)cnt;
+  cudaError_t e = cudaMemcpyToSymbol(g_tl_buf, &b, sizeof(b));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_tl_cnt, &c, sizeof(c));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_tl_cap, &cap, sizeof(cap));
+  return (int)e;
+}
+#endif

@@ -689,6 +689,52 @@ __device__ __noinline__ bool peer_put(double* hp_lo, double* hp_hi, const double
 // untaken runtime branch cost sweep A 0.5-1.3%).
 template <int M> struct HasPeer { enum { v = BaseOf<M>::v == TM_A || BaseOf<M>::v == TM_C }; };
 
+// Timeline instrumentation (experiments only: scripts/timeline.py builds a variant
+// library with -DPBICG_TIMELINE; the product build carries none of it).  Thread 0 of
+// every CTA appends one record per launch: %globaltimer at entry, after the PDL wait,
+// when the first unit's first plane has landed, after the unit loop and at exit.
+#ifdef PBICG_TIMELINE
+struct TlRec {
+  unsigned long long t[8];  // entry, wait, first plane, loop end, exit, grid reduce done,
+                            // publish done, spare
+  unsigned long long id;    // block | grid << 16 | mode << 32 | smid << 48
+  unsigned long long units;
+};
+__device__ TlRec* g_tl_buf;
+__device__ unsigned int* g_tl_cnt;
+__device__ unsigned int g_tl_cap;
+__device__ __forceinline__ unsigned long long tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TL_DECL unsigned long long tl_t[8] = {0, 0, 0, 0, 0, 0, 0, 0}; unsigned long long tl_units = 0
+#define TL_STAMP(k) do { if (threadIdx.x == 0 && tl_t[k] == 0) tl_t[k] = tl_now(); } while (0)
+#define TL_UNIT() (++tl_units)
+#define TL_FLUSH(mode)                                                                       \
+  do {                                                                                       \
+    if (threadIdx.x == 0) tl_t[4] = tl_now();                                                \
+    if (threadIdx.x == 0 && g_tl_buf) {                                                      \
+      unsigned smid;                                                                         \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));                                      \
+      const unsigned i = atomicAdd(g_tl_cnt, 1u);                                            \
+      if (i < g_tl_cap) {                                                                    \
+        TlRec r;                                                                             \
+        for (int k_ = 0; k_ < 8; ++k_) r.t[k_] = tl_t[k_];                                   \
+        r.id = blockIdx.x | ((unsigned long long)gridDim.x << 16) |                          \
+               ((unsigned long long)(mode) << 32) | ((unsigned long long)smid << 48);        \
+        r.units = tl_units;                                                                  \
+        g_tl_buf[i] = r;                                                                     \
+      }                                                                                      \
+    }                                                                                        \
+  } while (0)
+#else
+#define TL_DECL
+#define TL_STAMP(k) do { } while (0)
+#define TL_UNIT() do { } while (0)
+#define TL_FLUSH(mode) do { } while (0)
+#endif
+
 // The body of one tile step (a device function so the persistent iteration kernel
 // t_persist can run sweep A and sweep C back to back inside one launch).
 template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false, bool PEER = false>
@@ -713,12 +759,19 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
   // (their per-leg work is one or two flops; the transform's halo pairs and stores cost more)
   constexpr bool XF = BJP && BB >= 4;
   __shared__ double s_bi[64];                  // the inverse block (row-major BB x BB)
+  TL_DECL;
+  TL_STAMP(0);
   if (BJ > 0) {
     for (int q = threadIdx.x; q < BB * BB; q += blockDim.x) s_bi[q] = g.bi[q];
   }
   // PDL (tile_launch): nothing above reads the previous kernel's results; wait for it
   // to complete (a no-op without PDL)
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  TL_STAMP(1);
+  // the state the last CTA's bookkeeping starts from (Snap, state.cuh): loaded now by a
+  // thread that issues no TMA, consumed after the grid reduction
+  __shared__ Snap s_snap;
+  if (T::K > 0 && threadIdx.x == 32) snap_load(s_snap, sc);
   constexpr int SD = StreamDepth<MODE_>::v;  // stream ring depth; stencil barriers follow
   constexpr int SVR = SvDepth<MODE_>::v;      // stencil-plane ring depth
   static_assert(SD + SVR <= 8, "the mbarriers fit the 64-byte shared-memory header");
@@ -965,6 +1018,8 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
       const int s = svc % SVR;
       mbar_wait(&bar[SD + s], (ph >> (SD + s)) & 1u);
       ph ^= 1u << (SD + s);
+      TL_STAMP(2);
+      TL_UNIT();
       const double* b0p = sv + (size_t)s * NSV * svs + sv_off(z0 - 1);
       if (act) {
         if (DER) {
@@ -1171,6 +1226,7 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
     svc = (svc + nsv) % SVR;
     stc = (stc + nst) % SD;
   }
+  TL_STAMP(3);
   // PDL: this CTA's sweep is done; the next kernel may be scheduled (it still waits
   // for this grid's completion, the grid reduction included, before reading anything)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -1185,20 +1241,23 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
                    : MODE == TM_PC ? T_PC : MODE == TM_PCI1 ? T_PCI1 : MODE == TM_RR1 ? T_RR1
                    : T_PCI2;
     if (dd_grid_reduce<K>(acc, part, &sc->counter[slot], tot) && tid == 0) {
-      if (MODE == TM_A) publish<F_SWEEPA>(sc, h, tot);
-      else if (MODE == TM_C) publish<F_SWEEPC>(sc, h, tot);
-      else if (MODE == TM_RR2) publish<F_RR2>(sc, h, tot);
-      else if (MODE == TM_GAP) publish<F_GAP>(sc, h, tot);
-      else if (MODE == TM_INIT1 || MODE == TM_PCI1) publish<F_INIT1>(sc, h, tot);
-      else if (MODE == TM_INIT2) publish<F_INIT2>(sc, h, tot);
-      else if (MODE == TM_CL1) publish<F_CL1>(sc, h, tot);
-      else if (MODE == TM_CL2) publish<F_CL2>(sc, h, tot);
-      else if (MODE == TM_CL3) publish<F_CL3>(sc, h, tot);
-      else if (MODE == TM_PC) publish<F_PC>(sc, h, tot);
-      else if (MODE == TM_RR1) publish<F_RR1>(sc, h, tot);
-      else publish<F_PINIT2>(sc, h, tot);
+      TL_STAMP(5);
+      if (MODE == TM_A) publish<F_SWEEPA>(sc, h, tot, &s_snap);
+      else if (MODE == TM_C) publish<F_SWEEPC>(sc, h, tot, &s_snap);
+      else if (MODE == TM_RR2) publish<F_RR2>(sc, h, tot, &s_snap);
+      else if (MODE == TM_GAP) publish<F_GAP>(sc, h, tot, &s_snap);
+      else if (MODE == TM_INIT1 || MODE == TM_PCI1) publish<F_INIT1>(sc, h, tot, &s_snap);
+      else if (MODE == TM_INIT2) publish<F_INIT2>(sc, h, tot, &s_snap);
+      else if (MODE == TM_CL1) publish<F_CL1>(sc, h, tot, &s_snap);
+      else if (MODE == TM_CL2) publish<F_CL2>(sc, h, tot, &s_snap);
+      else if (MODE == TM_CL3) publish<F_CL3>(sc, h, tot, &s_snap);
+      else if (MODE == TM_PC) publish<F_PC>(sc, h, tot, &s_snap);
+      else if (MODE == TM_RR1) publish<F_RR1>(sc, h, tot, &s_snap);
+      else publish<F_PINIT2>(sc, h, tot, &s_snap);
+      TL_STAMP(6);
     }
   }
+  TL_FLUSH(MODE_);
 }
 
 template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false, bool PEER = false>
