@@ -137,11 +137,22 @@ __device__ __forceinline__ void dd_block_reduce(Dd (&acc)[K]) {
 // last CTA to arrive (ticket) reduces all gridDim.x partials with a fixed
 // strided + tree order and returns true with the totals in tot[] on thread 0.
 // The ticket counter is reset by the last CTA so the kernel can be relaunched.
-template <int K>
+// OVR: a mask of value slots whose block totals are not this kernel's but come from
+// ovr[blockIdx.x * popc(OVR) + j] (j-th set bit; the tile replacement step's stash).
+template <int K, unsigned OVR = 0u>  // OVR: slots 0..7 only
 __device__ __forceinline__ bool dd_grid_reduce(Dd (&acc)[K], Dd* __restrict__ part,
-                                               unsigned int* counter, Dd (&tot)[K]) {
+                                               unsigned int* counter, Dd (&tot)[K],
+                                               const Dd* __restrict__ ovr = nullptr) {
   __shared__ bool s_last;
   dd_block_reduce<K>(acc);
+  if (OVR != 0u && threadIdx.x == 0) {
+    constexpr int NO = ((OVR >> 0) & 1) + ((OVR >> 1) & 1) + ((OVR >> 2) & 1) + ((OVR >> 3) & 1) +
+                       ((OVR >> 4) & 1) + ((OVR >> 5) & 1) + ((OVR >> 6) & 1) + ((OVR >> 7) & 1);
+    int j = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if ((OVR >> k) & 1u) acc[k] = ovr[(size_t)blockIdx.x * NO + j++];
+  }
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) part[(size_t)blockIdx.x * K + k] = acc[k];

@@ -296,7 +296,13 @@ enum Phase { PH_INIT1, PH_INIT2, PH_SWEEPA, PH_SPMVB, PH_SWEEPC, PH_RR1, PH_RR2,
 
 template <int DIM, int MODE>
 void launch_tile(pbicg_ctx* h) {
-  const int per_sm = h->tile_occ[MODE] > 0 ? h->tile_occ[MODE] : 1;
+  int per_sm = h->tile_occ[MODE] > 0 ? h->tile_occ[MODE] : 1;
+  if (Stash<MODE>::w || Stash<MODE>::r) {  // RR1 and RR2 on the same grid (the stash)
+    const int a = h->tile_occ[BaseOf<MODE>::v != MODE ? TM_RR1N : TM_RR1];
+    const int b = h->tile_occ[BaseOf<MODE>::v != MODE ? TM_RR2N : TM_RR2];
+    per_sm = a < b ? a : b;
+    if (per_sm < 1) per_sm = 1;
+  }
   const int cap = h->num_sm * per_sm;
   const int grid = h->tg.units < cap ? h->tg.units : cap;
   if (h->tile_seg) {  // x-segmented instances live in tile_seg.cu
@@ -647,6 +653,12 @@ bool split_sched(const pbicg_ctx* h) {
          !h->auto_rr && h->tg.bj <= 1;
 }
 
+// the stencil replacement step runs on the tile kernels: RR2 forms w = A k, z = A l from
+// the stored k, l (their ghost planes move instead of r, s; tile_sweeps.cuh Stash)
+bool tile_rr(const pbicg_ctx* h) {
+  return h->kind == KIND_STENCIL && h->tile_ok && (h->tile_on || h->auto_rr);
+}
+
 // the fused schedule's z / w halos travel inside the tile sweeps (transport 1)
 bool fused_halo(const pbicg_ctx* h) {
   return h->p2p && h->kind == KIND_STENCIL && h->tile_ok && h->tile_on && !split_sched(h);
@@ -914,7 +926,10 @@ void enq_iter(const Members& G, bool with_rr, int par) {
         if (dist) comm_halo(G, {SX, SG});
         each(G, PH_RR1);
         if (h0->auto_rr) reduce_fin(G, F_RR1);
-        if (dist) comm_halo(G, {SR, SS});
+        if (dist) {
+          if (tile_rr(h0)) comm_halo(G, {SK, SL});
+          else comm_halo(G, {SR, SS});
+        }
         each(G, PH_RR2);
         reduce_fin(G, F_RR2);
       }
@@ -965,7 +980,10 @@ void enq_iter(const Members& G, bool with_rr, int par) {
       if (dist) comm_halo(G, {SX, SG});
       each(G, PH_RR1);
       if (h0->auto_rr) reduce_fin(G, F_RR1);  // norms of the replaced vectors
-      if (dist) comm_halo(G, {SR, SS});
+      if (dist) {
+        if (tile_rr(h0)) comm_halo(G, {SK, SL});
+        else comm_halo(G, {SR, SS});
+      }
       each(G, PH_RR2);
       reduce_fin(G, F_RR2);
     }
@@ -1373,6 +1391,9 @@ pbicg_status alloc_common(pbicg_ctx* h) {
   void* p = nullptr;
   ST(dalloc(h, &p, (size_t)gmax * RED_K * sizeof(Dd)));  // K <= RED_K partials per CTA
   h->part = (Dd*)p;
+  void* q = nullptr;  // the tile replacement step's per-CTA dot stash (tile_sweeps.cuh)
+  ST(dalloc(h, &q, (size_t)gmax * STASH_K * sizeof(Dd)));
+  h->V.stash = (Dd*)q;
   ST(ensure_hist(h, 1024));
   // rank fields of the device state (kept across solves)
   Scal s;
@@ -3095,8 +3116,10 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "iteration" && h->method == M_PIPECG) b = 16 * 8 * N;
     else if (n == "sweepA") b = 11 * 8 * N;  // read k,g,l,w,s,z,r; write g,s,l,z
     else if (n == "sweepC") b = 13 * 8 * N;  // read x,g,k,l,r,s,w,z,r^; write x,r,k,w
-    else if (n == "rr1") b = 7 * 8 * N;      // read x,b,g; write r,k,s,l
-    else if (n == "rr2") b = 5 * 8 * N;      // read r,s,r^; write w,z
+    // tile replacement step: read x,b,g,r^; write r,k,s,l / read k,l,r^; write w,z
+    // (line kernels: read x,b,g; write r,k,s,l / read r,s,r^; write w,z)
+    else if (n == "rr1") b = (tile_rr(h) ? 8 : 7) * 8 * N;
+    else if (n == "rr2") b = 5 * 8 * N;
     else if (n == "gap") b = 3 * 8 * N;
     else if (n == "apply") b = 2 * 8 * N;
     else if (n == "init") b = 4 * 8 * N;     // mean of init1 (x,b -> r,r^,k) and init2 (r,r^ -> w)

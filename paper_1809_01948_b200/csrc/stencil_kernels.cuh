@@ -41,6 +41,9 @@ struct Vecs {
   // neighbours' memory; nullptr = no neighbour / no fused halo
   double* hz[2][2];
   double* hw[2][2];
+  // tile replacement step: per-CTA block totals of the three line-21 dots RR1 forms
+  // ((r^, r), (r^, s), (r, r) of the replaced r, s), read back by RR2's grid reduction
+  Dd* stash;
 };
 
 template <int DIM>

@@ -71,8 +71,8 @@ template <> struct BaseOf<TM_INIT1N> { enum { v = TM_INIT1 }; };
 template <int M> struct TileTraits;
 template <> struct TileTraits<TM_A> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 5, NOUT = 4, K = 2 }; };
 template <> struct TileTraits<TM_C> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 7, NOUT = 4, K = 5 }; };
-template <> struct TileTraits<TM_RR1> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 0 }; };
-template <> struct TileTraits<TM_RR2> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 5 }; };
+template <> struct TileTraits<TM_RR1> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 2, NOUT = 4, K = 3 }; };
+template <> struct TileTraits<TM_RR2> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 2, K = 5 }; };
 template <> struct TileTraits<TM_GAP> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 2, NOUT = 0, K = 1 }; };
 template <> struct TileTraits<TM_INIT1> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 1, NOUT = 3, K = 2 }; };
 template <> struct TileTraits<TM_INIT2> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 1, NOUT = 1, K = 1 }; };
@@ -100,9 +100,42 @@ template <> struct StreamDepth<TM_CL3> { enum { v = 3 }; };  // measured: CL3 +4
 template <int M> struct SvDepth { enum { v = 3 }; };
 template <> struct SvDepth<TM_SPB> { enum { v = 6 }; };
 template <> struct SvDepth<TM_SPD> { enum { v = 6 }; };
+// The replacement and init steps stream one or two vectors per plane next to two
+// staged operands: a 4-deep stencil ring and a 3-deep stream ring keep two planes in
+// flight (measured, cfg4: rr1 78% -> 90%, init 66% -> 72% of HBM; a 5-deep ring adds
+// nothing; the gap step loses with it, so it keeps the default)
+template <> struct SvDepth<TM_RR1> { enum { v = 4 }; };
+template <> struct SvDepth<TM_RR2> { enum { v = 4 }; };
+template <> struct SvDepth<TM_RR1N> { enum { v = 4 }; };
+template <> struct SvDepth<TM_RR2N> { enum { v = 4 }; };
+template <> struct SvDepth<TM_INIT1> { enum { v = 4 }; };
+template <> struct SvDepth<TM_INIT2> { enum { v = 4 }; };
+template <> struct SvDepth<TM_INIT1N> { enum { v = 4 }; };
+template <> struct StreamDepth<TM_RR1> { enum { v = 3 }; };
+template <> struct StreamDepth<TM_RR2> { enum { v = 3 }; };
+template <> struct StreamDepth<TM_RR1N> { enum { v = 3 }; };
+template <> struct StreamDepth<TM_RR2N> { enum { v = 3 }; };
+template <> struct StreamDepth<TM_INIT1> { enum { v = 3 }; };
+template <> struct StreamDepth<TM_INIT2> { enum { v = 3 }; };
+template <> struct StreamDepth<TM_INIT1N> { enum { v = 3 }; };
+
+// The line-21 dots after a replacement (eq:rr, then P:187): (r^, r), (r^, s)
+// and (r, r) need only the replaced r and s, which RR1 forms -- RR1 accumulates them
+// (w: it streams r^ too) and stores each CTA's block totals (Vecs::stash); RR2 (r: it
+// forms w = A k and z = A l from the stored k = M^-1 r, l = M^-1 s, so its stencils need
+// no M^-1) accumulates only (r^, w), (r^, z) and takes the other three block totals from
+// the stash into dot slots 0, 2, 4 before its grid reduction.  Same rows, same thread
+// order, same per-value block tree (dd_block_reduce) and the same grid: the totals are
+// the bits the one-kernel form gives.  RR2 is then no longer fp64-issue-bound.
+template <int M> struct Stash { enum { w = 0, r = 0 }; };
+template <> struct Stash<TM_RR1> { enum { w = 1, r = 0 }; };
+template <> struct Stash<TM_RR1N> { enum { w = 1, r = 0 }; };
+template <> struct Stash<TM_RR2> { enum { w = 0, r = 1 }; };
+template <> struct Stash<TM_RR2N> { enum { w = 0, r = 1 }; };
+#define STASH_K 3  // stashed dots per CTA
 template <> struct TileTraits<TM_CN> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 7, NOUT = 4, K = 9 }; };
-template <> struct TileTraits<TM_RR1N> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 4, K = 4 }; };
-template <> struct TileTraits<TM_RR2N> { enum { NSV = 2, DER = 0, PREC = 1, NSTR = 1, NOUT = 2, K = 6 }; };
+template <> struct TileTraits<TM_RR1N> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 2, NOUT = 4, K = 7 }; };
+template <> struct TileTraits<TM_RR2N> { enum { NSV = 2, DER = 0, PREC = 0, NSTR = 1, NOUT = 2, K = 6 }; };
 template <> struct TileTraits<TM_INIT1N> { enum { NSV = 1, DER = 0, PREC = 0, NSTR = 1, NOUT = 3, K = 4 }; };
 template <> struct TileTraits<TM_SPB> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 0 }; };
 template <> struct TileTraits<TM_SPD> { enum { NSV = 1, DER = 0, PREC = 1, NSTR = 0, NOUT = 1, K = 0 }; };
@@ -568,12 +601,17 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
       nrm_add(acc[5 % K], xj); nrm_add(acc[6 % K], uu); nrm_add(acc[7 % K], nn);
       nrm_add(acc[8 % K], t1);
     }
-  } else if (MODE == TM_RR1) {  // c = x, g; t0 = A x, t1 = A g
+  } else if (MODE == TM_RR1) {  // c = x, g; t0 = A x, t1 = A g; streams b, r^
     const double rj = S[0] - t0;               // r := b - A x
+    const double rhj = S[st];
     o[0] = rj;
     o[1] = dinv * rj;                          // k := M^-1 r
     o[2] = t1;                                 // s := A g
     o[3] = dinv * t1;                          // l := M^-1 s
+    constexpr int KD = NRM ? 4 : 0;            // the stashed line-21 dots (Stash)
+    dd_fma(acc[KD % K], rhj, rj);              // (r^, r)
+    dd_fma(acc[(KD + 1) % K], rhj, t1);        // (r^, s)
+    dd_fma(acc[(KD + 2) % K], rj, rj);         // (r, r)
     if (NRM) {  // (block Jacobi: k, l norms after the shuffle in t_tile)
       nrm_add(acc[0], c0); nrm_add(acc[2 % K], o[2]);
       if (!BJ) {
@@ -581,15 +619,12 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
         nrm_add(acc[3 % K], o[3]);
       }
     }
-  } else if (MODE == TM_RR2) {  // c = r, s; t0 = A M^-1 r = A k, t1 = A M^-1 s = A l
+  } else if (MODE == TM_RR2) {  // c = k, l; t0 = A k = A M^-1 r, t1 = A l = A M^-1 s
     const double rhj = S[0];
     o[0] = t0;                                 // w := A k
     o[1] = t1;                                 // z := A l
-    dd_fma(acc[0], rhj, c0);                   // line 21 on the replaced vectors
-    dd_fma(acc[1 % K], rhj, t0);
-    dd_fma(acc[2 % K], rhj, c1);
-    dd_fma(acc[3 % K], rhj, t1);
-    dd_fma(acc[4 % K], c0, c0);
+    dd_fma(acc[1 % K], rhj, t0);               // line 21 on the replaced vectors; slots
+    dd_fma(acc[3 % K], rhj, t1);               // 0, 2, 4 come from RR1's stash
     if (NRM) nrm_add(acc[5 % K], t1);
   } else if (MODE == TM_GAP) {  // c = x; t0 = A x
     const double dg = (S[0] - t0) - S[st];     // (b - A x) - r
@@ -816,10 +851,10 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
     outp[3 % NOUT] = (it & 1) ? V.w0 : V.w1;         // w_{i+1}
   } else if (MODE == TM_RR1) {
     svp[0] = V.x; svp[1] = V.g;
-    stp[0] = V.b;
+    stp[0] = V.b; stp[1 % NSTR_MAX] = V.rh;
     outp[0] = V.r; outp[1 % NOUT] = V.k; outp[2 % NOUT] = V.s; outp[3 % NOUT] = V.l;
   } else if (MODE == TM_RR2) {
-    svp[0] = V.r; svp[1] = V.s;
+    svp[0] = V.k; svp[1] = V.l;                      // M^-1 r, M^-1 s as RR1 stored them
     stp[0] = V.rh;
     outp[0] = (it & 1) ? V.w0 : V.w1;                // w_{i+1}
     outp[1 % NOUT] = V.zrr;                          // replaced z_i (A26)
@@ -1233,14 +1268,29 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
   // remote ghost stores visible system-wide before this CTA's ticket: the last CTA's
   // release of the reduction flag then publishes them with the partials
   if (remote) __threadfence_system();
-  if (T::K > 0) {
+  if (Stash<MODE_>::w && !NRM) {
+    // RR1: no scalar of its own; each CTA's block totals of the three dots for RR2
+    dd_block_reduce<K>(acc);
+    if (tid == 0) {
+#pragma unroll
+      for (int j = 0; j < STASH_K; ++j) V.stash[(size_t)blockIdx.x * STASH_K + j] = acc[j];
+    }
+  } else if (T::K > 0) {
     Dd tot[K];
     const int slot = MODE == TM_A ? T_SWEEPA : MODE == TM_C ? T_SWEEPC : MODE == TM_RR2 ? T_RR2
                    : MODE == TM_GAP ? T_GAP : MODE == TM_INIT1 ? T_INIT1 : MODE == TM_INIT2 ? T_INIT2
                    : MODE == TM_CL1 ? T_CL1 : MODE == TM_CL2 ? T_CL2 : MODE == TM_CL3 ? T_CL3
                    : MODE == TM_PC ? T_PC : MODE == TM_PCI1 ? T_PCI1 : MODE == TM_RR1 ? T_RR1
                    : T_PCI2;
-    if (dd_grid_reduce<K>(acc, part, &sc->counter[slot], tot) && tid == 0) {
+    // RR2: dot slots 0, 2, 4 take RR1's stashed block totals (same grid, same units)
+    constexpr unsigned OVR = Stash<MODE_>::r ? 0x15u : 0u;
+    const bool last = dd_grid_reduce<K, OVR>(acc, part, &sc->counter[slot], tot, V.stash);
+    if (Stash<MODE_>::w && tid == 0) {  // RR1N: the dots ride after the four norms
+#pragma unroll
+      for (int j = 0; j < STASH_K; ++j)
+        V.stash[(size_t)blockIdx.x * STASH_K + j] = acc[K - STASH_K + j];
+    }
+    if (last && tid == 0) {
       TL_STAMP(5);
       if (MODE == TM_A) publish<F_SWEEPA>(sc, h, tot, &s_snap);
       else if (MODE == TM_C) publish<F_SWEEPC>(sc, h, tot, &s_snap);

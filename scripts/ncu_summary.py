@@ -10,7 +10,7 @@ import json
 import re
 
 ALG = {  # algorithmic bytes per row: passes x 8 B
-    "sweepA": 88, "sweepC": 104, "rr1": 56, "rr2": 40, "gap": 24, "init1": 40, "init2": 24,
+    "sweepA": 88, "sweepC": 104, "rr1": 64, "rr2": 40,  # rr1: tile form streams r^ (round 2) "gap": 24, "init1": 40, "init2": 24,
     "cl1": 48, "cl2": 16, "cl3": 56, "pcg": 128, "pcinit1": 32, "pcinit2": 16,
     # CSR at 27 nnz/row, Jacobi: window SpMV SELL-32 val 8 + int16 offset 2 per slot
     # (270 B/row); the int32 column-major ELL (12 per slot) for init / apply
