@@ -6,7 +6,8 @@ alike; prints the median per-kernel average duration and its fraction of the mea
 HBM peak (the library's algorithmic bytes per launch).
 
 usage: python scripts/ab_kernels.py LIB_A LIB_B [case ...]   (cases of ab_libs.py)
-       env AB_PREC=bj2|bj4|bj8|ilu0 (instead of Jacobi), AB_AUTO=1 (rr auto)
+       env AB_PREC=bj2|bj4|bj8|ilu0 (instead of Jacobi), AB_AUTO=1 (automated replacement)
+       AB_SCHED=2 (the split schedule)
 """
 import json
 import os
@@ -40,8 +41,11 @@ def run(handle, case, maxit=200, reps=2):
     x0 = torch.zeros_like(b)
     x = torch.empty_like(b)
     S.set_option("bench", 1)
+    if os.environ.get("AB_SCHED"):
+        S.set_option("schedule", int(os.environ["AB_SCHED"]))
     if os.environ.get("AB_AUTO") == "1":
         S.set_option("rr_auto", 1)
+        rr = 0
     for _ in range(2):
         S.solve(b, x0, tol=0.0, maxit=maxit, rr_period=rr, gap=True, x_out=x)
     torch.cuda.synchronize()

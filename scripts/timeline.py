@@ -10,6 +10,7 @@ grid's first wait return, first-plane latency, the spread of the unit loops, and
 grid-reduction tail.  The product library is untouched.
 
 usage: python scripts/timeline.py [--build-only] [case ...]   (cases as measure_persist.py)
+       env TL_OPTS="opt=value,...": solver options (e.g. defer=0)
 """
 import ctypes
 import json
@@ -61,7 +62,7 @@ def analyse(rec, peak, n, bytes_per_row):
     for L in launches:
         mc = int((L[0, 8] >> 32) & 0xFFFF)
         m = MODES.get(mc, str(mc))
-        t0, t1, t2, t3, t4, t5, t6 = (L[:, k].astype(np.int64) for k in range(7))
+        t0, t1, t2, t3, t4, t5, t6, t7 = (L[:, k].astype(np.int64) for k in range(8))
         last = np.nonzero(t5)[0]
         d = {"period": (t1.min() - prev_wait) if prev_wait is not None else None,
              "gap": (t1.min() - prev_end) if prev_end is not None else None,
@@ -76,7 +77,11 @@ def analyse(rec, peak, n, bytes_per_row):
              "last_publish": (t6[last[0]] - t5[last[0]]) if len(last) else None,
              "last_after": (t4[last[0]] - t6[last[0]]) if len(last) else None,
              "last_is_latest": bool(len(last) and t3[last[0]] == t3.max()),
-             "busy": t4.max() - t1.min()}
+             "busy": t4.max() - t1.min(),
+             # deferred finalize: the redundant reduction + step after the prologue issue
+             "df_fin": float(np.median(t7 - t1)) if t7.min() > 0 else None,
+             "df_cnt": float(np.median(t5 - t1)) if t7.min() > 0 else None,
+             "df_pre": float(np.median(t6 - t1)) if t7.min() > 0 else None}
         prev_end = t4.max()
         prev_wait = t1.min()
         rows.setdefault(m, []).append(d)
@@ -126,6 +131,9 @@ def main():
         x0 = torch.zeros_like(b)
         x = torch.empty_like(b)
         S.set_option("bench", 1)
+        for kv in filter(None, os.environ.get("TL_OPTS", "").split(",")):  # e.g. defer=0
+            k, v = kv.split("=")
+            S.set_option(k, int(v))
         for _ in range(3):
             S.solve(b, x0, tol=0.0, maxit=100, rr_period=0, gap=False, x_out=x)
         torch.cuda.synchronize()
