@@ -32,6 +32,7 @@
 #include "tile_jac.h"
 #include "tile_seg.h"
 #include "tile_sweeps.cuh"
+#include "spmv_tile.cuh"
 
 namespace {
 
@@ -80,6 +81,11 @@ struct pbicg_ctx {
   TileGeo tg{};
   bool tile_ok = false;  // TMA 2.5D sweeps eligible for this operator
   bool tile_vec = false; // ... with 16-byte aligned pairs (nx even)
+  // split schedule's stand-alone SpMVs on tall tiles (spmv_tile.cuh; 3D Jacobi, nx even)
+  bool spt_ok = false;
+  int spt_np = 4;        // row pairs per thread
+  size_t spt_smem = 0;
+  SpmvGeo sq{};
   bool tile_seg = false; // ... as x-segmented tiles (nx > 1024, or 3D planes too wide for
                          // full-line tiles; instances in tile_seg.cu)
   int tile_on = 1;       // option "tile"
@@ -328,6 +334,9 @@ void launch_tile(pbicg_ctx* h) {
                       h->part, h->hist);
 }
 
+template <int MODE>
+void launch_spt(pbicg_ctx* h);  // spmv_tile.cuh instances (below, with setup_spmv_tile)
+
 template <int DIM>
 void launch_stencil(pbicg_ctx* h, Phase p) {
   const Geo& g = h->geo;
@@ -398,8 +407,16 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
       else
         k_sweepC2<DIM><<<h->grid_c2, 256, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
-    case PH_SPB: { LaunchScope ls(h, K_SPMVB); launch_tile<DIM, TM_SPB>(h); } break;
-    case PH_SPD: { LaunchScope ls(h, K_SPMVD); launch_tile<DIM, TM_SPD>(h); } break;
+    case PH_SPB: {
+      LaunchScope ls(h, K_SPMVB);
+      if (DIM == 3 && h->spt_ok) launch_spt<TM_SPB>(h);
+      else launch_tile<DIM, TM_SPB>(h);
+    } break;
+    case PH_SPD: {
+      LaunchScope ls(h, K_SPMVD);
+      if (DIM == 3 && h->spt_ok) launch_spt<TM_SPD>(h);
+      else launch_tile<DIM, TM_SPD>(h);
+    } break;
     default:
       break;
   }
@@ -1196,6 +1213,72 @@ cudaError_t set_tile_attrs(pbicg_ctx* h) {
   return e;
 }
 
+// Tall tiles of the split schedule's stand-alone SpMVs (spmv_tile.cuh): TY lines with
+// up to spt_np row pairs per thread, chunks of planes as for the sweeps.
+template <int NP>
+cudaError_t spt_attr(size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute(t_spmv3<TM_SPB, NP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(t_spmv3<TM_SPD, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+  return e;
+}
+
+void setup_spmv_tile(pbicg_ctx* h, int smem_cap) {
+  h->spt_ok = false;
+  const Geo& g = h->geo;
+  if (h->dim != 3 || !h->tile_ok || h->tile_seg || !h->tile_vec || h->tg.bj > 1) return;
+  if (const char* e = getenv("PBICG_SPT_NP")) {  // tuning experiments only (2 or 4; 0 = off)
+    const long v = strtol(e, nullptr, 10);
+    if (v == 0) return;
+    if (v == 2 || v == 4) h->spt_np = (int)v;
+  }
+  SpmvGeo& q = h->sq;
+  int64_t TY = (2LL * TNT * h->spt_np) / g.nx;
+  if (TY > g.ny) TY = g.ny;
+  for (; TY >= 1; --TY) {
+    q.TY = (int32_t)TY;
+    q.sv_stride = (int32_t)((TY * g.nx + 2 * (g.nx + 2) + 2 + 1) & ~1LL);
+    if (spmv_smem_bytes(q) <= (size_t)smem_cap) break;
+  }
+  if (TY < 1) return;
+  q.ncols = (int32_t)((g.ny + TY - 1) / TY);
+  const int grid = h->num_sm;
+  int64_t best_n = 1;
+  double best_w = 1e30;
+  for (int64_t nch = 1; nch <= g.nol; ++nch) {
+    const int64_t chunk = (g.nol + nch - 1) / nch;
+    const int64_t nchk = (g.nol + chunk - 1) / chunk;
+    const int64_t units = nchk * q.ncols;
+    const int64_t rounds = (units + grid - 1) / grid;
+    const double w = (double)rounds * (double)(chunk + 2);
+    if (w < best_w - 1e-9) {
+      best_w = w;
+      best_n = nch;
+    }
+    if (units > 64LL * grid) break;
+  }
+  q.chunk = (int32_t)((g.nol + best_n - 1) / best_n);
+  q.units = (int32_t)(((g.nol + q.chunk - 1) / q.chunk) * q.ncols);
+  h->spt_smem = spmv_smem_bytes(q);
+  const cudaError_t e = h->spt_np == 2 ? spt_attr<2>(h->spt_smem) : spt_attr<4>(h->spt_smem);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return;
+  }
+  h->spt_ok = true;
+}
+
+template <int MODE>
+void launch_spt(pbicg_ctx* h) {
+  const int grid = h->sq.units < h->num_sm ? h->sq.units : h->num_sm;
+  if (h->spt_np == 2)
+    t_spmv3<MODE, 2><<<grid, TNT, h->spt_smem, h->stream>>>(h->tg, h->sq, h->V, h->scal);
+  else
+    t_spmv3<MODE, 4><<<grid, TNT, h->spt_smem, h->stream>>>(h->tg, h->sq, h->V, h->scal);
+}
+
 // Tile geometry of the TMA 2.5D sweeps (tile_sweeps.cuh): TY full x-lines per
 // tile (3D) or one x-line (2D), a chunk of planes per work unit, units spread
 // statically over one CTA per SM (deterministic accumulation order).
@@ -1341,6 +1424,7 @@ void setup_tile(pbicg_ctx* h) {
     }
     cudaGetLastError();
   }
+  setup_spmv_tile(h, max_smem - (int)reserve);
 }
 
 pbicg_status common_setup(pbicg_ctx* h, void* cuda_stream) {

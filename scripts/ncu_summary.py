@@ -34,6 +34,8 @@ def kernel_key(name: str):
                  ("c_apply", "csr_apply")):
         if name.startswith(k):
             return v
+    if name.startswith("t_spmv3"):
+        return "spmv"
     if name.startswith("k_sweepA2"):
         return "split_sweepA"
     if name.startswith("k_sweepC2"):

@@ -437,6 +437,22 @@ def test_split_schedule_sweep_paths(S, orc, dim, nx, ny, nz, kind):
         check_parity(res, ref, xs)
 
 
+@pytest.mark.parametrize("dim,nx,ny,nz", [
+    (3, 96, 45, 30),    # TY = 42 lines: two tile columns, the second 3 lines (ragged)
+    (3, 512, 13, 9),    # TY = 8: 5-line ragged column, 4 row pairs per thread
+    (3, 130, 33, 20),   # TY = 31: the fourth pair of the last threads past the tile
+    (3, 64, 32, 300)])  # one column of 32 lines, several chunks of planes
+def test_split_schedule_tall_spmv_tiles(S, orc, dim, nx, ny, nz):
+    """The split schedule's stand-alone SpMVs on 3D Jacobi stencils run on tall tiles
+    (spmv_tile.cuh: TY lines, up to 4 row pairs per thread): ragged tile columns, ragged
+    pair counts and several chunks give the oracle's iterates bitwise, with periodic
+    replacement and gap tracking."""
+    solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of("cd3"))
+    solver.set_option("schedule", 2)
+    res = solver.solve(b_d, tol=1e-11, maxit=150, rr_period=7, gap=True)
+    check_parity(res, orc.pbicgstab(A, b, tol=1e-11, maxit=150, rr_period=7), xs)
+
+
 @pytest.mark.parametrize("bw", [1, 7, 1001, 5119])
 def test_csr_odd_bandwidth(S, orc, bw):
     """A band whose half width is odd: the window SpMV rounds it up to even so the
