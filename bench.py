@@ -384,7 +384,7 @@ def run_ours(args, rank, world):
     launches, _ = S.kernel_time("all")
     per_kernel = {}
     for k in ("sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap", "init", "apply", "fin",
-              "cl1", "cl2", "cl3", "pcg", "prec", "persist"):
+              "cl1", "cl2", "cl3", "pcg", "prec"):
         nk, tk = S.kernel_time(k)
         if nk:
             per_kernel[k] = {"launches": nk, "avg_ms": tk / nk if args.kernel_timing else None,

@@ -206,11 +206,6 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *                the next sweep's CTAs are scheduled as the previous sweep's CTAs
  *                retire (griddepcontrol); same results.  Default 0: measured +1-15%
  *                without CUDA graphs, within +-2% with them
- *   "persist"    1 => one rank, fused stencil schedule (Jacobi, full-line tiles, rr_auto
- *                and gap tracking off): every stretch of iterations without a replacement
- *                runs as ONE cooperative launch of the persistent kernel t_persist (sweep
- *                A, grid barrier, sweep C, grid barrier per iteration; same arithmetic,
- *                bitwise); no kernel boundary per sweep.  Ignored where not eligible
  *   "schedule"   0 (default) auto (stencil: fused, CSR: split); 1 fused 2-sweep
  *                (stencil only: t, v recomputed inside the sweeps, 24 passes); 2 split
  *                4-phase (the paper's pipeline: stored t, v, stand-alone SpMVs the
@@ -275,8 +270,7 @@ pbicg_status pbicgstab_solve_host(pbicg_handle h, const double* b_host, const do
 /* Per-kernel statistics since the last reset (reset = 1 clears them).
  *   name: "init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap",
  *   "apply", "fin" (multi-rank scalar finalisation), "cl1", "cl2", "cl3" (classic
- *   BiCGStab), "pcg" (p-CG), "prec" (stand-alone M^-1: block Jacobi, ILU(0)),
- *   "persist" (option persist; launches = iterations it covered), or "all".
+ *   BiCGStab), "pcg" (p-CG), "prec" (stand-alone M^-1: block Jacobi, ILU(0)), or "all".
  *   launches: kernel launches issued (graph nodes count once per replay);
  *   ms: summed CUDA-event time (only with option "timing"; else NaN). */
 pbicg_status pbicgstab_kernel_time(pbicg_handle h, const char* name, int64_t* launches,

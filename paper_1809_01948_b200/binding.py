@@ -18,7 +18,7 @@ from . import _build
 STATUS = {0: "OK", 1: "EINVAL", 2: "ECUDA", 3: "ENCCL", 4: "ENOMEM", 5: "ESTATE"}
 OUTCOMES = {0: "converged", 1: "maxit", 2: "breakdown"}
 KERNELS = ["init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap", "apply", "fin",
-           "cl1", "cl2", "cl3", "pcg", "prec", "persist"]
+           "cl1", "cl2", "cl3", "pcg", "prec"]
 # option "method": 0 p-BiCGStab (Alg. 2), 1 classic BiCGStab (Alg. 1), 2 p-CG (reading A19)
 
 

@@ -40,9 +40,9 @@ thread_local std::string g_create_err;
 constexpr int WIN_SMEM = 64 + WRS * (int)sizeof(double);
 
 enum Kname { K_INIT = 0, K_SWEEPA, K_SWEEPC, K_SPMVB, K_SPMVD, K_RR1, K_RR2, K_GAP, K_APPLY, K_FIN,
-             K_CL1, K_CL2, K_CL3, K_PC, K_PREC, K_PERSIST, K_N };
+             K_CL1, K_CL2, K_CL3, K_PC, K_PREC, K_N };
 const char* kname_str[K_N] = {"init", "sweepA", "sweepC", "spmvB", "spmvD", "rr1", "rr2", "gap",
-                              "apply", "fin", "cl1", "cl2", "cl3", "pcg", "prec", "persist"};
+                              "apply", "fin", "cl1", "cl2", "cl3", "pcg", "prec"};
 
 // solver selected with option "method"
 enum Method { M_PBICGSTAB = 0, M_BICGSTAB = 1, M_PIPECG = 2 };
@@ -89,10 +89,6 @@ struct pbicg_ctx {
   bool tile_seg = false; // ... as x-segmented tiles (nx > 1024, or 3D planes too wide for
                          // full-line tiles; instances in tile_seg.cu)
   int tile_on = 1;       // option "tile"
-  int persist = 0;       // option "persist": t_persist iteration kernel (one rank)
-  bool persist_ok = false;
-  int persist_grid = 0;
-  size_t persist_smem = 0;
   size_t tile_smem[TM_N] = {0};
   int tile_occ[TM_N] = {0};  // resident CTAs per SM of each tile kernel
   CsrOp csr{};
@@ -1053,44 +1049,14 @@ void enq_iter(const Members& G, bool with_rr, int par) {
 
 // chunk of L iterations starting at a multiple of L (L even, multiple of P when
 // P > 0): offset o replaces iff P > 0 && (o+1) % P == 0.
-// the persistent iteration kernel covers stretches of iterations without replacement
-bool persist_eligible(const Members& G) {
-  const pbicg_ctx* h = G[0];
-  return h->persist && h->persist_ok && G.size() == 1 && !h->dist && h->kind == KIND_STENCIL &&
-         h->tile_ok && h->tile_on && h->method == M_PBICGSTAB && !h->auto_rr && !h->gap_on &&
-         !split_sched(h) && !h->tg.pdl;
-}
-
-void launch_persist(pbicg_ctx* h, int L) {
-  {
-    LaunchScope ls(h, K_PERSIST);
-    const cudaError_t e =
-        h->tile_vec ? tile_persist_launch_1(h->dim, h->persist_grid, h->persist_smem, h->stream,
-                                            h->tg, h->V, h->scal, h->part, h->hist, L)
-                    : tile_persist_launch_0(h->dim, h->persist_grid, h->persist_smem, h->stream,
-                                            h->tg, h->V, h->scal, h->part, h->hist, L);
-    (void)e;  // a failed launch surfaces through cudaGetLastError in run_chunk
-  }
-  h->launches[K_PERSIST] += L - 1;  // "persist" counts the iterations it covers
-}
-
 void enq_chunk(const Members& G, int L, int P) {
   // automated replacement: decided on the device, so every iteration carries the
   // (early-exiting) replacement kernels
   const bool every = G[0]->auto_rr != 0;
-  const bool pers = persist_eligible(G);
-  int stretch = 0;
   for (int o = 0; o < L; ++o) {
     const bool rr = every || (P > 0 && ((o + 1) % P) == 0);
-    if (pers && !rr) {
-      stretch++;
-      continue;
-    }
-    if (stretch) launch_persist(G[0], stretch);
-    stretch = 0;
     enq_iter(G, rr, o & 1);
   }
-  if (stretch) launch_persist(G[0], stretch);
 }
 
 void destroy_graphs(pbicg_ctx* h) {
@@ -1409,21 +1375,6 @@ void setup_tile(pbicg_ctx* h) {
     return;
   }
   h->tile_ok = true;
-  // persistent iteration kernel: sweeps A and C of full-line Jacobi tiles in one
-  // cooperative launch (grid = every resident CTA)
-  h->persist_ok = false;
-  if (!h->tile_seg && t.bj <= 1) {
-    h->persist_smem = h->tile_smem[TM_A] > h->tile_smem[TM_C] ? h->tile_smem[TM_A] : h->tile_smem[TM_C];
-    int occ = 0;
-    const cudaError_t pe = h->tile_vec ? tile_persist_attr_1(dim, (int)h->persist_smem, &occ)
-                                       : tile_persist_attr_0(dim, (int)h->persist_smem, &occ);
-    if (pe == cudaSuccess && occ >= 1) {
-      const int cap = occ * h->num_sm;
-      h->persist_grid = t.units < cap ? t.units : cap;
-      h->persist_ok = true;
-    }
-    cudaGetLastError();
-  }
   setup_spmv_tile(h, max_smem - (int)reserve);
 }
 
@@ -2986,9 +2937,6 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
     } else if (k == "csr_tma") {  // CSR: TMA-staged sweeps (1, default) or per-row loads
       m->cst_on = value != 0;
       destroy_graphs(m);
-    } else if (k == "persist") {  // persistent iteration kernel (one rank, see persist_eligible)
-      m->persist = value != 0;
-      destroy_graphs(m);
     } else if (k == "pdl") {  // programmatic dependent launch of the tile kernels
       m->tg.pdl = value != 0;
       destroy_graphs(m);
@@ -3207,7 +3155,6 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "gap") b = 3 * 8 * N;
     else if (n == "apply") b = 2 * 8 * N;
     else if (n == "init") b = 4 * 8 * N;     // mean of init1 (x,b -> r,r^,k) and init2 (r,r^ -> w)
-    else if (n == "persist") b = 24 * 8 * N;  // per iteration covered (sweeps A + C)
     else if (n == "iteration") b = 24 * 8 * N;
   } else {
     const double slots = (double)h->csr.width;  // ELL width

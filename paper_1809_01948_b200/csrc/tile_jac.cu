@@ -83,33 +83,6 @@ cudaError_t JAC_CAT(tile_jac_attr_, PBICG_VEC)(int dim, int mode, int smem, int*
   return dim == 3 ? dispatch_attr<3>(mode, smem, occ) : dispatch_attr<2>(mode, smem, occ);
 }
 
-// persistent iteration kernel (t_persist): attribute + occupancy, and the cooperative
-// launch (capturable in a CUDA graph); grid = resident CTAs (one per SM at the
-// sweeps' shared memory)
-cudaError_t JAC_CAT(tile_persist_attr_, PBICG_VEC)(int dim, int smem, int* occ) {
-  const void* k = dim == 3 ? (const void*)t_persist<3, kVec> : (const void*)t_persist<2, kVec>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k, TNT, smem);
-  return e;
-}
-
-cudaError_t JAC_CAT(tile_persist_launch_, PBICG_VEC)(int dim, int grid, size_t smem, cudaStream_t s,
-                                                     const TileGeo& g, const Vecs& V, Scal* sc,
-                                                     Dd* part, Hist h, int L) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(TNT);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return dim == 3 ? cudaLaunchKernelEx(&cfg, t_persist<3, kVec>, g, V, sc, part, h, L)
-                  : cudaLaunchKernelEx(&cfg, t_persist<2, kVec>, g, V, sc, part, h, L);
-}
-
 #if defined(PBICG_TIMELINE) && PBICG_VEC
 // timeline variant only: point the instrumentation at a device buffer (records, count)
 extern "C" int pbicg_timeline_set(void* buf, void* cnt, unsigned cap) {

@@ -14,11 +14,7 @@ struct Hist;
 #define PBICG_JAC_DECL(V)                                                                    \
   bool tile_jac_launch_##V(int dim, int mode, int grid, size_t smem, cudaStream_t s,         \
                            const TileGeo& g, const Vecs& V_, Scal* sc, Dd* part, Hist h);    \
-  cudaError_t tile_jac_attr_##V(int dim, int mode, int smem, int* occ);                     \
-  cudaError_t tile_persist_attr_##V(int dim, int smem, int* occ);                            \
-  cudaError_t tile_persist_launch_##V(int dim, int grid, size_t smem, cudaStream_t s,        \
-                                      const TileGeo& g, const Vecs& V_, Scal* sc, Dd* part,  \
-                                      Hist h, int L);
+  cudaError_t tile_jac_attr_##V(int dim, int mode, int smem, int* occ);
 PBICG_JAC_DECL(0)
 PBICG_JAC_DECL(1)
 #undef PBICG_JAC_DECL

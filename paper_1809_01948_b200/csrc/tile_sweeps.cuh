@@ -39,14 +39,12 @@
 // never written to HBM; it is formed with the same operations as the oracle's
 // stored vector, hence bitwise equal.
 #pragma once
-#include <cooperative_groups.h>
 
 #include "dd.cuh"
 #include "state.cuh"
 #include "stencil_kernels.cuh"
 #include "tma.cuh"
 
-namespace cg = cooperative_groups;
 
 #define TNT 512  // threads per CTA
 
@@ -770,8 +768,7 @@ __device__ __forceinline__ unsigned long long tl_now() {
 #define TL_FLUSH(mode) do { } while (0)
 #endif
 
-// The body of one tile step (a device function so the persistent iteration kernel
-// t_persist can run sweep A and sweep C back to back inside one launch).
+// The body of one tile step.
 template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false, bool PEER = false>
 __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Scal* __restrict__ sc,
                                             Dd* __restrict__ part, const Hist& h) {
@@ -1314,27 +1311,6 @@ template <int DIM, int MODE_, bool VEC, int BJ = 0, bool SEG = false, bool PEER 
 __global__ void __launch_bounds__(TNT, 1) t_tile(TileGeo g, Vecs V, Scal* __restrict__ sc,
                                                  Dd* __restrict__ part, Hist h) {
   t_tile_body<DIM, MODE_, VEC, BJ, SEG, PEER>(g, V, sc, part, h);
-}
-
-// Persistent iteration kernel (option "persist"; one rank, Jacobi, full-line tiles,
-// no replacement / gap in the stretch): L iterations of the fused schedule -- sweep
-// A, grid barrier, sweep C, grid barrier -- in ONE cooperative launch.  The scalars
-// the last CTA of each sweep forms (omega; beta, alpha, stop) are read by every CTA
-// after the barrier, exactly as the next kernel would read them, so the arithmetic
-// and its order are those of the two-kernel schedule (bitwise); what disappears is
-// the kernel boundary: launch, grid ramp-up and drain, twice per iteration (the
-// latency regime of small grids).
-template <int DIM, bool VEC>
-__global__ void __launch_bounds__(TNT, 1) t_persist(TileGeo g, Vecs V, Scal* __restrict__ sc,
-                                                    Dd* __restrict__ part, Hist h, int L) {
-  cg::grid_group grid = cg::this_grid();
-  for (int o = 0; o < L; ++o) {
-    if (*(volatile int32_t*)&sc->done) break;  // uniform: read after a grid barrier
-    t_tile_body<DIM, TM_A, VEC>(g, V, sc, part, h);
-    grid.sync();
-    t_tile_body<DIM, TM_C, VEC>(g, V, sc, part, h);
-    grid.sync();
-  }
 }
 
 // host-side helper: shared-memory bytes of a t_tile<., MODE, .> launch

@@ -1,8 +1,8 @@
 #!/usr/bin/env python
 """A/B timing of two builds of libpbicgstab.so in one process (experiments only):
 interleaves the two libraries case by case, several rounds, so clock / power drift
-hits both alike.  Same measurement as measure_persist.py (CUDA graphs, bench mode,
-200 iterations per solve, CUDA events around 5 solves on the solver stream).
+hits both alike.  CUDA graphs, bench mode, 200 iterations per solve, CUDA events
+around 5 solves on the solver stream (the iteration rates of DESIGN.md section 8).
 
 usage: python scripts/ab_libs.py LIB_A LIB_B [case ...]
 """

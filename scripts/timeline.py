@@ -9,7 +9,7 @@ launch-to-launch period, the gap between the previous grid's last exit and this
 grid's first wait return, first-plane latency, the spread of the unit loops, and the
 grid-reduction tail.  The product library is untouched.
 
-usage: python scripts/timeline.py [--build-only] [case ...]   (cases as measure_persist.py)
+usage: python scripts/timeline.py [--build-only] [case ...]   (cases as ab_libs.py)
        env TL_OPTS="opt=value,...": solver options (e.g. defer=0)
 """
 import ctypes

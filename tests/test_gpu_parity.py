@@ -490,19 +490,18 @@ def test_csr_odd_bandwidth(S, orc, bw):
 @pytest.mark.parametrize("dim,nx,ny,nz,kind", [(2, 100, 100, 1, "poisson"), (3, 40, 33, 31, "cd3"),
                                                (3, 13, 7, 19, "cd3"), (2, 37, 53, 1, "cd2")])
 @pytest.mark.parametrize("graphs", [0, 1])
-def test_persistent_iteration_kernel(S, orc, dim, nx, ny, nz, kind, graphs):
-    """option persist: stretches of iterations without replacement run inside one
-    cooperative launch (sweep A, grid barrier, sweep C, grid barrier); bitwise equal
-    to the oracle and to the two-kernel schedule, with replacement iterations in
-    between and convergence inside a stretch."""
+def test_graph_chunks_with_and_without_replacement(S, orc, dim, nx, ny, nz, kind, graphs):
+    """Chunks of iterations replayed as CUDA graphs or enqueued directly: bitwise equal
+    to the oracle with replacement iterations in between and convergence inside a
+    chunk, then a bench-mode run.  (The round-2 persistent iteration kernel, option
+    persist, measured 0.4-3.4% slower than graphed kernels and was removed: the option
+    is now rejected.)"""
     solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of(kind))
     solver.set_option("graphs", graphs)
-    solver.set_option("persist", 1)
+    with pytest.raises(Exception):
+        solver.set_option("persist", 1)
     for rr in (0, 7):
-        solver.kernel_time("all", reset=True)
         res = solver.solve(b_d, tol=1e-11, maxit=400, rr_period=rr, gap=False)
-        n_p, _ = solver.kernel_time("persist")
-        assert n_p > 0, "the persistent kernel must run"
         ref = orc.pbicgstab(A, b, tol=1e-11, maxit=400, rr_period=rr, gap=False)
         check_parity(res, ref, xs, bitwise=True)
     solver.set_option("bench", 1)
