@@ -156,24 +156,24 @@ __device__ __forceinline__ bool dd_grid_reduce(Dd (&acc)[K], Dd* __restrict__ pa
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < K; ++k) part[(size_t)blockIdx.x * K + k] = acc[k];
-    __threadfence();
-    unsigned int t = atomicAdd(counter, 1u);
+    // one acq_rel ticket instead of fence + atomic + fence: release orders this CTA's
+    // partials before its ticket; the last CTA's acquire orders every CTA's partials
+    // before its reads (the other threads read after the barrier below, through L2)
+    unsigned int t;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(t) : "l"(counter)
+                 : "memory");
     s_last = (t == gridDim.x - 1);
   }
   __syncthreads();
   if (!s_last) return false;
-  __threadfence();
   Dd v[K];
 #pragma unroll
   for (int k = 0; k < K; ++k) v[k] = dd_zero();
   for (unsigned int b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
 #pragma unroll
     for (int k = 0; k < K; ++k) {
-      const Dd* p = part + (size_t)b * K + k;
-      Dd pv;
-      pv.hi = __ldcg(&p->hi);
-      pv.lo = __ldcg(&p->lo);
-      v[k] = dd_add(v[k], pv);
+      const double2 pv = __ldcg(reinterpret_cast<const double2*>(part + (size_t)b * K + k));
+      v[k] = dd_add(v[k], Dd{pv.x, pv.y});
     }
   }
   dd_block_reduce<K>(v);

@@ -18,6 +18,8 @@ from test_gpu_parity import check_parity, noise_floor_parity  # noqa: E402
 
 # PBICG_FUZZ_SCALE=k runs k times the cases (a wider sweep than the default suite)
 SCALE = int(os.environ.get("PBICG_FUZZ_SCALE", "1"))
+# PBICG_FUZZ_OFFSET=j shifts every seed by j * 100000 (independent wide sweeps)
+OFFSET = 100000 * int(os.environ.get("PBICG_FUZZ_OFFSET", "0"))
 N_CASES = 24 * SCALE
 
 
@@ -40,7 +42,7 @@ def _rank0(S):
 def test_fuzz_stencil(orc, seed):
     from paper_1809_01948_b200 import Solver
     from paper_1809_01948_b200.binding import LoopbackGroup
-    rng = np.random.default_rng(1000 + seed)
+    rng = np.random.default_rng(1000 + seed + OFFSET)
     dim = int(rng.choice([2, 3]))
     nx = int(rng.integers(1, 70))
     ny = int(rng.integers(1, 40))
@@ -105,7 +107,7 @@ def test_fuzz_stencil(orc, seed):
 @pytest.mark.parametrize("seed", range(12 * SCALE))
 def test_fuzz_csr(orc, seed):
     from paper_1809_01948_b200 import Solver
-    rng = np.random.default_rng(2000 + seed)
+    rng = np.random.default_rng(2000 + seed + OFFSET)
     block = int(rng.choice([1, 1, 2, 4, 8, 16, 32]))
     n = int(rng.integers(64, 400)) * 32
     bw = int(rng.choice([8, 100, 1000, 5000]))
@@ -141,7 +143,7 @@ def test_fuzz_wide_grids(orc, seed):
     """nx > 1024 (x-segmented tiles for even nx, line kernels for odd nx), random
     solver / replacement options, bitwise above the noise floor."""
     from paper_1809_01948_b200 import Solver
-    rng = np.random.default_rng(3000 + seed)
+    rng = np.random.default_rng(3000 + seed + OFFSET)
     dim = int(rng.choice([2, 3]))
     nx = int(rng.integers(1025, 2400))
     ny = int(rng.integers(1, 12))
@@ -170,7 +172,7 @@ def test_fuzz_csr_loopback(orc, seed):
     rank >= PBICG_CSR_HALO rows, any parity), Jacobi or block Jacobi, random solver,
     transport, TMA sweeps on/off and replacement."""
     from paper_1809_01948_b200.binding import LoopbackGroup
-    rng = np.random.default_rng(4000 + seed)
+    rng = np.random.default_rng(4000 + seed + OFFSET)
     P = int(rng.choice([2, 3]))
     block = int(rng.choice([1, 1, 2, 4, 8]))
     halo = 4096
@@ -217,7 +219,7 @@ def test_fuzz_stencil_block_jacobi(orc, seed):
     the transform stage), 1 or P emulated ranks, random transport and replacement."""
     from paper_1809_01948_b200 import Solver
     from paper_1809_01948_b200.binding import LoopbackGroup
-    rng = np.random.default_rng(5000 + seed)
+    rng = np.random.default_rng(5000 + seed + OFFSET)
     block = int(rng.choice([2, 4, 8]))
     dim = int(rng.choice([2, 3]))
     nx = block * int(rng.integers(1, 840 // block if dim == 3 else 1024 // block))
