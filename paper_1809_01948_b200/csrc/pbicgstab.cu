@@ -82,10 +82,11 @@ struct pbicg_ctx {
   bool tile_ok = false;  // TMA 2.5D sweeps eligible for this operator
   bool tile_vec = false; // ... with 16-byte aligned pairs (nx even)
   // split schedule's stand-alone SpMVs on tall tiles (spmv_tile.cuh; 3D Jacobi, nx even)
-  bool spt_ok = false;
-  int spt_np = 4;        // row pairs per thread
-  size_t spt_smem = 0;
-  SpmvGeo sq{};
+  // light steps on tall tiles (spmv_tile.cuh; 3D Jacobi, nx even): the split
+  // schedule's stand-alone SpMVs (4 row pairs per thread) and the replacement step (2)
+  bool spt_ok = false, lrr_ok = false;
+  size_t spt_smem = 0, lrr_smem = 0;
+  SpmvGeo sq{}, sq_rr{};
   bool tile_seg = false; // ... as x-segmented tiles (nx > 1024, or 3D planes too wide for
                          // full-line tiles; instances in tile_seg.cu)
   int tile_on = 1;       // option "tile"
@@ -331,7 +332,7 @@ void launch_tile(pbicg_ctx* h) {
 }
 
 template <int MODE>
-void launch_spt(pbicg_ctx* h);  // spmv_tile.cuh instances (below, with setup_spmv_tile)
+void launch_light(pbicg_ctx* h);  // spmv_tile.cuh instances (below, with setup_light_tiles)
 
 template <int DIM>
 void launch_stencil(pbicg_ctx* h, Phase p) {
@@ -366,12 +367,14 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
     case PH_RR1: {
       LaunchScope ls(h, K_RR1);
       if (h->auto_rr) launch_tile<DIM, TM_RR1N>(h);
+      else if (DIM == 3 && tile && h->lrr_ok) launch_light<TM_RR1>(h);
       else if (tile) launch_tile<DIM, TM_RR1>(h);
       else k_rr1<DIM><<<h->grid[K_RR1], h->block, 0, h->stream>>>(g, h->V, h->scal);
     } break;
     case PH_RR2: {
       LaunchScope ls(h, K_RR2);
       if (h->auto_rr) launch_tile<DIM, TM_RR2N>(h);
+      else if (DIM == 3 && tile && h->lrr_ok) launch_light<TM_RR2>(h);
       else if (tile) launch_tile<DIM, TM_RR2>(h);
       else k_rr2<DIM><<<h->grid[K_RR2], h->block, 0, h->stream>>>(g, h->V, h->scal, h->part, h->hist);
     } break;
@@ -405,12 +408,12 @@ void launch_stencil(pbicg_ctx* h, Phase p) {
     } break;
     case PH_SPB: {
       LaunchScope ls(h, K_SPMVB);
-      if (DIM == 3 && h->spt_ok) launch_spt<TM_SPB>(h);
+      if (DIM == 3 && h->spt_ok) launch_light<TM_SPB>(h);
       else launch_tile<DIM, TM_SPB>(h);
     } break;
     case PH_SPD: {
       LaunchScope ls(h, K_SPMVD);
-      if (DIM == 3 && h->spt_ok) launch_spt<TM_SPD>(h);
+      if (DIM == 3 && h->spt_ok) launch_light<TM_SPD>(h);
       else launch_tile<DIM, TM_SPD>(h);
     } break;
     default:
@@ -1179,36 +1182,28 @@ cudaError_t set_tile_attrs(pbicg_ctx* h) {
   return e;
 }
 
-// Tall tiles of the split schedule's stand-alone SpMVs (spmv_tile.cuh): TY lines with
-// up to spt_np row pairs per thread, chunks of planes as for the sweeps.
-template <int NP>
-cudaError_t spt_attr(size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(t_spmv3<TM_SPB, NP>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess)
-    e = cudaFuncSetAttribute(t_spmv3<TM_SPD, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-  return e;
+// Tall tiles of the light steps (spmv_tile.cuh): TY lines with NP row pairs per thread
+// (LtTraits), chunks of planes as for the sweeps.  The SpMVs and the replacement step
+// have their own geometry; RR1 and RR2 share theirs (the dot stash is per CTA).
+template <int MODE>
+cudaError_t light_attr(size_t smem) {
+  return cudaFuncSetAttribute(t_light3<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem);
 }
 
-void setup_spmv_tile(pbicg_ctx* h, int smem_cap) {
-  h->spt_ok = false;
+// lines per tile and chunking for NP row pairs per thread; false if nothing fits
+bool light_geo(const pbicg_ctx* h, int np, int smem_cap, size_t (*smem)(const SpmvGeo&),
+               SpmvGeo& q) {
   const Geo& g = h->geo;
-  if (h->dim != 3 || !h->tile_ok || h->tile_seg || !h->tile_vec || h->tg.bj > 1) return;
-  if (const char* e = getenv("PBICG_SPT_NP")) {  // tuning experiments only (2 or 4; 0 = off)
-    const long v = strtol(e, nullptr, 10);
-    if (v == 0) return;
-    if (v == 2 || v == 4) h->spt_np = (int)v;
-  }
-  SpmvGeo& q = h->sq;
-  int64_t TY = (2LL * TNT * h->spt_np) / g.nx;
+  int64_t TY = (2LL * TNT * np) / g.nx;
   if (TY > g.ny) TY = g.ny;
   for (; TY >= 1; --TY) {
     q.TY = (int32_t)TY;
     q.sv_stride = (int32_t)((TY * g.nx + 2 * (g.nx + 2) + 2 + 1) & ~1LL);
-    if (spmv_smem_bytes(q) <= (size_t)smem_cap) break;
+    q.st_stride = (int32_t)((TY * g.nx + 2 + 1) & ~1LL);
+    if (smem(q) <= (size_t)smem_cap) break;
   }
-  if (TY < 1) return;
+  if (TY < 1) return false;
   q.ncols = (int32_t)((g.ny + TY - 1) / TY);
   const int grid = h->num_sm;
   int64_t best_n = 1;
@@ -1227,22 +1222,42 @@ void setup_spmv_tile(pbicg_ctx* h, int smem_cap) {
   }
   q.chunk = (int32_t)((g.nol + best_n - 1) / best_n);
   q.units = (int32_t)(((g.nol + q.chunk - 1) / q.chunk) * q.ncols);
-  h->spt_smem = spmv_smem_bytes(q);
-  const cudaError_t e = h->spt_np == 2 ? spt_attr<2>(h->spt_smem) : spt_attr<4>(h->spt_smem);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    return;
+  return true;
+}
+
+size_t smem_spmv(const SpmvGeo& q) { return light_smem_bytes<TM_SPB>(q); }
+size_t smem_rr(const SpmvGeo& q) {
+  const size_t a = light_smem_bytes<TM_RR1>(q), b = light_smem_bytes<TM_RR2>(q);
+  return a > b ? a : b;
+}
+
+void setup_light_tiles(pbicg_ctx* h, int smem_cap) {
+  h->spt_ok = h->lrr_ok = false;
+  if (h->dim != 3 || !h->tile_ok || h->tile_seg || !h->tile_vec || h->tg.bj > 1) return;
+  const char* off = getenv("PBICG_LIGHT");  // tuning experiments only: 0 = t_tile everywhere
+  if (off && strtol(off, nullptr, 10) == 0) return;
+  if (light_geo(h, LtTraits<TM_SPB>::NP, smem_cap, smem_spmv, h->sq)) {
+    h->spt_smem = smem_spmv(h->sq);
+    if (light_attr<TM_SPB>(h->spt_smem) == cudaSuccess &&
+        light_attr<TM_SPD>(h->spt_smem) == cudaSuccess)
+      h->spt_ok = true;
   }
-  h->spt_ok = true;
+  if (light_geo(h, LtTraits<TM_RR1>::NP, smem_cap, smem_rr, h->sq_rr)) {
+    h->lrr_smem = smem_rr(h->sq_rr);
+    if (light_attr<TM_RR1>(h->lrr_smem) == cudaSuccess &&
+        light_attr<TM_RR2>(h->lrr_smem) == cudaSuccess)
+      h->lrr_ok = true;
+  }
+  cudaGetLastError();
 }
 
 template <int MODE>
-void launch_spt(pbicg_ctx* h) {
-  const int grid = h->sq.units < h->num_sm ? h->sq.units : h->num_sm;
-  if (h->spt_np == 2)
-    t_spmv3<MODE, 2><<<grid, TNT, h->spt_smem, h->stream>>>(h->tg, h->sq, h->V, h->scal);
-  else
-    t_spmv3<MODE, 4><<<grid, TNT, h->spt_smem, h->stream>>>(h->tg, h->sq, h->V, h->scal);
+void launch_light(pbicg_ctx* h) {
+  const bool rr = MODE == TM_RR1 || MODE == TM_RR2;
+  const SpmvGeo& q = rr ? h->sq_rr : h->sq;
+  const int grid = q.units < h->num_sm ? q.units : h->num_sm;  // RR1, RR2: the same grid
+  t_light3<MODE><<<grid, TNT, rr ? h->lrr_smem : h->spt_smem, h->stream>>>(
+      h->tg, q, h->V, h->scal, h->part, h->hist);
 }
 
 // Tile geometry of the TMA 2.5D sweeps (tile_sweeps.cuh): TY full x-lines per
@@ -1375,7 +1390,7 @@ void setup_tile(pbicg_ctx* h) {
     return;
   }
   h->tile_ok = true;
-  setup_spmv_tile(h, max_smem - (int)reserve);
+  setup_light_tiles(h, max_smem - (int)reserve);
 }
 
 pbicg_status common_setup(pbicg_ctx* h, void* cuda_stream) {

@@ -36,6 +36,9 @@ def kernel_key(name: str):
             return v
     if name.startswith("t_spmv3"):
         return "spmv"
+    m = re.search(r"t_light3<(\d+)>", name)
+    if m:
+        return MODES[int(m.group(1))]
     if name.startswith("k_sweepA2"):
         return "split_sweepA"
     if name.startswith("k_sweepC2"):

@@ -453,6 +453,29 @@ def test_split_schedule_tall_spmv_tiles(S, orc, dim, nx, ny, nz):
     check_parity(res, orc.pbicgstab(A, b, tol=1e-11, maxit=150, rr_period=7), xs)
 
 
+@pytest.mark.parametrize("dim,nx,ny,nz", [
+    (3, 96, 45, 30),    # TY = 21 lines: three tile columns, the last 3 lines (ragged)
+    (3, 512, 13, 9),    # TY = 4: ragged last column, 2 row pairs per thread
+    (3, 130, 33, 20),   # TY = 15: the second pair of the last threads past the tile
+    (3, 64, 32, 300)])  # one column, several chunks of planes
+def test_replacement_tall_tiles(S, orc, dim, nx, ny, nz):
+    """The periodic replacement of 3D Jacobi stencils runs on tall tiles
+    (spmv_tile.cuh t_light3<TM_RR1/RR2>: two row pairs per thread, RR1's three line-21
+    dots stashed per CTA for RR2): ragged columns and pair counts give the oracle's
+    iterates bitwise, one rank and two loopback ranks (ghost planes of k, l)."""
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    solver, A, xs, b, b_d = stencil_case(S, orc, dim, nx, ny, nz, coef_of("cd3"))
+    ref = orc.pbicgstab(A, b, tol=1e-11, maxit=150, rr_period=3)
+    res = solver.solve(b_d, tol=1e-11, maxit=150, rr_period=3, gap=True)
+    check_parity(res, ref, xs)
+    solver.close()
+    G = LoopbackGroup.stencil(2, dim, nx, ny, nz, coef_of("cd3"))
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=1e-11, maxit=150, rr_period=3, gap=True)
+    check_parity(res, ref, xs)
+    G.close()
+
+
 @pytest.mark.parametrize("bw", [1, 7, 1001, 5119])
 def test_csr_odd_bandwidth(S, orc, bw):
     """A band whose half width is odd: the window SpMV rounds it up to even so the
