@@ -3152,6 +3152,7 @@ pbicg_status pbicgstab_kernel_bytes(pbicg_handle h, const char* name, double* by
     else if (n == "rr2") b = 5 * 8 * N;
     else if (n == "gap") b = 3 * 8 * N;
     else if (n == "apply") b = 2 * 8 * N;
+    else if (n == "init") b = 4 * 8 * N;     // mean of init1 and init2 (the tile kernels)
     else if (n == "iteration") b = 32 * 8 * N;
   } else if (h->kind == KIND_STENCIL) {
     // fused schedule: every vector read / written once per launch
