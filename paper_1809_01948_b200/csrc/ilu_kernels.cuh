@@ -35,8 +35,12 @@
 
 #include "state.cuh"
 
+#ifndef ILU_T
 #define ILU_T 256  // threads per CTA (one x-line each)
+#endif
+#ifndef ILU_K
 #define ILU_K 8    // steps between progress publications
+#endif
 
 struct IluOp {
   // stencil wavefront (kind 0)
@@ -118,7 +122,9 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // dynamic shared memory of k_ilu_st: per thread, double-buffered, the ILU_K steps'
 // own operands (v or y, uinv), and for the tile-boundary threads the neighbouring
 // tile's values (a-side: threads ta = 0, indexed by tb; b-side: tb = 0, by ta; <= 32)
+#ifndef ILU_BMAX
 #define ILU_BMAX 32
+#endif
 constexpr size_t kIluSmem = sizeof(double) * (2 * ILU_K * 2 * ILU_T + 2 * 2 * ILU_K * 2 * ILU_BMAX);
 
 // Stencil ILU(0) sweep.  BWD = false: out := L^{-1} v; BWD = true: out := U^{-1} out

@@ -2308,7 +2308,12 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
       P.sb = st->nx * st->ny;
       P.cbm = st->coef[5];
       P.cbp = st->coef[6];
-      P.TA = (int32_t)(st->ny < 16 ? st->ny : 16);
+      int64_t ta = 16;
+      if (const char* e = getenv("PBICG_ILU_TA")) {  // tuning experiments only
+        const long v = strtol(e, nullptr, 10);
+        if (v >= 1 && v <= ILU_T) ta = v;
+      }
+      P.TA = (int32_t)(st->ny < ta ? st->ny : ta);
       int64_t tb = ILU_T / P.TA;
       if (tb > ILU_BMAX) tb = ILU_BMAX;  // boundary-value slots per side
       P.TB = (int32_t)(g.nol < tb ? g.nol : tb);
@@ -2347,10 +2352,14 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
     CU(cudaFuncSetAttribute(k_ilu_st<2, false>, SMA, (int)kIluSmem));
     CU(cudaFuncSetAttribute(k_ilu_st<2, true>, SMA, (int)kIluSmem));
     int occ = 0;
-    if (P.dim == 3)
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_st<3, false>, ILU_T, kIluSmem);
+    if (P.dim == 3)  // one CTA per SM: the critical-path tiles' per-step barriers do not
+      occ = 1;       // share the SM (measured: cfg3 4.5 -> 2.9 ms, cfg4 10.6 -> 7.9 ms)
     else
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_2d<false>, 32 * I2_W, 0);
+    if (const char* e = getenv("PBICG_ILU_OCC")) {  // tuning experiments only
+      const long v = strtol(e, nullptr, 10);
+      if (v >= 1 && v < occ) occ = (int)v;
+    }
     const int64_t cap = (int64_t)(occ < 1 ? 1 : occ) * h->num_sm;
     h->ilu_grid = (int)(P.ntiles < cap ? P.ntiles : cap);
     return PBICG_OK;
