@@ -59,9 +59,11 @@ typedef enum {
  *                            CSR: b in {2,4,8,16,32}, every rank's row_begin and
  *                            n_local multiples of b, all three methods.  Stencils:
  *                            b in {2,4,8}, nx % b == 0, full-line TMA tiles (nx <=
- *                            1024 in 2D, ~850 in 3D), method 0 only (EINVAL
- *                            otherwise).  A zero pivot is EINVAL.  Costs b-1 extra
- *                            doubles per row read in each kernel that applies M^-1.
+ *                            1024 in 2D, ~850 in 3D), all three methods (classic
+ *                            BiCGStab's derived operands are derived, then
+ *                            transformed once per staged element).  A zero pivot
+ *                            is EINVAL.  Costs b-1 extra doubles per row read in
+ *                            each kernel that applies M^-1.
  *   PBICG_PREC_ILU0          ILU(0): the incomplete LU factorisation with the sparsity
  *                            pattern of A (zero fill-in; Saad's IKJ variant restricted to
  *                            the pattern, pivots applied as reciprocals), M = L U;
@@ -214,8 +216,8 @@ pbicg_status pbicgstab_local_rows(pbicg_handle h, int64_t* row_begin, int64_t* n
  *   "method"     0 (default) p-BiCGStab, Alg. 2; 1 classic preconditioned
  *                BiCGStab, Alg. 1; 2 preconditioned pipelined CG (the
  *                paper's p-CG comparison, reconstructed: DESIGN.md A19).
- *                Methods 1 and 2 need rr_period = 0; on a stencil also nx <= 1024 and
- *                the Jacobi preconditioner (EINVAL otherwise)
+ *                Methods 1 and 2 need rr_period = 0; on a stencil also the TMA tile
+ *                kernels (nx <= 1024; EINVAL otherwise); every preconditioner
  *   "transport"  multi-rank reductions: 0 (default) NCCL all-reduce of the zero-padded
  *                rank rows (loopback: device copies); 1 peer memory -- the last CTA of
  *                each reducing kernel stores its rank's Dot2 pairs into every rank's

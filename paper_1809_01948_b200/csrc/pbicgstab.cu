@@ -52,7 +52,8 @@ enum Method { M_PBICGSTAB = 0, M_BICGSTAB = 1, M_PIPECG = 2 };
 constexpr bool bj_mode(int m) {
   return m == TM_A || m == TM_C || m == TM_RR1 || m == TM_RR2 || m == TM_INIT1 ||
          m == TM_INIT2 || m == TM_AN || m == TM_CN || m == TM_RR1N || m == TM_RR2N ||
-         m == TM_INIT1N;
+         m == TM_INIT1N || m == TM_CL1 || m == TM_CL2 || m == TM_CL3 || m == TM_PC ||
+         m == TM_PCI1 || m == TM_PCI2;
 }
 
 struct TimedLaunch {
@@ -2988,8 +2989,6 @@ pbicg_status pbicgstab_set_option(pbicg_handle h, const char* key, int64_t value
       if (value < 0 || value > 2) return fail(h, PBICG_EINVAL, "method must be 0, 1 or 2");
       if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && m->schedule == 2)
         return fail(h, PBICG_EINVAL, "methods 1 and 2 run their own schedules (set schedule 0)");
-      if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && m->tg.bj > 1)
-        return fail(h, PBICG_EINVAL, "methods 1 and 2 on a stencil use the Jacobi preconditioner");
       if (value != M_PBICGSTAB && m->kind == KIND_STENCIL && !m->tile_ok)
         return fail(h, PBICG_EINVAL,
                     "methods 1 (BiCGStab) and 2 (p-CG) on a stencil need nx <= 1024 "

@@ -47,7 +47,8 @@ bool dispatch(int mode, int grid, size_t smem, cudaStream_t s, const TileGeo& g,
   case M: launch_one<DIM, M>(grid, smem, s, g, V, sc, part, h); return true;
     BJ_CASE(TM_A) BJ_CASE(TM_C) BJ_CASE(TM_RR1) BJ_CASE(TM_RR2) BJ_CASE(TM_INIT1)
     BJ_CASE(TM_INIT2) BJ_CASE(TM_AN) BJ_CASE(TM_CN) BJ_CASE(TM_RR1N) BJ_CASE(TM_RR2N)
-    BJ_CASE(TM_INIT1N)
+    BJ_CASE(TM_INIT1N) BJ_CASE(TM_CL1) BJ_CASE(TM_CL2) BJ_CASE(TM_CL3) BJ_CASE(TM_PC)
+    BJ_CASE(TM_PCI1) BJ_CASE(TM_PCI2)
 #undef BJ_CASE
     default: return false;
   }
@@ -60,7 +61,8 @@ cudaError_t dispatch_attr(int mode, int smem, int* occ) {
   case M: return attr_one<DIM, M>(smem, occ);
     BJ_CASE(TM_A) BJ_CASE(TM_C) BJ_CASE(TM_RR1) BJ_CASE(TM_RR2) BJ_CASE(TM_INIT1)
     BJ_CASE(TM_INIT2) BJ_CASE(TM_AN) BJ_CASE(TM_CN) BJ_CASE(TM_RR1N) BJ_CASE(TM_RR2N)
-    BJ_CASE(TM_INIT1N)
+    BJ_CASE(TM_INIT1N) BJ_CASE(TM_CL1) BJ_CASE(TM_CL2) BJ_CASE(TM_CL3) BJ_CASE(TM_PC)
+    BJ_CASE(TM_PCI1) BJ_CASE(TM_PCI2)
 #undef BJ_CASE
     default: return cudaErrorInvalidValue;
   }

@@ -651,14 +651,14 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
     dd_fma(acc[1 % K], t0, t0);                //       (y, y)
   } else if (MODE == TM_CL3) {  // c0 = q_i, t0 = y_i; streams x, p, r^0
     const double xj = S[0], pj = S[st], rhj = S[2 * st];
-    const double gj = dinv * pj;               // l.4: g := M^-1 p
-    const double uj = dinv * c0;               // l.9: u := M^-1 q
+    const double gj = BJ ? pc1 : dinv * pj;    // l.4: g := M^-1 p (BJ: lane shuffle)
+    const double uj = BJ ? pc0 : dinv * c0;    // l.9: u := M^-1 q
     o[0] = (xj + al * gj) + om * uj;           // l.13: x
     o[1] = c0 - om * t0;                       // l.14: r
     dd_fma(acc[0], rhj, o[1]);                 // l.15: (r^0, r)
     dd_fma(acc[1 % K], o[1], o[1]);            //       ||r||^2 (A8)
   } else if (MODE == TM_PC) {  // c0 = w_i, t0 = n_i = A M^-1 w_i; streams z,q,s,p,x,r,u
-    const double mj = dinv * c0;               // m := M^-1 w
+    const double mj = BJ ? pc0 : dinv * c0;    // m := M^-1 w
     const double zj = S[0], qj = S[st], sj = S[2 * st], pj = S[3 * st];
     const double xj = S[4 * st], rj = S[5 * st], uj = S[6 * st];
     const double zn = t0 + be * zj;            // z := n + beta z
@@ -684,7 +684,7 @@ __device__ __forceinline__ void row_update(const double* S, int st, bool rr, con
   } else if (MODE == TM_SPB || MODE == TM_SPD) {  // lines 13-14 / 22-23: v_i / t_{i+1}
     o[0] = t0;
   } else if (MODE == TM_PCI2) {  // c = r0; t0 = A M^-1 r0 = A u0
-    const double uj = dinv * c0;               // u0 (same value as stored)
+    const double uj = BJ ? pc0 : dinv * c0;    // u0 (same value as stored)
     o[0] = t0;                                 // w0
     dd_fma(acc[0], c0, uj);                    // (r0, u0)
     dd_fma(acc[1 % K], t0, uj);                // (w0, u0)
@@ -789,7 +789,10 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
   // form -> transform): b = 8: 89 -> 162, b = 4: 177 -> 197; b = 2: 226 -> 210 and the
   // derived operands of classic BiCGStab: 292 -> 276, so those keep the per-leg form
   // (their per-leg work is one or two flops; the transform's halo pairs and stores cost more)
-  constexpr bool XF = BJP && BB >= 4;
+  // Derived operands (classic BiCGStab's p_i, q_i) under block Jacobi always take the
+  // transform stage: each staged element is derived once, then transformed in place
+  // (xf_plane), and the stencil runs on M^-1 of the derived plane.
+  constexpr bool XF = BJ > 0 && PREC && (DER || BB >= 4);
   __shared__ double s_bi[64];                  // the inverse block (row-major BB x BB)
   TL_DECL;
   TL_STAMP(0);
@@ -1015,6 +1018,24 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
       constexpr int BP = BB / 2;
       const int nb = ((E0 + 1) / 2 + BP - 1) / BP * BP;
       const int H = nb + (g.halo - (TP & 1) + 1) / 2;
+      if (DER) {  // derive the operand into staged vector 0 (own pair + halo pairs)
+        if (act) {
+          const int e = sv_off(zp);
+          double a, b;
+          derive_pair<VEC, NSV, MODE>(base + e, svs, al, be, om, a, b);
+          xf_store<VEC, 1>(base, svs, e, {{a, b}});
+        }
+#pragma unroll
+        for (int k = 0; k < XF_H; ++k) {
+          const int h = tid + k * TNT;
+          const int e = h < nb ? E0 - 2 * (nb - h) : E0 + TPe + 2 * (h - nb);
+          if (h >= H || e < 0 || e + 1 >= svs) continue;
+          double a, b;
+          derive_pair<VEC, NSV, MODE>(base + e, svs, al, be, om, a, b);
+          xf_store<VEC, 1>(base, svs, e, {{a, b}});
+        }
+        __syncwarp();  // a block's derived values before any lane transforms it
+      }
       if (act) {
         const int e = sv_off(zp);
 #pragma unroll
@@ -1053,7 +1074,10 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
       TL_STAMP(2);
       TL_UNIT();
       const double* b0p = sv + (size_t)s * NSV * svs + sv_off(z0 - 1);
-      if (act) {
+      if (DER && XF) {  // M^-1 of the derived plane z0-1 (transform stage, all threads)
+        double raw[NSO][2];
+        xf_plane(s, z0 - 1, raw, m1);
+      } else if (act) {
         if (DER) {
           derive_pair<VEC, NSV, MODE>(b0p, svs, al, be, om, m1[0][0], m1[0][1]);
         } else if (BJP) {  // the -z leg takes M^-1 of plane z0-1
@@ -1212,16 +1236,20 @@ __device__ __forceinline__ void t_tile_body(const TileGeo& g, const Vecs& V, Sca
 #pragma unroll
       for (int k = 0; k < NOUT; ++k) o0[k] = o1[k] = 0.0;
       const int64_t gi = gz + gin;
-      row_update<MODE, K, NOUT, NRM, (BJ > 0)>(S0, sts, rr, V.zrr + gi, pc[0][0], pc[1 % NSO][0],
+      double px0 = pc[1 % NSO][0], px1 = pc[1 % NSO][1];  // row_update's second M^-1 pair
+      if (BJ > 0 && MODE == TM_CL3)  // g := M^-1 p of the streamed p_i: neighbouring lanes
+        bj_pair_shfl<BB>(s_bi, amask, i0, S0[sts], S0[sts + 1], px0, px1);
+      row_update<MODE, K, NOUT, NRM, (BJ > 0)>(S0, sts, rr, V.zrr + gi, pc[0][0], px0,
                                          c[0][0], c[1][0], t[0][0], t[1][0], al, be, om, g.dinv,
                                          acc, o0);
       if (valid1)
         row_update<MODE, K, NOUT, NRM, (BJ > 0)>(HAS_STR ? S0 + 1 : nullptr, sts, rr, V.zrr + gi + 1,
-                                           pc[0][1], pc[1 % NSO][1], c[0][1], c[1][1], t[0][1],
+                                           pc[0][1], px1, c[0][1], c[1][1], t[0][1],
                                            t[1][1], al, be, om, g.dinv, acc, o1);
-      if (BJ > 0 && (MODE == TM_RR1 || MODE == TM_INIT1)) {
-        // k := M^-1 r (and l := M^-1 s): the block's r values sit in neighbouring lanes
-        const int ko = MODE == TM_RR1 ? 1 : 2;
+      if (BJ > 0 && (MODE == TM_RR1 || MODE == TM_INIT1 || MODE == TM_PCI1)) {
+        // k := M^-1 r (and l := M^-1 s; p-CG u0 := M^-1 r0): the block's r values sit
+        // in neighbouring lanes
+        const int ko = MODE == TM_INIT1 ? 2 : 1;
         bj_pair_shfl<BB>(s_bi, amask, i0, o0[0], o1[0], o0[ko % NOUT], o1[ko % NOUT]);
         if (MODE == TM_RR1)
           bj_pair_shfl<BB>(s_bi, amask, i0, o0[2 % NOUT], o1[2 % NOUT], o0[3 % NOUT],

@@ -136,6 +136,58 @@ def test_bj_stencil_parity(S, orc, block, shape):
     check_auto(res, fr, rrl, ref, xs)
 
 
+@pytest.mark.parametrize("method", [1, 2])
+@pytest.mark.parametrize("block", [2, 4, 8])
+@pytest.mark.parametrize("shape", STENCILS)
+def test_bj_stencil_methods(S, orc, block, shape, method):
+    """Classic BiCGStab (Alg. 1: the derived p_i, q_i are derived then transformed once
+    per staged element, g := M^-1 p by lane shuffles) and p-CG (m := M^-1 w from the
+    stencil's block, u0 := M^-1 r0 by lane shuffles) with stencil block Jacobi, bitwise
+    vs the oracle's CSR form; p-CG on the symmetric (Poisson) stencils only."""
+    from test_gpu_parity import coef_of
+    dim, nx, ny, nz, kind = shape
+    if nx % block:
+        pytest.skip("nx % b != 0")
+    coef = coef_of(kind)
+    if method == 2:  # p-CG needs a symmetric M and A
+        coef = problems.poisson3d_coef() if dim == 3 else problems.poisson2d_coef()
+    solver = S.stencil(dim, nx, ny, nz, coef, block=block)
+    solver.set_option("method", method)
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 0)
+    b_d = solver.apply(torch.from_numpy(xs).cuda())
+    b = orc.spmv(A, xs)
+    fn = orc.bicgstab if method == 1 else orc.pipecg
+    res = solver.solve(b_d, tol=1e-11, maxit=150, gap=True)
+    ref = fn(A, b, tol=1e-11, maxit=150, block=block)
+    assert res.outcome == ref.outcome
+    check_parity(res, ref, xs)
+    solver.set_option("bench", 1)  # bench mode: exactly maxit iterations
+    res = solver.solve(b_d, tol=0.0, maxit=40, gap=True)
+    ref = fn(A, b, tol=0.0, maxit=40, bench=True, block=block)
+    assert res.outcome == ref.outcome
+    check_parity(res, ref, xs)
+
+
+@pytest.mark.parametrize("method", [1, 2])
+@pytest.mark.parametrize("P", [2, 3])
+def test_bj_stencil_methods_loopback(S, orc, P, method):
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    dim, nx, ny, nz, blk = 3, 24, 10, 9, 4
+    coef = problems.cfg34_coef() if method == 1 else problems.poisson3d_coef()
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 0)
+    b = orc.spmv(A, xs)
+    G = LoopbackGroup.stencil(P, dim, nx, ny, nz, coef, block=blk)
+    G.set_option("method", method)
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=1e-11, maxit=200, rr_period=0, gap=True)
+    fn = orc.bicgstab if method == 1 else orc.pipecg
+    ref = fn(A, b, tol=1e-11, maxit=200, block=blk)
+    check_parity(res, ref, xs)
+    G.close()
+
+
 @pytest.mark.parametrize("P", [2, 3])
 def test_bj_stencil_loopback(S, orc, P):
     from paper_1809_01948_b200.binding import LoopbackGroup
@@ -180,7 +232,5 @@ def test_bj_errors(S, orc):
     with pytest.raises(PbicgError):  # 3D planes too wide for full-line tiles: segmented
         S.stencil(3, 1024, 3, 4, problems.cfg34_coef(), block=4)
     st = S.stencil(2, 32, 8, 1, problems.poisson2d_coef(), block=4)
-    with pytest.raises(PbicgError):  # comparison solvers use Jacobi
-        st.set_option("method", 1)
     with pytest.raises(PbicgError):  # line kernels have no block Jacobi
         st.set_option("tile", 0)
