@@ -26,8 +26,11 @@
 template <int M> struct LtTraits;
 template <> struct LtTraits<TM_SPB> { enum { NSV = 1, NST = 0, NOUT = 1, K = 0, SVR = 4, SD = 1, NP = 4 }; };
 template <> struct LtTraits<TM_SPD> { enum { NSV = 1, NST = 0, NOUT = 1, K = 0, SVR = 4, SD = 1, NP = 4 }; };
-template <> struct LtTraits<TM_RR1> { enum { NSV = 2, NST = 2, NOUT = 4, K = 3, SVR = 3, SD = 2, NP = 2 }; };
-template <> struct LtTraits<TM_RR2> { enum { NSV = 2, NST = 1, NOUT = 2, K = 5, SVR = 3, SD = 3, NP = 2 }; };
+#ifndef PBICG_RR_NP  // row pairs per thread of the replacement step (experiments: -D)
+#define PBICG_RR_NP 2
+#endif
+template <> struct LtTraits<TM_RR1> { enum { NSV = 2, NST = 2, NOUT = 4, K = 3, SVR = 3, SD = 2, NP = PBICG_RR_NP }; };
+template <> struct LtTraits<TM_RR2> { enum { NSV = 2, NST = 1, NOUT = 2, K = 5, SVR = 3, SD = 3, NP = PBICG_RR_NP }; };
 
 struct SpmvGeo {
   int32_t TY, ncols, chunk, units, sv_stride, st_stride;

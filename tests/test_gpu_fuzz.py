@@ -247,3 +247,45 @@ def test_fuzz_stencil_block_jacobi(orc, seed):
     noise_floor_parity(_rank0(S), res, ref, xs, tag=f" stencil_bj[{seed}]")
     S.close()
 
+
+
+@pytest.mark.parametrize("seed", range(8 * SCALE))
+def test_fuzz_stencil_block_jacobi_methods(orc, seed):
+    """Classic BiCGStab and p-CG with stencil block Jacobi b = 2 / 4 / 8 (the derived
+    operands' transform stage, the lane-shuffled M^-1 of streamed vectors), 1 or P
+    emulated ranks, random transport, bench or tolerance mode."""
+    from paper_1809_01948_b200 import Solver
+    from paper_1809_01948_b200.binding import LoopbackGroup
+    rng = np.random.default_rng(7000 + seed + OFFSET)
+    block = int(rng.choice([2, 4, 8]))
+    method = int(rng.choice([1, 2]))
+    dim = int(rng.choice([2, 3]))
+    nx = block * int(rng.integers(1, 840 // block if dim == 3 else 1024 // block))
+    ny = int(rng.integers(1, 30 if dim == 3 else 60))
+    nz = int(rng.integers(1, 12)) if dim == 3 else 1
+    coef = rand_coef(rng, dim, spd=(method == 2))
+    A = orc.stencil_csr(dim, nx, ny, nz, coef)
+    if A.n > 400000:
+        pytest.skip("oracle size")
+    xs = problems.x_star(A.n, seed)
+    b = orc.spmv(A, xs)
+    outer = nz if dim == 3 else ny
+    P = int(rng.choice([1, 2, 3])) if outer >= 3 else 1
+    tol = float(rng.choice([0.0, 1e-11]))
+    maxit = int(rng.integers(5, 60))
+    if P == 1:
+        S = Solver.stencil(dim, nx, ny, nz, coef, block=block)
+        S.set_option("graphs", int(rng.integers(0, 2)))
+        bs = S.apply(torch.from_numpy(xs).cuda())
+    else:
+        S = LoopbackGroup.stencil(P, dim, nx, ny, nz, coef, block=block)
+        S.set_option("transport", int(rng.integers(0, 2)))
+        bs = S.apply(S.split(torch.from_numpy(xs).cuda()))
+    S.set_option("method", method)
+    S.set_option("bench", int(tol == 0.0))
+    res = S.solve(bs, tol=tol, maxit=maxit, rr_period=0, gap=True)
+    fn = orc.bicgstab if method == 1 else orc.pipecg
+    ref = fn(A, b, tol=tol, maxit=maxit, bench=tol == 0.0, block=block)
+    assert res.outcome == ref.outcome
+    noise_floor_parity(None, res, ref, xs, tag=f" stencil_bj_m{method}[{seed}]")
+    S.close()
