@@ -52,7 +52,7 @@ struct IluOp {
   int32_t TA, TB;         // line tile
   int32_t nta, ntb, ntiles;
   const int32_t* order;   // [ntiles] tile ids (ta + nta tb) in topological order (diagonals)
-  unsigned long long* prog_f;  // [ntiles] forward progress: (epoch << 32) | x-count done
+  unsigned long long* prog_f;  // [ntiles] forward progress: (epoch << 32) | steps done (k_ilu_st)
   unsigned long long* prog_b;  // [ntiles] backward progress
   // general CSR (kind 1): strictly lower / upper parts as column-major ELL in row order
   int64_t n;
@@ -191,12 +191,21 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
       i = base + (BWD ? P.nx - 1 - xs : xs);
       return true;
     };
-    auto wait_pred = [&](int upto) {  // predecessors' x-count >= min(nx, upto)
+    // Progress = steps a tile has completed (its end publishes ~0u).  A boundary line
+    // of this tile at step s' (< upto) reads the predecessor's edge line at the same x,
+    // which that tile computes at its step s' + TA - 1 (a-side: its thread TA - 1 of the
+    // same b line, x = s' - tb both ways) or s' + TB - 1 (b-side), whatever the line:
+    // so the predecessors must have completed upto + TA - 1 / upto + TB - 1 steps.
+    auto wait_pred = [&](int upto) {
       if (tid == 0) {
-        const unsigned long long need =
-            ep | (unsigned long long)((int64_t)upto < P.nx ? upto : P.nx);
-        if (pa) while (ld_acq_gpu(pa) < need) __nanosleep(20);
-        if (pb) while (ld_acq_gpu(pb) < need) __nanosleep(20);
+        if (pa) {
+          const unsigned long long need = ep | (unsigned long long)(upto + P.TA - 1);
+          while (ld_acq_gpu(pa) < need) __nanosleep(20);
+        }
+        if (pb) {
+          const unsigned long long need = ep | (unsigned long long)(upto + P.TB - 1);
+          while (ld_acq_gpu(pb) < need) __nanosleep(20);
+        }
       }
       __syncthreads();
     };
@@ -297,12 +306,10 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
         __syncthreads();
       }
       if (more) park_bnd(cur ^ 1);  // the next block's boundary loads have landed by now
-      if (tid == 0) {  // x-count every line of the tile has finished after step s1 - 1
-        int64_t done = (int64_t)s1 - (na_t - 1) - (nb_t - 1);
-        if (done < 0) done = 0;
-        if (done > P.nx) done = P.nx;
+      if (tid == 0) {  // steps completed (every line's rows of steps < s1 are stored)
+        const unsigned long long done = more ? (unsigned long long)s1 : 0xFFFFFFFFull;
         __threadfence();
-        st_rel_gpu(prog + tile, ep | (unsigned long long)done);
+        st_rel_gpu(prog + tile, ep | done);
       }
       cur ^= 1;
     }
