@@ -125,14 +125,24 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 #ifndef ILU_BMAX
 #define ILU_BMAX 32
 #endif
-constexpr size_t kIluSmem = sizeof(double) * (2 * ILU_K * 2 * ILU_T + 2 * 2 * ILU_K * 2 * ILU_BMAX);
+// Global memory is touched only by "transposed" warp instructions: ILU_K consecutive
+// lanes cover the ILU_K consecutive x of one line's block (one 64-byte run), so a warp
+// instruction touches 32 / ILU_K lines instead of 32 (a wavefront's rows are never
+// contiguous: one row per line).  kIluPfs pads the per-thread operand rows so those
+// lanes' shared-memory slots (stride 2 * kIluPfs per step) fall into distinct banks.
+static_assert(ILU_K == 4 || ILU_K == 8 || ILU_K == 16, "ILU_K lanes per line must divide a warp");
+constexpr int kIluLpi = 32 / ILU_K;             // lines per transposed warp instruction
+constexpr int kIluPfs = ILU_T + kIluLpi / 2;    // operand row stride (2 * kIluPfs = kIluLpi mod 16)
+constexpr size_t kIluSmem = sizeof(double) * (2 * ILU_K * 2 * kIluPfs + 2 * 2 * ILU_K * 2 * ILU_BMAX);
 
 // Stencil ILU(0) sweep.  BWD = false: out := L^{-1} v; BWD = true: out := U^{-1} out
 // (in place; v unused).  Operands are prefetched one block of ILU_K steps ahead
-// (own values by cp.async into shared memory; the neighbouring tiles' boundary values,
-// written during this kernel, by L2 loads into registers once that tile's progress
-// covers the next block, parked in shared memory at the end of the current block), so
-// a step costs shared-memory traffic, the row's arithmetic and one barrier.
+// (own values by transposed cp.async into shared memory; the neighbouring tiles'
+// boundary values, written during this kernel, by L2 loads into registers once that
+// tile's progress covers the next block, parked in shared memory at the end of the
+// current block), a row's result replaces its operand in shared memory and the block's
+// results leave by transposed stores at the end of the block, so a step costs
+// shared-memory traffic, the row's arithmetic and one barrier.
 template <int DIM, bool BWD>
 __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
                                                   const double* __restrict__ v,
@@ -141,8 +151,8 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
   __shared__ double pub[2][2][ILU_T];  // [step parity][+a / +b consumer][thread]
   __shared__ int s_tile;
   extern __shared__ __align__(16) double ilu_smem[];
-  double* pf = ilu_smem;                                   // [2][ILU_K][2][ILU_T]
-  double* pfa = ilu_smem + 2 * ILU_K * 2 * ILU_T;          // [2][ILU_K][2][ILU_BMAX]
+  double* pf = ilu_smem;                                   // [2][ILU_K][2][kIluPfs]
+  double* pfa = ilu_smem + 2 * ILU_K * 2 * kIluPfs;        // [2][ILU_K][2][ILU_BMAX]
   double* pfb = pfa + 2 * ILU_K * 2 * ILU_BMAX;            // [2][ILU_K][2][ILU_BMAX]
   unsigned int* ctr = P.ctr + (BWD ? 4 : 0);
   unsigned long long* prog = BWD ? P.prog_b : P.prog_f;
@@ -209,29 +219,60 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
       }
       __syncthreads();
     };
+    // transposed access: instruction j of a block serves the lines of threads
+    // tj0 + j * kIluLpi (this warp's), this lane step kk of the block
+    const int kk = tid % ILU_K, tj0 = (tid & ~31) + (tid & 31) / ILU_K;
+    int64_t jbase[ILU_K];
+    int jskew[ILU_K];
+#pragma unroll
+    for (int j = 0; j < ILU_K; ++j) {
+      const int tj = tj0 + j * kIluLpi;
+      const int tja = tj % P.TA, tjb = tj / P.TA;
+      const bool ok = tja < na_t && tjb < nb_t;
+      jbase[j] = (a0 + (BWD ? na_t - 1 - tja : tja)) * P.sa + (b0 + (BWD ? nb_t - 1 - tjb : tjb)) * P.sb;
+      jskew[j] = ok ? tja + tjb : (1 << 28);  // idle lines: x < 0 always
+    }
     // own operands of block [sb, sb + ILU_K) into buffer q (asynchronous copies)
     auto fetch_own = [&](int sb, int q) {
-      for (int k = 0; k < ILU_K; ++k) {
-        int64_t i;
-        if (!row_of(sb + k, i)) continue;
-        double* d = pf + ((size_t)(q * ILU_K + k) * 2) * ILU_T + tid;
-        cp_async8(d, BWD ? out + i : v + i);
-        cp_async8(d + ILU_T, P.uinv + i);
-        if (!BWD) {  // the neighbours' pivots (static) ride along
+      double* dq = pf + ((size_t)(q * ILU_K + kk) * 2) * kIluPfs + tj0;
+#pragma unroll
+      for (int j = 0; j < ILU_K; ++j) {
+        const int xs = sb + kk - jskew[j];
+        if (xs < 0 || xs >= P.nx) continue;
+        const int64_t i = jbase[j] + (BWD ? P.nx - 1 - xs : xs);
+        cp_async8(dq + j * kIluLpi, BWD ? out + i : v + i);
+        cp_async8(dq + j * kIluLpi + kIluPfs, P.uinv + i);
+      }
+      if (!BWD && (bnd_a || bnd_b)) {  // the neighbours' pivots (static) ride along
+        for (int k = 0; k < ILU_K; ++k) {
+          int64_t i;
+          if (!row_of(sb + k, i)) continue;
           if (bnd_a) cp_async8(pfa + ((size_t)(q * ILU_K + k) * 2 + 1) * ILU_BMAX + tb, P.uinv + i + da);
           if (bnd_b) cp_async8(pfb + ((size_t)(q * ILU_K + k) * 2 + 1) * ILU_BMAX + ta, P.uinv + i + db);
         }
       }
       cp_async_commit();
     };
+    // results of block [sb, sb + ILU_K) (left in the operand slots of buffer q) -> out
+    auto flush_own = [&](int sb, int q) {
+      const double* dq = pf + ((size_t)(q * ILU_K + kk) * 2) * kIluPfs + tj0;
+#pragma unroll
+      for (int j = 0; j < ILU_K; ++j) {
+        const int xs = sb + kk - jskew[j];
+        if (xs < 0 || xs >= P.nx) continue;
+        out[jbase[j] + (BWD ? P.nx - 1 - xs : xs)] = dq[j * kIluLpi];
+      }
+    };
     // the neighbouring tiles' values of block [sb, sb + ILU_K) (written in this kernel:
     // L2 loads) -> registers; parked in buffer q by park_bnd
     double ya[ILU_K], yb[ILU_K];
     auto load_bnd = [&](int sb) {
 #pragma unroll
+      for (int k = 0; k < ILU_K; ++k) ya[k] = yb[k] = 0.0;
+      if (!(bnd_a || bnd_b)) return;
+#pragma unroll
       for (int k = 0; k < ILU_K; ++k) {
         int64_t i;
-        ya[k] = yb[k] = 0.0;
         if (!row_of(sb + k, i)) continue;
         if (bnd_a) ya[k] = __ldcg(out + i + da);
         if (bnd_b) yb[k] = __ldcg(out + i + db);
@@ -270,11 +311,11 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
         if (row_of(s, i)) {
           const int xs = s - ta - tb;
           const int q = (s - 1) & 1;
-          const double* d = pf + ((size_t)(cur * ILU_K + k) * 2) * ILU_T + tid;
+          double* d = pf + ((size_t)(cur * ILU_K + k) * 2) * kIluPfs + tid;
           const size_t ob = ((size_t)(cur * ILU_K + k) * 2) * ILU_BMAX;
           // ascending column order: forward -b, -a, -x; backward +x, +a, +b
           double acc = d[0];
-          const double ui = d[ILU_T];
+          const double ui = d[kIluPfs];
           if (!BWD) {
             if (has_b) {
               const double term = own_b ? pub[q][1][tid - P.TA]
@@ -287,7 +328,7 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
               acc = acc - term;
             }
             if (xs > 0) acc = acc - (cx * uprev) * prev;
-            out[i] = acc;
+            d[0] = acc;  // leaves with the block's transposed stores
             pub[s & 1][0][tid] = (ca * ui) * acc;  // the +a neighbour's -a term
             pub[s & 1][1][tid] = (cb * ui) * acc;  // the +b neighbour's -b term
             prev = acc;
@@ -297,7 +338,7 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
             if (has_a) acc = acc - (own_a ? pub[q][0][tid - 1] : ca * pfa[ob + tb]);
             if (has_b) acc = acc - (own_b ? pub[q][1][tid - P.TA] : cb * pfb[ob + ta]);
             const double xi = acc * ui;
-            out[i] = xi;
+            d[0] = xi;
             pub[s & 1][0][tid] = ca * xi;
             pub[s & 1][1][tid] = cb * xi;
             prev = xi;
@@ -305,7 +346,9 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
         }
         __syncthreads();
       }
+      flush_own(s0, cur);
       if (more) park_bnd(cur ^ 1);  // the next block's boundary loads have landed by now
+      __syncthreads();  // the block's rows are stored (and buffer cur is free again)
       if (tid == 0) {  // steps completed (every line's rows of steps < s1 are stored)
         const unsigned long long done = more ? (unsigned long long)s1 : 0xFFFFFFFFull;
         __threadfence();
