@@ -41,6 +41,9 @@
 #ifndef ILU_K
 #define ILU_K 8    // steps between progress publications
 #endif
+#ifndef ILU_OCC3
+#define ILU_OCC3 1  // CTAs per SM of the 3D sweeps (resident tiles = ILU_OCC3 x SMs)
+#endif
 
 struct IluOp {
   // stencil wavefront (kind 0)
@@ -119,9 +122,11 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* g) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-// dynamic shared memory of k_ilu_st: per thread, double-buffered, the ILU_K steps'
-// own operands (v or y, uinv), and for the tile-boundary threads the neighbouring
-// tile's values (a-side: threads ta = 0, indexed by tb; b-side: tb = 0, by ta; <= 32)
+// dynamic shared memory of k_ilu_st: per thread, double-buffered, the ILU_K steps' own
+// operands (v or y, uinv; the row's result replaces the first), and the two term rings
+// (-a / -b terms by step within the block): a column per thread plus, double-buffered,
+// ILU_BMAX columns for the neighbouring tile's values (a-side: lines ta = 0, indexed
+// by tb; b-side: tb = 0, by ta)
 #ifndef ILU_BMAX
 #define ILU_BMAX 32
 #endif
@@ -131,38 +136,51 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // contiguous: one row per line).  kIluPfs pads the per-thread operand rows so those
 // lanes' shared-memory slots (stride 2 * kIluPfs per step) fall into distinct banks.
 static_assert(ILU_K == 4 || ILU_K == 8 || ILU_K == 16, "ILU_K lanes per line must divide a warp");
+static_assert(ILU_T >= 64 && ILU_T % 32 == 0, "warps 0 and 1 serve the two tile boundaries");
 constexpr int kIluLpi = 32 / ILU_K;             // lines per transposed warp instruction
 constexpr int kIluPfs = ILU_T + kIluLpi / 2;    // operand row stride (2 * kIluPfs = kIluLpi mod 16)
-constexpr size_t kIluSmem = sizeof(double) * (2 * ILU_K * 2 * kIluPfs + 2 * 2 * ILU_K * 2 * ILU_BMAX);
+constexpr int kIluRs = ILU_T + 2 * ILU_BMAX + kIluLpi;  // term ring row stride (= kIluLpi mod 16)
+constexpr int kIluZc = ILU_T + 2 * ILU_BMAX;     // ring column of zeros (the terms of missing legs)
+constexpr int kIluNbj = ILU_BMAX / kIluLpi;     // transposed instructions per boundary block
+constexpr size_t kIluSmem = sizeof(double) * (2 * ILU_K * 2 * kIluPfs + 2 * ILU_K * kIluRs);
 
 // Stencil ILU(0) sweep.  BWD = false: out := L^{-1} v; BWD = true: out := U^{-1} out
-// (in place; v unused).  Operands are prefetched one block of ILU_K steps ahead
-// (own values by transposed cp.async into shared memory; the neighbouring tiles'
-// boundary values, written during this kernel, by L2 loads into registers once that
-// tile's progress covers the next block, parked in shared memory at the end of the
-// current block), a row's result replaces its operand in shared memory and the block's
-// results leave by transposed stores at the end of the block, so a step costs
-// shared-memory traffic, the row's arithmetic and one barrier.
+// (in place; v unused).  Operands are prefetched one block of ILU_K steps ahead: own
+// values by transposed cp.async into shared memory; the neighbouring tiles' boundary
+// values (written during this kernel) by transposed L2 loads of warp 0 (a-side) and
+// warp 1 (b-side) once that tile's progress covers the next block, parked as finished
+// terms in the rings before the current block's last barrier.  A row's result replaces
+// its operand in shared memory and the block's results leave by transposed stores, so
+// a step is branch-free: four shared loads, the row's arithmetic (selects for the
+// zero terms of missing legs; idle lanes compute on garbage nobody reads), three shared stores and
+// ONE barrier -- the only CTA barriers of the step loop (a warp's transposed copies
+// and stores serve its own 32 lines, so they need warp-level ordering only, and a
+// block's progress is published after the next block's first barrier).
 template <int DIM, bool BWD>
 __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
                                                   const double* __restrict__ v,
                                                   double* __restrict__ out) {
   if (ilu_skip(sc, gate)) return;
-  __shared__ double pub[2][2][ILU_T];  // [step parity][+a / +b consumer][thread]
   __shared__ int s_tile;
   extern __shared__ __align__(16) double ilu_smem[];
-  double* pf = ilu_smem;                                   // [2][ILU_K][2][kIluPfs]
-  double* pfa = ilu_smem + 2 * ILU_K * 2 * kIluPfs;        // [2][ILU_K][2][ILU_BMAX]
-  double* pfb = pfa + 2 * ILU_K * 2 * ILU_BMAX;            // [2][ILU_K][2][ILU_BMAX]
+  double* pf = ilu_smem;                                  // [2][ILU_K][2][kIluPfs]
+  double* ringA = ilu_smem + 2 * ILU_K * 2 * kIluPfs;     // [ILU_K][kIluRs]
+  double* ringB = ringA + ILU_K * kIluRs;                 // [ILU_K][kIluRs]
   unsigned int* ctr = P.ctr + (BWD ? 4 : 0);
   unsigned long long* prog = BWD ? P.prog_b : P.prog_f;
   const unsigned long long ep = (unsigned long long)ilu_epoch(ctr) << 32;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ta = tid % P.TA, tb = tid / P.TA;
+  const int nx = (int)P.nx;
   // leg coefficients in this direction: "m" legs feed the row from a / b / x - 1
   // (forward) or + 1 (backward)
   const double ca = BWD ? P.cap : P.cam, cb = BWD ? P.cbp : P.cbm, cx = BWD ? P.cxp : P.cxm;
+  // transposed access: instruction j of a block serves the lines of threads
+  // tj0 + j * kIluLpi (this warp's), this lane step kk of the block
+  const int kk = lane % ILU_K, lj = lane / ILU_K, tj0 = (tid & ~31) + lj;
+  if (tid < ILU_K) ringA[tid * kIluRs + kIluZc] = ringB[tid * kIluRs + kIluZc] = 0.0;
   for (;;) {
+    __syncthreads();  // the previous tile's rings and s_tile are no longer read
     if (tid == 0) s_tile = (int)atomicAdd(ctr, 1u);
     __syncthreads();
     const int t = s_tile;
@@ -173,14 +191,18 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
     const int na_t = (int)((P.na - a0) < P.TA ? (P.na - a0) : P.TA);
     const int nb_t = (int)((P.nb - b0) < P.TB ? (P.nb - b0) : P.TB);
     // this thread's line (forward: ascending; backward: mirrored inside the tile)
-    const int la = BWD ? na_t - 1 - ta : ta, lb = BWD ? nb_t - 1 - tb : tb;
     const bool valid = ta < na_t && tb < nb_t;
-    const int64_t a = a0 + la, b = b0 + lb;
+    const int64_t a = a0 + (BWD ? na_t - 1 - ta : ta), b = b0 + (BWD ? nb_t - 1 - tb : tb);
     // does the row have the leg towards the previous line in a / b (the dependency)?
     const bool has_a = BWD ? (a + 1 < P.na) : (a > 0);
     const bool has_b = BWD ? (b + 1 < P.nb) : (b > 0);
-    const bool own_a = ta > 0, own_b = tb > 0;  // neighbour line inside this tile
-    const bool bnd_a = valid && has_a && !own_a, bnd_b = valid && has_b && !own_b;
+    const int skew = valid ? ta + tb : (1 << 28);  // x = s - skew; idle lines: x < 0 always
+    // where this line's -a / -b terms come from: the neighbour thread's ring column, or
+    // (tile-boundary lines) the boundary columns of the block's parity
+    // (a line without that leg reads the zero column)
+    const int srcA = !has_a ? kIluZc : (ta > 0 ? tid - 1 : ILU_T + tb);
+    const int srcB = !has_b ? kIluZc : (tb > 0 ? tid - P.TA : ILU_T + ta);
+    const int bndA = has_a && ta == 0 ? ILU_BMAX : 0, bndB = has_b && tb == 0 ? ILU_BMAX : 0;
     // predecessor tiles (their progress gates the tile-boundary lines)
     const unsigned long long* pa = nullptr;
     const unsigned long long* pb = nullptr;
@@ -191,37 +213,7 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
       if (A > 0) pa = prog + (A - 1) + (int64_t)P.nta * B;
       if (B > 0) pb = prog + A + (int64_t)P.nta * (B - 1);
     }
-    const int64_t base = a * P.sa + b * P.sb;
-    const int steps = (int)P.nx + na_t + nb_t - 2;
-    const int da = BWD ? (int)P.sa : -(int)P.sa;  // offset of the a / b dependency
-    const int64_t db = BWD ? P.sb : -P.sb;
-    auto row_of = [&](int s, int64_t& i) -> bool {  // row of step s; false if idle
-      const int xs = s - ta - tb;
-      if (!valid || xs < 0 || xs >= P.nx) return false;
-      i = base + (BWD ? P.nx - 1 - xs : xs);
-      return true;
-    };
-    // Progress = steps a tile has completed (its end publishes ~0u).  A boundary line
-    // of this tile at step s' (< upto) reads the predecessor's edge line at the same x,
-    // which that tile computes at its step s' + TA - 1 (a-side: its thread TA - 1 of the
-    // same b line, x = s' - tb both ways) or s' + TB - 1 (b-side), whatever the line:
-    // so the predecessors must have completed upto + TA - 1 / upto + TB - 1 steps.
-    auto wait_pred = [&](int upto) {
-      if (tid == 0) {
-        if (pa) {
-          const unsigned long long need = ep | (unsigned long long)(upto + P.TA - 1);
-          while (ld_acq_gpu(pa) < need) __nanosleep(20);
-        }
-        if (pb) {
-          const unsigned long long need = ep | (unsigned long long)(upto + P.TB - 1);
-          while (ld_acq_gpu(pb) < need) __nanosleep(20);
-        }
-      }
-      __syncthreads();
-    };
-    // transposed access: instruction j of a block serves the lines of threads
-    // tj0 + j * kIluLpi (this warp's), this lane step kk of the block
-    const int kk = tid % ILU_K, tj0 = (tid & ~31) + (tid & 31) / ILU_K;
+    const int steps = nx + na_t + nb_t - 2;
     int64_t jbase[ILU_K];
     int jskew[ILU_K];
 #pragma unroll
@@ -230,7 +222,7 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
       const int tja = tj % P.TA, tjb = tj / P.TA;
       const bool ok = tja < na_t && tjb < nb_t;
       jbase[j] = (a0 + (BWD ? na_t - 1 - tja : tja)) * P.sa + (b0 + (BWD ? nb_t - 1 - tjb : tjb)) * P.sb;
-      jskew[j] = ok ? tja + tjb : (1 << 28);  // idle lines: x < 0 always
+      jskew[j] = ok ? tja + tjb : (1 << 28);
     }
     // own operands of block [sb, sb + ILU_K) into buffer q (asynchronous copies)
     auto fetch_own = [&](int sb, int q) {
@@ -238,18 +230,10 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
 #pragma unroll
       for (int j = 0; j < ILU_K; ++j) {
         const int xs = sb + kk - jskew[j];
-        if (xs < 0 || xs >= P.nx) continue;
-        const int64_t i = jbase[j] + (BWD ? P.nx - 1 - xs : xs);
+        if ((unsigned)xs >= (unsigned)nx) continue;
+        const int64_t i = jbase[j] + (BWD ? nx - 1 - xs : xs);
         cp_async8(dq + j * kIluLpi, BWD ? out + i : v + i);
         cp_async8(dq + j * kIluLpi + kIluPfs, P.uinv + i);
-      }
-      if (!BWD && (bnd_a || bnd_b)) {  // the neighbours' pivots (static) ride along
-        for (int k = 0; k < ILU_K; ++k) {
-          int64_t i;
-          if (!row_of(sb + k, i)) continue;
-          if (bnd_a) cp_async8(pfa + ((size_t)(q * ILU_K + k) * 2 + 1) * ILU_BMAX + tb, P.uinv + i + da);
-          if (bnd_b) cp_async8(pfb + ((size_t)(q * ILU_K + k) * 2 + 1) * ILU_BMAX + ta, P.uinv + i + db);
-        }
       }
       cp_async_commit();
     };
@@ -259,104 +243,118 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
 #pragma unroll
       for (int j = 0; j < ILU_K; ++j) {
         const int xs = sb + kk - jskew[j];
-        if (xs < 0 || xs >= P.nx) continue;
-        out[jbase[j] + (BWD ? P.nx - 1 - xs : xs)] = dq[j * kIluLpi];
+        if ((unsigned)xs >= (unsigned)nx) continue;
+        out[jbase[j] + (BWD ? nx - 1 - xs : xs)] = dq[j * kIluLpi];
       }
     };
-    // the neighbouring tiles' values of block [sb, sb + ILU_K) (written in this kernel:
-    // L2 loads) -> registers; parked in buffer q by park_bnd
-    double ya[ILU_K], yb[ILU_K];
-    auto load_bnd = [&](int sb) {
+    // Tile boundaries: warp 0 serves the a-side (lines ta = 0, slot = tb), warp 1 the
+    // b-side (tb = 0, slot = ta), one code path on per-warp data.  A boundary line of
+    // this tile at step s' (< upto) reads the predecessor's edge line at the same x,
+    // which that tile computes at its step s' + TA - 1 (a-side: its thread TA - 1 of the
+    // same b line) or s' + TB - 1 (b-side), whatever the line: so the predecessor must
+    // have completed upto + TA - 1 / upto + TB - 1 steps (progress = completed steps).
+    const bool side_b = warp == 1;
+    const unsigned long long* pp = warp == 0 ? pa : (warp == 1 ? pb : nullptr);
+    const int plag = (side_b ? P.TB : P.TA) - 1;
+    const double sc_ = side_b ? cb : ca;
+    double* sring = (side_b ? ringB : ringA) + ILU_T + lj;
+    const int nslot = side_b ? na_t : nb_t;
+    int64_t sbase[kIluNbj];  // the neighbouring tile's row at x = 0 (forward) / nx - 1
+    if (pp) {
 #pragma unroll
-      for (int k = 0; k < ILU_K; ++k) ya[k] = yb[k] = 0.0;
-      if (!(bnd_a || bnd_b)) return;
+      for (int j = 0; j < kIluNbj; ++j) {
+        const int slot = j * kIluLpi + lj;
+        const int sa_ = side_b ? slot : 0, sb_ = side_b ? 0 : slot;
+        sbase[j] = (a0 + (BWD ? na_t - 1 - sa_ : sa_)) * P.sa + (b0 + (BWD ? nb_t - 1 - sb_ : sb_)) * P.sb +
+                   (side_b ? (BWD ? P.sb : -P.sb) : (BWD ? P.sa : -P.sa));
+      }
+    }
+    double yv[kIluNbj], uv[kIluNbj];
+    auto load_bnd = [&](int sb) {  // block [sb, sb + ILU_K): L2 loads -> registers
+      if (!pp) return;
+      if (lane == 0) {
+        const unsigned long long need = ep | (unsigned long long)(sb + ILU_K + plag);
+        while (ld_acq_gpu(pp) < need) __nanosleep(20);
+      }
+      __syncwarp();
 #pragma unroll
-      for (int k = 0; k < ILU_K; ++k) {
-        int64_t i;
-        if (!row_of(sb + k, i)) continue;
-        if (bnd_a) ya[k] = __ldcg(out + i + da);
-        if (bnd_b) yb[k] = __ldcg(out + i + db);
+      for (int j = 0; j < kIluNbj; ++j) {
+        const int xs = sb + kk - (j * kIluLpi + lj);
+        const bool ok = j * kIluLpi + lj < nslot && (unsigned)xs < (unsigned)nx;
+        const int64_t i = sbase[j] + (BWD ? nx - 1 - xs : xs);
+        yv[j] = ok ? __ldcg(out + i) : 0.0;
+        if (!BWD) uv[j] = ok ? __ldg(P.uinv + i) : 0.0;
       }
     };
-    auto park_bnd = [&](int q) {
+    auto park_bnd = [&](int q) {  // ... -> finished terms in the boundary columns of parity q
+      if (!pp) return;
 #pragma unroll
-      for (int k = 0; k < ILU_K; ++k) {
-        if (bnd_a) pfa[((size_t)(q * ILU_K + k) * 2) * ILU_BMAX + tb] = ya[k];
-        if (bnd_b) pfb[((size_t)(q * ILU_K + k) * 2) * ILU_BMAX + ta] = yb[k];
-      }
+      for (int j = 0; j < kIluNbj; ++j)
+        sring[((kk + ILU_K - 1) % ILU_K) * kIluRs + q * ILU_BMAX + j * kIluLpi] =
+            BWD ? sc_ * yv[j] : (sc_ * uv[j]) * yv[j];
+    };
+    auto publish = [&](unsigned long long done) {  // steps completed (their rows are stored)
+      __threadfence();
+      st_rel_gpu(prog + tile, ep | done);
     };
     double prev = 0.0, uprev = 0.0;  // own value (and forward: its uinv) at x -/+ 1
     // prologue: block 0's operands
-    wait_pred(ILU_K);
     fetch_own(0, 0);
     load_bnd(0);
     park_bnd(0);
+    __syncthreads();
     int cur = 0;
     for (int s0 = 0; s0 < steps; s0 += ILU_K) {
       const int s1 = (s0 + ILU_K) < steps ? (s0 + ILU_K) : steps;
       const bool more = s1 < steps;
-      if (more) {  // next block: predecessors far enough, then prefetch
-        wait_pred(s1 + ILU_K);
+      __syncwarp();  // buffer cur ^ 1 was flushed by this warp's lanes
+      if (more) {    // next block: prefetch (boundaries: once the predecessors are far enough)
         fetch_own(s1, cur ^ 1);
         load_bnd(s1);
       } else {
         cp_async_commit();  // (empty group: keeps wait_group 1 meaningful)
       }
-      cp_async_wait1();  // this block's own copies (this thread's) have landed
-      __syncthreads();   // ... and the parked boundary values of the previous block
+      cp_async_wait1();  // this block's own copies (this lane's) have landed ...
+      __syncwarp();      // ... and the warp's other lanes'
+      double* pfc = pf + (size_t)cur * ILU_K * 2 * kIluPfs + tid;
+      const double* rA = ringA + srcA + cur * bndA;
+      const double* rB = ringB + srcB + cur * bndB;
+      const int xs0 = s0 - skew;
+#pragma unroll
       for (int k = 0; k < ILU_K; ++k) {
-        const int s = s0 + k;
-        if (s >= s1) break;  // uniform
-        int64_t i;
-        if (row_of(s, i)) {
-          const int xs = s - ta - tb;
-          const int q = (s - 1) & 1;
-          double* d = pf + ((size_t)(cur * ILU_K + k) * 2) * kIluPfs + tid;
-          const size_t ob = ((size_t)(cur * ILU_K + k) * 2) * ILU_BMAX;
-          // ascending column order: forward -b, -a, -x; backward +x, +a, +b
-          double acc = d[0];
-          const double ui = d[kIluPfs];
-          if (!BWD) {
-            if (has_b) {
-              const double term = own_b ? pub[q][1][tid - P.TA]
-                                        : (cb * pfb[ob + ILU_BMAX + ta]) * pfb[ob + ta];
-              acc = acc - term;
-            }
-            if (has_a) {
-              const double term = own_a ? pub[q][0][tid - 1]
-                                        : (ca * pfa[ob + ILU_BMAX + tb]) * pfa[ob + tb];
-              acc = acc - term;
-            }
-            if (xs > 0) acc = acc - (cx * uprev) * prev;
-            d[0] = acc;  // leaves with the block's transposed stores
-            pub[s & 1][0][tid] = (ca * ui) * acc;  // the +a neighbour's -a term
-            pub[s & 1][1][tid] = (cb * ui) * acc;  // the +b neighbour's -b term
-            prev = acc;
-            uprev = ui;
-          } else {
-            if (xs > 0) acc = acc - cx * prev;
-            if (has_a) acc = acc - (own_a ? pub[q][0][tid - 1] : ca * pfa[ob + tb]);
-            if (has_b) acc = acc - (own_b ? pub[q][1][tid - P.TA] : cb * pfb[ob + ta]);
-            const double xi = acc * ui;
-            d[0] = xi;
-            pub[s & 1][0][tid] = ca * xi;
-            pub[s & 1][1][tid] = cb * xi;
-            prev = xi;
-          }
+        // ascending column order: forward -b, -a, -x; backward +x, +a, +b
+        double acc = pfc[k * 2 * kIluPfs];
+        const double ui = pfc[k * 2 * kIluPfs + kIluPfs];
+        const double tA = rA[((k + ILU_K - 1) % ILU_K) * kIluRs];
+        const double tB = rB[((k + ILU_K - 1) % ILU_K) * kIluRs];
+        // a missing leg's term is +0.0 (x - (+0.0) = x bitwise, -0.0 included)
+        const double tX = xs0 + k > 0 ? (BWD ? cx * prev : (cx * uprev) * prev) : 0.0;
+        double res;
+        if (!BWD) {
+          acc = ((acc - tB) - tA) - tX;
+          res = acc;
+          ringA[k * kIluRs + tid] = (ca * ui) * acc;  // the +a neighbour's -a term
+          ringB[k * kIluRs + tid] = (cb * ui) * acc;  // the +b neighbour's -b term
+          uprev = ui;
+        } else {
+          acc = ((acc - tX) - tA) - tB;
+          res = acc * ui;
+          ringA[k * kIluRs + tid] = ca * res;
+          ringB[k * kIluRs + tid] = cb * res;
         }
+        pfc[k * 2 * kIluPfs] = res;  // leaves with the block's transposed stores
+        prev = res;
+        if (k == ILU_K - 1 && more) park_bnd(cur ^ 1);  // the next block's loads have landed
         __syncthreads();
+        // the previous block's rows were stored before this barrier by every warp
+        if (k == 0 && s0 > 0 && tid == 0) publish((unsigned long long)s0);
       }
       flush_own(s0, cur);
-      if (more) park_bnd(cur ^ 1);  // the next block's boundary loads have landed by now
-      __syncthreads();  // the block's rows are stored (and buffer cur is free again)
-      if (tid == 0) {  // steps completed (every line's rows of steps < s1 are stored)
-        const unsigned long long done = more ? (unsigned long long)s1 : 0xFFFFFFFFull;
-        __threadfence();
-        st_rel_gpu(prog + tile, ep | done);
-      }
       cur ^= 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();  // every warp's last rows are stored
+    if (tid == 0) publish(0xFFFFFFFFull);
   }
   ilu_finish(ctr);
 }

@@ -2312,7 +2312,7 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
       int64_t ta = 16;
       if (const char* e = getenv("PBICG_ILU_TA")) {  // tuning experiments only
         const long v = strtol(e, nullptr, 10);
-        if (v >= 1 && v <= ILU_T) ta = v;
+        if (v >= 1 && v <= ILU_BMAX) ta = v;  // boundary-value slots per side
       }
       P.TA = (int32_t)(st->ny < ta ? st->ny : ta);
       int64_t tb = ILU_T / P.TA;
@@ -2350,16 +2350,17 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
     const auto SMA = cudaFuncAttributeMaxDynamicSharedMemorySize;
     CU(cudaFuncSetAttribute(k_ilu_st<3, false>, SMA, (int)kIluSmem));
     CU(cudaFuncSetAttribute(k_ilu_st<3, true>, SMA, (int)kIluSmem));
-    CU(cudaFuncSetAttribute(k_ilu_st<2, false>, SMA, (int)kIluSmem));
-    CU(cudaFuncSetAttribute(k_ilu_st<2, true>, SMA, (int)kIluSmem));
-    int occ = 0;
-    if (P.dim == 3)  // one CTA per SM: the critical-path tiles' per-step barriers do not
-      occ = 1;       // share the SM (measured: cfg3 4.5 -> 2.9 ms, cfg4 10.6 -> 7.9 ms)
-    else
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_ilu_2d<false>, 32 * I2_W, 0);
+    int occ = 0, occ_max = 0;
+    if (P.dim == 3) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_max, k_ilu_st<3, false>, ILU_T, kIluSmem);
+      occ = ILU_OCC3 < occ_max ? ILU_OCC3 : occ_max;
+    } else {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_max, k_ilu_2d<false>, 32 * I2_W, 0);
+      occ = occ_max;
+    }
     if (const char* e = getenv("PBICG_ILU_OCC")) {  // tuning experiments only
       const long v = strtol(e, nullptr, 10);
-      if (v >= 1 && v < occ) occ = (int)v;
+      if (v >= 1 && v <= occ_max) occ = (int)v;
     }
     const int64_t cap = (int64_t)(occ < 1 ? 1 : occ) * h->num_sm;
     h->ilu_grid = (int)(P.ntiles < cap ? P.ntiles : cap);

@@ -2,9 +2,9 @@
 # 3D ILU(0) sweeps: transposed (coalesced) operand copies and result stores vs one
 # row per lane per instruction; M^-1 application time (ablib/libI1.so = before,
 # product library = after), ILU parity suite, bench lines, ncu of the cfg4 sweeps
-O=gpurun_out/ab_ilu_tr
+O=gpurun_out/ab_ilu_v2
 mkdir -p $O
-L=ablib/libI1.so,paper_1809_01948_b200/libpbicgstab.so
+L=ablib/libI2.so,paper_1809_01948_b200/libpbicgstab.so
 timeout 900 python -m pytest tests/test_gpu_ilu.py -q -x 2>&1 | tail -3 > $O/tests.txt
 cat $O/tests.txt
 for c in cfg3 cfg4; do timeout 600 python scripts/ilu_exp.py $c $L 16 > $O/$c.txt 2>&1; cat $O/$c.txt; done
