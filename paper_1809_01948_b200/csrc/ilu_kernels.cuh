@@ -136,7 +136,7 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // contiguous: one row per line).  kIluPfs pads the per-thread operand rows so those
 // lanes' shared-memory slots (stride 2 * kIluPfs per step) fall into distinct banks.
 static_assert(ILU_K == 4 || ILU_K == 8 || ILU_K == 16, "ILU_K lanes per line must divide a warp");
-static_assert(ILU_T >= 64 && ILU_T % 32 == 0, "warps 0 and 1 serve the two tile boundaries");
+static_assert(ILU_T % 32 == 0, "whole compute warps; one more warp helps");
 constexpr int kIluLpi = 32 / ILU_K;             // lines per transposed warp instruction
 constexpr int kIluPfs = ILU_T + kIluLpi / 2;    // operand row stride (2 * kIluPfs = kIluLpi mod 16)
 constexpr int kIluRs = ILU_T + 2 * ILU_BMAX + kIluLpi;  // term ring row stride (= kIluLpi mod 16)
@@ -144,20 +144,36 @@ constexpr int kIluZc = ILU_T + 2 * ILU_BMAX;     // ring column of zeros (the te
 constexpr int kIluNbj = ILU_BMAX / kIluLpi;     // transposed instructions per boundary block
 constexpr size_t kIluSmem = sizeof(double) * (2 * ILU_K * 2 * kIluPfs + 2 * ILU_K * kIluRs);
 
+// named barriers of k_ilu_st (0 = __syncthreads of all ILU_T + 32 threads)
+constexpr int kIluBarStep = 1;   // the compute warps' per-step barrier
+constexpr int kIluBarFull = 2;   // 2, 3: boundary terms of a block parked (helper arrives)
+constexpr int kIluBarEmpty = 4;  // 4, 5: block finished and stored (compute threads arrive)
+__device__ __forceinline__ void ilu_bar_step() {
+  asm volatile("bar.sync %0, %1;" ::"n"(kIluBarStep), "n"(ILU_T) : "memory");
+}
+__device__ __forceinline__ void ilu_bar_sync(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(ILU_T + 32) : "memory");
+}
+__device__ __forceinline__ void ilu_bar_arrive(int id) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(ILU_T + 32) : "memory");
+}
+
 // Stencil ILU(0) sweep.  BWD = false: out := L^{-1} v; BWD = true: out := U^{-1} out
-// (in place; v unused).  Operands are prefetched one block of ILU_K steps ahead: own
-// values by transposed cp.async into shared memory; the neighbouring tiles' boundary
-// values (written during this kernel) by transposed L2 loads of warp 0 (a-side) and
-// warp 1 (b-side) once that tile's progress covers the next block, parked as finished
-// terms in the rings before the current block's last barrier.  A row's result replaces
-// its operand in shared memory and the block's results leave by transposed stores, so
-// a step is branch-free: four shared loads, the row's arithmetic (selects for the
-// zero terms of missing legs; idle lanes compute on garbage nobody reads), three shared stores and
-// ONE barrier -- the only CTA barriers of the step loop (a warp's transposed copies
-// and stores serve its own 32 lines, so they need warp-level ordering only, and a
-// block's progress is published after the next block's first barrier).
+// (in place; v unused).  ILU_T compute threads (one x-line each) and one helper warp.
+// Compute warps: operands are prefetched one block of ILU_K steps ahead by transposed
+// cp.async into shared memory; a row's result replaces its operand there and the
+// block's results leave by transposed stores.  A step is branch-free: four shared
+// loads, the row's arithmetic (+0.0 terms for missing legs; idle lanes compute on
+// garbage nobody reads), three shared stores and ONE named barrier of the compute
+// warps (a warp's transposed copies and stores serve its own 32 lines: warp-level
+// ordering).  Helper warp: everything with a long latency that would otherwise sit
+// between two step barriers -- it polls the predecessor tiles' progress, loads their
+// boundary values from L2 (transposed) two blocks ahead, parks them as finished terms
+// in the rings (FULL / EMPTY named barriers per block parity), and publishes this
+// tile's progress (a release store, i.e. a GPU-scope fence) once a block's rows are
+// stored.
 template <int DIM, bool BWD>
-__global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
+__global__ void __launch_bounds__(ILU_T + 32) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
                                                   const double* __restrict__ v,
                                                   double* __restrict__ out) {
   if (ilu_skip(sc, gate)) return;
@@ -247,79 +263,91 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
         out[jbase[j] + (BWD ? nx - 1 - xs : xs)] = dq[j * kIluLpi];
       }
     };
-    // Tile boundaries: warp 0 serves the a-side (lines ta = 0, slot = tb), warp 1 the
-    // b-side (tb = 0, slot = ta), one code path on per-warp data.  A boundary line of
-    // this tile at step s' (< upto) reads the predecessor's edge line at the same x,
-    // which that tile computes at its step s' + TA - 1 (a-side: its thread TA - 1 of the
-    // same b line) or s' + TB - 1 (b-side), whatever the line: so the predecessor must
-    // have completed upto + TA - 1 / upto + TB - 1 steps (progress = completed steps).
-    const bool side_b = warp == 1;
-    const unsigned long long* pp = warp == 0 ? pa : (warp == 1 ? pb : nullptr);
-    const int plag = (side_b ? P.TB : P.TA) - 1;
-    const double sc_ = side_b ? cb : ca;
-    double* sring = (side_b ? ringB : ringA) + ILU_T + lj;
-    const int nslot = side_b ? na_t : nb_t;
-    int64_t sbase[kIluNbj];  // the neighbouring tile's row at x = 0 (forward) / nx - 1
-    if (pp) {
+    const int nblk = (steps + ILU_K - 1) / ILU_K;
+    if (warp == ILU_T / 32) {
+      // ---- helper warp: everything that waits on other CTAs or on the memory system.
+      // Tile boundaries (a-side: lines ta = 0, slot = tb; b-side: tb = 0, slot = ta): a
+      // boundary line of this tile at step s' reads the predecessor's edge line at the
+      // same x, which that tile computes at its step s' + TA - 1 (a-side: its thread
+      // TA - 1 of the same b line) or s' + TB - 1 (b-side), whatever the line: so for
+      // block [sb, sb + ILU_K) the predecessor must have completed sb + ILU_K + TA - 1 /
+      // TB - 1 steps (progress = completed steps).  The block's values are loaded from
+      // L2 (transposed) and parked as finished terms in the boundary columns of the
+      // block's parity; FULL[parity] hands them to the compute warps, EMPTY[parity]
+      // (arrived by every compute thread after the block's stores) gives the columns
+      // back and tells that the block's rows are stored -> progress is published here.
+      int64_t sbase[2][kIluNbj];  // the neighbouring tile's row at x = 0 (forward) / nx - 1
 #pragma unroll
-      for (int j = 0; j < kIluNbj; ++j) {
-        const int slot = j * kIluLpi + lj;
-        const int sa_ = side_b ? slot : 0, sb_ = side_b ? 0 : slot;
-        sbase[j] = (a0 + (BWD ? na_t - 1 - sa_ : sa_)) * P.sa + (b0 + (BWD ? nb_t - 1 - sb_ : sb_)) * P.sb +
-                   (side_b ? (BWD ? P.sb : -P.sb) : (BWD ? P.sa : -P.sa));
+      for (int side = 0; side < 2; ++side)
+#pragma unroll
+        for (int j = 0; j < kIluNbj; ++j) {
+          const int slot = j * kIluLpi + lj;
+          const int sa_ = side ? slot : 0, sb_ = side ? 0 : slot;
+          sbase[side][j] = (a0 + (BWD ? na_t - 1 - sa_ : sa_)) * P.sa +
+                           (b0 + (BWD ? nb_t - 1 - sb_ : sb_)) * P.sb +
+                           (side ? (BWD ? P.sb : -P.sb) : (BWD ? P.sa : -P.sa));
+        }
+      auto prepare = [&](int m) {
+        const int sb = m * ILU_K, q = m & 1;
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          const unsigned long long* pp = side ? pb : pa;
+          if (!pp) continue;  // (uniform)
+          if (lane == 0) {
+            const unsigned long long need =
+                ep | (unsigned long long)(sb + ILU_K + (side ? P.TB : P.TA) - 1);
+            while (ld_acq_gpu(pp) < need) __nanosleep(20);
+          }
+          __syncwarp();
+          const int nslot = side ? na_t : nb_t;
+          const double c = side ? cb : ca;
+          double* ring = (side ? ringB : ringA) + ((kk + ILU_K - 1) % ILU_K) * kIluRs + ILU_T +
+                         q * ILU_BMAX + lj;
+          double yv[kIluNbj], uv[kIluNbj];
+#pragma unroll
+          for (int j = 0; j < kIluNbj; ++j) {
+            const int xs = sb + kk - (j * kIluLpi + lj);
+            const bool ok = j * kIluLpi + lj < nslot && (unsigned)xs < (unsigned)nx;
+            const int64_t i = sbase[side][j] + (BWD ? nx - 1 - xs : xs);
+            yv[j] = ok ? __ldcg(out + i) : 0.0;
+            uv[j] = (!BWD && ok) ? __ldg(P.uinv + i) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < kIluNbj; ++j)
+            ring[j * kIluLpi] = BWD ? c * yv[j] : (c * uv[j]) * yv[j];
+        }
+        __syncwarp();
+        ilu_bar_arrive(kIluBarFull + q);
+      };
+      prepare(0);
+      if (nblk > 1) prepare(1);
+      for (int n = 0; n < nblk; ++n) {
+        ilu_bar_sync(kIluBarEmpty + (n & 1));  // block n: columns consumed, rows stored
+        if (lane == 0)
+          st_rel_gpu(prog + tile, ep | (n + 1 < nblk ? (unsigned long long)(n + 1) * ILU_K : 0xFFFFFFFFull));
+        __syncwarp();
+        if (n + 2 < nblk) prepare(n + 2);
       }
+      continue;
     }
-    double yv[kIluNbj], uv[kIluNbj];
-    auto load_bnd = [&](int sb) {  // block [sb, sb + ILU_K): L2 loads -> registers
-      if (!pp) return;
-      if (lane == 0) {
-        const unsigned long long need = ep | (unsigned long long)(sb + ILU_K + plag);
-        while (ld_acq_gpu(pp) < need) __nanosleep(20);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int j = 0; j < kIluNbj; ++j) {
-        const int xs = sb + kk - (j * kIluLpi + lj);
-        const bool ok = j * kIluLpi + lj < nslot && (unsigned)xs < (unsigned)nx;
-        const int64_t i = sbase[j] + (BWD ? nx - 1 - xs : xs);
-        yv[j] = ok ? __ldcg(out + i) : 0.0;
-        if (!BWD) uv[j] = ok ? __ldg(P.uinv + i) : 0.0;
-      }
-    };
-    auto park_bnd = [&](int q) {  // ... -> finished terms in the boundary columns of parity q
-      if (!pp) return;
-#pragma unroll
-      for (int j = 0; j < kIluNbj; ++j)
-        sring[((kk + ILU_K - 1) % ILU_K) * kIluRs + q * ILU_BMAX + j * kIluLpi] =
-            BWD ? sc_ * yv[j] : (sc_ * uv[j]) * yv[j];
-    };
-    auto publish = [&](unsigned long long done) {  // steps completed (their rows are stored)
-      __threadfence();
-      st_rel_gpu(prog + tile, ep | done);
-    };
+    // ---- compute warps
     double prev = 0.0, uprev = 0.0;  // own value (and forward: its uinv) at x -/+ 1
-    // prologue: block 0's operands
-    fetch_own(0, 0);
-    load_bnd(0);
-    park_bnd(0);
-    __syncthreads();
+    fetch_own(0, 0);  // prologue: block 0's operands
     int cur = 0;
     for (int s0 = 0; s0 < steps; s0 += ILU_K) {
-      const int s1 = (s0 + ILU_K) < steps ? (s0 + ILU_K) : steps;
-      const bool more = s1 < steps;
+      const bool more = s0 + ILU_K < steps;
       __syncwarp();  // buffer cur ^ 1 was flushed by this warp's lanes
-      if (more) {    // next block: prefetch (boundaries: once the predecessors are far enough)
-        fetch_own(s1, cur ^ 1);
-        load_bnd(s1);
-      } else {
+      if (more)      // next block's operands
+        fetch_own(s0 + ILU_K, cur ^ 1);
+      else
         cp_async_commit();  // (empty group: keeps wait_group 1 meaningful)
-      }
       cp_async_wait1();  // this block's own copies (this lane's) have landed ...
       __syncwarp();      // ... and the warp's other lanes'
       double* pfc = pf + (size_t)cur * ILU_K * 2 * kIluPfs + tid;
       const double* rA = ringA + srcA + cur * bndA;
       const double* rB = ringB + srcB + cur * bndB;
       const int xs0 = s0 - skew;
+      ilu_bar_sync(kIluBarFull + cur);  // the block's boundary terms are parked
 #pragma unroll
       for (int k = 0; k < ILU_K; ++k) {
         // ascending column order: forward -b, -a, -x; backward +x, +a, +b
@@ -344,17 +372,13 @@ __global__ void __launch_bounds__(ILU_T) k_ilu_st(IluOp P, Scal* __restrict__ sc
         }
         pfc[k * 2 * kIluPfs] = res;  // leaves with the block's transposed stores
         prev = res;
-        if (k == ILU_K - 1 && more) park_bnd(cur ^ 1);  // the next block's loads have landed
-        __syncthreads();
-        // the previous block's rows were stored before this barrier by every warp
-        if (k == 0 && s0 > 0 && tid == 0) publish((unsigned long long)s0);
+        ilu_bar_step();
       }
       flush_own(s0, cur);
+      ilu_bar_arrive(kIluBarEmpty + cur);
       cur ^= 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();  // every warp's last rows are stored
-    if (tid == 0) publish(0xFFFFFFFFull);
   }
   ilu_finish(ctr);
 }
