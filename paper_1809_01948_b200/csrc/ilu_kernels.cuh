@@ -14,15 +14,17 @@
 // * k_ilu_st<DIM, BWD> -- 5/7-point stencils (constant coefficients; l_ik =
 //   fl(c_leg uinv_k), u_ij = c_leg since the zero-fill factorisation of a
 //   5/7-point stencil only updates the diagonal).  A "pipelined line wavefront":
-//   one thread per x-line (y, z); thread (ty, tz) of a TY x TZ line tile handles x =
-//   s - ty - tz at step s, taking the -x term from its own registers and the -y /
-//   -z terms from its neighbour threads' step s-1 results through shared memory
-//   (one barrier per step).  Tiles are taken in topological order (diagonals of
-//   the tile grid) from a ticket counter by a persistent grid; a tile's boundary
-//   lines read the neighbouring tiles' values from global memory after acquiring
-//   their progress counters, published every ILU_K steps.  The critical path is
-//   nx + ny + nz steps (the hyperplane count); at large sizes the kernel is HBM-
-//   bound (v, uinv read, out written per row).
+//   one compute thread per x-line (y, z); thread (ty, tz) of a TY x TZ line tile
+//   handles x = s - ty - tz at step s, taking the -x term from its own registers and
+//   the -y / -z terms from its neighbour threads' step s-1 results through shared
+//   memory (one named barrier per step).  A wavefront's rows are never contiguous, so
+//   global memory is touched by transposed warp instructions only (a block of ILU_K
+//   steps of a line = one 64-byte run), staged through shared memory.  Tiles are
+//   taken in topological order (diagonals of the tile grid) from a ticket counter by
+//   a persistent grid; a tile's boundary lines take the neighbouring tiles' values
+//   from global memory after acquiring their progress counters, published every
+//   ILU_K steps -- both by helper warps, off the compute warps' path.  The critical
+//   path is nx + ny + nz steps plus the tile lags.
 // * k_ilu_csr<BWD> -- general CSR: rows in level order (host-computed level sets),
 //   one thread per row, persistent grid; a row spins on the per-row epoch flags
 //   of its dependencies (all at earlier positions of the order), so no grid-wide
@@ -144,18 +146,27 @@ constexpr int kIluZc = ILU_T + 2 * ILU_BMAX;     // ring column of zeros (the te
 constexpr int kIluNbj = ILU_BMAX / kIluLpi;     // transposed instructions per boundary block
 constexpr size_t kIluSmem = sizeof(double) * (2 * ILU_K * 2 * kIluPfs + 2 * ILU_K * kIluRs);
 
-// named barriers of k_ilu_st (0 = __syncthreads of all ILU_T + 32 threads)
+// named barriers of k_ilu_st (0 = __syncthreads of all kIluThreads threads)
+constexpr int kIluThreads = ILU_T + 64;  // compute threads + loader warp + publisher warp
 constexpr int kIluBarStep = 1;   // the compute warps' per-step barrier
 constexpr int kIluBarFull = 2;   // 2, 3: boundary terms of a block parked (helper arrives)
 constexpr int kIluBarEmpty = 4;  // 4, 5: block finished and stored (compute threads arrive)
 __device__ __forceinline__ void ilu_bar_step() {
   asm volatile("bar.sync %0, %1;" ::"n"(kIluBarStep), "n"(ILU_T) : "memory");
 }
-__device__ __forceinline__ void ilu_bar_sync(int id) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(ILU_T + 32) : "memory");
+// FULL: the loader warp arrives, the compute threads wait; EMPTY: the compute threads
+// arrive, both helper warps wait
+__device__ __forceinline__ void ilu_full_sync(int q) {
+  asm volatile("bar.sync %0, %1;" ::"r"(kIluBarFull + q), "n"(ILU_T + 32) : "memory");
 }
-__device__ __forceinline__ void ilu_bar_arrive(int id) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "n"(ILU_T + 32) : "memory");
+__device__ __forceinline__ void ilu_full_arrive(int q) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(kIluBarFull + q), "n"(ILU_T + 32) : "memory");
+}
+__device__ __forceinline__ void ilu_empty_sync(int q) {
+  asm volatile("bar.sync %0, %1;" ::"r"(kIluBarEmpty + q), "n"(ILU_T + 64) : "memory");
+}
+__device__ __forceinline__ void ilu_empty_arrive(int q) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(kIluBarEmpty + q), "n"(ILU_T + 64) : "memory");
 }
 
 // Stencil ILU(0) sweep.  BWD = false: out := L^{-1} v; BWD = true: out := U^{-1} out
@@ -173,7 +184,7 @@ __device__ __forceinline__ void ilu_bar_arrive(int id) {
 // tile's progress (a release store, i.e. a GPU-scope fence) once a block's rows are
 // stored.
 template <int DIM, bool BWD>
-__global__ void __launch_bounds__(ILU_T + 32) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
+__global__ void __launch_bounds__(kIluThreads) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
                                                   const double* __restrict__ v,
                                                   double* __restrict__ out) {
   if (ilu_skip(sc, gate)) return;
@@ -264,18 +275,31 @@ __global__ void __launch_bounds__(ILU_T + 32) k_ilu_st(IluOp P, Scal* __restrict
       }
     };
     const int nblk = (steps + ILU_K - 1) / ILU_K;
+    if (warp == ILU_T / 32 + 1) {
+      // ---- publisher warp: a block's rows are stored -> this tile's progress (a release
+      // store, i.e. a GPU-scope fence: kept off every other warp's path)
+      for (int n = 0; n < nblk; ++n) {
+        ilu_empty_sync(n & 1);
+        if (lane == 0)
+          st_rel_gpu(prog + tile, ep | (n + 1 < nblk ? (unsigned long long)(n + 1) * ILU_K : 0xFFFFFFFFull));
+        __syncwarp();
+      }
+      continue;
+    }
     if (warp == ILU_T / 32) {
-      // ---- helper warp: everything that waits on other CTAs or on the memory system.
+      // ---- loader warp: everything that waits on other CTAs.
       // Tile boundaries (a-side: lines ta = 0, slot = tb; b-side: tb = 0, slot = ta): a
       // boundary line of this tile at step s' reads the predecessor's edge line at the
       // same x, which that tile computes at its step s' + TA - 1 (a-side: its thread
       // TA - 1 of the same b line) or s' + TB - 1 (b-side), whatever the line: so for
       // block [sb, sb + ILU_K) the predecessor must have completed sb + ILU_K + TA - 1 /
-      // TB - 1 steps (progress = completed steps).  The block's values are loaded from
-      // L2 (transposed) and parked as finished terms in the boundary columns of the
-      // block's parity; FULL[parity] hands them to the compute warps, EMPTY[parity]
-      // (arrived by every compute thread after the block's stores) gives the columns
-      // back and tells that the block's rows are stored -> progress is published here.
+      // TB - 1 steps (progress = completed steps; polled only when the last value seen
+      // does not cover the block).  The block's values are loaded from L2 (transposed,
+      // both sides in flight together) and parked as finished terms in the boundary
+      // columns of the block's parity; FULL[parity] hands them to the compute warps,
+      // EMPTY[parity] (arrived by every compute thread after the block's stores) gives
+      // the columns back.
+      unsigned long long seen[2] = {0ull, 0ull};
       int64_t sbase[2][kIluNbj];  // the neighbouring tile's row at x = 0 (forward) / nx - 1
 #pragma unroll
       for (int side = 0; side < 2; ++side)
@@ -289,6 +313,7 @@ __global__ void __launch_bounds__(ILU_T + 32) k_ilu_st(IluOp P, Scal* __restrict
         }
       auto prepare = [&](int m) {
         const int sb = m * ILU_K, q = m & 1;
+        double yv[2][kIluNbj], uv[2][kIluNbj];
 #pragma unroll
         for (int side = 0; side < 2; ++side) {
           const unsigned long long* pp = side ? pb : pa;
@@ -296,36 +321,39 @@ __global__ void __launch_bounds__(ILU_T + 32) k_ilu_st(IluOp P, Scal* __restrict
           if (lane == 0) {
             const unsigned long long need =
                 ep | (unsigned long long)(sb + ILU_K + (side ? P.TB : P.TA) - 1);
-            while (ld_acq_gpu(pp) < need) __nanosleep(20);
+            while (seen[side] < need) {
+              seen[side] = ld_acq_gpu(pp);
+              if (seen[side] < need) __nanosleep(20);
+            }
           }
           __syncwarp();
           const int nslot = side ? na_t : nb_t;
-          const double c = side ? cb : ca;
-          double* ring = (side ? ringB : ringA) + ((kk + ILU_K - 1) % ILU_K) * kIluRs + ILU_T +
-                         q * ILU_BMAX + lj;
-          double yv[kIluNbj], uv[kIluNbj];
 #pragma unroll
           for (int j = 0; j < kIluNbj; ++j) {
             const int xs = sb + kk - (j * kIluLpi + lj);
             const bool ok = j * kIluLpi + lj < nslot && (unsigned)xs < (unsigned)nx;
             const int64_t i = sbase[side][j] + (BWD ? nx - 1 - xs : xs);
-            yv[j] = ok ? __ldcg(out + i) : 0.0;
-            uv[j] = (!BWD && ok) ? __ldg(P.uinv + i) : 0.0;
+            yv[side][j] = ok ? __ldcg(out + i) : 0.0;
+            uv[side][j] = (!BWD && ok) ? __ldg(P.uinv + i) : 0.0;
           }
+        }
+#pragma unroll
+        for (int side = 0; side < 2; ++side) {
+          if (!(side ? pb : pa)) continue;
+          const double c = side ? cb : ca;
+          double* ring = (side ? ringB : ringA) + ((kk + ILU_K - 1) % ILU_K) * kIluRs + ILU_T +
+                         q * ILU_BMAX + lj;
 #pragma unroll
           for (int j = 0; j < kIluNbj; ++j)
-            ring[j * kIluLpi] = BWD ? c * yv[j] : (c * uv[j]) * yv[j];
+            ring[j * kIluLpi] = BWD ? c * yv[side][j] : (c * uv[side][j]) * yv[side][j];
         }
         __syncwarp();
-        ilu_bar_arrive(kIluBarFull + q);
+        ilu_full_arrive(q);
       };
       prepare(0);
       if (nblk > 1) prepare(1);
       for (int n = 0; n < nblk; ++n) {
-        ilu_bar_sync(kIluBarEmpty + (n & 1));  // block n: columns consumed, rows stored
-        if (lane == 0)
-          st_rel_gpu(prog + tile, ep | (n + 1 < nblk ? (unsigned long long)(n + 1) * ILU_K : 0xFFFFFFFFull));
-        __syncwarp();
+        ilu_empty_sync(n & 1);  // block n: its boundary columns are consumed
         if (n + 2 < nblk) prepare(n + 2);
       }
       continue;
@@ -347,7 +375,7 @@ __global__ void __launch_bounds__(ILU_T + 32) k_ilu_st(IluOp P, Scal* __restrict
       const double* rA = ringA + srcA + cur * bndA;
       const double* rB = ringB + srcB + cur * bndB;
       const int xs0 = s0 - skew;
-      ilu_bar_sync(kIluBarFull + cur);  // the block's boundary terms are parked
+      ilu_full_sync(cur);  // the block's boundary terms are parked
 #pragma unroll
       for (int k = 0; k < ILU_K; ++k) {
         // ascending column order: forward -b, -a, -x; backward +x, +a, +b
@@ -375,7 +403,7 @@ __global__ void __launch_bounds__(ILU_T + 32) k_ilu_st(IluOp P, Scal* __restrict
         ilu_bar_step();
       }
       flush_own(s0, cur);
-      ilu_bar_arrive(kIluBarEmpty + cur);
+      ilu_empty_arrive(cur);
       cur ^= 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");

@@ -582,8 +582,8 @@ void launch_ilu(pbicg_ctx* h, const double* in, double* out, int gate) {
   const IluOp& P = h->ilu_op;
   if (h->ilu_st) {
     if (P.dim == 3) {
-      k_ilu_st<3, false><<<h->ilu_grid, ILU_T + 32, kIluSmem, h->stream>>>(P, h->scal, gate, in, out);
-      k_ilu_st<3, true><<<h->ilu_grid, ILU_T + 32, kIluSmem, h->stream>>>(P, h->scal, gate, in, out);
+      k_ilu_st<3, false><<<h->ilu_grid, kIluThreads, kIluSmem, h->stream>>>(P, h->scal, gate, in, out);
+      k_ilu_st<3, true><<<h->ilu_grid, kIluThreads, kIluSmem, h->stream>>>(P, h->scal, gate, in, out);
     } else {
       k_ilu_2d<false><<<h->ilu_grid, 32 * I2_W, 0, h->stream>>>(P, h->scal, gate, in, out);
       k_ilu_2d<true><<<h->ilu_grid, 32 * I2_W, 0, h->stream>>>(P, h->scal, gate, in, out);
@@ -2352,7 +2352,7 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
     CU(cudaFuncSetAttribute(k_ilu_st<3, true>, SMA, (int)kIluSmem));
     int occ = 0, occ_max = 0;
     if (P.dim == 3) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_max, k_ilu_st<3, false>, ILU_T + 32, kIluSmem);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_max, k_ilu_st<3, false>, kIluThreads, kIluSmem);
       occ = ILU_OCC3 < occ_max ? ILU_OCC3 : occ_max;
     } else {
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_max, k_ilu_2d<false>, 32 * I2_W, 0);
