@@ -43,6 +43,9 @@
 #ifndef ILU_K
 #define ILU_K 8    // steps between progress publications
 #endif
+#ifndef ILU_MINB
+#define ILU_MINB 1  // register cap of k_ilu_st: CTAs per SM the compiler must allow
+#endif
 #ifndef ILU_OCC3
 #define ILU_OCC3 1  // CTAs per SM of the 3D sweeps (resident tiles = ILU_OCC3 x SMs)
 #endif
@@ -184,7 +187,7 @@ __device__ __forceinline__ void ilu_empty_arrive(int q) {
 // tile's progress (a release store, i.e. a GPU-scope fence) once a block's rows are
 // stored.
 template <int DIM, bool BWD>
-__global__ void __launch_bounds__(kIluThreads) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
+__global__ void __launch_bounds__(kIluThreads, ILU_MINB) k_ilu_st(IluOp P, Scal* __restrict__ sc, int gate,
                                                   const double* __restrict__ v,
                                                   double* __restrict__ out) {
   if (ilu_skip(sc, gate)) return;

@@ -6,7 +6,7 @@ R=/tmp/ncu_ilu_src
 mkdir -p $R
 I4="python scripts/profile_ilu.py ${1:-cfg4} 2"
 $I4 > $O/plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ilu -s 2 -c 2 -o $R/ilu4 $I4 > $R/ilu4.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -f -k regex:k_ilu -s 2 -c 2 -o $R/ilu4 $I4 > $O/ncu.log 2>&1
 echo "ilu4=$?"
 ncu -i $R/ilu4.ncu-rep --page raw --csv > $O/raw.csv 2>/dev/null
 ncu -i $R/ilu4.ncu-rep --page source --csv --print-source sass > $O/source_sass.csv 2>/dev/null
