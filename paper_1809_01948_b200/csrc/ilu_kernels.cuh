@@ -124,6 +124,28 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* g) {
                "l"(g)
                : "memory");
 }
+__device__ __forceinline__ double ld_vol_shared(const double* p) {
+  double v;
+  asm volatile("ld.volatile.shared.f64 %0, [%1];"
+               : "=d"(v)
+               : "r"((uint32_t)__cvta_generic_to_shared((const void*)p))
+               : "memory");
+  return v;
+}
+// predicated, on a shared-window address computed once (no branch, no address
+// conversion per copy)
+__device__ __forceinline__ void cp_async8_if(uint32_t smem, const double* g, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q cp.async.ca.shared.global [%0], [%1], 8;\n\t}" ::"r"(smem),
+      "l"(g), "r"((int)pred)
+      : "memory");
+}
+__device__ __forceinline__ void st_global_if(double* p, double v, bool pred) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q st.global.f64 [%0], %1;\n\t}" ::"l"(p),
+      "d"(v), "r"((int)pred)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
@@ -244,37 +266,45 @@ __global__ void __launch_bounds__(kIluThreads, ILU_MINB) k_ilu_st(IluOp P, Scal*
       if (B > 0) pb = prog + A + (int64_t)P.nta * (B - 1);
     }
     const int steps = nx + na_t + nb_t - 2;
-    int64_t jbase[ILU_K];
-    int jskew[ILU_K];
+    // transposed access: 32-bit row offsets inside the tile (host: ilu_setup keeps a
+    // tile's extent below 2^30 rows), row (j, block sb) = tile base + jo[j] +/- sb
+    const int64_t tbase = a0 * P.sa + b0 * P.sb;
+    const double* srcT = (BWD ? out : v) + tbase;
+    const double* uinvT = P.uinv + tbase;
+    double* outT = out + tbase;
+    int jo[ILU_K], jskew[ILU_K];
 #pragma unroll
     for (int j = 0; j < ILU_K; ++j) {
       const int tj = tj0 + j * kIluLpi;
       const int tja = tj % P.TA, tjb = tj / P.TA;
       const bool ok = tja < na_t && tjb < nb_t;
-      jbase[j] = (a0 + (BWD ? na_t - 1 - tja : tja)) * P.sa + (b0 + (BWD ? nb_t - 1 - tjb : tjb)) * P.sb;
-      jskew[j] = ok ? tja + tjb : (1 << 28);
+      const int lbase = ok ? (BWD ? na_t - 1 - tja : tja) * (int)P.sa + (BWD ? nb_t - 1 - tjb : tjb) * (int)P.sb : 0;
+      jskew[j] = ok ? tja + tjb : (1 << 28);  // idle lines: x < 0 always
+      jo[j] = ok ? (BWD ? lbase + nx - 1 - kk + jskew[j] : lbase + kk - jskew[j]) : 0;
     }
     // own operands of block [sb, sb + ILU_K) into buffer q (asynchronous copies)
+    const uint32_t pfs0 = (uint32_t)__cvta_generic_to_shared(pf + (size_t)kk * 2 * kIluPfs + tj0);
     auto fetch_own = [&](int sb, int q) {
-      double* dq = pf + ((size_t)(q * ILU_K + kk) * 2) * kIluPfs + tj0;
+      const uint32_t dq = pfs0 + (uint32_t)(q * ILU_K * 2 * kIluPfs * sizeof(double));
+      const int xk = sb + kk;
 #pragma unroll
       for (int j = 0; j < ILU_K; ++j) {
-        const int xs = sb + kk - jskew[j];
-        if ((unsigned)xs >= (unsigned)nx) continue;
-        const int64_t i = jbase[j] + (BWD ? nx - 1 - xs : xs);
-        cp_async8(dq + j * kIluLpi, BWD ? out + i : v + i);
-        cp_async8(dq + j * kIluLpi + kIluPfs, P.uinv + i);
+        const bool ok = (unsigned)(xk - jskew[j]) < (unsigned)nx;
+        const int o = ok ? (BWD ? jo[j] - sb : jo[j] + sb) : 0;
+        cp_async8_if(dq + j * kIluLpi * sizeof(double), srcT + o, ok);
+        cp_async8_if(dq + (j * kIluLpi + kIluPfs) * sizeof(double), uinvT + o, ok);
       }
       cp_async_commit();
     };
     // results of block [sb, sb + ILU_K) (left in the operand slots of buffer q) -> out
     auto flush_own = [&](int sb, int q) {
       const double* dq = pf + ((size_t)(q * ILU_K + kk) * 2) * kIluPfs + tj0;
+      const int xk = sb + kk;
 #pragma unroll
       for (int j = 0; j < ILU_K; ++j) {
-        const int xs = sb + kk - jskew[j];
-        if ((unsigned)xs >= (unsigned)nx) continue;
-        out[jbase[j] + (BWD ? nx - 1 - xs : xs)] = dq[j * kIluLpi];
+        const bool ok = (unsigned)(xk - jskew[j]) < (unsigned)nx;
+        const int o = ok ? (BWD ? jo[j] - sb : jo[j] + sb) : 0;
+        st_global_if(outT + o, dq[j * kIluLpi], ok);
       }
     };
     const int nblk = (steps + ILU_K - 1) / ILU_K;
@@ -379,16 +409,20 @@ __global__ void __launch_bounds__(kIluThreads, ILU_MINB) k_ilu_st(IluOp P, Scal*
       const double* rB = ringB + srcB + cur * bndB;
       const int xs0 = s0 - skew;
       ilu_full_sync(cur);  // the block's boundary terms are parked
+      // the step's own operands are read before the previous step's barrier (they do
+      // not depend on it): only the two term loads follow a barrier
+      double vk = pfc[0], uk = pfc[kIluPfs];
 #pragma unroll
       for (int k = 0; k < ILU_K; ++k) {
         // ascending column order: forward -b, -a, -x; backward +x, +a, +b
-        double acc = pfc[k * 2 * kIluPfs];
-        const double ui = pfc[k * 2 * kIluPfs + kIluPfs];
-        const double tA = rA[((k + ILU_K - 1) % ILU_K) * kIluRs];
-        const double tB = rB[((k + ILU_K - 1) % ILU_K) * kIluRs];
+        // (volatile loads, issued back to back: the compiler otherwise waits for the
+        // first term's subtraction before it loads the second)
+        const double tA = ld_vol_shared(rA + ((k + ILU_K - 1) % ILU_K) * kIluRs);
+        const double tB = ld_vol_shared(rB + ((k + ILU_K - 1) % ILU_K) * kIluRs);
         // a missing leg's term is +0.0 (x - (+0.0) = x bitwise, -0.0 included)
         const double tX = xs0 + k > 0 ? (BWD ? cx * prev : (cx * uprev) * prev) : 0.0;
-        double res;
+        const double ui = uk;
+        double acc = vk, res;
         if (!BWD) {
           acc = ((acc - tB) - tA) - tX;
           res = acc;
@@ -403,6 +437,10 @@ __global__ void __launch_bounds__(kIluThreads, ILU_MINB) k_ilu_st(IluOp P, Scal*
         }
         pfc[k * 2 * kIluPfs] = res;  // leaves with the block's transposed stores
         prev = res;
+        if (k + 1 < ILU_K) {
+          vk = pfc[(k + 1) * 2 * kIluPfs];
+          uk = pfc[(k + 1) * 2 * kIluPfs + kIluPfs];
+        }
         ilu_bar_step();
       }
       flush_own(s0, cur);
@@ -436,14 +474,6 @@ __device__ __forceinline__ void st_global_pred(double* p, double v, bool pred) {
       : "memory");
 }
 
-__device__ __forceinline__ double ld_vol_shared(const double* p) {
-  double v;
-  asm volatile("ld.volatile.shared.f64 %0, [%1];"
-               : "=d"(v)
-               : "r"((uint32_t)__cvta_generic_to_shared((const void*)p))
-               : "memory");
-  return v;
-}
 
 template <bool BWD>
 __global__ void __launch_bounds__(32 * I2_W) k_ilu_2d(IluOp P, Scal* __restrict__ sc, int gate,

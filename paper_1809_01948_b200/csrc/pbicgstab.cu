@@ -2293,6 +2293,11 @@ pbicg_status ilu_setup(pbicg_ctx* h, const pbicg_csr* op, const pbicg_stencil* s
         if (lu[(size_t)(p - p0)] != want) { st_ok = false; break; }
       }
   }
+  // k_ilu_st addresses a tile's rows by 32-bit offsets: (ILU_BMAX + 1) planes and lines
+  // must stay below 2^30 rows (else the general CSR sweeps run)
+  if (st_ok && st->dim == 3 &&
+      (int64_t)(ILU_BMAX + 1) * (st->nx * st->ny + st->nx) + st->nx >= ((int64_t)1 << 30))
+    st_ok = false;
   h->ilu_st = st_ok;
   if (st_ok) {
     const Geo& g = h->geo;  // set by the stencil create path

@@ -136,6 +136,47 @@ def test_ilu_csr_pipecg_symmetric(orc):
     S.close()
 
 
+def _random_shapes():
+    """Seeded 3D grids around the k_ilu_st tile geometry (16 x 16 lines per tile, blocks of
+    8 steps): x shorter than a block, ragged last tiles in y / z, one to five tiles per
+    direction, plus two fixed many-tile cases."""
+    rng = np.random.default_rng(20181809)
+    shapes = [(96, 80, 72), (9, 70, 83)]
+    for _ in range(22):
+        shapes.append((int(rng.integers(2, 71)), int(rng.integers(2, 52)), int(rng.integers(2, 52))))
+    return shapes
+
+
+@pytest.mark.parametrize("case,shape", list(enumerate(_random_shapes())))
+def test_ilu_stencil_random_shapes(orc, case, shape):
+    """The 3D wavefront sweeps (transposed staging, loader / publisher warps, tile
+    hand-over) on randomised grids: a short ILU(0) solve per shape, histories and x
+    bitwise vs the oracle (any wrong row, stale boundary value or missed hand-over
+    changes the first iterations' bits)."""
+    from paper_1809_01948_b200 import Solver
+    nx, ny, nz = shape
+    method = case % 3
+    coef = problems.cfg34_coef() if method != 2 else [6.0] + [-1.0] * 6
+    prec = "ilu0" if method != 2 else "icc0"
+    A = orc.stencil_csr(3, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 100 + case)
+    b = orc.spmv(A, xs)
+    S = Solver.stencil(3, nx, ny, nz, coef, block=prec)
+    S.set_option("method", method)
+    b_d = S.apply(torch.from_numpy(xs).cuda())
+    rr = 5 if method == 0 else 0
+    for rep in range(2):  # the second solve reuses the epoch-stamped progress counters
+        res = S.solve(b_d, tol=1e-13, maxit=12, rr_period=rr, gap=False)
+        ref = _ref(orc, method, A, b, tol=1e-13, maxit=12, **({"rr_period": rr} if method == 0 else {}))
+        assert res.outcome == ref.outcome
+        k = min(res.iters, ref.iters) + 1
+        assert np.array_equal(res.rnorm[:k], ref.rnorm[:k]), (shape, method, rep)
+        assert np.array_equal(res.x.cpu().numpy(), ref.x), (shape, method, rep)
+    n, _ = S.kernel_time("prec")
+    assert n > 0, "the ILU kernels must run"
+    S.close()
+
+
 @pytest.mark.parametrize("P", [2, 3])
 def test_ilu_stencil_loopback_block_reading(orc, P):
     """P ranks: each factorises its own slab (the block-diagonal part of A, A34)."""
