@@ -2133,7 +2133,11 @@ pbicg_status build_csr(pbicg_ctx* h, const pbicg_csr* op, const std::vector<doub
   // the window's first element R0 - bw must be 16-byte aligned for the bulk copies:
   // round the half bandwidth up to even (rows of an odd band just stage one more column)
   bw = (bw + 1) & ~(int64_t)1;
-  if (3LL * WTB + 2 * bw <= WRS) {
+  // ... and so must the ghosted operand's local part: with an odd ghost width H (a rank's
+  // odd stencil plane) every chunk start R0 - bw + H and the first ring position off - H
+  // are odd -- such handles keep the gather SpMV (found by the randomised ILU shapes:
+  // 35 x 47 x 3 on three loopback ranks faulted with "misaligned address")
+  if (3LL * WTB + 2 * bw <= WRS && h->H % 2 == 0) {
     // the window SpMV's operands as sliced ELL (SELL-32) with 16-bit column offsets
     // (|col - row| <= bw < 2^15): 10 bytes per slot, immediate-offset loads
     const int64_t ns = (n + 31) / 32;

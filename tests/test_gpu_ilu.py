@@ -5,6 +5,8 @@ wavefront kernels: one tile, several tiles in y / z, ragged tiles) and general
 CSR (the level-ordered row kernel), periodic replacement, loopback ranks with the
 block-diagonal reading, the one-rank NCCL path, and the error cases.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -140,9 +142,9 @@ def _random_shapes():
     """Seeded 3D grids around the k_ilu_st tile geometry (16 x 16 lines per tile, blocks of
     8 steps): x shorter than a block, ragged last tiles in y / z, one to five tiles per
     direction, plus two fixed many-tile cases."""
-    rng = np.random.default_rng(20181809)
+    rng = np.random.default_rng(20181809 + int(os.environ.get("PBICG_FUZZ_OFFSET", "0")))
     shapes = [(96, 80, 72), (9, 70, 83)]
-    for _ in range(22):
+    for _ in range(int(os.environ.get("PBICG_ILU_SHAPES", "22"))):  # wide sweeps: more shapes
         shapes.append((int(rng.integers(2, 71)), int(rng.integers(2, 52)), int(rng.integers(2, 52))))
     return shapes
 
@@ -175,6 +177,55 @@ def test_ilu_stencil_random_shapes(orc, case, shape):
     n, _ = S.kernel_time("prec")
     assert n > 0, "the ILU kernels must run"
     S.close()
+
+
+@pytest.mark.parametrize("case,shape", [(c, sh) for c, sh in enumerate(_random_shapes()) if c % 3 == 0])
+def test_ilu_stencil_random_shapes_loopback(orc, case, shape):
+    """The same sweeps on P = 2 / 3 loopback ranks (each rank's slab is its own tile grid,
+    block-diagonal reading A35) for every third random shape, both transports."""
+    from paper_1809_01948_b200.binding import LoopbackGroup, stencil_partition
+    nx, ny, nz = shape
+    P = 2 + (case // 3) % 2
+    if nz < P:
+        pytest.skip("fewer planes than ranks")
+    coef = problems.cfg34_coef()
+    A = orc.stencil_csr(3, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 200 + case)
+    b = orc.spmv(A, xs)
+    cuts = [stencil_partition(3, nx, ny, nz, P, r)[0] for r in range(P)] + [A.n]
+    with orc.prec_matrix(orc.block_diagonal(A, cuts)):
+        ref = orc.pbicgstab(A, b, tol=1e-13, maxit=12, rr_period=5, block="ilu0")
+    G = LoopbackGroup.stencil(P, 3, nx, ny, nz, coef, block="ilu0")
+    for transport in (0, 1):
+        G.set_option("transport", transport)
+        bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+        res = G.solve(bs, tol=1e-13, maxit=12, rr_period=5, gap=False)
+        assert res.outcome == ref.outcome
+        k = min(res.iters, ref.iters) + 1
+        assert np.array_equal(res.rnorm[:k], ref.rnorm[:k]), (shape, P, transport)
+        x = res.x.cpu().numpy() if hasattr(res.x, "cpu") else res.x
+        assert np.array_equal(x, ref.x), (shape, P, transport)
+    G.close()
+
+
+def test_ilu_loopback_odd_plane_window_alignment(orc):
+    """Regression (round 2): three loopback ranks of one 35 x 47 plane each -- an odd ghost
+    width -- made the window SpMV's bulk copies misaligned ("misaligned address"); such
+    handles now keep the gather SpMV.  Bitwise vs the oracle's block-diagonal reading."""
+    from paper_1809_01948_b200.binding import LoopbackGroup, stencil_partition
+    nx, ny, nz, P = 35, 47, 3, 3
+    coef = problems.cfg34_coef()
+    A = orc.stencil_csr(3, nx, ny, nz, coef)
+    xs = problems.x_star(A.n, 7)
+    b = orc.spmv(A, xs)
+    cuts = [stencil_partition(3, nx, ny, nz, P, r)[0] for r in range(P)] + [A.n]
+    with orc.prec_matrix(orc.block_diagonal(A, cuts)):
+        ref = orc.pbicgstab(A, b, tol=1e-12, maxit=60, rr_period=9, block="ilu0")
+    G = LoopbackGroup.stencil(P, 3, nx, ny, nz, coef, block="ilu0")
+    bs = G.apply(G.split(torch.from_numpy(xs).cuda()))
+    res = G.solve(bs, tol=1e-12, maxit=60, rr_period=9, gap=True)
+    check_parity(res, ref, xs, bitwise=True)
+    G.close()
 
 
 @pytest.mark.parametrize("P", [2, 3])
